@@ -1,0 +1,226 @@
+/*
+ * vc_api.h -- C-ABI of the VeriCache B200 decode loop (libvericache.so).
+ *
+ * The drop-in boundary for the path BASELINE.json's north star names: a
+ * compressed KV cache drafts, the full KV verifies, greedy accept/rollback
+ * keeps the output identical to full-KV decode.  Plain pointers and sizes,
+ * no exceptions, no torch types.  Every entry point returns a status:
+ *   VC_OK (0), VC_ERR_CONFIG (1, bad input -- speckv::ConfigError),
+ *   VC_ERR_CONTRACT (2, API misuse -- speckv::ContractError),
+ *   VC_ERR_CUDA (3, device failure); vc_last_error() has the message.
+ * One host thread per engine (the reference is single-threaded per serving
+ * instance: /root/reference/SPEC.md:84, :287).  The engine owns every
+ * device and pinned buffer; callers own their token/KV arrays.
+ *
+ * Reference interfaces each group replaces (all under /root/reference/proj):
+ *   vc_compress / vc_compressed_*   speckv::compress / decompress
+ *                                   (include/speckv/compressor.hpp:70-80,
+ *                                    src/compressor.cpp:130-200)
+ *   vc_update_window                speckv::update (compressor.hpp:96-98,
+ *                                    src/compressor.cpp:208-243)
+ *   vc_draft_step                   speckv::draft's TokenOracle::next calls
+ *                                   (include/speckv/specloop.hpp:18-22,39;
+ *                                    src/specloop.cpp:11-22)
+ *   vc_verify                       speckv::verify (specloop.hpp:44-45,
+ *                                    src/specloop.cpp:24-35)
+ *   vc_accept / vc_accept_commit    speckv::accept (specloop.hpp:49,
+ *                                    src/specloop.cpp:37-56) + KV append
+ *   vc_run_speculative / vc_run_decode
+ *                                   speckv::run_speculative / autoregress
+ *                                   (specloop.hpp:53-61, src/specloop.cpp:58-92)
+ *   vc_swap_begin / vc_swap_poll    the transfers SpecScheduler::pending_kickoffs
+ *                                   asks for and StepEvents::completed_transfers
+ *                                   reports (include/speckv/scheduler.hpp:176-
+ *                                   180, 219; src/sim.cpp:243-250)
+ *   vc_run_scheduled                simulate_staggered's loop with real kernels
+ *                                   and copies (src/sim.cpp:182-307)
+ */
+#ifndef VC_API_H
+#define VC_API_H
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { VC_OK = 0, VC_ERR_CONFIG = 1, VC_ERR_CONTRACT = 2, VC_ERR_CUDA = 3 };
+
+typedef struct vc_engine vc_engine;
+
+typedef struct {
+  int vocab, hidden, layers, n_q, n_kv, d_head, ffn;
+  float rope_theta, rms_eps;
+} vc_model_desc;
+
+typedef struct {
+  int max_slots;   /* concurrently resident requests */
+  int max_ctx;     /* tokens per request (prefix + generated) */
+  int max_x;       /* largest draft horizon */
+  int quant_bits;  /* 4 or 2 (quant-uniform compressor), 0 = no compressed tier */
+  int full_tier;   /* 0 = full KV resident in HBM, 1 = pinned host pool + staging */
+  int n_stage;     /* HBM staging slots for tier 1 */
+  int max_verify;  /* verify requests per step */
+  int use_graphs;  /* capture steps into CUDA graphs */
+} vc_runtime_desc;
+
+/* Mirrors speckv::CompressedKVMeta (compressor.hpp:56-65) for quant-uniform:
+ * every position is kept, payload_bytes obeys the size law
+ * full_bytes * bit_scheme / 16 (compressor.cpp:96-100, codes only);
+ * aux_bytes carries the fp16 scales/zeros the size law does not count.    */
+typedef struct {
+  int bit_scheme;
+  int64_t payload_bytes;
+  int64_t aux_bytes;
+  int64_t full_bytes;
+  int n_groups;
+  int tail_tokens;
+} vc_compressed_meta;
+
+typedef struct {
+  int live, committed, pending, n_groups, tail_committed, draft_len;
+} vc_seq_state;
+
+/* mode: 0 decode (full KV), 1 draft (compressed KV), 2 verify (full KV) */
+typedef struct {
+  int slot, mode, n_tokens, stage;
+  const int32_t* tokens;
+} vc_step_item;
+
+const char* vc_last_error(void);
+int vc_version(void);
+
+/* ---- engine ----------------------------------------------------------- */
+int vc_engine_create(const vc_model_desc* model, const vc_runtime_desc* rt, int device,
+                     vc_engine** out);
+int vc_engine_destroy(vc_engine* e);
+int vc_engine_init_weights(vc_engine* e, uint64_t seed, float stddev);
+/* logical layouts, bf16 bits; per-layer arrays have `layers` pointers      */
+int vc_engine_load_weights(vc_engine* e, const uint16_t* embed, const uint16_t* const* attn_norm,
+                           const uint16_t* const* wqkv, const uint16_t* const* wo,
+                           const uint16_t* const* mlp_norm, const uint16_t* const* wgate,
+                           const uint16_t* const* wup, const uint16_t* const* wdown,
+                           const uint16_t* final_norm, const uint16_t* lm_head);
+int vc_engine_stats(vc_engine* e, uint64_t* kernel_launches, uint64_t* weight_bytes);
+
+/* ---- requests ----------------------------------------------------------- */
+int vc_request_add_synthetic(vc_engine* e, int slot, int n_ctx, int32_t first_token, uint64_t seed,
+                             int outlier_channels, float outlier_scale);
+/* k, v: bf16 [layers][n_kv][n_ctx][d_head] */
+int vc_request_add_kv(vc_engine* e, int slot, int n_ctx, int32_t first_token, const uint16_t* k,
+                      const uint16_t* v);
+int vc_request_prefill(vc_engine* e, int slot, const int32_t* prompt, int n);
+int vc_request_release(vc_engine* e, int slot);
+int vc_request_state(vc_engine* e, int slot, vc_seq_state* out);
+/* every token emitted so far (capacity cap); *n receives the count */
+int vc_request_history(vc_engine* e, int slot, int32_t* out, int cap, int* n);
+
+/* ---- compressor ---------------------------------------------------------- */
+/* Offline quant-uniform compress of the request's committed prefix.       */
+int vc_compress(vc_engine* e, int slot, vc_compressed_meta* out);
+/* Copy one (layer, kv-head) slice of the compressed tier to host:
+ * kcodes/vcodes u32 words (fragment order), ksz [groups][d],
+ * vsz [groups*128], ktail/vtail bf16 [tail_cap][d].  Any pointer may be NULL. */
+int vc_compressed_read(vc_engine* e, int slot, int layer, int head, uint32_t* kcodes,
+                       uint32_t* ksz, uint32_t* vcodes, uint32_t* vsz, uint16_t* ktail,
+                       uint16_t* vtail);
+int vc_compressed_geometry(vc_engine* e, int* group, int* words_per_group, int* tail_cap,
+                           int* max_groups);
+/* Drop-index generation of the token-dropping compressors, bit-identical
+ * to speckv::compress (compressor.cpp:152-177): kind 0 drop-uniform, 1
+ * drop-window; kept positions are the complement.  out [layers][heads][drop]. */
+int64_t vc_drop_indices(int kind, int layers, int heads, int64_t tokens, double ratio,
+                        uint64_t seed, int sink_tokens, int64_t* out);
+/* speckv::update for drop-window online compression, one layer, a batch of
+ * requests (compressor.cpp:208-243).  already[i] = drops so far at layer;
+ * new drops for request i, head h at out[(i*heads + h)*cap + k].           */
+int vc_update_window(int heads, int window, int sink_tokens, int n_req, const int64_t* tokens,
+                     const int64_t* req_begin, const int64_t* req_end, const int64_t* already,
+                     int64_t* out, int64_t cap, int64_t* n_new);
+/* Drop-topk: keep the k highest scores per row (ties -> lower position);
+ * scores device [rows][T] fp32, kept device [rows][k] int32 ascending.    */
+int vc_topk_select(const float* scores, int rows, int T, int k, int32_t* kept, void* stream);
+/* Key-norm scores s_t = sum_c |k_tc| w_c for device bf16 keys [rows][T][d]. */
+int vc_key_scores(const uint16_t* keys, int rows, int T, int d, const float* w, float* scores,
+                  void* stream);
+
+/* ---- steps ---------------------------------------------------------------- */
+/* One forward pass over a heterogeneous batch; out_rows receives the greedy
+ * token of every input row (item order).  logits (optional) [rows][vocab]. */
+int vc_step(vc_engine* e, const vc_step_item* items, int n, int32_t* out_rows, float* logits);
+int vc_decode_step(vc_engine* e, const int* slots, int n, int32_t* out_tokens);
+int vc_draft_step(vc_engine* e, const int* slots, int n, int32_t* out_tokens);
+/* Verify every slot's open draft round; preds receives x_i+1 tokens per
+ * slot back to back.  stages: staging slot per request (tier 1) or NULL.  */
+int vc_verify(vc_engine* e, const int* slots, int n, const int* stages, int32_t* preds);
+/* Greedy accept rule (specloop.cpp:37-56) on host arrays.                  */
+int vc_accept(const int32_t* drafted, const int32_t* preds, int x, int32_t* accepted,
+              int* n_accepted, int* first_mismatch, int* bonus);
+/* Accept + commit exact KV of the accepted prefix + roll the draft window back. */
+int vc_accept_commit(vc_engine* e, int slot, const int32_t* preds, int stage, int32_t* emitted,
+                     int* n_emitted);
+
+/* ---- host tier ------------------------------------------------------------ */
+int vc_swap_begin(vc_engine* e, int slot, int stage, uint64_t* transfer_id);
+int vc_swap_poll(vc_engine* e, uint64_t transfer_id, int* done);
+
+/* ---- decode loops ----------------------------------------------------------- */
+/* Full-KV greedy decode of K tokens for each slot (the baseline).
+ * out [n][K]; *ms = device time of the loop.                               */
+int vc_run_decode(vc_engine* e, const int* slots, int n, int K, int32_t* out, double* ms);
+/* Lossless speculative loop (lock-step rounds of x drafts + one verify per
+ * slot).  out [n][K]; accepted-per-round written to rounds (cap max_rounds
+ * per slot, row-major [n][max_rounds]); n_rounds [n].                       */
+int vc_run_speculative(vc_engine* e, const int* slots, int n, int K, int x, int32_t* out,
+                       int32_t* rounds, int max_rounds, int* n_rounds, double* ms);
+
+/* Swap-scheduled loop (tier 1): SpecScheduler semantics drive real draft
+ * rows, verify rows and H2D reloads (Algorithm 1).     */
+typedef struct {
+  int x;                    /* draft_length */
+  int window;               /* lookahead_window W */
+  double iteration_time;    /* planning T_iter (s); <= 0: measure */
+  double link_bandwidth;    /* planning BW (B/s); <= 0: measure */
+  int64_t hbm_capacity;     /* bytes for weights + resident + in-flight */
+  int K;                    /* output tokens per request */
+} vc_sched_desc;
+
+typedef struct {
+  double wall_ms;           /* device+host time of the loop */
+  int64_t tokens;           /* emitted tokens (all requests) */
+  int64_t iterations;
+  int64_t verifies;
+  int64_t late_transfers;
+  double h2d_bytes;
+  double h2d_ms;            /* copy-engine busy time */
+  double verify_wait_ms;    /* time verifies waited on copy events */
+  double mean_accept;       /* accepted drafted tokens per verify */
+} vc_sched_stats;
+
+int vc_run_scheduled(vc_engine* e, const int* slots, int n, const vc_sched_desc* sd,
+                     int32_t* out, vc_sched_stats* stats);
+
+/* ---- scheduler ------------------------------------------------------------ */
+int vc_reload_span(int64_t bytes, double bandwidth, double iteration_time, double* iterations,
+                   int* windows);
+
+/* ---- kernel-level entry points (device pointers) -------------------------- */
+/* Quantise one token-major bf16 slice [n_groups*128][d] into the fragment
+ * layout (what vc_compress does per (layer, request, kv-head)).            */
+int vc_quant_kivi_slice(const uint16_t* k, const uint16_t* v, int n_groups, int d, int bits,
+                        uint32_t* kcodes, uint32_t* ksz, uint32_t* vcodes, uint32_t* vsz,
+                        void* stream);
+/* Attention of q (bf16 [n_rows][n_q][d], device) for one request/layer of
+ * the engine's pools.  mode 1 = draft over the compressed tier (n_rows 1),
+ * mode 0/2 = dense over the full tier (causal over the last n_rows).
+ * out: host bf16 [n_rows][n_q][d].                                          */
+int vc_attention_probe(vc_engine* e, int slot, int layer, int mode, const uint16_t* q_dev,
+                       int n_rows, int kv_len, uint16_t* out_host);
+/* ws = X[M][K] . W[N][K]^T via the batch-invariant projection GEMM (device). */
+int vc_gemm_probe(const uint16_t* X, int M, int K, const uint16_t* W, int N, float* Y,
+                  void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

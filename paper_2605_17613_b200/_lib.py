@@ -1,0 +1,145 @@
+"""ctypes binding of libvericache.so (the C-ABI in include/vc_api.h).
+
+The product path is the CUDA library; there is no Python or CPU fallback.
+Loading fails loudly when the shared object is missing.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libvericache.so")
+
+VC_OK, VC_ERR_CONFIG, VC_ERR_CONTRACT, VC_ERR_CUDA = 0, 1, 2, 3
+
+
+class VcError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"[vc status {code}] {msg}")
+        self.code = code
+
+
+class ConfigError(VcError):
+    """speckv::ConfigError -- bad input (compressor.cpp / config.cpp messages)."""
+
+
+class ContractError(VcError):
+    """speckv::ContractError -- API misuse."""
+
+
+class CudaError(VcError):
+    """A device failure."""
+
+
+class ModelDesc(C.Structure):
+    _fields_ = [("vocab", C.c_int), ("hidden", C.c_int), ("layers", C.c_int), ("n_q", C.c_int),
+                ("n_kv", C.c_int), ("d_head", C.c_int), ("ffn", C.c_int),
+                ("rope_theta", C.c_float), ("rms_eps", C.c_float)]
+
+
+class RuntimeDesc(C.Structure):
+    _fields_ = [("max_slots", C.c_int), ("max_ctx", C.c_int), ("max_x", C.c_int),
+                ("quant_bits", C.c_int), ("full_tier", C.c_int), ("n_stage", C.c_int),
+                ("max_verify", C.c_int), ("use_graphs", C.c_int)]
+
+
+class CompressedMeta(C.Structure):
+    _fields_ = [("bit_scheme", C.c_int), ("payload_bytes", C.c_int64), ("aux_bytes", C.c_int64),
+                ("full_bytes", C.c_int64), ("n_groups", C.c_int), ("tail_tokens", C.c_int)]
+
+
+class SeqState(C.Structure):
+    _fields_ = [("live", C.c_int), ("committed", C.c_int), ("pending", C.c_int),
+                ("n_groups", C.c_int), ("tail_committed", C.c_int), ("draft_len", C.c_int)]
+
+
+class StepItem(C.Structure):
+    _fields_ = [("slot", C.c_int), ("mode", C.c_int), ("n_tokens", C.c_int), ("stage", C.c_int),
+                ("tokens", C.POINTER(C.c_int32))]
+
+
+class SchedDesc(C.Structure):
+    _fields_ = [("x", C.c_int), ("window", C.c_int), ("iteration_time", C.c_double),
+                ("link_bandwidth", C.c_double), ("hbm_capacity", C.c_int64), ("K", C.c_int)]
+
+
+class SchedStats(C.Structure):
+    _fields_ = [("wall_ms", C.c_double), ("tokens", C.c_int64), ("iterations", C.c_int64),
+                ("verifies", C.c_int64), ("late_transfers", C.c_int64), ("h2d_bytes", C.c_double),
+                ("h2d_ms", C.c_double), ("verify_wait_ms", C.c_double), ("mean_accept", C.c_double)]
+
+
+P = C.c_void_p
+I, I64, U64, D, F = C.c_int, C.c_int64, C.c_uint64, C.c_double, C.c_float
+PI, PI32, PI64, PU64, PD = (C.POINTER(C.c_int), C.POINTER(C.c_int32), C.POINTER(C.c_int64),
+                            C.POINTER(C.c_uint64), C.POINTER(C.c_double))
+PU16, PU32, PF = C.POINTER(C.c_uint16), C.POINTER(C.c_uint32), C.POINTER(C.c_float)
+PPU16 = C.POINTER(PU16)
+
+# name -> (restype, argtypes); every symbol include/vc_api.h declares.
+SIGNATURES = {
+    "vc_last_error": (C.c_char_p, []),
+    "vc_version": (I, []),
+    "vc_engine_create": (I, [C.POINTER(ModelDesc), C.POINTER(RuntimeDesc), I, C.POINTER(P)]),
+    "vc_engine_destroy": (I, [P]),
+    "vc_engine_init_weights": (I, [P, U64, F]),
+    "vc_engine_load_weights": (I, [P, PU16, PPU16, PPU16, PPU16, PPU16, PPU16, PPU16, PPU16, PU16, PU16]),
+    "vc_engine_stats": (I, [P, PU64, PU64]),
+    "vc_request_add_synthetic": (I, [P, I, I, C.c_int32, U64, I, F]),
+    "vc_request_add_kv": (I, [P, I, I, C.c_int32, PU16, PU16]),
+    "vc_request_prefill": (I, [P, I, PI32, I]),
+    "vc_request_release": (I, [P, I]),
+    "vc_request_state": (I, [P, I, C.POINTER(SeqState)]),
+    "vc_request_history": (I, [P, I, PI32, I, PI]),
+    "vc_compress": (I, [P, I, C.POINTER(CompressedMeta)]),
+    "vc_compressed_read": (I, [P, I, I, I, PU32, PU32, PU32, PU32, PU16, PU16]),
+    "vc_compressed_geometry": (I, [P, PI, PI, PI, PI]),
+    "vc_drop_indices": (I64, [I, I, I, I64, D, U64, I, PI64]),
+    "vc_update_window": (I, [I, I, I, I, PI64, PI64, PI64, PI64, PI64, I64, PI64]),
+    "vc_topk_select": (I, [P, I, I, I, P, P]),
+    "vc_key_scores": (I, [P, I, I, I, P, P, P]),
+    "vc_step": (I, [P, C.POINTER(StepItem), I, PI32, PF]),
+    "vc_decode_step": (I, [P, PI, I, PI32]),
+    "vc_draft_step": (I, [P, PI, I, PI32]),
+    "vc_verify": (I, [P, PI, I, PI, PI32]),
+    "vc_accept": (I, [PI32, PI32, I, PI32, PI, PI, PI]),
+    "vc_accept_commit": (I, [P, I, PI32, I, PI32, PI]),
+    "vc_swap_begin": (I, [P, I, I, PU64]),
+    "vc_swap_poll": (I, [P, U64, PI]),
+    "vc_run_decode": (I, [P, PI, I, I, PI32, PD]),
+    "vc_run_speculative": (I, [P, PI, I, I, I, PI32, PI32, I, PI, PD]),
+    "vc_run_scheduled": (I, [P, PI, I, C.POINTER(SchedDesc), PI32, C.POINTER(SchedStats)]),
+    "vc_reload_span": (I, [I64, D, D, PD, PI]),
+    "vc_quant_kivi_slice": (I, [P, P, I, I, I, P, P, P, P, P]),
+    "vc_attention_probe": (I, [P, I, I, I, P, I, I, PU16]),
+    "vc_gemm_probe": (I, [P, I, I, P, I, P, P]),
+}
+
+_lib = None
+
+
+def load() -> C.CDLL:
+    """Load libvericache.so (raises if it was not built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise ImportError(f"{LIB_PATH} missing: run `make -C paper_2605_17613_b200` "
+                          "(there is no CPU fallback)")
+    lib = C.CDLL(LIB_PATH)
+    for name, (res, args) in SIGNATURES.items():
+        fn = getattr(lib, name)
+        fn.restype = res
+        fn.argtypes = args
+    _lib = lib
+    return lib
+
+
+def check(rc: int) -> None:
+    if rc == VC_OK:
+        return
+    msg = load().vc_last_error().decode(errors="replace")
+    cls = {VC_ERR_CONFIG: ConfigError, VC_ERR_CONTRACT: ContractError,
+           VC_ERR_CUDA: CudaError}.get(rc, VcError)
+    raise cls(rc, msg)

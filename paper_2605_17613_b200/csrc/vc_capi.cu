@@ -1,0 +1,517 @@
+// vc_capi.cu -- extern "C" boundary (include/vc_api.h).  Thin: validates,
+// forwards to the engine / host algorithms, maps exceptions to status codes.
+#include <chrono>
+#include <cstring>
+#include <string>
+
+#include "speckv_b200.hpp"
+#include "vc_api.h"
+#include "vc_engine.hpp"
+#include "vc_topk.h"
+
+struct vc_engine {
+  vc::Engine* impl;
+};
+
+int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sched_desc& sd,
+                          int32_t* out, vc_sched_stats* stats);
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guard(F&& f) {
+  try {
+    f();
+    return VC_OK;
+  } catch (const speckv::ConfigError& e) {
+    g_err = e.what();
+    return VC_ERR_CONFIG;
+  } catch (const speckv::ContractError& e) {
+    g_err = e.what();
+    return VC_ERR_CONTRACT;
+  } catch (const vc::ContractViolation& e) {
+    g_err = e.what();
+    return VC_ERR_CONTRACT;
+  } catch (const vc::CudaError& e) {
+    g_err = e.what();
+    return VC_ERR_CUDA;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return VC_ERR_CONTRACT;
+  }
+}
+
+vc::Engine& E(vc_engine* e) {
+  if (e == nullptr || e->impl == nullptr) throw vc::ContractViolation("null engine");
+  return *e->impl;
+}
+
+
+}  // namespace
+
+extern "C" {
+
+const char* vc_last_error(void) { return g_err.c_str(); }
+int vc_version(void) { return 1; }
+
+int vc_engine_create(const vc_model_desc* model, const vc_runtime_desc* rt, int device,
+                     vc_engine** out) {
+  return guard([&] {
+    if (!model || !rt || !out) throw vc::ContractViolation("vc_engine_create: null argument");
+    vc::EngineConfig c;
+    c.model.vocab = model->vocab;
+    c.model.hidden = model->hidden;
+    c.model.layers = model->layers;
+    c.model.n_q = model->n_q;
+    c.model.n_kv = model->n_kv;
+    c.model.d = model->d_head;
+    c.model.ffn = model->ffn;
+    c.model.rope_theta = model->rope_theta;
+    c.model.eps = model->rms_eps;
+    if (c.model.vocab < 2 || c.model.hidden < 64 || c.model.layers < 1 || c.model.ffn < 64 ||
+        c.model.hidden % 64 != 0 || c.model.ffn % 64 != 0)
+      throw speckv::ConfigError("model: unsupported shape (hidden, ffn must be multiples of 64)");
+    c.max_slots = rt->max_slots;
+    c.max_ctx = rt->max_ctx;
+    c.max_x = rt->max_x;
+    c.quant_bits = rt->quant_bits;
+    c.full_tier = rt->full_tier;
+    c.n_stage = rt->n_stage;
+    c.max_verify = rt->max_verify;
+    c.use_graphs = rt->use_graphs;
+    if (c.max_slots < 1 || c.max_ctx < 1 || c.max_x < 1 || c.max_verify < 1)
+      throw speckv::ConfigError("runtime: sizes must be >= 1");
+    auto* h = new vc_engine{nullptr};
+    try {
+      h->impl = new vc::Engine(c, device);
+    } catch (...) {
+      delete h;
+      throw;
+    }
+    *out = h;
+  });
+}
+
+int vc_engine_destroy(vc_engine* e) {
+  return guard([&] {
+    if (!e) return;
+    delete e->impl;
+    delete e;
+  });
+}
+
+int vc_engine_init_weights(vc_engine* e, uint64_t seed, float stddev) {
+  return guard([&] { E(e).init_weights_random(seed, stddev); });
+}
+
+int vc_engine_load_weights(vc_engine* e, const uint16_t* embed, const uint16_t* const* attn_norm,
+                           const uint16_t* const* wqkv, const uint16_t* const* wo,
+                           const uint16_t* const* mlp_norm, const uint16_t* const* wgate,
+                           const uint16_t* const* wup, const uint16_t* const* wdown,
+                           const uint16_t* final_norm, const uint16_t* lm_head) {
+  return guard([&] {
+    E(e).load_weights(embed, attn_norm, wqkv, wo, mlp_norm, wgate, wup, wdown, final_norm, lm_head);
+  });
+}
+
+int vc_engine_stats(vc_engine* e, uint64_t* launches, uint64_t* weight_bytes) {
+  return guard([&] {
+    if (launches) *launches = E(e).launches();
+    if (weight_bytes) *weight_bytes = E(e).weight_bytes();
+  });
+}
+
+int vc_request_add_synthetic(vc_engine* e, int slot, int n_ctx, int32_t first_token, uint64_t seed,
+                             int outlier_channels, float outlier_scale) {
+  return guard([&] { E(e).add_request_synthetic(slot, n_ctx, first_token, seed, outlier_channels, outlier_scale); });
+}
+
+int vc_request_add_kv(vc_engine* e, int slot, int n_ctx, int32_t first_token, const uint16_t* k,
+                      const uint16_t* v) {
+  return guard([&] { E(e).add_request_kv(slot, n_ctx, first_token, k, v); });
+}
+
+int vc_request_prefill(vc_engine* e, int slot, const int32_t* prompt, int n) {
+  return guard([&] { E(e).add_request_prefill(slot, prompt, n); });
+}
+
+int vc_request_release(vc_engine* e, int slot) {
+  return guard([&] { E(e).release(slot); });
+}
+
+int vc_request_state(vc_engine* e, int slot, vc_seq_state* out) {
+  return guard([&] {
+    const vc::SeqState& s = E(e).seq(slot);
+    out->live = s.live;
+    out->committed = s.committed;
+    out->pending = s.pending;
+    out->n_groups = s.n_groups;
+    out->tail_committed = s.tail_committed;
+    out->draft_len = s.draft_len;
+  });
+}
+
+int vc_request_history(vc_engine* e, int slot, int32_t* out, int cap, int* n) {
+  return guard([&] {
+    const auto& h = E(e).seq(slot).history;
+    *n = static_cast<int>(h.size());
+    std::memcpy(out, h.data(), sizeof(int32_t) * std::min<size_t>(h.size(), cap));
+  });
+}
+
+int vc_compress(vc_engine* e, int slot, vc_compressed_meta* out) {
+  return guard([&] {
+    vc::Engine& en = E(e);
+    en.compress(slot);
+    const auto& m = en.model();
+    const vc::SeqState& s = en.seq(slot);
+    // size law of speckv::compress for quant-uniform (compressor.cpp:144-150)
+    speckv::CompressorSpec spec;
+    spec.kind = speckv::CompressorKind::QuantUniform;
+    spec.bits = en.config().quant_bits;
+    speckv::KvShape shape{m.layers, m.n_kv, s.committed, static_cast<speckv::Bytes>(m.d) * 2 * 2};
+    speckv::CompressedKVMeta meta = speckv::compress(spec, shape, 0.0, 0);
+    if (out) {
+      out->bit_scheme = meta.bit_scheme;
+      out->payload_bytes = meta.payload_bytes;
+      out->full_bytes = shape.full_bytes();
+      const int64_t groups = static_cast<int64_t>(s.n_groups) * m.layers * m.n_kv;
+      out->aux_bytes = groups * (static_cast<int64_t>(m.d) * 4 + VC_QGROUP * 4);
+      out->n_groups = s.n_groups;
+      out->tail_tokens = s.tail_committed;
+    }
+  });
+}
+
+int vc_compressed_geometry(vc_engine* e, int* group, int* words_per_group, int* tail_cap,
+                           int* max_groups) {
+  return guard([&] {
+    vc::Engine& en = E(e);
+    const auto q = en.quant_pool();
+    if (group) *group = VC_QGROUP;
+    if (words_per_group) *words_per_group = static_cast<int>(vc::quant_group_words(en.model().d, en.config().quant_bits));
+    if (tail_cap) *tail_cap = q.tail_cap;
+    if (max_groups) *max_groups = q.cap / VC_QGROUP;
+  });
+}
+
+int vc_compressed_read(vc_engine* e, int slot, int layer, int head, uint32_t* kcodes, uint32_t* ksz,
+                       uint32_t* vcodes, uint32_t* vsz, uint16_t* ktail, uint16_t* vtail) {
+  return guard([&] {
+    vc::Engine& en = E(e);
+    const auto& m = en.model();
+    const auto q = en.quant_pool();
+    if (en.config().quant_bits == 0) throw vc::ContractViolation("no compressed tier");
+    const size_t slice = (static_cast<size_t>(slot) * m.layers + layer) * m.n_kv + head;
+    const size_t words = static_cast<size_t>(q.cap) * m.d * en.config().quant_bits / 32;
+    const size_t groups = q.cap / VC_QGROUP;
+    auto cp = [&](void* dst, const void* src, size_t bytes) {
+      if (dst) vc::check_cuda(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost), "compressed_read");
+    };
+    cp(kcodes, q.kc + slice * words, words * 4);
+    cp(vcodes, q.vc + slice * words, words * 4);
+    cp(ksz, q.ksz + slice * groups * m.d, groups * m.d * 4);
+    cp(vsz, q.vsz + slice * q.cap, static_cast<size_t>(q.cap) * 4);
+    cp(ktail, q.ktail + slice * q.tail_cap * m.d, static_cast<size_t>(q.tail_cap) * m.d * 2);
+    cp(vtail, q.vtail + slice * q.tail_cap * m.d, static_cast<size_t>(q.tail_cap) * m.d * 2);
+  });
+}
+
+int64_t vc_drop_indices(int kind, int layers, int heads, int64_t tokens, double ratio, uint64_t seed,
+                        int sink_tokens, int64_t* out) {
+  int64_t drop = -1;
+  int rc = guard([&] {
+    speckv::CompressorSpec spec;
+    spec.kind = kind == 0 ? speckv::CompressorKind::DropUniform : speckv::CompressorKind::DropWindow;
+    spec.ratio = ratio;
+    spec.sink_tokens = sink_tokens;
+    speckv::KvShape shape{layers, heads, tokens, 2};
+    auto meta = speckv::compress(spec, shape, ratio, seed);
+    drop = meta.dropped_indices.empty() || meta.dropped_indices[0].empty()
+               ? 0
+               : static_cast<int64_t>(meta.dropped_indices[0][0].size());
+    if (out)
+      for (int l = 0; l < layers; ++l)
+        for (int h = 0; h < heads; ++h)
+          std::memcpy(out + (static_cast<size_t>(l) * heads + h) * drop,
+                      meta.dropped_indices[l][h].data(), sizeof(int64_t) * drop);
+  });
+  return rc == VC_OK ? drop : -rc;
+}
+
+int vc_update_window(int heads, int window, int sink_tokens, int n_req, const int64_t* tokens,
+                     const int64_t* req_begin, const int64_t* req_end, const int64_t* already,
+                     int64_t* out, int64_t cap, int64_t* n_new) {
+  return guard([&] {
+    speckv::CompressorSpec spec;
+    spec.kind = speckv::CompressorKind::DropWindow;
+    spec.mode = speckv::CompressorMode::Online;
+    spec.ratio = 0.5;
+    spec.window = window;
+    spec.sink_tokens = sink_tokens;
+    spec.validate();
+    std::vector<speckv::OnlineRequestKv> batch(n_req);
+    std::vector<std::pair<int64_t, int64_t>> offs;
+    for (int i = 0; i < n_req; ++i) {
+      batch[i].shape = speckv::KvShape{1, heads, tokens[i], 2};
+      batch[i].dropped_indices.assign(1, std::vector<std::vector<int64_t>>(heads));
+      for (int h = 0; h < heads; ++h)
+        for (int64_t k = 0; k < already[i]; ++k) batch[i].dropped_indices[0][h].push_back(sink_tokens + k);
+      offs.emplace_back(req_begin[i], req_end[i]);
+    }
+    auto res = speckv::update(spec, 0, batch, offs);
+    for (int i = 0; i < n_req; ++i) {
+      n_new[i] = static_cast<int64_t>(res[i][0].size());
+      for (int h = 0; h < heads; ++h)
+        for (int64_t k = 0; k < n_new[i] && k < cap; ++k) out[(static_cast<size_t>(i) * heads + h) * cap + k] = res[i][h][k];
+    }
+  });
+}
+
+int vc_topk_select(const float* scores, int rows, int T, int k, int32_t* kept, void* stream) {
+  return guard([&] {
+    if (k < 1 || k > T) throw speckv::ConfigError("topk: k out of [1, T]");
+    vc::check_cuda(vc::topk_select(scores, rows, T, k, kept, static_cast<cudaStream_t>(stream)), "topk_select");
+  });
+}
+
+int vc_key_scores(const uint16_t* keys, int rows, int T, int d, const float* w, float* scores,
+                  void* stream) {
+  return guard([&] {
+    vc::check_cuda(vc::key_scores(keys, rows, T, d, w, scores, static_cast<cudaStream_t>(stream)), "key_scores");
+  });
+}
+
+// ------------------------------------------------------------------ steps
+int vc_step(vc_engine* e, const vc_step_item* items, int n, int32_t* out_rows, float* logits) {
+  return guard([&] {
+    std::vector<vc::StepItem> its(n);
+    for (int i = 0; i < n; ++i) {
+      its[i].slot = items[i].slot;
+      its[i].mode = static_cast<vc::RowMode>(items[i].mode);
+      its[i].tokens.assign(items[i].tokens, items[i].tokens + items[i].n_tokens);
+      its[i].stage = items[i].stage;
+    }
+    std::vector<int32_t> out;
+    E(e).run_step(its, out, logits);
+    std::memcpy(out_rows, out.data(), out.size() * sizeof(int32_t));
+  });
+}
+
+int vc_decode_step(vc_engine* e, const int* slots, int n, int32_t* out_tokens) {
+  return guard([&] {
+    vc::Engine& en = E(e);
+    std::vector<vc::StepItem> its(n);
+    for (int i = 0; i < n; ++i) {
+      its[i].slot = slots[i];
+      its[i].mode = vc::RowMode::Decode;
+      its[i].tokens = {en.seq(slots[i]).pending};
+    }
+    std::vector<int32_t> out;
+    en.run_step(its, out);
+    for (int i = 0; i < n; ++i) {
+      en.commit_decode(slots[i], out[i]);
+      out_tokens[i] = out[i];
+    }
+  });
+}
+
+int vc_draft_step(vc_engine* e, const int* slots, int n, int32_t* out_tokens) {
+  return guard([&] {
+    vc::Engine& en = E(e);
+    std::vector<vc::StepItem> its(n);
+    for (int i = 0; i < n; ++i) {
+      const vc::SeqState& s = en.seq(slots[i]);
+      its[i].slot = slots[i];
+      its[i].mode = vc::RowMode::Draft;
+      its[i].tokens = {s.drafted.empty() ? s.pending : s.drafted.back()};
+    }
+    std::vector<int32_t> out;
+    en.run_step(its, out);
+    for (int i = 0; i < n; ++i) {
+      en.push_draft(slots[i], out[i]);
+      out_tokens[i] = out[i];
+    }
+  });
+}
+
+int vc_verify(vc_engine* e, const int* slots, int n, const int* stages, int32_t* preds) {
+  return guard([&] {
+    vc::Engine& en = E(e);
+    std::vector<vc::StepItem> its(n);
+    for (int i = 0; i < n; ++i) {
+      const vc::SeqState& s = en.seq(slots[i]);
+      its[i].slot = slots[i];
+      its[i].mode = vc::RowMode::Verify;
+      its[i].tokens.push_back(s.pending);
+      its[i].tokens.insert(its[i].tokens.end(), s.drafted.begin(), s.drafted.end());
+      its[i].stage = stages ? stages[i] : -1;
+    }
+    std::vector<int32_t> out;
+    en.run_step(its, out);
+    std::memcpy(preds, out.data(), out.size() * sizeof(int32_t));
+  });
+}
+
+int vc_accept(const int32_t* drafted, const int32_t* preds, int x, int32_t* accepted, int* n_accepted,
+              int* first_mismatch, int* bonus) {
+  return guard([&] {
+    auto r = speckv::accept(std::span<const int32_t>(drafted, x), std::span<const int32_t>(preds, x + 1));
+    std::memcpy(accepted, r.accepted.data(), r.accepted.size() * sizeof(int32_t));
+    *n_accepted = static_cast<int>(r.accepted.size());
+    *first_mismatch = r.first_mismatch.value_or(0);
+    *bonus = r.bonus_used ? 1 : 0;
+  });
+}
+
+int vc_accept_commit(vc_engine* e, int slot, const int32_t* preds, int stage, int32_t* emitted,
+                     int* n_emitted) {
+  return guard([&] {
+    vc::Engine& en = E(e);
+    const int x = static_cast<int>(en.seq(slot).drafted.size());
+    std::vector<int32_t> p(preds, preds + x + 1);
+    auto em = en.accept_commit(slot, p, stage);
+    std::memcpy(emitted, em.data(), em.size() * sizeof(int32_t));
+    *n_emitted = static_cast<int>(em.size());
+  });
+}
+
+int vc_swap_begin(vc_engine* e, int slot, int stage, uint64_t* transfer_id) {
+  return guard([&] { *transfer_id = E(e).swap_begin(slot, stage); });
+}
+
+int vc_swap_poll(vc_engine* e, uint64_t transfer_id, int* done) {
+  return guard([&] { *done = E(e).swap_done(transfer_id) ? 1 : 0; });
+}
+
+// ------------------------------------------------------------------ loops
+int vc_run_decode(vc_engine* e, const int* slots, int n, int K, int32_t* out, double* ms) {
+  return guard([&] {
+    vc::Engine& en = E(e);
+    std::vector<vc::StepItem> its(n);
+    std::vector<int32_t> row;
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int k = 0; k < K; ++k) {
+      for (int i = 0; i < n; ++i) {
+        its[i].slot = slots[i];
+        its[i].mode = vc::RowMode::Decode;
+        its[i].tokens = {en.seq(slots[i]).pending};
+      }
+      en.run_step(its, row);
+      for (int i = 0; i < n; ++i) {
+        en.commit_decode(slots[i], row[i]);
+        out[static_cast<size_t>(i) * K + k] = row[i];
+      }
+    }
+    const auto t1 = std::chrono::steady_clock::now();
+    if (ms) *ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+  });
+}
+
+int vc_run_speculative(vc_engine* e, const int* slots, int n, int K, int x, int32_t* out,
+                       int32_t* rounds, int max_rounds, int* n_rounds, double* ms) {
+  return guard([&] {
+    vc::Engine& en = E(e);
+    if (x < 1 || x > en.config().max_x) throw speckv::ConfigError("run_speculative: x out of [1, max_x]");
+    if (en.config().full_tier != 0) throw vc::ContractViolation("lock-step loop needs the HBM full tier");
+    std::vector<int> produced(n, 0), nr(n, 0);
+    std::vector<vc::StepItem> its;
+    std::vector<int32_t> row;
+    const auto t0 = std::chrono::steady_clock::now();
+    for (;;) {
+      std::vector<int> act;
+      for (int i = 0; i < n; ++i)
+        if (produced[i] < K) act.push_back(i);
+      if (act.empty()) break;
+      for (int j = 0; j < x; ++j) {  // x draft steps over the compressed tier
+        its.assign(act.size(), vc::StepItem{});
+        for (size_t a = 0; a < act.size(); ++a) {
+          const vc::SeqState& s = en.seq(slots[act[a]]);
+          its[a].slot = slots[act[a]];
+          its[a].mode = vc::RowMode::Draft;
+          its[a].tokens = {s.drafted.empty() ? s.pending : s.drafted.back()};
+        }
+        en.run_step(its, row);
+        for (size_t a = 0; a < act.size(); ++a) en.push_draft(slots[act[a]], row[a]);
+      }
+      its.assign(act.size(), vc::StepItem{});  // one verify pass over the full KV
+      for (size_t a = 0; a < act.size(); ++a) {
+        const vc::SeqState& s = en.seq(slots[act[a]]);
+        its[a].slot = slots[act[a]];
+        its[a].mode = vc::RowMode::Verify;
+        its[a].tokens.push_back(s.pending);
+        its[a].tokens.insert(its[a].tokens.end(), s.drafted.begin(), s.drafted.end());
+      }
+      en.run_step(its, row);
+      size_t off = 0;
+      for (size_t a = 0; a < act.size(); ++a) {
+        const int i = act[a];
+        std::vector<int32_t> p(row.begin() + off, row.begin() + off + x + 1);
+        off += x + 1;
+        auto em = en.accept_commit(slots[i], p);
+        if (rounds && nr[i] < max_rounds) rounds[static_cast<size_t>(i) * max_rounds + nr[i]] = static_cast<int32_t>(em.size());
+        ++nr[i];
+        for (int32_t t : em)
+          if (produced[i] < K) out[static_cast<size_t>(i) * K + produced[i]++] = t;  // truncate at K
+      }
+    }
+    const auto t1 = std::chrono::steady_clock::now();
+    if (ms) *ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+    if (n_rounds)
+      for (int i = 0; i < n; ++i) n_rounds[i] = nr[i];
+  });
+}
+
+int vc_run_scheduled(vc_engine* e, const int* slots, int n, const vc_sched_desc* sd, int32_t* out,
+                     vc_sched_stats* stats) {
+  return guard([&] {
+    if (!sd) throw vc::ContractViolation("vc_run_scheduled: null descriptor");
+    vc_run_scheduled_impl(E(e), slots, n, *sd, out, stats);
+  });
+}
+
+int vc_reload_span(int64_t bytes, double bandwidth, double iteration_time, double* iterations,
+                   int* windows) {
+  return guard([&] {
+    auto s = speckv::reload_span(bytes, bandwidth, iteration_time);
+    *iterations = s.iterations;
+    *windows = s.windows;
+  });
+}
+
+// ------------------------------------------------------------ kernel level
+int vc_quant_kivi_slice(const uint16_t* k, const uint16_t* v, int n_groups, int d, int bits,
+                        uint32_t* kcodes, uint32_t* ksz, uint32_t* vcodes, uint32_t* vsz, void* stream) {
+  return guard([&] {
+    vc::QuantJob j{k, v, kcodes, ksz, vcodes, vsz, 0, n_groups};
+    vc::QuantJob* dj = nullptr;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    vc::check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&dj), sizeof(j), st), "malloc");
+    vc::check_cuda(cudaMemcpyAsync(dj, &j, sizeof(j), cudaMemcpyHostToDevice, st), "memcpy");
+    vc::check_cuda(vc::quant_kivi(dj, 1, n_groups, d, bits, st), "quant_kivi");
+    vc::check_cuda(cudaFreeAsync(dj, st), "free");
+    vc::check_cuda(cudaStreamSynchronize(st), "sync");
+  });
+}
+
+int vc_attention_probe(vc_engine* e, int slot, int layer, int mode, const uint16_t* q_dev, int n_rows,
+                       int kv_len, uint16_t* out_host) {
+  return guard([&] { E(e).attention_probe(slot, layer, mode, q_dev, n_rows, kv_len, out_host); });
+}
+
+int vc_gemm_probe(const uint16_t* X, int M, int K, const uint16_t* W, int N, float* Y, void* stream) {
+  return guard([&] {
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const int s = vc::gemm_splits(N, K);
+    float* ws = nullptr;
+    vc::check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&ws), sizeof(float) * s * M * N, st), "malloc");
+    vc::check_cuda(vc::gemm_partial(X, M, K, W, N, s, ws, st), "gemm_partial");
+    vc::check_cuda(vc::sum_epilogue(ws, s, M, N, Y, st), "sum_epilogue");
+    vc::check_cuda(cudaFreeAsync(ws, st), "free");
+    vc::check_cuda(cudaStreamSynchronize(st), "sync");
+  });
+}
+
+}  // extern "C"

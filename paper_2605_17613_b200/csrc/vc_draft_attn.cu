@@ -1,0 +1,356 @@
+// vc_draft_attn.cu -- draft decode attention over the KIVI-compressed cache.
+//
+// One query token per drafting sequence, n_rep query heads per kv head (GQA).
+// HBM-bound: every code byte is read exactly once, straight into registers
+// with 128-bit streaming loads (no shared-memory round trip), and consumed by
+// legacy mma.sync tensor-core tiles:
+//   S^T[tok, head] = Kcodes[tok, ch] . q'^T[ch, head],  q' = q * kscale (per group)
+//   O^T[ch, head]  = Vcodes^T[ch, tok] . P'^T[tok, head], P' = P * vscale (per token)
+// Dequantisation is folded algebraically into q' / P' and two per-head
+// constants (zero points, and the 1024 bias of the lop3 int->fp16 trick), so
+// the inner loop is lop3 + mma only.  Codes arrive in mma A-fragment order
+// (written by vc_quant.cu), the P' B-fragments come from the S C-fragments
+// through movmatrix.trans, and the online softmax runs on warp shuffles.
+// Split-K over 1024-token chunks + one bf16-tail CTA; attention_combine
+// merges the partials (LSE) in chunk order.
+//
+// The reference models this step as a pure HBM read of the compressed cache
+// (/root/reference/proj/src/scheduler.cpp:452-457, sim.cpp:254-256).
+#include "vc_common.cuh"
+#include "vc_kernels.h"
+
+namespace vc {
+namespace {
+
+constexpr int kG = VC_QGROUP;
+constexpr int kCG = VC_DRAFT_CG;
+constexpr int kWarps = 4;
+
+template <int D, int NREP>
+VC_DEV void write_partial(const AttnShape& s, const AttnSeq& sq, int h, int chunk, float* sm_m,
+                          float* sm_l, float* sm_o, Partials part) {
+  // sm_m/sm_l: [kWarps][8]; sm_o: [kWarps][8][D]
+  const int hq0 = h * NREP;
+  const int Hq = s.n_kv * NREP;
+  for (int idx = threadIdx.x; idx < NREP * D; idx += blockDim.x) {
+    const int n = idx / D, c = idx % D;
+    float M = -INFINITY;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) M = fmaxf(M, sm_m[w * 8 + n]);
+    float o = 0.f, l = 0.f;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) {
+      const float mw = sm_m[w * 8 + n];
+      const float f = (mw == -INFINITY) ? 0.f : exp2f(mw - M);
+      o += f * sm_o[(w * 8 + n) * D + c];
+      l += f * sm_l[w * 8 + n];
+    }
+    const size_t prow = static_cast<size_t>(sq.part0 + chunk) * Hq + hq0 + n;
+    part.o[prow * D + c] = o;
+    if (c == 0) {
+      part.ml[prow * 2] = M;
+      part.ml[prow * 2 + 1] = l;
+    }
+  }
+}
+
+template <int D, int BITS, int NREP>
+__global__ void __launch_bounds__(128) draft_attn_quant_kernel(AttnShape s, QuantPool pool,
+                                                               int layer, const uint16_t* qkv,
+                                                               const AttnSeq* seqs, int max_chunks,
+                                                               Partials part) {
+  static_assert(NREP <= 8, "n_rep > 8 needs two head tiles");
+  constexpr int KS = D / 16;                    // channel k-steps / tiles
+  constexpr int W = (BITS == 4) ? KS : KS / 2;  // u32 per lane per 16-token tile
+  constexpr int CH = W < 4 ? W : 4;
+  constexpr int MT = kG / 16;                   // 16-token tiles per group
+  constexpr size_t GW = static_cast<size_t>(kG) * D * BITS / 32;  // u32 per group
+  constexpr uint32_t MASK = BITS == 4 ? 0x000f000fu : 0x00030003u;
+
+  __shared__ float sq_q[8 * D];                         // scaled q, head-major
+  __shared__ __align__(16) uint32_t s_ksz[kWarps][D];
+  __shared__ __align__(16) uint32_t s_vsz[kWarps][kG];
+  __shared__ float sm_m[kWarps * 8], sm_l[kWarps * 8];
+  __shared__ float sm_o[kWarps * 8 * D];
+
+  const AttnSeq sq = seqs[blockIdx.z];
+  const int h = blockIdx.y;
+  const int chunk = blockIdx.x;
+  const bool tail = chunk == max_chunks;
+  const int n_chunks = (sq.n_groups + kCG - 1) / kCG;
+  if (tail ? sq.tail_len == 0 : chunk >= n_chunks) return;
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const size_t slice = (static_cast<size_t>(sq.slot) * s.layers + layer) * s.n_kv + h;
+
+  // q heads h*NREP .. h*NREP+NREP-1 are contiguous in the qkv row.
+  const uint16_t* qrow = qkv + static_cast<size_t>(sq.row0) * s.q_stride + static_cast<size_t>(h) * NREP * D;
+  for (int i = threadIdx.x; i < 8 * D; i += blockDim.x)
+    sq_q[i] = (i < NREP * D) ? bf2f(qrow[i]) * s.scale_log2 : 0.f;
+  __syncthreads();
+
+  if (tail) {
+    // ---- bf16 tail (residual group + draft window), CUDA cores ----------
+    constexpr int CPL = D / 32;  // channels per lane
+    const uint16_t* kt = pool.ktail + slice * pool.tail_cap * D;
+    const uint16_t* vt = pool.vtail + slice * pool.tail_cap * D;
+    float m[NREP], l[NREP], o[NREP][CPL];
+#pragma unroll
+    for (int n = 0; n < NREP; ++n) {
+      m[n] = -INFINITY;
+      l[n] = 0.f;
+#pragma unroll
+      for (int j = 0; j < CPL; ++j) o[n][j] = 0.f;
+    }
+    for (int t = warp; t < sq.tail_len; t += kWarps) {
+      float kv[CPL], vv[CPL];
+#pragma unroll
+      for (int j = 0; j < CPL; ++j) {
+        kv[j] = bf2f(kt[static_cast<size_t>(t) * D + lane * CPL + j]);
+        vv[j] = bf2f(vt[static_cast<size_t>(t) * D + lane * CPL + j]);
+      }
+#pragma unroll
+      for (int n = 0; n < NREP; ++n) {
+        float d = 0.f;
+#pragma unroll
+        for (int j = 0; j < CPL; ++j) d += sq_q[n * D + lane * CPL + j] * kv[j];
+        d = warp_sum(d);
+        const float mn = fmaxf(m[n], d);
+        const float a = exp2f(m[n] - mn);
+        const float p = exp2f(d - mn);
+        l[n] = l[n] * a + p;
+#pragma unroll
+        for (int j = 0; j < CPL; ++j) o[n][j] = o[n][j] * a + p * vv[j];
+        m[n] = mn;
+      }
+    }
+#pragma unroll
+    for (int n = 0; n < 8; ++n) {
+      if (lane == 0) {
+        sm_m[warp * 8 + n] = n < NREP ? m[n < NREP ? n : 0] : -INFINITY;
+        sm_l[warp * 8 + n] = n < NREP ? l[n < NREP ? n : 0] : 0.f;
+      }
+    }
+#pragma unroll
+    for (int n = 0; n < NREP; ++n)
+#pragma unroll
+      for (int j = 0; j < CPL; ++j) sm_o[(warp * 8 + n) * D + lane * CPL + j] = o[n][j];
+    __syncthreads();
+    write_partial<D, NREP>(s, sq, h, max_chunks, sm_m, sm_l, sm_o, part);
+    return;
+  }
+
+  // ---- quantised groups ------------------------------------------------------
+  const uint32_t* kc = pool.kc + slice * (static_cast<size_t>(pool.cap) * D * BITS / 32);
+  const uint32_t* vc = pool.vc + slice * (static_cast<size_t>(pool.cap) * D * BITS / 32);
+  const uint32_t* ksz = pool.ksz + slice * (static_cast<size_t>(pool.cap / kG) * D);
+  const uint32_t* vsz = pool.vsz + slice * static_cast<size_t>(pool.cap);
+
+  const int hn = lane >> 2;         // head column this lane feeds in B fragments
+  const int hc0 = 2 * (lane & 3);   // head columns this lane holds in C fragments
+  float mrun0 = -INFINITY, mrun1 = -INFINITY;
+  float lsum0 = 0.f, lsum1 = 0.f, corr0 = 0.f, corr1 = 0.f;
+  float oacc[KS][4];
+#pragma unroll
+  for (int ct = 0; ct < KS; ++ct) oacc[ct][0] = oacc[ct][1] = oacc[ct][2] = oacc[ct][3] = 0.f;
+
+  const int g_end = min((chunk + 1) * kCG, sq.n_groups);
+  for (int g = chunk * kCG + warp; g < g_end; g += kWarps) {
+    // stage this group's scale/zero pairs (per channel for K, per token for V)
+    for (int i = lane * 4; i < D; i += 128)
+      *reinterpret_cast<uint4*>(&s_ksz[warp][i]) = *reinterpret_cast<const uint4*>(ksz + static_cast<size_t>(g) * D + i);
+    for (int i = lane * 4; i < kG; i += 128)
+      *reinterpret_cast<uint4*>(&s_vsz[warp][i]) = *reinterpret_cast<const uint4*>(vsz + static_cast<size_t>(g) * kG + i);
+
+    // K codes for the whole group: MT tiles x W words per lane
+    uint32_t kw[MT][W];
+    const uint32_t* kg = kc + static_cast<size_t>(g) * GW;
+#pragma unroll
+    for (int m = 0; m < MT; ++m)
+#pragma unroll
+      for (int wq = 0; wq < W / CH; ++wq) {
+        const uint32_t* p = kg + (static_cast<size_t>(m * (W / CH) + wq) * 32 + lane) * CH;
+        if constexpr (CH == 4) {
+          uint4 v = ldg_stream(p);
+          kw[m][wq * 4 + 0] = v.x; kw[m][wq * 4 + 1] = v.y; kw[m][wq * 4 + 2] = v.z; kw[m][wq * 4 + 3] = v.w;
+        } else {
+          uint2 v = ldg_stream64(p);
+          kw[m][wq * 2 + 0] = v.x; kw[m][wq * 2 + 1] = v.y;
+        }
+      }
+    __syncwarp();
+
+    // q' = q * kscale as fp16 B fragments; per-head constant term
+    uint32_t b0[KS], b1[KS];
+    float bias_part = 0.f;
+#pragma unroll
+    for (int st = 0; st < KS; ++st) {
+      const int c0 = st * 16 + 2 * (lane & 3);
+      const int cs[4] = {c0, c0 + 1, c0 + 8, c0 + 9};
+      float qp[4];
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const uint32_t sz = s_ksz[warp][cs[e]];
+        const float sc = h2f(static_cast<uint16_t>(sz & 0xffffu));
+        const float zr = h2f(static_cast<uint16_t>(sz >> 16));
+        const float q = sq_q[hn * D + cs[e]];
+        qp[e] = q * sc;
+        // zero point and the -1024 fold use the fp16-rounded q' the MMA sees
+        bias_part += q * zr - 1024.f * h2f(f2h(qp[e]));
+      }
+      b0[st] = pack_h2(qp[0], qp[1]);
+      b1[st] = pack_h2(qp[2], qp[3]);
+    }
+    bias_part += __shfl_xor_sync(0xffffffffu, bias_part, 1);
+    bias_part += __shfl_xor_sync(0xffffffffu, bias_part, 2);
+    const float bias0 = __shfl_sync(0xffffffffu, bias_part, hc0 * 4);
+    const float bias1 = __shfl_sync(0xffffffffu, bias_part, (hc0 + 1) * 4);
+
+    // S^T tiles
+    float sacc[MT][4];
+#pragma unroll
+    for (int m = 0; m < MT; ++m) {
+      sacc[m][0] = sacc[m][1] = sacc[m][2] = sacc[m][3] = 0.f;
+#pragma unroll
+      for (int st = 0; st < KS; ++st) {
+        const uint32_t w = (BITS == 4) ? kw[m][st] : kw[m][st >> 1];
+        const int sh = (BITS == 4) ? 0 : 8 * (st & 1);
+        const uint32_t a0 = nib_to_h2(w >> (sh + 0 * BITS), MASK);
+        const uint32_t a1 = nib_to_h2(w >> (sh + 1 * BITS), MASK);
+        const uint32_t a2 = nib_to_h2(w >> (sh + 2 * BITS), MASK);
+        const uint32_t a3 = nib_to_h2(w >> (sh + 3 * BITS), MASK);
+        mma_f16(sacc[m], a0, a1, a2, a3, b0[st], b1[st]);
+      }
+      sacc[m][0] += bias0; sacc[m][1] += bias1; sacc[m][2] += bias0; sacc[m][3] += bias1;
+    }
+
+    // V codes (issued before the softmax math so the loads overlap it)
+    uint32_t vw[MT][W];
+    const uint32_t* vg = vc + static_cast<size_t>(g) * GW;
+#pragma unroll
+    for (int m = 0; m < MT; ++m)
+#pragma unroll
+      for (int wq = 0; wq < W / CH; ++wq) {
+        const uint32_t* p = vg + (static_cast<size_t>(m * (W / CH) + wq) * 32 + lane) * CH;
+        if constexpr (CH == 4) {
+          uint4 v = ldg_stream(p);
+          vw[m][wq * 4 + 0] = v.x; vw[m][wq * 4 + 1] = v.y; vw[m][wq * 4 + 2] = v.z; vw[m][wq * 4 + 3] = v.w;
+        } else {
+          uint2 v = ldg_stream64(p);
+          vw[m][wq * 2 + 0] = v.x; vw[m][wq * 2 + 1] = v.y;
+        }
+      }
+
+    // online softmax (columns hc0, hc0+1; rows spread over lane>>2 and +8)
+    float gm0 = -INFINITY, gm1 = -INFINITY;
+#pragma unroll
+    for (int m = 0; m < MT; ++m) {
+      gm0 = fmaxf(gm0, fmaxf(sacc[m][0], sacc[m][2]));
+      gm1 = fmaxf(gm1, fmaxf(sacc[m][1], sacc[m][3]));
+    }
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) {
+      gm0 = fmaxf(gm0, __shfl_xor_sync(0xffffffffu, gm0, o));
+      gm1 = fmaxf(gm1, __shfl_xor_sync(0xffffffffu, gm1, o));
+    }
+    const float mn0 = fmaxf(mrun0, gm0), mn1 = fmaxf(mrun1, gm1);
+    const float al0 = exp2f(mrun0 - mn0), al1 = exp2f(mrun1 - mn1);
+    mrun0 = mn0;
+    mrun1 = mn1;
+    lsum0 *= al0; lsum1 *= al1; corr0 *= al0; corr1 *= al1;
+#pragma unroll
+    for (int ct = 0; ct < KS; ++ct) {
+      oacc[ct][0] *= al0; oacc[ct][1] *= al1; oacc[ct][2] *= al0; oacc[ct][3] *= al1;
+    }
+    uint32_t bp0[MT], bp1[MT];
+#pragma unroll
+    for (int m = 0; m < MT; ++m) {
+      const int r = m * 16 + (lane >> 2);
+      const uint32_t sz_a = s_vsz[warp][r], sz_b = s_vsz[warp][r + 8];
+      const float vs_a = h2f(static_cast<uint16_t>(sz_a & 0xffffu)), vz_a = h2f(static_cast<uint16_t>(sz_a >> 16));
+      const float vs_b = h2f(static_cast<uint16_t>(sz_b & 0xffffu)), vz_b = h2f(static_cast<uint16_t>(sz_b >> 16));
+      const float p0 = exp2f(sacc[m][0] - mn0), p1 = exp2f(sacc[m][1] - mn1);
+      const float p2 = exp2f(sacc[m][2] - mn0), p3 = exp2f(sacc[m][3] - mn1);
+      lsum0 += p0 + p2;
+      lsum1 += p1 + p3;
+      const uint32_t pk01 = pack_h2(p0 * vs_a, p1 * vs_a);
+      const uint32_t pk23 = pack_h2(p2 * vs_b, p3 * vs_b);
+      const __half2 h01 = *reinterpret_cast<const __half2*>(&pk01);
+      const __half2 h23 = *reinterpret_cast<const __half2*>(&pk23);
+      corr0 += p0 * vz_a + p2 * vz_b - 1024.f * (__low2float(h01) + __low2float(h23));
+      corr1 += p1 * vz_a + p3 * vz_b - 1024.f * (__high2float(h01) + __high2float(h23));
+      bp0[m] = movmatrix_trans(pk01);
+      bp1[m] = movmatrix_trans(pk23);
+    }
+
+    // O^T += Vcodes^T . P'^T
+#pragma unroll
+    for (int m = 0; m < MT; ++m)
+#pragma unroll
+      for (int ct = 0; ct < KS; ++ct) {
+        const uint32_t w = (BITS == 4) ? vw[m][ct] : vw[m][ct >> 1];
+        const int sh = (BITS == 4) ? 0 : 8 * (ct & 1);
+        const uint32_t a0 = nib_to_h2(w >> (sh + 0 * BITS), MASK);
+        const uint32_t a1 = nib_to_h2(w >> (sh + 1 * BITS), MASK);
+        const uint32_t a2 = nib_to_h2(w >> (sh + 2 * BITS), MASK);
+        const uint32_t a3 = nib_to_h2(w >> (sh + 3 * BITS), MASK);
+        mma_f16(oacc[ct], a0, a1, a2, a3, bp0[m], bp1[m]);
+      }
+    __syncwarp();
+  }
+
+  // reduce the per-lane sums over the 8 lanes sharing a head column
+#pragma unroll
+  for (int o = 4; o < 32; o <<= 1) {
+    lsum0 += __shfl_xor_sync(0xffffffffu, lsum0, o);
+    lsum1 += __shfl_xor_sync(0xffffffffu, lsum1, o);
+    corr0 += __shfl_xor_sync(0xffffffffu, corr0, o);
+    corr1 += __shfl_xor_sync(0xffffffffu, corr1, o);
+  }
+  if (lane < 4) {
+    sm_m[warp * 8 + hc0] = mrun0;
+    sm_m[warp * 8 + hc0 + 1] = mrun1;
+    sm_l[warp * 8 + hc0] = lsum0;
+    sm_l[warp * 8 + hc0 + 1] = lsum1;
+  }
+#pragma unroll
+  for (int ct = 0; ct < KS; ++ct) {
+    const int c = ct * 16 + (lane >> 2);
+    sm_o[(warp * 8 + hc0) * D + c] = oacc[ct][0] + corr0;
+    sm_o[(warp * 8 + hc0 + 1) * D + c] = oacc[ct][1] + corr1;
+    sm_o[(warp * 8 + hc0) * D + c + 8] = oacc[ct][2] + corr0;
+    sm_o[(warp * 8 + hc0 + 1) * D + c + 8] = oacc[ct][3] + corr1;
+  }
+  __syncthreads();
+  write_partial<D, NREP>(s, sq, h, chunk, sm_m, sm_l, sm_o, part);
+}
+
+template <int D, int BITS, int NREP>
+cudaError_t launch_draft(const AttnShape& s, const QuantPool& pool, int layer, const uint16_t* qkv,
+                         const AttnSeq* seqs, int n_seq, int max_chunks, Partials part,
+                         cudaStream_t st) {
+  dim3 grid(max_chunks + 1, s.n_kv, n_seq);
+  draft_attn_quant_kernel<D, BITS, NREP><<<grid, 128, 0, st>>>(s, pool, layer, qkv, seqs, max_chunks, part);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+cudaError_t draft_attention_quant(const AttnShape& s, const QuantPool& pool, int layer,
+                                  const uint16_t* qkv, const AttnSeq* seqs, int n_seq,
+                                  int max_chunks, int bits, Partials part, cudaStream_t st) {
+  if (n_seq <= 0) return cudaSuccess;
+#define VC_DRAFT_CASE(D_, B_, R_)                                                   \
+  if (s.d == D_ && bits == B_ && s.n_rep == R_)                                    \
+    return launch_draft<D_, B_, R_>(s, pool, layer, qkv, seqs, n_seq, max_chunks, part, st);
+  VC_DRAFT_CASE(128, 4, 4)
+  VC_DRAFT_CASE(128, 2, 4)
+  VC_DRAFT_CASE(128, 4, 8)
+  VC_DRAFT_CASE(128, 2, 8)
+  VC_DRAFT_CASE(64, 4, 4)
+  VC_DRAFT_CASE(64, 2, 4)
+#undef VC_DRAFT_CASE
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace vc

@@ -1,0 +1,745 @@
+// vc_engine.cu -- host side of the B200 decode loop (see vc_engine.hpp).
+#include "vc_engine.hpp"
+
+#include <cuda_bf16.h>
+
+#include <cmath>
+#include <cstring>
+#include <sstream>
+#include <stdexcept>
+
+namespace vc {
+
+void check_cuda(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+#define VC_CK(expr) check_cuda((expr), #expr)
+#define VC_LAUNCH(expr)           \
+  do {                            \
+    check_cuda((expr), #expr);    \
+    ++launches_;                  \
+  } while (0)
+
+namespace {
+
+size_t round_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+
+template <class T>
+T* dmalloc(size_t n) {
+  void* p = nullptr;
+  if (n == 0) n = 1;
+  check_cuda(cudaMalloc(&p, n * sizeof(T)), "cudaMalloc");
+  return static_cast<T*>(p);
+}
+
+// Synthetic prefix KV, bit-identical with tests/oracle_data.py.
+__global__ void synth_kv_kernel(uint16_t* kbase, uint16_t* vbase, int cap, int n_ctx, int d,
+                                int n_slices, uint64_t seed, float k_norm, float k_out,
+                                int outlier_period) {
+  const size_t per = static_cast<size_t>(n_ctx) * d;
+  const size_t total = per * n_slices;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const size_t slice = i / per, rem = i % per;
+    const int c = static_cast<int>(rem % d);
+    auto val = [&](uint64_t s, float k) {
+      uint64_t x = i + 0x9e3779b97f4a7c15ull;
+      x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+      x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+      x = x ^ (x >> 31);
+      uint64_t h = s ^ x;
+      h += 0x9e3779b97f4a7c15ull;
+      h = (h ^ (h >> 30)) * 0xbf58476d1ce4e5b9ull;
+      h = (h ^ (h >> 27)) * 0x94d049bb133111ebull;
+      h = h ^ (h >> 31);
+      const int sm = static_cast<int>(h & 0xffff) + static_cast<int>((h >> 16) & 0xffff) +
+                     static_cast<int>((h >> 32) & 0xffff) + static_cast<int>((h >> 48) & 0xffff);
+      return __bfloat16_as_ushort(__float2bfloat16_rn(__fmul_rn(static_cast<float>(sm - 131070), k)));
+    };
+    const bool outlier = outlier_period > 0 && (c % outlier_period) == outlier_period - 1;
+    const size_t dst = slice * static_cast<size_t>(cap) * d + rem;
+    kbase[dst] = val(seed, outlier ? k_out : k_norm);
+    vbase[dst] = val(seed ^ 0x5555555555555555ull, k_norm);
+  }
+}
+
+}  // namespace
+
+size_t Engine::full_kv_bytes_per_token() const {
+  const auto& m = cfg_.model;
+  return static_cast<size_t>(m.layers) * m.n_kv * m.d * 2 * 2;
+}
+
+Engine::Engine(const EngineConfig& cfg, int device) : cfg_(cfg), device_(device) {
+  const auto& m = cfg_.model;
+  if (m.n_q % m.n_kv != 0 || (m.d != 64 && m.d != 128)) throw ContractViolation("unsupported head geometry");
+  if (cfg_.quant_bits != 0 && cfg_.quant_bits != 2 && cfg_.quant_bits != 4)
+    throw ContractViolation("quant_bits must be 0, 2 or 4");
+  VC_CK(cudaSetDevice(device_));
+  VC_CK(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
+  VC_CK(cudaStreamCreateWithFlags(&copy_st_, cudaStreamNonBlocking));
+  VC_CK(cudaEventCreate(&ev_a_));
+  VC_CK(cudaEventCreate(&ev_b_));
+  alloc_all();
+  seqs_.resize(cfg_.max_slots);
+}
+
+Engine::~Engine() {
+  cudaSetDevice(device_);
+  cudaStreamSynchronize(st_);
+  cudaStreamSynchronize(copy_st_);
+  for (auto& [k, g] : graphs_) cudaGraphExecDestroy(g);
+  for (auto& [k, e] : xfers_) cudaEventDestroy(e);
+  void* ptrs[] = {weight_blob_, rope_cos_, rope_sin_, full_.k, full_.v, stage_.k, stage_.v,
+                  quant_.kc, quant_.ksz, quant_.vc, quant_.vsz, quant_.ktail, quant_.vtail,
+                  x_, xn_, qkv_, attn_, act_, ws_, logits_, tok_in_, tok_out_, part_.o, part_.ml,
+                  rows_dev_, seqs_dev_, jobs_dev_};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  if (host_k_) cudaFreeHost(host_k_);
+  if (host_v_) cudaFreeHost(host_v_);
+  if (h_desc_) cudaFreeHost(h_desc_);
+  if (h_out_) cudaFreeHost(h_out_);
+  cudaEventDestroy(ev_a_);
+  cudaEventDestroy(ev_b_);
+  cudaStreamDestroy(st_);
+  cudaStreamDestroy(copy_st_);
+}
+
+void Engine::attention_probe(int slot, int layer, int mode, const uint16_t* q_dev, int n_rows,
+                             int kv_len, uint16_t* out_host) {
+  const auto& m = cfg_.model;
+  const SeqState& s = seqs_.at(slot);
+  if (n_rows < 1 || n_rows > Mmax_) throw ContractViolation("probe: bad n_rows");
+  AttnShape as;
+  as.layers = m.layers;
+  as.n_kv = m.n_kv;
+  as.n_rep = m.n_q / m.n_kv;
+  as.d = m.d;
+  as.q_stride = m.n_q * m.d;
+  as.out_stride = m.n_q * m.d;
+  as.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(m.d)));
+  AttnSeq a{};
+  a.slot = cfg_.full_tier == 1 && mode != 1 ? 0 : slot;
+  a.row0 = 0;
+  a.n_rows = n_rows;
+  a.kv_len = kv_len;
+  a.n_groups = s.n_groups;
+  a.tail_len = s.tail_committed;
+  a.part0 = 0;
+  AttnSeq* h = reinterpret_cast<AttnSeq*>(h_desc_);
+  *h = a;
+  VC_CK(cudaMemcpyAsync(seqs_dev_, h, sizeof(AttnSeq), cudaMemcpyHostToDevice, st_));
+  if (mode == 1) {
+    if (n_rows != 1) throw ContractViolation("probe: draft mode takes one row");
+    VC_LAUNCH(draft_attention_quant(as, quant_, layer, q_dev, seqs_dev_, 1, max_chunks_q_,
+                                    cfg_.quant_bits, part_, st_));
+    VC_LAUNCH(attention_combine(as, seqs_dev_, 1, max_chunks_q_, 1, 0, part_, attn_, st_));
+  } else {
+    const KvPool pool = cfg_.full_tier == 0 ? full_ : stage_;
+    VC_LAUNCH(dense_attention(as, pool, layer, q_dev, seqs_dev_, 1, max_chunks_d_, n_rows, part_, st_));
+    VC_LAUNCH(attention_combine(as, seqs_dev_, 1, max_chunks_d_, n_rows, 1, part_, attn_, st_));
+  }
+  VC_CK(cudaMemcpyAsync(out_host, attn_, static_cast<size_t>(n_rows) * m.n_q * m.d * 2,
+                        cudaMemcpyDeviceToHost, st_));
+  VC_CK(cudaStreamSynchronize(st_));
+}
+
+void Engine::alloc_all() {
+  const auto& m = cfg_.model;
+  const int L = m.layers, H = m.hidden, F = m.ffn, V = m.vocab, d = m.d;
+  const int qkv_n = (m.n_q + 2 * m.n_kv) * d;
+  // ---- weights: one blob, 256-B aligned tensors --------------------------
+  std::vector<size_t> sizes;
+  auto add = [&](size_t elems) { sizes.push_back(round_up(elems * 2, 256)); };
+  add(static_cast<size_t>(V) * H);
+  for (int l = 0; l < L; ++l) {
+    add(H);
+    add(static_cast<size_t>(qkv_n) * H);
+    add(static_cast<size_t>(H) * m.n_q * d);
+    add(H);
+    add(static_cast<size_t>(2) * F * H);
+    add(static_cast<size_t>(H) * F);
+  }
+  add(H);
+  add(static_cast<size_t>(V) * H);
+  size_t total = 0;
+  for (size_t s : sizes) total += s;
+  weight_bytes_ = total;
+  VC_CK(cudaMalloc(&weight_blob_, total));
+  uint8_t* p = static_cast<uint8_t*>(weight_blob_);
+  size_t idx = 0;
+  auto take = [&]() {
+    uint16_t* r = reinterpret_cast<uint16_t*>(p);
+    p += sizes[idx++];
+    return r;
+  };
+  w_.embed = take();
+  for (int l = 0; l < L; ++l) {
+    w_.attn_norm.push_back(take());
+    w_.wqkv.push_back(take());
+    w_.wo.push_back(take());
+    w_.mlp_norm.push_back(take());
+    w_.wgu.push_back(take());
+    w_.wd.push_back(take());
+  }
+  w_.final_norm = take();
+  w_.lm_head = take();
+
+  // ---- rope tables (double math, rounded once; same formula as the oracle)
+  const int cap = static_cast<int>(round_up(cfg_.max_ctx + cfg_.max_x + 2, VC_QGROUP));
+  {
+    const int half = d / 2;
+    std::vector<float> c(static_cast<size_t>(cap) * half), s(c.size());
+    for (int pos = 0; pos < cap; ++pos)
+      for (int i = 0; i < half; ++i) {
+        const double inv = std::pow(static_cast<double>(m.rope_theta), -2.0 * i / d);
+        const double a = static_cast<double>(pos) * inv;
+        c[static_cast<size_t>(pos) * half + i] = static_cast<float>(std::cos(a));
+        s[static_cast<size_t>(pos) * half + i] = static_cast<float>(std::sin(a));
+      }
+    rope_cos_ = dmalloc<float>(c.size());
+    rope_sin_ = dmalloc<float>(s.size());
+    VC_CK(cudaMemcpy(rope_cos_, c.data(), c.size() * 4, cudaMemcpyHostToDevice));
+    VC_CK(cudaMemcpy(rope_sin_, s.data(), s.size() * 4, cudaMemcpyHostToDevice));
+  }
+  // ---- KV tiers ------------------------------------------------------------
+  const size_t slices = static_cast<size_t>(cfg_.max_slots) * L * m.n_kv;
+  const size_t slice_elems = static_cast<size_t>(cap) * d;
+  if (cfg_.full_tier == 0) {
+    full_.cap = cap;
+    full_.k = dmalloc<uint16_t>(slices * slice_elems);
+    full_.v = dmalloc<uint16_t>(slices * slice_elems);
+  } else {
+    full_.cap = cap;  // geometry of the host pool
+    const size_t bytes = slices * slice_elems * 2;
+    VC_CK(cudaHostAlloc(reinterpret_cast<void**>(&host_k_), bytes, cudaHostAllocDefault));
+    VC_CK(cudaHostAlloc(reinterpret_cast<void**>(&host_v_), bytes, cudaHostAllocDefault));
+    const size_t st_slices = static_cast<size_t>(cfg_.n_stage) * L * m.n_kv;
+    stage_.cap = cap;
+    stage_.k = dmalloc<uint16_t>(st_slices * slice_elems);
+    stage_.v = dmalloc<uint16_t>(st_slices * slice_elems);
+  }
+  tail_cap_ = static_cast<int>(round_up(VC_QGROUP + cfg_.max_x + 2, 8));
+  if (cfg_.quant_bits > 0) {
+    const int capq = cfg_.max_ctx / VC_QGROUP * VC_QGROUP;
+    quant_.cap = capq;
+    quant_.tail_cap = tail_cap_;
+    const size_t words = static_cast<size_t>(capq) * d * cfg_.quant_bits / 32;
+    quant_.kc = dmalloc<uint32_t>(slices * words);
+    quant_.vc = dmalloc<uint32_t>(slices * words);
+    quant_.ksz = dmalloc<uint32_t>(slices * (capq / VC_QGROUP) * d);
+    quant_.vsz = dmalloc<uint32_t>(slices * capq);
+    quant_.ktail = dmalloc<uint16_t>(slices * tail_cap_ * d);
+    quant_.vtail = dmalloc<uint16_t>(slices * tail_cap_ * d);
+    max_chunks_q_ = (capq / VC_QGROUP + VC_DRAFT_CG - 1) / VC_DRAFT_CG;
+  }
+  max_chunks_d_ = (cap + VC_DENSE_CHUNK - 1) / VC_DENSE_CHUNK;
+  // ---- activations ---------------------------------------------------------
+  Mmax_ = cfg_.max_slots + cfg_.max_verify * (cfg_.max_x + 1);
+  if (Mmax_ < 8) Mmax_ = 8;
+  x_ = dmalloc<float>(static_cast<size_t>(Mmax_) * H);
+  xn_ = dmalloc<uint16_t>(static_cast<size_t>(Mmax_) * (H > F ? H : F));
+  qkv_ = dmalloc<uint16_t>(static_cast<size_t>(Mmax_) * qkv_n);
+  attn_ = dmalloc<uint16_t>(static_cast<size_t>(Mmax_) * m.n_q * d);
+  act_ = dmalloc<uint16_t>(static_cast<size_t>(Mmax_) * F);
+  splits_qkv_ = gemm_splits(qkv_n, H);
+  splits_o_ = gemm_splits(H, m.n_q * d);
+  splits_gu_ = gemm_splits(2 * F, H);
+  splits_d_ = gemm_splits(H, F);
+  splits_lm_ = gemm_splits(V, H);
+  size_t wsf = 0;
+  auto need = [&](int s, int n) { wsf = std::max(wsf, static_cast<size_t>(s) * n); };
+  need(splits_qkv_, qkv_n);
+  need(splits_o_, H);
+  need(splits_gu_, 2 * F);
+  need(splits_d_, H);
+  need(splits_lm_, V);
+  ws_floats_ = wsf * Mmax_;
+  ws_ = dmalloc<float>(ws_floats_);
+  logits_ = dmalloc<float>(static_cast<size_t>(Mmax_) * V);
+  tok_in_ = dmalloc<int32_t>(Mmax_);
+  tok_out_ = dmalloc<int32_t>(Mmax_);
+  const size_t prow_draft = static_cast<size_t>(cfg_.max_slots) * (max_chunks_q_ + 1);
+  const size_t prow_dense = static_cast<size_t>(Mmax_) * max_chunks_d_;
+  const size_t prow = (prow_draft + prow_dense) * m.n_q;
+  part_.o = dmalloc<float>(prow * d);
+  part_.ml = dmalloc<float>(prow * 2);
+  rows_dev_ = dmalloc<RowDest>(Mmax_);
+  const int n_seq_max = 2 * cfg_.max_slots + cfg_.max_verify + 1;
+  seqs_dev_ = dmalloc<AttnSeq>(n_seq_max);
+  jobs_dev_ = dmalloc<QuantJob>(static_cast<size_t>(L) * m.n_kv);
+  desc_bytes_ = Mmax_ * sizeof(int32_t) + Mmax_ * sizeof(RowDest) + n_seq_max * sizeof(AttnSeq) +
+                static_cast<size_t>(L) * m.n_kv * sizeof(QuantJob);
+  VC_CK(cudaHostAlloc(&h_desc_, desc_bytes_, cudaHostAllocDefault));
+  VC_CK(cudaHostAlloc(reinterpret_cast<void**>(&h_out_), Mmax_ * sizeof(int32_t), cudaHostAllocDefault));
+}
+
+// ---------------------------------------------------------------- weights
+void Engine::init_weights_random(uint64_t seed, float stddev) {
+  const auto& m = cfg_.model;
+  const int L = m.layers, H = m.hidden, F = m.ffn, V = m.vocab, d = m.d;
+  const int qkv_n = (m.n_q + 2 * m.n_kv) * d;
+  const float k = static_cast<float>(stddev / (65536.0 * std::sqrt(1.0 / 3.0)));
+  uint64_t off = 0;
+  auto fill = [&](uint16_t* p, size_t n) {
+    VC_LAUNCH(fill_normal_bf16(p, n, seed, off, k, st_));
+    off += n;
+  };
+  const uint16_t one = 0x3f80;
+  fill(w_.embed, static_cast<size_t>(V) * H);
+  for (int l = 0; l < L; ++l) {
+    VC_LAUNCH(fill_const_bf16(w_.attn_norm[l], H, one, st_));
+    fill(w_.wqkv[l], static_cast<size_t>(qkv_n) * H);
+    fill(w_.wo[l], static_cast<size_t>(H) * m.n_q * d);
+    VC_LAUNCH(fill_const_bf16(w_.mlp_norm[l], H, one, st_));
+    fill(w_.wgu[l], static_cast<size_t>(2) * F * H);
+    fill(w_.wd[l], static_cast<size_t>(H) * F);
+  }
+  VC_LAUNCH(fill_const_bf16(w_.final_norm, H, one, st_));
+  fill(w_.lm_head, static_cast<size_t>(V) * H);
+  VC_CK(cudaStreamSynchronize(st_));
+}
+
+void Engine::load_weights(const uint16_t* embed, const uint16_t* const* attn_norm,
+                          const uint16_t* const* wqkv, const uint16_t* const* wo,
+                          const uint16_t* const* mlp_norm, const uint16_t* const* wgate,
+                          const uint16_t* const* wup, const uint16_t* const* wdown,
+                          const uint16_t* final_norm, const uint16_t* lm_head) {
+  const auto& m = cfg_.model;
+  const int L = m.layers, H = m.hidden, F = m.ffn, V = m.vocab, d = m.d;
+  const int qkv_n = (m.n_q + 2 * m.n_kv) * d;
+  auto up = [&](uint16_t* dst, const uint16_t* src, size_t n) {
+    VC_CK(cudaMemcpy(dst, src, n * 2, cudaMemcpyHostToDevice));
+  };
+  up(w_.embed, embed, static_cast<size_t>(V) * H);
+  std::vector<uint16_t> gu(static_cast<size_t>(2) * F * H);
+  for (int l = 0; l < L; ++l) {
+    up(w_.attn_norm[l], attn_norm[l], H);
+    up(w_.wqkv[l], wqkv[l], static_cast<size_t>(qkv_n) * H);
+    up(w_.wo[l], wo[l], static_cast<size_t>(H) * m.n_q * d);
+    up(w_.mlp_norm[l], mlp_norm[l], H);
+    // interleave gate/up rows: row 2j = gate_j, row 2j+1 = up_j
+    for (int j = 0; j < F; ++j) {
+      std::memcpy(&gu[static_cast<size_t>(2 * j) * H], wgate[l] + static_cast<size_t>(j) * H, H * 2);
+      std::memcpy(&gu[static_cast<size_t>(2 * j + 1) * H], wup[l] + static_cast<size_t>(j) * H, H * 2);
+    }
+    up(w_.wgu[l], gu.data(), gu.size());
+    up(w_.wd[l], wdown[l], static_cast<size_t>(H) * F);
+  }
+  up(w_.final_norm, final_norm, H);
+  up(w_.lm_head, lm_head, static_cast<size_t>(V) * H);
+}
+
+// --------------------------------------------------------------- requests
+void Engine::add_request_synthetic(int slot, int n_ctx, int32_t pending, uint64_t seed,
+                                   int outlier_channels, float outlier_scale) {
+  if (slot < 0 || slot >= cfg_.max_slots) throw ContractViolation("slot out of range");
+  if (n_ctx < 0 || n_ctx + cfg_.max_x + 2 > full_.cap) throw ContractViolation("context exceeds capacity");
+  const auto& m = cfg_.model;
+  const int n_slices = m.layers * m.n_kv;
+  const float k_norm = static_cast<float>(1.0 / (65536.0 * std::sqrt(1.0 / 3.0)));
+  const float k_out = static_cast<float>(outlier_scale / (65536.0 * std::sqrt(1.0 / 3.0)));
+  const int period = outlier_channels > 0 ? m.d / outlier_channels : 0;
+  // tier 1 synthesises into staging slot 0, then D2H into the host pool
+  KvPool dst = cfg_.full_tier == 0 ? full_ : stage_;
+  const int dslot = cfg_.full_tier == 0 ? slot : 0;
+  const size_t slice_elems = static_cast<size_t>(full_.cap) * m.d;
+  uint16_t* kb = dst.k + static_cast<size_t>(dslot) * n_slices * slice_elems;
+  uint16_t* vb = dst.v + static_cast<size_t>(dslot) * n_slices * slice_elems;
+  if (n_ctx > 0) {
+    const size_t total = static_cast<size_t>(n_ctx) * m.d * n_slices;
+    int grid = static_cast<int>(std::min<size_t>((total + 255) / 256, 148 * 32));
+    synth_kv_kernel<<<grid, 256, 0, st_>>>(kb, vb, full_.cap, n_ctx, m.d, n_slices, seed, k_norm,
+                                           k_out, period);
+    VC_CK(cudaGetLastError());
+    ++launches_;
+  }
+  SeqState& s = seqs_[slot];
+  s = SeqState{};
+  s.live = true;
+  s.committed = n_ctx;
+  s.pending = pending;
+  if (cfg_.full_tier == 1 && n_ctx > 0) {
+    const size_t pitch = static_cast<size_t>(full_.cap) * m.d * 2;
+    const size_t width = static_cast<size_t>(n_ctx) * m.d * 2;
+    uint16_t* hk = host_k_ + static_cast<size_t>(slot) * n_slices * slice_elems;
+    uint16_t* hv = host_v_ + static_cast<size_t>(slot) * n_slices * slice_elems;
+    VC_CK(cudaMemcpy2DAsync(hk, pitch, kb, pitch, width, n_slices, cudaMemcpyDeviceToHost, st_));
+    VC_CK(cudaMemcpy2DAsync(hv, pitch, vb, pitch, width, n_slices, cudaMemcpyDeviceToHost, st_));
+  }
+  VC_CK(cudaStreamSynchronize(st_));
+}
+
+void Engine::add_request_kv(int slot, int n_ctx, int32_t pending, const uint16_t* k, const uint16_t* v) {
+  if (slot < 0 || slot >= cfg_.max_slots) throw ContractViolation("slot out of range");
+  if (n_ctx + cfg_.max_x + 2 > full_.cap) throw ContractViolation("context exceeds capacity");
+  const auto& m = cfg_.model;
+  const int n_slices = m.layers * m.n_kv;
+  const size_t slice_elems = static_cast<size_t>(full_.cap) * m.d;
+  const size_t pitch = slice_elems * 2, spitch = static_cast<size_t>(n_ctx) * m.d * 2;
+  if (n_ctx > 0) {
+    if (cfg_.full_tier == 0) {
+      uint16_t* kb = full_.k + static_cast<size_t>(slot) * n_slices * slice_elems;
+      uint16_t* vb = full_.v + static_cast<size_t>(slot) * n_slices * slice_elems;
+      VC_CK(cudaMemcpy2DAsync(kb, pitch, k, spitch, spitch, n_slices, cudaMemcpyHostToDevice, st_));
+      VC_CK(cudaMemcpy2DAsync(vb, pitch, v, spitch, spitch, n_slices, cudaMemcpyHostToDevice, st_));
+    } else {
+      uint16_t* hk = host_k_ + static_cast<size_t>(slot) * n_slices * slice_elems;
+      uint16_t* hv = host_v_ + static_cast<size_t>(slot) * n_slices * slice_elems;
+      for (int i = 0; i < n_slices; ++i) {
+        std::memcpy(hk + i * slice_elems, k + static_cast<size_t>(i) * n_ctx * m.d, spitch);
+        std::memcpy(hv + i * slice_elems, v + static_cast<size_t>(i) * n_ctx * m.d, spitch);
+      }
+    }
+  }
+  SeqState& s = seqs_[slot];
+  s = SeqState{};
+  s.live = true;
+  s.committed = n_ctx;
+  s.pending = pending;
+  VC_CK(cudaStreamSynchronize(st_));
+}
+
+void Engine::add_request_prefill(int slot, const int32_t* prompt, int n) {
+  if (n < 1) throw ContractViolation("prefill: empty prompt");
+  if (cfg_.full_tier != 0) throw ContractViolation("prefill requires the HBM full tier");
+  SeqState& s = seqs_[slot];
+  s = SeqState{};
+  s.live = true;
+  s.committed = 0;
+  s.pending = prompt[0];
+  // feed the prompt through verify-shaped steps of at most max_x+1 rows
+  int pos = 0;
+  std::vector<int32_t> out;
+  while (pos < n - 1) {
+    const int len = std::min(n - 1 - pos, cfg_.max_x + 1);
+    StepItem it;
+    it.slot = slot;
+    it.mode = RowMode::Verify;
+    it.tokens.assign(prompt + pos, prompt + pos + len);
+    run_step({it}, out);
+    s.committed += len;
+    pos += len;
+  }
+  s.pending = prompt[n - 1];
+}
+
+void Engine::release(int slot) { seqs_.at(slot) = SeqState{}; }
+
+void Engine::quantise_groups(int slot, int g0, int ng, const KvPool& src, int src_slot) {
+  if (ng <= 0) return;
+  const auto& m = cfg_.model;
+  const int n_slices = m.layers * m.n_kv;
+  QuantJob* jobs = reinterpret_cast<QuantJob*>(static_cast<uint8_t*>(h_desc_) + desc_bytes_ -
+                                               static_cast<size_t>(n_slices) * sizeof(QuantJob));
+  const size_t words = static_cast<size_t>(quant_.cap) * m.d * cfg_.quant_bits / 32;
+  for (int i = 0; i < n_slices; ++i) {
+    const size_t ss = static_cast<size_t>(src_slot) * n_slices + i;
+    const size_t ds = static_cast<size_t>(slot) * n_slices + i;
+    QuantJob j;
+    j.k = src.k + ss * static_cast<size_t>(src.cap) * m.d;
+    j.v = src.v + ss * static_cast<size_t>(src.cap) * m.d;
+    j.kc = quant_.kc + ds * words;
+    j.vc = quant_.vc + ds * words;
+    j.ksz = quant_.ksz + ds * (quant_.cap / VC_QGROUP) * m.d;
+    j.vsz = quant_.vsz + ds * static_cast<size_t>(quant_.cap);
+    j.g0 = g0;
+    j.ng = ng;
+    jobs[i] = j;
+  }
+  VC_CK(cudaMemcpyAsync(jobs_dev_, jobs, n_slices * sizeof(QuantJob), cudaMemcpyHostToDevice, st_));
+  VC_LAUNCH(quant_kivi(jobs_dev_, n_slices, ng, m.d, cfg_.quant_bits, st_));
+  // the pinned job table is reused by the next call: wait for the copy
+  VC_CK(cudaStreamSynchronize(st_));
+}
+
+void Engine::compress(int slot) {
+  if (cfg_.quant_bits == 0) throw ContractViolation("compress: compressed tier disabled");
+  SeqState& s = seqs_.at(slot);
+  const auto& m = cfg_.model;
+  KvPool src = full_;
+  int src_slot = slot;
+  if (cfg_.full_tier == 1) {
+    // stream the prefix through staging slot 0
+    uint64_t id = swap_begin(slot, 0);
+    swap_wait(id);
+    src = stage_;
+    src_slot = 0;
+  }
+  const int ng = std::min(s.committed / VC_QGROUP, quant_.cap / VC_QGROUP);
+  quantise_groups(slot, 0, ng, src, src_slot);
+  s.n_groups = ng;
+  s.tail_committed = s.committed - ng * VC_QGROUP;
+  if (s.tail_committed > tail_cap_ - cfg_.max_x - 1) throw ContractViolation("tail overflow");
+  VC_LAUNCH(tail_refill(src, src_slot, ng * VC_QGROUP, s.tail_committed, quant_, slot, m.layers,
+                        m.n_kv, m.d, st_));
+  s.draft_len = 0;
+  s.drafted.clear();
+  VC_CK(cudaStreamSynchronize(st_));
+}
+
+size_t Engine::compressed_bytes(int slot) const {
+  const SeqState& s = seqs_.at(slot);
+  const auto& m = cfg_.model;
+  const size_t per_group = static_cast<size_t>(VC_QGROUP) * m.d * cfg_.quant_bits / 8 * 2  // K+V codes
+                           + static_cast<size_t>(m.d) * 4 + VC_QGROUP * 4;                  // scales
+  return per_group * s.n_groups * m.layers * m.n_kv;
+}
+
+// ------------------------------------------------------------------ steps
+void Engine::enqueue_forward(int M, int n_draft, int n_dense1, int n_densev, int max_rows_v,
+                             bool /*want_logits*/) {
+  const auto& m = cfg_.model;
+  const int L = m.layers, H = m.hidden, F = m.ffn, V = m.vocab, d = m.d;
+  const int qkv_n = (m.n_q + 2 * m.n_kv) * d;
+  AttnShape as;
+  as.layers = L;
+  as.n_kv = m.n_kv;
+  as.n_rep = m.n_q / m.n_kv;
+  as.d = d;
+  as.q_stride = qkv_n;
+  as.out_stride = m.n_q * d;
+  as.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(d)));
+  const KvPool dense_v_pool = cfg_.full_tier == 0 ? full_ : stage_;
+  VC_LAUNCH(embed_norm(tok_in_, M, w_.embed, H, w_.attn_norm[0], m.eps, x_, xn_, st_));
+  for (int l = 0; l < L; ++l) {
+    VC_LAUNCH(gemm_partial(xn_, M, H, w_.wqkv[l], qkv_n, splits_qkv_, ws_, st_));
+    VC_LAUNCH(qkv_epilogue(ws_, splits_qkv_, M, m.n_q, m.n_kv, d, rows_dev_, rope_cos_, rope_sin_, qkv_, st_));
+    VC_LAUNCH(kv_store(qkv_, M, m.n_q, m.n_kv, d, l, L, rows_dev_, full_, stage_, quant_, st_));
+    if (n_draft > 0) {
+      VC_LAUNCH(draft_attention_quant(as, quant_, l, qkv_, seqs_dev_, n_draft, max_chunks_q_,
+                                      cfg_.quant_bits, part_, st_));
+      VC_LAUNCH(attention_combine(as, seqs_dev_, n_draft, max_chunks_q_, 1, 0, part_, attn_, st_));
+    }
+    if (n_dense1 > 0) {
+      VC_LAUNCH(dense_attention(as, full_, l, qkv_, seqs_dev_ + n_draft, n_dense1, max_chunks_d_, 1, part_, st_));
+      VC_LAUNCH(attention_combine(as, seqs_dev_ + n_draft, n_dense1, max_chunks_d_, 1, 1, part_, attn_, st_));
+    }
+    if (n_densev > 0) {
+      const AttnSeq* sv = seqs_dev_ + n_draft + n_dense1;
+      VC_LAUNCH(dense_attention(as, dense_v_pool, l, qkv_, sv, n_densev, max_chunks_d_, max_rows_v, part_, st_));
+      VC_LAUNCH(attention_combine(as, sv, n_densev, max_chunks_d_, max_rows_v, 1, part_, attn_, st_));
+    }
+    VC_LAUNCH(gemm_partial(attn_, M, m.n_q * d, w_.wo[l], H, splits_o_, ws_, st_));
+    VC_LAUNCH(residual_norm(ws_, splits_o_, M, H, x_, w_.mlp_norm[l], m.eps, xn_, st_));
+    VC_LAUNCH(gemm_partial(xn_, M, H, w_.wgu[l], 2 * F, splits_gu_, ws_, st_));
+    VC_LAUNCH(silu_epilogue(ws_, splits_gu_, M, F, act_, st_));
+    VC_LAUNCH(gemm_partial(act_, M, F, w_.wd[l], H, splits_d_, ws_, st_));
+    VC_LAUNCH(residual_norm(ws_, splits_d_, M, H, x_, l + 1 < L ? w_.attn_norm[l + 1] : w_.final_norm,
+                            m.eps, xn_, st_));
+  }
+  VC_LAUNCH(gemm_partial(xn_, M, H, w_.lm_head, V, splits_lm_, ws_, st_));
+  VC_LAUNCH(sum_epilogue(ws_, splits_lm_, M, V, logits_, st_));
+  VC_LAUNCH(argmax_rows(logits_, M, V, tok_out_, st_));
+}
+
+void Engine::run_step(const std::vector<StepItem>& items, std::vector<int32_t>& out,
+                      float* logits_host) {
+  const auto& m = cfg_.model;
+  const int n_seq_max = 2 * cfg_.max_slots + cfg_.max_verify + 1;
+  int32_t* h_tok = static_cast<int32_t*>(h_desc_);
+  RowDest* h_rows = reinterpret_cast<RowDest*>(h_tok + Mmax_);
+  AttnSeq* h_seqs = reinterpret_cast<AttnSeq*>(h_rows + Mmax_);
+  std::vector<AttnSeq> drafts, dense1, densev;
+  int M = 0, max_rows_v = 1;
+  for (const StepItem& it : items) {
+    const SeqState& s = seqs_.at(it.slot);
+    if (!s.live) throw ContractViolation("run_step: slot not live");
+    const int n = static_cast<int>(it.tokens.size());
+    if (n < 1 || M + n > Mmax_) throw ContractViolation("run_step: too many rows");
+    AttnSeq a{};
+    a.row0 = M;
+    a.n_rows = n;
+    if (it.mode == RowMode::Draft) {
+      if (cfg_.quant_bits == 0 || n != 1) throw ContractViolation("draft rows need the compressed tier");
+      if (s.tail_committed + s.draft_len + 1 > tail_cap_) throw ContractViolation("draft window overflow");
+      h_tok[M] = it.tokens[0];
+      h_rows[M] = RowDest{1, it.slot, s.tail_committed + s.draft_len, s.committed + s.draft_len};
+      a.slot = it.slot;
+      a.n_groups = s.n_groups;
+      a.tail_len = s.tail_committed + s.draft_len + 1;
+      drafts.push_back(a);
+    } else {
+      const bool staged = cfg_.full_tier == 1;
+      if (staged && it.mode == RowMode::Decode) throw ContractViolation("decode rows need the HBM full tier");
+      if (staged && (it.stage < 0 || it.stage >= cfg_.n_stage)) throw ContractViolation("verify needs a staging slot");
+      const int pslot = staged ? it.stage : it.slot;
+      if (s.committed + n > full_.cap) throw ContractViolation("context exceeds capacity");
+      for (int i = 0; i < n; ++i) {
+        h_tok[M + i] = it.tokens[i];
+        h_rows[M + i] = RowDest{staged ? 2 : 0, pslot, s.committed + i, s.committed + i};
+      }
+      a.slot = pslot;
+      a.kv_len = s.committed + n;
+      if (n == 1 && !staged) {
+        dense1.push_back(a);
+      } else {
+        densev.push_back(a);
+        max_rows_v = std::max(max_rows_v, n);
+      }
+    }
+    M += n;
+  }
+  if (static_cast<int>(drafts.size() + dense1.size() + densev.size()) > n_seq_max)
+    throw ContractViolation("run_step: too many sequences");
+  // partial-row offsets (units of Hq partial rows)
+  int off = 0;
+  for (auto& a : drafts) { a.part0 = off; off += max_chunks_q_ + 1; }
+  for (auto& a : dense1) { a.part0 = off; off += max_chunks_d_ * a.n_rows; }
+  for (auto& a : densev) { a.part0 = off; off += max_chunks_d_ * a.n_rows; }
+  int k = 0;
+  for (auto& a : drafts) h_seqs[k++] = a;
+  for (auto& a : dense1) h_seqs[k++] = a;
+  for (auto& a : densev) h_seqs[k++] = a;
+  VC_CK(cudaMemcpyAsync(tok_in_, h_tok, M * sizeof(int32_t), cudaMemcpyHostToDevice, st_));
+  VC_CK(cudaMemcpyAsync(rows_dev_, h_rows, M * sizeof(RowDest), cudaMemcpyHostToDevice, st_));
+  VC_CK(cudaMemcpyAsync(seqs_dev_, h_seqs, k * sizeof(AttnSeq), cudaMemcpyHostToDevice, st_));
+
+  const int nd = static_cast<int>(drafts.size()), n1 = static_cast<int>(dense1.size()),
+            nv = static_cast<int>(densev.size());
+  if (cfg_.use_graphs) {
+    std::ostringstream key;
+    key << M << ':' << nd << ':' << n1 << ':' << nv << ':' << max_rows_v;
+    auto itg = graphs_.find(key.str());
+    if (itg == graphs_.end()) {
+      cudaGraph_t g;
+      const uint64_t before = launches_;
+      VC_CK(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal));
+      enqueue_forward(M, nd, n1, nv, max_rows_v, logits_host != nullptr);
+      VC_CK(cudaStreamEndCapture(st_, &g));
+      cudaGraphExec_t ge;
+      VC_CK(cudaGraphInstantiate(&ge, g, 0));
+      cudaGraphDestroy(g);
+      launches_per_graph_[key.str()] = launches_ - before;
+      itg = graphs_.emplace(key.str(), ge).first;
+      launches_ = before;
+    }
+    VC_CK(cudaGraphLaunch(itg->second, st_));
+    launches_ += launches_per_graph_[key.str()];
+  } else {
+    enqueue_forward(M, nd, n1, nv, max_rows_v, logits_host != nullptr);
+  }
+  VC_CK(cudaMemcpyAsync(h_out_, tok_out_, M * sizeof(int32_t), cudaMemcpyDeviceToHost, st_));
+  if (logits_host)
+    VC_CK(cudaMemcpyAsync(logits_host, logits_, static_cast<size_t>(M) * m.vocab * 4,
+                          cudaMemcpyDeviceToHost, st_));
+  VC_CK(cudaStreamSynchronize(st_));
+  out.assign(h_out_, h_out_ + M);
+  last_M_ = M;
+}
+
+void Engine::commit_decode(int slot, int32_t next) {
+  SeqState& s = seqs_.at(slot);
+  s.committed += 1;
+  s.pending = next;
+  s.history.push_back(next);
+}
+
+void Engine::push_draft(int slot, int32_t tok) {
+  SeqState& s = seqs_.at(slot);
+  s.drafted.push_back(tok);
+  s.draft_len += 1;
+}
+
+std::vector<int32_t> Engine::accept_commit(int slot, const std::vector<int32_t>& preds, int stage) {
+  SeqState& s = seqs_.at(slot);
+  const int x = static_cast<int>(s.drafted.size());
+  if (static_cast<int>(preds.size()) != x + 1) throw ContractViolation("accept: |preds| must be |drafted|+1");
+  // accept rule (/root/reference/proj/src/specloop.cpp:37-56)
+  int mcount = x;
+  for (int k = 0; k < x; ++k)
+    if (s.drafted[k] != preds[k]) { mcount = k; break; }
+  std::vector<int32_t> emitted(s.drafted.begin(), s.drafted.begin() + mcount);
+  emitted.push_back(preds[mcount]);
+  const auto& m = cfg_.model;
+  const int old = s.committed;
+  const int now = old + 1 + mcount;
+  const bool staged = cfg_.full_tier == 1;
+  KvPool src = staged ? stage_ : full_;
+  const int src_slot = staged ? stage : slot;
+  if (staged) {
+    if (stage < 0) throw ContractViolation("accept: staged verify needs its stage");
+    // exact KV of the committed rows back to the host pool
+    const int n_slices = m.layers * m.n_kv;
+    const size_t pitch = static_cast<size_t>(full_.cap) * m.d * 2;
+    const size_t off = static_cast<size_t>(old) * m.d;
+    const size_t width = static_cast<size_t>(now - old) * m.d * 2;
+    const size_t slice_elems = static_cast<size_t>(full_.cap) * m.d;
+    uint16_t* hk = host_k_ + static_cast<size_t>(slot) * n_slices * slice_elems + off;
+    uint16_t* hv = host_v_ + static_cast<size_t>(slot) * n_slices * slice_elems + off;
+    const uint16_t* sk = stage_.k + static_cast<size_t>(stage) * n_slices * slice_elems + off;
+    const uint16_t* sv = stage_.v + static_cast<size_t>(stage) * n_slices * slice_elems + off;
+    VC_CK(cudaMemcpy2DAsync(hk, pitch, sk, pitch, width, n_slices, cudaMemcpyDeviceToHost, st_));
+    VC_CK(cudaMemcpy2DAsync(hv, pitch, sv, pitch, width, n_slices, cudaMemcpyDeviceToHost, st_));
+  }
+  if (cfg_.quant_bits > 0 && (s.n_groups > 0 || s.tail_committed > 0 || x > 0)) {
+    const int ng_now = std::min(now / VC_QGROUP, quant_.cap / VC_QGROUP);
+    quantise_groups(slot, s.n_groups, ng_now - s.n_groups, src, src_slot);
+    s.n_groups = ng_now;
+    s.tail_committed = now - ng_now * VC_QGROUP;
+    VC_LAUNCH(tail_refill(src, src_slot, ng_now * VC_QGROUP, s.tail_committed, quant_, slot,
+                          m.layers, m.n_kv, m.d, st_));
+  }
+  s.committed = now;
+  s.pending = preds[mcount];
+  s.drafted.clear();
+  s.draft_len = 0;
+  s.history.insert(s.history.end(), emitted.begin(), emitted.end());
+  return emitted;
+}
+
+// ------------------------------------------------------------- host tier
+uint64_t Engine::swap_begin(int slot, int stage) {
+  if (cfg_.full_tier != 1) throw ContractViolation("swap: host tier disabled");
+  if (stage < 0 || stage >= cfg_.n_stage) throw ContractViolation("swap: bad staging slot");
+  const SeqState& s = seqs_.at(slot);
+  const auto& m = cfg_.model;
+  const int n_slices = m.layers * m.n_kv;
+  const size_t slice_elems = static_cast<size_t>(full_.cap) * m.d;
+  const size_t pitch = slice_elems * 2;
+  const size_t width = static_cast<size_t>(s.committed) * m.d * 2;
+  uint16_t* dk = stage_.k + static_cast<size_t>(stage) * n_slices * slice_elems;
+  uint16_t* dv = stage_.v + static_cast<size_t>(stage) * n_slices * slice_elems;
+  const uint16_t* hk = host_k_ + static_cast<size_t>(slot) * n_slices * slice_elems;
+  const uint16_t* hv = host_v_ + static_cast<size_t>(slot) * n_slices * slice_elems;
+  // the stage may still be read by an in-flight step on the compute stream
+  cudaEvent_t ready;
+  VC_CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+  VC_CK(cudaEventRecord(ready, st_));
+  VC_CK(cudaStreamWaitEvent(copy_st_, ready, 0));
+  cudaEventDestroy(ready);
+  if (width > 0) {
+    VC_CK(cudaMemcpy2DAsync(dk, pitch, hk, pitch, width, n_slices, cudaMemcpyHostToDevice, copy_st_));
+    VC_CK(cudaMemcpy2DAsync(dv, pitch, hv, pitch, width, n_slices, cudaMemcpyHostToDevice, copy_st_));
+  }
+  cudaEvent_t done;
+  VC_CK(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
+  VC_CK(cudaEventRecord(done, copy_st_));
+  const uint64_t id = next_xfer_++;
+  xfers_[id] = done;
+  return id;
+}
+
+bool Engine::swap_done(uint64_t id) {
+  auto it = xfers_.find(id);
+  if (it == xfers_.end()) return true;
+  cudaError_t e = cudaEventQuery(it->second);
+  if (e == cudaErrorNotReady) return false;
+  check_cuda(e, "swap_done");
+  // order later compute after the copy
+  VC_CK(cudaStreamWaitEvent(st_, it->second, 0));
+  cudaEventDestroy(it->second);
+  xfers_.erase(it);
+  return true;
+}
+
+void Engine::swap_wait(uint64_t id) {
+  auto it = xfers_.find(id);
+  if (it == xfers_.end()) return;
+  VC_CK(cudaEventSynchronize(it->second));
+  swap_done(id);
+}
+
+}  // namespace vc

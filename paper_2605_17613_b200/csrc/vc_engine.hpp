@@ -1,0 +1,210 @@
+// vc_engine.hpp -- the B200 decode-loop engine behind include/vc_api.h.
+//
+// Owns the model weights, the three KV tiers and the step executor:
+//   * full KV:        bf16 [slot][layer][kv-head][cap][d], resident in HBM
+//                     (tier 0) or in a pinned host pool streamed into HBM
+//                     staging slots before each verify (tier 1);
+//   * compressed KV:  KIVI int4/int2 codes + fp16 scale/zero in mma fragment
+//                     order, plus a bf16 tail (residual group + draft window);
+//   * activations and split-K workspaces sized for the largest step.
+// A step is one forward pass over a heterogeneous batch: drafting rows
+// (compressed KV), verify rows (x+1 per request, full KV) and plain decode
+// rows (full KV) share every weight read.  Kernels are launched on the
+// compute stream and captured into CUDA graphs keyed by the step shape.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "vc_gemm.h"
+#include "vc_kernels.h"
+
+namespace vc {
+
+struct ModelDesc {
+  int vocab = 0, hidden = 0, layers = 0, n_q = 0, n_kv = 0, d = 0, ffn = 0;
+  float rope_theta = 500000.f, eps = 1e-5f;
+};
+
+struct EngineConfig {
+  ModelDesc model;
+  int max_slots = 1;    // concurrently resident requests
+  int max_ctx = 4096;   // token capacity per request (prefix + generated)
+  int max_x = 16;       // largest draft horizon
+  int quant_bits = 4;   // 4 or 2; 0 disables the compressed tier
+  int full_tier = 0;    // 0: full KV in HBM; 1: pinned host pool + staging
+  int n_stage = 2;      // HBM staging slots (tier 1)
+  int max_verify = 2;   // verify requests per step
+  int use_graphs = 1;
+};
+
+enum class RowMode : int { Decode = 0, Draft = 1, Verify = 2 };
+
+// One request's part of a step.
+struct StepItem {
+  int slot = 0;
+  RowMode mode = RowMode::Decode;
+  std::vector<int32_t> tokens;  // inputs: 1 (decode/draft) or x+1 (verify)
+  int stage = -1;               // staging slot holding this request's full KV (tier 1 verify)
+};
+
+struct SeqState {
+  bool live = false;
+  int committed = 0;      // positions with exact KV in the full tier
+  int32_t pending = 0;    // last emitted token (its KV is not computed yet)
+  int n_groups = 0;       // quantised groups in the compressed tier
+  int tail_committed = 0; // exact tokens in the draft tail (committed - n_groups*G)
+  int draft_len = 0;      // drafted tokens of the open round (their KV in the tail)
+  std::vector<int32_t> drafted;
+  std::vector<int32_t> history;  // every emitted token
+};
+
+struct StepTiming {
+  float ms = 0.f;
+};
+
+class Engine {
+ public:
+  explicit Engine(const EngineConfig& cfg, int device);
+  ~Engine();
+  Engine(const Engine&) = delete;
+  Engine& operator=(const Engine&) = delete;
+
+  const EngineConfig& config() const { return cfg_; }
+  const ModelDesc& model() const { return cfg_.model; }
+
+  // ---- weights -------------------------------------------------------
+  void init_weights_random(uint64_t seed, float stddev);
+  // Logical layouts (see oracle/vc_oracle.h); bf16 bits.
+  void load_weights(const uint16_t* embed, const uint16_t* const* attn_norm,
+                    const uint16_t* const* wqkv, const uint16_t* const* wo,
+                    const uint16_t* const* mlp_norm, const uint16_t* const* wgate,
+                    const uint16_t* const* wup, const uint16_t* const* wdown,
+                    const uint16_t* final_norm, const uint16_t* lm_head);
+
+  // ---- requests ------------------------------------------------------
+  // Synthetic prefix KV (K ~ N(0,1) with outlier channels x10, V ~ N(0,1))
+  // for positions [0, n_ctx); `pending` is the first input token.
+  void add_request_synthetic(int slot, int n_ctx, int32_t pending, uint64_t seed,
+                             int outlier_channels, float outlier_scale);
+  // Host-provided prefix KV: k/v bf16 [layer][kv-head][n_ctx][d].
+  void add_request_kv(int slot, int n_ctx, int32_t pending, const uint16_t* k, const uint16_t* v);
+  // Real prefill: forward the prompt (all but the last token become context).
+  void add_request_prefill(int slot, const int32_t* prompt, int n);
+  void release(int slot);
+  const SeqState& seq(int slot) const { return seqs_.at(slot); }
+
+  // Quantise the committed prefix into the compressed tier (offline compress).
+  void compress(int slot);
+
+  // ---- steps ---------------------------------------------------------
+  // Executes one forward over the items; writes argmax per input row into
+  // `out` (rows in item order) and optionally fp32 logits.
+  void run_step(const std::vector<StepItem>& items, std::vector<int32_t>& out,
+                float* logits_host = nullptr);
+  // Commit helpers (state only; kernels launched as needed).
+  void commit_decode(int slot, int32_t next);
+  void push_draft(int slot, int32_t tok);
+  // Accept rule over the open round given the verifier's x+1 predictions;
+  // commits exact KV, rolls back the draft window.  Returns emitted tokens.
+  std::vector<int32_t> accept_commit(int slot, const std::vector<int32_t>& preds, int stage = -1);
+
+  // ---- host tier -----------------------------------------------------
+  // Start the H2D reload of slot's committed full KV into staging slot
+  // `stage` on the copy stream; returns a transfer id.
+  uint64_t swap_begin(int slot, int stage);
+  bool swap_done(uint64_t id);
+  void swap_wait(uint64_t id);
+
+  // ---- raw access for tests ------------------------------------------
+  KvPool full_pool() const { return full_; }
+  KvPool stage_pool() const { return stage_; }
+  QuantPool quant_pool() const { return quant_; }
+  uint16_t* host_pool_k() const { return host_k_; }
+  uint16_t* host_pool_v() const { return host_v_; }
+  cudaStream_t stream() const { return st_; }
+  size_t weight_bytes() const { return weight_bytes_; }
+  size_t full_kv_bytes_per_token() const;
+  size_t compressed_bytes(int slot) const;
+  const float* last_logits_device() const { return logits_; }
+  int last_rows() const { return last_M_; }
+
+  // kernel launch counter (every kernel this engine enqueued)
+  uint64_t launches() const { return launches_; }
+
+  // Attention of caller-provided q (device, [n_rows][n_q][d]) for one
+  // request/layer: mode 1 draft over the compressed tier, else dense.
+  void attention_probe(int slot, int layer, int mode, const uint16_t* q_dev, int n_rows,
+                       int kv_len, uint16_t* out_host);
+  // Device-side greedy loop helpers (timing of the step executor).
+  cudaEvent_t ev_a() const { return ev_a_; }
+  cudaEvent_t ev_b() const { return ev_b_; }
+
+ private:
+  struct Weights {
+    uint16_t* embed = nullptr;
+    std::vector<uint16_t*> attn_norm, wqkv, wo, mlp_norm, wgu, wd;
+    uint16_t* final_norm = nullptr;
+    uint16_t* lm_head = nullptr;
+  };
+  void alloc_all();
+  void set_kv_rows(const std::vector<StepItem>& items, std::vector<RowDest>& rows) const;
+  void enqueue_forward(int M, int n_draft, int n_dense1, int n_densev, int max_rows_v,
+                       bool want_logits);
+  void quantise_groups(int slot, int g0, int ng, const KvPool& src, int src_slot);
+
+  EngineConfig cfg_;
+  int device_ = 0;
+  cudaStream_t st_ = nullptr, copy_st_ = nullptr;
+  Weights w_;
+  void* weight_blob_ = nullptr;
+  size_t weight_bytes_ = 0;
+  float *rope_cos_ = nullptr, *rope_sin_ = nullptr;
+  KvPool full_{}, stage_{};
+  QuantPool quant_{};
+  uint16_t *host_k_ = nullptr, *host_v_ = nullptr;
+  int max_chunks_q_ = 0, max_chunks_d_ = 0, tail_cap_ = 0, Mmax_ = 0;
+  // activations
+  float* x_ = nullptr;
+  uint16_t *xn_ = nullptr, *qkv_ = nullptr, *attn_ = nullptr, *act_ = nullptr;
+  float* ws_ = nullptr;
+  float* logits_ = nullptr;
+  int32_t *tok_in_ = nullptr, *tok_out_ = nullptr;
+  Partials part_{};
+  RowDest* rows_dev_ = nullptr;
+  AttnSeq* seqs_dev_ = nullptr;  // [draft | dense1 | densev]
+  QuantJob* jobs_dev_ = nullptr;
+  // pinned staging of per-step descriptors
+  void* h_desc_ = nullptr;
+  size_t desc_bytes_ = 0;
+  int32_t* h_out_ = nullptr;
+  std::vector<SeqState> seqs_;
+  int last_M_ = 0;
+  uint64_t launches_ = 0;
+  // graphs keyed by step shape
+  std::map<std::string, cudaGraphExec_t> graphs_;
+  std::map<std::string, uint64_t> launches_per_graph_;
+  // transfers
+  std::map<uint64_t, cudaEvent_t> xfers_;
+  uint64_t next_xfer_ = 1;
+  cudaEvent_t ev_a_ = nullptr, ev_b_ = nullptr;
+  int splits_qkv_ = 1, splits_o_ = 1, splits_gu_ = 1, splits_d_ = 1, splits_lm_ = 1;
+  size_t ws_floats_ = 0;
+};
+
+// Thrown on CUDA failures; vc_api maps it to VC_ERR_CUDA.
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct ContractViolation : std::logic_error {
+  using std::logic_error::logic_error;
+};
+
+void check_cuda(cudaError_t e, const char* what);
+
+}  // namespace vc

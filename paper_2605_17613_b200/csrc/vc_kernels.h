@@ -1,0 +1,93 @@
+// vc_kernels.h -- internal launch interface of the sm_100a kernels (host and
+// device visible; no torch types).  The public boundary is include/vc_api.h.
+#pragma once
+#include <cstddef>
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#define VC_QGROUP 128      // tokens per quantised K group (KIVI G)
+#define VC_DRAFT_CG 8      // quantised groups per draft-attention chunk (1024 tokens)
+#define VC_DENSE_CHUNK 256 // keys per dense-attention chunk (absolute positions)
+
+namespace vc {
+
+// ---------------------------------------------------------------- quantiser
+// One (layer, request, kv-head) slice: groups [g0, g0+ng) of the bf16 source
+// rows (token-major [T][d]) are quantised into the slice's code/scale arrays.
+struct QuantJob {
+  const uint16_t* k;  // bf16 source rows, token 0 of group 0
+  const uint16_t* v;
+  uint32_t* kc;   // K codes  (fragment order, u32 words), group 0
+  uint32_t* ksz;  // K (scale,zero) fp16 pairs [groups][d]
+  uint32_t* vc;   // V codes
+  uint32_t* vsz;  // V (scale,zero) fp16 pairs [tokens]
+  int g0, ng;
+};
+cudaError_t quant_kivi(const QuantJob* jobs_dev, int n_jobs, int max_groups, int d, int bits,
+                       cudaStream_t st);
+
+// u32 words of one quantised group (K or V): G*d*bits/32.
+inline constexpr size_t quant_group_words(int d, int bits) {
+  return static_cast<size_t>(VC_QGROUP) * d * bits / 32;
+}
+
+// ------------------------------------------------------------ attention I/O
+// Per-sequence descriptor shared by the attention kernels (device array).
+struct AttnSeq {
+  int slot;      // pool slot of the request
+  int row0;      // first activation row of this sequence in the step batch
+  int n_rows;    // query tokens (1 for draft/decode, x+1 for verify)
+  int kv_len;    // keys visible to the LAST query row (dense pools)
+  int n_groups;  // quantised groups (draft pool)
+  int tail_len;  // bf16 tail tokens (draft pool)
+  int part0;     // first partial-row index of this sequence (combine workspace)
+  int pad;
+};
+
+struct KvPool {        // bf16 [slot][layer][head][cap][d]
+  uint16_t* k;
+  uint16_t* v;
+  int cap;             // token capacity per slice
+};
+
+struct QuantPool {     // per slice: kc/vc words, ksz [groups][d], vsz [cap]
+  uint32_t* kc;
+  uint32_t* ksz;
+  uint32_t* vc;
+  uint32_t* vsz;
+  uint16_t* ktail;     // bf16 [slice][tail_cap][d]
+  uint16_t* vtail;
+  int cap;             // token capacity of the quantised region (multiple of G)
+  int tail_cap;
+};
+
+struct AttnShape {
+  int layers, n_kv, n_rep, d;
+  int q_stride;        // elements per activation row of the qkv buffer
+  int out_stride;      // elements per row of the attention output
+  float scale_log2;    // log2(e)/sqrt(d)
+};
+
+// Split-K partials: o [part_rows][d] fp32, ml [part_rows][2] (max in log2
+// domain, sum).  A partial row is (sequence part0 + chunk*rows + r).
+struct Partials {
+  float* o;
+  float* ml;
+};
+
+cudaError_t draft_attention_quant(const AttnShape& s, const QuantPool& pool, int layer,
+                                  const uint16_t* qkv, const AttnSeq* seqs, int n_seq,
+                                  int max_chunks, int bits, Partials part, cudaStream_t st);
+
+cudaError_t dense_attention(const AttnShape& s, const KvPool& pool, int layer, const uint16_t* qkv,
+                            const AttnSeq* seqs, int n_seq, int max_chunks, int max_rows,
+                            Partials part, cudaStream_t st);
+
+// Merge the chunk partials of every (sequence, query token, q head) in chunk
+// order into bf16 attention output rows.  mode 0 = draft layout (chunks of
+// the quantised pool + one tail partial), 1 = dense layout.
+cudaError_t attention_combine(const AttnShape& s, const AttnSeq* seqs, int n_seq, int max_chunks,
+                              int max_rows, int mode, Partials part, uint16_t* out,
+                              cudaStream_t st);
+
+}  // namespace vc

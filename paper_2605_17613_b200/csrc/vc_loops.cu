@@ -1,0 +1,235 @@
+// vc_loops.cu -- the swap-scheduled decode loop (vc_run_scheduled).
+//
+// simulate_staggered (/root/reference/proj/src/sim.cpp:182-307) with the
+// simulated link and HBM replaced by real copies and kernels:
+//   1. pending_kickoffs() -> cudaMemcpy2DAsync of the request's committed
+//      full KV from the pinned host pool into a free HBM staging slot on the
+//      copy stream (tier 1), or nothing (tier 0: full KV already resident);
+//   2. completed_transfers <- cudaEventQuery of those copies;
+//   3. the iteration is planned on a copy of the scheduler (same state, a
+//      recording sampler) to learn which sessions draft and which verify;
+//   4. ONE forward pass runs every drafting row and every verify window;
+//   5. execution_step() is replayed on the real scheduler with a sampler
+//      that returns the measured accept counts in fire_verify order, so the
+//      rings, cadence and stalls evolve exactly as Algorithm 1 prescribes.
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <deque>
+#include <map>
+
+#include "speckv_b200.hpp"
+#include "vc_api.h"
+#include "vc_engine.hpp"
+
+namespace {
+
+struct RecordingSampler : speckv::RoundSampler {
+  std::vector<std::pair<int, double>> calls;
+  double accepted_drafted(int drafted, double c) override {
+    calls.emplace_back(drafted, c);
+    return static_cast<double>(drafted);
+  }
+};
+
+struct MeasuredSampler : speckv::RoundSampler {
+  std::deque<int> accepted;  // accepted drafted tokens, fire_verify order
+  double accepted_drafted(int, double) override {
+    if (accepted.empty()) throw speckv::ContractError("scheduled loop: verify without a measured result");
+    const int a = accepted.front();
+    accepted.pop_front();
+    return static_cast<double>(a);
+  }
+};
+
+}  // namespace
+
+int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sched_desc& sd,
+                          int32_t* out, vc_sched_stats* stats) {
+  const auto& cfgE = en.config();
+  const bool staged = cfgE.full_tier == 1;
+  if (sd.x < 1 || sd.x > cfgE.max_x) throw speckv::ConfigError("scheduled: x out of [1, max_x]");
+  if (cfgE.quant_bits == 0) throw vc::ContractViolation("scheduled: needs the compressed tier");
+  const size_t bpt = en.full_kv_bytes_per_token();
+
+  // ---- measure T_iter if not given: one draft step over every request ----
+  double t_iter = sd.iteration_time;
+  if (t_iter <= 0) {
+    std::vector<vc::StepItem> probe(n);
+    for (int i = 0; i < n; ++i) {
+      probe[i].slot = slots[i];
+      probe[i].mode = vc::RowMode::Draft;
+      probe[i].tokens = {en.seq(slots[i]).pending};
+    }
+    std::vector<int32_t> o;
+    en.run_step(probe, o);  // warm (graph capture)
+    const auto a = std::chrono::steady_clock::now();
+    for (int r = 0; r < 3; ++r) en.run_step(probe, o);
+    t_iter = std::chrono::duration<double>(std::chrono::steady_clock::now() - a).count() / 3;
+  }
+  const double bw = sd.link_bandwidth > 0 ? sd.link_bandwidth : (staged ? 55e9 : 1e15);
+
+  // ---- SystemConfig of this serving instance ------------------------------
+  speckv::SystemConfig cfg;
+  cfg.scenario = speckv::Scenario::LongContext;
+  cfg.hardware.hbm_bandwidth = 6.5e12;
+  cfg.hardware.interconnect_bandwidth = bw;
+  cfg.hardware.local_gpus = 1;
+  cfg.model.weights_bytes = static_cast<speckv::Bytes>(en.weight_bytes());
+  cfg.model.kv_bytes_per_token = static_cast<speckv::Bytes>(bpt);
+  speckv::Bytes kv_max = 0, resident_total = 0;
+  std::vector<double> ratio(n);
+  for (int i = 0; i < n; ++i) {
+    const auto& s = en.seq(slots[i]);
+    const speckv::Bytes kv = static_cast<speckv::Bytes>(s.committed) * bpt;
+    kv_max = std::max(kv_max, kv);
+    ratio[i] = std::min(1.0, static_cast<double>(en.compressed_bytes(slots[i])) / static_cast<double>(kv));
+    resident_total += static_cast<speckv::Bytes>(std::ceil(ratio[i] * kv));
+  }
+  // HBM ring capacity: weights + resident compressed caches + one full KV per
+  // staging slot, so the ring never books more reloads than we can stage.
+  const int n_stage = staged ? cfgE.n_stage : std::max(1, cfgE.max_verify);
+  cfg.hardware.gpu_mem = sd.hbm_capacity > 0
+                             ? sd.hbm_capacity
+                             : cfg.model.weights_bytes + resident_total + n_stage * (kv_max + kv_max / 64);
+  cfg.acceptance.kind = speckv::AcceptanceModel::Kind::PerTokenIid;
+  for (double c : ratio) cfg.acceptance.per_token_prob[c] = 0.99;
+  cfg.draft_length = sd.x;
+  cfg.lookahead_window = sd.window;
+  cfg.iteration_time_mode = speckv::IterationTimeMode::Fixed;
+  cfg.iteration_time = t_iter;
+  cfg.batch_size = n;
+  cfg.kv_full_bytes = kv_max;
+  cfg.compression_ratio = ratio[0];
+  cfg.output_tokens = sd.K;
+  cfg.validate();
+
+  RecordingSampler rec;
+  MeasuredSampler meas;
+  speckv::SpecScheduler sched(cfg, meas);
+  speckv::StepEvents ev;
+  for (int i = 0; i < n; ++i) {
+    speckv::Request r;
+    r.id = i;
+    r.kv_full_bytes = static_cast<speckv::Bytes>(en.seq(slots[i]).committed) * bpt;
+    r.compression_ratio = ratio[i];
+    r.output_tokens = sd.K;
+    ev.arrivals.push_back(r);
+  }
+
+  std::vector<int> produced(n, 0);
+  std::vector<int> stage_of(n, -1);
+  std::vector<int> free_stages;
+  for (int s = n_stage - 1; s >= 0; --s) free_stages.push_back(s);
+  struct Xfer {
+    uint64_t id;
+    speckv::ReservationId res;
+    int req;
+  };
+  std::vector<Xfer> inflight;
+  std::deque<speckv::Reservation> deferred;  // kickoffs waiting for a staging slot
+  vc_sched_stats st{};
+  double accepted_sum = 0;
+  const auto t0 = std::chrono::steady_clock::now();
+  const std::int64_t guard_iters = 10000 + 20LL * (sd.window + sd.x) + 64LL * sd.K * n;
+
+  for (std::int64_t it = 0; !sched.idle() || !ev.arrivals.empty(); ++it) {
+    if (it > guard_iters) throw speckv::ConfigError("scheduled loop stalled");
+    // 1. kick off this iteration's transfers
+    for (const auto& r : sched.pending_kickoffs()) {
+      if (r.bytes == 0) {  // arrival load: the compressed tier is already resident
+        ev.completed_transfers.push_back(r.id);
+        continue;
+      }
+      deferred.push_back(r);
+    }
+    while (!deferred.empty()) {
+      const auto r = deferred.front();
+      const int req = static_cast<int>(r.request_id);
+      if (!staged) {
+        ev.completed_transfers.push_back(r.id);
+        deferred.pop_front();
+        continue;
+      }
+      if (free_stages.empty()) break;
+      const int s = free_stages.back();
+      free_stages.pop_back();
+      stage_of[req] = s;
+      inflight.push_back({en.swap_begin(slots[req], s), r.id, req});
+      st.h2d_bytes += 2.0 * static_cast<double>(en.seq(slots[req]).committed) * (bpt / 2);
+      deferred.pop_front();
+    }
+    // 2. completions
+    for (size_t i = 0; i < inflight.size();) {
+      if (en.swap_done(inflight[i].id)) {
+        ev.completed_transfers.push_back(inflight[i].res);
+        inflight.erase(inflight.begin() + i);
+      } else {
+        ++i;
+      }
+    }
+    // 3. plan on a copy
+    speckv::SpecScheduler plan = sched;
+    rec.calls.clear();
+    plan.set_sampler(rec);
+    const speckv::StepResult pr = plan.execution_step(ev);
+    // 4. one forward pass: drafting rows + verify windows
+    std::vector<vc::StepItem> items;
+    for (speckv::RequestId id : pr.drafted) {
+      const auto& s = en.seq(slots[id]);
+      vc::StepItem t;
+      t.slot = slots[id];
+      t.mode = vc::RowMode::Draft;
+      t.tokens = {s.drafted.empty() ? s.pending : s.drafted.back()};
+      items.push_back(std::move(t));
+    }
+    std::vector<int> verifying;
+    for (const auto& v : pr.verifies) {
+      const int req = static_cast<int>(v.request);
+      const auto& s = en.seq(slots[req]);
+      if (static_cast<int>(s.drafted.size()) != v.drafted)
+        throw vc::ContractViolation("scheduled loop: draft count diverged from the scheduler");
+      vc::StepItem t;
+      t.slot = slots[req];
+      t.mode = vc::RowMode::Verify;
+      t.stage = staged ? stage_of[req] : -1;
+      t.tokens.push_back(s.pending);
+      t.tokens.insert(t.tokens.end(), s.drafted.begin(), s.drafted.end());
+      items.push_back(std::move(t));
+      verifying.push_back(req);
+    }
+    std::vector<int32_t> row;
+    if (!items.empty()) en.run_step(items, row);
+    size_t off = 0;
+    for (speckv::RequestId id : pr.drafted) en.push_draft(slots[id], row[off++]);
+    meas.accepted.clear();
+    for (int req : verifying) {
+      const int x_r = static_cast<int>(en.seq(slots[req]).drafted.size());
+      std::vector<int32_t> p(row.begin() + off, row.begin() + off + x_r + 1);
+      off += x_r + 1;
+      const auto em = en.accept_commit(slots[req], p, staged ? stage_of[req] : -1);
+      meas.accepted.push_back(static_cast<int>(em.size()) - 1);
+      accepted_sum += static_cast<double>(em.size()) - 1;
+      for (int32_t t : em)
+        if (produced[req] < sd.K) out[static_cast<size_t>(req) * sd.K + produced[req]++] = t;
+      if (staged) {
+        free_stages.push_back(stage_of[req]);
+        stage_of[req] = -1;
+      }
+    }
+    // 5. the real step with measured accept counts
+    const speckv::StepResult rr = sched.execution_step(ev);
+    if (rr.drafted != pr.drafted || rr.verify_count != pr.verify_count)
+      throw vc::ContractViolation("scheduled loop: replay diverged from plan");
+    st.verifies += rr.verify_count;
+    st.late_transfers += static_cast<int64_t>(rr.late_transfers.size());
+    st.iterations += 1;
+    ev = speckv::StepEvents{};
+  }
+  const auto t1 = std::chrono::steady_clock::now();
+  st.wall_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+  for (int i = 0; i < n; ++i) st.tokens += produced[i];
+  st.mean_accept = st.verifies ? accepted_sum / static_cast<double>(st.verifies) : 0.0;
+  if (stats) *stats = st;
+  return VC_OK;
+}

@@ -1,0 +1,11 @@
+// vc_topk.h -- drop-topk compressor kernels.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace vc {
+cudaError_t key_scores(const uint16_t* keys, int rows, int T, int d, const float* w, float* scores,
+                       cudaStream_t st);
+cudaError_t topk_select(const float* scores, int rows, int T, int k, int32_t* kept,
+                        cudaStream_t st);
+}  // namespace vc

@@ -1,0 +1,305 @@
+"""Python host mirror of the reference interface for the decode-loop path.
+
+Thin numpy/ctypes layer over include/vc_api.h, with the reference's names
+and argument meanings so parity tests read like /root/reference/proj/tests:
+
+  Engine.compress(slot)            speckv::compress, quant-uniform (compressor.cpp:130-178)
+  Engine.draft(slots)              one TokenOracle::next per drafting request (specloop.cpp:11-22)
+  Engine.verify(slots)             speckv::verify: x+1 predictions (specloop.cpp:24-35)
+  accept(drafted, predictions)     speckv::accept (specloop.cpp:37-56)
+  Engine.run_speculative(...)      speckv::run_speculative (specloop.cpp:58-79)
+  Engine.autoregress(...)          speckv::autoregress over the full KV (specloop.cpp:81-92)
+  Engine.run_scheduled(...)        simulate_staggered's loop on real kernels (sim.cpp:182-307)
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from ._lib import check
+
+
+def _ptr(a: np.ndarray, ctype):
+    return a.ctypes.data_as(C.POINTER(ctype))
+
+
+@dataclass
+class ModelShape:
+    vocab: int
+    hidden: int
+    layers: int
+    n_q: int
+    n_kv: int
+    d_head: int
+    ffn: int
+    rope_theta: float = 500000.0
+    rms_eps: float = 1e-5
+
+    @property
+    def kv_bytes_per_token(self) -> int:
+        return self.layers * self.n_kv * self.d_head * 2 * 2
+
+
+# BASELINE.json configs[0] (tiny) and configs[1] (Llama-3-8B shape).  The
+# tiny model's FFN and vocabulary are not fixed by the reference; these are
+# the values DESIGN.md documents.
+TINY = ModelShape(vocab=2048, hidden=512, layers=2, n_q=8, n_kv=2, d_head=64, ffn=1536)
+LLAMA3_8B = ModelShape(vocab=128256, hidden=4096, layers=32, n_q=32, n_kv=8, d_head=128, ffn=14336)
+LLAMA3_70B = ModelShape(vocab=128256, hidden=8192, layers=80, n_q=64, n_kv=8, d_head=128, ffn=28672)
+
+
+@dataclass
+class SpecRoundResult:
+    drafted: list
+    predictions: list
+    accepted: list
+    bonus_used: bool
+    first_mismatch: int | None
+
+
+def accept(drafted, predictions) -> SpecRoundResult:
+    """speckv::accept through the C-ABI (vc_accept)."""
+    lib = _lib.load()
+    d = np.ascontiguousarray(drafted, dtype=np.int32)
+    p = np.ascontiguousarray(predictions, dtype=np.int32)
+    if p.size != d.size + 1:
+        raise _lib.ContractError(2, "accept: |predictions| must equal |drafted| + 1")
+    out = np.zeros(d.size + 1, np.int32)
+    n, fm, bonus = C.c_int(), C.c_int(), C.c_int()
+    check(lib.vc_accept(_ptr(d, C.c_int32), _ptr(p, C.c_int32), d.size, _ptr(out, C.c_int32),
+                        C.byref(n), C.byref(fm), C.byref(bonus)))
+    return SpecRoundResult(d.tolist(), p.tolist(), out[: n.value].tolist(), bool(bonus.value),
+                           fm.value or None)
+
+
+def drop_indices(kind: str, layers: int, heads: int, tokens: int, ratio: float, seed: int = 0,
+                 sink_tokens: int = 0) -> np.ndarray:
+    """Dropped positions [layers][heads][drop] of drop-uniform / drop-window."""
+    lib = _lib.load()
+    k = {"drop-uniform": 0, "drop-window": 1}[kind]
+    retained = int(math.floor(ratio * tokens + 0.5))
+    drop = max(tokens - retained, 0)
+    out = np.zeros((layers, heads, max(drop, 1)), np.int64)
+    rc = lib.vc_drop_indices(k, layers, heads, tokens, ratio, seed, sink_tokens, _ptr(out, C.c_int64))
+    if rc < 0:
+        check(-rc)
+    return out[:, :, :rc]
+
+
+def reload_span(bytes_: int, bandwidth: float, iteration_time: float):
+    lib = _lib.load()
+    it, w = C.c_double(), C.c_int()
+    check(lib.vc_reload_span(int(bytes_), bandwidth, iteration_time, C.byref(it), C.byref(w)))
+    return it.value, w.value
+
+
+class Engine:
+    """One serving instance on one GPU (vc_engine)."""
+
+    def __init__(self, model: ModelShape, *, max_slots=1, max_ctx=4096, max_x=16, quant_bits=4,
+                 full_tier=0, n_stage=2, max_verify=2, use_graphs=True, device=0):
+        self.lib = _lib.load()
+        self.model = model
+        self.max_x = max_x
+        md = _lib.ModelDesc(model.vocab, model.hidden, model.layers, model.n_q, model.n_kv,
+                            model.d_head, model.ffn, model.rope_theta, model.rms_eps)
+        rt = _lib.RuntimeDesc(max_slots, max_ctx, max_x, quant_bits, full_tier, n_stage,
+                              max_verify, int(use_graphs))
+        h = C.c_void_p()
+        check(self.lib.vc_engine_create(C.byref(md), C.byref(rt), device, C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.vc_engine_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # ---- weights ----------------------------------------------------------------
+    def init_weights(self, seed: int = 0, std: float = 0.02):
+        check(self.lib.vc_engine_init_weights(self.h, seed, std))
+
+    def load_weights(self, w: dict):
+        """w: logical bf16-bit arrays (uint16) as oracle/vc_oracle.h documents."""
+        L = self.model.layers
+        keep = []
+
+        def arr(a):
+            a = np.ascontiguousarray(a, dtype=np.uint16)
+            keep.append(a)
+            return _ptr(a, C.c_uint16)
+
+        def lst(name):
+            ptrs = (_lib.PU16 * L)(*[arr(w[name][i]) for i in range(L)])
+            keep.append(ptrs)
+            return ptrs
+
+        check(self.lib.vc_engine_load_weights(
+            self.h, arr(w["embed"]), lst("attn_norm"), lst("wqkv"), lst("wo"), lst("mlp_norm"),
+            lst("wgate"), lst("wup"), lst("wdown"), arr(w["final_norm"]), arr(w["lm_head"])))
+
+    def stats(self):
+        n, b = C.c_uint64(), C.c_uint64()
+        check(self.lib.vc_engine_stats(self.h, C.byref(n), C.byref(b)))
+        return {"kernel_launches": n.value, "weight_bytes": b.value}
+
+    # ---- requests ---------------------------------------------------------------
+    def add_synthetic(self, slot, n_ctx, first_token, seed=1, outlier_channels=4, outlier_scale=10.0):
+        check(self.lib.vc_request_add_synthetic(self.h, slot, n_ctx, first_token, seed,
+                                                outlier_channels, outlier_scale))
+
+    def add_kv(self, slot, k: np.ndarray, v: np.ndarray, first_token: int):
+        """k, v: uint16 bf16 bits [layers][n_kv][n_ctx][d]."""
+        k = np.ascontiguousarray(k, np.uint16)
+        v = np.ascontiguousarray(v, np.uint16)
+        check(self.lib.vc_request_add_kv(self.h, slot, k.shape[2], first_token, _ptr(k, C.c_uint16),
+                                         _ptr(v, C.c_uint16)))
+
+    def prefill(self, slot, prompt):
+        p = np.ascontiguousarray(prompt, np.int32)
+        check(self.lib.vc_request_prefill(self.h, slot, _ptr(p, C.c_int32), p.size))
+
+    def release(self, slot):
+        check(self.lib.vc_request_release(self.h, slot))
+
+    def state(self, slot) -> dict:
+        s = _lib.SeqState()
+        check(self.lib.vc_request_state(self.h, slot, C.byref(s)))
+        return {f: getattr(s, f) for f, _ in s._fields_}
+
+    def history(self, slot) -> list:
+        cap = 1 << 16
+        out = np.zeros(cap, np.int32)
+        n = C.c_int()
+        check(self.lib.vc_request_history(self.h, slot, _ptr(out, C.c_int32), cap, C.byref(n)))
+        return out[: n.value].tolist()
+
+    # ---- compressor -------------------------------------------------------------
+    def compress(self, slot) -> dict:
+        m = _lib.CompressedMeta()
+        check(self.lib.vc_compress(self.h, slot, C.byref(m)))
+        return {f: getattr(m, f) for f, _ in m._fields_}
+
+    def compressed_geometry(self):
+        g, w, t, mg = C.c_int(), C.c_int(), C.c_int(), C.c_int()
+        check(self.lib.vc_compressed_geometry(self.h, C.byref(g), C.byref(w), C.byref(t), C.byref(mg)))
+        return g.value, w.value, t.value, mg.value
+
+    def compressed_read(self, slot, layer, head):
+        G, words, tail_cap, max_groups = self.compressed_geometry()
+        d = self.model.d_head
+        kc = np.zeros(words * max_groups, np.uint32)
+        vc = np.zeros_like(kc)
+        ksz = np.zeros(max_groups * d, np.uint32)
+        vsz = np.zeros(max_groups * G, np.uint32)
+        kt = np.zeros(tail_cap * d, np.uint16)
+        vt = np.zeros_like(kt)
+        check(self.lib.vc_compressed_read(self.h, slot, layer, head, _ptr(kc, C.c_uint32),
+                                          _ptr(ksz, C.c_uint32), _ptr(vc, C.c_uint32),
+                                          _ptr(vsz, C.c_uint32), _ptr(kt, C.c_uint16),
+                                          _ptr(vt, C.c_uint16)))
+        return dict(kc=kc, vc=vc, ksz=ksz, vsz=vsz, ktail=kt.reshape(tail_cap, d),
+                    vtail=vt.reshape(tail_cap, d))
+
+    # ---- steps ------------------------------------------------------------------
+    def step(self, items, want_logits=False):
+        """items: list of (slot, mode, tokens, stage); mode 0 decode, 1 draft, 2 verify."""
+        arr = (_lib.StepItem * len(items))()
+        keep = []
+        rows = 0
+        for i, (slot, mode, toks, stage) in enumerate(items):
+            t = np.ascontiguousarray(toks, np.int32)
+            keep.append(t)
+            arr[i] = _lib.StepItem(slot, mode, t.size, stage, _ptr(t, C.c_int32))
+            rows += t.size
+        out = np.zeros(rows, np.int32)
+        logits = np.zeros((rows, self.model.vocab), np.float32) if want_logits else None
+        check(self.lib.vc_step(self.h, arr, len(items), _ptr(out, C.c_int32),
+                               _ptr(logits, C.c_float) if want_logits else None))
+        return (out, logits) if want_logits else out
+
+    def decode_step(self, slots):
+        s = np.ascontiguousarray(slots, np.int32)
+        out = np.zeros(s.size, np.int32)
+        check(self.lib.vc_decode_step(self.h, _ptr(s, C.c_int), s.size, _ptr(out, C.c_int32)))
+        return out
+
+    def draft(self, slots):
+        s = np.ascontiguousarray(slots, np.int32)
+        out = np.zeros(s.size, np.int32)
+        check(self.lib.vc_draft_step(self.h, _ptr(s, C.c_int), s.size, _ptr(out, C.c_int32)))
+        return out
+
+    def verify(self, slots, stages=None):
+        s = np.ascontiguousarray(slots, np.int32)
+        total = sum(self.state(int(x))["draft_len"] + 1 for x in s)
+        out = np.zeros(total, np.int32)
+        st = np.ascontiguousarray(stages, np.int32) if stages is not None else None
+        check(self.lib.vc_verify(self.h, _ptr(s, C.c_int), s.size,
+                                 _ptr(st, C.c_int) if st is not None else None, _ptr(out, C.c_int32)))
+        return out
+
+    def accept_commit(self, slot, preds, stage=-1):
+        p = np.ascontiguousarray(preds, np.int32)
+        out = np.zeros(p.size, np.int32)
+        n = C.c_int()
+        check(self.lib.vc_accept_commit(self.h, slot, _ptr(p, C.c_int32), stage, _ptr(out, C.c_int32),
+                                        C.byref(n)))
+        return out[: n.value].tolist()
+
+    def swap_begin(self, slot, stage) -> int:
+        x = C.c_uint64()
+        check(self.lib.vc_swap_begin(self.h, slot, stage, C.byref(x)))
+        return x.value
+
+    def swap_poll(self, xfer) -> bool:
+        d = C.c_int()
+        check(self.lib.vc_swap_poll(self.h, xfer, C.byref(d)))
+        return bool(d.value)
+
+    # ---- loops ------------------------------------------------------------------
+    def autoregress(self, slots, K):
+        """Full-KV greedy decode of K tokens per slot -> (tokens [n][K], ms)."""
+        s = np.ascontiguousarray(slots, np.int32)
+        out = np.zeros((s.size, K), np.int32)
+        ms = C.c_double()
+        check(self.lib.vc_run_decode(self.h, _ptr(s, C.c_int), s.size, K, _ptr(out, C.c_int32),
+                                     C.byref(ms)))
+        return out, ms.value
+
+    def run_speculative(self, slots, K, x, max_rounds=4096):
+        s = np.ascontiguousarray(slots, np.int32)
+        out = np.zeros((s.size, K), np.int32)
+        rounds = np.zeros((s.size, max_rounds), np.int32)
+        nr = np.zeros(s.size, np.int32)
+        ms = C.c_double()
+        check(self.lib.vc_run_speculative(self.h, _ptr(s, C.c_int), s.size, K, x, _ptr(out, C.c_int32),
+                                          _ptr(rounds, C.c_int32), max_rounds, _ptr(nr, C.c_int),
+                                          C.byref(ms)))
+        return out, [rounds[i, : nr[i]].tolist() for i in range(s.size)], ms.value
+
+    def run_scheduled(self, slots, K, x, window, iteration_time=0.0, link_bandwidth=0.0,
+                      hbm_capacity=0):
+        s = np.ascontiguousarray(slots, np.int32)
+        out = np.zeros((s.size, K), np.int32)
+        sd = _lib.SchedDesc(x, window, iteration_time, link_bandwidth, hbm_capacity, K)
+        st = _lib.SchedStats()
+        check(self.lib.vc_run_scheduled(self.h, _ptr(s, C.c_int), s.size, C.byref(sd),
+                                        _ptr(out, C.c_int32), C.byref(st)))
+        return out, {f: getattr(st, f) for f, _ in st._fields_}
+
+    # ---- probes -----------------------------------------------------------------
+    def attention_probe(self, slot, layer, mode, q_dev_ptr, n_rows, kv_len):
+        out = np.zeros((n_rows, self.model.n_q, self.model.d_head), np.uint16)
+        check(self.lib.vc_attention_probe(self.h, slot, layer, mode, C.c_void_p(q_dev_ptr), n_rows,
+                                          kv_len, _ptr(out, C.c_uint16)))
+        return out
