@@ -102,6 +102,14 @@ int vc_engine_load_weights(vc_engine* e, const uint16_t* embed, const uint16_t* 
                            const uint16_t* const* wup, const uint16_t* const* wdown,
                            const uint16_t* final_norm, const uint16_t* lm_head);
 int vc_engine_stats(vc_engine* e, uint64_t* kernel_launches, uint64_t* weight_bytes);
+/* Device time (CUDA events, H2D of a step's inputs -> D2H of its tokens)
+ * summed over steps since the last reset.                                  */
+int vc_engine_timing(vc_engine* e, double* device_ms, int64_t* steps, int reset);
+/* Isolated timing of one kernel family over every layer for the given
+ * requests: kind 0 draft attention, 1 dense attention.  *bytes = the
+ * algorithmic bytes one launch-set moves.           */
+int vc_kernel_bench(vc_engine* e, int kind, const int* slots, int n, int reps, double* ms,
+                    double* bytes);
 
 /* ---- requests ----------------------------------------------------------- */
 int vc_request_add_synthetic(vc_engine* e, int slot, int n_ctx, int32_t first_token, uint64_t seed,
@@ -183,6 +191,8 @@ typedef struct {
   double link_bandwidth;    /* planning BW (B/s); <= 0: measure */
   int64_t hbm_capacity;     /* bytes for weights + resident + in-flight */
   int K;                    /* output tokens per request */
+  int64_t warmup_iterations;  /* iterations before the timed window */
+  int64_t timed_iterations;   /* length of the timed window; 0 = run to completion */
 } vc_sched_desc;
 
 typedef struct {
@@ -195,6 +205,11 @@ typedef struct {
   double h2d_ms;            /* copy-engine busy time */
   double verify_wait_ms;    /* time verifies waited on copy events */
   double mean_accept;       /* accepted drafted tokens per verify */
+  int64_t timed_iterations; /* iterations inside the timed window */
+  int64_t timed_tokens;     /* tokens emitted inside the timed window */
+  double timed_wall_ms;     /* host wall time of the timed window (e2e) */
+  double timed_device_ms;   /* device time of the window's steps */
+  double timed_rows;        /* activation rows executed in the window */
 } vc_sched_stats;
 
 int vc_run_scheduled(vc_engine* e, const int* slots, int n, const vc_sched_desc* sd,

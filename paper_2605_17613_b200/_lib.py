@@ -61,13 +61,17 @@ class StepItem(C.Structure):
 
 class SchedDesc(C.Structure):
     _fields_ = [("x", C.c_int), ("window", C.c_int), ("iteration_time", C.c_double),
-                ("link_bandwidth", C.c_double), ("hbm_capacity", C.c_int64), ("K", C.c_int)]
+                ("link_bandwidth", C.c_double), ("hbm_capacity", C.c_int64), ("K", C.c_int),
+                ("warmup_iterations", C.c_int64), ("timed_iterations", C.c_int64)]
 
 
 class SchedStats(C.Structure):
     _fields_ = [("wall_ms", C.c_double), ("tokens", C.c_int64), ("iterations", C.c_int64),
                 ("verifies", C.c_int64), ("late_transfers", C.c_int64), ("h2d_bytes", C.c_double),
-                ("h2d_ms", C.c_double), ("verify_wait_ms", C.c_double), ("mean_accept", C.c_double)]
+                ("h2d_ms", C.c_double), ("verify_wait_ms", C.c_double), ("mean_accept", C.c_double),
+                ("timed_iterations", C.c_int64), ("timed_tokens", C.c_int64),
+                ("timed_wall_ms", C.c_double), ("timed_device_ms", C.c_double),
+                ("timed_rows", C.c_double)]
 
 
 P = C.c_void_p
@@ -86,6 +90,8 @@ SIGNATURES = {
     "vc_engine_init_weights": (I, [P, U64, F]),
     "vc_engine_load_weights": (I, [P, PU16, PPU16, PPU16, PPU16, PPU16, PPU16, PPU16, PPU16, PU16, PU16]),
     "vc_engine_stats": (I, [P, PU64, PU64]),
+    "vc_engine_timing": (I, [P, PD, PI64, I]),
+    "vc_kernel_bench": (I, [P, I, PI, I, I, PD, PD]),
     "vc_request_add_synthetic": (I, [P, I, I, C.c_int32, U64, I, F]),
     "vc_request_add_kv": (I, [P, I, I, C.c_int32, PU16, PU16]),
     "vc_request_prefill": (I, [P, I, PI32, I]),

@@ -123,6 +123,23 @@ int vc_engine_stats(vc_engine* e, uint64_t* launches, uint64_t* weight_bytes) {
   });
 }
 
+int vc_engine_timing(vc_engine* e, double* device_ms, int64_t* steps, int reset) {
+  return guard([&] {
+    vc::Engine& en = E(e);
+    if (device_ms) *device_ms = en.device_ms();
+    if (steps) *steps = en.steps();
+    if (reset) en.reset_timing();
+  });
+}
+
+int vc_kernel_bench(vc_engine* e, int kind, const int* slots, int n, int reps, double* ms,
+                    double* bytes) {
+  return guard([&] {
+    if (reps < 1 || n < 1) throw speckv::ConfigError("kernel_bench: reps and n must be >= 1");
+    E(e).kernel_bench(kind, std::vector<int>(slots, slots + n), reps, ms, bytes);
+  });
+}
+
 int vc_request_add_synthetic(vc_engine* e, int slot, int n_ctx, int32_t first_token, uint64_t seed,
                              int outlier_channels, float outlier_scale) {
   return guard([&] { E(e).add_request_synthetic(slot, n_ctx, first_token, seed, outlier_channels, outlier_scale); });

@@ -593,6 +593,7 @@ void Engine::run_step(const std::vector<StepItem>& items, std::vector<int32_t>& 
   for (auto& a : drafts) h_seqs[k++] = a;
   for (auto& a : dense1) h_seqs[k++] = a;
   for (auto& a : densev) h_seqs[k++] = a;
+  VC_CK(cudaEventRecord(ev_a_, st_));
   VC_CK(cudaMemcpyAsync(tok_in_, h_tok, M * sizeof(int32_t), cudaMemcpyHostToDevice, st_));
   VC_CK(cudaMemcpyAsync(rows_dev_, h_rows, M * sizeof(RowDest), cudaMemcpyHostToDevice, st_));
   VC_CK(cudaMemcpyAsync(seqs_dev_, h_seqs, k * sizeof(AttnSeq), cudaMemcpyHostToDevice, st_));
@@ -625,9 +626,74 @@ void Engine::run_step(const std::vector<StepItem>& items, std::vector<int32_t>& 
   if (logits_host)
     VC_CK(cudaMemcpyAsync(logits_host, logits_, static_cast<size_t>(M) * m.vocab * 4,
                           cudaMemcpyDeviceToHost, st_));
+  VC_CK(cudaEventRecord(ev_b_, st_));
   VC_CK(cudaStreamSynchronize(st_));
+  float ms = 0.f;
+  VC_CK(cudaEventElapsedTime(&ms, ev_a_, ev_b_));
+  device_ms_ += ms;
+  ++steps_;
   out.assign(h_out_, h_out_ + M);
   last_M_ = M;
+}
+
+void Engine::kernel_bench(int kind, const std::vector<int>& slots, int reps, double* ms,
+                          double* bytes) {
+  const auto& m = cfg_.model;
+  const int n = static_cast<int>(slots.size());
+  AttnShape as;
+  as.layers = m.layers;
+  as.n_kv = m.n_kv;
+  as.n_rep = m.n_q / m.n_kv;
+  as.d = m.d;
+  as.q_stride = (m.n_q + 2 * m.n_kv) * m.d;
+  as.out_stride = m.n_q * m.d;
+  as.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(m.d)));
+  AttnSeq* h = reinterpret_cast<AttnSeq*>(static_cast<int32_t*>(h_desc_) + Mmax_) ;
+  h = reinterpret_cast<AttnSeq*>(reinterpret_cast<RowDest*>(h) + Mmax_);
+  double b = 0.0;
+  const double g = VC_QGROUP;
+  for (int i = 0; i < n; ++i) {
+    const SeqState& s = seqs_.at(slots[i]);
+    AttnSeq a{};
+    a.slot = slots[i];
+    a.row0 = i;
+    a.n_rows = 1;
+    a.kv_len = s.committed;
+    a.n_groups = s.n_groups;
+    a.tail_len = s.tail_committed;
+    a.part0 = kind == 0 ? i * (max_chunks_q_ + 1) : i * max_chunks_d_;
+    h[i] = a;
+    // algorithmic bytes per (layer, request, kv-head) -- DESIGN.md §Roofline
+    if (kind == 0)
+      b += s.n_groups * g * m.d * cfg_.quant_bits / 8.0 * 2  // K + V codes
+           + s.n_groups * m.d * 4.0 + s.n_groups * g * 4.0   // K per-channel, V per-token (scale, zero)
+           + s.tail_committed * m.d * 2.0 * 2;                // bf16 tail
+    else
+      b += static_cast<double>(s.committed) * m.d * 2 * 2;
+  }
+  b *= static_cast<double>(m.layers) * m.n_kv;
+  VC_CK(cudaMemcpyAsync(seqs_dev_, h, n * sizeof(AttnSeq), cudaMemcpyHostToDevice, st_));
+  auto launch_all = [&] {
+    for (int l = 0; l < m.layers; ++l) {
+      if (kind == 0) {
+        VC_LAUNCH(draft_attention_quant(as, quant_, l, qkv_, seqs_dev_, n, max_chunks_q_, cfg_.quant_bits, part_, st_));
+        VC_LAUNCH(attention_combine(as, seqs_dev_, n, max_chunks_q_, 1, 0, part_, attn_, st_));
+      } else {
+        const KvPool pool = cfg_.full_tier == 0 ? full_ : stage_;
+        VC_LAUNCH(dense_attention(as, pool, l, qkv_, seqs_dev_, n, max_chunks_d_, 1, part_, st_));
+        VC_LAUNCH(attention_combine(as, seqs_dev_, n, max_chunks_d_, 1, 1, part_, attn_, st_));
+      }
+    }
+  };
+  launch_all();  // warm
+  VC_CK(cudaEventRecord(ev_a_, st_));
+  for (int r = 0; r < reps; ++r) launch_all();
+  VC_CK(cudaEventRecord(ev_b_, st_));
+  VC_CK(cudaEventSynchronize(ev_b_));
+  float t = 0.f;
+  VC_CK(cudaEventElapsedTime(&t, ev_a_, ev_b_));
+  *ms = t / reps;
+  *bytes = b;
 }
 
 void Engine::commit_decode(int slot, int32_t next) {

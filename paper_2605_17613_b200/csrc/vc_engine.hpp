@@ -141,9 +141,14 @@ class Engine {
   // request/layer: mode 1 draft over the compressed tier, else dense.
   void attention_probe(int slot, int layer, int mode, const uint16_t* q_dev, int n_rows,
                        int kv_len, uint16_t* out_host);
-  // Device-side greedy loop helpers (timing of the step executor).
-  cudaEvent_t ev_a() const { return ev_a_; }
-  cudaEvent_t ev_b() const { return ev_b_; }
+  // Device time of run_step (H2D descriptors -> D2H tokens), accumulated.
+  double device_ms() const { return device_ms_; }
+  int64_t steps() const { return steps_; }
+  void reset_timing() { device_ms_ = 0.0; steps_ = 0; }
+  // Isolated timing of one kernel family over the given requests (all
+  // layers): kind 0 draft attention (+combine), 1 dense attention (+combine).
+  // Returns ms per launch-set and the algorithmic bytes it moves.
+  void kernel_bench(int kind, const std::vector<int>& slots, int reps, double* ms, double* bytes);
 
  private:
   struct Weights {
@@ -193,6 +198,8 @@ class Engine {
   std::map<uint64_t, cudaEvent_t> xfers_;
   uint64_t next_xfer_ = 1;
   cudaEvent_t ev_a_ = nullptr, ev_b_ = nullptr;
+  double device_ms_ = 0.0;
+  int64_t steps_ = 0;
   int splits_qkv_ = 1, splits_o_ = 1, splits_gu_ = 1, splits_d_ = 1, splits_lm_ = 1;
   size_t ws_floats_ = 0;
 };

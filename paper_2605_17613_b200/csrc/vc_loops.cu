@@ -133,8 +133,20 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
   const auto t0 = std::chrono::steady_clock::now();
   const std::int64_t guard_iters = 10000 + 20LL * (sd.window + sd.x) + 64LL * sd.K * n;
 
+  int64_t tokens_at_window = 0;
+  double rows_in_window = 0;
+  auto window_start = t0;
+  const bool bounded = sd.timed_iterations > 0;
   for (std::int64_t it = 0; !sched.idle() || !ev.arrivals.empty(); ++it) {
     if (it > guard_iters) throw speckv::ConfigError("scheduled loop stalled");
+    if (it == sd.warmup_iterations) {  // open the timed window
+      int64_t tk = 0;
+      for (int i = 0; i < n; ++i) tk += produced[i];
+      tokens_at_window = tk;
+      en.reset_timing();
+      window_start = std::chrono::steady_clock::now();
+    }
+    if (bounded && it == sd.warmup_iterations + sd.timed_iterations) break;
     // 1. kick off this iteration's transfers
     for (const auto& r : sched.pending_kickoffs()) {
       if (r.bytes == 0) {  // arrival load: the compressed tier is already resident
@@ -200,6 +212,7 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
     }
     std::vector<int32_t> row;
     if (!items.empty()) en.run_step(items, row);
+    if (it >= sd.warmup_iterations) rows_in_window += static_cast<double>(row.size());
     size_t off = 0;
     for (speckv::RequestId id : pr.drafted) en.push_draft(slots[id], row[off++]);
     meas.accepted.clear();
@@ -229,6 +242,13 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
   const auto t1 = std::chrono::steady_clock::now();
   st.wall_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
   for (int i = 0; i < n; ++i) st.tokens += produced[i];
+  if (st.iterations > sd.warmup_iterations) {
+    st.timed_iterations = st.iterations - sd.warmup_iterations;
+    st.timed_tokens = st.tokens - tokens_at_window;
+    st.timed_wall_ms = std::chrono::duration<double, std::milli>(t1 - window_start).count();
+    st.timed_device_ms = en.device_ms();
+    st.timed_rows = rows_in_window;
+  }
   st.mean_accept = st.verifies ? accepted_sum / static_cast<double>(st.verifies) : 0.0;
   if (stats) *stats = st;
   return VC_OK;

@@ -287,11 +287,24 @@ class Engine:
                                           C.byref(ms)))
         return out, [rounds[i, : nr[i]].tolist() for i in range(s.size)], ms.value
 
+    def timing(self, reset=False):
+        ms, n = C.c_double(), C.c_int64()
+        check(self.lib.vc_engine_timing(self.h, C.byref(ms), C.byref(n), int(reset)))
+        return ms.value, n.value
+
+    def kernel_bench(self, kind, slots, reps=5):
+        s = np.ascontiguousarray(slots, np.int32)
+        ms, b = C.c_double(), C.c_double()
+        check(self.lib.vc_kernel_bench(self.h, kind, _ptr(s, C.c_int), s.size, reps, C.byref(ms),
+                                       C.byref(b)))
+        return ms.value, b.value
+
     def run_scheduled(self, slots, K, x, window, iteration_time=0.0, link_bandwidth=0.0,
-                      hbm_capacity=0):
+                      hbm_capacity=0, warmup_iterations=0, timed_iterations=0):
         s = np.ascontiguousarray(slots, np.int32)
         out = np.zeros((s.size, K), np.int32)
-        sd = _lib.SchedDesc(x, window, iteration_time, link_bandwidth, hbm_capacity, K)
+        sd = _lib.SchedDesc(x, window, iteration_time, link_bandwidth, hbm_capacity, K,
+                            warmup_iterations, timed_iterations)
         st = _lib.SchedStats()
         check(self.lib.vc_run_scheduled(self.h, _ptr(s, C.c_int), s.size, C.byref(sd),
                                         _ptr(out, C.c_int32), C.byref(st)))
