@@ -521,12 +521,18 @@ int vc_attention_probe(vc_engine* e, int slot, int layer, int mode, const uint16
 int vc_gemm_probe(const uint16_t* X, int M, int K, const uint16_t* W, int N, float* Y, void* stream) {
   return guard([&] {
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    const int s = vc::gemm_splits(N, K);
-    float* ws = nullptr;
-    vc::check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&ws), sizeof(float) * s * M * N, st), "malloc");
-    vc::check_cuda(vc::gemm_partial(X, M, K, W, N, s, ws, st), "gemm_partial");
-    vc::check_cuda(vc::sum_epilogue(ws, s, M, N, Y, st), "sum_epilogue");
-    vc::check_cuda(cudaFreeAsync(ws, st), "free");
+    vc::GemmWorkspace ws;
+    ws.partial_floats = vc::gemm_partial_floats(M > 128 ? 128 : M, N, K);
+    ws.n_counters = N / 128 + 1;
+    vc::check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&ws.partial), sizeof(float) * ws.partial_floats, st), "malloc");
+    vc::check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&ws.counters), sizeof(int) * ws.n_counters, st), "malloc");
+    vc::check_cuda(cudaMemsetAsync(ws.counters, 0, sizeof(int) * ws.n_counters, st), "memset");
+    vc::GemmEpilogue ep;
+    ep.kind = vc::Epi::StoreF32;
+    ep.out_f32 = Y;
+    vc::check_cuda(vc::gemm(X, M, K, W, N, 1, ep, ws, st), "gemm");
+    vc::check_cuda(cudaFreeAsync(ws.partial, st), "free");
+    vc::check_cuda(cudaFreeAsync(ws.counters, st), "free");
     vc::check_cuda(cudaStreamSynchronize(st), "sync");
   });
 }

@@ -93,8 +93,8 @@ Engine::~Engine() {
   for (auto& [k, e] : xfers_) cudaEventDestroy(e);
   void* ptrs[] = {weight_blob_, rope_cos_, rope_sin_, full_.k, full_.v, stage_.k, stage_.v,
                   quant_.kc, quant_.ksz, quant_.vc, quant_.vsz, quant_.ktail, quant_.vtail,
-                  x_, xn_, qkv_, attn_, act_, ws_, logits_, tok_in_, tok_out_, part_.o, part_.ml,
-                  rows_dev_, seqs_dev_, jobs_dev_};
+                  x_, xn_, qkv_, attn_, act_, gws_.partial, gws_.counters, ss_part_, logits_,
+                  tok_in_, tok_out_, part_.o, part_.ml, rows_dev_, seqs_dev_, jobs_dev_};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (host_k_) cudaFreeHost(host_k_);
@@ -237,27 +237,28 @@ void Engine::alloc_all() {
   }
   max_chunks_d_ = (cap + VC_DENSE_CHUNK - 1) / VC_DENSE_CHUNK;
   // ---- activations ---------------------------------------------------------
-  Mmax_ = cfg_.max_slots + cfg_.max_verify * (cfg_.max_x + 1);
-  if (Mmax_ < 8) Mmax_ = 8;
+  Mmax_ = static_cast<int>(round_up(cfg_.max_slots + cfg_.max_verify * (cfg_.max_x + 1), 64));
   x_ = dmalloc<float>(static_cast<size_t>(Mmax_) * H);
   xn_ = dmalloc<uint16_t>(static_cast<size_t>(Mmax_) * (H > F ? H : F));
   qkv_ = dmalloc<uint16_t>(static_cast<size_t>(Mmax_) * qkv_n);
   attn_ = dmalloc<uint16_t>(static_cast<size_t>(Mmax_) * m.n_q * d);
   act_ = dmalloc<uint16_t>(static_cast<size_t>(Mmax_) * F);
-  splits_qkv_ = gemm_splits(qkv_n, H);
-  splits_o_ = gemm_splits(H, m.n_q * d);
-  splits_gu_ = gemm_splits(2 * F, H);
-  splits_d_ = gemm_splits(H, F);
-  splits_lm_ = gemm_splits(V, H);
-  size_t wsf = 0;
-  auto need = [&](int s, int n) { wsf = std::max(wsf, static_cast<size_t>(s) * n); };
-  need(splits_qkv_, qkv_n);
-  need(splits_o_, H);
-  need(splits_gu_, 2 * F);
-  need(splits_d_, H);
-  need(splits_lm_, V);
-  ws_floats_ = wsf * Mmax_;
-  ws_ = dmalloc<float>(ws_floats_);
+  {
+    size_t pf = 0;
+    for (int mm : {16, 32, 64, 128}) {
+      pf = std::max(pf, gemm_partial_floats(mm, qkv_n, H));
+      pf = std::max(pf, gemm_partial_floats(mm, H, m.n_q * d));
+      pf = std::max(pf, gemm_partial_floats(mm, 2 * F, H));
+      pf = std::max(pf, gemm_partial_floats(mm, H, F));
+      pf = std::max(pf, gemm_partial_floats(mm, V, H));
+    }
+    gws_.partial_floats = pf;
+    gws_.partial = dmalloc<float>(pf);
+    gws_.n_counters = std::max(std::max(qkv_n, H), std::max(2 * F, V)) / 128 + 1;
+    gws_.counters = dmalloc<int>(gws_.n_counters);
+    VC_CK(cudaMemset(gws_.counters, 0, gws_.n_counters * sizeof(int)));
+  }
+  ss_part_ = dmalloc<float>(static_cast<size_t>(Mmax_) * (H / 128));
   logits_ = dmalloc<float>(static_cast<size_t>(Mmax_) * V);
   tok_in_ = dmalloc<int32_t>(Mmax_);
   tok_out_ = dmalloc<int32_t>(Mmax_);
@@ -267,7 +268,7 @@ void Engine::alloc_all() {
   part_.o = dmalloc<float>(prow * d);
   part_.ml = dmalloc<float>(prow * 2);
   rows_dev_ = dmalloc<RowDest>(Mmax_);
-  const int n_seq_max = 2 * cfg_.max_slots + cfg_.max_verify + 1;
+  const int n_seq_max = 2 * (cfg_.max_slots + 4) + cfg_.max_verify + 4;
   seqs_dev_ = dmalloc<AttnSeq>(n_seq_max);
   jobs_dev_ = dmalloc<QuantJob>(static_cast<size_t>(L) * m.n_kv);
   desc_bytes_ = Mmax_ * sizeof(int32_t) + Mmax_ * sizeof(RowDest) + n_seq_max * sizeof(AttnSeq) +
@@ -503,11 +504,33 @@ void Engine::enqueue_forward(int M, int n_draft, int n_dense1, int n_densev, int
   as.out_stride = m.n_q * d;
   as.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(d)));
   const KvPool dense_v_pool = cfg_.full_tier == 0 ? full_ : stage_;
+  GemmEpilogue eq;
+  eq.kind = Epi::Qkv;
+  eq.out_bf16 = qkv_;
+  eq.rows = rows_dev_;
+  eq.rope_cos = rope_cos_;
+  eq.rope_sin = rope_sin_;
+  eq.n_q = m.n_q;
+  eq.n_kv = m.n_kv;
+  eq.d = d;
+  eq.layers = L;
+  eq.full = full_;
+  eq.stage = stage_;
+  eq.draft = quant_;
+  GemmEpilogue er;
+  er.kind = Epi::Residual;
+  er.x = x_;
+  er.ss_part = ss_part_;
+  GemmEpilogue es;
+  es.kind = Epi::Silu;
+  es.out_bf16 = act_;
+  GemmEpilogue ef;
+  ef.kind = Epi::StoreF32;
+  ef.out_f32 = logits_;
   VC_LAUNCH(embed_norm(tok_in_, M, w_.embed, H, w_.attn_norm[0], m.eps, x_, xn_, st_));
   for (int l = 0; l < L; ++l) {
-    VC_LAUNCH(gemm_partial(xn_, M, H, w_.wqkv[l], qkv_n, splits_qkv_, ws_, st_));
-    VC_LAUNCH(qkv_epilogue(ws_, splits_qkv_, M, m.n_q, m.n_kv, d, rows_dev_, rope_cos_, rope_sin_, qkv_, st_));
-    VC_LAUNCH(kv_store(qkv_, M, m.n_q, m.n_kv, d, l, L, rows_dev_, full_, stage_, quant_, st_));
+    eq.layer = l;
+    VC_LAUNCH(gemm(xn_, M, H, w_.wqkv[l], qkv_n, 1, eq, gws_, st_));
     if (n_draft > 0) {
       VC_LAUNCH(draft_attention_quant(as, quant_, l, qkv_, seqs_dev_, n_draft, max_chunks_q_,
                                       cfg_.quant_bits, part_, st_));
@@ -522,23 +545,35 @@ void Engine::enqueue_forward(int M, int n_draft, int n_dense1, int n_densev, int
       VC_LAUNCH(dense_attention(as, dense_v_pool, l, qkv_, sv, n_densev, max_chunks_d_, max_rows_v, part_, st_));
       VC_LAUNCH(attention_combine(as, sv, n_densev, max_chunks_d_, max_rows_v, 1, part_, attn_, st_));
     }
-    VC_LAUNCH(gemm_partial(attn_, M, m.n_q * d, w_.wo[l], H, splits_o_, ws_, st_));
-    VC_LAUNCH(residual_norm(ws_, splits_o_, M, H, x_, w_.mlp_norm[l], m.eps, xn_, st_));
-    VC_LAUNCH(gemm_partial(xn_, M, H, w_.wgu[l], 2 * F, splits_gu_, ws_, st_));
-    VC_LAUNCH(silu_epilogue(ws_, splits_gu_, M, F, act_, st_));
-    VC_LAUNCH(gemm_partial(act_, M, F, w_.wd[l], H, splits_d_, ws_, st_));
-    VC_LAUNCH(residual_norm(ws_, splits_d_, M, H, x_, l + 1 < L ? w_.attn_norm[l + 1] : w_.final_norm,
-                            m.eps, xn_, st_));
+    VC_LAUNCH(gemm(attn_, M, m.n_q * d, w_.wo[l], H, 1, er, gws_, st_));
+    VC_LAUNCH(rms_apply(x_, ss_part_, M, H, w_.mlp_norm[l], m.eps, xn_, st_));
+    VC_LAUNCH(gemm(xn_, M, H, w_.wgu[l], 2 * F, 1, es, gws_, st_));
+    VC_LAUNCH(gemm(act_, M, F, w_.wd[l], H, 1, er, gws_, st_));
+    VC_LAUNCH(rms_apply(x_, ss_part_, M, H, l + 1 < L ? w_.attn_norm[l + 1] : w_.final_norm, m.eps,
+                        xn_, st_));
   }
-  VC_LAUNCH(gemm_partial(xn_, M, H, w_.lm_head, V, splits_lm_, ws_, st_));
-  VC_LAUNCH(sum_epilogue(ws_, splits_lm_, M, V, logits_, st_));
+  VC_LAUNCH(gemm(xn_, M, H, w_.lm_head, V, 1, ef, gws_, st_));
   VC_LAUNCH(argmax_rows(logits_, M, V, tok_out_, st_));
 }
+
+namespace {
+int bucket_rows(int M) {
+  if (M <= 64) return (M + 15) / 16 * 16;
+  if (M <= 128) return (M + 31) / 32 * 32;
+  return (M + 63) / 64 * 64;
+}
+int bucket_seqs(int n) { return n == 0 ? 0 : (n + 3) / 4 * 4; }
+int bucket_pow2(int n) {
+  int b = 1;
+  while (b < n) b <<= 1;
+  return b;
+}
+}  // namespace
 
 void Engine::run_step(const std::vector<StepItem>& items, std::vector<int32_t>& out,
                       float* logits_host) {
   const auto& m = cfg_.model;
-  const int n_seq_max = 2 * cfg_.max_slots + cfg_.max_verify + 1;
+  const int n_seq_max = 2 * (cfg_.max_slots + 4) + cfg_.max_verify + 4;
   int32_t* h_tok = static_cast<int32_t*>(h_desc_);
   RowDest* h_rows = reinterpret_cast<RowDest*>(h_tok + Mmax_);
   AttnSeq* h_seqs = reinterpret_cast<AttnSeq*>(h_rows + Mmax_);
@@ -589,38 +624,55 @@ void Engine::run_step(const std::vector<StepItem>& items, std::vector<int32_t>& 
   for (auto& a : drafts) { a.part0 = off; off += max_chunks_q_ + 1; }
   for (auto& a : dense1) { a.part0 = off; off += max_chunks_d_ * a.n_rows; }
   for (auto& a : densev) { a.part0 = off; off += max_chunks_d_ * a.n_rows; }
+  // Bucket the step shape (padding rows / empty sequences) so a handful of
+  // CUDA graphs cover every step; padding never changes a real row's math.
+  const int Mb = std::min(bucket_rows(M), Mmax_);
+  for (int i = M; i < Mb; ++i) {
+    h_tok[i] = 0;
+    h_rows[i] = RowDest{-1, 0, 0, 0};
+  }
+  const int nd = bucket_seqs(static_cast<int>(drafts.size()));
+  const int n1 = bucket_seqs(static_cast<int>(dense1.size()));
+  const int nv = static_cast<int>(densev.size());
+  const int mrv = nv ? bucket_pow2(max_rows_v) : 1;
   int k = 0;
-  for (auto& a : drafts) h_seqs[k++] = a;
-  for (auto& a : dense1) h_seqs[k++] = a;
+  const AttnSeq empty{};
+  for (int i = 0; i < nd; ++i) h_seqs[k++] = i < static_cast<int>(drafts.size()) ? drafts[i] : empty;
+  for (int i = 0; i < n1; ++i) h_seqs[k++] = i < static_cast<int>(dense1.size()) ? dense1[i] : empty;
   for (auto& a : densev) h_seqs[k++] = a;
-  VC_CK(cudaEventRecord(ev_a_, st_));
-  VC_CK(cudaMemcpyAsync(tok_in_, h_tok, M * sizeof(int32_t), cudaMemcpyHostToDevice, st_));
-  VC_CK(cudaMemcpyAsync(rows_dev_, h_rows, M * sizeof(RowDest), cudaMemcpyHostToDevice, st_));
-  VC_CK(cudaMemcpyAsync(seqs_dev_, h_seqs, k * sizeof(AttnSeq), cudaMemcpyHostToDevice, st_));
+  if (k > n_seq_max) throw ContractViolation("run_step: too many sequences");
 
-  const int nd = static_cast<int>(drafts.size()), n1 = static_cast<int>(dense1.size()),
-            nv = static_cast<int>(densev.size());
-  if (cfg_.use_graphs) {
-    std::ostringstream key;
-    key << M << ':' << nd << ':' << n1 << ':' << nv << ':' << max_rows_v;
-    auto itg = graphs_.find(key.str());
+  cudaGraphExec_t exec = nullptr;
+  std::string key;
+  if (cfg_.use_graphs) {  // capture (host work) before the timed device window opens
+    std::ostringstream ks;
+    ks << Mb << ':' << nd << ':' << n1 << ':' << nv << ':' << mrv;
+    key = ks.str();
+    auto itg = graphs_.find(key);
     if (itg == graphs_.end()) {
       cudaGraph_t g;
       const uint64_t before = launches_;
       VC_CK(cudaStreamBeginCapture(st_, cudaStreamCaptureModeThreadLocal));
-      enqueue_forward(M, nd, n1, nv, max_rows_v, logits_host != nullptr);
+      enqueue_forward(Mb, nd, n1, nv, mrv, logits_host != nullptr);
       VC_CK(cudaStreamEndCapture(st_, &g));
       cudaGraphExec_t ge;
       VC_CK(cudaGraphInstantiate(&ge, g, 0));
       cudaGraphDestroy(g);
-      launches_per_graph_[key.str()] = launches_ - before;
-      itg = graphs_.emplace(key.str(), ge).first;
+      launches_per_graph_[key] = launches_ - before;
+      itg = graphs_.emplace(key, ge).first;
       launches_ = before;
     }
-    VC_CK(cudaGraphLaunch(itg->second, st_));
-    launches_ += launches_per_graph_[key.str()];
+    exec = itg->second;
+  }
+  VC_CK(cudaEventRecord(ev_a_, st_));
+  VC_CK(cudaMemcpyAsync(tok_in_, h_tok, Mb * sizeof(int32_t), cudaMemcpyHostToDevice, st_));
+  VC_CK(cudaMemcpyAsync(rows_dev_, h_rows, Mb * sizeof(RowDest), cudaMemcpyHostToDevice, st_));
+  VC_CK(cudaMemcpyAsync(seqs_dev_, h_seqs, k * sizeof(AttnSeq), cudaMemcpyHostToDevice, st_));
+  if (exec) {
+    VC_CK(cudaGraphLaunch(exec, st_));
+    launches_ += launches_per_graph_[key];
   } else {
-    enqueue_forward(M, nd, n1, nv, max_rows_v, logits_host != nullptr);
+    enqueue_forward(Mb, nd, n1, nv, mrv, logits_host != nullptr);
   }
   VC_CK(cudaMemcpyAsync(h_out_, tok_out_, M * sizeof(int32_t), cudaMemcpyDeviceToHost, st_));
   if (logits_host)

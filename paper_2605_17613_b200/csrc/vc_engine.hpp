@@ -177,7 +177,8 @@ class Engine {
   // activations
   float* x_ = nullptr;
   uint16_t *xn_ = nullptr, *qkv_ = nullptr, *attn_ = nullptr, *act_ = nullptr;
-  float* ws_ = nullptr;
+  GemmWorkspace gws_{};
+  float* ss_part_ = nullptr;  // per-(row, 128-feature tile) sums of squares
   float* logits_ = nullptr;
   int32_t *tok_in_ = nullptr, *tok_out_ = nullptr;
   Partials part_{};
@@ -200,8 +201,6 @@ class Engine {
   cudaEvent_t ev_a_ = nullptr, ev_b_ = nullptr;
   double device_ms_ = 0.0;
   int64_t steps_ = 0;
-  int splits_qkv_ = 1, splits_o_ = 1, splits_gu_ = 1, splits_d_ = 1, splits_lm_ = 1;
-  size_t ws_floats_ = 0;
 };
 
 // Thrown on CUDA failures; vc_api maps it to VC_ERR_CUDA.

@@ -1,4 +1,5 @@
-// vc_gemm.h -- batch-invariant projection GEMM + fused epilogues + model glue.
+// vc_gemm.h -- batch-invariant projection GEMM with fused split-K fixup and
+// fused epilogues, plus the remaining model glue.
 #pragma once
 #include <cstdint>
 #include <cuda_runtime.h>
@@ -7,39 +8,57 @@
 
 namespace vc {
 
-// Split count for a weight shape; a function of (N, K) only (batch invariance).
-int gemm_splits(int N, int K);
-// ws[split][M][N] fp32 partial sums of X[M][K] . W[N][K]^T.
-cudaError_t gemm_partial(const uint16_t* X, int M, int K, const uint16_t* W, int N, int splits,
-                         float* ws, cudaStream_t st);
-
-// Where a row's freshly computed K/V go (kv_store).
+// Where a row's freshly computed K/V go (QKV epilogue).
 struct RowDest {
   int kind;  // 0: full pool, 2: staging pool (slot, pos); 1: draft tail (pos = tail index); -1: none
   int slot;
-  int pos;   // absolute position (also the RoPE position for kind 0); see rope_pos
-  int rope_pos;
+  int pos;       // position inside the destination (absolute, or tail index for kind 1)
+  int rope_pos;  // absolute position (RoPE)
 };
+
+enum class Epi : int {
+  StoreF32 = 0,  // out_f32[m][n] = y
+  Residual = 1,  // x[m][n] += y; ss_part[m][n/128] = sum over the tile of x^2
+  Qkv = 2,       // bf16(y) -> RoPE on q/k heads -> qkv[m][n]; K/V heads also scattered to the pools
+  Silu = 3,      // (g,u) interleaved columns -> act[m][n/2] = bf16(silu(g) * u)
+};
+
+struct GemmEpilogue {
+  Epi kind = Epi::StoreF32;
+  float* out_f32 = nullptr;
+  float* x = nullptr;
+  float* ss_part = nullptr;
+  uint16_t* out_bf16 = nullptr;
+  // Qkv
+  const RowDest* rows = nullptr;
+  const float* rope_cos = nullptr;
+  const float* rope_sin = nullptr;
+  int n_q = 0, n_kv = 0, d = 0, layer = 0, layers = 0;
+  KvPool full{}, stage{};
+  QuantPool draft{};
+};
+
+struct GemmWorkspace {
+  float* partial = nullptr;   // split partials, fragment order
+  int* counters = nullptr;    // one per output tile, self-resetting
+  size_t partial_floats = 0;
+  int n_counters = 0;
+};
+
+// Split count for a weight shape; a function of (N, K) only (batch invariance).
+int gemm_splits(int N, int K);
+size_t gemm_partial_floats(int M, int N, int K);
+int gemm_tiles(int M, int N);
+// y = X[M][K] . W[N][K]^T, then the epilogue.  N must be a multiple of 128.
+cudaError_t gemm(const uint16_t* X, int M, int K, const uint16_t* W, int N, int splits,
+                 const GemmEpilogue& epi, const GemmWorkspace& ws, cudaStream_t st);
 
 // x[m][H] fp32 = embed[tok[m]]; xn = bf16(rmsnorm(x) * w).
 cudaError_t embed_norm(const int32_t* tokens, int M, const uint16_t* embed, int H,
                        const uint16_t* norm_w, float eps, float* x, uint16_t* xn, cudaStream_t st);
-// qkv[m][:] = bf16(rope(bf16(sum_s ws[s][m][:]))) for q and k heads; v plain.
-cudaError_t qkv_epilogue(const float* ws, int splits, int M, int n_q, int n_kv, int d,
-                         const RowDest* rows, const float* rope_cos, const float* rope_sin,
-                         uint16_t* qkv, cudaStream_t st);
-// Scatter every row's K/V heads into the pools.
-cudaError_t kv_store(const uint16_t* qkv, int M, int n_q, int n_kv, int d, int layer, int layers,
-                     const RowDest* rows, KvPool full, KvPool stage, QuantPool draft,
-                     cudaStream_t st);
-// x += sum_s ws; xn = bf16(rmsnorm(x) * w)   (w == nullptr: no xn)
-cudaError_t residual_norm(const float* ws, int splits, int M, int H, float* x,
-                          const uint16_t* norm_w, float eps, uint16_t* xn, cudaStream_t st);
-// act[m][j] = bf16(silu(g) * u), (g,u) = interleaved columns (2j, 2j+1).
-cudaError_t silu_epilogue(const float* ws, int splits, int M, int F, uint16_t* act,
-                          cudaStream_t st);
-// logits[m][n] = sum_s ws
-cudaError_t sum_epilogue(const float* ws, int splits, int M, int N, float* out, cudaStream_t st);
+// xn = bf16(x * rsqrt(sum(ss_part[m][:]) / H + eps) * w)
+cudaError_t rms_apply(const float* x, const float* ss_part, int M, int H, const uint16_t* norm_w,
+                      float eps, uint16_t* xn, cudaStream_t st);
 // out[m] = argmax_n logits[m][n], ties -> smallest n.
 cudaError_t argmax_rows(const float* logits, int M, int N, int32_t* out, cudaStream_t st);
 // Synthetic bf16 init shared bit-for-bit with oracle/vc_oracle.c.

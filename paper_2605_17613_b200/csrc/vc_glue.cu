@@ -1,7 +1,7 @@
-// vc_glue.cu -- model glue around the projections: embedding + RMSNorm,
-// split-sum epilogues (RoPE, residual + RMSNorm, SiLU-gate), KV scatter into
-// the pools, greedy argmax, synthetic init.  All reductions run in a fixed
-// order so a row's result never depends on the other rows of the batch.
+// vc_glue.cu -- model glue outside the GEMM epilogues: embedding + RMSNorm,
+// the RMSNorm apply that follows a residual epilogue, greedy argmax, the
+// synthetic initialiser and the draft-tail refill.  All reductions run in a
+// fixed order so a row's result never depends on the other rows of the batch.
 #include "vc_common.cuh"
 #include "vc_gemm.h"
 
@@ -40,101 +40,24 @@ __global__ void embed_norm_kernel(const int32_t* tokens, const uint16_t* embed, 
     xn[static_cast<size_t>(m) * H + i] = f2bf(__fmul_rn(__fmul_rn(xr[i], r), bf2f(norm_w[i])));
 }
 
-__global__ void residual_norm_kernel(const float* ws, int splits, int M, int H, float* x,
-                                     const uint16_t* norm_w, float eps, uint16_t* xn) {
-  __shared__ float red[32];
+// grid (M, H / 1024): every CTA recomputes the row's r from the per-tile
+// partial sums (fixed order) and normalises its 1024-wide chunk.
+__global__ void rms_apply_kernel(const float* x, const float* ss_part, int H, const uint16_t* w,
+                                 float eps, uint16_t* xn) {
+  __shared__ float r_s;
   const int m = blockIdx.x;
-  float* xr = x + static_cast<size_t>(m) * H;
-  float ss = 0.f;
-  for (int i = threadIdx.x; i < H; i += blockDim.x) {
-    float acc = 0.f;
-    for (int s = 0; s < splits; ++s) acc += ws[(static_cast<size_t>(s) * M + m) * H + i];
-    const float v = xr[i] + acc;
-    xr[i] = v;
-    ss += v * v;
+  const int tiles = H / 128;
+  if (threadIdx.x == 0) {
+    const float* sp = ss_part + static_cast<size_t>(m) * tiles;
+    float s = 0.f;
+    for (int t = 0; t < tiles; ++t) s += sp[t];
+    r_s = rsqrtf(s / H + eps);
   }
-  if (norm_w == nullptr) return;
-  ss = block_sum(ss, red);
-  const float r = rsqrtf(ss / H + eps);
-  for (int i = threadIdx.x; i < H; i += blockDim.x)
-    xn[static_cast<size_t>(m) * H + i] = f2bf(__fmul_rn(__fmul_rn(xr[i], r), bf2f(norm_w[i])));
-}
-
-// one CTA per row; thread i handles rotation pairs of one head
-__global__ void qkv_epilogue_kernel(const float* ws, int splits, int M, int n_q, int n_kv, int d,
-                                    const RowDest* rows, const float* rope_cos,
-                                    const float* rope_sin, uint16_t* qkv) {
-  const int m = blockIdx.x;
-  const int N = (n_q + 2 * n_kv) * d;
-  const int half = d / 2;
-  const int pos = rows[m].rope_pos;
-  uint16_t* out = qkv + static_cast<size_t>(m) * N;
-  auto load = [&](int n) {
-    float acc = 0.f;
-    for (int s = 0; s < splits; ++s) acc += ws[(static_cast<size_t>(s) * M + m) * N + n];
-    return bf2f(f2bf(acc));  // projections round to bf16 before RoPE
-  };
-  const int n_rot = (n_q + n_kv) * half;  // rotation pairs in q and k heads
-  for (int i = threadIdx.x; i < n_rot; i += blockDim.x) {
-    const int head = i / half, j = i % half;
-    const int a = head * d + j, b = a + half;
-    const float x1 = load(a), x2 = load(b);
-    const float c = rope_cos[static_cast<size_t>(pos) * half + j];
-    const float s = rope_sin[static_cast<size_t>(pos) * half + j];
-    out[a] = f2bf(__fsub_rn(__fmul_rn(x1, c), __fmul_rn(x2, s)));
-    out[b] = f2bf(__fadd_rn(__fmul_rn(x2, c), __fmul_rn(x1, s)));
-  }
-  for (int n = (n_q + n_kv) * d + threadIdx.x; n < N; n += blockDim.x) out[n] = f2bf(load(n));
-}
-
-__global__ void kv_store_kernel(const uint16_t* qkv, int n_q, int n_kv, int d, int layer,
-                                int layers, const RowDest* rows, KvPool full, KvPool stage,
-                                QuantPool draft) {
-  const int m = blockIdx.x, h = blockIdx.y;
-  const RowDest rd = rows[m];
-  if (rd.kind < 0) return;
-  const int N = (n_q + 2 * n_kv) * d;
-  const uint16_t* k = qkv + static_cast<size_t>(m) * N + static_cast<size_t>(n_q + h) * d;
-  const uint16_t* v = qkv + static_cast<size_t>(m) * N + static_cast<size_t>(n_q + n_kv + h) * d;
-  const size_t slice = (static_cast<size_t>(rd.slot) * layers + layer) * n_kv + h;
-  uint16_t *dk, *dv;
-  if (rd.kind == 0 || rd.kind == 2) {
-    const KvPool& p = rd.kind == 0 ? full : stage;
-    dk = p.k + (slice * p.cap + rd.pos) * d;
-    dv = p.v + (slice * p.cap + rd.pos) * d;
-  } else {
-    dk = draft.ktail + (slice * draft.tail_cap + rd.pos) * d;
-    dv = draft.vtail + (slice * draft.tail_cap + rd.pos) * d;
-  }
-  for (int i = threadIdx.x; i < d / 8; i += blockDim.x) {
-    reinterpret_cast<uint4*>(dk)[i] = reinterpret_cast<const uint4*>(k)[i];
-    reinterpret_cast<uint4*>(dv)[i] = reinterpret_cast<const uint4*>(v)[i];
-  }
-}
-
-__global__ void silu_kernel(const float* ws, int splits, int M, int F, uint16_t* act) {
-  const size_t total = static_cast<size_t>(M) * F;
-  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
-    const size_t m = i / F, j = i % F;
-    float g = 0.f, u = 0.f;
-    for (int s = 0; s < splits; ++s) {
-      const float2 gu = *reinterpret_cast<const float2*>(ws + (static_cast<size_t>(s) * M + m) * 2 * F + 2 * j);
-      g += gu.x;
-      u += gu.y;
-    }
-    const float sg = __fdiv_rn(g, __fadd_rn(1.0f, expf(-g)));
-    act[i] = f2bf(__fmul_rn(sg, u));
-  }
-}
-
-__global__ void sum_kernel(const float* ws, int splits, size_t total, float* out) {
-  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
-       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
-    float acc = 0.f;
-    for (int s = 0; s < splits; ++s) acc += ws[static_cast<size_t>(s) * total + i];
-    out[i] = acc;
-  }
+  __syncthreads();
+  const float r = r_s;
+  const int base = blockIdx.y * 1024;
+  for (int i = base + threadIdx.x; i < min(H, base + 1024); i += blockDim.x)
+    xn[static_cast<size_t>(m) * H + i] = f2bf(__fmul_rn(__fmul_rn(x[static_cast<size_t>(m) * H + i], r), bf2f(w[i])));
 }
 
 __global__ void argmax_kernel(const float* logits, int N, int32_t* out) {
@@ -147,9 +70,8 @@ __global__ void argmax_kernel(const float* logits, int N, int32_t* out) {
     const float v = row[i];
     if (v > best) { best = v; bi = i; }  // ascending i per thread: first max kept
   }
-  // warp then block reduction; ties -> smaller index
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
+  for (int o = 16; o > 0; o >>= 1) {  // ties -> smaller index (specloop.cpp:260)
     const float ov = __shfl_xor_sync(0xffffffffu, best, o);
     const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
     if (ov > best || (ov == best && oi < bi)) { best = ov; bi = oi; }
@@ -219,41 +141,10 @@ cudaError_t embed_norm(const int32_t* tokens, int M, const uint16_t* embed, int 
   return cudaGetLastError();
 }
 
-cudaError_t qkv_epilogue(const float* ws, int splits, int M, int n_q, int n_kv, int d,
-                         const RowDest* rows, const float* rope_cos, const float* rope_sin,
-                         uint16_t* qkv, cudaStream_t st) {
+cudaError_t rms_apply(const float* x, const float* ss_part, int M, int H, const uint16_t* norm_w,
+                      float eps, uint16_t* xn, cudaStream_t st) {
   if (M <= 0) return cudaSuccess;
-  qkv_epilogue_kernel<<<M, 512, 0, st>>>(ws, splits, M, n_q, n_kv, d, rows, rope_cos, rope_sin, qkv);
-  return cudaGetLastError();
-}
-
-cudaError_t kv_store(const uint16_t* qkv, int M, int n_q, int n_kv, int d, int layer, int layers,
-                     const RowDest* rows, KvPool full, KvPool stage, QuantPool draft,
-                     cudaStream_t st) {
-  if (M <= 0) return cudaSuccess;
-  kv_store_kernel<<<dim3(M, n_kv), 32, 0, st>>>(qkv, n_q, n_kv, d, layer, layers, rows, full, stage, draft);
-  return cudaGetLastError();
-}
-
-cudaError_t residual_norm(const float* ws, int splits, int M, int H, float* x,
-                          const uint16_t* norm_w, float eps, uint16_t* xn, cudaStream_t st) {
-  if (M <= 0) return cudaSuccess;
-  residual_norm_kernel<<<M, kNormThreads, 0, st>>>(ws, splits, M, H, x, norm_w, eps, xn);
-  return cudaGetLastError();
-}
-
-cudaError_t silu_epilogue(const float* ws, int splits, int M, int F, uint16_t* act,
-                          cudaStream_t st) {
-  if (M <= 0) return cudaSuccess;
-  const size_t n = static_cast<size_t>(M) * F;
-  silu_kernel<<<grid_for(n, 256), 256, 0, st>>>(ws, splits, M, F, act);
-  return cudaGetLastError();
-}
-
-cudaError_t sum_epilogue(const float* ws, int splits, int M, int N, float* out, cudaStream_t st) {
-  if (M <= 0) return cudaSuccess;
-  const size_t n = static_cast<size_t>(M) * N;
-  sum_kernel<<<grid_for(n, 256), 256, 0, st>>>(ws, splits, n, out);
+  rms_apply_kernel<<<dim3(M, (H + 1023) / 1024), 256, 0, st>>>(x, ss_part, H, norm_w, eps, xn);
   return cudaGetLastError();
 }
 

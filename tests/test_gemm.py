@@ -1,0 +1,50 @@
+"""The stream-K projection GEMM: correct against an fp64 reference, and
+batch-invariant -- a row's result is bit-identical for any number of rows
+in the batch (the property the losslessness invariant rests on).
+Tolerance: bf16 inputs, fp32 accumulate: |y - y64| <= 1e-3 * sqrt(K) * rms(y64) + 1e-5."""
+import numpy as np
+import pytest
+
+import vc_testlib as T
+from paper_2605_17613_b200 import _lib
+
+pytestmark = pytest.mark.gpu
+
+
+def _gemm(torch, X, W):
+    lib = _lib.load()
+    M, K = X.shape
+    N = W.shape[0]
+    xd = torch.from_numpy(X.view(np.int16).copy()).cuda()
+    wd = torch.from_numpy(W.view(np.int16).copy()).cuda()
+    y = torch.zeros((M, N), dtype=torch.float32, device="cuda")
+    rc = lib.vc_gemm_probe(xd.data_ptr(), M, K, wd.data_ptr(), N, y.data_ptr(),
+                           torch.cuda.current_stream().cuda_stream)
+    assert rc == 0, lib.vc_last_error()
+    torch.cuda.synchronize()
+    return y.cpu().numpy()
+
+
+@pytest.mark.parametrize("M,N,K", [(16, 6144, 4096), (3, 4096, 14336), (80, 768, 512), (200, 1024, 1024),
+                                   (1, 128256 // 8 * 8 // 128 * 128, 4096)])
+def test_gemm_matches_fp64(cuda, M, N, K):
+    rng = np.random.default_rng(M + N + K)
+    X = T.f32_to_bf16(rng.standard_normal((M, K)).astype(np.float32))
+    W = T.f32_to_bf16((rng.standard_normal((N, K)) * 0.02).astype(np.float32))
+    y = _gemm(cuda, X, W)
+    ref = T.bf16_to_f32(X).astype(np.float64) @ T.bf16_to_f32(W).astype(np.float64).T
+    tol = 1e-3 * np.sqrt(K) * np.sqrt((ref ** 2).mean()) + 1e-5
+    assert np.abs(y - ref).max() <= tol
+
+
+def test_gemm_batch_invariance(cuda):
+    rng = np.random.default_rng(0)
+    K, N = 4096, 6144
+    X = T.f32_to_bf16(rng.standard_normal((200, K)).astype(np.float32))
+    W = T.f32_to_bf16((rng.standard_normal((N, K)) * 0.02).astype(np.float32))
+    full = _gemm(cuda, X, W)
+    for m in (1, 7, 16, 33, 80, 129):
+        sub = _gemm(cuda, X[:m].copy(), W)
+        np.testing.assert_array_equal(sub, full[:m])
+    # a row in the middle of a batch == the same row alone
+    np.testing.assert_array_equal(_gemm(cuda, X[150:151].copy(), W)[0], full[150])
