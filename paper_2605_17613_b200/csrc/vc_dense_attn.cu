@@ -24,6 +24,7 @@ namespace {
 constexpr int kChunk = VC_DENSE_CHUNK;
 constexpr int kTile = 32;
 constexpr int kStages = 3;
+constexpr int kMaxParts = 512;  // chunks per sequence the combine can merge (256K ctx)
 
 template <int D>
 VC_DEV int swz(int row, int chunk16) {  // 16-B chunk index within a row
@@ -253,26 +254,35 @@ __global__ void combine_kernel(AttnShape s, const AttnSeq* seqs, int max_chunks,
     return mode == 0 ? static_cast<size_t>(sq.part0 + c) * Hq + hq
                      : static_cast<size_t>(sq.part0 + c * sq.n_rows + tok) * Hq + hq;
   };
-  const bool has_tail = mode == 0 && sq.tail_len > 0;
-  float M = -INFINITY;
-  for (int c = 0; c < n_parts; ++c) M = fmaxf(M, part.ml[prow_of(c) * 2]);
-  if (has_tail) M = fmaxf(M, part.ml[prow_of(max_chunks) * 2]);
+  // the tail partial (draft mode) is merged last, after the chunks in order
+  const int n_all = n_parts + ((mode == 0 && sq.tail_len > 0) ? 1 : 0);
+  __shared__ float s_m[kMaxParts], s_f[kMaxParts];
+  __shared__ size_t s_row[kMaxParts];
+  __shared__ float s_M, s_l;
+  for (int c = threadIdx.x; c < n_all; c += blockDim.x) {
+    const size_t pr = prow_of(c < n_parts ? c : max_chunks);
+    s_row[c] = pr;
+    s_m[c] = part.ml[pr * 2];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float M = -INFINITY;
+    for (int c = 0; c < n_all; ++c) M = fmaxf(M, s_m[c]);
+    float l = 0.f;
+    for (int c = 0; c < n_all; ++c) {  // fixed order
+      const float f = (s_m[c] == -INFINITY) ? 0.f : exp2f(s_m[c] - M);
+      s_f[c] = f;
+      l += f * part.ml[s_row[c] * 2 + 1];
+    }
+    s_M = M;
+    s_l = l;
+  }
+  __syncthreads();
+  const float l = s_l;
   for (int c0 = threadIdx.x; c0 < D; c0 += blockDim.x) {
-    float o = 0.f, l = 0.f;
-    for (int c = 0; c < n_parts; ++c) {
-      const size_t pr = prow_of(c);
-      const float mc = part.ml[pr * 2];
-      const float f = (mc == -INFINITY) ? 0.f : exp2f(mc - M);
-      o += f * part.o[pr * D + c0];
-      l += f * part.ml[pr * 2 + 1];
-    }
-    if (has_tail) {
-      const size_t pr = prow_of(max_chunks);
-      const float mc = part.ml[pr * 2];
-      const float f = (mc == -INFINITY) ? 0.f : exp2f(mc - M);
-      o += f * part.o[pr * D + c0];
-      l += f * part.ml[pr * 2 + 1];
-    }
+    float o = 0.f;
+#pragma unroll 4
+    for (int c = 0; c < n_all; ++c) o += s_f[c] * part.o[s_row[c] * D + c0];
     out[static_cast<size_t>(sq.row0 + tok) * s.out_stride + static_cast<size_t>(hq) * D + c0] =
         f2bf(l > 0.f ? o / l : 0.f);
   }

@@ -46,7 +46,9 @@ struct Cfg {
 VC_DEV int swz8(int row, int c) { return c ^ (row & 7); }
 
 // CTA index owning global k-tile g under the split [q*T/P, (q+1)*T/P).
-__host__ __device__ inline long owner(long g, long T) { return ((g + 1) * kP - 1) / T; }
+// P = min(kP, T) so every CTA owns at least one k-tile (a function of N, K).
+__host__ __device__ inline long grid_of(long T) { return T < kP ? T : kP; }
+__host__ __device__ inline long owner(long g, long T) { return ((g + 1) * grid_of(T) - 1) / T; }
 
 template <int NT, Epi E>
 __device__ void epilogue(const float* sT, int m0, int M, int n0, int N, const GemmEpilogue& ep,
@@ -146,8 +148,9 @@ gemm_streamk_kernel(const uint16_t* __restrict__ X, int M, int K, const uint16_t
   const int tiles = N / kBN;
   const long T = static_cast<long>(tiles) * KT;
   const long p = blockIdx.x;
-  long beg = p * T / kP;
-  const long end = (p + 1) * T / kP;
+  const long P = grid_of(T);
+  long beg = p * T / P;
+  const long end = (p + 1) * T / P;
 
   while (beg < end) {
     const int tile = static_cast<int>(beg / KT);
@@ -280,7 +283,8 @@ cudaError_t launch_nt(const uint16_t* X, int M, int K, const uint16_t* W, int N,
   const int mc = max_contributors(N, K);
   for (int m0 = 0, blk = 0; m0 < M; m0 += NT, ++blk) {
     // one launch per 128-row block keeps the schedule independent of M
-    kern<<<dim3(kP, 1), kThreads, smem, st>>>(X, M, K, W, N, m0, ep, ws, mc);
+    const long T = static_cast<long>(N / kBN) * (K / kBK);
+    kern<<<dim3(static_cast<unsigned>(grid_of(T)), 1), kThreads, smem, st>>>(X, M, K, W, N, m0, ep, ws, mc);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
   }

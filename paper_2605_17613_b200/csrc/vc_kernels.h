@@ -7,7 +7,7 @@
 
 #define VC_QGROUP 128      // tokens per quantised K group (KIVI G)
 #define VC_DRAFT_CG 8      // quantised groups per draft-attention chunk (1024 tokens)
-#define VC_DENSE_CHUNK 256 // keys per dense-attention chunk (absolute positions)
+#define VC_DENSE_CHUNK 512 // keys per dense-attention chunk (absolute positions)
 
 namespace vc {
 
