@@ -1,16 +1,20 @@
 // vc_draft_attn.cu -- draft decode attention over the KIVI-compressed cache.
 //
 // One query token per drafting sequence, n_rep query heads per kv head (GQA).
-// HBM-bound: every code byte is read exactly once, straight into registers
-// with 128-bit streaming loads (no shared-memory round trip), and consumed by
-// legacy mma.sync tensor-core tiles:
+// HBM-bound: every code byte is read exactly once.  Each warp runs its own
+// two-stage TMA pipeline: one lane issues 1-D bulk copies
+// (cp.async.bulk ... mbarrier::complete_tx) of the next 64-token unit --
+// K codes, V codes, V scale/zero, and per group the K scale/zero -- into
+// shared memory while the warp computes on the previous unit, so the memory
+// system sees ~9 KB in flight per warp without holding registers for it.
+// The math runs on legacy mma.sync tensor-core tiles fed from LDS:
 //   S^T[tok, head] = Kcodes[tok, ch] . q'^T[ch, head],  q' = q * kscale (per group)
 //   O^T[ch, head]  = Vcodes^T[ch, tok] . P'^T[tok, head], P' = P * vscale (per token)
 // Dequantisation is folded algebraically into q' / P' and two per-head
 // constants (zero points, and the 1024 bias of the lop3 int->fp16 trick), so
-// the inner loop is lop3 + mma only.  Codes arrive in mma A-fragment order
-// (written by vc_quant.cu), the P' B-fragments come from the S C-fragments
-// through movmatrix.trans, and the online softmax runs on warp shuffles.
+// the inner loop is lop3 + mma only.  Codes are stored in mma A-fragment
+// order (vc_quant.cu), the P' B-fragments come from the S C-fragments through
+// movmatrix.trans, and the online softmax runs on warp shuffles.
 // Split-K over 1024-token chunks + one bf16-tail CTA; attention_combine
 // merges the partials (LSE) in chunk order.
 //
@@ -25,6 +29,21 @@ namespace {
 constexpr int kG = VC_QGROUP;
 constexpr int kCG = VC_DRAFT_CG;
 constexpr int kWarps = 4;
+constexpr int kUnit = 64;  // tokens per pipeline unit (half a K group)
+
+template <int D, int BITS>
+struct Geo {
+  static constexpr int KS = D / 16;                    // channel k-steps / tiles
+  static constexpr int W = (BITS == 4) ? KS : KS / 2;  // u32 per lane per 16-token tile
+  static constexpr int CH = W < 4 ? W : 4;
+  static constexpr int UMT = kUnit / 16;               // 16-token tiles per unit
+  static constexpr int UW = UMT * W * 32;              // u32 of K (or V) codes per unit
+  // stage layout (u32): [K codes UW][V codes UW][vsz kUnit][ksz D]
+  static constexpr int OFF_V = UW;
+  static constexpr int OFF_VSZ = 2 * UW;
+  static constexpr int OFF_KSZ = 2 * UW + kUnit;
+  static constexpr int STAGE = 2 * UW + kUnit + D;     // u32
+};
 
 template <int D, int NREP>
 VC_DEV void write_partial(const AttnShape& s, const AttnSeq& sq, int h, int chunk, float* sm_m,
@@ -60,18 +79,16 @@ __global__ void __launch_bounds__(128) draft_attn_quant_kernel(AttnShape s, Quan
                                                                const AttnSeq* seqs, int max_chunks,
                                                                Partials part) {
   static_assert(NREP <= 8, "n_rep > 8 needs two head tiles");
-  constexpr int KS = D / 16;                    // channel k-steps / tiles
-  constexpr int W = (BITS == 4) ? KS : KS / 2;  // u32 per lane per 16-token tile
-  constexpr int CH = W < 4 ? W : 4;
-  constexpr int MT = kG / 16;                   // 16-token tiles per group
+  using GEO = Geo<D, BITS>;
+  constexpr int KS = GEO::KS, W = GEO::W, CH = GEO::CH, UMT = GEO::UMT;
   constexpr size_t GW = static_cast<size_t>(kG) * D * BITS / 32;  // u32 per group
   constexpr uint32_t MASK = BITS == 4 ? 0x000f000fu : 0x00030003u;
 
-  __shared__ float sq_q[8 * D];                         // scaled q, head-major
-  __shared__ __align__(16) uint32_t s_ksz[kWarps][D];
-  __shared__ __align__(16) uint32_t s_vsz[kWarps][kG];
+  extern __shared__ __align__(128) uint32_t dsm[];   // [kWarps][2][STAGE]
+  __shared__ float sq_q[NREP * D];                   // scaled q, head-major
+  __shared__ __align__(8) uint64_t bars[kWarps][2];
   __shared__ float sm_m[kWarps * 8], sm_l[kWarps * 8];
-  __shared__ float sm_o[kWarps * 8 * D];
+  float* sm_o = reinterpret_cast<float*>(dsm);       // reused after the pipeline drains
 
   const AttnSeq sq = seqs[blockIdx.z];
   const int h = blockIdx.y;
@@ -85,11 +102,10 @@ __global__ void __launch_bounds__(128) draft_attn_quant_kernel(AttnShape s, Quan
 
   // q heads h*NREP .. h*NREP+NREP-1 are contiguous in the qkv row.
   const uint16_t* qrow = qkv + static_cast<size_t>(sq.row0) * s.q_stride + static_cast<size_t>(h) * NREP * D;
-  for (int i = threadIdx.x; i < 8 * D; i += blockDim.x)
-    sq_q[i] = (i < NREP * D) ? bf2f(qrow[i]) * s.scale_log2 : 0.f;
-  __syncthreads();
+  for (int i = threadIdx.x; i < NREP * D; i += blockDim.x) sq_q[i] = bf2f(qrow[i]) * s.scale_log2;
 
   if (tail) {
+    __syncthreads();
     // ---- bf16 tail (residual group + draft window), CUDA cores ----------
     constexpr int CPL = D / 32;  // channels per lane
     const uint16_t* kt = pool.ktail + slice * pool.tail_cap * D;
@@ -124,9 +140,9 @@ __global__ void __launch_bounds__(128) draft_attn_quant_kernel(AttnShape s, Quan
         m[n] = mn;
       }
     }
+    if (lane == 0) {
 #pragma unroll
-    for (int n = 0; n < 8; ++n) {
-      if (lane == 0) {
+      for (int n = 0; n < 8; ++n) {
         sm_m[warp * 8 + n] = n < NREP ? m[n < NREP ? n : 0] : -INFINITY;
         sm_l[warp * 8 + n] = n < NREP ? l[n < NREP ? n : 0] : 0.f;
       }
@@ -140,11 +156,42 @@ __global__ void __launch_bounds__(128) draft_attn_quant_kernel(AttnShape s, Quan
     return;
   }
 
-  // ---- quantised groups ------------------------------------------------------
+  // ---- quantised groups: per-warp TMA pipeline over 64-token units ----------
   const uint32_t* kc = pool.kc + slice * (static_cast<size_t>(pool.cap) * D * BITS / 32);
   const uint32_t* vc = pool.vc + slice * (static_cast<size_t>(pool.cap) * D * BITS / 32);
   const uint32_t* ksz = pool.ksz + slice * (static_cast<size_t>(pool.cap / kG) * D);
   const uint32_t* vsz = pool.vsz + slice * static_cast<size_t>(pool.cap);
+  uint32_t* stage0 = dsm + static_cast<size_t>(warp) * 2 * GEO::STAGE;
+  uint64_t* bar = bars[warp];
+
+  // this warp's groups: chunk*kCG + warp, + kWarps, ... ; two units each
+  const int g_first = chunk * kCG + warp;
+  const int g_end = min((chunk + 1) * kCG, sq.n_groups);
+  const int n_mine = g_first < g_end ? (g_end - g_first + kWarps - 1) / kWarps : 0;
+  const int n_units = 2 * n_mine;
+
+  auto issue = [&](int u, int st) {  // lane 0 only
+    const int g = g_first + (u >> 1) * kWarps;
+    const int half = u & 1;
+    uint32_t* dst = stage0 + st * GEO::STAGE;
+    const uint32_t bytes_codes = GEO::UW * 4;
+    const uint32_t bytes = 2 * bytes_codes + kUnit * 4 + (half == 0 ? D * 4 : 0);
+    mbar_expect_tx(bar + st, bytes);
+    tma_load_1d(dst, kc + static_cast<size_t>(g) * GW + half * GEO::UW, bytes_codes, bar + st);
+    tma_load_1d(dst + GEO::OFF_V, vc + static_cast<size_t>(g) * GW + half * GEO::UW, bytes_codes, bar + st);
+    tma_load_1d(dst + GEO::OFF_VSZ, vsz + static_cast<size_t>(g) * kG + half * kUnit, kUnit * 4, bar + st);
+    if (half == 0) tma_load_1d(dst + GEO::OFF_KSZ, ksz + static_cast<size_t>(g) * D, D * 4, bar + st);
+  };
+  if (lane == 0) {
+    mbar_init(bar + 0, 1);
+    mbar_init(bar + 1, 1);
+    fence_mbar_init();
+  }
+  __syncthreads();  // sq_q and barrier init visible
+  if (lane == 0) {
+    if (n_units > 0) issue(0, 0);
+    if (n_units > 1) issue(1, 1);
+  }
 
   const int hn = lane >> 2;         // head column this lane feeds in B fragments
   const int hc0 = 2 * (lane & 3);   // head columns this lane holds in C fragments
@@ -153,98 +200,74 @@ __global__ void __launch_bounds__(128) draft_attn_quant_kernel(AttnShape s, Quan
   float oacc[KS][4];
 #pragma unroll
   for (int ct = 0; ct < KS; ++ct) oacc[ct][0] = oacc[ct][1] = oacc[ct][2] = oacc[ct][3] = 0.f;
+  uint32_t b0[KS], b1[KS];
+  float bias0 = 0.f, bias1 = 0.f;
 
-  const int g_end = min((chunk + 1) * kCG, sq.n_groups);
-  for (int g = chunk * kCG + warp; g < g_end; g += kWarps) {
-    // stage this group's scale/zero pairs (per channel for K, per token for V)
-    for (int i = lane * 4; i < D; i += 128)
-      *reinterpret_cast<uint4*>(&s_ksz[warp][i]) = *reinterpret_cast<const uint4*>(ksz + static_cast<size_t>(g) * D + i);
-    for (int i = lane * 4; i < kG; i += 128)
-      *reinterpret_cast<uint4*>(&s_vsz[warp][i]) = *reinterpret_cast<const uint4*>(vsz + static_cast<size_t>(g) * kG + i);
-
-    // K codes for the whole group: MT tiles x W words per lane
-    uint32_t kw[MT][W];
-    const uint32_t* kg = kc + static_cast<size_t>(g) * GW;
+  for (int u = 0; u < n_units; ++u) {
+    const int st = u & 1;
+    mbar_wait(bar + st, (u >> 1) & 1);
+    const uint32_t* sb = stage0 + st * GEO::STAGE;
+    if ((u & 1) == 0) {
+      // new group: q' = q * kscale as fp16 B fragments; per-head constant term
+      float bias_part = 0.f;
 #pragma unroll
-    for (int m = 0; m < MT; ++m)
+      for (int k = 0; k < KS; ++k) {
+        const int c0 = k * 16 + 2 * (lane & 3);
+        const int cs[4] = {c0, c0 + 1, c0 + 8, c0 + 9};
+        float qp[4];
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const uint32_t sz = sb[GEO::OFF_KSZ + cs[e]];
+          const float sc = h2f(static_cast<uint16_t>(sz & 0xffffu));
+          const float zr = h2f(static_cast<uint16_t>(sz >> 16));
+          const float q = hn < NREP ? sq_q[hn * D + cs[e]] : 0.f;  // padding head columns
+          qp[e] = q * sc;
+          // zero point and the -1024 fold use the fp16-rounded q' the MMA sees
+          bias_part += q * zr - 1024.f * h2f(f2h(qp[e]));
+        }
+        b0[k] = pack_h2(qp[0], qp[1]);
+        b1[k] = pack_h2(qp[2], qp[3]);
+      }
+      bias_part += __shfl_xor_sync(0xffffffffu, bias_part, 1);
+      bias_part += __shfl_xor_sync(0xffffffffu, bias_part, 2);
+      bias0 = __shfl_sync(0xffffffffu, bias_part, hc0 * 4);
+      bias1 = __shfl_sync(0xffffffffu, bias_part, (hc0 + 1) * 4);
+    }
+
+    // S^T tiles of the unit's 64 tokens
+    float sacc[UMT][4];
+#pragma unroll
+    for (int m = 0; m < UMT; ++m) {
+      uint32_t kw[W];
 #pragma unroll
       for (int wq = 0; wq < W / CH; ++wq) {
-        const uint32_t* p = kg + (static_cast<size_t>(m * (W / CH) + wq) * 32 + lane) * CH;
+        const uint32_t* p = sb + (static_cast<size_t>(m * (W / CH) + wq) * 32 + lane) * CH;
         if constexpr (CH == 4) {
-          uint4 v = ldg_stream(p);
-          kw[m][wq * 4 + 0] = v.x; kw[m][wq * 4 + 1] = v.y; kw[m][wq * 4 + 2] = v.z; kw[m][wq * 4 + 3] = v.w;
+          const uint4 v = lds128(p);
+          kw[wq * 4 + 0] = v.x; kw[wq * 4 + 1] = v.y; kw[wq * 4 + 2] = v.z; kw[wq * 4 + 3] = v.w;
         } else {
-          uint2 v = ldg_stream64(p);
-          kw[m][wq * 2 + 0] = v.x; kw[m][wq * 2 + 1] = v.y;
+          const uint2 v = lds64(p);
+          kw[wq * 2 + 0] = v.x; kw[wq * 2 + 1] = v.y;
         }
       }
-    __syncwarp();
-
-    // q' = q * kscale as fp16 B fragments; per-head constant term
-    uint32_t b0[KS], b1[KS];
-    float bias_part = 0.f;
-#pragma unroll
-    for (int st = 0; st < KS; ++st) {
-      const int c0 = st * 16 + 2 * (lane & 3);
-      const int cs[4] = {c0, c0 + 1, c0 + 8, c0 + 9};
-      float qp[4];
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const uint32_t sz = s_ksz[warp][cs[e]];
-        const float sc = h2f(static_cast<uint16_t>(sz & 0xffffu));
-        const float zr = h2f(static_cast<uint16_t>(sz >> 16));
-        const float q = sq_q[hn * D + cs[e]];
-        qp[e] = q * sc;
-        // zero point and the -1024 fold use the fp16-rounded q' the MMA sees
-        bias_part += q * zr - 1024.f * h2f(f2h(qp[e]));
-      }
-      b0[st] = pack_h2(qp[0], qp[1]);
-      b1[st] = pack_h2(qp[2], qp[3]);
-    }
-    bias_part += __shfl_xor_sync(0xffffffffu, bias_part, 1);
-    bias_part += __shfl_xor_sync(0xffffffffu, bias_part, 2);
-    const float bias0 = __shfl_sync(0xffffffffu, bias_part, hc0 * 4);
-    const float bias1 = __shfl_sync(0xffffffffu, bias_part, (hc0 + 1) * 4);
-
-    // S^T tiles
-    float sacc[MT][4];
-#pragma unroll
-    for (int m = 0; m < MT; ++m) {
       sacc[m][0] = sacc[m][1] = sacc[m][2] = sacc[m][3] = 0.f;
 #pragma unroll
-      for (int st = 0; st < KS; ++st) {
-        const uint32_t w = (BITS == 4) ? kw[m][st] : kw[m][st >> 1];
-        const int sh = (BITS == 4) ? 0 : 8 * (st & 1);
+      for (int k = 0; k < KS; ++k) {
+        const uint32_t w = (BITS == 4) ? kw[k] : kw[k >> 1];
+        const int sh = (BITS == 4) ? 0 : 8 * (k & 1);
         const uint32_t a0 = nib_to_h2(w >> (sh + 0 * BITS), MASK);
         const uint32_t a1 = nib_to_h2(w >> (sh + 1 * BITS), MASK);
         const uint32_t a2 = nib_to_h2(w >> (sh + 2 * BITS), MASK);
         const uint32_t a3 = nib_to_h2(w >> (sh + 3 * BITS), MASK);
-        mma_f16(sacc[m], a0, a1, a2, a3, b0[st], b1[st]);
+        mma_f16(sacc[m], a0, a1, a2, a3, b0[k], b1[k]);
       }
       sacc[m][0] += bias0; sacc[m][1] += bias1; sacc[m][2] += bias0; sacc[m][3] += bias1;
     }
 
-    // V codes (issued before the softmax math so the loads overlap it)
-    uint32_t vw[MT][W];
-    const uint32_t* vg = vc + static_cast<size_t>(g) * GW;
-#pragma unroll
-    for (int m = 0; m < MT; ++m)
-#pragma unroll
-      for (int wq = 0; wq < W / CH; ++wq) {
-        const uint32_t* p = vg + (static_cast<size_t>(m * (W / CH) + wq) * 32 + lane) * CH;
-        if constexpr (CH == 4) {
-          uint4 v = ldg_stream(p);
-          vw[m][wq * 4 + 0] = v.x; vw[m][wq * 4 + 1] = v.y; vw[m][wq * 4 + 2] = v.z; vw[m][wq * 4 + 3] = v.w;
-        } else {
-          uint2 v = ldg_stream64(p);
-          vw[m][wq * 2 + 0] = v.x; vw[m][wq * 2 + 1] = v.y;
-        }
-      }
-
     // online softmax (columns hc0, hc0+1; rows spread over lane>>2 and +8)
     float gm0 = -INFINITY, gm1 = -INFINITY;
 #pragma unroll
-    for (int m = 0; m < MT; ++m) {
+    for (int m = 0; m < UMT; ++m) {
       gm0 = fmaxf(gm0, fmaxf(sacc[m][0], sacc[m][2]));
       gm1 = fmaxf(gm1, fmaxf(sacc[m][1], sacc[m][3]));
     }
@@ -262,11 +285,11 @@ __global__ void __launch_bounds__(128) draft_attn_quant_kernel(AttnShape s, Quan
     for (int ct = 0; ct < KS; ++ct) {
       oacc[ct][0] *= al0; oacc[ct][1] *= al1; oacc[ct][2] *= al0; oacc[ct][3] *= al1;
     }
-    uint32_t bp0[MT], bp1[MT];
+    uint32_t bp0[UMT], bp1[UMT];
 #pragma unroll
-    for (int m = 0; m < MT; ++m) {
+    for (int m = 0; m < UMT; ++m) {
       const int r = m * 16 + (lane >> 2);
-      const uint32_t sz_a = s_vsz[warp][r], sz_b = s_vsz[warp][r + 8];
+      const uint32_t sz_a = sb[GEO::OFF_VSZ + r], sz_b = sb[GEO::OFF_VSZ + r + 8];
       const float vs_a = h2f(static_cast<uint16_t>(sz_a & 0xffffu)), vz_a = h2f(static_cast<uint16_t>(sz_a >> 16));
       const float vs_b = h2f(static_cast<uint16_t>(sz_b & 0xffffu)), vz_b = h2f(static_cast<uint16_t>(sz_b >> 16));
       const float p0 = exp2f(sacc[m][0] - mn0), p1 = exp2f(sacc[m][1] - mn1);
@@ -285,10 +308,22 @@ __global__ void __launch_bounds__(128) draft_attn_quant_kernel(AttnShape s, Quan
 
     // O^T += Vcodes^T . P'^T
 #pragma unroll
-    for (int m = 0; m < MT; ++m)
+    for (int m = 0; m < UMT; ++m) {
+      uint32_t vw[W];
+#pragma unroll
+      for (int wq = 0; wq < W / CH; ++wq) {
+        const uint32_t* p = sb + GEO::OFF_V + (static_cast<size_t>(m * (W / CH) + wq) * 32 + lane) * CH;
+        if constexpr (CH == 4) {
+          const uint4 v = lds128(p);
+          vw[wq * 4 + 0] = v.x; vw[wq * 4 + 1] = v.y; vw[wq * 4 + 2] = v.z; vw[wq * 4 + 3] = v.w;
+        } else {
+          const uint2 v = lds64(p);
+          vw[wq * 2 + 0] = v.x; vw[wq * 2 + 1] = v.y;
+        }
+      }
 #pragma unroll
       for (int ct = 0; ct < KS; ++ct) {
-        const uint32_t w = (BITS == 4) ? vw[m][ct] : vw[m][ct >> 1];
+        const uint32_t w = (BITS == 4) ? vw[ct] : vw[ct >> 1];
         const int sh = (BITS == 4) ? 0 : 8 * (ct & 1);
         const uint32_t a0 = nib_to_h2(w >> (sh + 0 * BITS), MASK);
         const uint32_t a1 = nib_to_h2(w >> (sh + 1 * BITS), MASK);
@@ -296,7 +331,9 @@ __global__ void __launch_bounds__(128) draft_attn_quant_kernel(AttnShape s, Quan
         const uint32_t a3 = nib_to_h2(w >> (sh + 3 * BITS), MASK);
         mma_f16(oacc[ct], a0, a1, a2, a3, bp0[m], bp1[m]);
       }
-    __syncwarp();
+    }
+    __syncwarp();  // every lane has consumed the stage (all LDS results used)
+    if (lane == 0 && u + 2 < n_units) issue(u + 2, st);
   }
 
   // reduce the per-lane sums over the 8 lanes sharing a head column
@@ -307,6 +344,7 @@ __global__ void __launch_bounds__(128) draft_attn_quant_kernel(AttnShape s, Quan
     corr0 += __shfl_xor_sync(0xffffffffu, corr0, o);
     corr1 += __shfl_xor_sync(0xffffffffu, corr1, o);
   }
+  __syncthreads();  // all warps done with their stages before sm_o reuses them
   if (lane < 4) {
     sm_m[warp * 8 + hc0] = mrun0;
     sm_m[warp * 8 + hc0 + 1] = mrun1;
@@ -329,8 +367,15 @@ template <int D, int BITS, int NREP>
 cudaError_t launch_draft(const AttnShape& s, const QuantPool& pool, int layer, const uint16_t* qkv,
                          const AttnSeq* seqs, int n_seq, int max_chunks, Partials part,
                          cudaStream_t st) {
+  using GEO = Geo<D, BITS>;
+  size_t smem = static_cast<size_t>(kWarps) * 2 * GEO::STAGE * 4;
+  const size_t need_o = static_cast<size_t>(kWarps) * 8 * D * 4;  // sm_o reuse
+  if (smem < need_o) smem = need_o;
+  auto kern = draft_attn_quant_kernel<D, BITS, NREP>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
   dim3 grid(max_chunks + 1, s.n_kv, n_seq);
-  draft_attn_quant_kernel<D, BITS, NREP><<<grid, 128, 0, st>>>(s, pool, layer, qkv, seqs, max_chunks, part);
+  kern<<<grid, kWarps * 32, smem, st>>>(s, pool, layer, qkv, seqs, max_chunks, part);
   return cudaGetLastError();
 }
 
