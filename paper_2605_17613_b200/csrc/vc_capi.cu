@@ -530,9 +530,19 @@ int vc_gemm_probe(const uint16_t* X, int M, int K, const uint16_t* W, int N, flo
     vc::GemmEpilogue ep;
     ep.kind = vc::Epi::StoreF32;
     ep.out_f32 = Y;
-    vc::check_cuda(vc::gemm(X, M, K, W, N, 1, ep, ws, st), "gemm");
+    // logical inputs -> the tiled HBM layouts the GEMM streams
+    uint16_t *xt = nullptr, *wt = nullptr;
+    const size_t xe = static_cast<size_t>(M + 128) * K, we = static_cast<size_t>(N) * K;
+    vc::check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&xt), xe * 2, st), "malloc");
+    vc::check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&wt), we * 2, st), "malloc");
+    vc::check_cuda(cudaMemsetAsync(xt, 0, xe * 2, st), "memset");
+    vc::check_cuda(vc::retile_act(X, M, K, M, xt, st), "retile_act");
+    vc::check_cuda(vc::retile_weight(W, N, K, wt, st), "retile_weight");
+    vc::check_cuda(vc::gemm(xt, M, M, K, wt, N, ep, ws, st), "gemm");
     vc::check_cuda(cudaFreeAsync(ws.partial, st), "free");
     vc::check_cuda(cudaFreeAsync(ws.counters, st), "free");
+    vc::check_cuda(cudaFreeAsync(xt, st), "free");
+    vc::check_cuda(cudaFreeAsync(wt, st), "free");
     vc::check_cuda(cudaStreamSynchronize(st), "sync");
   });
 }

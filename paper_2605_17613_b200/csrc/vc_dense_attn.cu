@@ -17,6 +17,7 @@
 // scheduler.cpp:366); verify returns x+1 predictions (specloop.cpp:24-35).
 #include "vc_common.cuh"
 #include "vc_kernels.h"
+#include "vc_tiled.cuh"
 
 namespace vc {
 namespace {
@@ -283,8 +284,11 @@ __global__ void combine_kernel(AttnShape s, const AttnSeq* seqs, int max_chunks,
     float o = 0.f;
 #pragma unroll 4
     for (int c = 0; c < n_all; ++c) o += s_f[c] * part.o[s_row[c] * D + c0];
-    out[static_cast<size_t>(sq.row0 + tok) * s.out_stride + static_cast<size_t>(hq) * D + c0] =
-        f2bf(l > 0.f ? o / l : 0.f);
+    const uint16_t v = f2bf(l > 0.f ? o / l : 0.f);
+    if (s.out_mp > 0)
+      out[atile_idx(sq.row0 + tok, hq * D + c0, s.out_mp)] = v;
+    else
+      out[static_cast<size_t>(sq.row0 + tok) * s.out_stride + static_cast<size_t>(hq) * D + c0] = v;
   }
 }
 

@@ -119,6 +119,7 @@ void Engine::attention_probe(int slot, int layer, int mode, const uint16_t* q_de
   as.d = m.d;
   as.q_stride = m.n_q * m.d;
   as.out_stride = m.n_q * m.d;
+  as.out_mp = 0;
   as.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(m.d)));
   AttnSeq a{};
   a.slot = cfg_.full_tier == 1 && mode != 1 ? 0 : slot;
@@ -239,10 +240,11 @@ void Engine::alloc_all() {
   // ---- activations ---------------------------------------------------------
   Mmax_ = static_cast<int>(round_up(cfg_.max_slots + cfg_.max_verify * (cfg_.max_x + 1), 64));
   x_ = dmalloc<float>(static_cast<size_t>(Mmax_) * H);
-  xn_ = dmalloc<uint16_t>(static_cast<size_t>(Mmax_) * (H > F ? H : F));
+  // tiled GEMM inputs carry 128 rows of slack (the last NT block may overrun Mp)
+  xn_ = dmalloc<uint16_t>(static_cast<size_t>(Mmax_ + 128) * (H > F ? H : F));
   qkv_ = dmalloc<uint16_t>(static_cast<size_t>(Mmax_) * qkv_n);
-  attn_ = dmalloc<uint16_t>(static_cast<size_t>(Mmax_) * m.n_q * d);
-  act_ = dmalloc<uint16_t>(static_cast<size_t>(Mmax_) * F);
+  attn_ = dmalloc<uint16_t>(static_cast<size_t>(Mmax_ + 128) * m.n_q * d);
+  act_ = dmalloc<uint16_t>(static_cast<size_t>(Mmax_ + 128) * F);
   {
     size_t pf = 0;
     for (int mm : {16, 32, 64, 128}) {
@@ -314,23 +316,33 @@ void Engine::load_weights(const uint16_t* embed, const uint16_t* const* attn_nor
   auto up = [&](uint16_t* dst, const uint16_t* src, size_t n) {
     VC_CK(cudaMemcpy(dst, src, n * 2, cudaMemcpyHostToDevice));
   };
+  // GEMM weights: logical [N][K] -> staging -> tiled layout (vc_tiled.cuh)
+  const size_t max_elems = std::max(std::max(static_cast<size_t>(V) * H, static_cast<size_t>(2) * F * H),
+                                    std::max(static_cast<size_t>(qkv_n) * H, static_cast<size_t>(H) * F));
+  uint16_t* tmp = dmalloc<uint16_t>(max_elems);
+  auto up_tiled = [&](uint16_t* dst, const uint16_t* src, int N, int K) {
+    up(tmp, src, static_cast<size_t>(N) * K);
+    VC_LAUNCH(retile_weight(tmp, N, K, dst, st_));
+    VC_CK(cudaStreamSynchronize(st_));
+  };
   up(w_.embed, embed, static_cast<size_t>(V) * H);
   std::vector<uint16_t> gu(static_cast<size_t>(2) * F * H);
   for (int l = 0; l < L; ++l) {
     up(w_.attn_norm[l], attn_norm[l], H);
-    up(w_.wqkv[l], wqkv[l], static_cast<size_t>(qkv_n) * H);
-    up(w_.wo[l], wo[l], static_cast<size_t>(H) * m.n_q * d);
+    up_tiled(w_.wqkv[l], wqkv[l], qkv_n, H);
+    up_tiled(w_.wo[l], wo[l], H, m.n_q * d);
     up(w_.mlp_norm[l], mlp_norm[l], H);
     // interleave gate/up rows: row 2j = gate_j, row 2j+1 = up_j
     for (int j = 0; j < F; ++j) {
       std::memcpy(&gu[static_cast<size_t>(2 * j) * H], wgate[l] + static_cast<size_t>(j) * H, H * 2);
       std::memcpy(&gu[static_cast<size_t>(2 * j + 1) * H], wup[l] + static_cast<size_t>(j) * H, H * 2);
     }
-    up(w_.wgu[l], gu.data(), gu.size());
-    up(w_.wd[l], wdown[l], static_cast<size_t>(H) * F);
+    up_tiled(w_.wgu[l], gu.data(), 2 * F, H);
+    up_tiled(w_.wd[l], wdown[l], H, F);
   }
   up(w_.final_norm, final_norm, H);
-  up(w_.lm_head, lm_head, static_cast<size_t>(V) * H);
+  up_tiled(w_.lm_head, lm_head, V, H);
+  cudaFree(tmp);
 }
 
 // --------------------------------------------------------------- requests
@@ -502,6 +514,7 @@ void Engine::enqueue_forward(int M, int n_draft, int n_dense1, int n_densev, int
   as.d = d;
   as.q_stride = qkv_n;
   as.out_stride = m.n_q * d;
+  as.out_mp = M;  // attention output feeds o_proj in the tiled layout
   as.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(d)));
   const KvPool dense_v_pool = cfg_.full_tier == 0 ? full_ : stage_;
   GemmEpilogue eq;
@@ -527,10 +540,10 @@ void Engine::enqueue_forward(int M, int n_draft, int n_dense1, int n_densev, int
   GemmEpilogue ef;
   ef.kind = Epi::StoreF32;
   ef.out_f32 = logits_;
-  VC_LAUNCH(embed_norm(tok_in_, M, w_.embed, H, w_.attn_norm[0], m.eps, x_, xn_, st_));
+  VC_LAUNCH(embed_norm(tok_in_, M, M, w_.embed, H, w_.attn_norm[0], m.eps, x_, xn_, st_));
   for (int l = 0; l < L; ++l) {
     eq.layer = l;
-    VC_LAUNCH(gemm(xn_, M, H, w_.wqkv[l], qkv_n, 1, eq, gws_, st_));
+    VC_LAUNCH(gemm(xn_, M, M, H, w_.wqkv[l], qkv_n, eq, gws_, st_));
     if (n_draft > 0) {
       VC_LAUNCH(draft_attention_quant(as, quant_, l, qkv_, seqs_dev_, n_draft, max_chunks_q_,
                                       cfg_.quant_bits, part_, st_));
@@ -545,14 +558,14 @@ void Engine::enqueue_forward(int M, int n_draft, int n_dense1, int n_densev, int
       VC_LAUNCH(dense_attention(as, dense_v_pool, l, qkv_, sv, n_densev, max_chunks_d_, max_rows_v, part_, st_));
       VC_LAUNCH(attention_combine(as, sv, n_densev, max_chunks_d_, max_rows_v, 1, part_, attn_, st_));
     }
-    VC_LAUNCH(gemm(attn_, M, m.n_q * d, w_.wo[l], H, 1, er, gws_, st_));
-    VC_LAUNCH(rms_apply(x_, ss_part_, M, H, w_.mlp_norm[l], m.eps, xn_, st_));
-    VC_LAUNCH(gemm(xn_, M, H, w_.wgu[l], 2 * F, 1, es, gws_, st_));
-    VC_LAUNCH(gemm(act_, M, F, w_.wd[l], H, 1, er, gws_, st_));
-    VC_LAUNCH(rms_apply(x_, ss_part_, M, H, l + 1 < L ? w_.attn_norm[l + 1] : w_.final_norm, m.eps,
+    VC_LAUNCH(gemm(attn_, M, M, m.n_q * d, w_.wo[l], H, er, gws_, st_));
+    VC_LAUNCH(rms_apply(x_, ss_part_, M, M, H, w_.mlp_norm[l], m.eps, xn_, st_));
+    VC_LAUNCH(gemm(xn_, M, M, H, w_.wgu[l], 2 * F, es, gws_, st_));
+    VC_LAUNCH(gemm(act_, M, M, F, w_.wd[l], H, er, gws_, st_));
+    VC_LAUNCH(rms_apply(x_, ss_part_, M, M, H, l + 1 < L ? w_.attn_norm[l + 1] : w_.final_norm, m.eps,
                         xn_, st_));
   }
-  VC_LAUNCH(gemm(xn_, M, H, w_.lm_head, V, 1, ef, gws_, st_));
+  VC_LAUNCH(gemm(xn_, M, M, H, w_.lm_head, V, ef, gws_, st_));
   VC_LAUNCH(argmax_rows(logits_, M, V, tok_out_, st_));
 }
 
@@ -699,6 +712,7 @@ void Engine::kernel_bench(int kind, const std::vector<int>& slots, int reps, dou
   as.d = m.d;
   as.q_stride = (m.n_q + 2 * m.n_kv) * m.d;
   as.out_stride = m.n_q * m.d;
+  as.out_mp = 0;
   as.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(m.d)));
   AttnSeq* h = reinterpret_cast<AttnSeq*>(static_cast<int32_t*>(h_desc_) + Mmax_) ;
   h = reinterpret_cast<AttnSeq*>(reinterpret_cast<RowDest*>(h) + Mmax_);

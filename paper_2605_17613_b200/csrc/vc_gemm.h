@@ -49,16 +49,21 @@ struct GemmWorkspace {
 int gemm_splits(int N, int K);
 size_t gemm_partial_floats(int M, int N, int K);
 int gemm_tiles(int M, int N);
-// y = X[M][K] . W[N][K]^T, then the epilogue.  N must be a multiple of 128.
-cudaError_t gemm(const uint16_t* X, int M, int K, const uint16_t* W, int N, int splits,
+// y = X[M][K] . W[N][K]^T, then the epilogue.  Xt: activations in the tiled
+// layout with Mp padded rows; Wt: weights in the tiled layout (vc_tiled.cuh).
+// N must be a multiple of 128, K of 64.
+cudaError_t gemm(const uint16_t* Xt, int Mp, int M, int K, const uint16_t* Wt, int N,
                  const GemmEpilogue& epi, const GemmWorkspace& ws, cudaStream_t st);
+// Logical row-major -> tiled layouts (weights at load time, probes).
+cudaError_t retile_weight(const uint16_t* src, int N, int K, uint16_t* dst, cudaStream_t st);
+cudaError_t retile_act(const uint16_t* src, int M, int K, int Mp, uint16_t* dst, cudaStream_t st);
 
-// x[m][H] fp32 = embed[tok[m]]; xn = bf16(rmsnorm(x) * w).
-cudaError_t embed_norm(const int32_t* tokens, int M, const uint16_t* embed, int H,
+// x[m][H] fp32 = embed[tok[m]]; xn (tiled, Mp rows) = bf16(rmsnorm(x) * w).
+cudaError_t embed_norm(const int32_t* tokens, int M, int Mp, const uint16_t* embed, int H,
                        const uint16_t* norm_w, float eps, float* x, uint16_t* xn, cudaStream_t st);
-// xn = bf16(x * rsqrt(sum(ss_part[m][:]) / H + eps) * w)
-cudaError_t rms_apply(const float* x, const float* ss_part, int M, int H, const uint16_t* norm_w,
-                      float eps, uint16_t* xn, cudaStream_t st);
+// xn (tiled) = bf16(x * rsqrt(sum(ss_part[m][:]) / H + eps) * w)
+cudaError_t rms_apply(const float* x, const float* ss_part, int M, int Mp, int H,
+                      const uint16_t* norm_w, float eps, uint16_t* xn, cudaStream_t st);
 // out[m] = argmax_n logits[m][n], ties -> smallest n.
 cudaError_t argmax_rows(const float* logits, int M, int N, int32_t* out, cudaStream_t st);
 // Synthetic bf16 init shared bit-for-bit with oracle/vc_oracle.c.

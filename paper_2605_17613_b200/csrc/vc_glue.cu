@@ -4,6 +4,7 @@
 // fixed order so a row's result never depends on the other rows of the batch.
 #include "vc_common.cuh"
 #include "vc_gemm.h"
+#include "vc_tiled.cuh"
 
 namespace vc {
 namespace {
@@ -22,7 +23,7 @@ VC_DEV float block_sum(float v, float* red) {
   return t;
 }
 
-__global__ void embed_norm_kernel(const int32_t* tokens, const uint16_t* embed, int H,
+__global__ void embed_norm_kernel(const int32_t* tokens, int Mp, const uint16_t* embed, int H,
                                   const uint16_t* norm_w, float eps, float* x, uint16_t* xn) {
   __shared__ float red[32];
   const int m = blockIdx.x;
@@ -37,13 +38,13 @@ __global__ void embed_norm_kernel(const int32_t* tokens, const uint16_t* embed, 
   ss = block_sum(ss, red);
   const float r = rsqrtf(ss / H + eps);
   for (int i = threadIdx.x; i < H; i += blockDim.x)
-    xn[static_cast<size_t>(m) * H + i] = f2bf(__fmul_rn(__fmul_rn(xr[i], r), bf2f(norm_w[i])));
+    xn[atile_idx(m, i, Mp)] = f2bf(__fmul_rn(__fmul_rn(xr[i], r), bf2f(norm_w[i])));
 }
 
 // grid (M, H / 1024): every CTA recomputes the row's r from the per-tile
 // partial sums (fixed order) and normalises its 1024-wide chunk.
-__global__ void rms_apply_kernel(const float* x, const float* ss_part, int H, const uint16_t* w,
-                                 float eps, uint16_t* xn) {
+__global__ void rms_apply_kernel(const float* x, const float* ss_part, int H, int Mp,
+                                 const uint16_t* w, float eps, uint16_t* xn) {
   __shared__ float r_s;
   const int m = blockIdx.x;
   const int tiles = H / 128;
@@ -57,7 +58,7 @@ __global__ void rms_apply_kernel(const float* x, const float* ss_part, int H, co
   const float r = r_s;
   const int base = blockIdx.y * 1024;
   for (int i = base + threadIdx.x; i < min(H, base + 1024); i += blockDim.x)
-    xn[static_cast<size_t>(m) * H + i] = f2bf(__fmul_rn(__fmul_rn(x[static_cast<size_t>(m) * H + i], r), bf2f(w[i])));
+    xn[atile_idx(m, i, Mp)] = f2bf(__fmul_rn(__fmul_rn(x[static_cast<size_t>(m) * H + i], r), bf2f(w[i])));
 }
 
 __global__ void argmax_kernel(const float* logits, int N, int32_t* out) {
@@ -134,17 +135,17 @@ int grid_for(size_t n, int threads) {
 
 }  // namespace
 
-cudaError_t embed_norm(const int32_t* tokens, int M, const uint16_t* embed, int H,
+cudaError_t embed_norm(const int32_t* tokens, int M, int Mp, const uint16_t* embed, int H,
                        const uint16_t* norm_w, float eps, float* x, uint16_t* xn, cudaStream_t st) {
   if (M <= 0) return cudaSuccess;
-  embed_norm_kernel<<<M, kNormThreads, 0, st>>>(tokens, embed, H, norm_w, eps, x, xn);
+  embed_norm_kernel<<<M, kNormThreads, 0, st>>>(tokens, Mp, embed, H, norm_w, eps, x, xn);
   return cudaGetLastError();
 }
 
-cudaError_t rms_apply(const float* x, const float* ss_part, int M, int H, const uint16_t* norm_w,
-                      float eps, uint16_t* xn, cudaStream_t st) {
+cudaError_t rms_apply(const float* x, const float* ss_part, int M, int Mp, int H,
+                      const uint16_t* norm_w, float eps, uint16_t* xn, cudaStream_t st) {
   if (M <= 0) return cudaSuccess;
-  rms_apply_kernel<<<dim3(M, (H + 1023) / 1024), 256, 0, st>>>(x, ss_part, H, norm_w, eps, xn);
+  rms_apply_kernel<<<dim3(M, (H + 1023) / 1024), 256, 0, st>>>(x, ss_part, H, Mp, norm_w, eps, xn);
   return cudaGetLastError();
 }
 

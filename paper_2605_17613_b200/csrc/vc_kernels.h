@@ -64,7 +64,8 @@ struct QuantPool {     // per slice: kc/vc words, ksz [groups][d], vsz [cap]
 struct AttnShape {
   int layers, n_kv, n_rep, d;
   int q_stride;        // elements per activation row of the qkv buffer
-  int out_stride;      // elements per row of the attention output
+  int out_stride;      // elements per row of the attention output (row-major)
+  int out_mp;          // > 0: write the output in the GEMM's tiled layout with Mp rows
   float scale_log2;    // log2(e)/sqrt(d)
 };
 
