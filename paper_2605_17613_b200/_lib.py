@@ -9,7 +9,7 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libvericache.so")
+LIB_PATH = os.environ.get("VC_LIB", os.path.join(_HERE, "libvericache.so"))
 
 VC_OK, VC_ERR_CONFIG, VC_ERR_CONTRACT, VC_ERR_CUDA = 0, 1, 2, 3
 

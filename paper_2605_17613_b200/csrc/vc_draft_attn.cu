@@ -332,7 +332,8 @@ __global__ void __launch_bounds__(128) draft_attn_quant_kernel(AttnShape s, Quan
         mma_f16(oacc[ct], a0, a1, a2, a3, bp0[m], bp1[m]);
       }
     }
-    __syncwarp();  // every lane has consumed the stage (all LDS results used)
+    fence_proxy_async();  // LDS reads of the stage before the next TMA write into it
+    __syncwarp();
     if (lane == 0 && u + 2 < n_units) issue(u + 2, st);
   }
 

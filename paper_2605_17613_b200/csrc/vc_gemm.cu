@@ -224,6 +224,9 @@ gemm_tma_kernel(const uint16_t* __restrict__ Xt, int Mp, int M, int K,
           mma_bf16(acc[f + 1], a[0], a[1], a[2], a[3], b[2], b[3]);
         }
       }
+      // order this warp's generic-proxy reads of the stage before the producer's
+      // next async-proxy (TMA) write into it -- without it the refill can race
+      fence_proxy_async();
       __syncwarp();
       if (lane == 0) mbar_arrive(&empty[st]);  // this warp is done with the stage
     }
