@@ -231,9 +231,17 @@ int vc_quant_kivi_slice(const uint16_t* k, const uint16_t* v, int n_groups, int 
  * out: host bf16 [n_rows][n_q][d].                                          */
 int vc_attention_probe(vc_engine* e, int slot, int layer, int mode, const uint16_t* q_dev,
                        int n_rows, int kv_len, uint16_t* out_host);
+/* Read n token rows of one (layer, kv-head) slice of a KV pool to host bf16
+ * buffers [n][d]: pool 0 = HBM full tier, 1 = staging slots, 2 = host pool. */
+int vc_kv_read(vc_engine* e, int pool, int slot, int layer, int head, int pos, int n, uint16_t* k,
+               uint16_t* v);
 /* ws = X[M][K] . W[N][K]^T via the batch-invariant projection GEMM (device). */
 int vc_gemm_probe(const uint16_t* X, int M, int K, const uint16_t* W, int N, float* Y,
                   void* stream);
+/* Same with a fused epilogue: epi 0 = fp32 store, 3 = SiLU-gate over
+ * interleaved (gate, up) columns into bf16 act [M][N/2] (tiled layout).     */
+int vc_gemm_probe_epi(const uint16_t* X, int M, int K, const uint16_t* W, int N, int epi, void* Y,
+                      void* stream);
 
 #ifdef __cplusplus
 }

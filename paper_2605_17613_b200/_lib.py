@@ -119,7 +119,9 @@ SIGNATURES = {
     "vc_reload_span": (I, [I64, D, D, PD, PI]),
     "vc_quant_kivi_slice": (I, [P, P, I, I, I, P, P, P, P, P]),
     "vc_attention_probe": (I, [P, I, I, I, P, I, I, PU16]),
+    "vc_kv_read": (I, [P, I, I, I, I, I, I, PU16, PU16]),
     "vc_gemm_probe": (I, [P, I, I, P, I, P, P]),
+    "vc_gemm_probe_epi": (I, [P, I, I, P, I, I, P, P]),
 }
 
 _lib = None

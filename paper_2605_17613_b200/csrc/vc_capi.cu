@@ -513,12 +513,38 @@ int vc_quant_kivi_slice(const uint16_t* k, const uint16_t* v, int n_groups, int 
   });
 }
 
+int vc_kv_read(vc_engine* e, int pool, int slot, int layer, int head, int pos, int n, uint16_t* k,
+               uint16_t* v) {
+  return guard([&] {
+    vc::Engine& en = E(e);
+    const auto& m = en.model();
+    const vc::KvPool p = pool == 1 ? en.stage_pool() : en.full_pool();
+    const size_t slice = (static_cast<size_t>(slot) * m.layers + layer) * m.n_kv + head;
+    const size_t off = (slice * p.cap + pos) * m.d;
+    const size_t bytes = static_cast<size_t>(n) * m.d * 2;
+    if (pool == 2) {
+      if (!en.host_pool_k()) throw vc::ContractViolation("no host pool");
+      std::memcpy(k, en.host_pool_k() + off, bytes);
+      std::memcpy(v, en.host_pool_v() + off, bytes);
+      return;
+    }
+    if (!p.k) throw vc::ContractViolation("pool not allocated");
+    vc::check_cuda(cudaMemcpy(k, p.k + off, bytes, cudaMemcpyDeviceToHost), "kv_read");
+    vc::check_cuda(cudaMemcpy(v, p.v + off, bytes, cudaMemcpyDeviceToHost), "kv_read");
+  });
+}
+
 int vc_attention_probe(vc_engine* e, int slot, int layer, int mode, const uint16_t* q_dev, int n_rows,
                        int kv_len, uint16_t* out_host) {
   return guard([&] { E(e).attention_probe(slot, layer, mode, q_dev, n_rows, kv_len, out_host); });
 }
 
 int vc_gemm_probe(const uint16_t* X, int M, int K, const uint16_t* W, int N, float* Y, void* stream) {
+  return vc_gemm_probe_epi(X, M, K, W, N, 0, Y, stream);
+}
+
+int vc_gemm_probe_epi(const uint16_t* X, int M, int K, const uint16_t* W, int N, int epi, void* Y,
+                      void* stream) {
   return guard([&] {
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     vc::GemmWorkspace ws;
@@ -528,8 +554,13 @@ int vc_gemm_probe(const uint16_t* X, int M, int K, const uint16_t* W, int N, flo
     vc::check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&ws.counters), sizeof(int) * ws.n_counters, st), "malloc");
     vc::check_cuda(cudaMemsetAsync(ws.counters, 0, sizeof(int) * ws.n_counters, st), "memset");
     vc::GemmEpilogue ep;
-    ep.kind = vc::Epi::StoreF32;
-    ep.out_f32 = Y;
+    if (epi == 3) {  // SiLU-gate: Y = bf16 act in the tiled layout (Mp = M)
+      ep.kind = vc::Epi::Silu;
+      ep.out_bf16 = static_cast<uint16_t*>(Y);
+    } else {
+      ep.kind = vc::Epi::StoreF32;
+      ep.out_f32 = static_cast<float*>(Y);
+    }
     // logical inputs -> the tiled HBM layouts the GEMM streams
     uint16_t *xt = nullptr, *wt = nullptr;
     const size_t xe = static_cast<size_t>(M + 128) * K, we = static_cast<size_t>(N) * K;

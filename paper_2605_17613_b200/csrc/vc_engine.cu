@@ -4,6 +4,8 @@
 #include <cuda_bf16.h>
 
 #include <cmath>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <sstream>
 #include <stdexcept>
@@ -202,8 +204,9 @@ void Engine::alloc_all() {
       }
     rope_cos_ = dmalloc<float>(c.size());
     rope_sin_ = dmalloc<float>(s.size());
-    VC_CK(cudaMemcpy(rope_cos_, c.data(), c.size() * 4, cudaMemcpyHostToDevice));
-    VC_CK(cudaMemcpy(rope_sin_, s.data(), s.size() * 4, cudaMemcpyHostToDevice));
+    VC_CK(cudaMemcpyAsync(rope_cos_, c.data(), c.size() * 4, cudaMemcpyHostToDevice, st_));
+    VC_CK(cudaMemcpyAsync(rope_sin_, s.data(), s.size() * 4, cudaMemcpyHostToDevice, st_));
+    VC_CK(cudaStreamSynchronize(st_));
   }
   // ---- KV tiers ------------------------------------------------------------
   const size_t slices = static_cast<size_t>(cfg_.max_slots) * L * m.n_kv;
@@ -313,8 +316,11 @@ void Engine::load_weights(const uint16_t* embed, const uint16_t* const* attn_nor
   const auto& m = cfg_.model;
   const int L = m.layers, H = m.hidden, F = m.ffn, V = m.vocab, d = m.d;
   const int qkv_n = (m.n_q + 2 * m.n_kv) * d;
+  // Every upload is stream-ordered on st_: a plain cudaMemcpy from pageable
+  // memory may return before its DMA lands, and st_ does not synchronise with
+  // the legacy default stream, so the retile kernel could read stale bytes.
   auto up = [&](uint16_t* dst, const uint16_t* src, size_t n) {
-    VC_CK(cudaMemcpy(dst, src, n * 2, cudaMemcpyHostToDevice));
+    VC_CK(cudaMemcpyAsync(dst, src, n * 2, cudaMemcpyHostToDevice, st_));
   };
   // GEMM weights: logical [N][K] -> staging -> tiled layout (vc_tiled.cuh)
   const size_t max_elems = std::max(std::max(static_cast<size_t>(V) * H, static_cast<size_t>(2) * F * H),
@@ -323,7 +329,6 @@ void Engine::load_weights(const uint16_t* embed, const uint16_t* const* attn_nor
   auto up_tiled = [&](uint16_t* dst, const uint16_t* src, int N, int K) {
     up(tmp, src, static_cast<size_t>(N) * K);
     VC_LAUNCH(retile_weight(tmp, N, K, dst, st_));
-    VC_CK(cudaStreamSynchronize(st_));
   };
   up(w_.embed, embed, static_cast<size_t>(V) * H);
   std::vector<uint16_t> gu(static_cast<size_t>(2) * F * H);
@@ -342,6 +347,7 @@ void Engine::load_weights(const uint16_t* embed, const uint16_t* const* attn_nor
   }
   up(w_.final_norm, final_norm, H);
   up_tiled(w_.lm_head, lm_head, V, H);
+  VC_CK(cudaStreamSynchronize(st_));
   cudaFree(tmp);
 }
 
@@ -517,6 +523,17 @@ void Engine::enqueue_forward(int M, int n_draft, int n_dense1, int n_densev, int
   as.out_mp = M;  // attention output feeds o_proj in the tiled layout
   as.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(d)));
   const KvPool dense_v_pool = cfg_.full_tier == 0 ? full_ : stage_;
+  // VC_TRACE=1 (eager engines only): checksum every stage's output buffer
+  static const bool tracing = std::getenv("VC_TRACE") != nullptr;
+  auto trace = [&](const char* name, const void* p, size_t bytes) {
+    if (!tracing || cfg_.use_graphs) return;
+    VC_CK(cudaStreamSynchronize(st_));
+    std::vector<uint8_t> h(bytes);
+    VC_CK(cudaMemcpy(h.data(), p, bytes, cudaMemcpyDeviceToHost));
+    uint64_t x = 0xcbf29ce484222325ull;
+    for (uint8_t c : h) x = (x ^ c) * 0x100000001b3ull;
+    std::fprintf(stderr, "TRACE %s %016llx\n", name, static_cast<unsigned long long>(x));
+  };
   GemmEpilogue eq;
   eq.kind = Epi::Qkv;
   eq.out_bf16 = qkv_;
@@ -541,9 +558,13 @@ void Engine::enqueue_forward(int M, int n_draft, int n_dense1, int n_densev, int
   ef.kind = Epi::StoreF32;
   ef.out_f32 = logits_;
   VC_LAUNCH(embed_norm(tok_in_, M, M, w_.embed, H, w_.attn_norm[0], m.eps, x_, xn_, st_));
+  trace("embed.x", x_, static_cast<size_t>(M) * H * 4);
+  trace("w.gu0", w_.wgu[0], static_cast<size_t>(2) * F * H * 2);
+  trace("w.qkv0", w_.wqkv[0], static_cast<size_t>(qkv_n) * H * 2);
   for (int l = 0; l < L; ++l) {
     eq.layer = l;
     VC_LAUNCH(gemm(xn_, M, M, H, w_.wqkv[l], qkv_n, eq, gws_, st_));
+    trace("qkv", qkv_, static_cast<size_t>(M) * qkv_n * 2);
     if (n_draft > 0) {
       VC_LAUNCH(draft_attention_quant(as, quant_, l, qkv_, seqs_dev_, n_draft, max_chunks_q_,
                                       cfg_.quant_bits, part_, st_));
@@ -559,13 +580,39 @@ void Engine::enqueue_forward(int M, int n_draft, int n_dense1, int n_densev, int
       VC_LAUNCH(attention_combine(as, sv, n_densev, max_chunks_d_, max_rows_v, 1, part_, attn_, st_));
     }
     VC_LAUNCH(gemm(attn_, M, M, m.n_q * d, w_.wo[l], H, er, gws_, st_));
+    trace("attn", attn_, static_cast<size_t>(M) * m.n_q * d * 2);
+    trace("x.o", x_, static_cast<size_t>(M) * H * 4);
+    trace("ss.o", ss_part_, static_cast<size_t>(M) * (H / 128) * 4);
+    if (tracing && !cfg_.use_graphs) {
+      std::vector<int> cnt(gws_.n_counters);
+      VC_CK(cudaMemcpy(cnt.data(), gws_.counters, cnt.size() * 4, cudaMemcpyDeviceToHost));
+      int nz = 0;
+      for (int c : cnt) nz += c != 0;
+      std::fprintf(stderr, "TRACE counters_nonzero %d\n", nz);
+      VC_CK(cudaMemset(act_, 0xff, static_cast<size_t>(M) * F * 2));
+    }
     VC_LAUNCH(rms_apply(x_, ss_part_, M, M, H, w_.mlp_norm[l], m.eps, xn_, st_));
+    trace("xn.o", xn_, static_cast<size_t>(M) * H * 2);
     VC_LAUNCH(gemm(xn_, M, M, H, w_.wgu[l], 2 * F, es, gws_, st_));
+    trace("act", act_, static_cast<size_t>(M) * F * 2);
+    if (tracing && !cfg_.use_graphs) {
+      std::vector<uint16_t> a(static_cast<size_t>(M) * F);
+      VC_CK(cudaMemcpy(a.data(), act_, a.size() * 2, cudaMemcpyDeviceToHost));
+      std::vector<int> bad_tiles(F / 64, 0);
+      for (size_t i = 0; i < a.size(); ++i)
+        if (a[i] == 0xffff) bad_tiles[i / (64 * M)]++;
+      std::fprintf(stderr, "TRACE act_unwritten");
+      for (size_t t = 0; t < bad_tiles.size(); ++t)
+        if (bad_tiles[t]) std::fprintf(stderr, " t%zu:%d", t, bad_tiles[t]);
+      std::fprintf(stderr, "\n");
+    }
     VC_LAUNCH(gemm(act_, M, M, F, w_.wd[l], H, er, gws_, st_));
+    trace("x.d", x_, static_cast<size_t>(M) * H * 4);
     VC_LAUNCH(rms_apply(x_, ss_part_, M, M, H, l + 1 < L ? w_.attn_norm[l + 1] : w_.final_norm, m.eps,
                         xn_, st_));
   }
   VC_LAUNCH(gemm(xn_, M, M, H, w_.lm_head, V, ef, gws_, st_));
+  trace("logits", logits_, static_cast<size_t>(M) * V * 4);
   VC_LAUNCH(argmax_rows(logits_, M, V, tok_out_, st_));
 }
 

@@ -311,6 +311,15 @@ class Engine:
         return out, {f: getattr(st, f) for f, _ in st._fields_}
 
     # ---- probes -----------------------------------------------------------------
+    def kv_read(self, pool, slot, layer, head, pos, n):
+        """pool 0 full (HBM), 1 staging, 2 host; returns bf16 bits k, v [n][d]."""
+        d = self.model.d_head
+        k = np.zeros((n, d), np.uint16)
+        v = np.zeros_like(k)
+        check(self.lib.vc_kv_read(self.h, pool, slot, layer, head, pos, n, _ptr(k, C.c_uint16),
+                                  _ptr(v, C.c_uint16)))
+        return k, v
+
     def attention_probe(self, slot, layer, mode, q_dev_ptr, n_rows, kv_len):
         out = np.zeros((n_rows, self.model.n_q, self.model.d_head), np.uint16)
         check(self.lib.vc_attention_probe(self.h, slot, layer, mode, C.c_void_p(q_dev_ptr), n_rows,
