@@ -106,6 +106,10 @@ int vc_engine_init_weights(vc_engine* e, uint64_t seed, float stddev) {
   return guard([&] { E(e).init_weights_random(seed, stddev); });
 }
 
+int vc_engine_init_weights_scaled(vc_engine* e, uint64_t seed, float stddev, float resid_std) {
+  return guard([&] { E(e).init_weights_random(seed, stddev, resid_std); });
+}
+
 int vc_engine_load_weights(vc_engine* e, const uint16_t* embed, const uint16_t* const* attn_norm,
                            const uint16_t* const* wqkv, const uint16_t* const* wo,
                            const uint16_t* const* mlp_norm, const uint16_t* const* wgate,

@@ -283,25 +283,29 @@ void Engine::alloc_all() {
 }
 
 // ---------------------------------------------------------------- weights
-void Engine::init_weights_random(uint64_t seed, float stddev) {
+void Engine::init_weights_random(uint64_t seed, float stddev, float resid_std) {
   const auto& m = cfg_.model;
   const int L = m.layers, H = m.hidden, F = m.ffn, V = m.vocab, d = m.d;
   const int qkv_n = (m.n_q + 2 * m.n_kv) * d;
   const float k = static_cast<float>(stddev / (65536.0 * std::sqrt(1.0 / 3.0)));
+  // residual-branch outputs (o_proj, down_proj) may use a smaller std
+  // (GPT-2 style std / sqrt(2 L)); resid_std <= 0 keeps stddev
+  const float kr = resid_std > 0.f ? static_cast<float>(resid_std / (65536.0 * std::sqrt(1.0 / 3.0))) : k;
   uint64_t off = 0;
-  auto fill = [&](uint16_t* p, size_t n) {
-    VC_LAUNCH(fill_normal_bf16(p, n, seed, off, k, st_));
+  auto fill_k = [&](uint16_t* p, size_t n, float kk) {
+    VC_LAUNCH(fill_normal_bf16(p, n, seed, off, kk, st_));
     off += n;
   };
+  auto fill = [&](uint16_t* p, size_t n) { fill_k(p, n, k); };
   const uint16_t one = 0x3f80;
   fill(w_.embed, static_cast<size_t>(V) * H);
   for (int l = 0; l < L; ++l) {
     VC_LAUNCH(fill_const_bf16(w_.attn_norm[l], H, one, st_));
     fill(w_.wqkv[l], static_cast<size_t>(qkv_n) * H);
-    fill(w_.wo[l], static_cast<size_t>(H) * m.n_q * d);
+    fill_k(w_.wo[l], static_cast<size_t>(H) * m.n_q * d, kr);
     VC_LAUNCH(fill_const_bf16(w_.mlp_norm[l], H, one, st_));
     fill(w_.wgu[l], static_cast<size_t>(2) * F * H);
-    fill(w_.wd[l], static_cast<size_t>(H) * F);
+    fill_k(w_.wd[l], static_cast<size_t>(H) * F, kr);
   }
   VC_LAUNCH(fill_const_bf16(w_.final_norm, H, one, st_));
   fill(w_.lm_head, static_cast<size_t>(V) * H);
@@ -583,29 +587,10 @@ void Engine::enqueue_forward(int M, int n_draft, int n_dense1, int n_densev, int
     trace("attn", attn_, static_cast<size_t>(M) * m.n_q * d * 2);
     trace("x.o", x_, static_cast<size_t>(M) * H * 4);
     trace("ss.o", ss_part_, static_cast<size_t>(M) * (H / 128) * 4);
-    if (tracing && !cfg_.use_graphs) {
-      std::vector<int> cnt(gws_.n_counters);
-      VC_CK(cudaMemcpy(cnt.data(), gws_.counters, cnt.size() * 4, cudaMemcpyDeviceToHost));
-      int nz = 0;
-      for (int c : cnt) nz += c != 0;
-      std::fprintf(stderr, "TRACE counters_nonzero %d\n", nz);
-      VC_CK(cudaMemset(act_, 0xff, static_cast<size_t>(M) * F * 2));
-    }
     VC_LAUNCH(rms_apply(x_, ss_part_, M, M, H, w_.mlp_norm[l], m.eps, xn_, st_));
     trace("xn.o", xn_, static_cast<size_t>(M) * H * 2);
     VC_LAUNCH(gemm(xn_, M, M, H, w_.wgu[l], 2 * F, es, gws_, st_));
     trace("act", act_, static_cast<size_t>(M) * F * 2);
-    if (tracing && !cfg_.use_graphs) {
-      std::vector<uint16_t> a(static_cast<size_t>(M) * F);
-      VC_CK(cudaMemcpy(a.data(), act_, a.size() * 2, cudaMemcpyDeviceToHost));
-      std::vector<int> bad_tiles(F / 64, 0);
-      for (size_t i = 0; i < a.size(); ++i)
-        if (a[i] == 0xffff) bad_tiles[i / (64 * M)]++;
-      std::fprintf(stderr, "TRACE act_unwritten");
-      for (size_t t = 0; t < bad_tiles.size(); ++t)
-        if (bad_tiles[t]) std::fprintf(stderr, " t%zu:%d", t, bad_tiles[t]);
-      std::fprintf(stderr, "\n");
-    }
     VC_LAUNCH(gemm(act_, M, M, F, w_.wd[l], H, er, gws_, st_));
     trace("x.d", x_, static_cast<size_t>(M) * H * 4);
     VC_LAUNCH(rms_apply(x_, ss_part_, M, M, H, l + 1 < L ? w_.attn_norm[l + 1] : w_.final_norm, m.eps,
