@@ -96,8 +96,10 @@ int vc_engine_create(const vc_model_desc* model, const vc_runtime_desc* rt, int 
 int vc_engine_destroy(vc_engine* e);
 int vc_engine_init_weights(vc_engine* e, uint64_t seed, float stddev);
 /* Same, with the residual-branch output projections (o_proj, down_proj)
- * drawn with resid_std (GPT-2 style stddev / sqrt(2 * layers)).             */
-int vc_engine_init_weights_scaled(vc_engine* e, uint64_t seed, float stddev, float resid_std);
+ * drawn with resid_std (GPT-2 style stddev / sqrt(2 * layers)) and the Q
+ * projection rows with q_std (attention temperature); <= 0 keeps stddev.   */
+int vc_engine_init_weights_scaled(vc_engine* e, uint64_t seed, float stddev, float resid_std,
+                                  float q_std);
 /* logical layouts, bf16 bits; per-layer arrays have `layers` pointers      */
 int vc_engine_load_weights(vc_engine* e, const uint16_t* embed, const uint16_t* const* attn_norm,
                            const uint16_t* const* wqkv, const uint16_t* const* wo,

@@ -88,7 +88,7 @@ SIGNATURES = {
     "vc_engine_create": (I, [C.POINTER(ModelDesc), C.POINTER(RuntimeDesc), I, C.POINTER(P)]),
     "vc_engine_destroy": (I, [P]),
     "vc_engine_init_weights": (I, [P, U64, F]),
-    "vc_engine_init_weights_scaled": (I, [P, U64, F, F]),
+    "vc_engine_init_weights_scaled": (I, [P, U64, F, F, F]),
     "vc_engine_load_weights": (I, [P, PU16, PPU16, PPU16, PPU16, PPU16, PPU16, PPU16, PPU16, PU16, PU16]),
     "vc_engine_stats": (I, [P, PU64, PU64]),
     "vc_engine_timing": (I, [P, PD, PI64, I]),

@@ -106,8 +106,9 @@ int vc_engine_init_weights(vc_engine* e, uint64_t seed, float stddev) {
   return guard([&] { E(e).init_weights_random(seed, stddev); });
 }
 
-int vc_engine_init_weights_scaled(vc_engine* e, uint64_t seed, float stddev, float resid_std) {
-  return guard([&] { E(e).init_weights_random(seed, stddev, resid_std); });
+int vc_engine_init_weights_scaled(vc_engine* e, uint64_t seed, float stddev, float resid_std,
+                                  float q_std) {
+  return guard([&] { E(e).init_weights_random(seed, stddev, resid_std, q_std); });
 }
 
 int vc_engine_load_weights(vc_engine* e, const uint16_t* embed, const uint16_t* const* attn_norm,

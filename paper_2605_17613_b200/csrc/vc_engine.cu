@@ -283,7 +283,7 @@ void Engine::alloc_all() {
 }
 
 // ---------------------------------------------------------------- weights
-void Engine::init_weights_random(uint64_t seed, float stddev, float resid_std) {
+void Engine::init_weights_random(uint64_t seed, float stddev, float resid_std, float q_std) {
   const auto& m = cfg_.model;
   const int L = m.layers, H = m.hidden, F = m.ffn, V = m.vocab, d = m.d;
   const int qkv_n = (m.n_q + 2 * m.n_kv) * d;
@@ -301,7 +301,16 @@ void Engine::init_weights_random(uint64_t seed, float stddev, float resid_std) {
   fill(w_.embed, static_cast<size_t>(V) * H);
   for (int l = 0; l < L; ++l) {
     VC_LAUNCH(fill_const_bf16(w_.attn_norm[l], H, one, st_));
-    fill(w_.wqkv[l], static_cast<size_t>(qkv_n) * H);
+    if (q_std > 0.f) {
+      // the Q projection rows are the first n_q*d rows = a contiguous prefix
+      // of the tiled layout (blocks are n-tile major)
+      const float kq = static_cast<float>(q_std / (65536.0 * std::sqrt(1.0 / 3.0)));
+      const size_t nq_elems = static_cast<size_t>(m.n_q) * d * H;
+      fill_k(w_.wqkv[l], nq_elems, kq);
+      fill(w_.wqkv[l] + nq_elems, static_cast<size_t>(qkv_n) * H - nq_elems);
+    } else {
+      fill(w_.wqkv[l], static_cast<size_t>(qkv_n) * H);
+    }
     fill_k(w_.wo[l], static_cast<size_t>(H) * m.n_q * d, kr);
     VC_LAUNCH(fill_const_bf16(w_.mlp_norm[l], H, one, st_));
     fill(w_.wgu[l], static_cast<size_t>(2) * F * H);

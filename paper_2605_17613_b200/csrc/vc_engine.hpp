@@ -79,7 +79,7 @@ class Engine {
   const ModelDesc& model() const { return cfg_.model; }
 
   // ---- weights -------------------------------------------------------
-  void init_weights_random(uint64_t seed, float stddev, float resid_std = 0.f);
+  void init_weights_random(uint64_t seed, float stddev, float resid_std = 0.f, float q_std = 0.f);
   // Logical layouts (see oracle/vc_oracle.h); bf16 bits.
   void load_weights(const uint16_t* embed, const uint16_t* const* attn_norm,
                     const uint16_t* const* wqkv, const uint16_t* const* wo,

@@ -125,10 +125,12 @@ class Engine:
             pass
 
     # ---- weights ----------------------------------------------------------------
-    def init_weights(self, seed: int = 0, std: float = 0.02, resid_std: float = 0.0):
-        """Random init; resid_std > 0 scales o_proj/down_proj (GPT-2: std/sqrt(2L))."""
-        if resid_std > 0:
-            check(self.lib.vc_engine_init_weights_scaled(self.h, seed, std, resid_std))
+    def init_weights(self, seed: int = 0, std: float = 0.02, resid_std: float = 0.0,
+                     q_std: float = 0.0):
+        """Random init; resid_std > 0 scales o_proj/down_proj (GPT-2: std/sqrt(2L)),
+        q_std > 0 the Q projection (attention temperature)."""
+        if resid_std > 0 or q_std > 0:
+            check(self.lib.vc_engine_init_weights_scaled(self.h, seed, std, resid_std, q_std))
         else:
             check(self.lib.vc_engine_init_weights(self.h, seed, std))
 
