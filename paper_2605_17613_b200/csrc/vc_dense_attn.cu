@@ -33,7 +33,7 @@ VC_DEV int swz(int row, int chunk16) {  // 16-B chunk index within a row
 }
 
 template <int D, int NREP>
-__global__ void dense_attn_kernel(AttnShape s, KvPool pool, int layer, const uint16_t* qkv,
+__global__ void __launch_bounds__(256, 2) dense_attn_kernel(AttnShape s, KvPool pool, int layer, const uint16_t* qkv,
                                   const AttnSeq* seqs, int max_chunks, int row_blocks,
                                   Partials part) {
   constexpr int KS = D / 16;       // k-steps over channels
@@ -86,7 +86,9 @@ __global__ void dense_attn_kernel(AttnShape s, KvPool pool, int layer, const uin
     cp_async_commit();
   }
 
-  // Q fragments of this warp's 16 rows (A operand, row-major)
+  // This warp's 16 query rows staged in shared memory (swizzled like the K
+  // tiles); A fragments are re-read with ldmatrix per k-step, which keeps the
+  // register budget for the O accumulators.
   const int r0 = row_base + warp * 16 + (lane >> 2);
   const int r1 = r0 + 8;
   auto qptr = [&](int r) -> const uint16_t* {
@@ -94,17 +96,15 @@ __global__ void dense_attn_kernel(AttnShape s, KvPool pool, int layer, const uin
     return qkv + static_cast<size_t>(sq.row0 + tok) * s.q_stride + static_cast<size_t>(h * NREP + rep) * D;
   };
   const bool v0 = r0 < n_rows, v1 = r1 < n_rows;
-  const uint16_t* q0 = qptr(v0 ? r0 : 0);
-  const uint16_t* q1 = qptr(v1 ? r1 : 0);
-  uint32_t qa[KS][4];
-#pragma unroll
-  for (int st = 0; st < KS; ++st) {
-    const int c = st * 16 + 2 * (lane & 3);
-    qa[st][0] = v0 ? *reinterpret_cast<const uint32_t*>(q0 + c) : 0u;
-    qa[st][1] = v1 ? *reinterpret_cast<const uint32_t*>(q1 + c) : 0u;
-    qa[st][2] = v0 ? *reinterpret_cast<const uint32_t*>(q0 + c + 8) : 0u;
-    qa[st][3] = v1 ? *reinterpret_cast<const uint32_t*>(q1 + c + 8) : 0u;
+  uint8_t* sQw = smem + 2 * kStages * kTile * RB + warp * 16 * RB;
+  for (int i = lane; i < 16 * C16; i += 32) {
+    const int r = i / C16, c = i % C16;
+    const int row = row_base + warp * 16 + r;
+    uint4 val = make_uint4(0, 0, 0, 0);
+    if (row < n_rows) val = *reinterpret_cast<const uint4*>(qptr(row) + c * 8);
+    *reinterpret_cast<uint4*>(sQw + r * RB + swz<D>(r, c) * 16) = val;
   }
+  __syncwarp();
   // causal limits of this lane's two rows
   const int lim0 = sq.kv_len - sq.n_rows + (v0 ? r0 : 0) / NREP + 1;
   const int lim1 = sq.kv_len - sq.n_rows + (v1 ? r1 : 0) / NREP + 1;
@@ -129,18 +129,25 @@ __global__ void dense_attn_kernel(AttnShape s, KvPool pool, int layer, const uin
       // ---- S = Q K^T : 16 rows x 32 keys -------------------------------
       float sc[4][4];
 #pragma unroll
-      for (int nk = 0; nk < 4; ++nk) {
-        sc[nk][0] = sc[nk][1] = sc[nk][2] = sc[nk][3] = 0.f;
+      for (int nk = 0; nk < 4; ++nk) sc[nk][0] = sc[nk][1] = sc[nk][2] = sc[nk][3] = 0.f;
+      // every S element accumulates its k-steps in order 0..KS-1
 #pragma unroll
-        for (int st = 0; st < KS; st += 2) {
-          // x4: matrices (keys nk*8.., ch st*16+0/8), (.., st*16+16/24)
-          const int mi = lane >> 3;            // which 8x8 matrix this lane addresses
-          const int kr = nk * 8 + (lane & 7);  // key row
-          const int cc = (st * 16 + mi * 8) / 8;
+      for (int st = 0; st < KS; ++st) {
+        uint32_t a[4];
+        {
+          const int r = (lane & 7) + ((lane >> 3) & 1) * 8;
+          const int c = st * 2 + (lane >> 4);
+          ldmatrix_x4(a[0], a[1], a[2], a[3], sQw + r * RB + swz<D>(r, c) * 16);
+        }
+#pragma unroll
+        for (int nk = 0; nk < 4; nk += 2) {
+          // x4: (keys nk*8.., ch lo), (.., ch hi), (keys (nk+1)*8.., ch lo), (.., ch hi)
+          const int kr = nk * 8 + (lane & 7) + (lane >> 4) * 8;
+          const int cc = st * 2 + ((lane >> 3) & 1);
           uint32_t b[4];
           ldmatrix_x4(b[0], b[1], b[2], b[3], tk + kr * RB + swz<D>(kr, cc) * 16);
-          mma_bf16(sc[nk], qa[st][0], qa[st][1], qa[st][2], qa[st][3], b[0], b[1]);
-          mma_bf16(sc[nk], qa[st + 1][0], qa[st + 1][1], qa[st + 1][2], qa[st + 1][3], b[2], b[3]);
+          mma_bf16(sc[nk], a[0], a[1], a[2], a[3], b[0], b[1]);
+          mma_bf16(sc[nk + 1], a[0], a[1], a[2], a[3], b[2], b[3]);
         }
       }
       // scale to log2 domain + causal / range mask
@@ -299,7 +306,7 @@ cudaError_t launch_dense(const AttnShape& s, const KvPool& pool, int layer, cons
   const int m_tiles = (max_rows * NREP + 15) / 16;
   const int warps = m_tiles < 8 ? m_tiles : 8;
   const int row_blocks = (m_tiles + warps - 1) / warps;
-  const size_t smem = 2 * kStages * kTile * D * 2;
+  const size_t smem = 2 * kStages * kTile * D * 2 + static_cast<size_t>(warps) * 16 * D * 2;  // + Q tiles
   auto kern = dense_attn_kernel<D, NREP>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;

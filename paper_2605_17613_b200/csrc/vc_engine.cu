@@ -617,11 +617,6 @@ int bucket_rows(int M) {
   return (M + 63) / 64 * 64;
 }
 int bucket_seqs(int n) { return n == 0 ? 0 : (n + 3) / 4 * 4; }
-int bucket_pow2(int n) {
-  int b = 1;
-  while (b < n) b <<= 1;
-  return b;
-}
 }  // namespace
 
 void Engine::run_step(const std::vector<StepItem>& items, std::vector<int32_t>& out,
@@ -688,7 +683,8 @@ void Engine::run_step(const std::vector<StepItem>& items, std::vector<int32_t>& 
   const int nd = bucket_seqs(static_cast<int>(drafts.size()));
   const int n1 = bucket_seqs(static_cast<int>(dense1.size()));
   const int nv = static_cast<int>(densev.size());
-  const int mrv = nv ? bucket_pow2(max_rows_v) : 1;
+  // verify windows: bucket to multiples of 4 tokens (one 16-row MMA tile at n_rep 4)
+  const int mrv = nv ? (max_rows_v + 3) / 4 * 4 : 1;
   int k = 0;
   const AttnSeq empty{};
   for (int i = 0; i < nd; ++i) h_seqs[k++] = i < static_cast<int>(drafts.size()) ? drafts[i] : empty;
