@@ -262,13 +262,14 @@ __global__ void combine_kernel(AttnShape s, const AttnSeq* seqs, int max_chunks,
     return mode == 0 ? static_cast<size_t>(sq.part0 + c) * Hq + hq
                      : static_cast<size_t>(sq.part0 + c * sq.n_rows + tok) * Hq + hq;
   };
-  // the tail partial (draft mode) is merged last, after the chunks in order
-  const int n_all = n_parts + ((mode == 0 && sq.tail_len > 0) ? 1 : 0);
+  // draft mode: the tail-chunk partials are merged after the quantised chunks, in order
+  const int n_tail = mode == 0 ? (sq.tail_len + VC_TAIL_CHUNK - 1) / VC_TAIL_CHUNK : 0;
+  const int n_all = n_parts + n_tail;
   __shared__ float s_m[kMaxParts], s_f[kMaxParts];
   __shared__ size_t s_row[kMaxParts];
   __shared__ float s_M, s_l;
   for (int c = threadIdx.x; c < n_all; c += blockDim.x) {
-    const size_t pr = prow_of(c < n_parts ? c : max_chunks);
+    const size_t pr = prow_of(c < n_parts ? c : max_chunks + (c - n_parts));
     s_row[c] = pr;
     s_m[c] = part.ml[pr * 2];
   }

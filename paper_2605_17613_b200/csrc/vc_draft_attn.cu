@@ -93,9 +93,10 @@ __global__ void __launch_bounds__(128) draft_attn_quant_kernel(AttnShape s, Quan
   const AttnSeq sq = seqs[blockIdx.z];
   const int h = blockIdx.y;
   const int chunk = blockIdx.x;
-  const bool tail = chunk == max_chunks;
+  const bool tail = chunk >= max_chunks;              // bf16 tail chunks follow the quantised ones
+  const int t_lo = (chunk - max_chunks) * VC_TAIL_CHUNK;
   const int n_chunks = (sq.n_groups + kCG - 1) / kCG;
-  if (tail ? sq.tail_len == 0 : chunk >= n_chunks) return;
+  if (tail ? t_lo >= sq.tail_len : chunk >= n_chunks) return;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const size_t slice = (static_cast<size_t>(sq.slot) * s.layers + layer) * s.n_kv + h;
@@ -118,27 +119,52 @@ __global__ void __launch_bounds__(128) draft_attn_quant_kernel(AttnShape s, Quan
 #pragma unroll
       for (int j = 0; j < CPL; ++j) o[n][j] = 0.f;
     }
-    for (int t = warp; t < sq.tail_len; t += kWarps) {
-      float kv[CPL], vv[CPL];
+    // this warp's 8 tokens of the 32-token chunk: all loads issued up front
+    constexpr int TPW = VC_TAIL_CHUNK / kWarps;
+    const int tw = t_lo + warp * TPW;
+    const int nt = max(0, min(TPW, sq.tail_len - tw));
+    float kv[TPW][CPL], vv[TPW][CPL];
+#pragma unroll
+    for (int i = 0; i < TPW; ++i) {
+      const int t = i < nt ? tw + i : tw;  // clamp; unused when i >= nt
 #pragma unroll
       for (int j = 0; j < CPL; ++j) {
-        kv[j] = bf2f(kt[static_cast<size_t>(t) * D + lane * CPL + j]);
-        vv[j] = bf2f(vt[static_cast<size_t>(t) * D + lane * CPL + j]);
+        kv[i][j] = i < nt ? bf2f(kt[static_cast<size_t>(t) * D + lane * CPL + j]) : 0.f;
+        vv[i][j] = i < nt ? bf2f(vt[static_cast<size_t>(t) * D + lane * CPL + j]) : 0.f;
       }
+    }
+    float dots[TPW][NREP];
+#pragma unroll
+    for (int i = 0; i < TPW; ++i)
 #pragma unroll
       for (int n = 0; n < NREP; ++n) {
         float d = 0.f;
 #pragma unroll
-        for (int j = 0; j < CPL; ++j) d += sq_q[n * D + lane * CPL + j] * kv[j];
-        d = warp_sum(d);
-        const float mn = fmaxf(m[n], d);
-        const float a = exp2f(m[n] - mn);
-        const float p = exp2f(d - mn);
-        l[n] = l[n] * a + p;
-#pragma unroll
-        for (int j = 0; j < CPL; ++j) o[n][j] = o[n][j] * a + p * vv[j];
-        m[n] = mn;
+        for (int j = 0; j < CPL; ++j) d += sq_q[n * D + lane * CPL + j] * kv[i][j];
+        dots[i][n] = d;
       }
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1)  // all TPW*NREP reductions in flight together
+#pragma unroll
+      for (int i = 0; i < TPW; ++i)
+#pragma unroll
+        for (int n = 0; n < NREP; ++n) dots[i][n] += __shfl_xor_sync(0xffffffffu, dots[i][n], off);
+#pragma unroll
+    for (int n = 0; n < NREP; ++n) {
+      float mx = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < TPW; ++i)
+        if (i < nt) mx = fmaxf(mx, dots[i][n]);
+      m[n] = mx;
+      float ls = 0.f;
+#pragma unroll
+      for (int i = 0; i < TPW; ++i) {
+        const float p = i < nt ? exp2f(dots[i][n] - mx) : 0.f;
+        ls += p;
+#pragma unroll
+        for (int j = 0; j < CPL; ++j) o[n][j] += p * vv[i][j];
+      }
+      l[n] = ls;
     }
     if (lane == 0) {
 #pragma unroll
@@ -152,7 +178,7 @@ __global__ void __launch_bounds__(128) draft_attn_quant_kernel(AttnShape s, Quan
 #pragma unroll
       for (int j = 0; j < CPL; ++j) sm_o[(warp * 8 + n) * D + lane * CPL + j] = o[n][j];
     __syncthreads();
-    write_partial<D, NREP>(s, sq, h, max_chunks, sm_m, sm_l, sm_o, part);
+    write_partial<D, NREP>(s, sq, h, chunk, sm_m, sm_l, sm_o, part);
     return;
   }
 
@@ -375,7 +401,7 @@ cudaError_t launch_draft(const AttnShape& s, const QuantPool& pool, int layer, c
   auto kern = draft_attn_quant_kernel<D, BITS, NREP>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  dim3 grid(max_chunks + 1, s.n_kv, n_seq);
+  dim3 grid(draft_parts_per_seq(max_chunks, pool.tail_cap), s.n_kv, n_seq);
   kern<<<grid, kWarps * 32, smem, st>>>(s, pool, layer, qkv, seqs, max_chunks, part);
   return cudaGetLastError();
 }

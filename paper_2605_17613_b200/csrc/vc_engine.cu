@@ -267,7 +267,8 @@ void Engine::alloc_all() {
   logits_ = dmalloc<float>(static_cast<size_t>(Mmax_) * V);
   tok_in_ = dmalloc<int32_t>(Mmax_);
   tok_out_ = dmalloc<int32_t>(Mmax_);
-  const size_t prow_draft = static_cast<size_t>(cfg_.max_slots) * (max_chunks_q_ + 1);
+  const size_t prow_draft =
+      static_cast<size_t>(cfg_.max_slots + 4) * draft_parts_per_seq(max_chunks_q_, tail_cap_);
   const size_t prow_dense = static_cast<size_t>(Mmax_) * max_chunks_d_;
   const size_t prow = (prow_draft + prow_dense) * m.n_q;
   part_.o = dmalloc<float>(prow * d);
@@ -670,7 +671,7 @@ void Engine::run_step(const std::vector<StepItem>& items, std::vector<int32_t>& 
     throw ContractViolation("run_step: too many sequences");
   // partial-row offsets (units of Hq partial rows)
   int off = 0;
-  for (auto& a : drafts) { a.part0 = off; off += max_chunks_q_ + 1; }
+  for (auto& a : drafts) { a.part0 = off; off += draft_parts_per_seq(max_chunks_q_, tail_cap_); }
   for (auto& a : dense1) { a.part0 = off; off += max_chunks_d_ * a.n_rows; }
   for (auto& a : densev) { a.part0 = off; off += max_chunks_d_ * a.n_rows; }
   // Bucket the step shape (padding rows / empty sequences) so a handful of
@@ -734,6 +735,10 @@ void Engine::run_step(const std::vector<StepItem>& items, std::vector<int32_t>& 
   VC_CK(cudaEventElapsedTime(&ms, ev_a_, ev_b_));
   device_ms_ += ms;
   ++steps_;
+  static const bool step_log = std::getenv("VC_STEP_LOG") != nullptr;
+  if (step_log)
+    std::fprintf(stderr, "STEP M=%d Mb=%d drafts=%zu dense1=%zu verify=%zu rows_v=%d ms=%.3f\n", M, Mb,
+                 drafts.size(), dense1.size(), densev.size(), max_rows_v, ms);
   out.assign(h_out_, h_out_ + M);
   last_M_ = M;
 }
@@ -764,7 +769,7 @@ void Engine::kernel_bench(int kind, const std::vector<int>& slots, int reps, dou
     a.kv_len = s.committed;
     a.n_groups = s.n_groups;
     a.tail_len = s.tail_committed;
-    a.part0 = kind == 0 ? i * (max_chunks_q_ + 1) : i * max_chunks_d_;
+    a.part0 = kind == 0 ? i * draft_parts_per_seq(max_chunks_q_, tail_cap_) : i * max_chunks_d_;
     h[i] = a;
     // algorithmic bytes per (layer, request, kv-head) -- DESIGN.md §Roofline
     if (kind == 0)

@@ -7,6 +7,12 @@
 
 #define VC_QGROUP 128      // tokens per quantised K group (KIVI G)
 #define VC_DRAFT_CG 8      // quantised groups per draft-attention chunk (1024 tokens)
+#define VC_TAIL_CHUNK 32   // bf16-tail tokens per draft-attention tail CTA
+
+// Draft partial slots per sequence: the quantised chunks, then the tail chunks.
+inline int draft_parts_per_seq(int max_chunks, int tail_cap) {
+  return max_chunks + (tail_cap + VC_TAIL_CHUNK - 1) / VC_TAIL_CHUNK;
+}
 #define VC_DENSE_CHUNK 512 // keys per dense-attention chunk (absolute positions)
 
 namespace vc {
