@@ -1,5 +1,7 @@
 // vc_capi.cu -- extern "C" boundary (include/vc_api.h).  Thin: validates,
 // forwards to the engine / host algorithms, maps exceptions to status codes.
+#include <algorithm>
+#include <vector>
 #include <chrono>
 #include <cstring>
 #include <string>
@@ -227,15 +229,26 @@ int vc_compressed_read(vc_engine* e, int slot, int layer, int head, uint32_t* kc
     const auto q = en.quant_pool();
     if (en.config().quant_bits == 0) throw vc::ContractViolation("no compressed tier");
     const size_t slice = (static_cast<size_t>(slot) * m.layers + layer) * m.n_kv + head;
-    const size_t words = static_cast<size_t>(q.cap) * m.d * en.config().quant_bits / 32;
+    const int bits = en.config().quant_bits;
     const size_t groups = q.cap / VC_QGROUP;
+    const size_t rw = vc::quant_record_words(m.d, bits), uw = vc::quant_unit_words(m.d, bits);
+    const size_t ucw = vc::quant_unit_code_words(m.d, bits), gw = vc::quant_group_words(m.d, bits);
     auto cp = [&](void* dst, const void* src, size_t bytes) {
       if (dst) vc::check_cuda(cudaMemcpy(dst, src, bytes, cudaMemcpyDeviceToHost), "compressed_read");
     };
-    cp(kcodes, q.kc + slice * words, words * 4);
-    cp(vcodes, q.vc + slice * words, words * 4);
-    cp(ksz, q.ksz + slice * groups * m.d, groups * m.d * 4);
-    cp(vsz, q.vsz + slice * q.cap, static_cast<size_t>(q.cap) * 4);
+    // de-interleave the group records into the flat per-stream layout of the ABI
+    std::vector<uint32_t> recs(groups * rw);
+    cp(recs.data(), q.rec + slice * groups * rw, recs.size() * 4);
+    for (size_t g = 0; g < groups; ++g) {
+      const uint32_t* r = recs.data() + g * rw;
+      if (ksz) std::copy(r, r + m.d, ksz + g * m.d);
+      for (int u = 0; u < VC_QGROUP / VC_QUNIT; ++u) {
+        const uint32_t* ur = r + m.d + u * uw;
+        if (kcodes) std::copy(ur, ur + ucw, kcodes + g * gw + u * ucw);
+        if (vcodes) std::copy(ur + ucw, ur + 2 * ucw, vcodes + g * gw + u * ucw);
+        if (vsz) std::copy(ur + 2 * ucw, ur + 2 * ucw + VC_QUNIT, vsz + g * VC_QGROUP + u * VC_QUNIT);
+      }
+    }
     cp(ktail, q.ktail + slice * q.tail_cap * m.d, static_cast<size_t>(q.tail_cap) * m.d * 2);
     cp(vtail, q.vtail + slice * q.tail_cap * m.d, static_cast<size_t>(q.tail_cap) * m.d * 2);
   });
@@ -507,13 +520,32 @@ int vc_reload_span(int64_t bytes, double bandwidth, double iteration_time, doubl
 int vc_quant_kivi_slice(const uint16_t* k, const uint16_t* v, int n_groups, int d, int bits,
                         uint32_t* kcodes, uint32_t* ksz, uint32_t* vcodes, uint32_t* vsz, void* stream) {
   return guard([&] {
-    vc::QuantJob j{k, v, kcodes, ksz, vcodes, vsz, 0, n_groups};
-    vc::QuantJob* dj = nullptr;
+    if (n_groups <= 0) return;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const size_t rw = vc::quant_record_words(d, bits), uw = vc::quant_unit_words(d, bits);
+    const size_t ucw = vc::quant_unit_code_words(d, bits), gw = vc::quant_group_words(d, bits);
+    uint32_t* rec = nullptr;
+    vc::QuantJob* dj = nullptr;
+    vc::check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&rec), n_groups * rw * 4, st), "malloc");
+    vc::QuantJob j{k, v, rec, 0, n_groups};
     vc::check_cuda(cudaMallocAsync(reinterpret_cast<void**>(&dj), sizeof(j), st), "malloc");
     vc::check_cuda(cudaMemcpyAsync(dj, &j, sizeof(j), cudaMemcpyHostToDevice, st), "memcpy");
     vc::check_cuda(vc::quant_kivi(dj, 1, n_groups, d, bits, st), "quant_kivi");
+    // group records -> the flat per-stream layout of this entry point
+    auto cp2d = [&](uint32_t* dst, size_t dpitch, const uint32_t* src, size_t width) {
+      if (dst)
+        vc::check_cuda(cudaMemcpy2DAsync(dst, dpitch * 4, src, rw * 4, width * 4, n_groups,
+                                         cudaMemcpyDeviceToDevice, st), "memcpy2d");
+    };
+    cp2d(ksz, d, rec, d);
+    for (int u = 0; u < VC_QGROUP / VC_QUNIT; ++u) {
+      const uint32_t* ur = rec + d + u * uw;
+      cp2d(kcodes ? kcodes + u * ucw : nullptr, gw, ur, ucw);
+      cp2d(vcodes ? vcodes + u * ucw : nullptr, gw, ur + ucw, ucw);
+      cp2d(vsz ? vsz + u * VC_QUNIT : nullptr, VC_QGROUP, ur + 2 * ucw, VC_QUNIT);
+    }
     vc::check_cuda(cudaFreeAsync(dj, st), "free");
+    vc::check_cuda(cudaFreeAsync(rec, st), "free");
     vc::check_cuda(cudaStreamSynchronize(st), "sync");
   });
 }

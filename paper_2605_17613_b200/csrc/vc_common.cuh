@@ -17,6 +17,17 @@ VC_DEV uint16_t f2h(float f) { return __half_as_ushort(__float2half_rn(f)); }
 VC_DEV uint32_t pack_h2(float lo, float hi) {
   return static_cast<uint32_t>(f2h(lo)) | (static_cast<uint32_t>(f2h(hi)) << 16);
 }
+VC_DEV float2 h2_to_f2(uint32_t h) {
+  __half2 v;
+  memcpy(&v, &h, 4);
+  return __half22float2(v);
+}
+// 2^x on the SFU (MUFU.EX2), flushing subnormals; ex2(-inf) = +0
+VC_DEV float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 VC_DEV uint32_t pack_bf2(float lo, float hi) {
   return static_cast<uint32_t>(f2bf(lo)) | (static_cast<uint32_t>(f2bf(hi)) << 16);
 }

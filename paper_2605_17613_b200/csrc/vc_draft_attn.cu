@@ -29,7 +29,8 @@ namespace {
 constexpr int kG = VC_QGROUP;
 constexpr int kCG = VC_DRAFT_CG;
 constexpr int kWarps = 4;
-constexpr int kUnit = 64;  // tokens per pipeline unit (half a K group)
+constexpr int kUnit = VC_QUNIT;  // tokens per pipeline unit = one unit record
+constexpr float kTau = 8.0f;      // lazy rescale: running max may lag the true max by 2^8
 
 template <int D, int BITS>
 struct Geo {
@@ -38,11 +39,17 @@ struct Geo {
   static constexpr int CH = W < 4 ? W : 4;
   static constexpr int UMT = kUnit / 16;               // 16-token tiles per unit
   static constexpr int UW = UMT * W * 32;              // u32 of K (or V) codes per unit
-  // stage layout (u32): [K codes UW][V codes UW][vsz kUnit][ksz D]
-  static constexpr int OFF_V = UW;
-  static constexpr int OFF_VSZ = 2 * UW;
-  static constexpr int OFF_KSZ = 2 * UW + kUnit;
-  static constexpr int STAGE = 2 * UW + kUnit + D;     // u32
+  static constexpr int UREC = static_cast<int>(quant_unit_words(D, BITS));
+  static constexpr int GREC = static_cast<int>(quant_record_words(D, BITS));
+  static_assert(UW == static_cast<int>(quant_unit_code_words(D, BITS)), "unit geometry");
+  // stage (u32) mirrors the group record: [ksz D][K codes UW][V codes UW][vsz kUnit];
+  // the ksz slot is filled by the first unit of each group only
+  static constexpr int OFF_KSZ = 0;
+  static constexpr int OFF_K = D;
+  static constexpr int OFF_V = D + UW;
+  static constexpr int OFF_VSZ = D + 2 * UW;
+  static constexpr int STAGE = D + UREC;
+  static_assert((STAGE * 4) % 16 == 0 && (D * 4) % 16 == 0, "TMA bulk alignment");
 };
 
 template <int D, int NREP>
@@ -81,7 +88,6 @@ __global__ void __launch_bounds__(128) draft_attn_quant_kernel(AttnShape s, Quan
   static_assert(NREP <= 8, "n_rep > 8 needs two head tiles");
   using GEO = Geo<D, BITS>;
   constexpr int KS = GEO::KS, W = GEO::W, CH = GEO::CH, UMT = GEO::UMT;
-  constexpr size_t GW = static_cast<size_t>(kG) * D * BITS / 32;  // u32 per group
   constexpr uint32_t MASK = BITS == 4 ? 0x000f000fu : 0x00030003u;
 
   extern __shared__ __align__(128) uint32_t dsm[];   // [kWarps][2][STAGE]
@@ -182,32 +188,48 @@ __global__ void __launch_bounds__(128) draft_attn_quant_kernel(AttnShape s, Quan
     return;
   }
 
-  // ---- quantised groups: per-warp TMA pipeline over 64-token units ----------
-  const uint32_t* kc = pool.kc + slice * (static_cast<size_t>(pool.cap) * D * BITS / 32);
-  const uint32_t* vc = pool.vc + slice * (static_cast<size_t>(pool.cap) * D * BITS / 32);
-  const uint32_t* ksz = pool.ksz + slice * (static_cast<size_t>(pool.cap / kG) * D);
-  const uint32_t* vsz = pool.vsz + slice * static_cast<size_t>(pool.cap);
+  // ---- quantised groups: per-warp TMA pipeline over kUnit-token units --------
+  const uint32_t* recs = pool.rec + slice * (static_cast<size_t>(pool.cap / kG) * GEO::GREC);
   uint32_t* stage0 = dsm + static_cast<size_t>(warp) * 2 * GEO::STAGE;
   uint64_t* bar = bars[warp];
 
-  // this warp's groups: chunk*kCG + warp, + kWarps, ... ; two units each
+  // this warp's groups: chunk*kCG + warp, + kWarps, ... ; kUPG units each
+  constexpr int kUPG = kG / kUnit;
   const int g_first = chunk * kCG + warp;
   const int g_end = min((chunk + 1) * kCG, sq.n_groups);
   const int n_mine = g_first < g_end ? (g_end - g_first + kWarps - 1) / kWarps : 0;
-  const int n_units = 2 * n_mine;
+  const int n_units = kUPG * n_mine;
 
-  auto issue = [&](int u, int st) {  // lane 0 only
-    const int g = g_first + (u >> 1) * kWarps;
-    const int half = u & 1;
+  auto issue = [&](int u, int st) {  // lane 0 only: one bulk copy per unit
+    const int g = g_first + (u / kUPG) * kWarps;
+    const int part = u % kUPG;
+    const uint32_t* src = recs + static_cast<size_t>(g) * GEO::GREC;
     uint32_t* dst = stage0 + st * GEO::STAGE;
-    const uint32_t bytes_codes = GEO::UW * 4;
-    const uint32_t bytes = 2 * bytes_codes + kUnit * 4 + (half == 0 ? D * 4 : 0);
-    mbar_expect_tx(bar + st, bytes);
-    tma_load_1d(dst, kc + static_cast<size_t>(g) * GW + half * GEO::UW, bytes_codes, bar + st);
-    tma_load_1d(dst + GEO::OFF_V, vc + static_cast<size_t>(g) * GW + half * GEO::UW, bytes_codes, bar + st);
-    tma_load_1d(dst + GEO::OFF_VSZ, vsz + static_cast<size_t>(g) * kG + half * kUnit, kUnit * 4, bar + st);
-    if (half == 0) tma_load_1d(dst + GEO::OFF_KSZ, ksz + static_cast<size_t>(g) * D, D * 4, bar + st);
+    if (part == 0) {
+      mbar_expect_tx(bar + st, GEO::STAGE * 4);
+      tma_load_1d(dst, src, GEO::STAGE * 4, bar + st);
+    } else {
+      mbar_expect_tx(bar + st, GEO::UREC * 4);
+      tma_load_1d(dst + GEO::OFF_K, src + D + part * GEO::UREC, GEO::UREC * 4, bar + st);
+    }
   };
+  // A-fragment registers of one code word.  int4: one shift + four lop3,
+  // pairs 2/3 (k or token +8) arrive as 1024 + 16c -- their B operand carries
+  // the matching 1/16.  int2: word holds two k-steps, sub selects one.
+  auto unpack = [&](uint32_t w, int sub, uint32_t* a) {
+    if constexpr (BITS == 4) {
+      const uint32_t w8 = w >> 8;
+      a[0] = nib_to_h2(w, 0x000f000fu);
+      a[1] = nib_to_h2(w8, 0x000f000fu);
+      a[2] = nib_to_h2(w, 0x00f000f0u);
+      a[3] = nib_to_h2(w8, 0x00f000f0u);
+    } else {
+      const int sh = 8 * sub;
+#pragma unroll
+      for (int j = 0; j < 4; ++j) a[j] = nib_to_h2(w >> (sh + j * BITS), MASK);
+    }
+  };
+  constexpr float kHiScale = BITS == 4 ? 0.0625f : 1.0f;  // B-operand scale of pairs 2/3
   if (lane == 0) {
     mbar_init(bar + 0, 1);
     mbar_init(bar + 1, 1);
@@ -233,26 +255,28 @@ __global__ void __launch_bounds__(128) draft_attn_quant_kernel(AttnShape s, Quan
     const int st = u & 1;
     mbar_wait(bar + st, (u >> 1) & 1);
     const uint32_t* sb = stage0 + st * GEO::STAGE;
-    if ((u & 1) == 0) {
+    if (u % kUPG == 0) {
       // new group: q' = q * kscale as fp16 B fragments; per-head constant term
       float bias_part = 0.f;
+      const float* qh = sq_q + (hn < NREP ? hn : 0) * D;
+      const float qmask = hn < NREP ? 1.f : 0.f;  // padding head columns feed zeros
 #pragma unroll
       for (int k = 0; k < KS; ++k) {
         const int c0 = k * 16 + 2 * (lane & 3);
-        const int cs[4] = {c0, c0 + 1, c0 + 8, c0 + 9};
-        float qp[4];
 #pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const uint32_t sz = sb[GEO::OFF_KSZ + cs[e]];
-          const float sc = h2f(static_cast<uint16_t>(sz & 0xffffu));
-          const float zr = h2f(static_cast<uint16_t>(sz >> 16));
-          const float q = hn < NREP ? sq_q[hn * D + cs[e]] : 0.f;  // padding head columns
-          qp[e] = q * sc;
+        for (int hi = 0; hi < 2; ++hi) {  // channels c0,c0+1 then c0+8,c0+9
+          const int c = c0 + 8 * hi;
+          const uint2 sz = *reinterpret_cast<const uint2*>(sb + GEO::OFF_KSZ + c);
+          const float2 sz0 = h2_to_f2(sz.x), sz1 = h2_to_f2(sz.y);  // (scale, zero)
+          const float2 q = *reinterpret_cast<const float2*>(qh + c);
+          const float q0 = q.x * qmask, q1 = q.y * qmask;
+          const float f = hi ? kHiScale : 1.0f;
+          const uint32_t bq = pack_h2(q0 * sz0.x * f, q1 * sz1.x * f);
           // zero point and the -1024 fold use the fp16-rounded q' the MMA sees
-          bias_part += q * zr - 1024.f * h2f(f2h(qp[e]));
+          const float2 qr = h2_to_f2(bq);
+          bias_part += q0 * sz0.y + q1 * sz1.y - 1024.f * (qr.x + qr.y);
+          (hi ? b1 : b0)[k] = bq;
         }
-        b0[k] = pack_h2(qp[0], qp[1]);
-        b1[k] = pack_h2(qp[2], qp[3]);
       }
       bias_part += __shfl_xor_sync(0xffffffffu, bias_part, 1);
       bias_part += __shfl_xor_sync(0xffffffffu, bias_part, 2);
@@ -260,14 +284,14 @@ __global__ void __launch_bounds__(128) draft_attn_quant_kernel(AttnShape s, Quan
       bias1 = __shfl_sync(0xffffffffu, bias_part, (hc0 + 1) * 4);
     }
 
-    // S^T tiles of the unit's 64 tokens
+    // S^T tiles of the unit's kUnit tokens
     float sacc[UMT][4];
 #pragma unroll
     for (int m = 0; m < UMT; ++m) {
       uint32_t kw[W];
 #pragma unroll
       for (int wq = 0; wq < W / CH; ++wq) {
-        const uint32_t* p = sb + (static_cast<size_t>(m * (W / CH) + wq) * 32 + lane) * CH;
+        const uint32_t* p = sb + GEO::OFF_K + (static_cast<size_t>(m * (W / CH) + wq) * 32 + lane) * CH;
         if constexpr (CH == 4) {
           const uint4 v = lds128(p);
           kw[wq * 4 + 0] = v.x; kw[wq * 4 + 1] = v.y; kw[wq * 4 + 2] = v.z; kw[wq * 4 + 3] = v.w;
@@ -279,13 +303,9 @@ __global__ void __launch_bounds__(128) draft_attn_quant_kernel(AttnShape s, Quan
       sacc[m][0] = sacc[m][1] = sacc[m][2] = sacc[m][3] = 0.f;
 #pragma unroll
       for (int k = 0; k < KS; ++k) {
-        const uint32_t w = (BITS == 4) ? kw[k] : kw[k >> 1];
-        const int sh = (BITS == 4) ? 0 : 8 * (k & 1);
-        const uint32_t a0 = nib_to_h2(w >> (sh + 0 * BITS), MASK);
-        const uint32_t a1 = nib_to_h2(w >> (sh + 1 * BITS), MASK);
-        const uint32_t a2 = nib_to_h2(w >> (sh + 2 * BITS), MASK);
-        const uint32_t a3 = nib_to_h2(w >> (sh + 3 * BITS), MASK);
-        mma_f16(sacc[m], a0, a1, a2, a3, b0[k], b1[k]);
+        uint32_t a[4];
+        unpack((BITS == 4) ? kw[k] : kw[k >> 1], k & 1, a);
+        mma_f16(sacc[m], a[0], a[1], a[2], a[3], b0[k], b1[k]);
       }
       sacc[m][0] += bias0; sacc[m][1] += bias1; sacc[m][2] += bias0; sacc[m][3] += bias1;
     }
@@ -302,14 +322,18 @@ __global__ void __launch_bounds__(128) draft_attn_quant_kernel(AttnShape s, Quan
       gm0 = fmaxf(gm0, __shfl_xor_sync(0xffffffffu, gm0, o));
       gm1 = fmaxf(gm1, __shfl_xor_sync(0xffffffffu, gm1, o));
     }
-    const float mn0 = fmaxf(mrun0, gm0), mn1 = fmaxf(mrun1, gm1);
-    const float al0 = exp2f(mrun0 - mn0), al1 = exp2f(mrun1 - mn1);
-    mrun0 = mn0;
-    mrun1 = mn1;
-    lsum0 *= al0; lsum1 *= al1; corr0 *= al0; corr1 *= al1;
+    // lazy rescale: keep the running max unless a column's max outgrew it by
+    // more than kTau (p <= 2^kTau then), so most units skip the O rescale
+    if (__any_sync(0xffffffffu, gm0 > mrun0 + kTau || gm1 > mrun1 + kTau)) {
+      const float mn0 = fmaxf(mrun0, gm0), mn1 = fmaxf(mrun1, gm1);
+      const float al0 = ex2(mrun0 - mn0), al1 = ex2(mrun1 - mn1);
+      mrun0 = mn0;
+      mrun1 = mn1;
+      lsum0 *= al0; lsum1 *= al1; corr0 *= al0; corr1 *= al1;
 #pragma unroll
-    for (int ct = 0; ct < KS; ++ct) {
-      oacc[ct][0] *= al0; oacc[ct][1] *= al1; oacc[ct][2] *= al0; oacc[ct][3] *= al1;
+      for (int ct = 0; ct < KS; ++ct) {
+        oacc[ct][0] *= al0; oacc[ct][1] *= al1; oacc[ct][2] *= al0; oacc[ct][3] *= al1;
+      }
     }
     uint32_t bp0[UMT], bp1[UMT];
 #pragma unroll
@@ -318,12 +342,12 @@ __global__ void __launch_bounds__(128) draft_attn_quant_kernel(AttnShape s, Quan
       const uint32_t sz_a = sb[GEO::OFF_VSZ + r], sz_b = sb[GEO::OFF_VSZ + r + 8];
       const float vs_a = h2f(static_cast<uint16_t>(sz_a & 0xffffu)), vz_a = h2f(static_cast<uint16_t>(sz_a >> 16));
       const float vs_b = h2f(static_cast<uint16_t>(sz_b & 0xffffu)), vz_b = h2f(static_cast<uint16_t>(sz_b >> 16));
-      const float p0 = exp2f(sacc[m][0] - mn0), p1 = exp2f(sacc[m][1] - mn1);
-      const float p2 = exp2f(sacc[m][2] - mn0), p3 = exp2f(sacc[m][3] - mn1);
+      const float p0 = ex2(sacc[m][0] - mrun0), p1 = ex2(sacc[m][1] - mrun1);
+      const float p2 = ex2(sacc[m][2] - mrun0), p3 = ex2(sacc[m][3] - mrun1);
       lsum0 += p0 + p2;
       lsum1 += p1 + p3;
       const uint32_t pk01 = pack_h2(p0 * vs_a, p1 * vs_a);
-      const uint32_t pk23 = pack_h2(p2 * vs_b, p3 * vs_b);
+      const uint32_t pk23 = pack_h2(p2 * vs_b * kHiScale, p3 * vs_b * kHiScale);  // tokens +8
       const __half2 h01 = *reinterpret_cast<const __half2*>(&pk01);
       const __half2 h23 = *reinterpret_cast<const __half2*>(&pk23);
       corr0 += p0 * vz_a + p2 * vz_b - 1024.f * (__low2float(h01) + __low2float(h23));
@@ -349,13 +373,9 @@ __global__ void __launch_bounds__(128) draft_attn_quant_kernel(AttnShape s, Quan
       }
 #pragma unroll
       for (int ct = 0; ct < KS; ++ct) {
-        const uint32_t w = (BITS == 4) ? vw[ct] : vw[ct >> 1];
-        const int sh = (BITS == 4) ? 0 : 8 * (ct & 1);
-        const uint32_t a0 = nib_to_h2(w >> (sh + 0 * BITS), MASK);
-        const uint32_t a1 = nib_to_h2(w >> (sh + 1 * BITS), MASK);
-        const uint32_t a2 = nib_to_h2(w >> (sh + 2 * BITS), MASK);
-        const uint32_t a3 = nib_to_h2(w >> (sh + 3 * BITS), MASK);
-        mma_f16(oacc[ct], a0, a1, a2, a3, bp0[m], bp1[m]);
+        uint32_t a[4];
+        unpack((BITS == 4) ? vw[ct] : vw[ct >> 1], ct & 1, a);
+        mma_f16(oacc[ct], a[0], a[1], a[2], a[3], bp0[m], bp1[m]);
       }
     }
     fence_proxy_async();  // LDS reads of the stage before the next TMA write into it

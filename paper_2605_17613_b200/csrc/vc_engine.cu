@@ -94,7 +94,7 @@ Engine::~Engine() {
   for (auto& [k, g] : graphs_) cudaGraphExecDestroy(g);
   for (auto& [k, e] : xfers_) cudaEventDestroy(e);
   void* ptrs[] = {weight_blob_, rope_cos_, rope_sin_, full_.k, full_.v, stage_.k, stage_.v,
-                  quant_.kc, quant_.ksz, quant_.vc, quant_.vsz, quant_.ktail, quant_.vtail,
+                  quant_.rec, quant_.ktail, quant_.vtail,
                   x_, xn_, qkv_, attn_, act_, gws_.partial, gws_.counters, ss_part_, logits_,
                   tok_in_, tok_out_, part_.o, part_.ml, rows_dev_, seqs_dev_, jobs_dev_};
   for (void* p : ptrs)
@@ -230,11 +230,7 @@ void Engine::alloc_all() {
     const int capq = cfg_.max_ctx / VC_QGROUP * VC_QGROUP;
     quant_.cap = capq;
     quant_.tail_cap = tail_cap_;
-    const size_t words = static_cast<size_t>(capq) * d * cfg_.quant_bits / 32;
-    quant_.kc = dmalloc<uint32_t>(slices * words);
-    quant_.vc = dmalloc<uint32_t>(slices * words);
-    quant_.ksz = dmalloc<uint32_t>(slices * (capq / VC_QGROUP) * d);
-    quant_.vsz = dmalloc<uint32_t>(slices * capq);
+    quant_.rec = dmalloc<uint32_t>(slices * (capq / VC_QGROUP) * quant_record_words(d, cfg_.quant_bits));
     quant_.ktail = dmalloc<uint16_t>(slices * tail_cap_ * d);
     quant_.vtail = dmalloc<uint16_t>(slices * tail_cap_ * d);
     max_chunks_q_ = (capq / VC_QGROUP + VC_DRAFT_CG - 1) / VC_DRAFT_CG;
@@ -467,17 +463,14 @@ void Engine::quantise_groups(int slot, int g0, int ng, const KvPool& src, int sr
   const int n_slices = m.layers * m.n_kv;
   QuantJob* jobs = reinterpret_cast<QuantJob*>(static_cast<uint8_t*>(h_desc_) + desc_bytes_ -
                                                static_cast<size_t>(n_slices) * sizeof(QuantJob));
-  const size_t words = static_cast<size_t>(quant_.cap) * m.d * cfg_.quant_bits / 32;
+  const size_t slice_words = static_cast<size_t>(quant_.cap / VC_QGROUP) * quant_record_words(m.d, cfg_.quant_bits);
   for (int i = 0; i < n_slices; ++i) {
     const size_t ss = static_cast<size_t>(src_slot) * n_slices + i;
     const size_t ds = static_cast<size_t>(slot) * n_slices + i;
     QuantJob j;
     j.k = src.k + ss * static_cast<size_t>(src.cap) * m.d;
     j.v = src.v + ss * static_cast<size_t>(src.cap) * m.d;
-    j.kc = quant_.kc + ds * words;
-    j.vc = quant_.vc + ds * words;
-    j.ksz = quant_.ksz + ds * (quant_.cap / VC_QGROUP) * m.d;
-    j.vsz = quant_.vsz + ds * static_cast<size_t>(quant_.cap);
+    j.rec = quant_.rec + ds * slice_words;
     j.g0 = g0;
     j.ng = ng;
     jobs[i] = j;

@@ -23,10 +23,7 @@ namespace vc {
 struct QuantJob {
   const uint16_t* k;  // bf16 source rows, token 0 of group 0
   const uint16_t* v;
-  uint32_t* kc;   // K codes  (fragment order, u32 words), group 0
-  uint32_t* ksz;  // K (scale,zero) fp16 pairs [groups][d]
-  uint32_t* vc;   // V codes
-  uint32_t* vsz;  // V (scale,zero) fp16 pairs [tokens]
+  uint32_t* rec;      // the slice's group records (quant_record_words each), group 0
   int g0, ng;
 };
 cudaError_t quant_kivi(const QuantJob* jobs_dev, int n_jobs, int max_groups, int d, int bits,
@@ -35,6 +32,21 @@ cudaError_t quant_kivi(const QuantJob* jobs_dev, int n_jobs, int max_groups, int
 // u32 words of one quantised group (K or V): G*d*bits/32.
 inline constexpr size_t quant_group_words(int d, int bits) {
   return static_cast<size_t>(VC_QGROUP) * d * bits / 32;
+}
+// Quantised group record, the unit one draft-attention TMA copy streams
+// (DESIGN.md "Compressed KV layout"), in u32 words:
+//   [ksz: d (scale,zero) fp16 pairs]
+//   G/VC_QUNIT unit records: [K codes U*d*bits/32][V codes U*d*bits/32][vsz: U pairs]
+// Codes inside a unit record are in mma.sync A-fragment order (vc_quant.cu).
+#define VC_QUNIT 32  // tokens per unit record
+inline constexpr size_t quant_unit_code_words(int d, int bits) {
+  return static_cast<size_t>(VC_QUNIT) * d * bits / 32;
+}
+inline constexpr size_t quant_unit_words(int d, int bits) {
+  return 2 * quant_unit_code_words(d, bits) + VC_QUNIT;
+}
+inline constexpr size_t quant_record_words(int d, int bits) {
+  return static_cast<size_t>(d) + (VC_QGROUP / VC_QUNIT) * quant_unit_words(d, bits);
 }
 
 // ------------------------------------------------------------ attention I/O
@@ -56,11 +68,8 @@ struct KvPool {        // bf16 [slot][layer][head][cap][d]
   int cap;             // token capacity per slice
 };
 
-struct QuantPool {     // per slice: kc/vc words, ksz [groups][d], vsz [cap]
-  uint32_t* kc;
-  uint32_t* ksz;
-  uint32_t* vc;
-  uint32_t* vsz;
+struct QuantPool {     // per slice: cap/G group records, then the bf16 tail
+  uint32_t* rec;       // [slice][cap/G][quant_record_words]
   uint16_t* ktail;     // bf16 [slice][tail_cap][d]
   uint16_t* vtail;
   int cap;             // token capacity of the quantised region (multiple of G)

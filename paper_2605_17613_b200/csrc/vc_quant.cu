@@ -17,6 +17,8 @@ namespace vc {
 namespace {
 
 constexpr int kG = VC_QGROUP;  // tokens per K group
+// bit offset of fragment pair j (a0a1, a2a3, a4a5, a6a7) inside an int4 word
+__device__ constexpr int kNibble[4] = {0, 8, 4, 12};
 
 VC_DEV uint32_t quant_code(float x, float sf, float zf, int qmax) {
   if (sf == 0.0f) return 0u;
@@ -47,6 +49,9 @@ __global__ void __launch_bounds__(128) quant_kivi_kernel(const QuantJob* __restr
   float* vzero = vscale + kG;                              // [kG]
   const int tid = threadIdx.x;
   constexpr int QMAX = (1 << BITS) - 1;
+  constexpr int UCW = static_cast<int>(quant_unit_code_words(D, BITS));  // codes of one unit
+  constexpr int UREC = static_cast<int>(quant_unit_words(D, BITS));
+  uint32_t* rec = job.rec + static_cast<size_t>(g) * quant_record_words(D, BITS);
 
   // 1. stage the group's bf16 K and V rows (contiguous: kG*D elements each)
   const uint4* srck = reinterpret_cast<const uint4*>(job.k + static_cast<size_t>(g) * kG * D);
@@ -71,7 +76,7 @@ __global__ void __launch_bounds__(128) quant_kivi_kernel(const QuantJob* __restr
     uint16_t s16 = f2h(sc), z16 = f2h(mn);
     kscale[c] = h2f(s16);
     kzero[c] = h2f(z16);
-    job.ksz[static_cast<size_t>(g) * D + c] = static_cast<uint32_t>(s16) | (static_cast<uint32_t>(z16) << 16);
+    rec[c] = static_cast<uint32_t>(s16) | (static_cast<uint32_t>(z16) << 16);
   }
   // 3. V: per-token min/max over the head's channels
   for (int t = tid; t < kG; t += 128) {
@@ -86,7 +91,8 @@ __global__ void __launch_bounds__(128) quant_kivi_kernel(const QuantJob* __restr
     uint16_t s16 = f2h(sc), z16 = f2h(mn);
     vscale[t] = h2f(s16);
     vzero[t] = h2f(z16);
-    job.vsz[static_cast<size_t>(g) * kG + t] = static_cast<uint32_t>(s16) | (static_cast<uint32_t>(z16) << 16);
+    rec[D + (t / VC_QUNIT) * UREC + 2 * UCW + t % VC_QUNIT] =
+        static_cast<uint32_t>(s16) | (static_cast<uint32_t>(z16) << 16);
   }
   __syncthreads();
 
@@ -96,8 +102,7 @@ __global__ void __launch_bounds__(128) quant_kivi_kernel(const QuantJob* __restr
   constexpr int CH = W < 4 ? W : 4;            // u32 per vector load
   constexpr int MT = kG / 16;
   constexpr int TOTAL = MT * W * 32;           // u32 per group (K or V)
-  uint32_t* kc = job.kc + static_cast<size_t>(g) * TOTAL;
-  uint32_t* vc = job.vc + static_cast<size_t>(g) * TOTAL;
+  static_assert(TOTAL % UCW == 0, "unit records split the group's code stream");
   for (int idx = tid; idx < TOTAL; idx += 128) {
     // idx = ((m * (W/CH) + w/CH) * 32 + lane) * CH + w%CH
     const int wl = idx % CH;
@@ -115,7 +120,10 @@ __global__ void __launch_bounds__(128) quant_kivi_kernel(const QuantJob* __restr
         for (int e = 0; e < 2; ++e) {
           int r, c;
           frag_rc(lane, j, e, r, c);
-          const int shift = (BITS == 4) ? (4 * j + 16 * e) : (8 * sub + 2 * j + 16 * e);
+          // int4: pairs 0,1 sit in the low nibble of bytes 0/1 (and 2/3), pairs
+          // 2,3 in the high nibbles, so the consumer unpacks a word with one
+          // shift + four lop3 (high nibbles arrive x16, folded into its B operand)
+          const int shift = (BITS == 4) ? (kNibble[j] + 16 * e) : (8 * sub + 2 * j + 16 * e);
           // K tile: rows = tokens (m), cols = channels (s)
           const int tk = m * 16 + r, ck = s * 16 + c;
           kword |= quant_code(bf2f(sk[tk * D + ck]), kscale[ck], kzero[ck], QMAX) << shift;
@@ -125,8 +133,10 @@ __global__ void __launch_bounds__(128) quant_kivi_kernel(const QuantJob* __restr
         }
       }
     }
-    kc[idx] = kword;
-    vc[idx] = vword;
+    // the group's code stream idx is m-tile major, so unit idx / UCW holds it
+    uint32_t* urec = rec + D + (idx / UCW) * UREC + idx % UCW;
+    urec[0] = kword;
+    urec[UCW] = vword;
   }
 }
 

@@ -174,7 +174,8 @@ def frag_map(d: int, bits: int, G: int = 128):
                         for e in range(2):
                             r = lane // 4 + (8 if j & 1 else 0)
                             c = 2 * (lane % 4) + e + (8 if j & 2 else 0)
-                            sh = 4 * j + 16 * e if bits == 4 else 8 * sub + 2 * j + 16 * e
+                            # int4: pairs 0,1 in low nibbles, 2,3 in high (vc_quant.cu kNibble)
+                            sh = (0, 8, 4, 12)[j] + 16 * e if bits == 4 else 8 * sub + 2 * j + 16 * e
                             widx.append(idx)
                             shift.append(sh)
                             a_r.append(m * 16 + r)   # tile row -> token (K) / tok-step rows

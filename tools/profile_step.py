@@ -24,12 +24,14 @@ def main():
     p.add_argument("--ctx", type=int, default=32768)
     p.add_argument("--x", type=int, default=16)
     p.add_argument("--graphs", type=int, default=1)
+    p.add_argument("--q-std", type=float, default=0.0)
+    p.add_argument("--resid-std", type=float, default=0.0)
     a = p.parse_args()
     B, x = a.batch, a.x
     comp = a.mode != "decode"
     e = vc.Engine(vc.LLAMA3_8B, max_slots=B, max_ctx=a.ctx + 256, max_x=x, quant_bits=4 if comp else 0,
                   max_verify=2, use_graphs=bool(a.graphs))
-    e.init_weights(0, 0.02)
+    e.init_weights(0, 0.02, resid_std=a.resid_std, q_std=a.q_std)
     for i in range(B):
         e.add_synthetic(i, a.ctx, 100 + i, seed=1 + i)
         if comp:
@@ -37,6 +39,7 @@ def main():
     if comp:  # open a draft round of x tokens on request 0 so it can verify
         for _ in range(x):
             e.draft([0])
+    e.timing(reset=True)
     for _ in range(a.steps):
         if a.mode == "decode":
             e.decode_step(list(range(B)))
