@@ -1,12 +1,16 @@
 // vc_draft_attn.cu -- draft decode attention over the KIVI-compressed cache.
 //
 // One query token per drafting sequence, n_rep query heads per kv head (GQA).
-// HBM-bound: every code byte is read exactly once.  Each warp runs its own
-// two-stage TMA pipeline: one lane issues 1-D bulk copies
-// (cp.async.bulk ... mbarrier::complete_tx) of the next 64-token unit --
-// K codes, V codes, V scale/zero, and per group the K scale/zero -- into
-// shared memory while the warp computes on the previous unit, so the memory
-// system sees ~9 KB in flight per warp without holding registers for it.
+// HBM-bound: every code byte is read exactly once.  The kernel is persistent
+// (one wave) and splits the step's (sequence, kv head, group) tasks into equal
+// contiguous ranges, one per warp (draft_task_begin, vc_kernels.h), so every
+// warp streams the same bytes whatever the batch's context lengths.  Each warp
+// runs its own two-stage TMA pipeline: one lane issues ONE 1-D bulk copy
+// (cp.async.bulk ... mbarrier::complete_tx) per 32-token unit record -- K
+// codes, V codes, V scale/zero, and for a group's first unit the K
+// scale/zero (vc_kernels.h quant_record_words) -- into shared memory while the
+// warp computes on the previous unit; the stream runs on across group and
+// head boundaries, so a warp never drains its pipeline until its range ends.
 // The math runs on legacy mma.sync tensor-core tiles fed from LDS:
 //   S^T[tok, head] = Kcodes[tok, ch] . q'^T[ch, head],  q' = q * kscale (per group)
 //   O^T[ch, head]  = Vcodes^T[ch, tok] . P'^T[tok, head], P' = P * vscale (per token)
@@ -15,8 +19,9 @@
 // the inner loop is lop3 + mma only.  Codes are stored in mma A-fragment
 // order (vc_quant.cu), the P' B-fragments come from the S C-fragments through
 // movmatrix.trans, and the online softmax runs on warp shuffles.
-// Split-K over 1024-token chunks + one bf16-tail CTA; attention_combine
-// merges the partials (LSE) in chunk order.
+// A warp emits one partial (m, l, O) per (sequence, head) it touches, the
+// bf16 tail (residual group + draft window) runs in separate 32-token CTAs,
+// and attention_combine merges the partials (LSE) in token order.
 //
 // The reference models this step as a pure HBM read of the compressed cache
 // (/root/reference/proj/src/scheduler.cpp:452-457, sim.cpp:254-256).
@@ -27,8 +32,10 @@ namespace vc {
 namespace {
 
 constexpr int kG = VC_QGROUP;
-constexpr int kCG = VC_DRAFT_CG;
 constexpr int kWarps = 4;
+#ifndef VC_DRAFT_MINB
+#define VC_DRAFT_MINB 4  // resident CTAs/SM the n_rep<=4 register budget targets
+#endif
 constexpr int kUnit = VC_QUNIT;  // tokens per pipeline unit = one unit record
 constexpr float kTau = 8.0f;      // lazy rescale: running max may lag the true max by 2^8
 
@@ -52,181 +59,244 @@ struct Geo {
   static_assert((STAGE * 4) % 16 == 0 && (D * 4) % 16 == 0, "TMA bulk alignment");
 };
 
+
+// Sum over sequences [0, n) of the group tasks (n_groups * n_kv); all lanes get it.
+VC_DEV int warp_task_sum(const AttnSeq* seqs, int n, int n_kv, int lane) {
+  int acc = 0;
+  for (int i = lane; i < n; i += 32) acc += seqs[i].n_groups * n_kv;
+  return __reduce_add_sync(0xffffffffu, acc);
+}
+
 template <int D, int NREP>
-VC_DEV void write_partial(const AttnShape& s, const AttnSeq& sq, int h, int chunk, float* sm_m,
-                          float* sm_l, float* sm_o, Partials part) {
-  // sm_m/sm_l: [kWarps][8]; sm_o: [kWarps][8][D]
-  const int hq0 = h * NREP;
+__device__ void draft_tail(const AttnShape& s, const QuantPool& pool, int layer, const uint16_t* qkv,
+                           const AttnSeq& sq, int h, int tc, int max_chunks, Partials part,
+                           float* sm_o, float* sq_q) {
+  // ---- bf16 tail (residual group + draft window), CUDA cores ----------
+  __shared__ float sm_m[kWarps * 8], sm_l[kWarps * 8];
+  constexpr int CPL = D / 32;  // channels per lane
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int t_lo = tc * VC_TAIL_CHUNK;
+  const size_t slice = (static_cast<size_t>(sq.slot) * s.layers + layer) * s.n_kv + h;
+  const uint16_t* kt = pool.ktail + slice * pool.tail_cap * D;
+  const uint16_t* vt = pool.vtail + slice * pool.tail_cap * D;
+  const uint16_t* qrow = qkv + static_cast<size_t>(sq.row0) * s.q_stride + static_cast<size_t>(h) * NREP * D;
+  for (int i = threadIdx.x; i < NREP * D; i += blockDim.x) sq_q[i] = bf2f(qrow[i]) * s.scale_log2;
+  __syncthreads();
+  float m[NREP], l[NREP], o[NREP][CPL];
+#pragma unroll
+  for (int n = 0; n < NREP; ++n) {
+    m[n] = -INFINITY;
+    l[n] = 0.f;
+#pragma unroll
+    for (int j = 0; j < CPL; ++j) o[n][j] = 0.f;
+  }
+  // this warp's tokens of the 32-token chunk: all loads issued up front
+  constexpr int TPW = VC_TAIL_CHUNK / kWarps;
+  const int tw = t_lo + warp * TPW;
+  const int nt = max(0, min(TPW, sq.tail_len - tw));
+  float kv[TPW][CPL], vv[TPW][CPL];
+#pragma unroll
+  for (int i = 0; i < TPW; ++i) {
+    const int t = i < nt ? tw + i : tw;  // clamp; unused when i >= nt
+#pragma unroll
+    for (int j = 0; j < CPL; ++j) {
+      kv[i][j] = i < nt ? bf2f(kt[static_cast<size_t>(t) * D + lane * CPL + j]) : 0.f;
+      vv[i][j] = i < nt ? bf2f(vt[static_cast<size_t>(t) * D + lane * CPL + j]) : 0.f;
+    }
+  }
+  float dots[TPW][NREP];
+#pragma unroll
+  for (int i = 0; i < TPW; ++i)
+#pragma unroll
+    for (int n = 0; n < NREP; ++n) {
+      float d = 0.f;
+#pragma unroll
+      for (int j = 0; j < CPL; ++j) d += sq_q[n * D + lane * CPL + j] * kv[i][j];
+      dots[i][n] = d;
+    }
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1)  // all TPW*NREP reductions in flight together
+#pragma unroll
+    for (int i = 0; i < TPW; ++i)
+#pragma unroll
+      for (int n = 0; n < NREP; ++n) dots[i][n] += __shfl_xor_sync(0xffffffffu, dots[i][n], off);
+#pragma unroll
+  for (int n = 0; n < NREP; ++n) {
+    float mx = -INFINITY;
+#pragma unroll
+    for (int i = 0; i < TPW; ++i)
+      if (i < nt) mx = fmaxf(mx, dots[i][n]);
+    m[n] = mx;
+    float ls = 0.f;
+#pragma unroll
+    for (int i = 0; i < TPW; ++i) {
+      const float p = i < nt ? exp2f(dots[i][n] - mx) : 0.f;
+      ls += p;
+#pragma unroll
+      for (int j = 0; j < CPL; ++j) o[n][j] += p * vv[i][j];
+    }
+    l[n] = ls;
+  }
+  if (lane == 0) {
+#pragma unroll
+    for (int n = 0; n < 8; ++n) {
+      sm_m[warp * 8 + n] = n < NREP ? m[n < NREP ? n : 0] : -INFINITY;
+      sm_l[warp * 8 + n] = n < NREP ? l[n < NREP ? n : 0] : 0.f;
+    }
+  }
+#pragma unroll
+  for (int n = 0; n < NREP; ++n)
+#pragma unroll
+    for (int j = 0; j < CPL; ++j) sm_o[(warp * 8 + n) * D + lane * CPL + j] = o[n][j];
+  __syncthreads();
+  // merge the warps' partials into the chunk's partial row
   const int Hq = s.n_kv * NREP;
   for (int idx = threadIdx.x; idx < NREP * D; idx += blockDim.x) {
     const int n = idx / D, c = idx % D;
     float M = -INFINITY;
 #pragma unroll
     for (int w = 0; w < kWarps; ++w) M = fmaxf(M, sm_m[w * 8 + n]);
-    float o = 0.f, l = 0.f;
+    float ov = 0.f, lv = 0.f;
 #pragma unroll
     for (int w = 0; w < kWarps; ++w) {
       const float mw = sm_m[w * 8 + n];
       const float f = (mw == -INFINITY) ? 0.f : exp2f(mw - M);
-      o += f * sm_o[(w * 8 + n) * D + c];
-      l += f * sm_l[w * 8 + n];
+      ov += f * sm_o[(w * 8 + n) * D + c];
+      lv += f * sm_l[w * 8 + n];
     }
-    const size_t prow = static_cast<size_t>(sq.part0 + chunk) * Hq + hq0 + n;
-    part.o[prow * D + c] = o;
+    const size_t prow = static_cast<size_t>(sq.part0 + max_chunks + tc) * Hq + h * NREP + n;
+    part.o[prow * D + c] = ov;
     if (c == 0) {
       part.ml[prow * 2] = M;
-      part.ml[prow * 2 + 1] = l;
+      part.ml[prow * 2 + 1] = lv;
     }
   }
 }
 
+// grid: [n_seq * n_kv * tail chunks] tail CTAs, then s.draft_warps / kWarps
+// persistent quantised CTAs.
 template <int D, int BITS, int NREP>
-__global__ void __launch_bounds__(128) draft_attn_quant_kernel(AttnShape s, QuantPool pool,
-                                                               int layer, const uint16_t* qkv,
-                                                               const AttnSeq* seqs, int max_chunks,
-                                                               Partials part) {
+__global__ void __launch_bounds__(kWarps * 32, NREP == 8 ? 3 : VC_DRAFT_MINB) draft_attn_quant_kernel(AttnShape s, QuantPool pool,
+                                                                         int layer, const uint16_t* qkv,
+                                                                         const AttnSeq* seqs, int n_seq,
+                                                                         int max_chunks, Partials part) {
   static_assert(NREP <= 8, "n_rep > 8 needs two head tiles");
   using GEO = Geo<D, BITS>;
   constexpr int KS = GEO::KS, W = GEO::W, CH = GEO::CH, UMT = GEO::UMT;
   constexpr uint32_t MASK = BITS == 4 ? 0x000f000fu : 0x00030003u;
+  constexpr int kUPG = kG / kUnit;
 
   extern __shared__ __align__(128) uint32_t dsm[];   // [kWarps][2][STAGE]
-  __shared__ float sq_q[NREP * D];                   // scaled q, head-major
+  // per-warp q heads (bf16); the tail CTAs reuse it for NREP*D fp32 q values
+  __shared__ __align__(16) uint16_t sq_q[kWarps][NREP * D];
+  static_assert(kWarps * 2 >= 4, "tail q fits");
   __shared__ __align__(8) uint64_t bars[kWarps][2];
-  __shared__ float sm_m[kWarps * 8], sm_l[kWarps * 8];
-  float* sm_o = reinterpret_cast<float*>(dsm);       // reused after the pipeline drains
-
-  const AttnSeq sq = seqs[blockIdx.z];
-  const int h = blockIdx.y;
-  const int chunk = blockIdx.x;
-  const bool tail = chunk >= max_chunks;              // bf16 tail chunks follow the quantised ones
-  const int t_lo = (chunk - max_chunks) * VC_TAIL_CHUNK;
-  const int n_chunks = (sq.n_groups + kCG - 1) / kCG;
-  if (tail ? t_lo >= sq.tail_len : chunk >= n_chunks) return;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const size_t slice = (static_cast<size_t>(sq.slot) * s.layers + layer) * s.n_kv + h;
-
-  // q heads h*NREP .. h*NREP+NREP-1 are contiguous in the qkv row.
-  const uint16_t* qrow = qkv + static_cast<size_t>(sq.row0) * s.q_stride + static_cast<size_t>(h) * NREP * D;
-  for (int i = threadIdx.x; i < NREP * D; i += blockDim.x) sq_q[i] = bf2f(qrow[i]) * s.scale_log2;
-
-  if (tail) {
-    __syncthreads();
-    // ---- bf16 tail (residual group + draft window), CUDA cores ----------
-    constexpr int CPL = D / 32;  // channels per lane
-    const uint16_t* kt = pool.ktail + slice * pool.tail_cap * D;
-    const uint16_t* vt = pool.vtail + slice * pool.tail_cap * D;
-    float m[NREP], l[NREP], o[NREP][CPL];
-#pragma unroll
-    for (int n = 0; n < NREP; ++n) {
-      m[n] = -INFINITY;
-      l[n] = 0.f;
-#pragma unroll
-      for (int j = 0; j < CPL; ++j) o[n][j] = 0.f;
-    }
-    // this warp's 8 tokens of the 32-token chunk: all loads issued up front
-    constexpr int TPW = VC_TAIL_CHUNK / kWarps;
-    const int tw = t_lo + warp * TPW;
-    const int nt = max(0, min(TPW, sq.tail_len - tw));
-    float kv[TPW][CPL], vv[TPW][CPL];
-#pragma unroll
-    for (int i = 0; i < TPW; ++i) {
-      const int t = i < nt ? tw + i : tw;  // clamp; unused when i >= nt
-#pragma unroll
-      for (int j = 0; j < CPL; ++j) {
-        kv[i][j] = i < nt ? bf2f(kt[static_cast<size_t>(t) * D + lane * CPL + j]) : 0.f;
-        vv[i][j] = i < nt ? bf2f(vt[static_cast<size_t>(t) * D + lane * CPL + j]) : 0.f;
-      }
-    }
-    float dots[TPW][NREP];
-#pragma unroll
-    for (int i = 0; i < TPW; ++i)
-#pragma unroll
-      for (int n = 0; n < NREP; ++n) {
-        float d = 0.f;
-#pragma unroll
-        for (int j = 0; j < CPL; ++j) d += sq_q[n * D + lane * CPL + j] * kv[i][j];
-        dots[i][n] = d;
-      }
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1)  // all TPW*NREP reductions in flight together
-#pragma unroll
-      for (int i = 0; i < TPW; ++i)
-#pragma unroll
-        for (int n = 0; n < NREP; ++n) dots[i][n] += __shfl_xor_sync(0xffffffffu, dots[i][n], off);
-#pragma unroll
-    for (int n = 0; n < NREP; ++n) {
-      float mx = -INFINITY;
-#pragma unroll
-      for (int i = 0; i < TPW; ++i)
-        if (i < nt) mx = fmaxf(mx, dots[i][n]);
-      m[n] = mx;
-      float ls = 0.f;
-#pragma unroll
-      for (int i = 0; i < TPW; ++i) {
-        const float p = i < nt ? exp2f(dots[i][n] - mx) : 0.f;
-        ls += p;
-#pragma unroll
-        for (int j = 0; j < CPL; ++j) o[n][j] += p * vv[i][j];
-      }
-      l[n] = ls;
-    }
-    if (lane == 0) {
-#pragma unroll
-      for (int n = 0; n < 8; ++n) {
-        sm_m[warp * 8 + n] = n < NREP ? m[n < NREP ? n : 0] : -INFINITY;
-        sm_l[warp * 8 + n] = n < NREP ? l[n < NREP ? n : 0] : 0.f;
-      }
-    }
-#pragma unroll
-    for (int n = 0; n < NREP; ++n)
-#pragma unroll
-      for (int j = 0; j < CPL; ++j) sm_o[(warp * 8 + n) * D + lane * CPL + j] = o[n][j];
-    __syncthreads();
-    write_partial<D, NREP>(s, sq, h, chunk, sm_m, sm_l, sm_o, part);
+  const int TC = (pool.tail_cap + VC_TAIL_CHUNK - 1) / VC_TAIL_CHUNK;
+  const int n_tail_ctas = n_seq * s.n_kv * TC;
+  if (static_cast<int>(blockIdx.x) < n_tail_ctas) {
+    const int idx = blockIdx.x;
+    const int tc = idx % TC, h = (idx / TC) % s.n_kv, seq = idx / (TC * s.n_kv);
+    const AttnSeq sq = seqs[seq];
+    if (tc * VC_TAIL_CHUNK >= sq.tail_len) return;
+    draft_tail<D, NREP>(s, pool, layer, qkv, sq, h, tc, max_chunks, part, reinterpret_cast<float*>(dsm),
+                        reinterpret_cast<float*>(sq_q));
     return;
   }
 
-  // ---- quantised groups: per-warp TMA pipeline over kUnit-token units --------
-  const uint32_t* recs = pool.rec + slice * (static_cast<size_t>(pool.cap / kG) * GEO::GREC);
+  // ---- quantised groups: this warp's contiguous range of group tasks ----------
+  const int T = warp_task_sum(seqs, n_seq, s.n_kv, lane);
+  if (T == 0) return;
+  const int nw = draft_active_warps(T, s.draft_warps, s.draft_min_tasks);
+  const int w = (blockIdx.x - n_tail_ctas) * kWarps + warp;
+  if (w >= nw) return;  // no CTA-wide barriers below: warps are independent
+  const int t0 = draft_task_begin(w, T, nw), t1 = draft_task_begin(w + 1, T, nw);
+  const int n_units = (t1 - t0) * kUPG;
+
+  // locate task t0: sequence (warp scan over 32 sequences at a time), head, group
+  int seq0 = 0, base = 0;
+  for (int i0 = 0; i0 < n_seq; i0 += 32) {
+    const int i = i0 + lane;
+    const int c = i < n_seq ? seqs[i].n_groups * s.n_kv : 0;
+    int inc = c;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, inc, o);
+      if (lane >= o) inc += v;
+    }
+    const unsigned hit = __ballot_sync(0xffffffffu, t0 < base + inc);
+    if (hit) {
+      const int L = __ffs(hit) - 1;
+      seq0 = i0 + L;
+      base += __shfl_sync(0xffffffffu, inc - c, L);
+      break;
+    }
+    base += __shfl_sync(0xffffffffu, inc, 31);
+  }
+
+  // Task cursor: (sequence, head, group) plus the sequence's record base.
+  struct Cursor {
+    int seq, head, g, ng, base;  // base = first task of the sequence
+    const uint32_t* slice;       // group records of (slot, layer, head)
+  };
+  const size_t slice_words = static_cast<size_t>(pool.cap / kG) * GEO::GREC;
+  auto set_slice = [&](Cursor& c) {
+    c.slice = pool.rec + ((static_cast<size_t>(seqs[c.seq].slot) * s.layers + layer) * s.n_kv + c.head) * slice_words;
+  };
+  auto next_task = [&](Cursor& c) {
+    if (++c.g < c.ng) return;
+    c.g = 0;
+    if (++c.head < s.n_kv) { set_slice(c); return; }
+    c.head = 0;
+    c.base += c.ng * s.n_kv;
+    do { c.ng = seqs[++c.seq].n_groups; } while (c.ng == 0);  // tasks remain: terminates
+    set_slice(c);
+  };
+  Cursor pc;  // producer (lane 0 issues, all lanes track)
+  pc.seq = seq0;
+  pc.base = base;
+  pc.ng = seqs[seq0].n_groups;
+  pc.head = (t0 - base) / pc.ng;
+  pc.g = (t0 - base) % pc.ng;
+  set_slice(pc);
+  Cursor cc = pc;  // consumer
+  Cursor cur = pc; // (sequence, head) whose partial the accumulators hold
+  int ppart = 0;   // producer unit within its group
+
   uint32_t* stage0 = dsm + static_cast<size_t>(warp) * 2 * GEO::STAGE;
   uint64_t* bar = bars[warp];
-
-  // this warp's groups: chunk*kCG + warp, + kWarps, ... ; kUPG units each
-  constexpr int kUPG = kG / kUnit;
-  const int g_first = chunk * kCG + warp;
-  const int g_end = min((chunk + 1) * kCG, sq.n_groups);
-  const int n_mine = g_first < g_end ? (g_end - g_first + kWarps - 1) / kWarps : 0;
-  const int n_units = kUPG * n_mine;
-
-  auto issue = [&](int u, int st) {  // lane 0 only: one bulk copy per unit
-    const int g = g_first + (u / kUPG) * kWarps;
-    const int part = u % kUPG;
-    const uint32_t* src = recs + static_cast<size_t>(g) * GEO::GREC;
+  auto issue = [&](int st) {  // one bulk copy of the producer's next unit record
+    const uint32_t* src = pc.slice + static_cast<size_t>(pc.g) * GEO::GREC;
     uint32_t* dst = stage0 + st * GEO::STAGE;
-    if (part == 0) {
-      mbar_expect_tx(bar + st, GEO::STAGE * 4);
-      tma_load_1d(dst, src, GEO::STAGE * 4, bar + st);
-    } else {
-      mbar_expect_tx(bar + st, GEO::UREC * 4);
-      tma_load_1d(dst + GEO::OFF_K, src + D + part * GEO::UREC, GEO::UREC * 4, bar + st);
+    if (lane == 0) {
+      if (ppart == 0) {
+        mbar_expect_tx(bar + st, GEO::STAGE * 4);
+        tma_load_1d(dst, src, GEO::STAGE * 4, bar + st);
+      } else {
+        mbar_expect_tx(bar + st, GEO::UREC * 4);
+        tma_load_1d(dst + GEO::OFF_K, src + D + ppart * GEO::UREC, GEO::UREC * 4, bar + st);
+      }
+    }
+    if (++ppart == kUPG) {
+      ppart = 0;
+      next_task(pc);
     }
   };
   // A-fragment registers of one code word.  int4: one shift + four lop3,
   // pairs 2/3 (k or token +8) arrive as 1024 + 16c -- their B operand carries
   // the matching 1/16.  int2: word holds two k-steps, sub selects one.
-  auto unpack = [&](uint32_t w, int sub, uint32_t* a) {
+  auto unpack = [&](uint32_t wd, int sub, uint32_t* a) {
     if constexpr (BITS == 4) {
-      const uint32_t w8 = w >> 8;
-      a[0] = nib_to_h2(w, 0x000f000fu);
+      const uint32_t w8 = wd >> 8;
+      a[0] = nib_to_h2(wd, 0x000f000fu);
       a[1] = nib_to_h2(w8, 0x000f000fu);
-      a[2] = nib_to_h2(w, 0x00f000f0u);
+      a[2] = nib_to_h2(wd, 0x00f000f0u);
       a[3] = nib_to_h2(w8, 0x00f000f0u);
     } else {
       const int sh = 8 * sub;
 #pragma unroll
-      for (int j = 0; j < 4; ++j) a[j] = nib_to_h2(w >> (sh + j * BITS), MASK);
+      for (int j = 0; j < 4; ++j) a[j] = nib_to_h2(wd >> (sh + j * BITS), MASK);
     }
   };
   constexpr float kHiScale = BITS == 4 ? 0.0625f : 1.0f;  // B-operand scale of pairs 2/3
@@ -235,31 +305,88 @@ __global__ void __launch_bounds__(128) draft_attn_quant_kernel(AttnShape s, Quan
     mbar_init(bar + 1, 1);
     fence_mbar_init();
   }
-  __syncthreads();  // sq_q and barrier init visible
-  if (lane == 0) {
-    if (n_units > 0) issue(0, 0);
-    if (n_units > 1) issue(1, 1);
-  }
+  __syncwarp();
+  if (n_units > 0) issue(0);
+  if (n_units > 1) issue(1);
 
   const int hn = lane >> 2;         // head column this lane feeds in B fragments
   const int hc0 = 2 * (lane & 3);   // head columns this lane holds in C fragments
-  float mrun0 = -INFINITY, mrun1 = -INFINITY;
-  float lsum0 = 0.f, lsum1 = 0.f, corr0 = 0.f, corr1 = 0.f;
+  const int Hq = s.n_kv * NREP;
+  float mrun0, mrun1, lsum0, lsum1, corr0, corr1;
   float oacc[KS][4];
+  auto reset = [&]() {
+    mrun0 = mrun1 = -INFINITY;
+    lsum0 = lsum1 = corr0 = corr1 = 0.f;
 #pragma unroll
-  for (int ct = 0; ct < KS; ++ct) oacc[ct][0] = oacc[ct][1] = oacc[ct][2] = oacc[ct][3] = 0.f;
+    for (int ct = 0; ct < KS; ++ct) oacc[ct][0] = oacc[ct][1] = oacc[ct][2] = oacc[ct][3] = 0.f;
+  };
+  // the partial of the consumer's current (sequence, head)
+  auto emit = [&]() {
+    float l0 = lsum0, l1 = lsum1, c0 = corr0, c1 = corr1;
+#pragma unroll
+    for (int o = 4; o < 32; o <<= 1) {  // over the 8 lanes sharing a head column
+      l0 += __shfl_xor_sync(0xffffffffu, l0, o);
+      l1 += __shfl_xor_sync(0xffffffffu, l1, o);
+      c0 += __shfl_xor_sync(0xffffffffu, c0, o);
+      c1 += __shfl_xor_sync(0xffffffffu, c1, o);
+    }
+    const int p0 = cur.base + cur.head * cur.ng;  // first task of the (sequence, head)
+    const int slot = w - draft_task_warp(p0, T, nw);
+    const size_t prow = static_cast<size_t>(seqs[cur.seq].part0 + slot) * Hq + cur.head * NREP + hc0;
+    if (hc0 < NREP) {
+#pragma unroll
+      for (int ct = 0; ct < KS; ++ct) {
+        const int c = ct * 16 + (lane >> 2);
+        part.o[prow * D + c] = oacc[ct][0] + c0;
+        part.o[prow * D + c + 8] = oacc[ct][2] + c0;
+      }
+      if (lane < 4) {
+        part.ml[prow * 2] = mrun0;
+        part.ml[prow * 2 + 1] = l0;
+      }
+    }
+    if (hc0 + 1 < NREP) {
+#pragma unroll
+      for (int ct = 0; ct < KS; ++ct) {
+        const int c = ct * 16 + (lane >> 2);
+        part.o[(prow + 1) * D + c] = oacc[ct][1] + c1;
+        part.o[(prow + 1) * D + c + 8] = oacc[ct][3] + c1;
+      }
+      if (lane < 4) {
+        part.ml[(prow + 1) * 2] = mrun1;
+        part.ml[(prow + 1) * 2 + 1] = l1;
+      }
+    }
+  };
+  auto load_q = [&]() {  // the consumer head's NREP query rows, bf16
+    const uint16_t* qrow = qkv + static_cast<size_t>(seqs[cur.seq].row0) * s.q_stride +
+                           static_cast<size_t>(cur.head) * NREP * D;
+    __syncwarp();
+    for (int i = lane; i < NREP * D / 8; i += 32)
+      reinterpret_cast<uint4*>(sq_q[warp])[i] = reinterpret_cast<const uint4*>(qrow)[i];
+    __syncwarp();
+  };
+  reset();
+  load_q();
   uint32_t b0[KS], b1[KS];
   float bias0 = 0.f, bias1 = 0.f;
+  int cpart = 0;
 
   for (int u = 0; u < n_units; ++u) {
     const int st = u & 1;
+    if (cpart == 0 && (cc.seq != cur.seq || cc.head != cur.head)) {
+      emit();  // crossed into the next (sequence, head): flush its partial, restart
+      cur = cc;
+      reset();
+      load_q();
+    }
     mbar_wait(bar + st, (u >> 1) & 1);
     const uint32_t* sb = stage0 + st * GEO::STAGE;
-    if (u % kUPG == 0) {
+    if (cpart == 0) {
       // new group: q' = q * kscale as fp16 B fragments; per-head constant term
       float bias_part = 0.f;
-      const float* qh = sq_q + (hn < NREP ? hn : 0) * D;
-      const float qmask = hn < NREP ? 1.f : 0.f;  // padding head columns feed zeros
+      const uint16_t* qh = sq_q[warp] + (hn < NREP ? hn : 0) * D;
+      const float qmask = hn < NREP ? s.scale_log2 : 0.f;  // padding head columns feed zeros
 #pragma unroll
       for (int k = 0; k < KS; ++k) {
         const int c0 = k * 16 + 2 * (lane & 3);
@@ -268,8 +395,9 @@ __global__ void __launch_bounds__(128) draft_attn_quant_kernel(AttnShape s, Quan
           const int c = c0 + 8 * hi;
           const uint2 sz = *reinterpret_cast<const uint2*>(sb + GEO::OFF_KSZ + c);
           const float2 sz0 = h2_to_f2(sz.x), sz1 = h2_to_f2(sz.y);  // (scale, zero)
-          const float2 q = *reinterpret_cast<const float2*>(qh + c);
-          const float q0 = q.x * qmask, q1 = q.y * qmask;
+          const uint32_t qq = *reinterpret_cast<const uint32_t*>(qh + c);
+          const float q0 = bf2f(static_cast<uint16_t>(qq & 0xffffu)) * qmask;
+          const float q1 = bf2f(static_cast<uint16_t>(qq >> 16)) * qmask;
           const float f = hi ? kHiScale : 1.0f;
           const uint32_t bq = pack_h2(q0 * sz0.x * f, q1 * sz1.x * f);
           // zero point and the -1024 fold use the fp16-rounded q' the MMA sees
@@ -339,19 +467,16 @@ __global__ void __launch_bounds__(128) draft_attn_quant_kernel(AttnShape s, Quan
 #pragma unroll
     for (int m = 0; m < UMT; ++m) {
       const int r = m * 16 + (lane >> 2);
-      const uint32_t sz_a = sb[GEO::OFF_VSZ + r], sz_b = sb[GEO::OFF_VSZ + r + 8];
-      const float vs_a = h2f(static_cast<uint16_t>(sz_a & 0xffffu)), vz_a = h2f(static_cast<uint16_t>(sz_a >> 16));
-      const float vs_b = h2f(static_cast<uint16_t>(sz_b & 0xffffu)), vz_b = h2f(static_cast<uint16_t>(sz_b >> 16));
+      const float2 sza = h2_to_f2(sb[GEO::OFF_VSZ + r]), szb = h2_to_f2(sb[GEO::OFF_VSZ + r + 8]);
       const float p0 = ex2(sacc[m][0] - mrun0), p1 = ex2(sacc[m][1] - mrun1);
       const float p2 = ex2(sacc[m][2] - mrun0), p3 = ex2(sacc[m][3] - mrun1);
       lsum0 += p0 + p2;
       lsum1 += p1 + p3;
-      const uint32_t pk01 = pack_h2(p0 * vs_a, p1 * vs_a);
-      const uint32_t pk23 = pack_h2(p2 * vs_b * kHiScale, p3 * vs_b * kHiScale);  // tokens +8
-      const __half2 h01 = *reinterpret_cast<const __half2*>(&pk01);
-      const __half2 h23 = *reinterpret_cast<const __half2*>(&pk23);
-      corr0 += p0 * vz_a + p2 * vz_b - 1024.f * (__low2float(h01) + __low2float(h23));
-      corr1 += p1 * vz_a + p3 * vz_b - 1024.f * (__high2float(h01) + __high2float(h23));
+      const uint32_t pk01 = pack_h2(p0 * sza.x, p1 * sza.x);
+      const uint32_t pk23 = pack_h2(p2 * szb.x * kHiScale, p3 * szb.x * kHiScale);  // tokens +8
+      const float2 h01 = h2_to_f2(pk01), h23 = h2_to_f2(pk23);
+      corr0 += p0 * sza.y + p2 * szb.y - 1024.f * (h01.x + h23.x);
+      corr1 += p1 * sza.y + p3 * szb.y - 1024.f * (h01.y + h23.y);
       bp0[m] = movmatrix_trans(pk01);
       bp1[m] = movmatrix_trans(pk23);
     }
@@ -380,67 +505,72 @@ __global__ void __launch_bounds__(128) draft_attn_quant_kernel(AttnShape s, Quan
     }
     fence_proxy_async();  // LDS reads of the stage before the next TMA write into it
     __syncwarp();
-    if (lane == 0 && u + 2 < n_units) issue(u + 2, st);
+    if (u + 2 < n_units) issue(st);
+    if (++cpart == kUPG) {
+      cpart = 0;
+      next_task(cc);
+    }
   }
+  emit();  // the last (sequence, head) of the range
+}
 
-  // reduce the per-lane sums over the 8 lanes sharing a head column
-#pragma unroll
-  for (int o = 4; o < 32; o <<= 1) {
-    lsum0 += __shfl_xor_sync(0xffffffffu, lsum0, o);
-    lsum1 += __shfl_xor_sync(0xffffffffu, lsum1, o);
-    corr0 += __shfl_xor_sync(0xffffffffu, corr0, o);
-    corr1 += __shfl_xor_sync(0xffffffffu, corr1, o);
-  }
-  __syncthreads();  // all warps done with their stages before sm_o reuses them
-  if (lane < 4) {
-    sm_m[warp * 8 + hc0] = mrun0;
-    sm_m[warp * 8 + hc0 + 1] = mrun1;
-    sm_l[warp * 8 + hc0] = lsum0;
-    sm_l[warp * 8 + hc0 + 1] = lsum1;
-  }
-#pragma unroll
-  for (int ct = 0; ct < KS; ++ct) {
-    const int c = ct * 16 + (lane >> 2);
-    sm_o[(warp * 8 + hc0) * D + c] = oacc[ct][0] + corr0;
-    sm_o[(warp * 8 + hc0 + 1) * D + c] = oacc[ct][1] + corr1;
-    sm_o[(warp * 8 + hc0) * D + c + 8] = oacc[ct][2] + corr0;
-    sm_o[(warp * 8 + hc0 + 1) * D + c + 8] = oacc[ct][3] + corr1;
-  }
-  __syncthreads();
-  write_partial<D, NREP>(s, sq, h, chunk, sm_m, sm_l, sm_o, part);
+template <int D, int BITS, int NREP>
+size_t draft_smem() {
+  using GEO = Geo<D, BITS>;
+  size_t smem = static_cast<size_t>(kWarps) * 2 * GEO::STAGE * 4;
+  const size_t need_o = static_cast<size_t>(kWarps) * 8 * D * 4;  // tail CTAs' sm_o
+  return smem < need_o ? need_o : smem;
+}
+
+template <int D, int BITS, int NREP>
+int quant_warps() {
+  auto kern = draft_attn_quant_kernel<D, BITS, NREP>;
+  const size_t smem = draft_smem<D, BITS, NREP>();
+  if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess)
+    return 0;
+  int dev = 0, sms = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, kWarps * 32, smem) != cudaSuccess)
+    return 0;
+  return sms * (per_sm > 0 ? per_sm : 1) * kWarps;
 }
 
 template <int D, int BITS, int NREP>
 cudaError_t launch_draft(const AttnShape& s, const QuantPool& pool, int layer, const uint16_t* qkv,
                          const AttnSeq* seqs, int n_seq, int max_chunks, Partials part,
                          cudaStream_t st) {
-  using GEO = Geo<D, BITS>;
-  size_t smem = static_cast<size_t>(kWarps) * 2 * GEO::STAGE * 4;
-  const size_t need_o = static_cast<size_t>(kWarps) * 8 * D * 4;  // sm_o reuse
-  if (smem < need_o) smem = need_o;
   auto kern = draft_attn_quant_kernel<D, BITS, NREP>;
+  const size_t smem = draft_smem<D, BITS, NREP>();
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  dim3 grid(draft_parts_per_seq(max_chunks, pool.tail_cap), s.n_kv, n_seq);
-  kern<<<grid, kWarps * 32, smem, st>>>(s, pool, layer, qkv, seqs, max_chunks, part);
+  if (s.draft_warps <= 0 || s.draft_warps % kWarps || s.draft_min_tasks <= 0) return cudaErrorInvalidValue;
+  const int tail_ctas = n_seq * s.n_kv * ((pool.tail_cap + VC_TAIL_CHUNK - 1) / VC_TAIL_CHUNK);
+  kern<<<tail_ctas + s.draft_warps / kWarps, kWarps * 32, smem, st>>>(s, pool, layer, qkv, seqs, n_seq,
+                                                                       max_chunks, part);
   return cudaGetLastError();
 }
 
 }  // namespace
 
+#define VC_DRAFT_SHAPES(X) X(128, 4, 4) X(128, 2, 4) X(128, 4, 8) X(128, 2, 8) X(64, 4, 4) X(64, 2, 4)
+
+int draft_quant_warps(int d, int bits, int n_rep) {
+#define VC_DRAFT_CASE(D_, B_, R_) \
+  if (d == D_ && bits == B_ && n_rep == R_) return quant_warps<D_, B_, R_>();
+  VC_DRAFT_SHAPES(VC_DRAFT_CASE)
+#undef VC_DRAFT_CASE
+  return 0;
+}
+
 cudaError_t draft_attention_quant(const AttnShape& s, const QuantPool& pool, int layer,
                                   const uint16_t* qkv, const AttnSeq* seqs, int n_seq,
                                   int max_chunks, int bits, Partials part, cudaStream_t st) {
   if (n_seq <= 0) return cudaSuccess;
-#define VC_DRAFT_CASE(D_, B_, R_)                                                   \
-  if (s.d == D_ && bits == B_ && s.n_rep == R_)                                    \
+#define VC_DRAFT_CASE(D_, B_, R_)                \
+  if (s.d == D_ && bits == B_ && s.n_rep == R_) \
     return launch_draft<D_, B_, R_>(s, pool, layer, qkv, seqs, n_seq, max_chunks, part, st);
-  VC_DRAFT_CASE(128, 4, 4)
-  VC_DRAFT_CASE(128, 2, 4)
-  VC_DRAFT_CASE(128, 4, 8)
-  VC_DRAFT_CASE(128, 2, 8)
-  VC_DRAFT_CASE(64, 4, 4)
-  VC_DRAFT_CASE(64, 2, 4)
+  VC_DRAFT_SHAPES(VC_DRAFT_CASE)
 #undef VC_DRAFT_CASE
   return cudaErrorInvalidValue;
 }

@@ -32,6 +32,8 @@ T* dmalloc(size_t n) {
   void* p = nullptr;
   if (n == 0) n = 1;
   check_cuda(cudaMalloc(&p, n * sizeof(T)), "cudaMalloc");
+  // zeroed: tile loads may read past a sequence's last key (masked, but finite)
+  check_cuda(cudaMemset(p, 0, n * sizeof(T)), "cudaMemset");
   return static_cast<T*>(p);
 }
 
@@ -123,6 +125,8 @@ void Engine::attention_probe(int slot, int layer, int mode, const uint16_t* q_de
   as.out_stride = m.n_q * m.d;
   as.out_mp = 0;
   as.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(m.d)));
+  as.draft_warps = draft_warps_;
+  as.draft_min_tasks = draft_min_tasks_;
   AttnSeq a{};
   a.slot = cfg_.full_tier == 1 && mode != 1 ? 0 : slot;
   a.row0 = 0;
@@ -141,7 +145,10 @@ void Engine::attention_probe(int slot, int layer, int mode, const uint16_t* q_de
     VC_LAUNCH(attention_combine(as, seqs_dev_, 1, max_chunks_q_, 1, 0, part_, attn_, st_));
   } else {
     const KvPool pool = cfg_.full_tier == 0 ? full_ : stage_;
-    VC_LAUNCH(dense_attention(as, pool, layer, q_dev, seqs_dev_, 1, max_chunks_d_, n_rows, part_, st_));
+    DenseMaps maps = dense_maps_;
+    if (!make_q_map(&maps, q_dev, m.d, m.n_q, n_rows, m.n_q * m.d, m.n_q / m.n_kv))
+      throw ContractViolation("probe: cannot encode the query tensor map");
+    VC_LAUNCH(dense_attention(as, pool, maps, layer, seqs_dev_, 1, max_chunks_d_, n_rows, part_, st_));
     VC_LAUNCH(attention_combine(as, seqs_dev_, 1, max_chunks_d_, n_rows, 1, part_, attn_, st_));
   }
   VC_CK(cudaMemcpyAsync(out_host, attn_, static_cast<size_t>(n_rows) * m.n_q * m.d * 2,
@@ -233,7 +240,13 @@ void Engine::alloc_all() {
     quant_.rec = dmalloc<uint32_t>(slices * (capq / VC_QGROUP) * quant_record_words(d, cfg_.quant_bits));
     quant_.ktail = dmalloc<uint16_t>(slices * tail_cap_ * d);
     quant_.vtail = dmalloc<uint16_t>(slices * tail_cap_ * d);
-    max_chunks_q_ = (capq / VC_QGROUP + VC_DRAFT_CG - 1) / VC_DRAFT_CG;
+    // draft partial slots per (sequence, head): a warp takes >= draft_min_tasks_
+    // groups, so at most ceil(groups / min) + 1 warps touch one head
+    const int capg = capq / VC_QGROUP;
+    draft_min_tasks_ = std::max(4, (capg + 479) / 480);
+    max_chunks_q_ = (capg + draft_min_tasks_ - 1) / draft_min_tasks_ + 1;
+    draft_warps_ = draft_quant_warps(d, cfg_.quant_bits, m.n_q / m.n_kv);
+    if (draft_warps_ <= 0) throw ContractViolation("no draft-attention kernel for this head shape");
   }
   max_chunks_d_ = (cap + VC_DENSE_CHUNK - 1) / VC_DENSE_CHUNK;
   // ---- activations ---------------------------------------------------------
@@ -243,6 +256,14 @@ void Engine::alloc_all() {
   xn_ = dmalloc<uint16_t>(static_cast<size_t>(Mmax_ + 128) * (H > F ? H : F));
   qkv_ = dmalloc<uint16_t>(static_cast<size_t>(Mmax_) * qkv_n);
   attn_ = dmalloc<uint16_t>(static_cast<size_t>(Mmax_ + 128) * m.n_q * d);
+  // TMA tensor maps of the dense attention path (K/V pool of each tier + the q heads)
+  {
+    const KvPool& dp = cfg_.full_tier == 0 ? full_ : stage_;
+    const size_t dslices = cfg_.full_tier == 0 ? slices : static_cast<size_t>(cfg_.n_stage) * L * m.n_kv;
+    if (!make_kv_maps(&dense_maps_, dp, dslices, d) ||
+        !make_q_map(&dense_maps_, qkv_, d, m.n_q + 2 * m.n_kv, Mmax_, qkv_n, m.n_q / m.n_kv))
+      throw ContractViolation("dense attention: cannot encode TMA tensor maps for this shape");
+  }
   act_ = dmalloc<uint16_t>(static_cast<size_t>(Mmax_ + 128) * F);
   {
     size_t pf = 0;
@@ -529,6 +550,8 @@ void Engine::enqueue_forward(int M, int n_draft, int n_dense1, int n_densev, int
   as.out_stride = m.n_q * d;
   as.out_mp = M;  // attention output feeds o_proj in the tiled layout
   as.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(d)));
+  as.draft_warps = draft_warps_;
+  as.draft_min_tasks = draft_min_tasks_;
   const KvPool dense_v_pool = cfg_.full_tier == 0 ? full_ : stage_;
   // VC_TRACE=1 (eager engines only): checksum every stage's output buffer
   static const bool tracing = std::getenv("VC_TRACE") != nullptr;
@@ -578,12 +601,12 @@ void Engine::enqueue_forward(int M, int n_draft, int n_dense1, int n_densev, int
       VC_LAUNCH(attention_combine(as, seqs_dev_, n_draft, max_chunks_q_, 1, 0, part_, attn_, st_));
     }
     if (n_dense1 > 0) {
-      VC_LAUNCH(dense_attention(as, full_, l, qkv_, seqs_dev_ + n_draft, n_dense1, max_chunks_d_, 1, part_, st_));
+      VC_LAUNCH(dense_attention(as, full_, dense_maps_, l, seqs_dev_ + n_draft, n_dense1, max_chunks_d_, 1, part_, st_));
       VC_LAUNCH(attention_combine(as, seqs_dev_ + n_draft, n_dense1, max_chunks_d_, 1, 1, part_, attn_, st_));
     }
     if (n_densev > 0) {
       const AttnSeq* sv = seqs_dev_ + n_draft + n_dense1;
-      VC_LAUNCH(dense_attention(as, dense_v_pool, l, qkv_, sv, n_densev, max_chunks_d_, max_rows_v, part_, st_));
+      VC_LAUNCH(dense_attention(as, dense_v_pool, dense_maps_, l, sv, n_densev, max_chunks_d_, max_rows_v, part_, st_));
       VC_LAUNCH(attention_combine(as, sv, n_densev, max_chunks_d_, max_rows_v, 1, part_, attn_, st_));
     }
     VC_LAUNCH(gemm(attn_, M, M, m.n_q * d, w_.wo[l], H, er, gws_, st_));
@@ -749,6 +772,8 @@ void Engine::kernel_bench(int kind, const std::vector<int>& slots, int reps, dou
   as.out_stride = m.n_q * m.d;
   as.out_mp = 0;
   as.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(m.d)));
+  as.draft_warps = draft_warps_;
+  as.draft_min_tasks = draft_min_tasks_;
   AttnSeq* h = reinterpret_cast<AttnSeq*>(static_cast<int32_t*>(h_desc_) + Mmax_) ;
   h = reinterpret_cast<AttnSeq*>(reinterpret_cast<RowDest*>(h) + Mmax_);
   double b = 0.0;
@@ -781,7 +806,7 @@ void Engine::kernel_bench(int kind, const std::vector<int>& slots, int reps, dou
         VC_LAUNCH(attention_combine(as, seqs_dev_, n, max_chunks_q_, 1, 0, part_, attn_, st_));
       } else {
         const KvPool pool = cfg_.full_tier == 0 ? full_ : stage_;
-        VC_LAUNCH(dense_attention(as, pool, l, qkv_, seqs_dev_, n, max_chunks_d_, 1, part_, st_));
+        VC_LAUNCH(dense_attention(as, pool, dense_maps_, l, seqs_dev_, n, max_chunks_d_, 1, part_, st_));
         VC_LAUNCH(attention_combine(as, seqs_dev_, n, max_chunks_d_, 1, 1, part_, attn_, st_));
       }
     }

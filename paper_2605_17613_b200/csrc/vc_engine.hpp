@@ -171,9 +171,11 @@ class Engine {
   size_t weight_bytes_ = 0;
   float *rope_cos_ = nullptr, *rope_sin_ = nullptr;
   KvPool full_{}, stage_{};
+  DenseMaps dense_maps_{};  // tensor maps of the HBM pool the dense kernel reads (tier 0 full, tier 1 stage)
   QuantPool quant_{};
   uint16_t *host_k_ = nullptr, *host_v_ = nullptr;
   int max_chunks_q_ = 0, max_chunks_d_ = 0, tail_cap_ = 0, Mmax_ = 0;
+  int draft_warps_ = 0, draft_min_tasks_ = 4;  // quantised draft-attention work split
   // activations
   float* x_ = nullptr;
   uint16_t *xn_ = nullptr, *qkv_ = nullptr, *attn_ = nullptr, *act_ = nullptr;

@@ -3,17 +3,19 @@
 #pragma once
 #include <cstddef>
 #include <cstdint>
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #define VC_QGROUP 128      // tokens per quantised K group (KIVI G)
-#define VC_DRAFT_CG 8      // quantised groups per draft-attention chunk (1024 tokens)
 #define VC_TAIL_CHUNK 32   // bf16-tail tokens per draft-attention tail CTA
 
 // Draft partial slots per sequence: the quantised chunks, then the tail chunks.
-inline int draft_parts_per_seq(int max_chunks, int tail_cap) {
+inline int draft_parts_per_seq(int max_chunks, int tail_cap) {  // quantised slots + tail chunks
   return max_chunks + (tail_cap + VC_TAIL_CHUNK - 1) / VC_TAIL_CHUNK;
 }
+#ifndef VC_DENSE_CHUNK
 #define VC_DENSE_CHUNK 512 // keys per dense-attention chunk (absolute positions)
+#endif
 
 namespace vc {
 
@@ -82,7 +84,28 @@ struct AttnShape {
   int out_stride;      // elements per row of the attention output (row-major)
   int out_mp;          // > 0: write the output in the GEMM's tiled layout with Mp rows
   float scale_log2;    // log2(e)/sqrt(d)
+  int draft_warps;     // quantised-draft warps launched (persistent, draft_quant_warps)
+  int draft_min_tasks; // fewest group tasks a draft warp takes (bounds partials per head)
 };
+
+// Draft-attention work split: the T = sum(n_groups * n_kv) group tasks of a
+// step, ordered (sequence, kv head, group), are cut into nw contiguous ranges
+// of near-equal length, one per warp (stream-K style), so every warp streams
+// the same number of bytes whatever the batch's context lengths are.  A warp
+// emits one partial per (sequence, head) it touches; its slot is the warp's
+// ordinal among the warps touching that head.
+__host__ __device__ inline int draft_active_warps(int T, int nw, int min_tasks) {
+  const int cap = T / min_tasks;
+  return cap < 1 ? 1 : (cap < nw ? cap : nw);
+}
+__host__ __device__ inline int draft_task_begin(int w, int T, int nw) {
+  return static_cast<int>(static_cast<long long>(w) * T / nw);
+}
+__host__ __device__ inline int draft_task_warp(int t, int T, int nw) {  // warp owning task t
+  return static_cast<int>((static_cast<long long>(t + 1) * nw - 1) / T);
+}
+// warps launched for the quantised draft path (one full wave; 0 = unsupported shape)
+int draft_quant_warps(int d, int bits, int n_rep);
 
 // Split-K partials: o [part_rows][d] fp32, ml [part_rows][2] (max in log2
 // domain, sum).  A partial row is (sequence part0 + chunk*rows + r).
@@ -95,9 +118,17 @@ cudaError_t draft_attention_quant(const AttnShape& s, const QuantPool& pool, int
                                   const uint16_t* qkv, const AttnSeq* seqs, int n_seq,
                                   int max_chunks, int bits, Partials part, cudaStream_t st);
 
-cudaError_t dense_attention(const AttnShape& s, const KvPool& pool, int layer, const uint16_t* qkv,
-                            const AttnSeq* seqs, int n_seq, int max_chunks, int max_rows,
-                            Partials part, cudaStream_t st);
+// TMA tensor maps of the dense path: K and V pools as 2-D [slices*cap, d]
+// (128-key x 64-channel boxes) and the query heads of the activation rows as
+// 3-D [rows, heads, d] (n_rep heads x 128/n_rep tokens per box), 128B swizzle.
+struct DenseMaps {
+  CUtensorMap k, v, q;
+};
+bool make_kv_maps(DenseMaps* m, const KvPool& pool, size_t slices, int d);
+bool make_q_map(DenseMaps* m, const uint16_t* qkv, int d, int heads_per_row, int rows, int q_stride, int n_rep);
+cudaError_t dense_attention(const AttnShape& s, const KvPool& pool, const DenseMaps& maps, int layer,
+                            const AttnSeq* seqs, int n_seq, int max_chunks, int max_rows, Partials part,
+                            cudaStream_t st);
 
 // Merge the chunk partials of every (sequence, query token, q head) in chunk
 // order into bf16 attention output rows.  mode 0 = draft layout (chunks of

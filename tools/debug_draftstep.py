@@ -27,3 +27,17 @@ ms, n = e.timing(reset=True)
 print(f"max_ctx={max_ctx} n_stage={n_stage}: draft() {ms / n:.3f} ms")
 kms, kb = e.kernel_bench(0, list(range(B)), reps=3)
 print(f"kernel_bench draft attention {kms:.3f} ms {kb / kms / 1e6:.0f} GB/s")
+e.close()
+e = vc.Engine(vc.LLAMA3_8B, max_slots=B, max_ctx=max_ctx, max_x=16, quant_bits=0, full_tier=0, max_verify=2)
+e.init_weights(0, 0.02, resid_std=0.0005, q_std=0.005)
+for i in range(B):
+    e.add_synthetic(i, ctx, 100 + i, seed=1 + i)
+kms, kb = e.kernel_bench(1, list(range(B)), reps=3)
+print(f"kernel_bench dense (decode) attention {kms:.3f} ms {kb / kms / 1e6:.0f} GB/s")
+for _ in range(3):
+    e.decode_step(list(range(B)))
+e.timing(reset=True)
+for _ in range(6):
+    e.decode_step(list(range(B)))
+ms, n = e.timing(reset=True)
+print(f"full-KV decode step {ms / n:.3f} ms")
