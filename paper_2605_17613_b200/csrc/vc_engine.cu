@@ -298,6 +298,10 @@ void Engine::alloc_all() {
                 static_cast<size_t>(L) * m.n_kv * sizeof(QuantJob);
   VC_CK(cudaHostAlloc(&h_desc_, desc_bytes_, cudaHostAllocDefault));
   VC_CK(cudaHostAlloc(reinterpret_cast<void**>(&h_out_), Mmax_ * sizeof(int32_t), cudaHostAllocDefault));
+  // dmalloc's cudaMemsets run on the legacy stream, which the non-blocking
+  // compute/copy streams do not order against: finish them before any work
+  // (e.g. synth_kv_kernel) lands in these buffers.
+  VC_CK(cudaDeviceSynchronize());
 }
 
 // ---------------------------------------------------------------- weights
