@@ -196,6 +196,8 @@ def main():
     tier = 1 if args.tier == "host" else 0
     x = args.x or (64 if tier == 1 else 16)
     window = args.window or max(2 * x + 8, 48 if tier == 0 else 256)
+    from paper_2605_17613_b200.shard import reduce_window, weak_shard
+    shard = weak_shard(B, world, rank)  # this rank's requests (no data-path collective)
     rng = np.random.default_rng(2 + rank)
     first = [int(t) for t in rng.integers(0, shape.vocab, B)]
     # ---------------- baseline: full-KV greedy decode, same engine, HBM resident
@@ -205,7 +207,7 @@ def main():
     qs = args.q_std if args.q_std >= 0 else (0.005 if not args.small else 0.0)
     eb.init_weights(seed=0, std=0.02, resid_std=rs, q_std=qs)
     for i in range(B):
-        eb.add_synthetic(i, ctx, first[i], seed=1 + rank * 1000 + i)
+        eb.add_synthetic(i, ctx, first[i], seed=shard.seeds[i])
     slots = list(range(B))
     base_warm, _ = eb.autoregress(slots, W)
     eb.timing(reset=True)
@@ -224,7 +226,7 @@ def main():
                    max_verify=3 if tier else max(2, B // (x + 1) + 2), device=local)
     ev.init_weights(seed=0, std=0.02, resid_std=rs, q_std=qs)
     for i in range(B):
-        ev.add_synthetic(i, ctx, first[i], seed=1 + rank * 1000 + i)
+        ev.add_synthetic(i, ctx, first[i], seed=shard.seeds[i])
         meta = ev.compress(i)
     # roofline probe: draft attention over every layer of every request
     ka_ms, ka_bytes = ev.kernel_bench(0, slots, reps=5)
@@ -249,14 +251,8 @@ def main():
     tok = float(st["timed_tokens"])
     dev_s = st["timed_device_ms"] / 1e3
     wall_s = st["timed_wall_ms"] / 1e3
-    vals = torch.tensor([tok, dev_s, wall_s, base_dev / 1e3, base_wall / 1e3, ka_ms], dtype=torch.float64,
-                        device="cuda")
-    if dist:
-        tsum = vals[:1].clone()
-        dist.all_reduce(tsum)
-        dist.all_reduce(vals, op=dist.ReduceOp.MAX)
-        vals[0] = tsum[0]
-    tok_all, dev_s, wall_s, bdev_s, bwall_s, ka_ms_max = vals.tolist()
+    tok_all, (dev_s, wall_s, bdev_s, bwall_s, ka_ms_max) = reduce_window(
+        tok, [dev_s, wall_s, base_dev / 1e3, base_wall / 1e3, ka_ms], dist, device="cuda")
     value = tok_all / dev_s
     base_value = B * world * K / bdev_s
     achieved = ka_bytes / (ka_ms / 1e3) / 1e9

@@ -34,6 +34,10 @@ T* dmalloc(size_t n) {
   check_cuda(cudaMalloc(&p, n * sizeof(T)), "cudaMalloc");
   // zeroed: tile loads may read past a sequence's last key (masked, but finite)
   check_cuda(cudaMemset(p, 0, n * sizeof(T)), "cudaMemset");
+  // the memset runs on the legacy stream, which the engine's non-blocking
+  // streams do not order against (a weight upload into a fresh staging
+  // buffer raced it): finish it before the buffer is handed out
+  check_cuda(cudaDeviceSynchronize(), "cudaDeviceSynchronize");
   return static_cast<T*>(p);
 }
 
@@ -278,7 +282,6 @@ void Engine::alloc_all() {
     gws_.partial = dmalloc<float>(pf);
     gws_.n_counters = std::max(std::max(qkv_n, H), std::max(2 * F, V)) / 128 + 1;
     gws_.counters = dmalloc<int>(gws_.n_counters);
-    VC_CK(cudaMemset(gws_.counters, 0, gws_.n_counters * sizeof(int)));
   }
   ss_part_ = dmalloc<float>(static_cast<size_t>(Mmax_) * (H / 128));
   logits_ = dmalloc<float>(static_cast<size_t>(Mmax_) * V);
@@ -298,10 +301,6 @@ void Engine::alloc_all() {
                 static_cast<size_t>(L) * m.n_kv * sizeof(QuantJob);
   VC_CK(cudaHostAlloc(&h_desc_, desc_bytes_, cudaHostAllocDefault));
   VC_CK(cudaHostAlloc(reinterpret_cast<void**>(&h_out_), Mmax_ * sizeof(int32_t), cudaHostAllocDefault));
-  // dmalloc's cudaMemsets run on the legacy stream, which the non-blocking
-  // compute/copy streams do not order against: finish them before any work
-  // (e.g. synth_kv_kernel) lands in these buffers.
-  VC_CK(cudaDeviceSynchronize());
 }
 
 // ---------------------------------------------------------------- weights
@@ -803,26 +802,34 @@ void Engine::kernel_bench(int kind, const std::vector<int>& slots, int reps, dou
   }
   b *= static_cast<double>(m.layers) * m.n_kv;
   VC_CK(cudaMemcpyAsync(seqs_dev_, h, n * sizeof(AttnSeq), cudaMemcpyHostToDevice, st_));
-  auto launch_all = [&] {
-    for (int l = 0; l < m.layers; ++l) {
+  // time the attention kernel alone (events on the launching stream around
+  // each launch); the combine that follows it is launched but not timed
+  const int n_ev = m.layers * (reps + 1);
+  std::vector<cudaEvent_t> ev(2 * n_ev);
+  for (auto& x : ev) VC_CK(cudaEventCreate(&x));
+  int k = 0;
+  for (int r = 0; r <= reps; ++r)
+    for (int l = 0; l < m.layers; ++l, ++k) {
+      VC_CK(cudaEventRecord(ev[2 * k], st_));
       if (kind == 0) {
         VC_LAUNCH(draft_attention_quant(as, quant_, l, qkv_, seqs_dev_, n, max_chunks_q_, cfg_.quant_bits, part_, st_));
-        VC_LAUNCH(attention_combine(as, seqs_dev_, n, max_chunks_q_, 1, 0, part_, attn_, st_));
       } else {
         const KvPool pool = cfg_.full_tier == 0 ? full_ : stage_;
         VC_LAUNCH(dense_attention(as, pool, dense_maps_, l, seqs_dev_, n, max_chunks_d_, 1, part_, st_));
-        VC_LAUNCH(attention_combine(as, seqs_dev_, n, max_chunks_d_, 1, 1, part_, attn_, st_));
       }
+      VC_CK(cudaEventRecord(ev[2 * k + 1], st_));
+      VC_LAUNCH(attention_combine(as, seqs_dev_, n, kind == 0 ? max_chunks_q_ : max_chunks_d_, 1, kind == 0 ? 0 : 1,
+                                  part_, attn_, st_));
     }
-  };
-  launch_all();  // warm
-  VC_CK(cudaEventRecord(ev_a_, st_));
-  for (int r = 0; r < reps; ++r) launch_all();
-  VC_CK(cudaEventRecord(ev_b_, st_));
-  VC_CK(cudaEventSynchronize(ev_b_));
-  float t = 0.f;
-  VC_CK(cudaEventElapsedTime(&t, ev_a_, ev_b_));
-  *ms = t / reps;
+  VC_CK(cudaStreamSynchronize(st_));
+  double total = 0.0;
+  for (int j = m.layers; j < n_ev; ++j) {  // the first pass is warm-up
+    float t = 0.f;
+    VC_CK(cudaEventElapsedTime(&t, ev[2 * j], ev[2 * j + 1]));
+    total += t;
+  }
+  for (auto& x : ev) cudaEventDestroy(x);
+  *ms = total / reps;  // per launch-set (all layers)
   *bytes = b;
 }
 
