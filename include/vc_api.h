@@ -111,7 +111,8 @@ int vc_engine_stats(vc_engine* e, uint64_t* kernel_launches, uint64_t* weight_by
  * summed over steps since the last reset.                                  */
 int vc_engine_timing(vc_engine* e, double* device_ms, int64_t* steps, int reset);
 /* Isolated timing of one kernel family over every layer for the given
- * requests: kind 0 draft attention, 1 dense attention.  *bytes = the
+ * requests: kind 0 draft attention, 1 dense attention (one decode row),
+ * 2 dense attention of a verify window (max_x+1 rows).  *bytes = the
  * algorithmic bytes one launch-set moves.           */
 int vc_kernel_bench(vc_engine* e, int kind, const int* slots, int n, int reps, double* ms,
                     double* bytes);
@@ -207,8 +208,9 @@ typedef struct {
   int64_t verifies;
   int64_t late_transfers;
   double h2d_bytes;
-  double h2d_ms;            /* copy-engine busy time */
-  double verify_wait_ms;    /* time verifies waited on copy events */
+  double h2d_ms;            /* copy-engine busy time of the reloads (timed window) */
+  double verify_wait_ms;    /* exposed swap time: sum over iterations of (sessions
+                               stalled on a late reload) x iteration wall time */
   double mean_accept;       /* accepted drafted tokens per verify */
   int64_t timed_iterations; /* iterations inside the timed window */
   int64_t timed_tokens;     /* tokens emitted inside the timed window */

@@ -5,6 +5,9 @@
  */
 #include "vc_oracle.h"
 
+#include <pthread.h>
+#include <unistd.h>
+
 #include <math.h>
 #include <stdlib.h>
 #include <string.h>
@@ -14,6 +17,42 @@
 /* ------------------------------------------------------------------------ */
 
 /* Restates speckv::splitmix64 (/root/reference/proj/include/speckv/util.hpp:30-35). */
+/* ---- host threads (bench.py's CPU baseline uses every core) -------------
+ * par_for splits [0, n) into contiguous ranges, one per thread; each range's
+ * work is independent, so results are identical at any thread count.
+ * VCO_THREADS overrides the count (default: online cores). */
+typedef void (*vco_body)(void* ctx, long lo, long hi);
+struct vco_par { vco_body f; void* ctx; long lo, hi; };
+static void* vco_tramp(void* a) {
+  struct vco_par* p = (struct vco_par*)a;
+  p->f(p->ctx, p->lo, p->hi);
+  return NULL;
+}
+int vco_threads(void) {
+  const char* e = getenv("VCO_THREADS");
+  long n = e ? atol(e) : sysconf(_SC_NPROCESSORS_ONLN);
+  return n < 1 ? 1 : (n > 64 ? 64 : (int)n);
+}
+static void par_for(long n, long min_per_thread, vco_body f, void* ctx) {
+  int T = vco_threads();
+  if (T > n / (min_per_thread > 0 ? min_per_thread : 1)) T = (int)(n / (min_per_thread > 0 ? min_per_thread : 1));
+  if (T <= 1) {
+    f(ctx, 0, n);
+    return;
+  }
+  pthread_t th[64];
+  struct vco_par a[64];
+  for (int t = 0; t < T; ++t) {
+    a[t].f = f;
+    a[t].ctx = ctx;
+    a[t].lo = n * t / T;
+    a[t].hi = n * (t + 1) / T;
+  }
+  for (int t = 1; t < T; ++t) pthread_create(&th[t], NULL, vco_tramp, &a[t]);
+  vco_tramp(&a[0]);
+  for (int t = 1; t < T; ++t) pthread_join(th[t], NULL);
+}
+
 uint64_t vco_splitmix64(uint64_t x) {
   x += 0x9e3779b97f4a7c15ull;
   x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
@@ -161,31 +200,48 @@ void vco_dequant_kv(const uint8_t* kcodes, const uint16_t* ks, const uint16_t* k
 /* attention                                                                */
 /* ------------------------------------------------------------------------ */
 
+struct att_ctx {
+  const float* q; const float* k; const float* v; int d; double scale; double* s; const double* p;
+  double l; float* out; long nk;
+};
+static void att_scores(void* c, long lo, long hi) {
+  struct att_ctx* a = (struct att_ctx*)c;
+  for (long t = lo; t < hi; ++t) {
+    double dot = 0.0;
+    for (int ch = 0; ch < a->d; ++ch) dot += (double)a->q[ch] * (double)a->k[(size_t)t * a->d + ch];
+    a->s[t] = dot * a->scale;
+  }
+}
+static void att_values(void* c, long lo, long hi) {
+  struct att_ctx* a = (struct att_ctx*)c;
+  for (long ch = lo; ch < hi; ++ch) {  /* each channel's key loop in order */
+    double acc = 0.0;
+    for (long t = 0; t < a->nk; ++t) acc += a->p[t] * (double)a->v[(size_t)t * a->d + ch];
+    a->out[ch] = a->nk > 0 ? (float)(acc / a->l) : 0.0f;
+  }
+}
+
 void vco_attention(const float* q, int n_q, const float* k, const float* v, int n_keys, int d,
                    const int* lim, float* out) {
   double* s = (double*)malloc(sizeof(double) * (size_t)(n_keys > 0 ? n_keys : 1));
-  double* acc = (double*)malloc(sizeof(double) * (size_t)d);
-  const double scale = 1.0 / sqrt((double)d);
+  double* p = (double*)malloc(sizeof(double) * (size_t)(n_keys > 0 ? n_keys : 1));
   for (int r = 0; r < n_q; ++r) {
-    int nk = lim ? lim[r] : n_keys;
+    const int nk = lim ? lim[r] : n_keys;
+    struct att_ctx a = {q + (size_t)r * d, k, v, d, 1.0 / sqrt((double)d), s, p, 0.0, out + (size_t)r * d, nk};
+    par_for(nk, 4096, att_scores, &a);
     double mx = -INFINITY;
-    for (int t = 0; t < nk; ++t) {
-      double dot = 0.0;
-      for (int c = 0; c < d; ++c) dot += (double)q[(size_t)r * d + c] * (double)k[(size_t)t * d + c];
-      s[t] = dot * scale;
+    for (int t = 0; t < nk; ++t)
       if (s[t] > mx) mx = s[t];
-    }
     double l = 0.0;
-    for (int c = 0; c < d; ++c) acc[c] = 0.0;
     for (int t = 0; t < nk; ++t) {
-      double p = exp(s[t] - mx);
-      l += p;
-      for (int c = 0; c < d; ++c) acc[c] += p * (double)v[(size_t)t * d + c];
+      p[t] = exp(s[t] - mx);
+      l += p[t];
     }
-    for (int c = 0; c < d; ++c) out[(size_t)r * d + c] = nk > 0 ? (float)(acc[c] / l) : 0.0f;
+    a.l = l;
+    par_for(d, nk >= 4096 ? 1 : d, att_values, &a);
   }
   free(s);
-  free(acc);
+  free(p);
 }
 
 /* ------------------------------------------------------------------------ */
@@ -343,13 +399,19 @@ void vco_rope_tables(int max_pos, int d, double theta, float* cos_out, float* si
 static float bfr(float x) { return vco_bf16_to_f32(vco_f32_to_bf16(x)); }
 
 /* y[o] = sum_i x[i] * W[o][i], fp64 accumulate, W bf16 rows. */
-static void matvec(const float* x, const uint16_t* W, int out, int in, float* y) {
-  for (int o = 0; o < out; ++o) {
-    const uint16_t* row = W + (size_t)o * in;
+struct mv_ctx { const float* x; const uint16_t* W; int in; float* y; };
+static void mv_rows(void* c, long lo, long hi) {
+  struct mv_ctx* a = (struct mv_ctx*)c;
+  for (long o = lo; o < hi; ++o) {
+    const uint16_t* row = a->W + (size_t)o * a->in;
     double acc = 0.0;
-    for (int i = 0; i < in; ++i) acc += (double)x[i] * (double)vco_bf16_to_f32(row[i]);
-    y[o] = (float)acc;
+    for (int i = 0; i < a->in; ++i) acc += (double)a->x[i] * (double)vco_bf16_to_f32(row[i]);
+    a->y[o] = (float)acc;
   }
+}
+static void matvec(const float* x, const uint16_t* W, int out, int in, float* y) {
+  struct mv_ctx a = {x, W, in, y};
+  par_for(out, 64, mv_rows, &a);
 }
 
 /* xn = bf16((x * r) * w), r = 1/sqrt(mean(x^2) + eps). */

@@ -25,6 +25,9 @@
 extern "C" {
 #endif
 
+/* Host threads the oracle's matvec/attention use (VCO_THREADS, else all cores). */
+int vco_threads(void);
+
 /* ---- scalar helpers (bit-exact with the device code) -------------------- */
 uint64_t vco_splitmix64(uint64_t x);          /* util.hpp:30 restated */
 float    vco_bf16_to_f32(uint16_t h);

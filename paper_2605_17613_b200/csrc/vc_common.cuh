@@ -5,17 +5,50 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <utility>
+
 #define VC_DEV __device__ __forceinline__
 
 namespace vc {
+
+// ---- programmatic dependent launch (PDL) ----------------------------------
+// Every kernel of the decode step is launched with programmatic stream
+// serialisation: it may start (prologue: barriers, TMEM, tensor-map
+// prefetch, and loads of data no earlier kernel of the step writes -- weights,
+// compressed KV records) while its predecessor drains, and calls pdl_wait()
+// before touching anything the predecessor produces or consumes.  Both are
+// no-ops for a plain launch.
+VC_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+VC_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 // ---- conversions -----------------------------------------------------------
 VC_DEV float bf2f(uint16_t h) { return __uint_as_float(static_cast<uint32_t>(h) << 16); }
 VC_DEV uint16_t f2bf(float f) { return __bfloat16_as_ushort(__float2bfloat16_rn(f)); }
 VC_DEV float h2f(uint16_t h) { return __half2float(__ushort_as_half(h)); }
 VC_DEV uint16_t f2h(float f) { return __half_as_ushort(__float2half_rn(f)); }
+// f32 pair -> packed f16x2, round to nearest even: one F2FP.PACK_AB
+// instead of two F2F (fewer issue slots in the draft kernel's inner loop)
 VC_DEV uint32_t pack_h2(float lo, float hi) {
-  return static_cast<uint32_t>(f2h(lo)) | (static_cast<uint32_t>(f2h(hi)) << 16);
+  const __half2 h = __floats2half2_rn(lo, hi);
+  uint32_t r;
+  memcpy(&r, &h, 4);
+  return r;
 }
 VC_DEV float2 h2_to_f2(uint32_t h) {
   __half2 v;
@@ -157,6 +190,10 @@ VC_DEV void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* ba
           smem_u32(dst)),
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
+}
+// Bulk prefetch of global memory into L2 (no shared-memory destination).
+VC_DEV void prefetch_l2_bulk(const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");
 }
 VC_DEV uint4 lds128(const void* p) {
   uint4 r;

@@ -15,6 +15,8 @@ constexpr int kMaxParts = 512;  // chunks per sequence the combine can merge (25
 template <int D>
 __global__ void combine_kernel(AttnShape s, const AttnSeq* seqs, int max_chunks, int mode,
                                Partials part, uint16_t* out) {
+  pdl_trigger();
+  pdl_wait();
   const AttnSeq sq = seqs[blockIdx.x];
   const int tok = blockIdx.y;
   if (tok >= sq.n_rows) return;
@@ -91,10 +93,9 @@ cudaError_t attention_combine(const AttnShape& s, const AttnSeq* seqs, int n_seq
                               cudaStream_t st) {
   if (n_seq <= 0) return cudaSuccess;
   dim3 grid(n_seq, max_rows, s.n_kv * s.n_rep);
-  if (s.d == 128) combine_kernel<128><<<grid, 128, 0, st>>>(s, seqs, max_chunks, mode, part, out);
-  else if (s.d == 64) combine_kernel<64><<<grid, 64, 0, st>>>(s, seqs, max_chunks, mode, part, out);
-  else return cudaErrorInvalidValue;
-  return cudaGetLastError();
+  if (s.d == 128) return launch_pdl(combine_kernel<128>, grid, dim3(128), 0, st, s, seqs, max_chunks, mode, part, out);
+  if (s.d == 64) return launch_pdl(combine_kernel<64>, grid, dim3(64), 0, st, s, seqs, max_chunks, mode, part, out);
+  return cudaErrorInvalidValue;
 }
 
 }  // namespace vc

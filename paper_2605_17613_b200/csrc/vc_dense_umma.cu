@@ -159,6 +159,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_items = n_seq * row_blocks * s.n_kv * max_chunks;
+  pdl_trigger();
 
   if (threadIdx.x == 0) {
     mbar_init(&q_full, 1);
@@ -189,6 +190,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tmem_fence_after();
   const uint32_t tbase = tmem_base_sh;
+  pdl_wait();  // q rows and the window's new K/V come from the qkv epilogue
 
   if (warp == 0) {
     // ===================== TMA producer =====================
@@ -503,8 +505,8 @@ cudaError_t launch_umma(const DenseMaps& maps, const AttnShape& s, int layer, in
   if (e != cudaSuccess) return e;
   const int grid = n_items < sms ? n_items : sms;
   if (grid <= 0) return cudaSuccess;
-  kern<<<grid, kThreads, smem, st>>>(maps, s, layer, pool_cap, seqs, n_seq, max_chunks, row_blocks, part);
-  return cudaGetLastError();
+  return launch_pdl(kern, dim3(grid), dim3(kThreads), smem, st, maps, s, layer, pool_cap, seqs, n_seq, max_chunks,
+                    row_blocks, part);
 }
 
 PFN_cuTensorMapEncodeTiled_v12000 encoder() {

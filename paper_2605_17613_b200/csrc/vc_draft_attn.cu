@@ -195,7 +195,9 @@ __global__ void __launch_bounds__(kWarps * 32, NREP == 8 ? 3 : VC_DRAFT_MINB) dr
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int TC = (pool.tail_cap + VC_TAIL_CHUNK - 1) / VC_TAIL_CHUNK;
   const int n_tail_ctas = n_seq * s.n_kv * TC;
+  pdl_trigger();
   if (static_cast<int>(blockIdx.x) < n_tail_ctas) {
+    pdl_wait();  // the tail holds this step's new K/V (qkv epilogue)
     const int idx = blockIdx.x;
     const int tc = idx % TC, h = (idx / TC) % s.n_kv, seq = idx / (TC * s.n_kv);
     const AttnSeq sq = seqs[seq];
@@ -308,6 +310,7 @@ __global__ void __launch_bounds__(kWarps * 32, NREP == 8 ? 3 : VC_DRAFT_MINB) dr
   __syncwarp();
   if (n_units > 0) issue(0);
   if (n_units > 1) issue(1);
+  pdl_wait();  // compressed records are static within a step; q and the partials are not
 
   const int hn = lane >> 2;         // head column this lane feeds in B fragments
   const int hc0 = 2 * (lane & 3);   // head columns this lane holds in C fragments
@@ -546,9 +549,8 @@ cudaError_t launch_draft(const AttnShape& s, const QuantPool& pool, int layer, c
   if (e != cudaSuccess) return e;
   if (s.draft_warps <= 0 || s.draft_warps % kWarps || s.draft_min_tasks <= 0) return cudaErrorInvalidValue;
   const int tail_ctas = n_seq * s.n_kv * ((pool.tail_cap + VC_TAIL_CHUNK - 1) / VC_TAIL_CHUNK);
-  kern<<<tail_ctas + s.draft_warps / kWarps, kWarps * 32, smem, st>>>(s, pool, layer, qkv, seqs, n_seq,
-                                                                       max_chunks, part);
-  return cudaGetLastError();
+  return launch_pdl(kern, dim3(tail_ctas + s.draft_warps / kWarps), dim3(kWarps * 32), smem, st, s, pool, layer, qkv,
+                    seqs, n_seq, max_chunks, part);
 }
 
 }  // namespace

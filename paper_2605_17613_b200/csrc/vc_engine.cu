@@ -98,7 +98,10 @@ Engine::~Engine() {
   cudaStreamSynchronize(st_);
   cudaStreamSynchronize(copy_st_);
   for (auto& [k, g] : graphs_) cudaGraphExecDestroy(g);
-  for (auto& [k, e] : xfers_) cudaEventDestroy(e);
+  for (auto& [k, x] : xfers_) {
+    cudaEventDestroy(x.start);
+    cudaEventDestroy(x.done);
+  }
   void* ptrs[] = {weight_blob_, rope_cos_, rope_sin_, full_.k, full_.v, stage_.k, stage_.v,
                   quant_.rec, quant_.ktail, quant_.vtail,
                   x_, xn_, qkv_, attn_, act_, gws_.partial, gws_.counters, ss_part_, logits_,
@@ -785,12 +788,13 @@ void Engine::kernel_bench(int kind, const std::vector<int>& slots, int reps, dou
     const SeqState& s = seqs_.at(slots[i]);
     AttnSeq a{};
     a.slot = slots[i];
-    a.row0 = i;
-    a.n_rows = 1;
+    a.n_rows = kind == 2 ? cfg_.max_x + 1 : 1;  // kind 2: a verify window of max_x+1 rows
+    a.row0 = i * a.n_rows;
+    if ((i + 1) * a.n_rows > Mmax_) throw ContractViolation("kernel_bench: too many rows");
     a.kv_len = s.committed;
     a.n_groups = s.n_groups;
     a.tail_len = s.tail_committed;
-    a.part0 = kind == 0 ? i * draft_parts_per_seq(max_chunks_q_, tail_cap_) : i * max_chunks_d_;
+    a.part0 = kind == 0 ? i * draft_parts_per_seq(max_chunks_q_, tail_cap_) : i * max_chunks_d_ * a.n_rows;
     h[i] = a;
     // algorithmic bytes per (layer, request, kv-head) -- DESIGN.md §Roofline
     if (kind == 0)
@@ -815,10 +819,10 @@ void Engine::kernel_bench(int kind, const std::vector<int>& slots, int reps, dou
         VC_LAUNCH(draft_attention_quant(as, quant_, l, qkv_, seqs_dev_, n, max_chunks_q_, cfg_.quant_bits, part_, st_));
       } else {
         const KvPool pool = cfg_.full_tier == 0 ? full_ : stage_;
-        VC_LAUNCH(dense_attention(as, pool, dense_maps_, l, seqs_dev_, n, max_chunks_d_, 1, part_, st_));
+        VC_LAUNCH(dense_attention(as, pool, dense_maps_, l, seqs_dev_, n, max_chunks_d_, h[0].n_rows, part_, st_));
       }
       VC_CK(cudaEventRecord(ev[2 * k + 1], st_));
-      VC_LAUNCH(attention_combine(as, seqs_dev_, n, kind == 0 ? max_chunks_q_ : max_chunks_d_, 1, kind == 0 ? 0 : 1,
+      VC_LAUNCH(attention_combine(as, seqs_dev_, n, kind == 0 ? max_chunks_q_ : max_chunks_d_, h[0].n_rows, kind == 0 ? 0 : 1,
                                   part_, attn_, st_));
     }
   VC_CK(cudaStreamSynchronize(st_));
@@ -913,27 +917,33 @@ uint64_t Engine::swap_begin(int slot, int stage) {
   VC_CK(cudaEventRecord(ready, st_));
   VC_CK(cudaStreamWaitEvent(copy_st_, ready, 0));
   cudaEventDestroy(ready);
+  Xfer x{};
+  VC_CK(cudaEventCreate(&x.start));
+  VC_CK(cudaEventCreate(&x.done));
+  VC_CK(cudaEventRecord(x.start, copy_st_));
   if (width > 0) {
     VC_CK(cudaMemcpy2DAsync(dk, pitch, hk, pitch, width, n_slices, cudaMemcpyHostToDevice, copy_st_));
     VC_CK(cudaMemcpy2DAsync(dv, pitch, hv, pitch, width, n_slices, cudaMemcpyHostToDevice, copy_st_));
   }
-  cudaEvent_t done;
-  VC_CK(cudaEventCreateWithFlags(&done, cudaEventDisableTiming));
-  VC_CK(cudaEventRecord(done, copy_st_));
+  VC_CK(cudaEventRecord(x.done, copy_st_));
   const uint64_t id = next_xfer_++;
-  xfers_[id] = done;
+  xfers_[id] = x;
   return id;
 }
 
 bool Engine::swap_done(uint64_t id) {
   auto it = xfers_.find(id);
   if (it == xfers_.end()) return true;
-  cudaError_t e = cudaEventQuery(it->second);
+  cudaError_t e = cudaEventQuery(it->second.done);
   if (e == cudaErrorNotReady) return false;
   check_cuda(e, "swap_done");
   // order later compute after the copy
-  VC_CK(cudaStreamWaitEvent(st_, it->second, 0));
-  cudaEventDestroy(it->second);
+  VC_CK(cudaStreamWaitEvent(st_, it->second.done, 0));
+  float ms = 0.f;
+  VC_CK(cudaEventElapsedTime(&ms, it->second.start, it->second.done));
+  h2d_ms_ += ms;
+  cudaEventDestroy(it->second.start);
+  cudaEventDestroy(it->second.done);
   xfers_.erase(it);
   return true;
 }
@@ -941,7 +951,7 @@ bool Engine::swap_done(uint64_t id) {
 void Engine::swap_wait(uint64_t id) {
   auto it = xfers_.find(id);
   if (it == xfers_.end()) return;
-  VC_CK(cudaEventSynchronize(it->second));
+  VC_CK(cudaEventSynchronize(it->second.done));
   swap_done(id);
 }
 

@@ -120,6 +120,8 @@ class Engine {
   uint64_t swap_begin(int slot, int stage);
   bool swap_done(uint64_t id);
   void swap_wait(uint64_t id);
+  // copy-engine time of the completed H2D reloads (CUDA events on the copy stream)
+  double h2d_ms() const { return h2d_ms_; }
 
   // ---- raw access for tests ------------------------------------------
   KvPool full_pool() const { return full_; }
@@ -198,7 +200,11 @@ class Engine {
   std::map<std::string, cudaGraphExec_t> graphs_;
   std::map<std::string, uint64_t> launches_per_graph_;
   // transfers
-  std::map<uint64_t, cudaEvent_t> xfers_;
+  struct Xfer {
+    cudaEvent_t start, done;
+  };
+  std::map<uint64_t, Xfer> xfers_;
+  double h2d_ms_ = 0.0;
   uint64_t next_xfer_ = 1;
   cudaEvent_t ev_a_ = nullptr, ev_b_ = nullptr;
   double device_ms_ = 0.0;

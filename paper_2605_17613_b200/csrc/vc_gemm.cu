@@ -174,10 +174,25 @@ gemm_tma_kernel(const uint16_t* __restrict__ Xt, int Mp, int M, int K,
   }
   __syncthreads();
 
+  pdl_trigger();
   if (warp == kConsumers / 32) {  // ---- producer warp: one lane drives the TMA ring
     if (lane == 0) {
-      int it = 0;
-      for (long g = beg0; g < end; ++g, ++it) {
+      // PDL prologue: the first stages' weight tiles do not depend on the
+      // previous kernel -- stream them while it drains, then wait for it
+      // before the activation tiles (its output)
+      const int pre = static_cast<int>(min(static_cast<long>(ST), end - beg0));
+      for (int i = 0; i < pre; ++i) {
+        const long g = beg0 + i;
+        mbar_expect_tx(&full[i], WB + XB);
+        tma_load_1d(sW + i * WB, Wt + (static_cast<size_t>(g / KT) * KT + g % KT) * 8192, WB, &full[i]);
+      }
+      pdl_wait();
+      for (int i = 0; i < pre; ++i) {
+        const int kt = static_cast<int>((beg0 + i) % KT);
+        tma_load_1d(sX + i * XB, Xt + (static_cast<size_t>(kt) * Mp + m0) * 64, XB, &full[i]);
+      }
+      int it = pre;
+      for (long g = beg0 + pre; g < end; ++g, ++it) {
         const int st = it % ST;
         if (it >= ST) mbar_wait(&empty[st], ((it / ST) - 1) & 1);
         mbar_expect_tx(&full[st], WB + XB);
@@ -190,6 +205,7 @@ gemm_tma_kernel(const uint16_t* __restrict__ Xt, int Mp, int M, int K,
   }
 
   // ---- consumer warps ------------------------------------------------------
+  pdl_wait();  // epilogues read/write buffers the previous kernel touches
   int it = 0;
   long beg = beg0;
   while (beg < end) {
@@ -302,8 +318,8 @@ cudaError_t launch_nt(const uint16_t* Xt, int Mp, int M, int K, const uint16_t* 
   const long T = static_cast<long>(N / kBN) * (K / kBK);
   for (int m0 = 0; m0 < M; m0 += NT) {
     // one launch per NT-row block keeps the schedule independent of M
-    kern<<<dim3(static_cast<unsigned>(grid_of(T))), kThreads, smem, st>>>(Xt, Mp, M, K, Wt, N, m0, ep, ws, mc);
-    e = cudaGetLastError();
+    e = launch_pdl(kern, dim3(static_cast<unsigned>(grid_of(T))), dim3(kThreads), smem, st, Xt, Mp, M, K, Wt, N,
+                   m0, ep, ws, mc);
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;

@@ -45,6 +45,8 @@ __global__ void embed_norm_kernel(const int32_t* tokens, int Mp, const uint16_t*
 // partial sums (fixed order) and normalises its 1024-wide chunk.
 __global__ void rms_apply_kernel(const float* x, const float* ss_part, int H, int Mp,
                                  const uint16_t* w, float eps, uint16_t* xn) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ float r_s;
   const int m = blockIdx.x;
   const int tiles = H / 128;
@@ -62,6 +64,8 @@ __global__ void rms_apply_kernel(const float* x, const float* ss_part, int H, in
 }
 
 __global__ void argmax_kernel(const float* logits, int N, int32_t* out) {
+  pdl_trigger();
+  pdl_wait();
   __shared__ float sv[32];
   __shared__ int si[32];
   const float* row = logits + static_cast<size_t>(blockIdx.x) * N;
@@ -145,14 +149,13 @@ cudaError_t embed_norm(const int32_t* tokens, int M, int Mp, const uint16_t* emb
 cudaError_t rms_apply(const float* x, const float* ss_part, int M, int Mp, int H,
                       const uint16_t* norm_w, float eps, uint16_t* xn, cudaStream_t st) {
   if (M <= 0) return cudaSuccess;
-  rms_apply_kernel<<<dim3(M, (H + 1023) / 1024), 256, 0, st>>>(x, ss_part, H, Mp, norm_w, eps, xn);
-  return cudaGetLastError();
+  return launch_pdl(rms_apply_kernel, dim3(M, (H + 1023) / 1024), dim3(256), 0, st, x, ss_part, H, Mp, norm_w,
+                    eps, xn);
 }
 
 cudaError_t argmax_rows(const float* logits, int M, int N, int32_t* out, cudaStream_t st) {
   if (M <= 0) return cudaSuccess;
-  argmax_kernel<<<M, 1024, 0, st>>>(logits, N, out);
-  return cudaGetLastError();
+  return launch_pdl(argmax_kernel, dim3(M), dim3(1024), 0, st, logits, N, out);
 }
 
 cudaError_t fill_normal_bf16(uint16_t* out, size_t n, uint64_t seed, uint64_t offset, float k,

@@ -137,14 +137,24 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
   double rows_in_window = 0;
   auto window_start = t0;
   const bool bounded = sd.timed_iterations > 0;
+  // planning iteration time: the reference re-plans every iteration
+  // (sim.cpp:238-239); here it tracks the measured wall time of the loop's
+  // iterations (EMA), so reload spans are booked in real link seconds
+  double t_plan = t_iter;
+  const bool adapt = sd.iteration_time <= 0;
+  double stall_ms = 0.0, h2d_ms_at_window = 0.0;
+  auto t_prev = std::chrono::steady_clock::now();
   for (std::int64_t it = 0; !sched.idle() || !ev.arrivals.empty(); ++it) {
     if (it > guard_iters) throw speckv::ConfigError("scheduled loop stalled");
+    if (adapt) sched.set_planning_iteration_time(t_plan);
     if (it == sd.warmup_iterations) {  // open the timed window
       int64_t tk = 0;
       for (int i = 0; i < n; ++i) tk += produced[i];
       tokens_at_window = tk;
       en.reset_timing();
       window_start = std::chrono::steady_clock::now();
+      stall_ms = 0.0;
+      h2d_ms_at_window = en.h2d_ms();
     }
     if (bounded && it == sd.warmup_iterations + sd.timed_iterations) break;
     // 1. kick off this iteration's transfers
@@ -237,6 +247,14 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
     st.verifies += rr.verify_count;
     st.late_transfers += static_cast<int64_t>(rr.late_transfers.size());
     st.iterations += 1;
+    const auto t_now = std::chrono::steady_clock::now();
+    const double dt = std::chrono::duration<double>(t_now - t_prev).count();
+    t_prev = t_now;
+    t_plan = 0.8 * t_plan + 0.2 * dt;
+    // exposed swap time: a session whose reload is late stalls this iteration
+    int stalled = 0;
+    for (const auto& [id, ss] : sched.sessions()) stalled += ss.stalled ? 1 : 0;
+    stall_ms += 1e3 * dt * stalled;
     ev = speckv::StepEvents{};
   }
   const auto t1 = std::chrono::steady_clock::now();
@@ -249,6 +267,8 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
     st.timed_device_ms = en.device_ms();
     st.timed_rows = rows_in_window;
   }
+  st.h2d_ms = en.h2d_ms() - h2d_ms_at_window;
+  st.verify_wait_ms = stall_ms;
   st.mean_accept = st.verifies ? accepted_sum / static_cast<double>(st.verifies) : 0.0;
   if (stats) *stats = st;
   return VC_OK;
