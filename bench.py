@@ -54,9 +54,9 @@ def parse():
     p.add_argument("--tier", default="host", choices=["host", "hbm"])
     p.add_argument("--window", type=int, default=0)
     p.add_argument("--resid-std", type=float, default=-1.0,
-                   help="std of o_proj/down_proj init (-1: calibrated 5e-4; 0: 0.02)")
+                   help="std of o_proj/down_proj init (-1: calibrated 2e-4; 0: 0.02)")
     p.add_argument("--q-std", type=float, default=-1.0,
-                   help="std of the Q projection init (-1: calibrated 5e-3; 0: 0.02)")
+                   help="std of the Q projection init (-1: calibrated 2e-3; 0: 0.02)")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-secondary", action="store_true", help="skip the other tier's line")
     p.add_argument("--stages", type=int, default=4, help="HBM staging slots of the host tier")
@@ -239,8 +239,11 @@ def main():
     shard = weak_shard(B, world, rank)  # this rank's requests (no data-path collective)
     rng = np.random.default_rng(2 + shard.requests[0])
     first = [int(t) for t in rng.integers(0, shape.vocab, B)]
-    rs = args.resid_std if args.resid_std >= 0 else (0.0005 if not args.small else 0.0)
-    qs = args.q_std if args.q_std >= 0 else (0.005 if not args.small else 0.0)
+    # synthetic-init calibration (tools/accept_sweep.py): q_proj
+    # std 2e-3, o/down_proj std 2e-4 give 21.1 accepted drafted tokens per
+    # verify at x=30 (int4, 32K), inside the paper's ~19-23
+    rs = args.resid_std if args.resid_std >= 0 else (0.0002 if not args.small else 0.0)
+    qs = args.q_std if args.q_std >= 0 else (0.002 if not args.small else 0.0)
     slots = list(range(B))
 
     # ---------------- baseline: full-KV greedy decode, same engine, HBM resident
@@ -267,7 +270,10 @@ def main():
         in HBM; tier 1: full KV in pinned host memory, reloaded per verify)."""
         x = args.x or (64 if tier == 1 else 16)
         window = args.window or max(2 * x + 8, 48 if tier == 0 else 256)
-        ev = vc.Engine(shape, max_slots=B, max_ctx=ctx + W + K + 3 * (x + 1) + 8, max_x=x,
+        # the staggered loop reaches steady state only after every request has
+        # drafted and verified once: 2(x+1) ramp iterations precede the W warm-up
+        ramp = max(0, 2 * (x + 1) - W)
+        ev = vc.Engine(shape, max_slots=B, max_ctx=ctx + W + ramp + K + 3 * (x + 1) + 8, max_x=x,
                        quant_bits=args.bits, full_tier=tier, n_stage=args.stages if tier else 1,
                        max_verify=args.stages if tier else max(2, B // (x + 1) + 2), device=local)
         ev.init_weights(seed=0, std=0.02, resid_std=rs, q_std=qs)
@@ -280,8 +286,8 @@ def main():
             dist.barrier()
         torch.cuda.synchronize()
         with Clocks(local) as clk:
-            out, st = ev.run_scheduled(slots, K=(W + K) * (x + 1), x=x, window=window,
-                                       warmup_iterations=W, timed_iterations=K)
+            out, st = ev.run_scheduled(slots, K=(W + ramp + K) * (x + 1), x=x, window=window,
+                                       warmup_iterations=W + ramp, timed_iterations=K)
         torch.cuda.synchronize()
         if dist:
             dist.barrier()
@@ -296,7 +302,7 @@ def main():
         tok_all, (dev_s, wall_s) = reduce_window(float(st["timed_tokens"]),
                                                  [st["timed_device_ms"] / 1e3, st["timed_wall_ms"] / 1e3],
                                                  dist, device="cuda")
-        r = {"x": x, "window": window, "st": st, "meta": meta, "ka": ka, "launches": launches,
+        r = {"x": x, "window": window, "ramp": ramp, "st": st, "meta": meta, "ka": ka, "launches": launches,
              "clocks": clk.summary(), "identical": identical, "compared": int(sum(cmp)),
              "tok": tok_all, "dev_s": dev_s, "wall_s": wall_s}
         return r
@@ -315,13 +321,14 @@ def main():
     achieved = ka_bytes / (ka_ms / 1e3) / 1e9
     traffic, traffic_src = draft_traffic()
     rows = st["timed_rows"]
-    h2d = (rows * (4 + 16) + st["h2d_bytes"] * (K / max(st["iterations"], 1))) / K
+    h2d = (rows * (4 + 16) + st["h2d_bytes"]) / K  # step inputs (token + row descriptor) + KV reloads
 
     def tier_summary(r, tier):
         s = r["st"]
         d = {"value": round(r["tok"] / r["dev_s"], 2), "e2e": round(r["tok"] / r["wall_s"], 2),
              "speedup_vs_full_kv": round((r["tok"] / r["dev_s"]) / base_value, 3),
              "ms_per_step": round(r["dev_s"] * 1e3 / K, 3), "draft_x": r["x"], "lookahead_window": r["window"],
+             "ramp_iterations": r["ramp"],
              "accepted_per_verify": round(s["mean_accept"], 3), "verifies": s["verifies"],
              "tokens_identical_to_full_kv": bool(r["identical"]), "tokens_compared": r["compared"],
              "full_kv_in": "pinned host memory" if tier else "HBM"}
@@ -343,11 +350,12 @@ def main():
             "ms_per_step": round(dev_s * 1e3 / K, 3), "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "bf16",
             "data": f"synthetic (random-init weights N(0,0.02); q_proj N(0,{qs:.4g}), o/down_proj N(0,{rs:.4g}) "
-                    f"calibrated for paper-range acceptance; synthetic 32K prefix KV)",
+                    f"calibrated to the paper's acceptance, 21.1 of x=30; synthetic 32K prefix KV)",
             "config": {"workload": f"configs[1]: {'tiny' if args.small else 'Llama-3-8B shape'}, {ctx} ctx, "
                                    f"int{args.bits} KIVI, batch {B}/GPU, full KV in "
                                    f"{'pinned host memory' if head_tier else 'HBM'}",
                        "global_batch": B * world, "seq_len": ctx, "draft_x": x, "lookahead_window": h["window"],
+                       "ramp_iterations": h["ramp"],
                        "parallelism": f"request-sharded dp{world}",
                        "l2": "inputs larger than L2 (>= 34 GB of weights + compressed KV read per step)"},
             "e2e": {"value": round(tok_all / wall_s, 2), "unit": "tokens/s",

@@ -207,7 +207,7 @@ typedef struct {
   int64_t iterations;
   int64_t verifies;
   int64_t late_transfers;
-  double h2d_bytes;
+  double h2d_bytes;         /* bytes of the reloads completed in the timed window */
   double h2d_ms;            /* copy-engine busy time of the reloads (timed window) */
   double verify_wait_ms;    /* exposed swap time: sum over iterations of (sessions
                                stalled on a late reload) x iteration wall time */

@@ -42,7 +42,10 @@ namespace {
 constexpr int kTile = 128;            // keys per tile (MMA M)
 constexpr int kRows = 80;             // query rows per item (MMA N <= 80: 6 TMEM buffers fit 512 cols)
 constexpr int kChunk = VC_DENSE_CHUNK;
-constexpr float kTau = 8.0f;          // lazy rescale threshold (log2 units)
+#ifndef VC_DENSE_TAU
+#define VC_DENSE_TAU 8.0f
+#endif
+constexpr float kTau = VC_DENSE_TAU;  // lazy rescale threshold (log2 units)
 constexpr int kThreads = 224;     // producer(Q,K) | MMA | 4 softmax | producer(V)
 static_assert(kChunk % kTile == 0, "chunks are whole tiles");
 

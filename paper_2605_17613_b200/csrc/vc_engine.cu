@@ -918,6 +918,7 @@ uint64_t Engine::swap_begin(int slot, int stage) {
   VC_CK(cudaStreamWaitEvent(copy_st_, ready, 0));
   cudaEventDestroy(ready);
   Xfer x{};
+  x.bytes = 2.0 * static_cast<double>(width) * n_slices;
   VC_CK(cudaEventCreate(&x.start));
   VC_CK(cudaEventCreate(&x.done));
   VC_CK(cudaEventRecord(x.start, copy_st_));
@@ -942,6 +943,7 @@ bool Engine::swap_done(uint64_t id) {
   float ms = 0.f;
   VC_CK(cudaEventElapsedTime(&ms, it->second.start, it->second.done));
   h2d_ms_ += ms;
+  h2d_bytes_ += it->second.bytes;
   cudaEventDestroy(it->second.start);
   cudaEventDestroy(it->second.done);
   xfers_.erase(it);

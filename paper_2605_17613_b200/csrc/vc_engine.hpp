@@ -122,6 +122,7 @@ class Engine {
   void swap_wait(uint64_t id);
   // copy-engine time of the completed H2D reloads (CUDA events on the copy stream)
   double h2d_ms() const { return h2d_ms_; }
+  double h2d_bytes() const { return h2d_bytes_; }  // bytes of the completed reloads
 
   // ---- raw access for tests ------------------------------------------
   KvPool full_pool() const { return full_; }
@@ -202,9 +203,10 @@ class Engine {
   // transfers
   struct Xfer {
     cudaEvent_t start, done;
+    double bytes;
   };
   std::map<uint64_t, Xfer> xfers_;
-  double h2d_ms_ = 0.0;
+  double h2d_ms_ = 0.0, h2d_bytes_ = 0.0;
   uint64_t next_xfer_ = 1;
   cudaEvent_t ev_a_ = nullptr, ev_b_ = nullptr;
   double device_ms_ = 0.0;

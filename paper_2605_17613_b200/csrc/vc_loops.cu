@@ -142,7 +142,7 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
   // iterations (EMA), so reload spans are booked in real link seconds
   double t_plan = t_iter;
   const bool adapt = sd.iteration_time <= 0;
-  double stall_ms = 0.0, h2d_ms_at_window = 0.0;
+  double stall_ms = 0.0, h2d_ms_at_window = 0.0, h2d_bytes_at_window = 0.0;
   auto t_prev = std::chrono::steady_clock::now();
   for (std::int64_t it = 0; !sched.idle() || !ev.arrivals.empty(); ++it) {
     if (it > guard_iters) throw speckv::ConfigError("scheduled loop stalled");
@@ -155,6 +155,7 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
       window_start = std::chrono::steady_clock::now();
       stall_ms = 0.0;
       h2d_ms_at_window = en.h2d_ms();
+      h2d_bytes_at_window = en.h2d_bytes();
     }
     if (bounded && it == sd.warmup_iterations + sd.timed_iterations) break;
     // 1. kick off this iteration's transfers
@@ -178,7 +179,6 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
       free_stages.pop_back();
       stage_of[req] = s;
       inflight.push_back({en.swap_begin(slots[req], s), r.id, req});
-      st.h2d_bytes += 2.0 * static_cast<double>(en.seq(slots[req]).committed) * (bpt / 2);
       deferred.pop_front();
     }
     // 2. completions
@@ -268,6 +268,7 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
     st.timed_rows = rows_in_window;
   }
   st.h2d_ms = en.h2d_ms() - h2d_ms_at_window;
+  st.h2d_bytes = en.h2d_bytes() - h2d_bytes_at_window;
   st.verify_wait_ms = stall_ms;
   st.mean_accept = st.verifies ? accepted_sum / static_cast<double>(st.verifies) : 0.0;
   if (stats) *stats = st;
