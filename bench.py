@@ -59,7 +59,7 @@ def parse():
                    help="std of the Q projection init (-1: calibrated 2e-3; 0: 0.02)")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-secondary", action="store_true", help="skip the other tier's line")
-    p.add_argument("--stages", type=int, default=4, help="HBM staging slots of the host tier")
+    p.add_argument("--stages", type=int, default=8, help="HBM staging slots of the host tier")
     p.add_argument("--small", action="store_true", help="tiny model smoke run")
     return p.parse_args()
 
@@ -268,7 +268,7 @@ def main():
     def vericache(tier):
         """One VeriCache run: compressed drafting + full-KV verify (tier 0: full KV
         in HBM; tier 1: full KV in pinned host memory, reloaded per verify)."""
-        x = args.x or (64 if tier == 1 else 16)
+        x = args.x or (96 if tier == 1 else 16)
         window = args.window or max(2 * x + 8, 48 if tier == 0 else 256)
         # the staggered loop reaches steady state only after every request has
         # drafted and verified once: 2(x+1) ramp iterations precede the W warm-up

@@ -62,12 +62,16 @@ typedef struct {
   int n_stage;     /* HBM staging slots for tier 1 */
   int max_verify;  /* verify requests per step */
   int use_graphs;  /* capture steps into CUDA graphs */
+  double drop_ratio; /* > 0: drop-topk compressor (retained fraction c in (0,1));
+                        exclusive with quant_bits (compressor.cpp:245-254) */
 } vc_runtime_desc;
 
-/* Mirrors speckv::CompressedKVMeta (compressor.hpp:56-65) for quant-uniform:
+/* Mirrors speckv::CompressedKVMeta (compressor.hpp:56-65).  Quant-uniform:
  * every position is kept, payload_bytes obeys the size law
  * full_bytes * bit_scheme / 16 (compressor.cpp:96-100, codes only);
- * aux_bytes carries the fp16 scales/zeros the size law does not count.    */
+ * aux_bytes carries the fp16 scales/zeros the size law does not count.
+ * Drop-topk: bit_scheme 16, payload = retained * layers * heads * bytes per
+ * token per head (the same size law over the kept tokens).                */
 typedef struct {
   int bit_scheme;
   int64_t payload_bytes;
@@ -75,6 +79,7 @@ typedef struct {
   int64_t full_bytes;
   int n_groups;
   int tail_tokens;
+  int64_t retained_tokens; /* drop-topk: kept tokens per (layer, head); quant: all */
 } vc_compressed_meta;
 
 typedef struct {
@@ -138,6 +143,10 @@ int vc_compress(vc_engine* e, int slot, vc_compressed_meta* out);
 int vc_compressed_read(vc_engine* e, int slot, int layer, int head, uint32_t* kcodes,
                        uint32_t* ksz, uint32_t* vcodes, uint32_t* vsz, uint16_t* ktail,
                        uint16_t* vtail);
+/* Kept positions (ascending, int32) of one (layer, kv-head) from the most
+ * recent drop-topk vc_compress; *n = retained count.  Positions not listed
+ * are the reference's dropped_indices (compressor.hpp:57-59).              */
+int vc_drop_kept(vc_engine* e, int layer, int head, int32_t* out, int cap, int* n);
 int vc_compressed_geometry(vc_engine* e, int* group, int* words_per_group, int* tail_cap,
                            int* max_groups);
 /* Drop-index generation of the token-dropping compressors, bit-identical
@@ -239,7 +248,8 @@ int vc_quant_kivi_slice(const uint16_t* k, const uint16_t* v, int n_groups, int 
 int vc_attention_probe(vc_engine* e, int slot, int layer, int mode, const uint16_t* q_dev,
                        int n_rows, int kv_len, uint16_t* out_host);
 /* Read n token rows of one (layer, kv-head) slice of a KV pool to host bf16
- * buffers [n][d]: pool 0 = HBM full tier, 1 = staging slots, 2 = host pool. */
+ * buffers [n][d]: pool 0 = HBM full tier, 1 = staging slots, 2 = host pool,
+ * 3 = drop-topk compacted tier. */
 int vc_kv_read(vc_engine* e, int pool, int slot, int layer, int head, int pos, int n, uint16_t* k,
                uint16_t* v);
 /* ws = X[M][K] . W[N][K]^T via the batch-invariant projection GEMM (device). */

@@ -41,12 +41,13 @@ class ModelDesc(C.Structure):
 class RuntimeDesc(C.Structure):
     _fields_ = [("max_slots", C.c_int), ("max_ctx", C.c_int), ("max_x", C.c_int),
                 ("quant_bits", C.c_int), ("full_tier", C.c_int), ("n_stage", C.c_int),
-                ("max_verify", C.c_int), ("use_graphs", C.c_int)]
+                ("max_verify", C.c_int), ("use_graphs", C.c_int), ("drop_ratio", C.c_double)]
 
 
 class CompressedMeta(C.Structure):
     _fields_ = [("bit_scheme", C.c_int), ("payload_bytes", C.c_int64), ("aux_bytes", C.c_int64),
-                ("full_bytes", C.c_int64), ("n_groups", C.c_int), ("tail_tokens", C.c_int)]
+                ("full_bytes", C.c_int64), ("n_groups", C.c_int), ("tail_tokens", C.c_int),
+                ("retained_tokens", C.c_int64)]
 
 
 class SeqState(C.Structure):
@@ -102,6 +103,7 @@ SIGNATURES = {
     "vc_compress": (I, [P, I, C.POINTER(CompressedMeta)]),
     "vc_compressed_read": (I, [P, I, I, I, PU32, PU32, PU32, PU32, PU16, PU16]),
     "vc_compressed_geometry": (I, [P, PI, PI, PI, PI]),
+    "vc_drop_kept": (I, [P, I, I, C.POINTER(C.c_int32), I, PI]),
     "vc_drop_indices": (I64, [I, I, I, I64, D, U64, I, PI64]),
     "vc_update_window": (I, [I, I, I, I, PI64, PI64, PI64, PI64, PI64, I64, PI64]),
     "vc_topk_select": (I, [P, I, I, I, P, P]),

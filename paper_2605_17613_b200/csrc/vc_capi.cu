@@ -83,6 +83,11 @@ int vc_engine_create(const vc_model_desc* model, const vc_runtime_desc* rt, int 
     c.n_stage = rt->n_stage;
     c.max_verify = rt->max_verify;
     c.use_graphs = rt->use_graphs;
+    c.drop_ratio = rt->drop_ratio;
+    if (c.drop_ratio < 0.0 || c.drop_ratio >= 1.0)
+      throw speckv::ConfigError("compressor: drop ratio must be in (0, 1)");
+    if (c.drop_ratio > 0.0 && c.quant_bits != 0)  // speckv::check_mode_exclusivity (compressor.cpp:245-254)
+      throw speckv::ConfigError("compressor: token dropping and quantization are mutually exclusive");
     if (c.max_slots < 1 || c.max_ctx < 1 || c.max_x < 1 || c.max_verify < 1)
       throw speckv::ConfigError("runtime: sizes must be >= 1");
     auto* h = new vc_engine{nullptr};
@@ -191,6 +196,19 @@ int vc_compress(vc_engine* e, int slot, vc_compressed_meta* out) {
     en.compress(slot);
     const auto& m = en.model();
     const vc::SeqState& s = en.seq(slot);
+    if (en.drop_mode()) {
+      const speckv::Bytes bpt = static_cast<speckv::Bytes>(m.d) * 2 * 2;
+      if (out) {
+        out->bit_scheme = 16;
+        out->retained_tokens = s.drop_len;
+        out->payload_bytes = static_cast<int64_t>(s.drop_len) * m.layers * m.n_kv * bpt;
+        out->full_bytes = static_cast<int64_t>(s.committed) * m.layers * m.n_kv * bpt;
+        out->aux_bytes = 0;
+        out->n_groups = 0;
+        out->tail_tokens = 0;
+      }
+      return;
+    }
     // size law of speckv::compress for quant-uniform (compressor.cpp:144-150)
     speckv::CompressorSpec spec;
     spec.kind = speckv::CompressorKind::QuantUniform;
@@ -205,6 +223,24 @@ int vc_compress(vc_engine* e, int slot, vc_compressed_meta* out) {
       out->aux_bytes = groups * (static_cast<int64_t>(m.d) * 4 + VC_QGROUP * 4);
       out->n_groups = s.n_groups;
       out->tail_tokens = s.tail_committed;
+      out->retained_tokens = s.committed;
+    }
+  });
+}
+
+int vc_drop_kept(vc_engine* e, int layer, int head, int32_t* out, int cap, int* n) {
+  return guard([&] {
+    vc::Engine& en = E(e);
+    const auto& m = en.model();
+    if (!en.drop_mode()) throw vc::ContractViolation("drop_kept: no drop-topk tier");
+    if (layer < 0 || layer >= m.layers || head < 0 || head >= m.n_kv) throw vc::ContractViolation("drop_kept: bad slice");
+    const int k = en.last_kept_k();
+    if (n) *n = k;
+    if (out && k > 0) {
+      if (cap < k) throw vc::ContractViolation("drop_kept: capacity");
+      vc::check_cuda(cudaStreamSynchronize(en.stream()), "drop_kept");
+      vc::check_cuda(cudaMemcpy(out, en.last_kept_device() + (static_cast<size_t>(layer) * m.n_kv + head) * k,
+                                static_cast<size_t>(k) * 4, cudaMemcpyDeviceToHost), "drop_kept");
     }
   });
 }
@@ -315,7 +351,8 @@ int vc_topk_select(const float* scores, int rows, int T, int k, int32_t* kept, v
 int vc_key_scores(const uint16_t* keys, int rows, int T, int d, const float* w, float* scores,
                   void* stream) {
   return guard([&] {
-    vc::check_cuda(vc::key_scores(keys, rows, T, d, w, scores, static_cast<cudaStream_t>(stream)), "key_scores");
+    vc::check_cuda(vc::key_scores(keys, rows, T, d, static_cast<size_t>(T) * d, w, scores,
+                                  static_cast<cudaStream_t>(stream)), "key_scores");
   });
 }
 
@@ -555,7 +592,7 @@ int vc_kv_read(vc_engine* e, int pool, int slot, int layer, int head, int pos, i
   return guard([&] {
     vc::Engine& en = E(e);
     const auto& m = en.model();
-    const vc::KvPool p = pool == 1 ? en.stage_pool() : en.full_pool();
+    const vc::KvPool p = pool == 1 ? en.stage_pool() : (pool == 3 ? en.drop_pool() : en.full_pool());
     const size_t slice = (static_cast<size_t>(slot) * m.layers + layer) * m.n_kv + head;
     const size_t off = (slice * p.cap + pos) * m.d;
     const size_t bytes = static_cast<size_t>(n) * m.d * 2;

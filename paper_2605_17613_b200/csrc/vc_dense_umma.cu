@@ -404,30 +404,43 @@ __global__ void __launch_bounds__(kThreads, 1)
         tmem_fence_after();
         const uint32_t tS = tlane + (sb ? kColS1 : kColS0);
         uint8_t* pdst = sP + sb * P_BYTES;
+        // 16 columns of P from S values v (TMEM already waited on)
+        auto p16 = [&](const uint32_t* v, int c, bool track, float& over) {
+#pragma unroll
+          for (int j8 = 0; j8 < 16; j8 += 8) {
+            uint32_t pk[4];
+#pragma unroll
+            for (int j = 0; j < 8; j += 2) {
+              const int col = c + j8 + j;
+              const float2 m = *reinterpret_cast<const float2*>(m_run + col);
+              float x0 = __uint_as_float(v[j8 + j]) * s.scale_log2 - m.x;
+              float x1 = __uint_as_float(v[j8 + j + 1]) * s.scale_log2 - m.y;
+              if (masked_tile) {
+                const int2 lm = *reinterpret_cast<const int2*>(lim_col + col);
+                if (key >= lm.x) x0 = -INFINITY;
+                if (key >= lm.y) x1 = -INFINITY;
+              }
+              if (track) over = fmaxf(over, fmaxf(x0, x1));
+              pk[j >> 1] = pack_bf2(ex2(x0), ex2(x1));
+            }
+            st_shared_v4(pdst + mn_sw128_off(tid, c + j8), pk);
+          }
+        };
+        // 32 columns per TMEM load + wait where they fit (fewer serialised waits)
         auto write_p = [&](bool track, float& over) {
-          for (int c = 0; c < npad; c += 16) {
+          int c = 0;
+          for (; c + 32 <= npad; c += 32) {
+            uint32_t v[32];
+            tmem_ld32(tS + c, v);
+            tmem_wait_ld();
+            p16(v, c, track, over);
+            p16(v + 16, c + 16, track, over);
+          }
+          if (c < npad) {
             uint32_t v[16];
             tmem_ld16(tS + c, v);
             tmem_wait_ld();
-#pragma unroll
-            for (int j8 = 0; j8 < 16; j8 += 8) {
-              uint32_t pk[4];
-#pragma unroll
-              for (int j = 0; j < 8; j += 2) {
-                const int col = c + j8 + j;
-                const float2 m = *reinterpret_cast<const float2*>(m_run + col);
-                float x0 = __uint_as_float(v[j8 + j]) * s.scale_log2 - m.x;
-                float x1 = __uint_as_float(v[j8 + j + 1]) * s.scale_log2 - m.y;
-                if (masked_tile) {
-                  const int2 lm = *reinterpret_cast<const int2*>(lim_col + col);
-                  if (key >= lm.x) x0 = -INFINITY;
-                  if (key >= lm.y) x1 = -INFINITY;
-                }
-                if (track) over = fmaxf(over, fmaxf(x0, x1));
-                pk[j >> 1] = pack_bf2(ex2(x0), ex2(x1));
-              }
-              st_shared_v4(pdst + mn_sw128_off(tid, c + j8), pk);
-            }
+            p16(v, c, track, over);
           }
         };
         // optimistic pass: P with the running max; note how far any score overshoots it

@@ -1,5 +1,6 @@
 // vc_engine.cu -- host side of the B200 decode loop (see vc_engine.hpp).
 #include "vc_engine.hpp"
+#include "vc_topk.h"
 
 #include <cuda_bf16.h>
 
@@ -84,6 +85,9 @@ Engine::Engine(const EngineConfig& cfg, int device) : cfg_(cfg), device_(device)
   if (m.n_q % m.n_kv != 0 || (m.d != 64 && m.d != 128)) throw ContractViolation("unsupported head geometry");
   if (cfg_.quant_bits != 0 && cfg_.quant_bits != 2 && cfg_.quant_bits != 4)
     throw ContractViolation("quant_bits must be 0, 2 or 4");
+  if (cfg_.drop_ratio < 0.0 || cfg_.drop_ratio >= 1.0) throw ContractViolation("drop_ratio must be in [0, 1)");
+  if (cfg_.drop_ratio > 0.0 && cfg_.quant_bits != 0)
+    throw ContractViolation("token-dropping and quantising compressors are exclusive");  // compressor.cpp:245-254
   VC_CK(cudaSetDevice(device_));
   VC_CK(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
   VC_CK(cudaStreamCreateWithFlags(&copy_st_, cudaStreamNonBlocking));
@@ -103,7 +107,7 @@ Engine::~Engine() {
     cudaEventDestroy(x.done);
   }
   void* ptrs[] = {weight_blob_, rope_cos_, rope_sin_, full_.k, full_.v, stage_.k, stage_.v,
-                  quant_.rec, quant_.ktail, quant_.vtail,
+                  quant_.rec, quant_.ktail, quant_.vtail, drop_.k, drop_.v, score_buf_, score_w_, kept_buf_,
                   x_, xn_, qkv_, attn_, act_, gws_.partial, gws_.counters, ss_part_, logits_,
                   tok_in_, tok_out_, part_.o, part_.ml, rows_dev_, seqs_dev_, jobs_dev_};
   for (void* p : ptrs)
@@ -255,6 +259,20 @@ void Engine::alloc_all() {
     draft_warps_ = draft_quant_warps(d, cfg_.quant_bits, m.n_q / m.n_kv);
     if (draft_warps_ <= 0) throw ContractViolation("no draft-attention kernel for this head shape");
   }
+  if (drop_mode()) {
+    // kept tokens + up to kDropAppend exact appended tokens + the draft window
+    constexpr int kDropAppend = 4096;
+    const int kmax = static_cast<int>(std::ceil(cfg_.drop_ratio * cfg_.max_ctx)) + 1;
+    drop_.cap = static_cast<int>(round_up(static_cast<size_t>(kmax) + kDropAppend + cfg_.max_x + 2, 128));
+    drop_.k = dmalloc<uint16_t>(slices * static_cast<size_t>(drop_.cap) * d);
+    drop_.v = dmalloc<uint16_t>(slices * static_cast<size_t>(drop_.cap) * d);
+    max_chunks_x_ = (drop_.cap + VC_DENSE_CHUNK - 1) / VC_DENSE_CHUNK;
+    score_buf_ = dmalloc<float>(static_cast<size_t>(L) * m.n_kv * cap);
+    kept_buf_ = dmalloc<int32_t>(static_cast<size_t>(L) * m.n_kv * kmax);
+    score_w_ = dmalloc<float>(d);
+    std::vector<float> ones(d, 1.0f);  // score = L1 norm of the (post-RoPE) key
+    VC_CK(cudaMemcpy(score_w_, ones.data(), d * 4, cudaMemcpyHostToDevice));
+  }
   max_chunks_d_ = (cap + VC_DENSE_CHUNK - 1) / VC_DENSE_CHUNK;
   // ---- activations ---------------------------------------------------------
   Mmax_ = static_cast<int>(round_up(cfg_.max_slots + cfg_.max_verify * (cfg_.max_x + 1), 64));
@@ -270,6 +288,9 @@ void Engine::alloc_all() {
     if (!make_kv_maps(&dense_maps_, dp, dslices, d) ||
         !make_q_map(&dense_maps_, qkv_, d, m.n_q + 2 * m.n_kv, Mmax_, qkv_n, m.n_q / m.n_kv))
       throw ContractViolation("dense attention: cannot encode TMA tensor maps for this shape");
+    if (drop_mode() && (!make_kv_maps(&drop_maps_, drop_, slices, d) ||
+                        !make_q_map(&drop_maps_, qkv_, d, m.n_q + 2 * m.n_kv, Mmax_, qkv_n, m.n_q / m.n_kv)))
+      throw ContractViolation("drop tier: cannot encode TMA tensor maps for this shape");
   }
   act_ = dmalloc<uint16_t>(static_cast<size_t>(Mmax_ + 128) * F);
   {
@@ -291,7 +312,8 @@ void Engine::alloc_all() {
   tok_in_ = dmalloc<int32_t>(Mmax_);
   tok_out_ = dmalloc<int32_t>(Mmax_);
   const size_t prow_draft =
-      static_cast<size_t>(cfg_.max_slots + 4) * draft_parts_per_seq(max_chunks_q_, tail_cap_);
+      static_cast<size_t>(cfg_.max_slots + 4) *
+      (drop_mode() ? max_chunks_x_ : draft_parts_per_seq(max_chunks_q_, tail_cap_));
   const size_t prow_dense = static_cast<size_t>(Mmax_) * max_chunks_d_;
   const size_t prow = (prow_draft + prow_dense) * m.n_q;
   part_.o = dmalloc<float>(prow * d);
@@ -509,7 +531,7 @@ void Engine::quantise_groups(int slot, int g0, int ng, const KvPool& src, int sr
 }
 
 void Engine::compress(int slot) {
-  if (cfg_.quant_bits == 0) throw ContractViolation("compress: compressed tier disabled");
+  if (cfg_.quant_bits == 0 && !drop_mode()) throw ContractViolation("compress: compressed tier disabled");
   SeqState& s = seqs_.at(slot);
   const auto& m = cfg_.model;
   KvPool src = full_;
@@ -520,6 +542,10 @@ void Engine::compress(int slot) {
     swap_wait(id);
     src = stage_;
     src_slot = 0;
+  }
+  if (drop_mode()) {
+    compress_drop(slot, src, src_slot);
+    return;
   }
   const int ng = std::min(s.committed / VC_QGROUP, quant_.cap / VC_QGROUP);
   quantise_groups(slot, 0, ng, src, src_slot);
@@ -533,9 +559,36 @@ void Engine::compress(int slot) {
   VC_CK(cudaStreamSynchronize(st_));
 }
 
+// Drop-topk compress: per (layer, kv head) keep k = llround(c * T) tokens with
+// the highest key scores (ties -> lower position), compacted in position
+// order into the drop tier.  Count rule and error of speckv::compress
+// (/root/reference/proj/src/compressor.cpp:152-158); equal count per head
+// within a layer (the shape law, :83-86) by construction.
+void Engine::compress_drop(int slot, const KvPool& src, int src_slot) {
+  SeqState& s = seqs_.at(slot);
+  const auto& m = cfg_.model;
+  const int n_slices = m.layers * m.n_kv;
+  const int T = s.committed;
+  const long long k = std::llround(cfg_.drop_ratio * static_cast<double>(T));
+  if (k < 1) throw ContractViolation("compress: drop ratio retains < 1 token");
+  if (k + cfg_.max_x + 2 > drop_.cap) throw ContractViolation("compress: drop tier capacity exceeded");
+  const uint16_t* keys = src.k + static_cast<size_t>(src_slot) * n_slices * src.cap * m.d;
+  VC_LAUNCH(key_scores(keys, n_slices, T, m.d, static_cast<size_t>(src.cap) * m.d, score_w_, score_buf_, st_));
+  VC_LAUNCH(topk_select(score_buf_, n_slices, T, static_cast<int>(k), kept_buf_, st_));
+  VC_LAUNCH(gather_kept(src, src_slot, kept_buf_, static_cast<int>(k), drop_, slot, n_slices, m.d, st_));
+  last_kept_k_ = static_cast<int>(k);
+  s.drop_len = static_cast<int>(k);
+  s.n_groups = 0;
+  s.tail_committed = 0;
+  s.draft_len = 0;
+  s.drafted.clear();
+  VC_CK(cudaStreamSynchronize(st_));
+}
+
 size_t Engine::compressed_bytes(int slot) const {
   const SeqState& s = seqs_.at(slot);
   const auto& m = cfg_.model;
+  if (drop_mode()) return static_cast<size_t>(s.drop_len) * m.layers * m.n_kv * m.d * 2 * 2;
   const size_t per_group = static_cast<size_t>(VC_QGROUP) * m.d * cfg_.quant_bits / 8 * 2  // K+V codes
                            + static_cast<size_t>(m.d) * 4 + VC_QGROUP * 4;                  // scales
   return per_group * s.n_groups * m.layers * m.n_kv;
@@ -582,6 +635,7 @@ void Engine::enqueue_forward(int M, int n_draft, int n_dense1, int n_densev, int
   eq.layers = L;
   eq.full = full_;
   eq.stage = stage_;
+  eq.drop = drop_;
   eq.draft = quant_;
   GemmEpilogue er;
   er.kind = Epi::Residual;
@@ -601,7 +655,10 @@ void Engine::enqueue_forward(int M, int n_draft, int n_dense1, int n_densev, int
     eq.layer = l;
     VC_LAUNCH(gemm(xn_, M, M, H, w_.wqkv[l], qkv_n, eq, gws_, st_));
     trace("qkv", qkv_, static_cast<size_t>(M) * qkv_n * 2);
-    if (n_draft > 0) {
+    if (n_draft > 0 && drop_mode()) {
+      VC_LAUNCH(dense_attention(as, drop_, drop_maps_, l, seqs_dev_, n_draft, max_chunks_x_, 1, part_, st_));
+      VC_LAUNCH(attention_combine(as, seqs_dev_, n_draft, max_chunks_x_, 1, 1, part_, attn_, st_));
+    } else if (n_draft > 0) {
       VC_LAUNCH(draft_attention_quant(as, quant_, l, qkv_, seqs_dev_, n_draft, max_chunks_q_,
                                       cfg_.quant_bits, part_, st_));
       VC_LAUNCH(attention_combine(as, seqs_dev_, n_draft, max_chunks_q_, 1, 0, part_, attn_, st_));
@@ -659,7 +716,16 @@ void Engine::run_step(const std::vector<StepItem>& items, std::vector<int32_t>& 
     AttnSeq a{};
     a.row0 = M;
     a.n_rows = n;
-    if (it.mode == RowMode::Draft) {
+    if (it.mode == RowMode::Draft && drop_mode()) {
+      // drop tier: dense attention over the compacted kept + appended tokens
+      if (n != 1) throw ContractViolation("draft rows take one token");
+      if (s.drop_len + s.draft_len + 1 > drop_.cap) throw ContractViolation("drop tier full");
+      h_tok[M] = it.tokens[0];
+      h_rows[M] = RowDest{3, it.slot, s.drop_len + s.draft_len, s.committed + s.draft_len};
+      a.slot = it.slot;
+      a.kv_len = s.drop_len + s.draft_len + 1;
+      drafts.push_back(a);
+    } else if (it.mode == RowMode::Draft) {
       if (cfg_.quant_bits == 0 || n != 1) throw ContractViolation("draft rows need the compressed tier");
       if (s.tail_committed + s.draft_len + 1 > tail_cap_) throw ContractViolation("draft window overflow");
       h_tok[M] = it.tokens[0];
@@ -693,7 +759,7 @@ void Engine::run_step(const std::vector<StepItem>& items, std::vector<int32_t>& 
     throw ContractViolation("run_step: too many sequences");
   // partial-row offsets (units of Hq partial rows)
   int off = 0;
-  for (auto& a : drafts) { a.part0 = off; off += draft_parts_per_seq(max_chunks_q_, tail_cap_); }
+  for (auto& a : drafts) { a.part0 = off; off += drop_mode() ? max_chunks_x_ : draft_parts_per_seq(max_chunks_q_, tail_cap_); }
   for (auto& a : dense1) { a.part0 = off; off += max_chunks_d_ * a.n_rows; }
   for (auto& a : densev) { a.part0 = off; off += max_chunks_d_ * a.n_rows; }
   // Bucket the step shape (padding rows / empty sequences) so a handful of
@@ -881,7 +947,13 @@ std::vector<int32_t> Engine::accept_commit(int slot, const std::vector<int32_t>&
     VC_CK(cudaMemcpy2DAsync(hk, pitch, sk, pitch, width, n_slices, cudaMemcpyDeviceToHost, st_));
     VC_CK(cudaMemcpy2DAsync(hv, pitch, sv, pitch, width, n_slices, cudaMemcpyDeviceToHost, st_));
   }
-  if (cfg_.quant_bits > 0 && (s.n_groups > 0 || s.tail_committed > 0 || x > 0)) {
+  if (drop_mode()) {
+    // the accepted rows' exact K/V (full tier) are appended to the compacted
+    // tier; the draft window's entries beyond them are simply overwritten
+    if (s.drop_len + (now - old) + cfg_.max_x + 2 > drop_.cap) throw ContractViolation("drop tier full");
+    VC_LAUNCH(copy_rows(src, src_slot, old, now - old, drop_, slot, s.drop_len, m.layers * m.n_kv, m.d, st_));
+    s.drop_len += now - old;
+  } else if (cfg_.quant_bits > 0 && (s.n_groups > 0 || s.tail_committed > 0 || x > 0)) {
     const int ng_now = std::min(now / VC_QGROUP, quant_.cap / VC_QGROUP);
     quantise_groups(slot, s.n_groups, ng_now - s.n_groups, src, src_slot);
     s.n_groups = ng_now;

@@ -37,6 +37,7 @@ struct EngineConfig {
   int max_ctx = 4096;   // token capacity per request (prefix + generated)
   int max_x = 16;       // largest draft horizon
   int quant_bits = 4;   // 4 or 2; 0 disables the compressed tier
+  double drop_ratio = 0; // > 0: drop-topk compressed tier (retained fraction c), exclusive with quant
   int full_tier = 0;    // 0: full KV in HBM; 1: pinned host pool + staging
   int n_stage = 2;      // HBM staging slots (tier 1)
   int max_verify = 2;   // verify requests per step
@@ -60,6 +61,7 @@ struct SeqState {
   int n_groups = 0;       // quantised groups in the compressed tier
   int tail_committed = 0; // exact tokens in the draft tail (committed - n_groups*G)
   int draft_len = 0;      // drafted tokens of the open round (their KV in the tail)
+  int drop_len = 0;       // drop tier: kept prefix tokens + exact tokens appended since
   std::vector<int32_t> drafted;
   std::vector<int32_t> history;  // every emitted token
 };
@@ -128,6 +130,11 @@ class Engine {
   KvPool full_pool() const { return full_; }
   KvPool stage_pool() const { return stage_; }
   QuantPool quant_pool() const { return quant_; }
+  KvPool drop_pool() const { return drop_; }
+  bool drop_mode() const { return cfg_.drop_ratio > 0.0; }
+  // kept positions (ascending) of the last drop-mode compress, row = layer*n_kv+head
+  int last_kept_k() const { return last_kept_k_; }
+  const int32_t* last_kept_device() const { return kept_buf_; }
   uint16_t* host_pool_k() const { return host_k_; }
   uint16_t* host_pool_v() const { return host_v_; }
   cudaStream_t stream() const { return st_; }
@@ -165,6 +172,7 @@ class Engine {
   void enqueue_forward(int M, int n_draft, int n_dense1, int n_densev, int max_rows_v,
                        bool want_logits);
   void quantise_groups(int slot, int g0, int ng, const KvPool& src, int src_slot);
+  void compress_drop(int slot, const KvPool& src, int src_slot);
 
   EngineConfig cfg_;
   int device_ = 0;
@@ -176,6 +184,15 @@ class Engine {
   KvPool full_{}, stage_{};
   DenseMaps dense_maps_{};  // tensor maps of the HBM pool the dense kernel reads (tier 0 full, tier 1 stage)
   QuantPool quant_{};
+  // drop-topk tier: compacted bf16 K/V of the kept tokens (+ appended exact
+  // tokens + the open draft window), read by the dense kernel
+  KvPool drop_{};
+  DenseMaps drop_maps_{};
+  int max_chunks_x_ = 0;
+  float* score_buf_ = nullptr;  // [layers*n_kv][max_ctx] key scores of one compress
+  float* score_w_ = nullptr;    // [d] per-channel score weights (ones)
+  int32_t* kept_buf_ = nullptr; // [layers*n_kv][k] kept positions of the last compress
+  int last_kept_k_ = 0;
   uint16_t *host_k_ = nullptr, *host_v_ = nullptr;
   int max_chunks_q_ = 0, max_chunks_d_ = 0, tail_cap_ = 0, Mmax_ = 0;
   int draft_warps_ = 0, draft_min_tasks_ = 4;  // quantised draft-attention work split

@@ -133,7 +133,7 @@ __device__ void epilogue_pass(const float* sT, int mbase, int M, int Mp, int n0,
         if (rd.kind == 1) {
           dst = (is_v ? ep.draft.vtail : ep.draft.ktail) + (slice * ep.draft.tail_cap + rd.pos) * d;
         } else {
-          const KvPool& p = rd.kind == 0 ? ep.full : ep.stage;
+          const KvPool& p = rd.kind == 0 ? ep.full : (rd.kind == 2 ? ep.stage : ep.drop);
           dst = (is_v ? p.v : p.k) + (slice * p.cap + rd.pos) * d;
         }
         dst[jj] = ha;

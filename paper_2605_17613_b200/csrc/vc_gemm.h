@@ -10,7 +10,7 @@ namespace vc {
 
 // Where a row's freshly computed K/V go (QKV epilogue).
 struct RowDest {
-  int kind;  // 0: full pool, 2: staging pool (slot, pos); 1: draft tail (pos = tail index); -1: none
+  int kind;  // 0: full pool, 2: staging pool, 3: drop pool (slot, pos); 1: draft tail (pos = tail index); -1: none
   int slot;
   int pos;       // position inside the destination (absolute, or tail index for kind 1)
   int rope_pos;  // absolute position (RoPE)
@@ -34,7 +34,7 @@ struct GemmEpilogue {
   const float* rope_cos = nullptr;
   const float* rope_sin = nullptr;
   int n_q = 0, n_kv = 0, d = 0, layer = 0, layers = 0;
-  KvPool full{}, stage{};
+  KvPool full{}, stage{}, drop{};
   QuantPool draft{};
 };
 
@@ -74,5 +74,12 @@ cudaError_t fill_const_bf16(uint16_t* out, size_t n, uint16_t value, cudaStream_
 // slot from a full-style pool into the draft tail (tail index 0..n-1).
 cudaError_t tail_refill(KvPool src, int src_slot, int src_pos, int n, QuantPool dst, int dst_slot,
                         int layers, int n_kv, int d, cudaStream_t st);
+// Drop tier: rows kept[slice][0..k) of every (layer, head) slice of src_slot
+// -> positions 0..k of dst_slot (compacted, position order).
+cudaError_t gather_kept(KvPool src, int src_slot, const int32_t* kept, int k, KvPool dst, int dst_slot,
+                        int n_slices, int d, cudaStream_t st);
+// Copy token rows [src_pos, src_pos+n) of every slice to [dst_pos, dst_pos+n).
+cudaError_t copy_rows(KvPool src, int src_slot, int src_pos, int n, KvPool dst, int dst_slot, int dst_pos,
+                      int n_slices, int d, cudaStream_t st);
 
 }  // namespace vc

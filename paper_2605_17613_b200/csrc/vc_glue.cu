@@ -132,6 +132,40 @@ __global__ void tail_refill_kernel(KvPool src, int src_slot, int src_pos, int n,
   }
 }
 
+// one CTA per (slice, 64-row block); 16-byte copies
+__global__ void gather_kept_kernel(KvPool src, int src_slot, const int32_t* kept, int k, KvPool dst, int dst_slot,
+                                   int n_slices, int d) {
+  const int sl = blockIdx.y;
+  const size_t s_slice = static_cast<size_t>(src_slot) * n_slices + sl;
+  const size_t d_slice = static_cast<size_t>(dst_slot) * n_slices + sl;
+  const int vec = d / 8;  // uint4 per row
+  const int r0 = blockIdx.x * 64;
+  const int32_t* kp = kept + static_cast<size_t>(sl) * k;
+  for (int i = threadIdx.x; i < 64 * vec; i += blockDim.x) {
+    const int r = r0 + i / vec, c = i % vec;
+    if (r >= k) break;
+    const size_t so = (s_slice * src.cap + kp[r]) * d, dof = (d_slice * dst.cap + r) * d;
+    reinterpret_cast<uint4*>(dst.k + dof)[c] = reinterpret_cast<const uint4*>(src.k + so)[c];
+    reinterpret_cast<uint4*>(dst.v + dof)[c] = reinterpret_cast<const uint4*>(src.v + so)[c];
+  }
+}
+
+__global__ void copy_rows_kernel(KvPool src, int src_slot, int src_pos, int n, KvPool dst, int dst_slot,
+                                 int dst_pos, int n_slices, int d) {
+  const int sl = blockIdx.x;
+  const size_t s_slice = static_cast<size_t>(src_slot) * n_slices + sl;
+  const size_t d_slice = static_cast<size_t>(dst_slot) * n_slices + sl;
+  const uint4* sk = reinterpret_cast<const uint4*>(src.k + (s_slice * src.cap + src_pos) * d);
+  const uint4* sv = reinterpret_cast<const uint4*>(src.v + (s_slice * src.cap + src_pos) * d);
+  uint4* dk = reinterpret_cast<uint4*>(dst.k + (d_slice * dst.cap + dst_pos) * d);
+  uint4* dv = reinterpret_cast<uint4*>(dst.v + (d_slice * dst.cap + dst_pos) * d);
+  const int words = n * d / 8;
+  for (int i = threadIdx.x; i < words; i += blockDim.x) {
+    dk[i] = sk[i];
+    dv[i] = sv[i];
+  }
+}
+
 int grid_for(size_t n, int threads) {
   size_t b = (n + threads - 1) / threads;
   return static_cast<int>(b < 148 * 16 ? (b == 0 ? 1 : b) : 148 * 16);
@@ -175,6 +209,20 @@ cudaError_t tail_refill(KvPool src, int src_slot, int src_pos, int n, QuantPool 
                         int layers, int n_kv, int d, cudaStream_t st) {
   if (n <= 0) return cudaSuccess;
   tail_refill_kernel<<<layers * n_kv, 256, 0, st>>>(src, src_slot, src_pos, n, dst, dst_slot, layers, n_kv, d);
+  return cudaGetLastError();
+}
+
+cudaError_t gather_kept(KvPool src, int src_slot, const int32_t* kept, int k, KvPool dst, int dst_slot,
+                        int n_slices, int d, cudaStream_t st) {
+  if (k <= 0 || n_slices <= 0) return cudaSuccess;
+  gather_kept_kernel<<<dim3((k + 63) / 64, n_slices), 256, 0, st>>>(src, src_slot, kept, k, dst, dst_slot, n_slices, d);
+  return cudaGetLastError();
+}
+
+cudaError_t copy_rows(KvPool src, int src_slot, int src_pos, int n, KvPool dst, int dst_slot, int dst_pos,
+                      int n_slices, int d, cudaStream_t st) {
+  if (n <= 0 || n_slices <= 0) return cudaSuccess;
+  copy_rows_kernel<<<n_slices, 256, 0, st>>>(src, src_slot, src_pos, n, dst, dst_slot, dst_pos, n_slices, d);
   return cudaGetLastError();
 }
 

@@ -15,8 +15,11 @@
 #include <chrono>
 #include <cmath>
 #include <cstring>
+#include <algorithm>
+#include <cstdlib>
 #include <deque>
 #include <map>
+#include <set>
 
 #include "speckv_b200.hpp"
 #include "vc_api.h"
@@ -49,7 +52,7 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
   const auto& cfgE = en.config();
   const bool staged = cfgE.full_tier == 1;
   if (sd.x < 1 || sd.x > cfgE.max_x) throw speckv::ConfigError("scheduled: x out of [1, max_x]");
-  if (cfgE.quant_bits == 0) throw vc::ContractViolation("scheduled: needs the compressed tier");
+  if (cfgE.quant_bits == 0 && cfgE.drop_ratio <= 0.0) throw vc::ContractViolation("scheduled: needs a compressed tier");
   const size_t bpt = en.full_kv_bytes_per_token();
 
   // ---- measure T_iter if not given: one draft step over every request ----
@@ -127,7 +130,11 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
     int req;
   };
   std::vector<Xfer> inflight;
-  std::deque<speckv::Reservation> deferred;  // kickoffs waiting for a staging slot
+  std::set<speckv::ReservationId> kicked;  // reloads already started
+  static const bool early_kick = [] {
+    const char* v = std::getenv("VC_EARLY_KICK");
+    return !(v && v[0] == '0');
+  }();
   vc_sched_stats st{};
   double accepted_sum = 0;
   const auto t0 = std::chrono::steady_clock::now();
@@ -158,28 +165,35 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
       h2d_bytes_at_window = en.h2d_bytes();
     }
     if (bounded && it == sd.warmup_iterations + sd.timed_iterations) break;
-    // 1. kick off this iteration's transfers
+    // 1. kick off transfers.  The reference starts a reload at its span_begin
+    // (pending_kickoffs, sim.cpp:243-249).  The copy stream is a FIFO link, so
+    // starting a booked reload as soon as a staging slot is free (earliest
+    // verify first) can only make it land earlier: the link never idles while
+    // a booked reload waits.  VC_EARLY_KICK=0 restores span_begin kickoffs.
     for (const auto& r : sched.pending_kickoffs()) {
-      if (r.bytes == 0) {  // arrival load: the compressed tier is already resident
+      if (r.bytes == 0 || !staged) {  // arrival load (compressed tier resident) / tier 0
         ev.completed_transfers.push_back(r.id);
         continue;
       }
-      deferred.push_back(r);
     }
-    while (!deferred.empty()) {
-      const auto r = deferred.front();
-      const int req = static_cast<int>(r.request_id);
-      if (!staged) {
-        ev.completed_transfers.push_back(r.id);
-        deferred.pop_front();
-        continue;
+    if (staged) {
+      std::vector<speckv::Reservation> want;
+      for (const auto& [id, ss] : sched.sessions())
+        if (ss.pending && ss.pending->bytes > 0 && !kicked.count(ss.pending->id) &&
+            (early_kick || ss.pending->span_begin <= sched.iteration()))
+          want.push_back(*ss.pending);
+      std::sort(want.begin(), want.end(), [](const speckv::Reservation& a, const speckv::Reservation& b) {
+        return a.verify_iteration != b.verify_iteration ? a.verify_iteration < b.verify_iteration : a.id < b.id;
+      });
+      for (const auto& r : want) {
+        if (free_stages.empty()) break;
+        const int req = static_cast<int>(r.request_id);
+        const int s = free_stages.back();
+        free_stages.pop_back();
+        stage_of[req] = s;
+        inflight.push_back({en.swap_begin(slots[req], s), r.id, req});
+        kicked.insert(r.id);
       }
-      if (free_stages.empty()) break;
-      const int s = free_stages.back();
-      free_stages.pop_back();
-      stage_of[req] = s;
-      inflight.push_back({en.swap_begin(slots[req], s), r.id, req});
-      deferred.pop_front();
     }
     // 2. completions
     for (size_t i = 0; i < inflight.size();) {

@@ -19,12 +19,12 @@ VC_DEV uint32_t fkey(float f) {
   return (u & 0x80000000u) ? ~u : (u | 0x80000000u);
 }
 
-__global__ void key_scores_kernel(const uint16_t* keys, int rows, int T, int d, const float* w,
-                                  float* scores) {
+__global__ void key_scores_kernel(const uint16_t* keys, int rows, int T, int d, size_t pitch,
+                                  const float* w, float* scores) {
   const size_t total = static_cast<size_t>(rows) * T;
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<size_t>(gridDim.x) * blockDim.x) {
-    const uint16_t* k = keys + i * d;
+    const uint16_t* k = keys + (i / T) * pitch + (i % T) * d;
     float s = 0.f;
     for (int c = 0; c < d; ++c) s = __fmaf_rn(fabsf(bf2f(k[c])), w[c], s);  // channel order
     scores[i] = s;
@@ -122,12 +122,12 @@ __global__ void __launch_bounds__(kThreads) topk_kernel(const float* scores, int
 
 }  // namespace
 
-cudaError_t key_scores(const uint16_t* keys, int rows, int T, int d, const float* w, float* scores,
-                       cudaStream_t st) {
+cudaError_t key_scores(const uint16_t* keys, int rows, int T, int d, size_t row_pitch, const float* w,
+                       float* scores, cudaStream_t st) {
   const size_t n = static_cast<size_t>(rows) * T;
   if (n == 0) return cudaSuccess;
   const int grid = static_cast<int>(n / 256 + 1 < 148 * 16 ? n / 256 + 1 : 148 * 16);
-  key_scores_kernel<<<grid, 256, 0, st>>>(keys, rows, T, d, w, scores);
+  key_scores_kernel<<<grid, 256, 0, st>>>(keys, rows, T, d, row_pitch, w, scores);
   return cudaGetLastError();
 }
 

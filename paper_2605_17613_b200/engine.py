@@ -101,14 +101,17 @@ class Engine:
     """One serving instance on one GPU (vc_engine)."""
 
     def __init__(self, model: ModelShape, *, max_slots=1, max_ctx=4096, max_x=16, quant_bits=4,
-                 full_tier=0, n_stage=2, max_verify=2, use_graphs=True, device=0):
+                 full_tier=0, n_stage=2, max_verify=2, use_graphs=True, device=0, drop_ratio=0.0):
+        """quant_bits > 0: quant-uniform compressor (KIVI int4/int2);
+        drop_ratio in (0, 1): drop-topk compressor keeping llround(c*T) tokens per
+        (layer, head) -- the two are exclusive (compressor.cpp:245-254)."""
         self.lib = _lib.load()
         self.model = model
         self.max_x = max_x
         md = _lib.ModelDesc(model.vocab, model.hidden, model.layers, model.n_q, model.n_kv,
                             model.d_head, model.ffn, model.rope_theta, model.rms_eps)
         rt = _lib.RuntimeDesc(max_slots, max_ctx, max_x, quant_bits, full_tier, n_stage,
-                              max_verify, int(use_graphs))
+                              max_verify, int(use_graphs), float(drop_ratio))
         h = C.c_void_p()
         check(self.lib.vc_engine_create(C.byref(md), C.byref(rt), device, C.byref(h)))
         self.h = h
@@ -194,6 +197,14 @@ class Engine:
         m = _lib.CompressedMeta()
         check(self.lib.vc_compress(self.h, slot, C.byref(m)))
         return {f: getattr(m, f) for f, _ in m._fields_}
+
+    def drop_kept(self, layer, head):
+        """Kept positions (ascending) of one (layer, head) from the last drop-topk compress."""
+        n = C.c_int()
+        check(self.lib.vc_drop_kept(self.h, layer, head, None, 0, C.byref(n)))
+        out = np.zeros(max(n.value, 1), np.int32)
+        check(self.lib.vc_drop_kept(self.h, layer, head, _ptr(out, C.c_int32), out.size, C.byref(n)))
+        return out[: n.value]
 
     def compressed_geometry(self):
         g, w, t, mg = C.c_int(), C.c_int(), C.c_int(), C.c_int()
@@ -318,7 +329,7 @@ class Engine:
 
     # ---- probes -----------------------------------------------------------------
     def kv_read(self, pool, slot, layer, head, pos, n):
-        """pool 0 full (HBM), 1 staging, 2 host; returns bf16 bits k, v [n][d]."""
+        """pool 0 full (HBM), 1 staging, 2 host, 3 drop tier; returns bf16 bits k, v [n][d]."""
         d = self.model.d_head
         k = np.zeros((n, d), np.uint16)
         v = np.zeros_like(k)
