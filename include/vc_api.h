@@ -117,7 +117,8 @@ int vc_engine_stats(vc_engine* e, uint64_t* kernel_launches, uint64_t* weight_by
 int vc_engine_timing(vc_engine* e, double* device_ms, int64_t* steps, int reset);
 /* Isolated timing of one kernel family over every layer for the given
  * requests: kind 0 draft attention, 1 dense attention (one decode row),
- * 2 dense attention of a verify window (max_x+1 rows).  *bytes = the
+ * 2 dense attention of a verify window (max_x+1 rows), 3 drafting over the
+ * drop-topk tier (dense kernel, kept + appended tokens).  *bytes = the
  * algorithmic bytes one launch-set moves.           */
 int vc_kernel_bench(vc_engine* e, int kind, const int* slots, int n, int reps, double* ms,
                     double* bytes);

@@ -33,6 +33,10 @@ namespace {
 
 constexpr int kG = VC_QGROUP;
 constexpr int kWarps = 4;
+#ifndef VC_DRAFT_STAGES
+#define VC_DRAFT_STAGES 2  // unit records in flight per warp
+#endif
+constexpr int kStages = VC_DRAFT_STAGES;
 #ifndef VC_DRAFT_MINB
 #define VC_DRAFT_MINB 4  // resident CTAs/SM the n_rep<=4 register budget targets
 #endif
@@ -190,7 +194,7 @@ __global__ void __launch_bounds__(kWarps * 32, NREP == 8 ? 3 : VC_DRAFT_MINB) dr
   // per-warp q heads (bf16); the tail CTAs reuse it for NREP*D fp32 q values
   __shared__ __align__(16) uint16_t sq_q[kWarps][NREP * D];
   static_assert(kWarps * 2 >= 4, "tail q fits");
-  __shared__ __align__(8) uint64_t bars[kWarps][2];
+  __shared__ __align__(8) uint64_t bars[kWarps][kStages];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int TC = (pool.tail_cap + VC_TAIL_CHUNK - 1) / VC_TAIL_CHUNK;
@@ -266,7 +270,7 @@ __global__ void __launch_bounds__(kWarps * 32, NREP == 8 ? 3 : VC_DRAFT_MINB) dr
   Cursor cur = pc; // (sequence, head) whose partial the accumulators hold
   int ppart = 0;   // producer unit within its group
 
-  uint32_t* stage0 = dsm + static_cast<size_t>(warp) * 2 * GEO::STAGE;
+  uint32_t* stage0 = dsm + static_cast<size_t>(warp) * kStages * GEO::STAGE;
   uint64_t* bar = bars[warp];
   auto issue = [&](int st) {  // one bulk copy of the producer's next unit record
     const uint32_t* src = pc.slice + static_cast<size_t>(pc.g) * GEO::GREC;
@@ -303,13 +307,11 @@ __global__ void __launch_bounds__(kWarps * 32, NREP == 8 ? 3 : VC_DRAFT_MINB) dr
   };
   constexpr float kHiScale = BITS == 4 ? 0.0625f : 1.0f;  // B-operand scale of pairs 2/3
   if (lane == 0) {
-    mbar_init(bar + 0, 1);
-    mbar_init(bar + 1, 1);
+    for (int i = 0; i < kStages; ++i) mbar_init(bar + i, 1);
     fence_mbar_init();
   }
   __syncwarp();
-  if (n_units > 0) issue(0);
-  if (n_units > 1) issue(1);
+  for (int i = 0; i < kStages && i < n_units; ++i) issue(i);
   pdl_wait();  // compressed records are static within a step; q and the partials are not
 
   const int hn = lane >> 2;         // head column this lane feeds in B fragments
@@ -376,14 +378,14 @@ __global__ void __launch_bounds__(kWarps * 32, NREP == 8 ? 3 : VC_DRAFT_MINB) dr
   int cpart = 0;
 
   for (int u = 0; u < n_units; ++u) {
-    const int st = u & 1;
+    const int st = u % kStages;
     if (cpart == 0 && (cc.seq != cur.seq || cc.head != cur.head)) {
       emit();  // crossed into the next (sequence, head): flush its partial, restart
       cur = cc;
       reset();
       load_q();
     }
-    mbar_wait(bar + st, (u >> 1) & 1);
+    mbar_wait(bar + st, (u / kStages) & 1);
     const uint32_t* sb = stage0 + st * GEO::STAGE;
     if (cpart == 0) {
       // new group: q' = q * kscale as fp16 B fragments; per-head constant term
@@ -508,7 +510,7 @@ __global__ void __launch_bounds__(kWarps * 32, NREP == 8 ? 3 : VC_DRAFT_MINB) dr
     }
     fence_proxy_async();  // LDS reads of the stage before the next TMA write into it
     __syncwarp();
-    if (u + 2 < n_units) issue(st);
+    if (u + kStages < n_units) issue(st);
     if (++cpart == kUPG) {
       cpart = 0;
       next_task(cc);
@@ -520,7 +522,7 @@ __global__ void __launch_bounds__(kWarps * 32, NREP == 8 ? 3 : VC_DRAFT_MINB) dr
 template <int D, int BITS, int NREP>
 size_t draft_smem() {
   using GEO = Geo<D, BITS>;
-  size_t smem = static_cast<size_t>(kWarps) * 2 * GEO::STAGE * 4;
+  size_t smem = static_cast<size_t>(kWarps) * kStages * GEO::STAGE * 4;
   const size_t need_o = static_cast<size_t>(kWarps) * 8 * D * 4;  // tail CTAs' sm_o
   return smem < need_o ? need_o : smem;
 }

@@ -857,10 +857,12 @@ void Engine::kernel_bench(int kind, const std::vector<int>& slots, int reps, dou
     a.n_rows = kind == 2 ? cfg_.max_x + 1 : 1;  // kind 2: a verify window of max_x+1 rows
     a.row0 = i * a.n_rows;
     if ((i + 1) * a.n_rows > Mmax_) throw ContractViolation("kernel_bench: too many rows");
-    a.kv_len = s.committed;
+    a.kv_len = kind == 3 ? s.drop_len : s.committed;
     a.n_groups = s.n_groups;
     a.tail_len = s.tail_committed;
-    a.part0 = kind == 0 ? i * draft_parts_per_seq(max_chunks_q_, tail_cap_) : i * max_chunks_d_ * a.n_rows;
+    a.part0 = kind == 0 ? i * draft_parts_per_seq(max_chunks_q_, tail_cap_)
+                        : i * (kind == 3 ? max_chunks_x_ : max_chunks_d_) * a.n_rows;
+    if (kind == 3 && !drop_mode()) throw ContractViolation("kernel_bench: no drop tier");
     h[i] = a;
     // algorithmic bytes per (layer, request, kv-head) -- DESIGN.md §Roofline
     if (kind == 0)
@@ -868,7 +870,7 @@ void Engine::kernel_bench(int kind, const std::vector<int>& slots, int reps, dou
            + s.n_groups * m.d * 4.0 + s.n_groups * g * 4.0   // K per-channel, V per-token (scale, zero)
            + s.tail_committed * m.d * 2.0 * 2;                // bf16 tail
     else
-      b += static_cast<double>(s.committed) * m.d * 2 * 2;
+      b += static_cast<double>(a.kv_len) * m.d * 2 * 2;
   }
   b *= static_cast<double>(m.layers) * m.n_kv;
   VC_CK(cudaMemcpyAsync(seqs_dev_, h, n * sizeof(AttnSeq), cudaMemcpyHostToDevice, st_));
@@ -883,12 +885,15 @@ void Engine::kernel_bench(int kind, const std::vector<int>& slots, int reps, dou
       VC_CK(cudaEventRecord(ev[2 * k], st_));
       if (kind == 0) {
         VC_LAUNCH(draft_attention_quant(as, quant_, l, qkv_, seqs_dev_, n, max_chunks_q_, cfg_.quant_bits, part_, st_));
+      } else if (kind == 3) {  // drafting over the drop-topk tier
+        VC_LAUNCH(dense_attention(as, drop_, drop_maps_, l, seqs_dev_, n, max_chunks_x_, 1, part_, st_));
       } else {
         const KvPool pool = cfg_.full_tier == 0 ? full_ : stage_;
         VC_LAUNCH(dense_attention(as, pool, dense_maps_, l, seqs_dev_, n, max_chunks_d_, h[0].n_rows, part_, st_));
       }
       VC_CK(cudaEventRecord(ev[2 * k + 1], st_));
-      VC_LAUNCH(attention_combine(as, seqs_dev_, n, kind == 0 ? max_chunks_q_ : max_chunks_d_, h[0].n_rows, kind == 0 ? 0 : 1,
+      VC_LAUNCH(attention_combine(as, seqs_dev_, n, kind == 0 ? max_chunks_q_ : (kind == 3 ? max_chunks_x_ : max_chunks_d_),
+                                  h[0].n_rows, kind == 0 ? 0 : 1,
                                   part_, attn_, st_));
     }
   VC_CK(cudaStreamSynchronize(st_));
