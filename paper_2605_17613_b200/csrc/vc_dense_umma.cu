@@ -58,12 +58,15 @@ struct Item {
 template <int NREP>
 VC_DEV bool decode_item(int it, const AttnShape& s, const AttnSeq* seqs, int max_chunks, int row_blocks,
                         Item& I) {
-  I.chunk = it % max_chunks;
-  int r = it / max_chunks;
+  // row block innermost: the row blocks of one (sequence, head, chunk) run on
+  // neighbouring CTAs at the same time, so a long verify window's K/V chunk
+  // is fetched from HBM once and re-read from L2 by the other row blocks
+  I.rb = it % row_blocks;
+  int r = it / row_blocks;
+  I.chunk = r % max_chunks;
+  r /= max_chunks;
   I.h = r % s.n_kv;
-  r /= s.n_kv;
-  I.rb = r % row_blocks;
-  I.seq = r / row_blocks;
+  I.seq = r / s.n_kv;
   const AttnSeq sq = seqs[I.seq];
   const int rows = sq.n_rows * NREP;
   const int row_base = I.rb * kRows;

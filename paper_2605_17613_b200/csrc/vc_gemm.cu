@@ -21,21 +21,25 @@
 //     for qkv, SiLU-gate for gate/up (written in the tiled activation layout).
 // Batch invariance (verify logits == decode logits bit-for-bit): the work
 // split depends only on (N, K), never on the number of activation rows M;
-// activation rows ride the MMA N dimension (8 tokens per fragment), M only
-// selects how many fragments exist; M > 128 runs the same schedule per block.
-// Math: ldmatrix fragments from the swizzled stages, mma.sync bf16, fp32
-// accumulate, 8 consumer warps x 16 weight rows.
+// activation rows ride the UMMA N dimension, M only selects N (16..128);
+// M > 128 runs the same schedule per block.  tests/test_gemm.py checks
+// that a row's result is bit-identical at every M.
+// Math: 5th-gen tensor cores -- one thread issues tcgen05.mma (M = 128
+// weight rows, N = the step's token rows, K = 16) from the SW128 smem stages,
+// fp32 accumulators in TMEM (double-buffered across a CTA's tiles), 8
+// epilogue warps read them with tcgen05.ld.  (r1: the mma.sync version this
+// replaces ran a 113-row verify step's projections 2.4x slower.)
 #include "vc_common.cuh"
 #include "vc_gemm.h"
 #include "vc_tiled.cuh"
+#include "vc_umma.cuh"
 
 namespace vc {
 namespace {
 
 constexpr int kBN = 128;   // weight rows (output features) per tile
 constexpr int kBK = 64;    // k per stage (128 B per row)
-constexpr int kConsumers = 256;
-constexpr int kThreads = kConsumers + 32;  // + producer warp
+constexpr int kThreads = 320;  // producer warp + MMA warp + 8 epilogue warps
 constexpr int kCtasPerSm = 2;
 constexpr int kSms = 148;
 constexpr int kP = kCtasPerSm * kSms;  // stream-K grid upper bound
@@ -48,7 +52,7 @@ struct Cfg {
   static constexpr int kX = NT * 128;
   static constexpr int kStage = kW + kX;
   static constexpr int kStages = NT <= 32 ? 5 : (NT == 64 ? 4 : 3);
-  static constexpr int kSmem = kStages * kStage + kEpiRows * kLD * 4;
+  static constexpr int kSmem = kStages * kStage + kEpiRows * kLD * 4 + 1024;  // + 1 KB alignment slack
 };
 
 VC_DEV int swz8(int row, int c) { return c ^ (row & 7); }
@@ -61,8 +65,7 @@ __host__ __device__ inline long owner(long g, long T) { return ((g + 1) * grid_o
 // Epilogue over one staged pass of 16 tokens x 128 features (sT).
 template <Epi E>
 __device__ void epilogue_pass(const float* sT, int mbase, int M, int Mp, int n0, int N,
-                              const GemmEpilogue& ep) {
-  const int tid = threadIdx.x;
+                              const GemmEpilogue& ep, int tid) {
   const int t = tid >> 4;          // row of the pass
   const int sub = tid & 15;        // 16 threads per row
   const int m = mbase + t;
@@ -143,19 +146,30 @@ __device__ void epilogue_pass(const float* sT, int mbase, int M, int Mp, int n0,
   }
 }
 
+// Warp roles (kThreads = 320): warp 0 TMA producer, warp 1 MMA issuer (one
+// thread) + TMEM owner, warps 2..9 epilogue (256 threads; TMEM lane quarter =
+// warp & 3, the two warps of a quarter split the token columns).
+// D[feature, token] = W[feature, :] . X[token, :] accumulates in TMEM: weight
+// rows are the UMMA M (128 lanes), the step's token rows the UMMA N (NT), so a
+// decode step (16 rows) and a verify window (100+ rows) run the same
+// per-element arithmetic -- fixed k order inside a CTA's range, fixed
+// contributor order across CTAs -- whatever the batch (batch invariance).
 template <int NT, Epi E>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm)
-gemm_tma_kernel(const uint16_t* __restrict__ Xt, int Mp, int M, int K,
-                const uint16_t* __restrict__ Wt, int N, int m0, GemmEpilogue ep, GemmWorkspace ws,
-                int max_contrib) {
-  constexpr int NTF = NT / 8;
+gemm_umma_kernel(const uint16_t* __restrict__ Xt, int Mp, int M, int K,
+                 const uint16_t* __restrict__ Wt, int N, int m0, GemmEpilogue ep, GemmWorkspace ws,
+                 int max_contrib) {
   constexpr int ST = Cfg<NT>::kStages;
   constexpr int WB = Cfg<NT>::kW, XB = Cfg<NT>::kX;
-  extern __shared__ __align__(128) uint8_t smem[];
-  uint8_t* sW = smem;                                   // [ST][128 rows][128 B]
-  uint8_t* sX = smem + ST * WB;                         // [ST][NT rows][128 B]
+  constexpr uint32_t kAccCols = 2 * NT < 32 ? 32 : 2 * NT;  // two accumulator buffers
+  constexpr int kHalf = NT / 2;                             // token columns per epilogue warp
+  extern __shared__ uint8_t gsm_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(gsm_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sW = smem;                                   // [ST][128 rows][128 B], SW128 K-major
+  uint8_t* sX = smem + ST * WB;                         // [ST][NT rows][128 B], SW128 K-major
   float* sT = reinterpret_cast<float*>(smem + ST * (WB + XB));  // [16][kLD]
-  __shared__ __align__(8) uint64_t full[ST], empty[ST];
+  __shared__ __align__(8) uint64_t full[ST], empty[ST], acc_full[2], acc_empty[2];
+  __shared__ uint32_t tmem_base_sh;
   __shared__ int s_last;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int KT = K / kBK;
@@ -166,16 +180,24 @@ gemm_tma_kernel(const uint16_t* __restrict__ Xt, int Mp, int M, int K,
   const long beg0 = p * T / P, end = (p + 1) * T / P;
 
   if (tid == 0) {
-    for (int s = 0; s < ST; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], kConsumers / 32);
+    for (int s2 = 0; s2 < ST; ++s2) {
+      mbar_init(&full[s2], 1);
+      mbar_init(&empty[s2], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], 8);
     }
     fence_mbar_init();
   }
+  if (warp == 1) tmem_alloc(&tmem_base_sh, kAccCols);
+  tmem_fence_before();
   __syncthreads();
-
+  tmem_fence_after();
+  const uint32_t tbase = tmem_base_sh;
   pdl_trigger();
-  if (warp == kConsumers / 32) {  // ---- producer warp: one lane drives the TMA ring
+
+  if (warp == 0) {  // ---- TMA producer: one lane drives the ring
     if (lane == 0) {
       // PDL prologue: the first stages' weight tiles do not depend on the
       // previous kernel -- stream them while it drains, then wait for it
@@ -201,100 +223,136 @@ gemm_tma_kernel(const uint16_t* __restrict__ Xt, int Mp, int M, int K,
         tma_load_1d(sX + st * XB, Xt + (static_cast<size_t>(kt) * Mp + m0) * 64, XB, &full[st]);
       }
     }
-    return;
+  } else if (warp == 1) {  // ---- MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = umma_idesc_bf16(kBN, NT, false);  // A = W, B = X, both K-major
+      int it = 0, seg = 0;
+      for (long beg = beg0; beg < end; ++seg) {
+        const int k0 = static_cast<int>(beg % KT);
+        const int nk = static_cast<int>(min(static_cast<long>(KT - k0), end - beg));
+        beg += nk;
+        const int ab = seg & 1;
+        if (seg >= 2) mbar_wait(&acc_empty[ab], ((seg >> 1) - 1) & 1);
+        tmem_fence_after();
+        const uint32_t dacc = tbase + ab * NT;
+        for (int t = 0; t < nk; ++t, ++it) {
+          const int st = it % ST;
+          mbar_wait(&full[st], (it / ST) & 1);
+          tmem_fence_after();
+          const uint32_t wa = smem_u32(sW + st * WB), xa = smem_u32(sX + st * XB);
+#pragma unroll
+          for (int kk = 0; kk < kBK / 16; ++kk)
+            umma_ss(dacc, umma_sdesc_sw128(wa + kk * 32, 16, 1024), umma_sdesc_sw128(xa + kk * 32, 16, 1024), idesc,
+                    t > 0 || kk > 0);
+          umma_commit(&empty[st]);  // the stage is free once these MMAs have read it
+        }
+        umma_commit(&acc_full[ab]);
+      }
+    }
+  } else {  // ---- epilogue: split-K fixup + fused epilogue, 256 threads
+    pdl_wait();  // epilogues read/write buffers the previous kernel touches
+    const int et = tid - 64;                    // 0..255
+    const int quarter = warp & 3;
+    const int feat = quarter * 32 + lane;       // TMEM lane = output feature within the tile
+    const int tok0 = (et >= 128 ? kHalf : 0);   // this warp's token columns [tok0, tok0 + kHalf)
+    const uint32_t tlane = tbase + (static_cast<uint32_t>(quarter * 32) << 16);
+    int seg = 0;
+    for (long beg = beg0; beg < end; ++seg) {
+      const int tile = static_cast<int>(beg / KT);
+      const int k0 = static_cast<int>(beg % KT);
+      const int nk = static_cast<int>(min(static_cast<long>(KT - k0), end - beg));
+      const int n0 = tile * kBN;
+      beg += nk;
+      const int ab = seg & 1;
+      mbar_wait(&acc_full[ab], (seg >> 1) & 1);
+      tmem_fence_after();
+      const uint32_t tacc = tlane + ab * NT + tok0;  // this warp's token columns of the accumulator
+      // 8 token columns [c, c+8) of this warp's half from TMEM
+      auto ld8 = [&](int c, float* v) {
+        uint32_t u[8];
+        asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                     : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]), "=r"(u[4]), "=r"(u[5]), "=r"(u[6]), "=r"(u[7])
+                     : "r"(tacc + c));
+        tmem_wait_ld();
+#pragma unroll
+        for (int j = 0; j < 8; ++j) v[j] = __uint_as_float(u[j]);
+      };
+      // ---- split-K fixup: contributors of this tile, in increasing k ----------
+      const long g0 = static_cast<long>(tile) * KT;
+      const long q0 = owner(g0, T), q1 = owner(g0 + KT - 1, T);
+      const int n_contrib = static_cast<int>(q1 - q0 + 1);
+      // partial layout per contributor: [token / 4][feature][4] floats, so a
+      // warp moves 4 tokens of 32 consecutive features as one coalesced
+      // 512-B float4 access
+      float4* part = reinterpret_cast<float4*>(ws.partial + static_cast<size_t>(tile) * max_contrib * (NT * kBN));
+      constexpr int kPart4 = NT * kBN / 4;  // float4 per contributor
+      if (n_contrib > 1) {
+        const int c = static_cast<int>(p - q0);
+        float4* mine = part + static_cast<size_t>(c) * kPart4;
+        for (int cc = 0; cc < kHalf; cc += 8) {
+          float v[8];
+          ld8(cc, v);
+          const int t4 = (tok0 + cc) >> 2;
+          mine[t4 * kBN + feat] = make_float4(v[0], v[1], v[2], v[3]);
+          mine[(t4 + 1) * kBN + feat] = make_float4(v[4], v[5], v[6], v[7]);
+        }
+        tmem_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&acc_empty[ab]);  // accumulator free for segment seg+2
+        __threadfence();
+        named_bar(1, 256);
+        if (et == 0) {
+          const int prev = atomicAdd(ws.counters + tile, 1);
+          s_last = prev == n_contrib - 1;
+          if (s_last) ws.counters[tile] = 0;  // self-reset for the next launch / graph replay
+        }
+        named_bar(1, 256);
+        if (!s_last) continue;
+        __threadfence();
+      }
+      // ---- epilogue, 16 tokens per staged pass ---------------------------------
+      for (int q = 0; q < NT / kEpiRows; ++q) {
+        const int qlo = q * kEpiRows;
+        // this warp stages the pass's tokens that lie in its half, 8 at a time
+        for (int c8 = 0; c8 < kEpiRows; c8 += 8) {
+          const int tok = qlo + c8;
+          if (tok < tok0 || tok >= tok0 + kHalf) continue;
+          float v[8];
+          if (n_contrib > 1) {
+            // contributor order 0..n-1 per element (batch invariance); the
+            // loads of consecutive contributors are independent, so the
+            // unrolled loop keeps several in flight
+            const float4* src = part + (tok >> 2) * kBN + feat;
+            float4 a = __ldcg(src), b = __ldcg(src + kBN);
+#pragma unroll 4
+            for (int cc = 1; cc < n_contrib; ++cc) {
+              const float4 x = __ldcg(src + static_cast<size_t>(cc) * kPart4);
+              const float4 y = __ldcg(src + static_cast<size_t>(cc) * kPart4 + kBN);
+              a.x += x.x; a.y += x.y; a.z += x.z; a.w += x.w;
+              b.x += y.x; b.y += y.y; b.z += y.z; b.w += y.w;
+            }
+            v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+            v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+          } else {
+            ld8(tok - tok0, v);
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j) sT[(c8 + j) * kLD + feat] = v[j];
+        }
+        named_bar(1, 256);
+        if (m0 + q * kEpiRows < M) epilogue_pass<E>(sT, m0 + q * kEpiRows, M, Mp, n0, N, ep, et);
+        named_bar(1, 256);
+      }
+      if (n_contrib == 1) {
+        tmem_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&acc_empty[ab]);
+      }
+    }
   }
-
-  // ---- consumer warps ------------------------------------------------------
-  pdl_wait();  // epilogues read/write buffers the previous kernel touches
-  int it = 0;
-  long beg = beg0;
-  while (beg < end) {
-    const int tile = static_cast<int>(beg / KT);
-    const int k0 = static_cast<int>(beg % KT);
-    const int nk = static_cast<int>(min(static_cast<long>(KT - k0), end - beg));
-    const int n0 = tile * kBN;
-    beg += nk;
-    float acc[NTF][4];
-#pragma unroll
-    for (int f = 0; f < NTF; ++f) acc[f][0] = acc[f][1] = acc[f][2] = acc[f][3] = 0.f;
-    for (int t = 0; t < nk; ++t, ++it) {
-      const int st = it % ST;
-      mbar_wait(&full[st], (it / ST) & 1);
-      const uint8_t* w = sW + st * WB;
-      const uint8_t* x = sX + st * XB;
-#pragma unroll
-      for (int ks = 0; ks < kBK / 16; ++ks) {
-        uint32_t a[4];
-        {
-          const int r = warp * 16 + (lane & 7) + ((lane >> 3) & 1) * 8;
-          const int c = ks * 2 + (lane >> 4);
-          ldmatrix_x4(a[0], a[1], a[2], a[3], w + r * 128 + swz8(r, c) * 16);
-        }
-#pragma unroll
-        for (int f = 0; f < NTF; f += 2) {
-          const int r = f * 8 + (lane & 7) + (lane >> 4) * 8;
-          const int c = ks * 2 + ((lane >> 3) & 1);
-          uint32_t b[4];
-          ldmatrix_x4(b[0], b[1], b[2], b[3], x + r * 128 + swz8(r, c) * 16);
-          mma_bf16(acc[f], a[0], a[1], a[2], a[3], b[0], b[1]);
-          mma_bf16(acc[f + 1], a[0], a[1], a[2], a[3], b[2], b[3]);
-        }
-      }
-      // order this warp's generic-proxy reads of the stage before the producer's
-      // next async-proxy (TMA) write into it -- without it the refill can race
-      fence_proxy_async();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[st]);  // this warp is done with the stage
-    }
-
-    // ---- split-K fixup: contributors of this tile, in increasing k ----------
-    const long g0 = static_cast<long>(tile) * KT;
-    const long q0 = owner(g0, T), q1 = owner(g0 + KT - 1, T);
-    const int n_contrib = static_cast<int>(q1 - q0 + 1);
-    if (n_contrib > 1) {
-      const int c = static_cast<int>(p - q0);
-      float4* part = reinterpret_cast<float4*>(ws.partial + (static_cast<size_t>(tile) * max_contrib) * (NT * kBN));
-      float4* mine = part + static_cast<size_t>(c) * (NT * kBN / 4) + tid * NTF;
-#pragma unroll
-      for (int f = 0; f < NTF; ++f) mine[f] = make_float4(acc[f][0], acc[f][1], acc[f][2], acc[f][3]);
-      __threadfence();
-      named_bar(1, kConsumers);
-      if (tid == 0) {
-        const int prev = atomicAdd(ws.counters + tile, 1);
-        s_last = prev == n_contrib - 1;
-        if (s_last) ws.counters[tile] = 0;  // self-reset for the next launch / graph replay
-      }
-      named_bar(1, kConsumers);
-      if (!s_last) continue;
-      __threadfence();
-#pragma unroll
-      for (int f = 0; f < NTF; ++f) {
-        float4 s = __ldcg(part + tid * NTF + f);
-        for (int cc = 1; cc < n_contrib; ++cc) {
-          const float4 v = __ldcg(part + static_cast<size_t>(cc) * (NT * kBN / 4) + tid * NTF + f);
-          s.x += v.x; s.y += v.y; s.z += v.z; s.w += v.w;
-        }
-        acc[f][0] = s.x; acc[f][1] = s.y; acc[f][2] = s.z; acc[f][3] = s.w;
-      }
-    }
-    // ---- epilogue, 16 tokens per staged pass ---------------------------------
-    const int fa = warp * 16 + (lane >> 2);
-#pragma unroll
-    for (int q = 0; q < NT / kEpiRows; ++q) {
-#pragma unroll
-      for (int ff = 0; ff < 2; ++ff) {
-        const int f = 2 * q + ff;
-        const int tk = ff * 8 + 2 * (lane & 3);
-        sT[tk * kLD + fa] = acc[f][0];
-        sT[(tk + 1) * kLD + fa] = acc[f][1];
-        sT[tk * kLD + fa + 8] = acc[f][2];
-        sT[(tk + 1) * kLD + fa + 8] = acc[f][3];
-      }
-      named_bar(1, kConsumers);
-      if (m0 + q * kEpiRows < M) epilogue_pass<E>(sT, m0 + q * kEpiRows, M, Mp, n0, N, ep);
-      named_bar(1, kConsumers);
-    }
-  }
+  tmem_fence_before();
+  __syncthreads();
+  if (warp == 1) tmem_dealloc(tbase, kAccCols);
 }
 
 int max_contributors(int N, int K) {
@@ -310,7 +368,7 @@ int max_contributors(int N, int K) {
 template <int NT, Epi E>
 cudaError_t launch_nt(const uint16_t* Xt, int Mp, int M, int K, const uint16_t* Wt, int N,
                       const GemmEpilogue& ep, const GemmWorkspace& ws, cudaStream_t st) {
-  auto kern = gemm_tma_kernel<NT, E>;
+  auto kern = gemm_umma_kernel<NT, E>;
   const int smem = Cfg<NT>::kSmem;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
   if (e != cudaSuccess) return e;

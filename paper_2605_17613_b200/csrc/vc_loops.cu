@@ -13,6 +13,7 @@
 //      that returns the measured accept counts in fire_verify order, so the
 //      rings, cadence and stalls evolve exactly as Algorithm 1 prescribes.
 #include <chrono>
+#include <cstdio>
 #include <cmath>
 #include <cstring>
 #include <algorithm>
@@ -131,6 +132,7 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
   };
   std::vector<Xfer> inflight;
   std::set<speckv::ReservationId> kicked;  // reloads already started
+  constexpr int kLinkQueue = 2;            // copies kept queued on the link ahead of schedule
   static const bool early_kick = [] {
     const char* v = std::getenv("VC_EARLY_KICK");
     return !(v && v[0] == '0');
@@ -166,10 +168,14 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
     }
     if (bounded && it == sd.warmup_iterations + sd.timed_iterations) break;
     // 1. kick off transfers.  The reference starts a reload at its span_begin
-    // (pending_kickoffs, sim.cpp:243-249).  The copy stream is a FIFO link, so
-    // starting a booked reload as soon as a staging slot is free (earliest
-    // verify first) can only make it land earlier: the link never idles while
-    // a booked reload waits.  VC_EARLY_KICK=0 restores span_begin kickoffs.
+    // (pending_kickoffs, sim.cpp:243-249).  The copy stream is a FIFO link:
+    // here a booked reload (earliest verify first) starts as soon as a staging
+    // slot is free and fewer than kLinkQueue copies are queued on the link --
+    // the link never idles while a booked reload waits, and a staging slot is
+    // taken only about one copy-time before its reload can start, not at
+    // booking (which would pin slots for a whole round).  Landing earlier than
+    // the reference's schedule is always safe (done_ is checked at verify).
+    // VC_EARLY_KICK=0 restores span_begin kickoffs.
     for (const auto& r : sched.pending_kickoffs()) {
       if (r.bytes == 0 || !staged) {  // arrival load (compressed tier resident) / tier 0
         ev.completed_transfers.push_back(r.id);
@@ -187,6 +193,7 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
       });
       for (const auto& r : want) {
         if (free_stages.empty()) break;
+        if (early_kick && r.span_begin > sched.iteration() && static_cast<int>(inflight.size()) >= kLinkQueue) break;
         const int req = static_cast<int>(r.request_id);
         const int s = free_stages.back();
         free_stages.pop_back();
@@ -266,9 +273,18 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
     t_prev = t_now;
     t_plan = 0.8 * t_plan + 0.2 * dt;
     // exposed swap time: a session whose reload is late stalls this iteration
-    int stalled = 0;
-    for (const auto& [id, ss] : sched.sessions()) stalled += ss.stalled ? 1 : 0;
+    int stalled = 0, booked = 0, spec = 0;
+    for (const auto& [id, ss] : sched.sessions()) {
+      stalled += ss.stalled ? 1 : 0;
+      spec += ss.mode == speckv::SessionMode::Speculative ? 1 : 0;
+      booked += (ss.pending && !kicked.count(ss.pending->id)) ? 1 : 0;
+    }
     stall_ms += 1e3 * dt * stalled;
+    static const bool sched_log = std::getenv("VC_SCHED_LOG") != nullptr;
+    if (sched_log)
+      std::fprintf(stderr, "SCHED it=%lld dt=%.2f plan=%.2f spec=%d waiting=%zu stalled=%d booked=%d inflight=%zu free=%zu drafted=%zu verifies=%zu\n",
+                   static_cast<long long>(it), dt * 1e3, t_plan * 1e3, spec, sched.waiting_size(), stalled, booked,
+                   inflight.size(), free_stages.size(), rr.drafted.size(), rr.verifies.size());
     ev = speckv::StepEvents{};
   }
   const auto t1 = std::chrono::steady_clock::now();

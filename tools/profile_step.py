@@ -40,6 +40,10 @@ def main():
         for _ in range(x):
             e.draft([0])
     e.timing(reset=True)
+    # ncu --profile-from-start off: only the measured steps are profiled
+    import ctypes
+    cu = ctypes.CDLL("libcuda.so.1")
+    cu.cuProfilerStart()
     for _ in range(a.steps):
         if a.mode == "decode":
             e.decode_step(list(range(B)))
@@ -50,6 +54,7 @@ def main():
             items = [(0, 2, [st["pending"]] + [1] * x, -1)]
             items += [(i, 1, [e.state(i)["pending"]], -1) for i in range(1, B)]
             e.step(items)
+    cu.cuProfilerStop()
     ms, n = e.timing()
     print(f"mode={a.mode} steps={n} device_ms_per_step={ms / max(n, 1):.3f}")
     e.close()
