@@ -44,7 +44,7 @@ METRIC = "lossless decode tokens/s at 32K ctx vs full-KV decode; draft-attn HBM 
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=96)
+    p.add_argument("--steps", type=int, default=256)
     p.add_argument("--warmup", type=int, default=32)
     p.add_argument("--impl", default="ours", choices=["ours", "reference"])
     p.add_argument("--batch", type=int, default=16)
@@ -61,6 +61,8 @@ def parse():
     p.add_argument("--no-secondary", action="store_true", help="skip the other tier's line")
     p.add_argument("--stages", type=int, default=8, help="HBM staging slots of the host tier")
     p.add_argument("--small", action="store_true", help="tiny model smoke run")
+    p.add_argument("--config", type=int, default=2, choices=[2, 3],
+                   help="2: BASELINE.json configs[1] (headline); 3: configs[2] -- 128K ctx, drop-topk c=0.2")
     return p.parse_args()
 
 
@@ -235,6 +237,12 @@ def main():
     B, ctx, K, W = args.batch, args.ctx, args.steps, args.warmup
     if args.small:
         ctx = min(ctx, 4096)
+    cfg3 = args.config == 3  # configs[2]: 128K context, token-dropping compressor (20% top-k per head)
+    drop = 0.2 if cfg3 else 0.0
+    if cfg3:
+        ctx = 131072 if args.ctx == 32768 else ctx
+        B = 4 if args.batch == 16 else B  # 4 x 17.2 GB full KV + drop tier fit one B200 beside the weights
+        args.tier, args.no_secondary = "hbm", True
     head_tier = 1 if args.tier == "host" else 0
     shard = weak_shard(B, world, rank)  # this rank's requests (no data-path collective)
     rng = np.random.default_rng(2 + shard.requests[0])
@@ -268,19 +276,20 @@ def main():
     def vericache(tier):
         """One VeriCache run: compressed drafting + full-KV verify (tier 0: full KV
         in HBM; tier 1: full KV in pinned host memory, reloaded per verify)."""
-        x = args.x or (96 if tier == 1 else 16)
+        x = args.x or (96 if tier == 1 else (32 if cfg3 else 16))
         window = args.window or max(2 * x + 8, 48 if tier == 0 else 256)
         # the staggered loop reaches steady state only after every request has
         # drafted and verified once: 2(x+1) ramp iterations precede the W warm-up
         ramp = max(0, 2 * (x + 1) - W)
         ev = vc.Engine(shape, max_slots=B, max_ctx=ctx + W + ramp + K + 3 * (x + 1) + 8, max_x=x,
-                       quant_bits=args.bits, full_tier=tier, n_stage=args.stages if tier else 1,
+                       quant_bits=0 if drop else args.bits, drop_ratio=drop, full_tier=tier,
+                       n_stage=args.stages if tier else 1,
                        max_verify=args.stages if tier else max(2, B // (x + 1) + 2), device=local)
         ev.init_weights(seed=0, std=0.02, resid_std=rs, q_std=qs)
         for i in range(B):
             ev.add_synthetic(i, ctx, first[i], seed=shard.seeds[i])
             meta = ev.compress(i)
-        ka = ev.kernel_bench(0, slots, reps=5) if tier == head_tier else (None, None)
+        ka = ev.kernel_bench(3 if drop else 0, slots, reps=5) if tier == head_tier else (None, None)
         launches0 = ev.stats()["kernel_launches"]
         if dist:
             dist.barrier()
@@ -319,7 +328,7 @@ def main():
     base_value = B * world * K / bdev_s
     ka_bytes = h["ka"][1]
     achieved = ka_bytes / (ka_ms / 1e3) / 1e9
-    traffic, traffic_src = draft_traffic()
+    traffic, traffic_src = draft_traffic() if not cfg3 else (None, None)
     rows = st["timed_rows"]
     h2d = (rows * (4 + 16) + st["h2d_bytes"]) / K  # step inputs (token + row descriptor) + KV reloads
 
@@ -351,13 +360,15 @@ def main():
             "vs_baseline": None, "dtype": "bf16",
             "data": f"synthetic (random-init weights N(0,0.02); q_proj N(0,{qs:.4g}), o/down_proj N(0,{rs:.4g}) "
                     f"calibrated to the paper's acceptance, 21.1 of x=30; synthetic 32K prefix KV)",
-            "config": {"workload": f"configs[1]: {'tiny' if args.small else 'Llama-3-8B shape'}, {ctx} ctx, "
-                                   f"int{args.bits} KIVI, batch {B}/GPU, full KV in "
-                                   f"{'pinned host memory' if head_tier else 'HBM'}",
+            "config": {"workload": (f"configs[2]: Llama-3.1-8B shape, {ctx} ctx, drop-topk c={drop} (L1 key-norm "
+                                    f"scores, top-k per layer/head), batch {B}/GPU, full KV in HBM") if cfg3 else
+                                   (f"configs[1]: {'tiny' if args.small else 'Llama-3-8B shape'}, {ctx} ctx, "
+                                    f"int{args.bits} KIVI, batch {B}/GPU, full KV in "
+                                    f"{'pinned host memory' if head_tier else 'HBM'}"),
                        "global_batch": B * world, "seq_len": ctx, "draft_x": x, "lookahead_window": h["window"],
                        "ramp_iterations": h["ramp"],
                        "parallelism": f"request-sharded dp{world}",
-                       "l2": "inputs larger than L2 (>= 34 GB of weights + compressed KV read per step)"},
+                       "l2": "inputs larger than L2 (>= 30 GB of weights + compressed KV read per step)"},
             "e2e": {"value": round(tok_all / wall_s, 2), "unit": "tokens/s",
                     "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(rows / K * 4)},
             "full_kv_decode": {"value": round(base_value, 2), "unit": "tokens/s",
@@ -368,7 +379,8 @@ def main():
             "accepted_per_verify": round(st["mean_accept"], 3), "verifies": st["verifies"],
             "late_transfers": st["late_transfers"],
             "tiers": {("host" if t else "hbm"): tier_summary(r, t) for t, r in runs.items()},
-            "roofline": {"kernel": "draft_attn_quant_kernel<128,4,4> (one launch per layer, 16 requests)",
+            "roofline": {"kernel": ("dense_umma_kernel<128,4> drafting over the drop tier" if cfg3 else
+                                    "draft_attn_quant_kernel<128,4,4>") + f" (one launch per layer, {B} requests)",
                          "bound": "hbm", "achieved": round(achieved, 1), "peak": round(peak, 1), "unit": "GB/s",
                          "frac": round(achieved / peak, 3),
                          "traffic": traffic, "traffic_source": traffic_src,
