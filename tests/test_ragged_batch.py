@@ -1,0 +1,69 @@
+"""Ragged batches: requests with very different context lengths (including a
+1-token context with no quantised group, and contexts that are not multiples
+of the 128-token group) share one step.
+
+  * full-KV decode rows (the path verify shares) are batch-invariant: a row's
+    logits are bit-identical whether it is stepped alone or in the ragged batch
+    (the losslessness requirement, SURVEY.md §7 hard part 2);
+  * draft rows (int4 and int2 tiers, drop-topk tier) are not required to be
+    batch-invariant -- the draft kernel's stream-K split spans the batch -- but
+    must agree within the draft tolerance of tests/test_attention_parity.py."""
+import numpy as np
+import pytest
+
+import vc_testlib as T
+from paper_2605_17613_b200 import TINY, Engine
+
+pytestmark = pytest.mark.gpu
+
+CTX = [1, 130, 2000, 4096, 700]
+FIRST = [11, 23, 37, 41, 53]
+
+
+@pytest.fixture(scope="module")
+def weights():
+    return T.tiny_weights(TINY, seed=5, std=0.02)
+
+
+def _engine(weights, **kw):
+    e = Engine(TINY, max_slots=len(CTX), max_ctx=4096 + 64, max_x=8, max_verify=2, **kw)
+    e.load_weights(weights)
+    for s, (n, f) in enumerate(zip(CTX, FIRST)):
+        e.add_synthetic(s, n, f, seed=100 + s)
+    return e
+
+
+def test_drop_rejects_sub_token_retention(cuda, weights):
+    from paper_2605_17613_b200 import _lib
+    e = _engine(weights, quant_bits=0, drop_ratio=0.25)
+    with pytest.raises(_lib.ContractError):
+        e.compress(0)  # 1-token context: llround(0.25) = 0 retained
+    e.close()
+
+
+def test_decode_rows_batch_invariant(cuda, weights):
+    e = _engine(weights, quant_bits=0)
+    items = [(s, 0, [FIRST[s]], -1) for s in range(len(CTX))]
+    _, batch = e.step(items, want_logits=True)
+    for s in range(len(CTX)):
+        _, single = e.step([items[s]], want_logits=True)
+        assert np.array_equal(single[0].view(np.uint32), batch[s].view(np.uint32)), f"row {s} (ctx {CTX[s]})"
+    e.close()
+
+
+@pytest.mark.parametrize("mode", ["int4", "int2", "drop"])
+def test_draft_rows_ragged(cuda, weights, mode):
+    kw = {"int4": dict(quant_bits=4), "int2": dict(quant_bits=2),
+          "drop": dict(quant_bits=0, drop_ratio=0.25)}[mode]
+    e = _engine(weights, **kw)
+    # drop-topk keeps llround(c * T) tokens and rejects < 1 (compressor.cpp:154-157): skip the 1-token context
+    slots = [s for s in range(len(CTX)) if mode != "drop" or CTX[s] > 1]
+    for s in slots:
+        e.compress(s)
+    items = [(s, 1, [FIRST[s]], -1) for s in slots]
+    _, batch = e.step(items, want_logits=True)
+    for i, s in enumerate(slots):
+        _, single = e.step([items[i]], want_logits=True)
+        err = np.abs(single[0] - batch[i]).max()
+        assert err <= 2e-2 * np.abs(single[0]).max() + 2e-3, f"row {s} (ctx {CTX[s]}): {err}"
+    e.close()
