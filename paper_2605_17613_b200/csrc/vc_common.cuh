@@ -50,6 +50,15 @@ VC_DEV uint32_t pack_h2(float lo, float hi) {
   memcpy(&r, &h, 4);
   return r;
 }
+VC_DEV uint32_t hmul2_u32(uint32_t a, uint32_t b) {  // f16x2 multiply, round to nearest
+  __half2 x, y;
+  memcpy(&x, &a, 4);
+  memcpy(&y, &b, 4);
+  const __half2 r = __hmul2(x, y);
+  uint32_t u;
+  memcpy(&u, &r, 4);
+  return u;
+}
 VC_DEV float2 h2_to_f2(uint32_t h) {
   __half2 v;
   memcpy(&v, &h, 4);

@@ -191,9 +191,11 @@ __global__ void __launch_bounds__(kWarps * 32, NREP == 8 ? 3 : VC_DRAFT_MINB) dr
   constexpr int kUPG = kG / kUnit;
 
   extern __shared__ __align__(128) uint32_t dsm[];   // [kWarps][2][STAGE]
-  // per-warp q heads (bf16); the tail CTAs reuse it for NREP*D fp32 q values
-  __shared__ __align__(16) uint16_t sq_q[kWarps][NREP * D];
-  static_assert(kWarps * 2 >= 4, "tail q fits");
+  // per-warp q, fp32 pre-scaled by scale_log2, laid out [channel pair][8 head
+  // columns] (padding heads zero) so the group setup reads one conflict-free
+  // float2 per lane; the tail CTAs reuse it for NREP*D fp32 q values
+  __shared__ __align__(16) float2 sq_q[kWarps][D / 2 * 8];
+  static_assert(kWarps * (D / 2) * 8 * 2 >= NREP * D, "tail q fits");
   __shared__ __align__(8) uint64_t bars[kWarps][kStages];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -363,12 +365,20 @@ __global__ void __launch_bounds__(kWarps * 32, NREP == 8 ? 3 : VC_DRAFT_MINB) dr
       }
     }
   };
-  auto load_q = [&]() {  // the consumer head's NREP query rows, bf16
+  auto load_q = [&]() {  // the consumer head's NREP query rows -> fp32 * scale_log2, [pair][8 heads]
     const uint16_t* qrow = qkv + static_cast<size_t>(seqs[cur.seq].row0) * s.q_stride +
                            static_cast<size_t>(cur.head) * NREP * D;
     __syncwarp();
-    for (int i = lane; i < NREP * D / 8; i += 32)
-      reinterpret_cast<uint4*>(sq_q[warp])[i] = reinterpret_cast<const uint4*>(qrow)[i];
+    for (int i = lane; i < D / 2 * 8; i += 32) {
+      const int cp = i >> 3, h = i & 7;
+      float2 v = make_float2(0.f, 0.f);
+      if (h < NREP) {
+        const uint32_t qq = *reinterpret_cast<const uint32_t*>(qrow + h * D + 2 * cp);
+        v = make_float2(bf2f(static_cast<uint16_t>(qq & 0xffffu)) * s.scale_log2,
+                        bf2f(static_cast<uint16_t>(qq >> 16)) * s.scale_log2);
+      }
+      sq_q[warp][i] = v;
+    }
     __syncwarp();
   };
   reset();
@@ -388,33 +398,36 @@ __global__ void __launch_bounds__(kWarps * 32, NREP == 8 ? 3 : VC_DRAFT_MINB) dr
     mbar_wait(bar + st, (u / kStages) & 1);
     const uint32_t* sb = stage0 + st * GEO::STAGE;
     if (cpart == 0) {
-      // new group: q' = q * kscale as fp16 B fragments; per-head constant term
+      // new group: q' = q * kscale as fp16 B fragments (f16x2 multiply of the
+      // packed q and the two channels' scales, gathered with one PRMT), and the
+      // per-head constant  sum_c q_c z_c - 1024 sum_c q'_c : the zero-point
+      // part in fp32 FFMAs, the -1024 part (over the fp16 q' the MMA sees) by
+      // one extra MMA per k-step against a constant-1024 A tile
       float bias_part = 0.f;
-      const uint16_t* qh = sq_q[warp] + (hn < NREP ? hn : 0) * D;
-      const float qmask = hn < NREP ? s.scale_log2 : 0.f;  // padding head columns feed zeros
+      const float2* qf = sq_q[warp] + hn;
 #pragma unroll
       for (int k = 0; k < KS; ++k) {
         const int c0 = k * 16 + 2 * (lane & 3);
 #pragma unroll
         for (int hi = 0; hi < 2; ++hi) {  // channels c0,c0+1 then c0+8,c0+9
           const int c = c0 + 8 * hi;
-          const uint2 sz = *reinterpret_cast<const uint2*>(sb + GEO::OFF_KSZ + c);
-          const float2 sz0 = h2_to_f2(sz.x), sz1 = h2_to_f2(sz.y);  // (scale, zero)
-          const uint32_t qq = *reinterpret_cast<const uint32_t*>(qh + c);
-          const float q0 = bf2f(static_cast<uint16_t>(qq & 0xffffu)) * qmask;
-          const float q1 = bf2f(static_cast<uint16_t>(qq >> 16)) * qmask;
-          const float f = hi ? kHiScale : 1.0f;
-          const uint32_t bq = pack_h2(q0 * sz0.x * f, q1 * sz1.x * f);
-          // zero point and the -1024 fold use the fp16-rounded q' the MMA sees
-          const float2 qr = h2_to_f2(bq);
-          bias_part += q0 * sz0.y + q1 * sz1.y - 1024.f * (qr.x + qr.y);
+          const uint2 sz = *reinterpret_cast<const uint2*>(sb + GEO::OFF_KSZ + c);  // (s_c|z_c), (s_c1|z_c1)
+          const float2 q = qf[(c >> 1) * 8];
+          const uint32_t q16 = hi ? pack_h2(q.x * kHiScale, q.y * kHiScale) : pack_h2(q.x, q.y);
+          const uint32_t bq = hmul2_u32(q16, __byte_perm(sz.x, sz.y, 0x5410));
+          const float2 z = h2_to_f2(__byte_perm(sz.x, sz.y, 0x7632));
+          bias_part = fmaf(q.x, z.x, fmaf(q.y, z.y, bias_part));
           (hi ? b1 : b0)[k] = bq;
         }
       }
+      float c1024[4] = {0.f, 0.f, 0.f, 0.f};
+      constexpr uint32_t kA1024 = 0x64006400u;  // fp16 pair (1024, 1024)
+#pragma unroll
+      for (int k = 0; k < KS; ++k) mma_f16(c1024, kA1024, kA1024, kA1024, kA1024, b0[k], b1[k]);
       bias_part += __shfl_xor_sync(0xffffffffu, bias_part, 1);
       bias_part += __shfl_xor_sync(0xffffffffu, bias_part, 2);
-      bias0 = __shfl_sync(0xffffffffu, bias_part, hc0 * 4);
-      bias1 = __shfl_sync(0xffffffffu, bias_part, (hc0 + 1) * 4);
+      bias0 = __shfl_sync(0xffffffffu, bias_part, hc0 * 4) - c1024[0];
+      bias1 = __shfl_sync(0xffffffffu, bias_part, (hc0 + 1) * 4) - c1024[1];
     }
 
     // S^T tiles of the unit's kUnit tokens
