@@ -364,6 +364,10 @@ class SpecScheduler {
   // B200 extension: swap the sampler (the engine plans a step on a copy with
   // a recording sampler, then replays it with measured accept counts).
   void set_sampler(RoundSampler& sampler) { sampler_ = &sampler; }
+  // B200 extension: verify a fully drafted round as soon as its reload has
+  // landed rather than at the booked verify iteration (default off = the
+  // reference's Algorithm 1 exactly; the engine's scheduled loop turns it on).
+  void set_expedite(bool on) { expedite_ = on; }
 
  private:
   void admit_for_verify(SpecSession& s, StepResult& r);
@@ -379,6 +383,7 @@ class SpecScheduler {
   std::deque<RequestId> waiting_;
   std::vector<RequestId> readmit_;
   std::set<ReservationId> done_;
+  bool expedite_ = false;
 };
 
 }  // namespace speckv

@@ -766,6 +766,11 @@ StepResult SpecScheduler::execution_step(const StepEvents& ev) {  // scheduler.c
         r.drafting_count += 1;
         r.hbm_read_bytes += s.resident_bytes();
         r.drafted.push_back(id);
+      } else if (expedite_ && arrived) {
+        // B200 extension (off by default): the round is fully drafted and its
+        // reload has landed -- verify now instead of idling to the booked
+        // verify iteration; the ring bookings retire on their own schedule
+        verify_now(s, r, false);
       }
       continue;
     }

@@ -111,6 +111,15 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
   RecordingSampler rec;
   MeasuredSampler meas;
   speckv::SpecScheduler sched(cfg, meas);
+  // VC_EXPEDITE=1 (host tier): verify a drafted round as soon as its reload
+  // landed instead of at the booked verify iteration.  Off by default: with
+  // x=47 the booked schedule already saturates PCIe (link busy 0.99), and at
+  // large x the extra verify steps cost more GPU time than they save.
+  static const bool expedite = [] {
+    const char* v = std::getenv("VC_EXPEDITE");
+    return v && v[0] == '1';
+  }();
+  sched.set_expedite(expedite && staged);
   speckv::StepEvents ev;
   for (int i = 0; i < n; ++i) {
     speckv::Request r;
