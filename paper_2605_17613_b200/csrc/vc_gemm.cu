@@ -42,7 +42,10 @@ constexpr int kBK = 64;    // k per stage (128 B per row)
 constexpr int kThreads = 320;  // producer warp + MMA warp + 8 epilogue warps
 constexpr int kCtasPerSm = 2;
 constexpr int kSms = 148;
-constexpr int kP = kCtasPerSm * kSms;  // stream-K grid upper bound
+#ifndef VC_GEMM_GRID_PER_SM
+#define VC_GEMM_GRID_PER_SM kCtasPerSm
+#endif
+constexpr int kP = VC_GEMM_GRID_PER_SM * kSms;  // stream-K grid upper bound (a function of nothing but the GPU)
 constexpr int kEpiRows = 16;           // epilogue staging pass (tokens)
 constexpr int kLD = kBN + 4;
 
