@@ -258,7 +258,15 @@ __global__ void __launch_bounds__(kWarps * 32, NREP == 8 ? 3 : VC_DRAFT_MINB) dr
     if (++c.head < s.n_kv) { set_slice(c); return; }
     c.head = 0;
     c.base += c.ng * s.n_kv;
-    do { c.ng = seqs[++c.seq].n_groups; } while (c.ng == 0);  // tasks remain: terminates
+    // the cursors also step once past a warp's last task: stop at the batch end
+    // (compute-sanitizer memcheck caught the unbounded scan reading past seqs)
+    do {
+      if (++c.seq >= n_seq) {
+        c.ng = 1;
+        return;
+      }
+      c.ng = seqs[c.seq].n_groups;
+    } while (c.ng == 0);
     set_slice(c);
   };
   Cursor pc;  // producer (lane 0 issues, all lanes track)
