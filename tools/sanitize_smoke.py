@@ -1,5 +1,6 @@
 """Small end-to-end run for compute-sanitizer (memcheck / racecheck / synccheck):
-tiny model, int4 + int2 + drop tiers, tier 0 and tier 1 scheduled loops, no CUDA graphs."""
+d=64 and d=128 head shapes; int4, int2 and drop-topk tiers; tier 0 and tier 1
+scheduled loops; no CUDA graphs (so every launch is checked)."""
 import os
 import sys
 
@@ -9,23 +10,31 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 import vc_testlib as T  # noqa: E402
-from paper_2605_17613_b200 import TINY, Engine  # noqa: E402
+from paper_2605_17613_b200 import TINY, Engine, ModelShape  # noqa: E402
 
-w = T.tiny_weights(TINY, seed=7)
-ref = Engine(TINY, max_slots=2, max_ctx=700, max_x=8, quant_bits=0, use_graphs=False)
-ref.load_weights(w)
-for s in range(2):
-    ref.add_synthetic(s, 500, 17 + s, seed=1 + s)
-base, _ = ref.autoregress([0, 1], 12)
-ref.close()
-for kw in (dict(quant_bits=4), dict(quant_bits=2), dict(quant_bits=0, drop_ratio=0.3),
-           dict(quant_bits=4, full_tier=1, n_stage=2)):
-    e = Engine(TINY, max_slots=2, max_ctx=700, max_x=8, max_verify=2, use_graphs=False, **kw)
-    e.load_weights(w)
+D128 = ModelShape(vocab=256, hidden=512, layers=2, n_q=8, n_kv=2, d_head=128, ffn=512)
+
+
+def run(shape):
+    w = T.tiny_weights(shape, seed=7)
+    ref = Engine(shape, max_slots=2, max_ctx=700, max_x=8, quant_bits=0, use_graphs=False)
+    ref.load_weights(w)
     for s in range(2):
-        e.add_synthetic(s, 500, 17 + s, seed=1 + s)
-        e.compress(s)
-    out, st = e.run_scheduled([0, 1], 12, x=4, window=16)
-    assert np.array_equal(out, base), kw
-    e.close()
+        ref.add_synthetic(s, 500, 17 + s, seed=1 + s)
+    base, _ = ref.autoregress([0, 1], 12)
+    ref.close()
+    for kw in (dict(quant_bits=4), dict(quant_bits=2), dict(quant_bits=0, drop_ratio=0.3),
+               dict(quant_bits=4, full_tier=1, n_stage=2)):
+        e = Engine(shape, max_slots=2, max_ctx=700, max_x=8, max_verify=2, use_graphs=False, **kw)
+        e.load_weights(w)
+        for s in range(2):
+            e.add_synthetic(s, 500, 17 + s, seed=1 + s)
+            e.compress(s)
+        out, st = e.run_scheduled([0, 1], 12, x=4, window=16)
+        assert np.array_equal(out, base), (shape, kw)
+        e.close()
+
+
+for shape in (TINY, D128):
+    run(shape)
 print("sanitize smoke ok")
