@@ -34,6 +34,9 @@
  *                                   180, 219; src/sim.cpp:243-250)
  *   vc_run_scheduled                simulate_staggered's loop with real kernels
  *                                   and copies (src/sim.cpp:182-307)
+ *   vc_engine_attach_nccl / vc_tp_* no reference counterpart: the simulator
+ *                                   models TP only as GPU counts (core.hpp:45-46);
+ *                                   BASELINE.json configs[4] (TP=8 over NVLink)
  */
 #ifndef VC_API_H
 #define VC_API_H
@@ -64,6 +67,10 @@ typedef struct {
   int use_graphs;  /* capture steps into CUDA graphs */
   double drop_ratio; /* > 0: drop-topk compressor (retained fraction c in (0,1));
                         exclusive with quant_bits (compressor.cpp:245-254) */
+  int tp_size;       /* head-sharded tensor parallelism (configs[4]); 0 or 1 = off.
+                        vc_model_desc stays the FULL model; this rank holds
+                        n_q/tp_size and n_kv/tp_size heads and ffn/tp_size of the MLP */
+  int tp_rank;
 } vc_runtime_desc;
 
 /* Mirrors speckv::CompressedKVMeta (compressor.hpp:56-65).  Quant-uniform:
@@ -122,6 +129,19 @@ int vc_engine_timing(vc_engine* e, double* device_ms, int64_t* steps, int reset)
  * algorithmic bytes one launch-set moves.           */
 int vc_kernel_bench(vc_engine* e, int kind, const int* slots, int n, int reps, double* ms,
                     double* bytes);
+
+/* ---- tensor parallelism (head-sharded, configs[4]) -------------------------
+ * The o_proj / down_proj partials of the ranks are combined as an all-gather
+ * plus a fixed rank-order sum (batch-invariant, so verify logits still equal
+ * decode logits bit for bit).  Collectives: NCCL over NVLink (one process per
+ * GPU; rank 0 creates the 128-byte unique id and shares it), or an in-process
+ * loopback group (one host thread per rank on one device; steps run eagerly). */
+typedef struct vc_tp_group vc_tp_group;
+int vc_nccl_get_unique_id(uint8_t* out128);
+int vc_engine_attach_nccl(vc_engine* e, const uint8_t* unique_id128);
+int vc_tp_loopback_create(int size, vc_tp_group** out);
+int vc_tp_loopback_destroy(vc_tp_group* g);
+int vc_engine_attach_loopback(vc_engine* e, vc_tp_group* g);
 
 /* ---- requests ----------------------------------------------------------- */
 int vc_request_add_synthetic(vc_engine* e, int slot, int n_ctx, int32_t first_token, uint64_t seed,

@@ -41,7 +41,8 @@ class ModelDesc(C.Structure):
 class RuntimeDesc(C.Structure):
     _fields_ = [("max_slots", C.c_int), ("max_ctx", C.c_int), ("max_x", C.c_int),
                 ("quant_bits", C.c_int), ("full_tier", C.c_int), ("n_stage", C.c_int),
-                ("max_verify", C.c_int), ("use_graphs", C.c_int), ("drop_ratio", C.c_double)]
+                ("max_verify", C.c_int), ("use_graphs", C.c_int), ("drop_ratio", C.c_double),
+                ("tp_size", C.c_int), ("tp_rank", C.c_int)]
 
 
 class CompressedMeta(C.Structure):
@@ -104,6 +105,11 @@ SIGNATURES = {
     "vc_compressed_read": (I, [P, I, I, I, PU32, PU32, PU32, PU32, PU16, PU16]),
     "vc_compressed_geometry": (I, [P, PI, PI, PI, PI]),
     "vc_drop_kept": (I, [P, I, I, C.POINTER(C.c_int32), I, PI]),
+    "vc_nccl_get_unique_id": (I, [C.POINTER(C.c_uint8)]),
+    "vc_engine_attach_nccl": (I, [P, C.POINTER(C.c_uint8)]),
+    "vc_tp_loopback_create": (I, [I, C.POINTER(P)]),
+    "vc_tp_loopback_destroy": (I, [P]),
+    "vc_engine_attach_loopback": (I, [P, P]),
     "vc_drop_indices": (I64, [I, I, I, I64, D, U64, I, PI64]),
     "vc_update_window": (I, [I, I, I, I, PI64, PI64, PI64, PI64, PI64, I64, PI64]),
     "vc_topk_select": (I, [P, I, I, I, P, P]),

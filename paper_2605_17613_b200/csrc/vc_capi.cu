@@ -10,6 +10,9 @@
 #include "vc_api.h"
 #include "vc_engine.hpp"
 #include "vc_topk.h"
+#include "vc_tp.h"
+
+#include <memory>
 
 struct vc_engine {
   vc::Engine* impl;
@@ -84,6 +87,17 @@ int vc_engine_create(const vc_model_desc* model, const vc_runtime_desc* rt, int 
     c.max_verify = rt->max_verify;
     c.use_graphs = rt->use_graphs;
     c.drop_ratio = rt->drop_ratio;
+    c.tp_size = rt->tp_size > 1 ? rt->tp_size : 1;
+    c.tp_rank = c.tp_size > 1 ? rt->tp_rank : 0;
+    if (c.tp_size > 1) {  // this rank's shard of the heads and of the MLP
+      const int T = c.tp_size;
+      if (c.tp_rank < 0 || c.tp_rank >= T) throw speckv::ConfigError("tensor parallel: rank out of range");
+      if (c.model.n_kv % T || c.model.n_q % T || c.model.ffn % (64 * T))
+        throw speckv::ConfigError("tensor parallel: n_kv, n_q and ffn/64 must divide by tp_size");
+      c.model.n_q /= T;
+      c.model.n_kv /= T;
+      c.model.ffn /= T;
+    }
     if (c.drop_ratio < 0.0 || c.drop_ratio >= 1.0)
       throw speckv::ConfigError("compressor: drop ratio must be in (0, 1)");
     if (c.drop_ratio > 0.0 && c.quant_bits != 0)  // speckv::check_mode_exclusivity (compressor.cpp:245-254)
@@ -98,6 +112,43 @@ int vc_engine_create(const vc_model_desc* model, const vc_runtime_desc* rt, int 
       throw;
     }
     *out = h;
+  });
+}
+
+struct vc_tp_group {
+  std::shared_ptr<vc::LoopbackGroup> g;
+};
+
+int vc_nccl_get_unique_id(uint8_t* out128) {
+  return guard([&] {
+    if (!out128) throw vc::ContractViolation("nccl id: null buffer");
+    if (!vc::nccl_unique_id(out128)) throw vc::ContractViolation("libnccl.so.2 not found");
+  });
+}
+
+int vc_engine_attach_nccl(vc_engine* e, const uint8_t* id) {
+  return guard([&] {
+    vc::Engine& en = E(e);
+    en.attach_collective(vc::make_nccl(id, en.config().tp_rank, en.config().tp_size));
+  });
+}
+
+int vc_tp_loopback_create(int size, vc_tp_group** out) {
+  return guard([&] {
+    if (!out) throw vc::ContractViolation("loopback: null out");
+    *out = new vc_tp_group{vc::make_loopback_group(size)};
+  });
+}
+
+int vc_tp_loopback_destroy(vc_tp_group* g) {
+  return guard([&] { delete g; });
+}
+
+int vc_engine_attach_loopback(vc_engine* e, vc_tp_group* g) {
+  return guard([&] {
+    if (!g) throw vc::ContractViolation("loopback: null group");
+    vc::Engine& en = E(e);
+    en.attach_collective(vc::make_loopback(g->g, en.config().tp_rank));
   });
 }
 

@@ -108,6 +108,7 @@ Engine::~Engine() {
   }
   void* ptrs[] = {weight_blob_, rope_cos_, rope_sin_, full_.k, full_.v, stage_.k, stage_.v,
                   quant_.rec, quant_.ktail, quant_.vtail, drop_.k, drop_.v, score_buf_, score_w_, kept_buf_,
+                  tp_y_, tp_g_,
                   x_, xn_, qkv_, attn_, act_, gws_.partial, gws_.counters, ss_part_, logits_,
                   tok_in_, tok_out_, part_.o, part_.ml, rows_dev_, seqs_dev_, jobs_dev_};
   for (void* p : ptrs)
@@ -308,6 +309,10 @@ void Engine::alloc_all() {
     gws_.counters = dmalloc<int>(gws_.n_counters);
   }
   ss_part_ = dmalloc<float>(static_cast<size_t>(Mmax_) * (H / 128));
+  if (cfg_.tp_size > 1) {
+    tp_y_ = dmalloc<float>(static_cast<size_t>(Mmax_) * H);
+    tp_g_ = dmalloc<float>(static_cast<size_t>(cfg_.tp_size) * Mmax_ * H);
+  }
   logits_ = dmalloc<float>(static_cast<size_t>(Mmax_) * V);
   tok_in_ = dmalloc<int32_t>(Mmax_);
   tok_out_ = dmalloc<int32_t>(Mmax_);
@@ -326,6 +331,14 @@ void Engine::alloc_all() {
                 static_cast<size_t>(L) * m.n_kv * sizeof(QuantJob);
   VC_CK(cudaHostAlloc(&h_desc_, desc_bytes_, cudaHostAllocDefault));
   VC_CK(cudaHostAlloc(reinterpret_cast<void**>(&h_out_), Mmax_ * sizeof(int32_t), cudaHostAllocDefault));
+}
+
+void Engine::attach_collective(std::unique_ptr<Collective> c) {
+  if (cfg_.tp_size <= 1) throw ContractViolation("attach_collective: engine is not tensor-parallel");
+  coll_ = std::move(c);
+  for (auto& [k, g] : graphs_) cudaGraphExecDestroy(g);  // captured without the collective
+  graphs_.clear();
+  launches_per_graph_.clear();
 }
 
 // ---------------------------------------------------------------- weights
@@ -672,7 +685,21 @@ void Engine::enqueue_forward(int M, int n_draft, int n_dense1, int n_densev, int
       VC_LAUNCH(dense_attention(as, dense_v_pool, dense_maps_, l, sv, n_densev, max_chunks_d_, max_rows_v, part_, st_));
       VC_LAUNCH(attention_combine(as, sv, n_densev, max_chunks_d_, max_rows_v, 1, part_, attn_, st_));
     }
-    VC_LAUNCH(gemm(attn_, M, M, m.n_q * d, w_.wo[l], H, er, gws_, st_));
+    // residual projection: fused residual epilogue, or (tensor parallel) the
+    // rank's partial -> all-gather -> fixed rank-order sum + residual (vc_tp.h)
+    auto residual_gemm = [&](const uint16_t* Xt, int Kd, const uint16_t* Wt) {
+      if (cfg_.tp_size == 1) {
+        VC_LAUNCH(gemm(Xt, M, M, Kd, Wt, H, er, gws_, st_));
+        return;
+      }
+      GemmEpilogue ey;
+      ey.kind = Epi::StoreF32;
+      ey.out_f32 = tp_y_;
+      VC_LAUNCH(gemm(Xt, M, M, Kd, Wt, H, ey, gws_, st_));
+      coll_->all_gather(tp_y_, tp_g_, static_cast<size_t>(M) * H, st_);
+      VC_LAUNCH(tp_residual(x_, tp_g_, cfg_.tp_size, M, H, ss_part_, st_));
+    };
+    residual_gemm(attn_, m.n_q * d, w_.wo[l]);
     trace("attn", attn_, static_cast<size_t>(M) * m.n_q * d * 2);
     trace("x.o", x_, static_cast<size_t>(M) * H * 4);
     trace("ss.o", ss_part_, static_cast<size_t>(M) * (H / 128) * 4);
@@ -680,7 +707,7 @@ void Engine::enqueue_forward(int M, int n_draft, int n_dense1, int n_densev, int
     trace("xn.o", xn_, static_cast<size_t>(M) * H * 2);
     VC_LAUNCH(gemm(xn_, M, M, H, w_.wgu[l], 2 * F, es, gws_, st_));
     trace("act", act_, static_cast<size_t>(M) * F * 2);
-    VC_LAUNCH(gemm(act_, M, M, F, w_.wd[l], H, er, gws_, st_));
+    residual_gemm(act_, F, w_.wd[l]);
     trace("x.d", x_, static_cast<size_t>(M) * H * 4);
     VC_LAUNCH(rms_apply(x_, ss_part_, M, M, H, l + 1 < L ? w_.attn_norm[l + 1] : w_.final_norm, m.eps,
                         xn_, st_));
@@ -781,9 +808,10 @@ void Engine::run_step(const std::vector<StepItem>& items, std::vector<int32_t>& 
   for (auto& a : densev) h_seqs[k++] = a;
   if (k > n_seq_max) throw ContractViolation("run_step: too many sequences");
 
+  if (cfg_.tp_size > 1 && !coll_) throw ContractViolation("tensor-parallel engine: attach a collective first");
   cudaGraphExec_t exec = nullptr;
   std::string key;
-  if (cfg_.use_graphs) {  // capture (host work) before the timed device window opens
+  if (cfg_.use_graphs && (!coll_ || coll_->graph_capturable())) {  // capture before the timed window opens
     std::ostringstream ks;
     ks << Mb << ':' << nd << ':' << n1 << ':' << nv << ':' << mrv;
     key = ks.str();

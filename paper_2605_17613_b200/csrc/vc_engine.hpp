@@ -23,6 +23,7 @@
 
 #include "vc_gemm.h"
 #include "vc_kernels.h"
+#include "vc_tp.h"
 
 namespace vc {
 
@@ -42,6 +43,10 @@ struct EngineConfig {
   int n_stage = 2;      // HBM staging slots (tier 1)
   int max_verify = 2;   // verify requests per step
   int use_graphs = 1;
+  // head-sharded tensor parallelism: `model` is this rank's shard (n_q, n_kv,
+  // ffn already divided by tp_size); o_proj/down_proj partials are combined
+  // through the attached Collective (vc_tp.h)
+  int tp_size = 1, tp_rank = 0;
 };
 
 enum class RowMode : int { Decode = 0, Draft = 1, Verify = 2 };
@@ -79,6 +84,9 @@ class Engine {
 
   const EngineConfig& config() const { return cfg_; }
   const ModelDesc& model() const { return cfg_.model; }
+
+  // ---- tensor parallelism ---------------------------------------------
+  void attach_collective(std::unique_ptr<Collective> c);
 
   // ---- weights -------------------------------------------------------
   void init_weights_random(uint64_t seed, float stddev, float resid_std = 0.f, float q_std = 0.f);
@@ -214,6 +222,9 @@ class Engine {
   std::vector<SeqState> seqs_;
   int last_M_ = 0;
   uint64_t launches_ = 0;
+  // tensor parallelism: partial projection output and the gathered partials
+  std::unique_ptr<Collective> coll_;
+  float *tp_y_ = nullptr, *tp_g_ = nullptr;
   // graphs keyed by step shape
   std::map<std::string, cudaGraphExec_t> graphs_;
   std::map<std::string, uint64_t> launches_per_graph_;

@@ -101,17 +101,21 @@ class Engine:
     """One serving instance on one GPU (vc_engine)."""
 
     def __init__(self, model: ModelShape, *, max_slots=1, max_ctx=4096, max_x=16, quant_bits=4,
-                 full_tier=0, n_stage=2, max_verify=2, use_graphs=True, device=0, drop_ratio=0.0):
+                 full_tier=0, n_stage=2, max_verify=2, use_graphs=True, device=0, drop_ratio=0.0,
+                 tp_size=1, tp_rank=0):
         """quant_bits > 0: quant-uniform compressor (KIVI int4/int2);
         drop_ratio in (0, 1): drop-topk compressor keeping llround(c*T) tokens per
-        (layer, head) -- the two are exclusive (compressor.cpp:245-254)."""
+        (layer, head) -- the two are exclusive (compressor.cpp:245-254).
+        tp_size > 1: this engine is rank tp_rank of a head-sharded tensor-parallel
+        group (`model` is the full model; attach_nccl / attach_loopback before stepping)."""
         self.lib = _lib.load()
         self.model = model
         self.max_x = max_x
         md = _lib.ModelDesc(model.vocab, model.hidden, model.layers, model.n_q, model.n_kv,
                             model.d_head, model.ffn, model.rope_theta, model.rms_eps)
         rt = _lib.RuntimeDesc(max_slots, max_ctx, max_x, quant_bits, full_tier, n_stage,
-                              max_verify, int(use_graphs), float(drop_ratio))
+                              max_verify, int(use_graphs), float(drop_ratio), int(tp_size), int(tp_rank))
+        self.tp_size, self.tp_rank = int(tp_size), int(tp_rank)
         h = C.c_void_p()
         check(self.lib.vc_engine_create(C.byref(md), C.byref(rt), device, C.byref(h)))
         self.h = h
@@ -138,7 +142,10 @@ class Engine:
             check(self.lib.vc_engine_init_weights(self.h, seed, std))
 
     def load_weights(self, w: dict):
-        """w: logical bf16-bit arrays (uint16) as oracle/vc_oracle.h documents."""
+        """w: logical bf16-bit arrays (uint16) as oracle/vc_oracle.h documents
+        (the FULL model; a tensor-parallel rank takes its shard, tp_shard)."""
+        if self.tp_size > 1:
+            w = tp_shard(w, self.model, self.tp_size, self.tp_rank)
         L = self.model.layers
         keep = []
 
@@ -155,6 +162,14 @@ class Engine:
         check(self.lib.vc_engine_load_weights(
             self.h, arr(w["embed"]), lst("attn_norm"), lst("wqkv"), lst("wo"), lst("mlp_norm"),
             lst("wgate"), lst("wup"), lst("wdown"), arr(w["final_norm"]), arr(w["lm_head"])))
+
+    # ---- tensor parallelism -----------------------------------------------------
+    def attach_nccl(self, unique_id: bytes):
+        buf = (C.c_uint8 * 128).from_buffer_copy(unique_id)
+        check(self.lib.vc_engine_attach_nccl(self.h, buf))
+
+    def attach_loopback(self, group: "TpLoopback"):
+        check(self.lib.vc_engine_attach_loopback(self.h, group.h))
 
     def stats(self):
         n, b = C.c_uint64(), C.c_uint64()
@@ -342,3 +357,57 @@ class Engine:
         check(self.lib.vc_attention_probe(self.h, slot, layer, mode, C.c_void_p(q_dev_ptr), n_rows,
                                           kv_len, _ptr(out, C.c_uint16)))
         return out
+
+
+def tp_shard(w: dict, model: ModelShape, tp: int, rank: int) -> dict:
+    """Rank `rank`'s shard of full logical weights for head-sharded TP: q/k/v
+    rows of its n_q/tp query and n_kv/tp KV heads, the matching o_proj input
+    columns, ffn/tp gate/up rows and down_proj input columns; embedding, norms
+    and LM head replicated."""
+    d, nq, nkv, F = model.d_head, model.n_q, model.n_kv, model.ffn
+    ql, kl, fl = nq // tp * d, nkv // tp * d, F // tp
+    out = dict(w)
+
+    def qkv(a):
+        a = np.asarray(a).reshape((nq + 2 * nkv) * d, -1)
+        q = a[rank * ql:(rank + 1) * ql]
+        k = a[nq * d + rank * kl:nq * d + (rank + 1) * kl]
+        v = a[(nq + nkv) * d + rank * kl:(nq + nkv) * d + (rank + 1) * kl]
+        return np.ascontiguousarray(np.concatenate([q, k, v]))
+
+    out["wqkv"] = [qkv(a) for a in w["wqkv"]]
+    out["wo"] = [np.ascontiguousarray(np.asarray(a).reshape(model.hidden, nq * d)[:, rank * ql:(rank + 1) * ql])
+                 for a in w["wo"]]
+    out["wgate"] = [np.ascontiguousarray(np.asarray(a).reshape(F, -1)[rank * fl:(rank + 1) * fl]) for a in w["wgate"]]
+    out["wup"] = [np.ascontiguousarray(np.asarray(a).reshape(F, -1)[rank * fl:(rank + 1) * fl]) for a in w["wup"]]
+    out["wdown"] = [np.ascontiguousarray(np.asarray(a).reshape(model.hidden, F)[:, rank * fl:(rank + 1) * fl])
+                    for a in w["wdown"]]
+    return out
+
+
+class TpLoopback:
+    """In-process tensor-parallel group on one device (one host thread per rank)."""
+
+    def __init__(self, size: int):
+        self.lib = _lib.load()
+        h = C.c_void_p()
+        check(self.lib.vc_tp_loopback_create(size, C.byref(h)))
+        self.h = h
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.vc_tp_loopback_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def nccl_unique_id() -> bytes:
+    lib = _lib.load()
+    buf = (C.c_uint8 * 128)()
+    check(lib.vc_nccl_get_unique_id(buf))
+    return bytes(buf)
