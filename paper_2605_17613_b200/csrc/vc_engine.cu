@@ -334,7 +334,13 @@ void Engine::alloc_all() {
 }
 
 void Engine::attach_collective(std::unique_ptr<Collective> c) {
-  if (cfg_.tp_size <= 1) throw ContractViolation("attach_collective: engine is not tensor-parallel");
+  // tp_size 1 with a collective runs the TP residual path over a one-rank
+  // group (bit-identical to the fused epilogue; exercises the collective)
+  if (!tp_y_) {
+    const size_t n = static_cast<size_t>(Mmax_) * cfg_.model.hidden;
+    tp_y_ = dmalloc<float>(n);
+    tp_g_ = dmalloc<float>(static_cast<size_t>(cfg_.tp_size) * n);
+  }
   coll_ = std::move(c);
   for (auto& [k, g] : graphs_) cudaGraphExecDestroy(g);  // captured without the collective
   graphs_.clear();
@@ -688,7 +694,7 @@ void Engine::enqueue_forward(int M, int n_draft, int n_dense1, int n_densev, int
     // residual projection: fused residual epilogue, or (tensor parallel) the
     // rank's partial -> all-gather -> fixed rank-order sum + residual (vc_tp.h)
     auto residual_gemm = [&](const uint16_t* Xt, int Kd, const uint16_t* Wt) {
-      if (cfg_.tp_size == 1) {
+      if (!coll_) {
         VC_LAUNCH(gemm(Xt, M, M, Kd, Wt, H, er, gws_, st_));
         return;
       }

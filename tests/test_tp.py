@@ -6,8 +6,10 @@ thread each): the TP=2 forward matches the unsharded model within the logit
 tolerance, both ranks compute bit-identical logits, and speculative decoding
 over the sharded compressed tiers is lossless against the sharded full-KV
 decode (the all-gather + rank-order sum keeps the combine batch-invariant).
-The NCCL path (one process per GPU) is the same engine code with
-vc_engine_attach_nccl; it needs >= 2 GPUs and is not exercised here."""
+The NCCL path (one process per GPU, vc_engine_attach_nccl) runs the same
+engine code; with one GPU it is exercised as a one-rank NCCL group (all-gather
+captured in the CUDA graph), which must be bit-identical to the fused
+residual epilogue.  A multi-GPU TP run needs >= 2 GPUs."""
 import threading
 
 import numpy as np
@@ -112,3 +114,33 @@ def test_tp2_speculative_lossless(cuda, weights, bits):
     for e in ranks:
         e.close()
     group.close()
+
+
+@pytest.mark.gpu
+def test_nccl_one_rank_collective_bit_identical(cuda, weights):
+    """The NCCL collective path on real hardware: a one-rank NCCL group runs
+    the TP residual path (all-gather inside the CUDA graph + rank-order sum),
+    which must be bit-identical to the fused residual epilogue, and lossless."""
+    from paper_2605_17613_b200 import _lib, nccl_unique_id
+    try:
+        uid = nccl_unique_id()
+    except _lib.VcError:
+        pytest.skip("libnccl.so.2 not available")
+    kv = T.synthetic_kv(TINY.layers, TINY.n_kv, N_CTX, TINY.d_head, seed=8)
+    outs = []
+    for with_nccl in (False, True):
+        e = Engine(TINY, max_slots=2, max_ctx=N_CTX + 200, max_x=8, max_verify=2, quant_bits=4)
+        if with_nccl:
+            e.attach_nccl(uid)
+        e.load_weights(weights)
+        for s in range(2):
+            e.add_kv(s, kv[0], kv[1], first_token=17)
+        _, logits = e.step([(0, 0, [17], -1)], want_logits=True)
+        base, _ = e.autoregress([0], 16)
+        e.compress(1)
+        spec, _, _ = e.run_speculative([1], 16, 4)
+        outs.append((logits, base, spec))
+        e.close()
+    assert np.array_equal(outs[0][0].view(np.uint32), outs[1][0].view(np.uint32))
+    np.testing.assert_array_equal(outs[0][1], outs[1][1])
+    np.testing.assert_array_equal(outs[1][2], outs[1][1])
