@@ -218,6 +218,15 @@ int vc_run_decode(vc_engine* e, const int* slots, int n, int K, int32_t* out, do
 int vc_run_speculative(vc_engine* e, const int* slots, int n, int K, int x, int32_t* out,
                        int32_t* rounds, int max_rounds, int* n_rounds, double* ms);
 
+/* Same loop with the drafter composed with n-gram (prompt-lookup) drafts
+ * (BASELINE.json configs[4] "int4 compressor composed with n-gram speculative
+ * drafts"): a request whose emitted history repeats
+ * its last `ngram` tokens drafts the continuation that followed (up to x tokens,
+ * no draft steps); the others draft over the compressed tier; all verify in
+ * one full-KV pass.  ngram_rounds [n] = rounds that used an n-gram draft.     */
+int vc_run_speculative_ngram(vc_engine* e, const int* slots, int n, int K, int x, int ngram, int32_t* out,
+                             int32_t* rounds, int max_rounds, int* n_rounds, int* ngram_rounds, double* ms);
+
 /* Swap-scheduled loop (tier 1): SpecScheduler semantics drive real draft
  * rows, verify rows and H2D reloads (Algorithm 1).     */
 typedef struct {

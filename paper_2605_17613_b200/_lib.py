@@ -124,6 +124,7 @@ SIGNATURES = {
     "vc_swap_poll": (I, [P, U64, PI]),
     "vc_run_decode": (I, [P, PI, I, I, PI32, PD]),
     "vc_run_speculative": (I, [P, PI, I, I, I, PI32, PI32, I, PI, PD]),
+    "vc_run_speculative_ngram": (I, [P, PI, I, I, I, I, PI32, PI32, I, PI, PI, PD]),
     "vc_run_scheduled": (I, [P, PI, I, C.POINTER(SchedDesc), PI32, C.POINTER(SchedStats)]),
     "vc_reload_span": (I, [I64, D, D, PD, PI]),
     "vc_quant_kivi_slice": (I, [P, P, I, I, I, P, P, P, P, P]),

@@ -533,57 +533,105 @@ int vc_run_decode(vc_engine* e, const int* slots, int n, int K, int32_t* out, do
   });
 }
 
-int vc_run_speculative(vc_engine* e, const int* slots, int n, int K, int x, int32_t* out,
-                       int32_t* rounds, int max_rounds, int* n_rounds, double* ms) {
-  return guard([&] {
-    vc::Engine& en = E(e);
-    if (x < 1 || x > en.config().max_x) throw speckv::ConfigError("run_speculative: x out of [1, max_x]");
-    if (en.config().full_tier != 0) throw vc::ContractViolation("lock-step loop needs the HBM full tier");
-    std::vector<int> produced(n, 0), nr(n, 0);
-    std::vector<vc::StepItem> its;
-    std::vector<int32_t> row;
-    const auto t0 = std::chrono::steady_clock::now();
-    for (;;) {
-      std::vector<int> act;
-      for (int i = 0; i < n; ++i)
-        if (produced[i] < K) act.push_back(i);
-      if (act.empty()) break;
-      for (int j = 0; j < x; ++j) {  // x draft steps over the compressed tier
-        its.assign(act.size(), vc::StepItem{});
-        for (size_t a = 0; a < act.size(); ++a) {
-          const vc::SeqState& s = en.seq(slots[act[a]]);
-          its[a].slot = slots[act[a]];
-          its[a].mode = vc::RowMode::Draft;
-          its[a].tokens = {s.drafted.empty() ? s.pending : s.drafted.back()};
-        }
-        en.run_step(its, row);
-        for (size_t a = 0; a < act.size(); ++a) en.push_draft(slots[act[a]], row[a]);
+namespace {
+
+// Prompt-lookup n-gram proposal: the continuation (<= x tokens) that followed
+// the most recent earlier occurrence of the last `ng` emitted tokens.
+std::vector<int32_t> ngram_proposal(const std::vector<int32_t>& h, int ng, int x) {
+  std::vector<int32_t> out;
+  const int n = static_cast<int>(h.size());
+  if (ng < 1 || n <= ng) return out;
+  for (int j = n - ng - 1; j >= 0; --j) {
+    bool hit = true;
+    for (int k = 0; k < ng && hit; ++k) hit = h[j + k] == h[n - ng + k];
+    if (!hit) continue;
+    for (int k = j + ng; k < n && static_cast<int>(out.size()) < x; ++k) out.push_back(h[k]);
+    break;
+  }
+  return out;
+}
+
+// Lock-step rounds (speckv::run_speculative, specloop.cpp:58-79).  With
+// ngram > 0 the round's drafter is composed: a request whose emitted history
+// repeats its last `ngram` tokens takes the n-gram continuation as its draft
+// (no draft steps); the others draft x tokens over the compressed tier.  Both
+// kinds verify in the same full-KV pass; losslessness is unaffected because
+// the verifier alone decides what is emitted.
+void speculative_loop(vc::Engine& en, const int* slots, int n, int K, int x, int ngram, int32_t* out,
+                      int32_t* rounds, int max_rounds, int* n_rounds, int* ngram_rounds, double* ms) {
+  if (x < 1 || x > en.config().max_x) throw speckv::ConfigError("run_speculative: x out of [1, max_x]");
+  if (en.config().full_tier != 0) throw vc::ContractViolation("lock-step loop needs the HBM full tier");
+  std::vector<int> produced(n, 0), nr(n, 0), ngr(n, 0);
+  std::vector<vc::StepItem> its;
+  std::vector<int32_t> row;
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    std::vector<int> act, model;
+    for (int i = 0; i < n; ++i)
+      if (produced[i] < K) act.push_back(i);
+    if (act.empty()) break;
+    for (int i : act) {
+      const auto prop = ngram_proposal(en.seq(slots[i]).history, ngram, x);
+      if (prop.empty()) {
+        model.push_back(i);
+        continue;
       }
-      its.assign(act.size(), vc::StepItem{});  // one verify pass over the full KV
-      for (size_t a = 0; a < act.size(); ++a) {
-        const vc::SeqState& s = en.seq(slots[act[a]]);
-        its[a].slot = slots[act[a]];
-        its[a].mode = vc::RowMode::Verify;
-        its[a].tokens.push_back(s.pending);
-        its[a].tokens.insert(its[a].tokens.end(), s.drafted.begin(), s.drafted.end());
+      for (int32_t t : prop) en.push_draft(slots[i], t);  // drafted without a model step
+      ++ngr[i];
+    }
+    for (int j = 0; j < x && !model.empty(); ++j) {  // x draft steps over the compressed tier
+      its.assign(model.size(), vc::StepItem{});
+      for (size_t a = 0; a < model.size(); ++a) {
+        const vc::SeqState& s = en.seq(slots[model[a]]);
+        its[a].slot = slots[model[a]];
+        its[a].mode = vc::RowMode::Draft;
+        its[a].tokens = {s.drafted.empty() ? s.pending : s.drafted.back()};
       }
       en.run_step(its, row);
-      size_t off = 0;
-      for (size_t a = 0; a < act.size(); ++a) {
-        const int i = act[a];
-        std::vector<int32_t> p(row.begin() + off, row.begin() + off + x + 1);
-        off += x + 1;
-        auto em = en.accept_commit(slots[i], p);
-        if (rounds && nr[i] < max_rounds) rounds[static_cast<size_t>(i) * max_rounds + nr[i]] = static_cast<int32_t>(em.size());
-        ++nr[i];
-        for (int32_t t : em)
-          if (produced[i] < K) out[static_cast<size_t>(i) * K + produced[i]++] = t;  // truncate at K
-      }
+      for (size_t a = 0; a < model.size(); ++a) en.push_draft(slots[model[a]], row[a]);
     }
-    const auto t1 = std::chrono::steady_clock::now();
-    if (ms) *ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
-    if (n_rounds)
-      for (int i = 0; i < n; ++i) n_rounds[i] = nr[i];
+    its.assign(act.size(), vc::StepItem{});  // one verify pass over the full KV
+    for (size_t a = 0; a < act.size(); ++a) {
+      const vc::SeqState& s = en.seq(slots[act[a]]);
+      its[a].slot = slots[act[a]];
+      its[a].mode = vc::RowMode::Verify;
+      its[a].tokens.push_back(s.pending);
+      its[a].tokens.insert(its[a].tokens.end(), s.drafted.begin(), s.drafted.end());
+    }
+    en.run_step(its, row);
+    size_t off = 0;
+    for (size_t a = 0; a < act.size(); ++a) {
+      const int i = act[a];
+      const size_t xi = en.seq(slots[i]).drafted.size();
+      std::vector<int32_t> p(row.begin() + off, row.begin() + off + xi + 1);
+      off += xi + 1;
+      auto em = en.accept_commit(slots[i], p);
+      if (rounds && nr[i] < max_rounds) rounds[static_cast<size_t>(i) * max_rounds + nr[i]] = static_cast<int32_t>(em.size());
+      ++nr[i];
+      for (int32_t t : em)
+        if (produced[i] < K) out[static_cast<size_t>(i) * K + produced[i]++] = t;  // truncate at K
+    }
+  }
+  const auto t1 = std::chrono::steady_clock::now();
+  if (ms) *ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+  for (int i = 0; i < n; ++i) {
+    if (n_rounds) n_rounds[i] = nr[i];
+    if (ngram_rounds) ngram_rounds[i] = ngr[i];
+  }
+}
+
+}  // namespace
+
+int vc_run_speculative(vc_engine* e, const int* slots, int n, int K, int x, int32_t* out,
+                       int32_t* rounds, int max_rounds, int* n_rounds, double* ms) {
+  return guard([&] { speculative_loop(E(e), slots, n, K, x, 0, out, rounds, max_rounds, n_rounds, nullptr, ms); });
+}
+
+int vc_run_speculative_ngram(vc_engine* e, const int* slots, int n, int K, int x, int ngram, int32_t* out,
+                             int32_t* rounds, int max_rounds, int* n_rounds, int* ngram_rounds, double* ms) {
+  return guard([&] {
+    if (ngram < 1) throw speckv::ConfigError("run_speculative_ngram: ngram must be >= 1");
+    speculative_loop(E(e), slots, n, K, x, ngram, out, rounds, max_rounds, n_rounds, ngram_rounds, ms);
   });
 }
 

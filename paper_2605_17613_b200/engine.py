@@ -319,6 +319,20 @@ class Engine:
                                           C.byref(ms)))
         return out, [rounds[i, : nr[i]].tolist() for i in range(s.size)], ms.value
 
+    def run_speculative_ngram(self, slots, K, x, ngram=3, max_rounds=4096):
+        """run_speculative with the drafter composed with n-gram (prompt-lookup)
+        drafts -> (tokens [n][K], emitted per round, n-gram rounds per slot, ms)."""
+        s = np.ascontiguousarray(slots, np.int32)
+        out = np.zeros((s.size, K), np.int32)
+        rounds = np.zeros((s.size, max_rounds), np.int32)
+        nr = np.zeros(s.size, np.int32)
+        ng = np.zeros(s.size, np.int32)
+        ms = C.c_double()
+        check(self.lib.vc_run_speculative_ngram(self.h, _ptr(s, C.c_int), s.size, K, x, ngram,
+                                                _ptr(out, C.c_int32), _ptr(rounds, C.c_int32), max_rounds,
+                                                _ptr(nr, C.c_int), _ptr(ng, C.c_int), C.byref(ms)))
+        return out, [rounds[i, : nr[i]].tolist() for i in range(s.size)], ng.tolist(), ms.value
+
     def timing(self, reset=False):
         ms, n = C.c_double(), C.c_int64()
         check(self.lib.vc_engine_timing(self.h, C.byref(ms), C.byref(n), int(reset)))
