@@ -232,11 +232,18 @@ def main():
     import paper_2605_17613_b200 as vc
     from paper_2605_17613_b200.shard import reduce_window, weak_shard
 
-    torch.cuda.set_device(local)
+    n_dev = torch.cuda.device_count()
+    torch.cuda.set_device(local % n_dev)
+    local = local % n_dev
     dist = None
+    coll_dev = "cuda"
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if os.environ.get("BENCH_BACKEND", "nccl") == "gloo":  # ranks sharing a GPU (host-logic check)
+            dist.init_process_group("gloo")
+            coll_dev = "cpu"
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     peaks = json.load(open(PEAKS)) if os.path.exists(PEAKS) else {}
     peak, peak_src = hbm_peak(peaks)
     shape = vc.TINY if args.small else vc.LLAMA3_8B
@@ -324,7 +331,7 @@ def main():
         torch.cuda.empty_cache()
         tok_all, (dev_s, wall_s) = reduce_window(float(st["timed_tokens"]),
                                                  [st["timed_device_ms"] / 1e3, st["timed_wall_ms"] / 1e3],
-                                                 dist, device="cuda")
+                                                 dist, device=coll_dev)
         r = {"x": x, "window": window, "ramp": ramp, "st": st, "meta": meta, "ka": ka, "launches": launches,
              "clocks": clk.summary(), "identical": identical, "compared": int(sum(cmp)),
              "tok": tok_all, "dev_s": dev_s, "wall_s": wall_s}
@@ -337,7 +344,7 @@ def main():
     st, x = h["st"], h["x"]
     tok_all, dev_s, wall_s = h["tok"], h["dev_s"], h["wall_s"]
     _, (bdev_s, bwall_s, ka_ms) = reduce_window(0.0, [base_dev / 1e3, base_wall / 1e3, h["ka"][0]], dist,
-                                                device="cuda")
+                                                device=coll_dev)
     value = tok_all / dev_s
     base_value = B * world * Kb / bdev_s
     ka_bytes = h["ka"][1]
