@@ -71,6 +71,9 @@ typedef struct {
                         vc_model_desc stays the FULL model; this rank holds
                         n_q/tp_size and n_kv/tp_size heads and ffn/tp_size of the MLP */
   int tp_rank;
+  int drop_window;   /* drop-topk tier, online mode (speckv::update, compressor.cpp:
+                        208-243): tokens accepted after compress are kept in a
+                        sliding window of the latest drop_window..2*drop_window; 0 = keep all */
 } vc_runtime_desc;
 
 /* Mirrors speckv::CompressedKVMeta (compressor.hpp:56-65).  Quant-uniform:
@@ -91,6 +94,7 @@ typedef struct {
 
 typedef struct {
   int live, committed, pending, n_groups, tail_committed, draft_len;
+  int drop_base, drop_len; /* drop-topk tier: kept prefix rows, rows in the tier */
 } vc_seq_state;
 
 /* mode: 0 decode (full KV), 1 draft (compressed KV), 2 verify (full KV) */

@@ -42,7 +42,7 @@ class RuntimeDesc(C.Structure):
     _fields_ = [("max_slots", C.c_int), ("max_ctx", C.c_int), ("max_x", C.c_int),
                 ("quant_bits", C.c_int), ("full_tier", C.c_int), ("n_stage", C.c_int),
                 ("max_verify", C.c_int), ("use_graphs", C.c_int), ("drop_ratio", C.c_double),
-                ("tp_size", C.c_int), ("tp_rank", C.c_int)]
+                ("tp_size", C.c_int), ("tp_rank", C.c_int), ("drop_window", C.c_int)]
 
 
 class CompressedMeta(C.Structure):
@@ -53,7 +53,8 @@ class CompressedMeta(C.Structure):
 
 class SeqState(C.Structure):
     _fields_ = [("live", C.c_int), ("committed", C.c_int), ("pending", C.c_int),
-                ("n_groups", C.c_int), ("tail_committed", C.c_int), ("draft_len", C.c_int)]
+                ("n_groups", C.c_int), ("tail_committed", C.c_int), ("draft_len", C.c_int),
+                ("drop_base", C.c_int), ("drop_len", C.c_int)]
 
 
 class StepItem(C.Structure):

@@ -87,6 +87,9 @@ int vc_engine_create(const vc_model_desc* model, const vc_runtime_desc* rt, int 
     c.max_verify = rt->max_verify;
     c.use_graphs = rt->use_graphs;
     c.drop_ratio = rt->drop_ratio;
+    c.drop_window = rt->drop_window;
+    if (c.drop_window < 0 || (c.drop_window > 0 && c.drop_ratio <= 0.0))
+      throw speckv::ConfigError("compressor: drop_window needs the drop-topk compressor");
     c.tp_size = rt->tp_size > 1 ? rt->tp_size : 1;
     c.tp_rank = c.tp_size > 1 ? rt->tp_rank : 0;
     if (c.tp_size > 1) {  // this rank's shard of the heads and of the MLP
@@ -230,6 +233,8 @@ int vc_request_state(vc_engine* e, int slot, vc_seq_state* out) {
     out->n_groups = s.n_groups;
     out->tail_committed = s.tail_committed;
     out->draft_len = s.draft_len;
+    out->drop_base = s.drop_base;
+    out->drop_len = s.drop_len;
   });
 }
 

@@ -262,7 +262,7 @@ void Engine::alloc_all() {
   }
   if (drop_mode()) {
     // kept tokens + up to kDropAppend exact appended tokens + the draft window
-    constexpr int kDropAppend = 4096;
+    const int kDropAppend = cfg_.drop_window > 0 ? 2 * cfg_.drop_window + cfg_.max_x + 2 : 4096;
     const int kmax = static_cast<int>(std::ceil(cfg_.drop_ratio * cfg_.max_ctx)) + 1;
     drop_.cap = static_cast<int>(round_up(static_cast<size_t>(kmax) + kDropAppend + cfg_.max_x + 2, 128));
     drop_.k = dmalloc<uint16_t>(slices * static_cast<size_t>(drop_.cap) * d);
@@ -597,6 +597,7 @@ void Engine::compress_drop(int slot, const KvPool& src, int src_slot) {
   VC_LAUNCH(gather_kept(src, src_slot, kept_buf_, static_cast<int>(k), drop_, slot, n_slices, m.d, st_));
   last_kept_k_ = static_cast<int>(k);
   s.drop_len = static_cast<int>(k);
+  s.drop_base = static_cast<int>(k);
   s.n_groups = 0;
   s.tail_committed = 0;
   s.draft_len = 0;
@@ -992,6 +993,14 @@ std::vector<int32_t> Engine::accept_commit(int slot, const std::vector<int32_t>&
     if (s.drop_len + (now - old) + cfg_.max_x + 2 > drop_.cap) throw ContractViolation("drop tier full");
     VC_LAUNCH(copy_rows(src, src_slot, old, now - old, drop_, slot, s.drop_len, m.layers * m.n_kv, m.d, st_));
     s.drop_len += now - old;
+    // online mode (speckv::update semantics, compressor.cpp:208-243, with the
+    // kept prefix as the sink): once 2W tokens have been appended, keep the
+    // latest W and drop the older ones -- one non-overlapping row move
+    const int W = cfg_.drop_window;
+    if (W > 0 && s.drop_len - s.drop_base >= 2 * W) {
+      VC_LAUNCH(copy_rows(drop_, slot, s.drop_len - W, W, drop_, slot, s.drop_base, m.layers * m.n_kv, m.d, st_));
+      s.drop_len = s.drop_base + W;
+    }
   } else if (cfg_.quant_bits > 0 && (s.n_groups > 0 || s.tail_committed > 0 || x > 0)) {
     const int ng_now = std::min(now / VC_QGROUP, quant_.cap / VC_QGROUP);
     quantise_groups(slot, s.n_groups, ng_now - s.n_groups, src, src_slot);

@@ -39,6 +39,7 @@ struct EngineConfig {
   int max_x = 16;       // largest draft horizon
   int quant_bits = 4;   // 4 or 2; 0 disables the compressed tier
   double drop_ratio = 0; // > 0: drop-topk compressed tier (retained fraction c), exclusive with quant
+  int drop_window = 0;   // > 0: online sliding window over the tokens accepted after compress
   int full_tier = 0;    // 0: full KV in HBM; 1: pinned host pool + staging
   int n_stage = 2;      // HBM staging slots (tier 1)
   int max_verify = 2;   // verify requests per step
@@ -67,6 +68,7 @@ struct SeqState {
   int tail_committed = 0; // exact tokens in the draft tail (committed - n_groups*G)
   int draft_len = 0;      // drafted tokens of the open round (their KV in the tail)
   int drop_len = 0;       // drop tier: kept prefix tokens + exact tokens appended since
+  int drop_base = 0;      // drop tier: rows of the compress-time kept prefix
   std::vector<int32_t> drafted;
   std::vector<int32_t> history;  // every emitted token
 };

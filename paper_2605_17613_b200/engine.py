@@ -102,19 +102,22 @@ class Engine:
 
     def __init__(self, model: ModelShape, *, max_slots=1, max_ctx=4096, max_x=16, quant_bits=4,
                  full_tier=0, n_stage=2, max_verify=2, use_graphs=True, device=0, drop_ratio=0.0,
-                 tp_size=1, tp_rank=0):
+                 tp_size=1, tp_rank=0, drop_window=0):
         """quant_bits > 0: quant-uniform compressor (KIVI int4/int2);
         drop_ratio in (0, 1): drop-topk compressor keeping llround(c*T) tokens per
         (layer, head) -- the two are exclusive (compressor.cpp:245-254).
         tp_size > 1: this engine is rank tp_rank of a head-sharded tensor-parallel
-        group (`model` is the full model; attach_nccl / attach_loopback before stepping)."""
+        group (`model` is the full model; attach_nccl / attach_loopback before stepping).
+        drop_window > 0 (drop-topk only): online mode -- tokens accepted after
+        compress stay in a sliding window of the latest drop_window..2*drop_window."""
         self.lib = _lib.load()
         self.model = model
         self.max_x = max_x
         md = _lib.ModelDesc(model.vocab, model.hidden, model.layers, model.n_q, model.n_kv,
                             model.d_head, model.ffn, model.rope_theta, model.rms_eps)
         rt = _lib.RuntimeDesc(max_slots, max_ctx, max_x, quant_bits, full_tier, n_stage,
-                              max_verify, int(use_graphs), float(drop_ratio), int(tp_size), int(tp_rank))
+                              max_verify, int(use_graphs), float(drop_ratio), int(tp_size), int(tp_rank),
+                              int(drop_window))
         self.tp_size, self.tp_rank = int(tp_size), int(tp_rank)
         h = C.c_void_p()
         check(self.lib.vc_engine_create(C.byref(md), C.byref(rt), device, C.byref(h)))

@@ -135,3 +135,36 @@ def test_drop_scheduled_lossless(cuda, weights, tier):
     np.testing.assert_array_equal(out, base)
     assert st["verifies"] > 0
     e.close()
+
+
+@pytest.mark.gpu
+def test_drop_online_window_lossless_and_bounded(cuda, weights):
+    """Online mode (speckv::update, compressor.cpp:208-243): tokens accepted
+    after compress live in a sliding window; the tier stays bounded, holds the
+    exact K/V of the latest tokens, and decoding stays lossless."""
+    W, K = 32, 200
+    e = Engine(TINY, max_slots=2, max_ctx=N_CTX + K + 64, max_x=8, quant_bits=0, drop_ratio=RATIO,
+               drop_window=W)
+    e.load_weights(weights)
+    for s in range(2):
+        e.add_synthetic(s, N_CTX, 17, seed=3)
+    base, _ = e.autoregress([0], K)
+    e.compress(1)
+    spec, _, _ = e.run_speculative([1], K, 6)
+    np.testing.assert_array_equal(spec, base)
+    st = e.state(1)
+    k = int(math.floor(RATIO * N_CTX + 0.5))
+    assert st["drop_base"] == k
+    n_win = st["drop_len"] - st["drop_base"]
+    assert W <= n_win < 2 * W + 8  # bounded although ~K tokens were appended
+    for layer in range(TINY.layers):
+        for head in range(TINY.n_kv):
+            kd, vd = e.kv_read(3, 1, layer, head, k, n_win)
+            kf, vf = e.kv_read(0, 1, layer, head, st["committed"] - n_win, n_win)
+            assert np.array_equal(kd, kf) and np.array_equal(vd, vf)
+    e.close()
+
+
+def test_drop_window_needs_drop_compressor():
+    with pytest.raises(_lib.ConfigError):
+        Engine(TINY, max_ctx=256, quant_bits=4, drop_window=16)
