@@ -214,7 +214,7 @@ int vc_swap_poll(vc_engine* e, uint64_t transfer_id, int* done);
 
 /* ---- decode loops ----------------------------------------------------------- */
 /* Full-KV greedy decode of K tokens for each slot (the baseline).
- * out [n][K]; *ms = device time of the loop.                               */
+ * out [n][K]; *ms = device time of the loop (one CUDA event pair around it). */
 int vc_run_decode(vc_engine* e, const int* slots, int n, int K, int32_t* out, double* ms);
 /* Lossless speculative loop (lock-step rounds of x drafts + one verify per
  * slot).  out [n][K]; accepted-per-round written to rounds (cap max_rounds
@@ -258,7 +258,8 @@ typedef struct {
   int64_t timed_iterations; /* iterations inside the timed window */
   int64_t timed_tokens;     /* tokens emitted inside the timed window */
   double timed_wall_ms;     /* host wall time of the timed window (e2e) */
-  double timed_device_ms;   /* device time of the window's steps */
+  double timed_device_ms;   /* device time of the window: one CUDA event pair on the
+                               compute stream around all its steps (gaps included) */
   double timed_rows;        /* activation rows executed in the window */
 } vc_sched_stats;
 

@@ -520,7 +520,11 @@ int vc_run_decode(vc_engine* e, const int* slots, int n, int K, int32_t* out, do
     vc::Engine& en = E(e);
     std::vector<vc::StepItem> its(n);
     std::vector<int32_t> row;
-    const auto t0 = std::chrono::steady_clock::now();
+    // *ms: device time of the loop -- one event pair on the compute stream
+    cudaEvent_t w0, w1;
+    vc::check_cuda(cudaEventCreate(&w0), "event");
+    vc::check_cuda(cudaEventCreate(&w1), "event");
+    vc::check_cuda(cudaEventRecord(w0, en.stream()), "event");
     for (int k = 0; k < K; ++k) {
       for (int i = 0; i < n; ++i) {
         its[i].slot = slots[i];
@@ -533,8 +537,13 @@ int vc_run_decode(vc_engine* e, const int* slots, int n, int K, int32_t* out, do
         out[static_cast<size_t>(i) * K + k] = row[i];
       }
     }
-    const auto t1 = std::chrono::steady_clock::now();
-    if (ms) *ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+    vc::check_cuda(cudaEventRecord(w1, en.stream()), "event");
+    vc::check_cuda(cudaEventSynchronize(w1), "event");
+    float dms = 0.f;
+    vc::check_cuda(cudaEventElapsedTime(&dms, w0, w1), "event");
+    cudaEventDestroy(w0);
+    cudaEventDestroy(w1);
+    if (ms) *ms = dms;
   });
 }
 
@@ -569,7 +578,10 @@ void speculative_loop(vc::Engine& en, const int* slots, int n, int K, int x, int
   std::vector<int> produced(n, 0), nr(n, 0), ngr(n, 0);
   std::vector<vc::StepItem> its;
   std::vector<int32_t> row;
-  const auto t0 = std::chrono::steady_clock::now();
+  cudaEvent_t w0, w1;  // *ms: device time of the loop (one event pair on the compute stream)
+  vc::check_cuda(cudaEventCreate(&w0), "event");
+  vc::check_cuda(cudaEventCreate(&w1), "event");
+  vc::check_cuda(cudaEventRecord(w0, en.stream()), "event");
   for (;;) {
     std::vector<int> act, model;
     for (int i = 0; i < n; ++i)
@@ -617,8 +629,13 @@ void speculative_loop(vc::Engine& en, const int* slots, int n, int K, int x, int
         if (produced[i] < K) out[static_cast<size_t>(i) * K + produced[i]++] = t;  // truncate at K
     }
   }
-  const auto t1 = std::chrono::steady_clock::now();
-  if (ms) *ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+  vc::check_cuda(cudaEventRecord(w1, en.stream()), "event");
+  vc::check_cuda(cudaEventSynchronize(w1), "event");
+  float dms = 0.f;
+  vc::check_cuda(cudaEventElapsedTime(&dms, w0, w1), "event");
+  cudaEventDestroy(w0);
+  cudaEventDestroy(w1);
+  if (ms) *ms = dms;
   for (int i = 0; i < n; ++i) {
     if (n_rounds) n_rounds[i] = nr[i];
     if (ngram_rounds) ngram_rounds[i] = ngr[i];
