@@ -51,23 +51,25 @@ __global__ void combine_kernel(AttnShape s, const AttnSeq* seqs, int max_chunks,
   // draft mode: the tail-chunk partials are merged after the quantised chunks, in order
   const int n_tail = mode == 0 ? (sq.tail_len + VC_TAIL_CHUNK - 1) / VC_TAIL_CHUNK : 0;
   const int n_all = n_parts + n_tail;
-  __shared__ float s_m[kMaxParts], s_f[kMaxParts];
+  __shared__ float s_m[kMaxParts], s_f[kMaxParts], s_lp[kMaxParts];
   __shared__ size_t s_row[kMaxParts];
   __shared__ float s_M, s_l;
-  for (int c = threadIdx.x; c < n_all; c += blockDim.x) {
+  for (int c = threadIdx.x; c < n_all; c += blockDim.x) {  // every (m, l) load in parallel
     const size_t pr = prow_of(c < n_parts ? c : max_chunks + (c - n_parts));
     s_row[c] = pr;
-    s_m[c] = part.ml[pr * 2];
+    const float2 ml = *reinterpret_cast<const float2*>(part.ml + pr * 2);
+    s_m[c] = ml.x;
+    s_lp[c] = ml.y;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (threadIdx.x == 0) {  // shared memory only: no global-latency chain
     float M = -INFINITY;
     for (int c = 0; c < n_all; ++c) M = fmaxf(M, s_m[c]);
     float l = 0.f;
     for (int c = 0; c < n_all; ++c) {  // fixed order
       const float f = (s_m[c] == -INFINITY) ? 0.f : exp2f(s_m[c] - M);
       s_f[c] = f;
-      l += f * part.ml[s_row[c] * 2 + 1];
+      l += f * s_lp[c];
     }
     s_M = M;
     s_l = l;
