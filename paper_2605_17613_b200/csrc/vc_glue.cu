@@ -71,9 +71,21 @@ __global__ void argmax_kernel(const float* logits, int N, int32_t* out) {
   const float* row = logits + static_cast<size_t>(blockIdx.x) * N;
   float best = -INFINITY;
   int bi = 0x7fffffff;
-  for (int i = threadIdx.x; i < N; i += blockDim.x) {
-    const float v = row[i];
-    if (v > best) { best = v; bi = i; }  // ascending i per thread: first max kept
+  if ((N & 3) == 0) {  // float4 loads: 4x fewer instructions, more bytes in flight
+    const float4* r4 = reinterpret_cast<const float4*>(row);
+#pragma unroll 4
+    for (int j = threadIdx.x; j < N / 4; j += blockDim.x) {
+      const float4 v = r4[j];  // ascending indices per thread: the first max is kept
+      if (v.x > best) { best = v.x; bi = 4 * j; }
+      if (v.y > best) { best = v.y; bi = 4 * j + 1; }
+      if (v.z > best) { best = v.z; bi = 4 * j + 2; }
+      if (v.w > best) { best = v.w; bi = 4 * j + 3; }
+    }
+  } else {
+    for (int i = threadIdx.x; i < N; i += blockDim.x) {
+      const float v = row[i];
+      if (v > best) { best = v; bi = i; }  // ascending i per thread: first max kept
+    }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {  // ties -> smaller index (specloop.cpp:260)
