@@ -339,9 +339,20 @@ def main():
              "tok": tok_all, "dev_s": dev_s, "wall_s": wall_s}
         return r
 
-    runs = {head_tier: vericache(head_tier)}
-    if not args.no_secondary and not args.small:
-        runs[1 - head_tier] = vericache(1 - head_tier)
+    note = None
+    try:
+        runs = {head_tier: vericache(head_tier)}
+    except vc.VcError as ex:  # e.g. the pinned host pool cannot be allocated on this box
+        if head_tier != 1:
+            raise
+        note = f"host tier unavailable ({ex}); headline falls back to the HBM tier"
+        head_tier = 0
+        runs = {0: vericache(0)}
+    if not args.no_secondary and not args.small and note is None:
+        try:
+            runs[1 - head_tier] = vericache(1 - head_tier)
+        except vc.VcError as ex:
+            note = f"secondary tier skipped: {ex}"
     h = runs[head_tier]
     st, x = h["st"], h["x"]
     tok_all, dev_s, wall_s = h["tok"], h["dev_s"], h["wall_s"]
@@ -419,6 +430,8 @@ def main():
             "clocks": h["clocks"],
             "cpu_baseline": cpu,
         }
+        if note:
+            line["note"] = note
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
