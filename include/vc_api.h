@@ -266,6 +266,51 @@ typedef struct {
 int vc_run_scheduled(vc_engine* e, const int* slots, int n, const vc_sched_desc* sd,
                      int32_t* out, vc_sched_stats* stats);
 
+/* ---- remote prefix caching (BASELINE.json configs[3]) ---------------------
+ * The reference simulates this pipeline (remote_prefix, sim.cpp:510-665;
+ * closed form t_req_remote, analytics.cpp:25-35).  Here the storage node is
+ * pinned host memory holding one shared prefix in both forms:
+ *   vc_prefix_store(e, slot)  snapshot slot's committed (compressed) prefix;
+ *   vc_prefix_load(e, slot, what, first_token, &id)  stream one form into a
+ *     request slot on the copy stream: what 0 = the compressed payload
+ *     (drafting can start), 1 = the full KV (verification can start);
+ *     completion via vc_swap_poll.
+ * vc_run_remote_prefix runs a workload of n requests over that prefix:
+ * arrivals, the payload loads (compressed ahead of full on the link), drafting
+ * on the compressed KV while the full KV streams, verify once both are
+ * resident (the full KV stays cached, verify_cached), accept/rollback.  With
+ * baseline = 1 it is the reference's force_baseline arm: load the full KV,
+ * then decode. */
+typedef struct {
+  int x;                        /* draft horizon */
+  int K;                        /* output tokens per request */
+  int baseline;                 /* 1: full-KV baseline (load full KV, then decode) */
+  int link_queue;               /* transfers kept queued on the copy stream (>= 1) */
+  double arrival_gap_ms;        /* request i arrives i * gap after the start (0 = burst) */
+  const int32_t* first_tokens;  /* [n] each request's first input token (its own prompt suffix) */
+} vc_remote_desc;
+
+typedef struct {
+  double makespan_ms;       /* device time, start -> last token (event pair on the compute stream) */
+  double wall_ms;           /* host wall time of the loop */
+  int64_t tokens;           /* emitted tokens (all requests, truncated at K) */
+  int64_t iterations;       /* forward steps */
+  int64_t link_waits;       /* times the loop blocked on the link with nothing to compute */
+  int64_t verifies;
+  double mean_accept;       /* accepted drafted tokens per verify */
+  double ttft_ms_mean;      /* arrival -> first emitted token (host clock) */
+  double ttft_ms_max;
+  double compressed_ready_ms_mean; /* arrival -> compressed payload resident */
+  double full_ready_ms_mean;       /* arrival -> full KV resident */
+  double h2d_bytes;         /* bytes of all payload loads */
+  double h2d_ms;            /* copy-engine busy time of those loads */
+} vc_remote_stats;
+
+int vc_prefix_store(vc_engine* e, int slot);
+int vc_prefix_load(vc_engine* e, int slot, int what, int32_t first_token, uint64_t* transfer_id);
+int vc_run_remote_prefix(vc_engine* e, const int* slots, int n, const vc_remote_desc* rd, int32_t* out,
+                         vc_remote_stats* stats);
+
 /* ---- scheduler ------------------------------------------------------------ */
 int vc_reload_span(int64_t bytes, double bandwidth, double iteration_time, double* iterations,
                    int* windows);

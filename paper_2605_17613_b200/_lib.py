@@ -77,6 +77,19 @@ class SchedStats(C.Structure):
                 ("timed_rows", C.c_double)]
 
 
+class RemoteDesc(C.Structure):
+    _fields_ = [("x", C.c_int), ("K", C.c_int), ("baseline", C.c_int), ("link_queue", C.c_int),
+                ("arrival_gap_ms", C.c_double), ("first_tokens", C.POINTER(C.c_int32))]
+
+
+class RemoteStats(C.Structure):
+    _fields_ = [("makespan_ms", C.c_double), ("wall_ms", C.c_double), ("tokens", C.c_int64),
+                ("iterations", C.c_int64), ("link_waits", C.c_int64), ("verifies", C.c_int64),
+                ("mean_accept", C.c_double), ("ttft_ms_mean", C.c_double), ("ttft_ms_max", C.c_double),
+                ("compressed_ready_ms_mean", C.c_double), ("full_ready_ms_mean", C.c_double),
+                ("h2d_bytes", C.c_double), ("h2d_ms", C.c_double)]
+
+
 P = C.c_void_p
 I, I64, U64, D, F = C.c_int, C.c_int64, C.c_uint64, C.c_double, C.c_float
 PI, PI32, PI64, PU64, PD = (C.POINTER(C.c_int), C.POINTER(C.c_int32), C.POINTER(C.c_int64),
@@ -127,6 +140,9 @@ SIGNATURES = {
     "vc_run_speculative": (I, [P, PI, I, I, I, PI32, PI32, I, PI, PD]),
     "vc_run_speculative_ngram": (I, [P, PI, I, I, I, I, PI32, PI32, I, PI, PI, PD]),
     "vc_run_scheduled": (I, [P, PI, I, C.POINTER(SchedDesc), PI32, C.POINTER(SchedStats)]),
+    "vc_prefix_store": (I, [P, I]),
+    "vc_prefix_load": (I, [P, I, I, C.c_int32, PU64]),
+    "vc_run_remote_prefix": (I, [P, PI, I, C.POINTER(RemoteDesc), PI32, C.POINTER(RemoteStats)]),
     "vc_reload_span": (I, [I64, D, D, PD, PI]),
     "vc_quant_kivi_slice": (I, [P, P, I, I, I, P, P, P, P, P]),
     "vc_attention_probe": (I, [P, I, I, I, P, I, I, PU16]),

@@ -20,6 +20,8 @@ struct vc_engine {
 
 int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sched_desc& sd,
                           int32_t* out, vc_sched_stats* stats);
+int vc_run_remote_prefix_impl(vc::Engine& en, const int* slots, int n, const vc_remote_desc& rd,
+                              int32_t* out, vc_remote_stats* stats);
 
 namespace {
 
@@ -512,6 +514,28 @@ int vc_swap_begin(vc_engine* e, int slot, int stage, uint64_t* transfer_id) {
 
 int vc_swap_poll(vc_engine* e, uint64_t transfer_id, int* done) {
   return guard([&] { *done = E(e).swap_done(transfer_id) ? 1 : 0; });
+}
+
+// ---------------------------------------------------------- remote prefix
+int vc_prefix_store(vc_engine* e, int slot) {
+  return guard([&] {
+    const auto& c = E(e).config();
+    if (c.full_tier != 0) throw speckv::ConfigError("remote prefix: needs the HBM full tier (full_tier 0)");
+    if (c.quant_bits == 0) throw speckv::ConfigError("remote prefix: needs the quantising compressor");
+    E(e).prefix_store(slot);
+  });
+}
+
+int vc_prefix_load(vc_engine* e, int slot, int what, int32_t first_token, uint64_t* transfer_id) {
+  return guard([&] { *transfer_id = E(e).prefix_load(slot, what, first_token); });
+}
+
+int vc_run_remote_prefix(vc_engine* e, const int* slots, int n, const vc_remote_desc* rd, int32_t* out,
+                         vc_remote_stats* stats) {
+  return guard([&] {
+    if (!rd) throw vc::ContractViolation("vc_run_remote_prefix: null descriptor");
+    vc_run_remote_prefix_impl(E(e), slots, n, *rd, out, stats);
+  });
 }
 
 // ------------------------------------------------------------------ loops

@@ -187,7 +187,6 @@ __global__ void __launch_bounds__(kWarps * 32, NREP == 8 ? 3 : VC_DRAFT_MINB) dr
   static_assert(NREP <= 8, "n_rep > 8 needs two head tiles");
   using GEO = Geo<D, BITS>;
   constexpr int KS = GEO::KS, W = GEO::W, CH = GEO::CH, UMT = GEO::UMT;
-  constexpr uint32_t MASK = BITS == 4 ? 0x000f000fu : 0x00030003u;
   constexpr int kUPG = kG / kUnit;
 
   extern __shared__ __align__(128) uint32_t dsm[];   // [kWarps][2][STAGE]
@@ -310,12 +309,18 @@ __global__ void __launch_bounds__(kWarps * 32, NREP == 8 ? 3 : VC_DRAFT_MINB) dr
       a[2] = nib_to_h2(wd, 0x00f000f0u);
       a[3] = nib_to_h2(w8, 0x00f000f0u);
     } else {
-      const int sh = 8 * sub;
-#pragma unroll
-      for (int j = 0; j < 4; ++j) a[j] = nib_to_h2(wd >> (sh + j * BITS), MASK);
+      // int2: code j of a byte sits at bits 2j; pairs 0/1 read bits 0-1 of the
+      // byte and of the byte >> 2, pairs 2/3 bits 4-5 of the same two words
+      // (1024 + 16c, scaled back by the B operand like int4): 3 shifts + 8
+      // lop3 per word of 16 codes instead of a shift per pair
+      const uint32_t lo = sub ? wd >> 8 : wd, lo2 = lo >> 2;
+      a[0] = nib_to_h2(lo, 0x00030003u);
+      a[1] = nib_to_h2(lo2, 0x00030003u);
+      a[2] = nib_to_h2(lo, 0x00300030u);
+      a[3] = nib_to_h2(lo2, 0x00300030u);
     }
   };
-  constexpr float kHiScale = BITS == 4 ? 0.0625f : 1.0f;  // B-operand scale of pairs 2/3
+  constexpr float kHiScale = 0.0625f;  // B-operand scale of pairs 2/3 (their A holds 1024 + 16c)
   if (lane == 0) {
     for (int i = 0; i < kStages; ++i) mbar_init(bar + i, 1);
     fence_mbar_init();

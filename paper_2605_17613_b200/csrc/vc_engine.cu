@@ -115,6 +115,7 @@ Engine::~Engine() {
     if (p) cudaFree(p);
   if (host_k_) cudaFreeHost(host_k_);
   if (host_v_) cudaFreeHost(host_v_);
+  prefix_drop();
   if (h_desc_) cudaFreeHost(h_desc_);
   if (h_out_) cudaFreeHost(h_out_);
   cudaEventDestroy(ev_a_);
@@ -1015,6 +1016,140 @@ std::vector<int32_t> Engine::accept_commit(int slot, const std::vector<int32_t>&
   s.draft_len = 0;
   s.history.insert(s.history.end(), emitted.begin(), emitted.end());
   return emitted;
+}
+
+// ------------------------------------------------------------ remote prefix
+// Remote prefix caching (BASELINE.json configs[3]; the reference's simulated
+// remote_prefix, /root/reference/proj/src/sim.cpp:510-665).  The storage node
+// holds a precomputed prefix in both forms -- `compress` produced the payload
+// at storage -- and the engine streams them into request
+// slots: the compressed payload first (drafting can start, kCompressedLoaded
+// at sim.cpp:588-610), the full KV behind it (the verify prefetch,
+// start_cycle at sim.cpp:562-575).  The full KV stays resident after it
+// lands (verify_cached).
+void Engine::prefix_drop() {
+  for (void* p : {static_cast<void*>(pre_k_), static_cast<void*>(pre_v_), static_cast<void*>(pre_kt_),
+                  static_cast<void*>(pre_vt_), static_cast<void*>(pre_rec_)})
+    if (p) cudaFreeHost(p);
+  pre_k_ = pre_v_ = pre_kt_ = pre_vt_ = nullptr;
+  pre_rec_ = nullptr;
+  pre_T_ = pre_ng_ = pre_tc_ = 0;
+}
+
+double Engine::prefix_bytes(int what) const {
+  const auto& m = cfg_.model;
+  const double n_slices = static_cast<double>(m.layers) * m.n_kv;
+  if (what == 1) return 2.0 * n_slices * pre_T_ * m.d * 2;
+  return n_slices * (static_cast<double>(pre_ng_) * quant_record_words(m.d, cfg_.quant_bits) * 4 +
+                     2.0 * pre_tc_ * m.d * 2);
+}
+
+void Engine::prefix_store(int src_slot) {
+  if (cfg_.full_tier != 0) throw ContractViolation("remote prefix: needs the HBM full tier (full_tier 0)");
+  if (cfg_.quant_bits == 0) throw ContractViolation("remote prefix: needs the quantised compressed tier");
+  const SeqState& s = seqs_.at(src_slot);
+  if (!s.live || s.committed < 1) throw ContractViolation("prefix_store: slot holds no prefix");
+  if (s.n_groups * VC_QGROUP + s.tail_committed != s.committed || s.draft_len != 0)
+    throw ContractViolation("prefix_store: compress the prefix first (no open draft round)");
+  prefix_drop();
+  const auto& m = cfg_.model;
+  const int n_slices = m.layers * m.n_kv;
+  pre_T_ = s.committed;
+  pre_ng_ = s.n_groups;
+  pre_tc_ = s.tail_committed;
+  const size_t full_w = static_cast<size_t>(pre_T_) * m.d * 2;
+  const size_t words = quant_record_words(m.d, cfg_.quant_bits);
+  const size_t rec_w = static_cast<size_t>(pre_ng_) * words * 4;
+  const size_t tail_w = static_cast<size_t>(pre_tc_) * m.d * 2;
+  auto halloc = [&](size_t bytes) {
+    void* p = nullptr;
+    VC_CK(cudaHostAlloc(&p, std::max<size_t>(bytes, 256), cudaHostAllocDefault));
+    return p;
+  };
+  pre_k_ = static_cast<uint16_t*>(halloc(full_w * n_slices));
+  pre_v_ = static_cast<uint16_t*>(halloc(full_w * n_slices));
+  pre_rec_ = static_cast<uint32_t*>(halloc(rec_w * n_slices));
+  pre_kt_ = static_cast<uint16_t*>(halloc(tail_w * n_slices));
+  pre_vt_ = static_cast<uint16_t*>(halloc(tail_w * n_slices));
+  const size_t slice_elems = static_cast<size_t>(full_.cap) * m.d;
+  const size_t base = static_cast<size_t>(src_slot) * n_slices;
+  VC_CK(cudaMemcpy2DAsync(pre_k_, full_w, full_.k + base * slice_elems, slice_elems * 2, full_w, n_slices,
+                          cudaMemcpyDeviceToHost, st_));
+  VC_CK(cudaMemcpy2DAsync(pre_v_, full_w, full_.v + base * slice_elems, slice_elems * 2, full_w, n_slices,
+                          cudaMemcpyDeviceToHost, st_));
+  const size_t slice_words = static_cast<size_t>(quant_.cap / VC_QGROUP) * words;
+  if (rec_w)
+    VC_CK(cudaMemcpy2DAsync(pre_rec_, rec_w, quant_.rec + base * slice_words, slice_words * 4, rec_w, n_slices,
+                            cudaMemcpyDeviceToHost, st_));
+  const size_t tpitch = static_cast<size_t>(tail_cap_) * m.d * 2;
+  if (tail_w) {
+    VC_CK(cudaMemcpy2DAsync(pre_kt_, tail_w, quant_.ktail + base * tail_cap_ * m.d, tpitch, tail_w, n_slices,
+                            cudaMemcpyDeviceToHost, st_));
+    VC_CK(cudaMemcpy2DAsync(pre_vt_, tail_w, quant_.vtail + base * tail_cap_ * m.d, tpitch, tail_w, n_slices,
+                            cudaMemcpyDeviceToHost, st_));
+  }
+  VC_CK(cudaStreamSynchronize(st_));
+}
+
+uint64_t Engine::prefix_load(int slot, int what, int32_t pending) {
+  if (pre_T_ == 0) throw ContractViolation("prefix_load: no prefix stored");
+  if (slot < 0 || slot >= cfg_.max_slots) throw ContractViolation("slot out of range");
+  if (what != 0 && what != 1) throw ContractViolation("prefix_load: what is 0 (compressed) or 1 (full)");
+  if (pre_T_ + cfg_.max_x + 2 > full_.cap) throw ContractViolation("prefix exceeds the slot capacity");
+  const auto& m = cfg_.model;
+  const int n_slices = m.layers * m.n_kv;
+  const size_t base = static_cast<size_t>(slot) * n_slices;
+  // the slot may still be read by an in-flight step on the compute stream
+  cudaEvent_t ready;
+  VC_CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));
+  VC_CK(cudaEventRecord(ready, st_));
+  VC_CK(cudaStreamWaitEvent(copy_st_, ready, 0));
+  cudaEventDestroy(ready);
+  Xfer x{};
+  x.bytes = prefix_bytes(what);
+  VC_CK(cudaEventCreate(&x.start));
+  VC_CK(cudaEventCreate(&x.done));
+  VC_CK(cudaEventRecord(x.start, copy_st_));
+  if (what == 1) {
+    const size_t slice_elems = static_cast<size_t>(full_.cap) * m.d;
+    const size_t w = static_cast<size_t>(pre_T_) * m.d * 2;
+    VC_CK(cudaMemcpy2DAsync(full_.k + base * slice_elems, slice_elems * 2, pre_k_, w, w, n_slices,
+                            cudaMemcpyHostToDevice, copy_st_));
+    VC_CK(cudaMemcpy2DAsync(full_.v + base * slice_elems, slice_elems * 2, pre_v_, w, w, n_slices,
+                            cudaMemcpyHostToDevice, copy_st_));
+  } else {
+    const size_t words = quant_record_words(m.d, cfg_.quant_bits);
+    const size_t slice_words = static_cast<size_t>(quant_.cap / VC_QGROUP) * words;
+    const size_t rec_w = static_cast<size_t>(pre_ng_) * words * 4;
+    if (rec_w)
+      VC_CK(cudaMemcpy2DAsync(quant_.rec + base * slice_words, slice_words * 4, pre_rec_, rec_w, rec_w, n_slices,
+                              cudaMemcpyHostToDevice, copy_st_));
+    const size_t tail_w = static_cast<size_t>(pre_tc_) * m.d * 2;
+    const size_t tpitch = static_cast<size_t>(tail_cap_) * m.d * 2;
+    if (tail_w) {
+      VC_CK(cudaMemcpy2DAsync(quant_.ktail + base * tail_cap_ * m.d, tpitch, pre_kt_, tail_w, tail_w, n_slices,
+                              cudaMemcpyHostToDevice, copy_st_));
+      VC_CK(cudaMemcpy2DAsync(quant_.vtail + base * tail_cap_ * m.d, tpitch, pre_vt_, tail_w, tail_w, n_slices,
+                              cudaMemcpyHostToDevice, copy_st_));
+    }
+  }
+  VC_CK(cudaEventRecord(x.done, copy_st_));
+  const uint64_t id = next_xfer_++;
+  xfers_[id] = x;
+  // request state: the first load of a slot opens it; the compressed form
+  // carries the quant-tier geometry
+  SeqState& s = seqs_[slot];
+  if (!s.live) {
+    s = SeqState{};
+    s.live = true;
+    s.committed = pre_T_;
+    s.pending = pending;
+  }
+  if (what == 0) {
+    s.n_groups = pre_ng_;
+    s.tail_committed = pre_tc_;
+  }
+  return id;
 }
 
 // ------------------------------------------------------------- host tier

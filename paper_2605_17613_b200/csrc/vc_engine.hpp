@@ -132,6 +132,18 @@ class Engine {
   uint64_t swap_begin(int slot, int stage);
   bool swap_done(uint64_t id);
   void swap_wait(uint64_t id);
+  // ---- remote prefix (configs[3]) -------------------------------------
+  // The storage node's precomputed KV of one shared prefix: slot's committed
+  // full KV and its compressed image (quant tier) snapshotted into pinned
+  // host memory.  prefix_load() streams one form into a request slot on the
+  // copy stream (what 0 = compressed payload -> drafting can start; 1 = full
+  // KV -> verification can start) and returns a transfer id (swap_done).
+  void prefix_store(int src_slot);
+  void prefix_drop();
+  int prefix_tokens() const { return pre_T_; }
+  double prefix_bytes(int what) const;
+  uint64_t prefix_load(int slot, int what, int32_t pending);
+
   // copy-engine time of the completed H2D reloads (CUDA events on the copy stream)
   double h2d_ms() const { return h2d_ms_; }
   double h2d_bytes() const { return h2d_bytes_; }  // bytes of the completed reloads
@@ -204,6 +216,10 @@ class Engine {
   int32_t* kept_buf_ = nullptr; // [layers*n_kv][k] kept positions of the last compress
   int last_kept_k_ = 0;
   uint16_t *host_k_ = nullptr, *host_v_ = nullptr;
+  // prefix store (pinned): full K/V [slice][T][d], records [slice][ng][words], tails [slice][tc][d]
+  uint16_t *pre_k_ = nullptr, *pre_v_ = nullptr, *pre_kt_ = nullptr, *pre_vt_ = nullptr;
+  uint32_t* pre_rec_ = nullptr;
+  int pre_T_ = 0, pre_ng_ = 0, pre_tc_ = 0;
   int max_chunks_q_ = 0, max_chunks_d_ = 0, tail_cap_ = 0, Mmax_ = 0;
   int draft_warps_ = 0, draft_min_tasks_ = 4;  // quantised draft-attention work split
   // activations

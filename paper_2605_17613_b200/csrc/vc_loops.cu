@@ -21,6 +21,7 @@
 #include <deque>
 #include <map>
 #include <set>
+#include <thread>
 
 #include "speckv_b200.hpp"
 #include "vc_api.h"
@@ -322,6 +323,213 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
   cudaEventDestroy(win0);
   cudaEventDestroy(win1);
   st.mean_accept = st.verifies ? accepted_sum / static_cast<double>(st.verifies) : 0.0;
+  if (stats) *stats = st;
+  return VC_OK;
+}
+
+// ---------------------------------------------------------------------------
+// vc_run_remote_prefix: the remote-prefix pipeline on real copies and kernels.
+//
+// The reference's remote_prefix (/root/reference/proj/src/sim.cpp:510-665)
+// runs, per request: arrival -> compressed payload over the link
+// (kCompressedLoaded, :588-610) -> a cycle of x drafts on the compressed KV
+// while the full KV is prefetched (start_cycle, :562-575) -> verify when both
+// are done (:611-619) -> accept (:622-636) -> next cycle; with verify_cached
+// the full KV stays resident after its first load.  force_baseline (:605-608)
+// loads the full KV and decodes.  Here both "links" are the GPU's copy engine
+// (the storage node is pinned host memory on this box), so the two payloads
+// share one FIFO: compressed loads are issued ahead of full loads, at most
+// link_queue transfers queued.  One forward pass per iteration runs every
+// drafting row, up to max_verify verify windows (oldest ready first) and, in
+// the baseline, every decode row.
+int vc_run_remote_prefix_impl(vc::Engine& en, const int* slots, int n, const vc_remote_desc& rd,
+                              int32_t* out, vc_remote_stats* stats) {
+  const auto& cfgE = en.config();
+  const bool base = rd.baseline != 0;
+  if (n < 1 || n > cfgE.max_slots) throw speckv::ConfigError("remote prefix: n out of [1, max_slots]");
+  if (rd.K < 1) throw speckv::ConfigError("remote prefix: K must be >= 1");
+  if (!base && (rd.x < 1 || rd.x > cfgE.max_x)) throw speckv::ConfigError("remote prefix: x out of [1, max_x]");
+  if (rd.link_queue < 1) throw speckv::ConfigError("remote prefix: link_queue must be >= 1");
+  if (rd.arrival_gap_ms < 0) throw speckv::ConfigError("remote prefix: arrival gap must be >= 0");
+  if (en.prefix_tokens() < 1) throw vc::ContractViolation("remote prefix: no prefix stored (vc_prefix_store)");
+  if (!rd.first_tokens) throw vc::ContractViolation("remote prefix: null first_tokens");
+  if (en.prefix_tokens() + rd.K + cfgE.max_x > cfgE.max_ctx)
+    throw speckv::ConfigError("remote prefix: prefix + K + max_x exceeds max_ctx");
+
+  struct Req {
+    bool arrived = false, active = false, full = false, done = false;
+    bool comp_issued = false, full_issued = false;
+    uint64_t comp_id = 0, full_id = 0;
+    double t_arr = 0, t_comp = -1, t_full = -1, t_first = -1;
+    int produced = 0;
+    int64_t ready_seq = -1;  // order in which the request became verifiable
+  };
+  std::vector<Req> rq(n);
+  for (int i = 0; i < n; ++i) en.release(slots[i]);
+  const double h2d_ms0 = en.h2d_ms(), h2d_b0 = en.h2d_bytes();
+  cudaEvent_t win0 = nullptr, win1 = nullptr;
+  vc::check_cuda(cudaEventCreate(&win0), "window event");
+  vc::check_cuda(cudaEventCreate(&win1), "window event");
+  vc::check_cuda(cudaEventRecord(win0, en.stream()), "window event");
+  const auto t0 = std::chrono::steady_clock::now();
+  auto now_ms = [&] { return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count(); };
+
+  vc_remote_stats st{};
+  double accepted_sum = 0;
+  int64_t ready_counter = 0;
+  std::vector<int32_t> row;
+  const int64_t guard_iters = 100000 + 8LL * n * rd.K;
+  for (int64_t it = 0;; ++it) {
+    if (it > guard_iters) throw speckv::ConfigError("remote prefix loop stalled");
+    const double t = now_ms();
+    // arrivals (nominal times)
+    for (int i = 0; i < n; ++i)
+      if (!rq[i].arrived && t >= i * rd.arrival_gap_ms) {
+        rq[i].arrived = true;
+        rq[i].t_arr = i * rd.arrival_gap_ms;
+      }
+    // completions
+    int inflight = 0;
+    for (int i = 0; i < n; ++i) {
+      Req& r = rq[i];
+      if (r.comp_issued && !r.active) {
+        if (en.swap_done(r.comp_id)) { r.active = true; r.t_comp = now_ms(); } else ++inflight;
+      }
+      if (r.full_issued && !r.full) {
+        if (en.swap_done(r.full_id)) { r.full = true; r.t_full = now_ms(); } else ++inflight;
+      }
+    }
+    // feed the link: compressed payloads ahead of full KV, arrival order
+    while (inflight < rd.link_queue) {
+      int pick = -1, what = -1;
+      if (!base)
+        for (int i = 0; i < n && pick < 0; ++i)
+          if (rq[i].arrived && !rq[i].comp_issued) { pick = i; what = 0; }
+      for (int i = 0; i < n && pick < 0; ++i)
+        if (rq[i].arrived && !rq[i].full_issued) { pick = i; what = 1; }
+      if (pick < 0) break;
+      const uint64_t id = en.prefix_load(slots[pick], what, rd.first_tokens[pick]);
+      if (what == 0) { rq[pick].comp_issued = true; rq[pick].comp_id = id; }
+      else { rq[pick].full_issued = true; rq[pick].full_id = id; }
+      ++inflight;
+    }
+    // plan one forward pass
+    std::vector<vc::StepItem> items;
+    std::vector<int> drafting, verifying, decoding;
+    if (base) {
+      for (int i = 0; i < n; ++i)
+        if (rq[i].full && !rq[i].done) {
+          vc::StepItem s;
+          s.slot = slots[i];
+          s.mode = vc::RowMode::Decode;
+          s.tokens = {en.seq(slots[i]).pending};
+          items.push_back(std::move(s));
+          decoding.push_back(i);
+        }
+    } else {
+      std::vector<int> cand;
+      for (int i = 0; i < n; ++i) {
+        Req& r = rq[i];
+        if (!r.active || r.done) continue;
+        const int nd = static_cast<int>(en.seq(slots[i]).drafted.size());
+        if (nd == rd.x && r.full) {
+          if (r.ready_seq < 0) r.ready_seq = ready_counter++;
+          cand.push_back(i);
+        }
+      }
+      std::sort(cand.begin(), cand.end(), [&](int a, int b) { return rq[a].ready_seq < rq[b].ready_seq; });
+      if (static_cast<int>(cand.size()) > cfgE.max_verify) cand.resize(cfgE.max_verify);
+      verifying = cand;
+      for (int i = 0; i < n; ++i) {
+        Req& r = rq[i];
+        if (!r.active || r.done) continue;
+        const auto& s = en.seq(slots[i]);
+        if (static_cast<int>(s.drafted.size()) < rd.x) {
+          vc::StepItem d;
+          d.slot = slots[i];
+          d.mode = vc::RowMode::Draft;
+          d.tokens = {s.drafted.empty() ? s.pending : s.drafted.back()};
+          items.push_back(std::move(d));
+          drafting.push_back(i);
+        }
+      }
+      for (int i : verifying) {
+        const auto& s = en.seq(slots[i]);
+        vc::StepItem v;
+        v.slot = slots[i];
+        v.mode = vc::RowMode::Verify;
+        v.tokens.push_back(s.pending);
+        v.tokens.insert(v.tokens.end(), s.drafted.begin(), s.drafted.end());
+        items.push_back(std::move(v));
+      }
+    }
+    if (items.empty()) {
+      bool all_done = true;
+      for (const Req& r : rq) all_done = all_done && r.done;
+      if (all_done) break;
+      // nothing to compute: block on the oldest in-flight load, or the next arrival
+      uint64_t wait_id = 0;  // the earliest-issued (the link is FIFO)
+      auto consider = [&](uint64_t id) { if (!wait_id || id < wait_id) wait_id = id; };
+      for (const Req& r : rq) {
+        if (r.comp_issued && !r.active) consider(r.comp_id);
+        if (r.full_issued && !r.full) consider(r.full_id);
+      }
+      if (wait_id) {
+        en.swap_wait(wait_id);
+        ++st.link_waits;
+      } else {
+        std::this_thread::sleep_for(std::chrono::microseconds(100));
+      }
+      continue;
+    }
+    en.run_step(items, row);
+    st.iterations += 1;
+    const double t_out = now_ms();
+    auto emit = [&](int i, int32_t tok) {
+      Req& r = rq[i];
+      if (r.produced < rd.K) {
+        out[static_cast<size_t>(i) * rd.K + r.produced++] = tok;
+        st.tokens += 1;
+        if (r.t_first < 0) r.t_first = t_out;
+      }
+      if (r.produced >= rd.K) r.done = true;
+    };
+    size_t off = 0;
+    for (int i : decoding) {
+      const int32_t tok = row[off++];
+      en.commit_decode(slots[i], tok);
+      emit(i, tok);
+    }
+    for (int i : drafting) en.push_draft(slots[i], row[off++]);
+    for (int i : verifying) {
+      const int x_r = static_cast<int>(en.seq(slots[i]).drafted.size());
+      std::vector<int32_t> p(row.begin() + off, row.begin() + off + x_r + 1);
+      off += x_r + 1;
+      const auto em = en.accept_commit(slots[i], p);
+      accepted_sum += static_cast<double>(em.size()) - 1;
+      st.verifies += 1;
+      rq[i].ready_seq = -1;
+      for (int32_t tok : em) emit(i, tok);
+    }
+  }
+  vc::check_cuda(cudaEventRecord(win1, en.stream()), "window event");
+  vc::check_cuda(cudaEventSynchronize(win1), "window event");
+  float wms = 0.f;
+  vc::check_cuda(cudaEventElapsedTime(&wms, win0, win1), "window event");
+  cudaEventDestroy(win0);
+  cudaEventDestroy(win1);
+  st.makespan_ms = wms;
+  st.wall_ms = now_ms();
+  st.mean_accept = st.verifies ? accepted_sum / static_cast<double>(st.verifies) : 0.0;
+  for (const Req& r : rq) {
+    const double ttft = r.t_first - r.t_arr;
+    st.ttft_ms_mean += ttft / n;
+    st.ttft_ms_max = std::max(st.ttft_ms_max, ttft);
+    if (!base) st.compressed_ready_ms_mean += (r.t_comp - r.t_arr) / n;
+    st.full_ready_ms_mean += (r.t_full - r.t_arr) / n;
+  }
+  st.h2d_bytes = en.h2d_bytes() - h2d_b0;
+  st.h2d_ms = en.h2d_ms() - h2d_ms0;
   if (stats) *stats = st;
   return VC_OK;
 }

@@ -359,6 +359,34 @@ class Engine:
                                         _ptr(out, C.c_int32), C.byref(st)))
         return out, {f: getattr(st, f) for f, _ in st._fields_}
 
+    # ---- remote prefix (configs[3]) --------------------------------------------
+    def prefix_store(self, slot):
+        """Snapshot slot's compressed prefix (full KV + compressed payload) into
+        the pinned host store -- the storage node of remote_prefix (sim.cpp:510)."""
+        check(self.lib.vc_prefix_store(self.h, slot))
+
+    def prefix_load(self, slot, what, first_token) -> int:
+        """Stream the stored prefix into `slot` on the copy stream: what 0 = the
+        compressed payload, 1 = the full KV.  Returns a transfer id (swap_poll)."""
+        x = C.c_uint64()
+        check(self.lib.vc_prefix_load(self.h, slot, what, first_token, C.byref(x)))
+        return x.value
+
+    def run_remote_prefix(self, slots, K, x, first_tokens, baseline=False, link_queue=2,
+                          arrival_gap_ms=0.0):
+        """Requests over the stored prefix: (tokens [n][K], stats dict)."""
+        s = np.ascontiguousarray(slots, np.int32)
+        ft = np.ascontiguousarray(first_tokens, np.int32)
+        if ft.size != s.size:
+            raise ValueError("one first token per request")
+        out = np.zeros((s.size, K), np.int32)
+        rd = _lib.RemoteDesc(x, K, int(bool(baseline)), link_queue, arrival_gap_ms,
+                             _ptr(ft, C.c_int32))
+        st = _lib.RemoteStats()
+        check(self.lib.vc_run_remote_prefix(self.h, _ptr(s, C.c_int), s.size, C.byref(rd),
+                                            _ptr(out, C.c_int32), C.byref(st)))
+        return out, {f: getattr(st, f) for f, _ in st._fields_}
+
     # ---- probes -----------------------------------------------------------------
     def kv_read(self, pool, slot, layer, head, pos, n):
         """pool 0 full (HBM), 1 staging, 2 host, 3 drop tier; returns bf16 bits k, v [n][d]."""
