@@ -288,6 +288,8 @@ typedef struct {
   int link_queue;               /* transfers kept queued on the copy stream (>= 1) */
   double arrival_gap_ms;        /* request i arrives i * gap after the start (0 = burst) */
   const int32_t* first_tokens;  /* [n] each request's first input token (its own prompt suffix) */
+  int payload_order;            /* 0: per request (compressed_i, full_i, compressed_i+1, ...);
+                                   1: every arrived compressed payload ahead of any full KV */
 } vc_remote_desc;
 
 typedef struct {

@@ -79,7 +79,8 @@ class SchedStats(C.Structure):
 
 class RemoteDesc(C.Structure):
     _fields_ = [("x", C.c_int), ("K", C.c_int), ("baseline", C.c_int), ("link_queue", C.c_int),
-                ("arrival_gap_ms", C.c_double), ("first_tokens", C.POINTER(C.c_int32))]
+                ("arrival_gap_ms", C.c_double), ("first_tokens", C.POINTER(C.c_int32)),
+                ("payload_order", C.c_int)]
 
 
 class RemoteStats(C.Structure):

@@ -338,10 +338,12 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
 // the full KV stays resident after its first load.  force_baseline (:605-608)
 // loads the full KV and decodes.  Here both "links" are the GPU's copy engine
 // (the storage node is pinned host memory on this box), so the two payloads
-// share one FIFO: compressed loads are issued ahead of full loads, at most
-// link_queue transfers queued.  One forward pass per iteration runs every
-// drafting row, up to max_verify verify windows (oldest ready first) and, in
-// the baseline, every decode row.
+// share one FIFO, fed in arrival order with at most link_queue transfers
+// queued: per request (compressed, then full) by default, so each request
+// drafts while its own full KV streams and no later request's payload delays
+// an earlier request's first verify; or every compressed payload first.
+// One forward pass per iteration runs every drafting row, up to max_verify
+// verify windows (oldest ready first) and, in the baseline, every decode row.
 int vc_run_remote_prefix_impl(vc::Engine& en, const int* slots, int n, const vc_remote_desc& rd,
                               int32_t* out, vc_remote_stats* stats) {
   const auto& cfgE = en.config();
@@ -351,6 +353,7 @@ int vc_run_remote_prefix_impl(vc::Engine& en, const int* slots, int n, const vc_
   if (!base && (rd.x < 1 || rd.x > cfgE.max_x)) throw speckv::ConfigError("remote prefix: x out of [1, max_x]");
   if (rd.link_queue < 1) throw speckv::ConfigError("remote prefix: link_queue must be >= 1");
   if (rd.arrival_gap_ms < 0) throw speckv::ConfigError("remote prefix: arrival gap must be >= 0");
+  if (rd.payload_order != 0 && rd.payload_order != 1) throw speckv::ConfigError("remote prefix: payload_order is 0 or 1");
   if (en.prefix_tokens() < 1) throw vc::ContractViolation("remote prefix: no prefix stored (vc_prefix_store)");
   if (!rd.first_tokens) throw vc::ContractViolation("remote prefix: null first_tokens");
   if (en.prefix_tokens() + rd.K + cfgE.max_x > cfgE.max_ctx)
@@ -399,12 +402,16 @@ int vc_run_remote_prefix_impl(vc::Engine& en, const int* slots, int n, const vc_
         if (en.swap_done(r.full_id)) { r.full = true; r.t_full = now_ms(); } else ++inflight;
       }
     }
-    // feed the link: compressed payloads ahead of full KV, arrival order
+    // feed the link in arrival order: per request (its compressed payload, then
+    // its full KV -- the request drafts while its own full KV streams), or
+    // every compressed payload ahead of any full KV (payload_order 1)
     while (inflight < rd.link_queue) {
       int pick = -1, what = -1;
-      if (!base)
-        for (int i = 0; i < n && pick < 0; ++i)
-          if (rq[i].arrived && !rq[i].comp_issued) { pick = i; what = 0; }
+      for (int i = 0; i < n && pick < 0; ++i) {
+        if (!rq[i].arrived) continue;
+        if (!base && !rq[i].comp_issued) { pick = i; what = 0; }
+        else if (rd.payload_order == 0 && !rq[i].full_issued) { pick = i; what = 1; }
+      }
       for (int i = 0; i < n && pick < 0; ++i)
         if (rq[i].arrived && !rq[i].full_issued) { pick = i; what = 1; }
       if (pick < 0) break;

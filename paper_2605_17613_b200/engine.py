@@ -373,7 +373,7 @@ class Engine:
         return x.value
 
     def run_remote_prefix(self, slots, K, x, first_tokens, baseline=False, link_queue=2,
-                          arrival_gap_ms=0.0):
+                          arrival_gap_ms=0.0, payload_order=0):
         """Requests over the stored prefix: (tokens [n][K], stats dict)."""
         s = np.ascontiguousarray(slots, np.int32)
         ft = np.ascontiguousarray(first_tokens, np.int32)
@@ -381,7 +381,7 @@ class Engine:
             raise ValueError("one first token per request")
         out = np.zeros((s.size, K), np.int32)
         rd = _lib.RemoteDesc(x, K, int(bool(baseline)), link_queue, arrival_gap_ms,
-                             _ptr(ft, C.c_int32))
+                             _ptr(ft, C.c_int32), payload_order)
         st = _lib.RemoteStats()
         check(self.lib.vc_run_remote_prefix(self.h, _ptr(s, C.c_int), s.size, C.byref(rd),
                                             _ptr(out, C.c_int32), C.byref(st)))

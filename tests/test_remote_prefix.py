@@ -68,8 +68,10 @@ def test_remote_prefix_lossless_vs_baseline_and_greedy(cuda, weights, bits):
     assert 0 < ss["compressed_ready_ms_mean"] <= ss["full_ready_ms_mean"]
     assert ss["makespan_ms"] > 0 and ss["ttft_ms_max"] >= ss["ttft_ms_mean"] > 0
     # the loop releases and reloads its slots: a second run is identical
-    spec2, _ = e.run_remote_prefix(slots, K, 4, FIRST, link_queue=1)
+    spec2, s2 = e.run_remote_prefix(slots, K, 4, FIRST, link_queue=1, payload_order=1)
     np.testing.assert_array_equal(spec2, ref)
+    # every compressed payload first: all requests can draft before any full KV lands
+    assert s2["compressed_ready_ms_mean"] <= ss["compressed_ready_ms_mean"] + 50.0
     e.close()
 
 
