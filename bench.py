@@ -215,9 +215,9 @@ def hbm_peak(peaks):
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def draft_traffic():
+def draft_traffic(name="draft_attn_ncu.json"):
     """ncu --set full capture of the draft kernel (profiles/): DRAM bytes per launch."""
-    f = os.path.join(ROOT, "profiles", "draft_attn_ncu.json")
+    f = os.path.join(ROOT, "profiles", name)
     if not os.path.exists(f):
         return None, None
     d = json.load(open(f))
@@ -305,6 +305,8 @@ def main_remote(args, rank, world, local):
     base_value = b["tok"] / b["mk_s"]
     st = v["st"]
     achieved = ka_bytes / (ka_ms / 1e3) / 1e9
+    traffic, traffic_src = (draft_traffic("draft_attn_int2_ncu.json")
+                            if (bits, ctx, B) == (2, 65536, 12) else (None, None))
     if rank == 0:
         def arm_summary(r):
             s = r["st"]
@@ -341,7 +343,8 @@ def main_remote(args, rank, world, local):
             "tokens_identical_to_full_kv": identical, "tokens_compared": int(v["out"].size),
             "roofline": {"kernel": f"draft_attn_quant_kernel (int{bits}, one launch per layer, {B} requests, "
                                    f"{ctx} ctx)", "bound": "hbm", "achieved": round(achieved, 1),
-                         "peak": round(peak, 1), "unit": "GB/s", "frac": round(achieved / peak, 3), "traffic": None,
+                         "peak": round(peak, 1), "unit": "GB/s", "frac": round(achieved / peak, 3),
+                         "traffic": traffic, "traffic_source": traffic_src,
                          "bytes_per_launch": int(ka_bytes / shape.layers),
                          "ms_per_launch": round(ka_ms / shape.layers, 4), "peak_source": peak_src},
             "compressed": {"bit_scheme": meta["bit_scheme"], "payload_bytes": meta["payload_bytes"],
