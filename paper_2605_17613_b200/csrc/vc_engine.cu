@@ -668,6 +668,12 @@ void Engine::enqueue_forward(int M, int n_draft, int n_dense1, int n_densev, int
   GemmEpilogue ef;
   ef.kind = Epi::StoreF32;
   ef.out_f32 = logits_;
+  // VC_SKIP (diagnostics only, wrong results): bit 0 skips attention + combine,
+  // bit 1 skips rms_apply -- to time the rest of a step in its CUDA graph
+  static const int skip = [] {
+    const char* v = std::getenv("VC_SKIP");
+    return v ? std::atoi(v) : 0;
+  }();
   VC_LAUNCH(embed_norm(tok_in_, M, M, w_.embed, H, w_.attn_norm[0], m.eps, x_, xn_, st_));
   trace("embed.x", x_, static_cast<size_t>(M) * H * 4);
   trace("w.gu0", w_.wgu[0], static_cast<size_t>(2) * F * H * 2);
@@ -676,7 +682,8 @@ void Engine::enqueue_forward(int M, int n_draft, int n_dense1, int n_densev, int
     eq.layer = l;
     VC_LAUNCH(gemm(xn_, M, M, H, w_.wqkv[l], qkv_n, eq, gws_, st_));
     trace("qkv", qkv_, static_cast<size_t>(M) * qkv_n * 2);
-    if (n_draft > 0 && drop_mode()) {
+    if (skip & 1) {
+    } else if (n_draft > 0 && drop_mode()) {
       VC_LAUNCH(dense_attention(as, drop_, drop_maps_, l, seqs_dev_, n_draft, max_chunks_x_, 1, part_, st_));
       VC_LAUNCH(attention_combine(as, seqs_dev_, n_draft, max_chunks_x_, 1, 1, part_, attn_, st_));
     } else if (n_draft > 0) {
@@ -684,41 +691,42 @@ void Engine::enqueue_forward(int M, int n_draft, int n_dense1, int n_densev, int
                                       cfg_.quant_bits, part_, st_));
       VC_LAUNCH(attention_combine(as, seqs_dev_, n_draft, max_chunks_q_, 1, 0, part_, attn_, st_));
     }
-    if (n_dense1 > 0) {
+    if (n_dense1 > 0 && !(skip & 1)) {
       VC_LAUNCH(dense_attention(as, full_, dense_maps_, l, seqs_dev_ + n_draft, n_dense1, max_chunks_d_, 1, part_, st_));
       VC_LAUNCH(attention_combine(as, seqs_dev_ + n_draft, n_dense1, max_chunks_d_, 1, 1, part_, attn_, st_));
     }
-    if (n_densev > 0) {
+    if (n_densev > 0 && !(skip & 1)) {
       const AttnSeq* sv = seqs_dev_ + n_draft + n_dense1;
       VC_LAUNCH(dense_attention(as, dense_v_pool, dense_maps_, l, sv, n_densev, max_chunks_d_, max_rows_v, part_, st_));
       VC_LAUNCH(attention_combine(as, sv, n_densev, max_chunks_d_, max_rows_v, 1, part_, attn_, st_));
     }
     // residual projection: fused residual epilogue, or (tensor parallel) the
-    // rank's partial -> all-gather -> fixed rank-order sum + residual (vc_tp.h)
-    auto residual_gemm = [&](const uint16_t* Xt, int Kd, const uint16_t* Wt) {
+    // rank's partial -> all-gather -> fixed rank-order sum + residual (vc_tp.h);
+    // then the next RMSNorm.  (r1: fusing the RMSNorm into the residual
+    // epilogue -- tile finishers spin until every tile's ss_part is in -- was
+    // bit-identical but 3% slower per step than this launch.)
+    auto residual_gemm = [&](const uint16_t* Xt, int Kd, const uint16_t* Wt, const uint16_t* norm_w) {
       if (!coll_) {
         VC_LAUNCH(gemm(Xt, M, M, Kd, Wt, H, er, gws_, st_));
-        return;
+      } else {
+        GemmEpilogue ey;
+        ey.kind = Epi::StoreF32;
+        ey.out_f32 = tp_y_;
+        VC_LAUNCH(gemm(Xt, M, M, Kd, Wt, H, ey, gws_, st_));
+        coll_->all_gather(tp_y_, tp_g_, static_cast<size_t>(M) * H, st_);
+        VC_LAUNCH(tp_residual(x_, tp_g_, cfg_.tp_size, M, H, ss_part_, st_));
       }
-      GemmEpilogue ey;
-      ey.kind = Epi::StoreF32;
-      ey.out_f32 = tp_y_;
-      VC_LAUNCH(gemm(Xt, M, M, Kd, Wt, H, ey, gws_, st_));
-      coll_->all_gather(tp_y_, tp_g_, static_cast<size_t>(M) * H, st_);
-      VC_LAUNCH(tp_residual(x_, tp_g_, cfg_.tp_size, M, H, ss_part_, st_));
+      if (!(skip & 2)) VC_LAUNCH(rms_apply(x_, ss_part_, M, M, H, norm_w, m.eps, xn_, st_));
     };
-    residual_gemm(attn_, m.n_q * d, w_.wo[l]);
+    residual_gemm(attn_, m.n_q * d, w_.wo[l], w_.mlp_norm[l]);
     trace("attn", attn_, static_cast<size_t>(M) * m.n_q * d * 2);
     trace("x.o", x_, static_cast<size_t>(M) * H * 4);
     trace("ss.o", ss_part_, static_cast<size_t>(M) * (H / 128) * 4);
-    VC_LAUNCH(rms_apply(x_, ss_part_, M, M, H, w_.mlp_norm[l], m.eps, xn_, st_));
     trace("xn.o", xn_, static_cast<size_t>(M) * H * 2);
     VC_LAUNCH(gemm(xn_, M, M, H, w_.wgu[l], 2 * F, es, gws_, st_));
     trace("act", act_, static_cast<size_t>(M) * F * 2);
-    residual_gemm(act_, F, w_.wd[l]);
+    residual_gemm(act_, F, w_.wd[l], l + 1 < L ? w_.attn_norm[l + 1] : w_.final_norm);
     trace("x.d", x_, static_cast<size_t>(M) * H * 4);
-    VC_LAUNCH(rms_apply(x_, ss_part_, M, M, H, l + 1 < L ? w_.attn_norm[l + 1] : w_.final_norm, m.eps,
-                        xn_, st_));
   }
   VC_LAUNCH(gemm(xn_, M, M, H, w_.lm_head, V, ef, gws_, st_));
   trace("logits", logits_, static_cast<size_t>(M) * V * 4);
