@@ -1,0 +1,7 @@
+#!/bin/bash
+for lib in libvericache.so libvc_a.so libvc_b.so libvc_c.so; do
+  for m in "draft 1" "mixed 6" "mixed 16" "decode 1"; do set -- $m
+    echo "$lib $1 x=$2 $(VC_LIB=paper_2605_17613_b200/$lib timeout 300 python tools/profile_step.py --mode $1 --x $2 --steps 8 2>&1 | tail -1)"
+  done
+done
+VC_LIB=paper_2605_17613_b200/libvc_a.so timeout 600 python -m pytest tests/test_gemm.py tests/test_lossless.py tests/test_model_parity.py -x -q 2>&1 | tail -2
