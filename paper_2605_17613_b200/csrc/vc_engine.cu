@@ -1104,6 +1104,14 @@ uint64_t Engine::prefix_load(int slot, int what, int32_t pending) {
   if (slot < 0 || slot >= cfg_.max_slots) throw ContractViolation("slot out of range");
   if (what != 0 && what != 1) throw ContractViolation("prefix_load: what is 0 (compressed) or 1 (full)");
   if (pre_T_ + cfg_.max_x + 2 > full_.cap) throw ContractViolation("prefix exceeds the slot capacity");
+  {
+    const SeqState& s0 = seqs_.at(slot);
+    // a slot is opened by its first load; the other form may follow (the full
+    // KV lands while the request drafts), but nothing may overwrite a slot
+    // that has moved past the prefix or a compressed tier being drafted on
+    if (s0.live && (s0.committed != pre_T_ || (what == 0 && !s0.drafted.empty())))
+      throw ContractViolation("prefix_load: slot holds another request (release it first)");
+  }
   const auto& m = cfg_.model;
   const int n_slices = m.layers * m.n_kv;
   const size_t base = static_cast<size_t>(slot) * n_slices;

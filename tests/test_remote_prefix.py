@@ -103,6 +103,11 @@ def test_remote_prefix_contract_and_config_errors(cuda, weights):
         e.run_remote_prefix([1], K, 17, [17])     # x > max_x
     with pytest.raises(_lib.ConfigError):
         e.run_remote_prefix([1], 10 ** 6, 4, [17])  # beyond max_ctx
+    e.add_synthetic(2, 100, 17, seed=3)
+    with pytest.raises(_lib.ContractError):      # slot holds another request
+        e.prefix_load(2, 0, 17)
+    e.release(2)
+    assert e.prefix_load(2, 0, 17) > 0
     e.close()
     f = Engine(TINY, max_slots=2, max_ctx=N_CTX + 200, max_x=8, quant_bits=0)
     f.load_weights(weights)
