@@ -236,11 +236,13 @@ def main_remote(args, rank, world, local):
     import numpy as np
     import torch
     import paper_2605_17613_b200 as vc
-    from paper_2605_17613_b200.shard import reduce_window, weak_shard
+    from paper_2605_17613_b200.shard import bind_numa_local, reduce_window, weak_shard
 
     n_dev = torch.cuda.device_count()
     local = local % n_dev
     torch.cuda.set_device(local)
+    if world > 1:
+        bind_numa_local(local)
     dist = None
     coll_dev = "cuda"
     if world > 1:
@@ -371,11 +373,12 @@ def main():
     import numpy as np
     import torch
     import paper_2605_17613_b200 as vc
-    from paper_2605_17613_b200.shard import reduce_window, weak_shard
+    from paper_2605_17613_b200.shard import bind_numa_local, reduce_window, weak_shard
 
     n_dev = torch.cuda.device_count()
     torch.cuda.set_device(local % n_dev)
     local = local % n_dev
+    numa = bind_numa_local(local) if world > 1 else []  # NUMA-local pinned pool per rank
     dist = None
     coll_dev = "cuda"
     if world > 1:
@@ -544,6 +547,7 @@ def main():
                        "step": "one speculative round of the batch: x+1 scheduler iterations (each a forward "
                                "pass over every drafting row and verify window)",
                        "parallelism": f"request-sharded dp{world}",
+                       "host_numa_cpus": (f"{len(numa)} GPU-local cores" if numa else "unbound"),
                        "l2": "inputs larger than L2 (>= 30 GB of weights + compressed KV read per step)"},
             "e2e": {"value": round(tok_all / wall_s, 2), "unit": "tokens/s",
                     "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(rows / K * 4)},

@@ -49,3 +49,45 @@ def reduce_window(tokens: float, times: list, dist=None, device=None):
     dist.all_reduce(t)
     dist.all_reduce(m, op=dist.ReduceOp.MAX)
     return float(t.item()), [float(x) for x in m.tolist()]
+
+
+def parse_cpulist(text: str) -> list:
+    """'0-3,8,10-11' -> [0, 1, 2, 3, 8, 10, 11] (sysfs cpulist format)."""
+    cpus = []
+    for part in text.strip().split(","):
+        if not part:
+            continue
+        if "-" in part:
+            a, b = part.split("-")
+            cpus.extend(range(int(a), int(b) + 1))
+        else:
+            cpus.append(int(part))
+    return cpus
+
+
+def gpu_local_cpus(domain: int, bus: int, device: int, sysfs: str = "/sys/bus/pci/devices") -> list:
+    """CPUs on the GPU's NUMA node (the PCI function's local_cpulist), or []."""
+    import os
+    path = os.path.join(sysfs, f"{domain:04x}:{bus:02x}:{device:02x}.0", "local_cpulist")
+    try:
+        with open(path) as f:
+            return parse_cpulist(f.read())
+    except OSError:
+        return []
+
+
+def bind_numa_local(torch_device: int) -> list:
+    """Pin this rank's host threads to its GPU's NUMA node, so the pinned host
+    KV pool (first-touched by cudaHostAlloc in this thread) and the copy
+    engine's reads stay socket-local (each GPU owns a
+    NUMA-local pinned pool and its own PCIe link).  Returns the CPU set used
+    ([] when the topology is unknown -- nothing changes then)."""
+    import os
+    import torch
+    p = torch.cuda.get_device_properties(torch_device)
+    cpus = gpu_local_cpus(p.pci_domain_id, p.pci_bus_id, p.pci_device_id)
+    avail = os.sched_getaffinity(0)
+    cpus = [c for c in cpus if c in avail]
+    if cpus:
+        os.sched_setaffinity(0, cpus)
+    return cpus

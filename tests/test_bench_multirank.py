@@ -35,3 +35,19 @@ def test_two_ranks_small(cuda):
     d = json.loads(lines[0])
     assert d["n_gpus"] == 2 and d["config"]["global_batch"] == 32 and d["scaling"] == "weak"
     assert d["tokens_identical_to_full_kv"] and d["value"] > 0
+
+
+def test_two_ranks_remote_prefix_small(cuda):
+    """configs[3] under torchrun: each rank streams its own requests' payloads
+    over its own copy engine; tokens summed, makespan max over ranks."""
+    env = dict(os.environ, BENCH_BACKEND="gloo")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node", "2",
+           "--master-addr", "127.0.0.1", "--master-port", str(_port()), os.path.join(T.ROOT, "bench.py"),
+           "--gpus", "2", "--small", "--config", "4", "--out-tokens", "32"]
+    r = subprocess.run(cmd, capture_output=True, text=True, timeout=600, env=env, cwd=T.ROOT)
+    assert r.returncode == 0, r.stderr[-3000:]
+    lines = [ln for ln in r.stdout.splitlines() if ln.startswith("{")]
+    assert len(lines) == 1, r.stdout
+    d = json.loads(lines[0])
+    assert d["n_gpus"] == 2 and d["config"]["global_batch"] == 8 and d["tokens_identical_to_full_kv"]
+    assert d["value"] > 0 and d["vericache"]["verifies"] > 0

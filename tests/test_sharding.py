@@ -90,3 +90,15 @@ def test_gloo_two_ranks_reduce_window():
 def test_reduce_window_single_process():
     assert reduce_window(5, [1.5, 2.0]) == (5.0, [1.5, 2.0])
     assert torch.tensor(1).item() == 1
+
+
+def test_numa_cpulist_parsing_and_sysfs_lookup(tmp_path):
+    from paper_2605_17613_b200.shard import gpu_local_cpus, parse_cpulist
+    assert parse_cpulist("0-3,8,10-11\n") == [0, 1, 2, 3, 8, 10, 11]
+    assert parse_cpulist("") == []
+    dev = tmp_path / "0000:1b:00.0"
+    dev.mkdir()
+    (dev / "local_cpulist").write_text("56-111,168-223\n")
+    cpus = gpu_local_cpus(0, 0x1B, 0, sysfs=str(tmp_path))
+    assert cpus[:2] == [56, 57] and len(cpus) == 112 and cpus[-1] == 223
+    assert gpu_local_cpus(0, 0x2B, 0, sysfs=str(tmp_path)) == []  # unknown device: no binding
