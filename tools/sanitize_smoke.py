@@ -1,6 +1,6 @@
 """Small end-to-end run for compute-sanitizer (memcheck / racecheck / synccheck):
 d=64 and d=128 head shapes; int4, int2 and drop-topk tiers; tier 0 and tier 1
-scheduled loops; no CUDA graphs (so every launch is checked)."""
+scheduled loops; the remote-prefix loop; no CUDA graphs (so every launch is checked)."""
 import os
 import sys
 
@@ -33,6 +33,15 @@ def run(shape):
         out, st = e.run_scheduled([0, 1], 12, x=4, window=16)
         assert np.array_equal(out, base), (shape, kw)
         e.close()
+    # remote prefix: the stored prefix streamed into fresh slots (int2 payload)
+    e = Engine(shape, max_slots=3, max_ctx=700, max_x=8, max_verify=2, quant_bits=2, use_graphs=False)
+    e.load_weights(w)
+    e.add_synthetic(2, 500, 0, seed=1)
+    e.compress(2)
+    e.prefix_store(2)
+    out, _ = e.run_remote_prefix([0, 1], 12, 4, [17, 18])
+    assert np.array_equal(out[0], base[0]), (shape, "remote prefix")  # same prefix seed + first token
+    e.close()
 
 
 for shape in (TINY, D128):
