@@ -434,14 +434,17 @@ def main():
     del eb
     torch.cuda.empty_cache()
 
-    def vericache(tier):
+    def vericache(tier, x_force=None):
         """One VeriCache run: compressed drafting + full-KV verify (tier 0: full KV
         in HBM; tier 1: full KV in pinned host memory, reloaded per verify)."""
         # host tier x=47: the verify window plus 15 drafting rows stays within one
         # 64-row GEMM tile and the booked reloads saturate PCIe (link busy 0.99)
         # HBM tier x=6: the measured optimum of an x sweep {4,6,8,10,12,16,24}
         # (1398 / 1360 / 1343 / 1235 / 1045 tok/s at x = 6 / 8 / 12 / 16 / 24)
-        x = args.x or (47 if tier == 1 else (32 if cfg3 else 6))
+        # configs[2] x=3: the measured optimum of {3,4,6,8,10,16,32,64} (397 / 389 /
+        # 361 / 354 / 329 / 267 / 173 / 94 tok/s; the drop tier's acceptance on
+        # synthetic KV falls fast with x); the long horizon x=32 is reported beside it
+        x = x_force or args.x or (47 if tier == 1 else (3 if cfg3 else 6))
         window = args.window or max(2 * x + 8, 48 if tier == 0 else 256)
         ramp = 2 * (x + 1)  # warm-up includes two ramp rounds: every request has drafted and verified
         # a step = one speculative round: x+1 scheduler iterations (every request
@@ -496,6 +499,9 @@ def main():
             runs[1 - head_tier] = vericache(1 - head_tier)
         except vc.VcError as ex:
             note = f"secondary tier skipped: {ex}"
+    long_run = None
+    if cfg3 and not args.small and not args.x:
+        long_run = vericache(0, x_force=32)  # configs[2]'s "long draft horizon", same workload
     h = runs[head_tier]
     st, x = h["st"], h["x"]
     tok_all, dev_s, wall_s = h["tok"], h["dev_s"], h["wall_s"]
@@ -560,6 +566,7 @@ def main():
             "accepted_per_verify": round(st["mean_accept"], 3), "verifies": st["verifies"],
             "late_transfers": st["late_transfers"],
             "tiers": {("host" if t else "hbm"): tier_summary(r, t) for t, r in runs.items()},
+            **({"long_horizon": tier_summary(long_run, 0)} if long_run else {}),
             "roofline": {"kernel": ("dense_umma_kernel<128,4> drafting over the drop tier" if cfg3 else
                                     "draft_attn_quant_kernel<128,4,4>") + f" (one launch per layer, {B} requests)",
                          "bound": "hbm", "achieved": round(achieved, 1), "peak": round(peak, 1), "unit": "GB/s",
