@@ -260,9 +260,9 @@ def main_remote(args, rank, world, local):
     if args.small:
         ctx, B = min(ctx, 4096), min(B, 4)
     bits = 2 if args.bits == 4 else args.bits
-    # x=4: the measured optimum of {4, 6, 8, 12} (560 / 548 / 391 / 435 tok/s,
-    # 3.05 / 4.19 / 3.57 / 6.01 accepted per verify at int2)
-    x = args.x or 4
+    # x=3: the measured optimum of {2, 3, 4, 6, 8, 12} (583 / 589 / 576 / 548 /
+    # 391 / 435 tok/s; 1.76 / 2.46 / 3.05 / 4.19 / 3.57 / 6.01 accepted per verify, int2)
+    x = args.x or 3
     K = args.out_tokens
     shard = weak_shard(B, world, rank)
     rng = np.random.default_rng(2 + shard.requests[0])
