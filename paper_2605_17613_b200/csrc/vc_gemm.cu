@@ -58,7 +58,6 @@ struct Cfg {
   static constexpr int kSmem = kStages * kStage + kEpiRows * kLD * 4 + 1024;  // + 1 KB alignment slack
 };
 
-VC_DEV int swz8(int row, int c) { return c ^ (row & 7); }
 
 // P = min(kP, T) so every CTA owns at least one k-tile (a function of N, K).
 __host__ __device__ inline long grid_of(long T) { return T < kP ? T : kP; }
@@ -314,6 +313,58 @@ gemm_umma_kernel(const uint16_t* __restrict__ Xt, int Mp, int M, int K,
         __threadfence();
       }
       // ---- epilogue, 16 tokens per staged pass ---------------------------------
+      if constexpr (NT >= 32) {
+        // Pass pairs: the two warps of a TMEM lane quarter own token halves
+        // [0, kHalf) and [kHalf, NT); pass p stages tokens 16p.. of half 0 and
+        // pass p + NT/32 tokens 16p.. of half 1.  Every warp sums all
+        // contributors' partials for its 16 tokens of the pair up front, so
+        // both halves' loads are in flight together instead of pass after
+        // pass (same contributor order per element: bit-identical).
+#pragma unroll 1
+        for (int pp = 0; pp < NT / 32; ++pp) {
+          const int my_tok = tok0 + 16 * pp;  // this warp's 16 tokens of the pair
+          float4 acc[4];
+          if (m0 + my_tok >= M) {
+            // rows past the batch: this warp's pass is skipped (warp-uniform)
+          } else if (n_contrib > 1) {
+            const float4* src = part + (my_tok >> 2) * kBN + feat;
+#pragma unroll
+            for (int i = 0; i < 4; ++i) acc[i] = __ldcg(src + i * kBN);
+#pragma unroll 2
+            for (int cc = 1; cc < n_contrib; ++cc) {
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                const float4 x = __ldcg(src + static_cast<size_t>(cc) * kPart4 + i * kBN);
+                acc[i].x += x.x; acc[i].y += x.y; acc[i].z += x.z; acc[i].w += x.w;
+              }
+            }
+          } else {
+#pragma unroll
+            for (int g = 0; g < 2; ++g) {
+              float v[8];
+              ld8(16 * pp + g * 8, v);
+              acc[2 * g] = make_float4(v[0], v[1], v[2], v[3]);
+              acc[2 * g + 1] = make_float4(v[4], v[5], v[6], v[7]);
+            }
+          }
+#pragma unroll
+          for (int h2 = 0; h2 < 2; ++h2) {
+            const int qlo = h2 * kHalf + 16 * pp;  // first token of this pass
+            if (tok0 == h2 * kHalf) {
+#pragma unroll
+              for (int i = 0; i < 4; ++i) {
+                sT[(4 * i + 0) * kLD + feat] = acc[i].x;
+                sT[(4 * i + 1) * kLD + feat] = acc[i].y;
+                sT[(4 * i + 2) * kLD + feat] = acc[i].z;
+                sT[(4 * i + 3) * kLD + feat] = acc[i].w;
+              }
+            }
+            named_bar(1, 256);
+            if (m0 + qlo < M) epilogue_pass<E>(sT, m0 + qlo, M, Mp, n0, N, ep, et);
+            named_bar(1, 256);
+          }
+        }
+      } else
       for (int q = 0; q < NT / kEpiRows; ++q) {
         const int qlo = q * kEpiRows;
         // this warp stages the pass's tokens that lie in its half, 8 at a time
