@@ -48,6 +48,13 @@ constexpr int kSms = 148;
 constexpr int kP = VC_GEMM_GRID_PER_SM * kSms;  // stream-K grid upper bound (a function of nothing but the GPU)
 constexpr int kEpiRows = 16;           // epilogue staging pass (tokens)
 constexpr int kLD = kBN + 4;
+#ifndef VC_FIXUP_UNROLL
+#define VC_FIXUP_UNROLL 4       // contributors in flight per loop trip, NT = 16
+#endif
+#ifndef VC_FIXUP_UNROLL_WIDE
+#define VC_FIXUP_UNROLL_WIDE 2  // contributors in flight per loop trip, NT >= 32 (4 float4 each)
+#endif
+constexpr int kFixUnroll = VC_FIXUP_UNROLL, kFixUnrollWide = VC_FIXUP_UNROLL_WIDE;
 
 template <int NT>
 struct Cfg {
@@ -330,7 +337,7 @@ gemm_umma_kernel(const uint16_t* __restrict__ Xt, int Mp, int M, int K,
             const float4* src = part + (my_tok >> 2) * kBN + feat;
 #pragma unroll
             for (int i = 0; i < 4; ++i) acc[i] = __ldcg(src + i * kBN);
-#pragma unroll 2
+#pragma unroll kFixUnrollWide
             for (int cc = 1; cc < n_contrib; ++cc) {
 #pragma unroll
               for (int i = 0; i < 4; ++i) {
@@ -378,7 +385,7 @@ gemm_umma_kernel(const uint16_t* __restrict__ Xt, int Mp, int M, int K,
             // unrolled loop keeps several in flight
             const float4* src = part + (tok >> 2) * kBN + feat;
             float4 a = __ldcg(src), b = __ldcg(src + kBN);
-#pragma unroll 4
+#pragma unroll kFixUnroll
             for (int cc = 1; cc < n_contrib; ++cc) {
               const float4 x = __ldcg(src + static_cast<size_t>(cc) * kPart4);
               const float4 y = __ldcg(src + static_cast<size_t>(cc) * kPart4 + kBN);
