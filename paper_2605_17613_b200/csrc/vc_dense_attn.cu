@@ -13,12 +13,19 @@ namespace {
 constexpr int kMaxParts = 512;  // chunks per sequence the combine can merge (256K ctx)
 
 template <int D>
-__global__ void combine_kernel(AttnShape s, const AttnSeq* seqs, int max_chunks, int mode,
-                               Partials part, uint16_t* out) {
+__global__ void combine_kernel(AttnShape s, CombineSets cs, Partials part, uint16_t* out) {
   pdl_trigger();
   pdl_wait();
-  const AttnSeq sq = seqs[blockIdx.x];
-  const int tok = blockIdx.y;
+  // this block's (set, sequence, query row): set k covers n * rows blocks
+  int k = 0, b = blockIdx.x;
+  while (k + 1 < cs.n_sets && b >= cs.set[k].n * cs.set[k].rows) {
+    b -= cs.set[k].n * cs.set[k].rows;
+    ++k;
+  }
+  const AttnSeq* seqs = cs.set[k].seqs;
+  const int n_set = cs.set[k].n, max_chunks = cs.set[k].max_chunks, mode = cs.set[k].mode;
+  const int bx = b / cs.set[k].rows, tok = b % cs.set[k].rows;
+  const AttnSeq sq = seqs[bx];
   if (tok >= sq.n_rows) return;
   const int hq = blockIdx.z;
   const int Hq = s.n_kv * s.n_rep;
@@ -29,10 +36,10 @@ __global__ void combine_kernel(AttnShape s, const AttnSeq* seqs, int max_chunks,
     n_parts = 0;
     if (sq.n_groups > 0) {
       int T = 0, base = 0;
-      for (int i = threadIdx.x & 31; i < gridDim.x; i += 32) {
+      for (int i = threadIdx.x & 31; i < n_set; i += 32) {
         const int c = seqs[i].n_groups * s.n_kv;
         T += c;
-        base += i < static_cast<int>(blockIdx.x) ? c : 0;
+        base += i < bx ? c : 0;
       }
       T = __reduce_add_sync(0xffffffffu, T);
       base = __reduce_add_sync(0xffffffffu, base);
@@ -90,14 +97,33 @@ __global__ void combine_kernel(AttnShape s, const AttnSeq* seqs, int max_chunks,
 
 }  // namespace
 
+cudaError_t attention_combine_sets(const AttnShape& s, const CombineSets& cs, Partials part, uint16_t* out,
+                                   cudaStream_t st) {
+  if (cs.n_sets < 1 || cs.n_sets > 3) return cudaErrorInvalidValue;
+  int n = 0;
+  for (int k = 0; k < cs.n_sets; ++k) {
+    if (cs.set[k].rows < 1) return cudaErrorInvalidValue;
+    n += cs.set[k].n * cs.set[k].rows;
+  }
+  if (n <= 0) return cudaSuccess;
+  dim3 grid(n, 1, s.n_kv * s.n_rep);
+  if (s.d == 128) return launch_pdl(combine_kernel<128>, grid, dim3(128), 0, st, s, cs, part, out);
+  if (s.d == 64) return launch_pdl(combine_kernel<64>, grid, dim3(64), 0, st, s, cs, part, out);
+  return cudaErrorInvalidValue;
+}
+
 cudaError_t attention_combine(const AttnShape& s, const AttnSeq* seqs, int n_seq, int max_chunks,
                               int max_rows, int mode, Partials part, uint16_t* out,
                               cudaStream_t st) {
   if (n_seq <= 0) return cudaSuccess;
-  dim3 grid(n_seq, max_rows, s.n_kv * s.n_rep);
-  if (s.d == 128) return launch_pdl(combine_kernel<128>, grid, dim3(128), 0, st, s, seqs, max_chunks, mode, part, out);
-  if (s.d == 64) return launch_pdl(combine_kernel<64>, grid, dim3(64), 0, st, s, seqs, max_chunks, mode, part, out);
-  return cudaErrorInvalidValue;
+  CombineSets cs;
+  cs.set[0].seqs = seqs;
+  cs.set[0].n = n_seq;
+  cs.set[0].max_chunks = max_chunks;
+  cs.set[0].mode = mode;
+  cs.set[0].rows = max_rows;
+  cs.n_sets = 1;
+  return attention_combine_sets(s, cs, part, out, st);
 }
 
 }  // namespace vc

@@ -682,24 +682,35 @@ void Engine::enqueue_forward(int M, int n_draft, int n_dense1, int n_densev, int
     eq.layer = l;
     VC_LAUNCH(gemm(xn_, M, M, H, w_.wqkv[l], qkv_n, eq, gws_, st_));
     trace("qkv", qkv_, static_cast<size_t>(M) * qkv_n * 2);
+    // the step's attention kernels, then ONE combine over all their partials
+    CombineSets cs;
+    auto add_set = [&](const AttnSeq* sq, int n, int max_chunks, int mode, int rows) {
+      CombineSet& c = cs.set[cs.n_sets++];
+      c.seqs = sq;
+      c.n = n;
+      c.max_chunks = max_chunks;
+      c.mode = mode;
+      c.rows = rows;
+    };
     if (skip & 1) {
     } else if (n_draft > 0 && drop_mode()) {
       VC_LAUNCH(dense_attention(as, drop_, drop_maps_, l, seqs_dev_, n_draft, max_chunks_x_, 1, part_, st_));
-      VC_LAUNCH(attention_combine(as, seqs_dev_, n_draft, max_chunks_x_, 1, 1, part_, attn_, st_));
+      add_set(seqs_dev_, n_draft, max_chunks_x_, 1, 1);
     } else if (n_draft > 0) {
       VC_LAUNCH(draft_attention_quant(as, quant_, l, qkv_, seqs_dev_, n_draft, max_chunks_q_,
                                       cfg_.quant_bits, part_, st_));
-      VC_LAUNCH(attention_combine(as, seqs_dev_, n_draft, max_chunks_q_, 1, 0, part_, attn_, st_));
+      add_set(seqs_dev_, n_draft, max_chunks_q_, 0, 1);
     }
     if (n_dense1 > 0 && !(skip & 1)) {
       VC_LAUNCH(dense_attention(as, full_, dense_maps_, l, seqs_dev_ + n_draft, n_dense1, max_chunks_d_, 1, part_, st_));
-      VC_LAUNCH(attention_combine(as, seqs_dev_ + n_draft, n_dense1, max_chunks_d_, 1, 1, part_, attn_, st_));
+      add_set(seqs_dev_ + n_draft, n_dense1, max_chunks_d_, 1, 1);
     }
     if (n_densev > 0 && !(skip & 1)) {
       const AttnSeq* sv = seqs_dev_ + n_draft + n_dense1;
       VC_LAUNCH(dense_attention(as, dense_v_pool, dense_maps_, l, sv, n_densev, max_chunks_d_, max_rows_v, part_, st_));
-      VC_LAUNCH(attention_combine(as, sv, n_densev, max_chunks_d_, max_rows_v, 1, part_, attn_, st_));
+      add_set(sv, n_densev, max_chunks_d_, 1, max_rows_v);
     }
+    if (cs.n_sets > 0) VC_LAUNCH(attention_combine_sets(as, cs, part_, attn_, st_));
     // residual projection: fused residual epilogue, or (tensor parallel) the
     // rank's partial -> all-gather -> fixed rank-order sum + residual (vc_tp.h);
     // then the next RMSNorm.  (r1: fusing the RMSNorm into the residual

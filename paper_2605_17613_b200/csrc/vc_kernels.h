@@ -136,5 +136,19 @@ cudaError_t dense_attention(const AttnShape& s, const KvPool& pool, const DenseM
 cudaError_t attention_combine(const AttnShape& s, const AttnSeq* seqs, int n_seq, int max_chunks,
                               int max_rows, int mode, Partials part, uint16_t* out,
                               cudaStream_t st);
+// Up to three sequence sets of one step (drafting, dense decode, verify
+// windows) merged by ONE launch: same per-(sequence, token, head) arithmetic
+// and order as attention_combine, one kernel boundary instead of three.
+struct CombineSet {
+  const AttnSeq* seqs = nullptr;
+  int n = 0, max_chunks = 0, mode = 0;
+  int rows = 1;  // query rows per sequence the grid covers (max over the set)
+};
+struct CombineSets {
+  CombineSet set[3];
+  int n_sets = 0;
+};
+cudaError_t attention_combine_sets(const AttnShape& s, const CombineSets& cs, Partials part, uint16_t* out,
+                                   cudaStream_t st);
 
 }  // namespace vc
