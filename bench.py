@@ -463,10 +463,17 @@ def main():
         if dist:
             dist.barrier()
         torch.cuda.synchronize()
+        # BENCH_NCU=1: open the profiler window around this run only, so
+        # `ncu --profile-from-start off` lists exactly the serving loop's launches
+        prof = os.environ.get("BENCH_NCU") == "1" and tier == head_tier and not x_force
+        if prof:
+            torch.cuda.cudart().cudaProfilerStart()
         with Clocks(local) as clk:
             out, st = ev.run_scheduled(slots, K=(it_w + it_k) * (x + 1), x=x, window=window,
                                        warmup_iterations=it_w, timed_iterations=it_k)
         torch.cuda.synchronize()
+        if prof:
+            torch.cuda.cudart().cudaProfilerStop()
         if dist:
             dist.barrier()
         launches = ev.stats()["kernel_launches"] - launches0
