@@ -34,6 +34,13 @@
  *                                   180, 219; src/sim.cpp:243-250)
  *   vc_run_scheduled                simulate_staggered's loop with real kernels
  *                                   and copies (src/sim.cpp:182-307)
+ *   vc_prefix_store / vc_prefix_load / vc_run_remote_prefix
+ *                                   remote_prefix's payload transfers and
+ *                                   draft/verify cycles on real copies and
+ *                                   kernels (src/sim.cpp:510-665; closed form
+ *                                   t_req_remote, src/analytics.cpp:25-35)
+ *   vc_run_speculative_ngram        composition with an n-gram drafter
+ *                                   (composed_accept_length, analytics.cpp:413-422)
  *   vc_engine_attach_nccl / vc_tp_* no reference counterpart: the simulator
  *                                   models TP only as GPU counts (core.hpp:45-46);
  *                                   BASELINE.json configs[4] (TP=8 over NVLink)
