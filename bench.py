@@ -530,7 +530,10 @@ def main():
              "ramp_iterations": r["ramp"],
              "accepted_per_verify": round(s["mean_accept"], 3), "verifies": s["verifies"],
              "tokens_identical_to_full_kv": bool(r["identical"]), "tokens_compared": r["compared"],
-             "full_kv_in": "pinned host memory" if tier else "HBM"}
+             "full_kv_in": "pinned host memory" if tier else "HBM",
+             # share of the device window the steps themselves occupy (the rest:
+             # host planning between steps, which the next round can overlap)
+             "gpu_busy_frac": round(s["timed_step_device_ms"] / max(s["timed_device_ms"], 1e-9), 3)}
         if tier == 1:
             win_s = s["timed_wall_ms"] / 1e3
             d["swap"] = {"h2d_gbs": round(s["h2d_bytes"] / max(s["h2d_ms"], 1e-9) / 1e6, 1),

@@ -268,6 +268,9 @@ typedef struct {
   double timed_device_ms;   /* device time of the window: one CUDA event pair on the
                                compute stream around all its steps (gaps included) */
   double timed_rows;        /* activation rows executed in the window */
+  double timed_step_device_ms; /* sum over the window's steps of each step's own device time
+                                  (event pair around its H2D, graph and D2H): the window's
+                                  device time minus the host-planning gaps between steps */
 } vc_sched_stats;
 
 int vc_run_scheduled(vc_engine* e, const int* slots, int n, const vc_sched_desc* sd,

@@ -74,7 +74,7 @@ class SchedStats(C.Structure):
                 ("h2d_ms", C.c_double), ("verify_wait_ms", C.c_double), ("mean_accept", C.c_double),
                 ("timed_iterations", C.c_int64), ("timed_tokens", C.c_int64),
                 ("timed_wall_ms", C.c_double), ("timed_device_ms", C.c_double),
-                ("timed_rows", C.c_double)]
+                ("timed_rows", C.c_double), ("timed_step_device_ms", C.c_double)]
 
 
 class RemoteDesc(C.Structure):

@@ -316,6 +316,7 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
     vc::check_cuda(cudaEventElapsedTime(&wms, win0, win1), "window event");
     st.timed_device_ms = wms;
     st.timed_rows = rows_in_window;
+    st.timed_step_device_ms = en.device_ms();  // reset when the window opened
   }
   st.h2d_ms = en.h2d_ms() - h2d_ms_at_window;
   st.h2d_bytes = en.h2d_bytes() - h2d_bytes_at_window;
