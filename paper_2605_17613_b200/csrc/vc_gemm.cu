@@ -308,16 +308,22 @@ gemm_umma_kernel(const uint16_t* __restrict__ Xt, int Mp, int M, int K,
         tmem_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&acc_empty[ab]);  // accumulator free for segment seg+2
-        __threadfence();
+        // the barrier orders every epilogue thread's partial stores before
+        // thread 0's gpu-scope fence (cumulative), which precedes its atomic;
+        // the finisher's fence after the atomic orders the other threads'
+        // partial loads (after the second barrier) behind it
         named_bar(1, 256);
         if (et == 0) {
+          __threadfence();
           const int prev = atomicAdd(ws.counters + tile, 1);
           s_last = prev == n_contrib - 1;
-          if (s_last) ws.counters[tile] = 0;  // self-reset for the next launch / graph replay
+          if (s_last) {
+            ws.counters[tile] = 0;  // self-reset for the next launch / graph replay
+            __threadfence();
+          }
         }
         named_bar(1, 256);
         if (!s_last) continue;
-        __threadfence();
       }
       // ---- epilogue, 16 tokens per staged pass ---------------------------------
       if constexpr (NT >= 32) {
