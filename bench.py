@@ -450,10 +450,22 @@ def main():
         # a step = one speculative round: x+1 scheduler iterations (every request
         # drafts x tokens and verifies once per round in steady state)
         it_w, it_k = (W + 2) * (x + 1), K * (x + 1)
-        ev = vc.Engine(shape, max_slots=B, max_ctx=ctx + it_w + it_k + 3 * (x + 1) + 8, max_x=x,
-                       quant_bits=0 if drop else args.bits, drop_ratio=drop, full_tier=tier,
-                       n_stage=args.stages if tier else 1,
-                       max_verify=args.stages if tier else max(2, B // (x + 1) + 2), device=local)
+        ev, err = None, None
+        try:
+            ev = vc.Engine(shape, max_slots=B, max_ctx=ctx + it_w + it_k + 3 * (x + 1) + 8, max_x=x,
+                           quant_bits=0 if drop else args.bits, drop_ratio=drop, full_tier=tier,
+                           n_stage=args.stages if tier else 1,
+                           max_verify=args.stages if tier else max(2, B // (x + 1) + 2), device=local)
+        except vc.VcError as ex:
+            err = ex
+        if dist:  # every rank falls back together (the pinned pool may fail on one rank only)
+            flag = torch.tensor([0 if err else 1], dtype=torch.int32, device=coll_dev)
+            dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+            if int(flag.item()) == 0 and err is None:
+                ev.close()
+                err = vc.VcError("engine allocation failed on another rank")
+        if err is not None:
+            raise err
         ev.init_weights(seed=0, std=0.02, resid_std=rs, q_std=qs)
         for i in range(B):
             ev.add_synthetic(i, ctx, first[i], seed=shard.seeds[i])
