@@ -270,12 +270,25 @@ def main_remote(args, rank, world, local):
     rs = args.resid_std if args.resid_std >= 0 else (0.0002 if not args.small else 0.0)
     qs = args.q_std if args.q_std >= 0 else (0.002 if not args.small else 0.0)
     slots = list(range(B))
-    e = vc.Engine(shape, max_slots=B, max_ctx=ctx + K + x + 72, max_x=x, quant_bits=bits, full_tier=0,
-                  max_verify=max(2, B // (x + 1) + 2), device=local)
-    e.init_weights(seed=0, std=0.02, resid_std=rs, q_std=qs)
-    e.add_synthetic(0, ctx, 0, seed=1)  # the shared prefix (same on every rank: one storage node)
-    meta = e.compress(0)
-    e.prefix_store(0)
+    e, err = None, None
+    try:
+        e = vc.Engine(shape, max_slots=B, max_ctx=ctx + K + x + 72, max_x=x, quant_bits=bits, full_tier=0,
+                      max_verify=max(2, B // (x + 1) + 2), device=local)
+        e.init_weights(seed=0, std=0.02, resid_std=rs, q_std=qs)
+        e.add_synthetic(0, ctx, 0, seed=1)  # the shared prefix (same on every rank: one storage node)
+        meta = e.compress(0)
+        e.prefix_store(0)  # pinned host store
+    except vc.VcError as ex:
+        err = ex
+    if dist:  # agree before any timed collective: a failure on one rank stops every rank
+        flag = torch.tensor([0 if err else 1], dtype=torch.int32, device=coll_dev)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN)
+        if int(flag.item()) == 0 and err is None:
+            err = vc.VcError("remote-prefix setup failed on another rank")
+    if err is not None:
+        if e is not None:
+            e.close()
+        raise err
     runs = {}
     launches = 0
     clk_summary = None
