@@ -215,6 +215,19 @@ def hbm_peak(peaks):
     return 6650.0, "fallback (B200_PROFILING.md)"
 
 
+def combine_lossless(identical: bool, compared: int, dist=None, device=None):
+    """Losslessness over the whole job: every rank's flag (MIN) and its
+    compared-token count (SUM), so rank 0's line covers every rank's requests."""
+    if dist is None or not dist.is_initialized() or dist.get_world_size() == 1:
+        return bool(identical), int(compared)
+    import torch
+    f = torch.tensor([1 if identical else 0], dtype=torch.int64, device=device)
+    c = torch.tensor([int(compared)], dtype=torch.int64, device=device)
+    dist.all_reduce(f, op=dist.ReduceOp.MIN)
+    dist.all_reduce(c)
+    return bool(f.item()), int(c.item())
+
+
 def draft_traffic(name="draft_attn_ncu.json"):
     """ncu --set full capture of the draft kernel (profiles/): DRAM bytes per launch."""
     f = os.path.join(ROOT, "profiles", name)
@@ -316,6 +329,8 @@ def main_remote(args, rank, world, local):
     _, (ka_ms,) = reduce_window(0.0, [ka_ms], dist, device=coll_dev)
     v, b = runs["vericache"], runs["full_kv"]
     identical = bool(np.array_equal(v["out"], b["out"]))
+    compared = int(v["out"].size)
+    identical, compared = combine_lossless(identical, compared, dist, coll_dev)
     value = v["tok"] / v["mk_s"]
     base_value = b["tok"] / b["mk_s"]
     st = v["st"]
@@ -355,7 +370,7 @@ def main_remote(args, rank, world, local):
             "full_kv": arm_summary(b), "vericache": arm_summary(v),
             "speedup_vs_full_kv": round(value / base_value, 3),
             "ttft_ratio_full_over_vericache": round(b["ttft"] / max(v["ttft"], 1e-9), 3),
-            "tokens_identical_to_full_kv": identical, "tokens_compared": int(v["out"].size),
+            "tokens_identical_to_full_kv": identical, "tokens_compared": compared,
             "roofline": {"kernel": f"draft_attn_quant_kernel (int{bits}, one launch per layer, {B} requests, "
                                    f"{ctx} ctx)", "bound": "hbm", "achieved": round(achieved, 1),
                          "peak": round(peak, 1), "unit": "GB/s", "frac": round(achieved / peak, 3),
@@ -506,6 +521,8 @@ def main():
         hist = [ev.history(i) for i in slots]
         cmp = [min(len(h), base_tok.shape[1]) for h in hist]
         identical = all(hist[i][:cmp[i]] == base_tok[i, :cmp[i]].tolist() for i in slots)
+        # every rank's requests count: MIN of the flags, SUM of the compared tokens
+        identical, n_cmp = combine_lossless(identical, int(sum(cmp)), dist, coll_dev)
         ev.close()
         del ev
         torch.cuda.empty_cache()
@@ -513,7 +530,7 @@ def main():
                                                  [st["timed_device_ms"] / 1e3, st["timed_wall_ms"] / 1e3],
                                                  dist, device=coll_dev)
         r = {"x": x, "window": window, "ramp": ramp, "st": st, "meta": meta, "ka": ka, "launches": launches,
-             "clocks": clk.summary(), "identical": identical, "compared": int(sum(cmp)),
+             "clocks": clk.summary(), "identical": identical, "compared": n_cmp,
              "tok": tok_all, "dev_s": dev_s, "wall_s": wall_s}
         return r
 

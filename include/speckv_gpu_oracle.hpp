@@ -9,13 +9,12 @@
 // request's committed tokens and open draft round:
 //   * drafter(prefix)  prefix == prompt ++ emitted ++ open drafts
 //                        -> one draft step over the COMPRESSED KV (vc_draft_step);
-//                      prefix extends emitted by the last round's accepted
-//                      tokens -> first commit that round (vc_accept_commit with
-//                      the cached verify predictions: exact KV append + rollback);
 //   * verifier(prefix) inside a round: the first call (k = 0) runs ONE verify
 //                      pass over the whole window against the FULL KV
 //                      (vc_verify, x+1 predictions) and caches it; call k
-//                      returns prediction k (specloop.cpp:24-35);
+//                      returns prediction k (specloop.cpp:24-35); the last
+//                      call (k = x) commits the round (vc_accept_commit: the
+//                      accept rule, exact KV append + rollback);
 //                      with no open round: a full-KV decode step
 //                      (vc_decode_step), i.e. autoregress.
 // It compiles against either the reference headers or include/speckv_b200.hpp
@@ -95,7 +94,6 @@ class SlotOracles {
     }
     std::int32_t draft(std::span<const std::int32_t> p) {
       bind(p);
-      if (!preds.empty() && !is(p, drafts.size())) commit_round();
       if (!is(p, drafts.size())) throw std::logic_error("gpu oracle: drafter prefix is not the request's state");
       std::int32_t t = 0;
       ok(vc_draft_step(e, &slot, 1, &t));
@@ -124,7 +122,12 @@ class SlotOracles {
         preds.resize(drafts.size() + 1);
         ok(vc_verify(e, &slot, 1, stage >= 0 ? &stage : nullptr, preds.data()));
       }
-      return preds[k];
+      const std::int32_t t = preds[k];
+      // the round's last prediction (k == x, specloop.cpp:30-33): the accept
+      // decision depends only on the cached predictions, so commit now -- the
+      // engine's KV, pending token and history match what run_speculative returns
+      if (k == drafts.size()) commit_round();
+      return t;
     }
   };
   std::shared_ptr<State> st_;

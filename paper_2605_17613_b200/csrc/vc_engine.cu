@@ -970,6 +970,13 @@ void Engine::commit_decode(int slot, int32_t next) {
   s.history.push_back(next);
 }
 
+void Engine::discard_drafts(int slot) {
+  // the draft window's rows (tail / drop tier) are simply overwritten later
+  SeqState& s = seqs_.at(slot);
+  s.drafted.clear();
+  s.draft_len = 0;
+}
+
 void Engine::push_draft(int slot, int32_t tok) {
   SeqState& s = seqs_.at(slot);
   s.drafted.push_back(tok);
@@ -992,6 +999,13 @@ std::vector<int32_t> Engine::accept_commit(int slot, const std::vector<int32_t>&
   const bool staged = cfg_.full_tier == 1;
   KvPool src = staged ? stage_ : full_;
   const int src_slot = staged ? stage : slot;
+  if (cfg_.quant_bits > 0 && !drop_mode()) {
+    // the bf16 tail holds the residual group + the next draft window; past
+    // max_ctx the quantised tier cannot take more groups (same bound as compress)
+    const int ng_now = std::min(now / VC_QGROUP, quant_.cap / VC_QGROUP);
+    if (now - ng_now * VC_QGROUP > tail_cap_ - cfg_.max_x - 1)
+      throw ContractViolation("accept: request exceeds max_ctx (compressed tail overflow)");
+  }
   if (staged) {
     if (stage < 0) throw ContractViolation("accept: staged verify needs its stage");
     // exact KV of the committed rows back to the host pool

@@ -122,6 +122,8 @@ class Engine {
   // Commit helpers (state only; kernels launched as needed).
   void commit_decode(int slot, int32_t next);
   void push_draft(int slot, int32_t tok);
+  // Roll back an open draft round without verifying it.
+  void discard_drafts(int slot);
   // Accept rule over the open round given the verifier's x+1 predictions;
   // commits exact KV, rolls back the draft window.  Returns emitted tokens.
   std::vector<int32_t> accept_commit(int slot, const std::vector<int32_t>& preds, int stage = -1);

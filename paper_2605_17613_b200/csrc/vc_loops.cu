@@ -304,6 +304,10 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
     ev = speckv::StepEvents{};
   }
   const auto t1 = std::chrono::steady_clock::now();
+  // a bounded window may end mid-round: land the in-flight reloads and roll
+  // the open draft rounds back, so the slots can be scheduled again
+  for (const Xfer& x : inflight) en.swap_wait(x.id);
+  for (int i = 0; i < n; ++i) en.discard_drafts(slots[i]);
   st.wall_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
   for (int i = 0; i < n; ++i) st.tokens += produced[i];
   if (st.iterations > sd.warmup_iterations) {
