@@ -167,8 +167,29 @@ int vc_request_state(vc_engine* e, int slot, vc_seq_state* out);
 int vc_request_history(vc_engine* e, int slot, int32_t* out, int cap, int* n);
 
 /* ---- compressor ---------------------------------------------------------- */
-/* Offline quant-uniform compress of the request's committed prefix.       */
+/* Mirrors speckv::CompressorSpec (compressor.hpp:24-41).  kind: 0 drop-uniform,
+ * 1 drop-window, 2 quant-uniform (the reference's three), 3 drop-topk (score-
+ * based top-k per (layer, head), BASELINE.json configs[2]).  mode: 0 offline
+ * (1 online goes through vc_update_window).                                 */
+typedef struct {
+  int kind;
+  int mode;
+  int bits;         /* quant-uniform width */
+  int window;       /* drop-window: recent tokens kept (online) */
+  int sink_tokens;  /* drop-window: leading tokens never dropped */
+} vc_compressor_spec;
+
+/* Offline compress of the request's committed prefix with the engine's own
+ * tier (quant bits / drop_ratio given at creation).                        */
 int vc_compress(vc_engine* e, int slot, vc_compressed_meta* out);
+/* speckv::compress(spec, shape, ratio, seed) (compressor.hpp:70-71) on the GPU
+ * tier: shape = the request's committed prefix (layers, n_kv, T, 4*d_head);
+ * drop-uniform / drop-window drop exactly the reference's indices for `seed`
+ * (compressor.cpp:152-177) and keep the rest in the drop tier; drop-topk keeps
+ * llround(ratio*T) by score; quant-uniform needs spec.bits == quant_bits.
+ * The spec must fit the engine's tier (ContractError otherwise).           */
+int vc_compress_spec(vc_engine* e, int slot, const vc_compressor_spec* spec, double ratio,
+                     uint64_t seed, vc_compressed_meta* out);
 /* Copy one (layer, kv-head) slice of the compressed tier to host:
  * kcodes/vcodes u32 words (fragment order), ksz [groups][d],
  * vsz [groups*128], ktail/vtail bf16 [tail_cap][d].  Any pointer may be NULL. */
@@ -198,6 +219,12 @@ int vc_topk_select(const float* scores, int rows, int T, int k, int32_t* kept, v
 /* Key-norm scores s_t = sum_c |k_tc| w_c for device bf16 keys [rows][T][d]. */
 int vc_key_scores(const uint16_t* keys, int rows, int T, int d, const float* w, float* scores,
                   void* stream);
+
+/* Greedy argmax of device fp32 logits [rows][n] into device out[rows]:
+ * std::max_element semantics of speckv::greedy_oracle (specloop.cpp:256-263) --
+ * ties -> smallest index; NaNs never win; a NaN at index 0, or a row with
+ * nothing above -inf, gives index 0.                                        */
+int vc_argmax_rows(const float* logits, int rows, int n, int32_t* out, void* stream);
 
 /* ---- steps ---------------------------------------------------------------- */
 /* One forward pass over a heterogeneous batch; out_rows receives the greedy

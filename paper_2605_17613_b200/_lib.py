@@ -51,6 +51,12 @@ class CompressedMeta(C.Structure):
                 ("retained_tokens", C.c_int64)]
 
 
+class CompressorSpec(C.Structure):
+    """vc_compressor_spec (speckv::CompressorSpec, compressor.hpp:24-41)."""
+    _fields_ = [("kind", C.c_int), ("mode", C.c_int), ("bits", C.c_int), ("window", C.c_int),
+                ("sink_tokens", C.c_int)]
+
+
 class SeqState(C.Structure):
     _fields_ = [("live", C.c_int), ("committed", C.c_int), ("pending", C.c_int),
                 ("n_groups", C.c_int), ("tail_committed", C.c_int), ("draft_len", C.c_int),
@@ -117,6 +123,7 @@ SIGNATURES = {
     "vc_request_state": (I, [P, I, C.POINTER(SeqState)]),
     "vc_request_history": (I, [P, I, PI32, I, PI]),
     "vc_compress": (I, [P, I, C.POINTER(CompressedMeta)]),
+    "vc_compress_spec": (I, [P, I, C.POINTER(CompressorSpec), D, U64, C.POINTER(CompressedMeta)]),
     "vc_compressed_read": (I, [P, I, I, I, PU32, PU32, PU32, PU32, PU16, PU16]),
     "vc_compressed_geometry": (I, [P, PI, PI, PI, PI]),
     "vc_drop_kept": (I, [P, I, I, C.POINTER(C.c_int32), I, PI]),
@@ -129,6 +136,7 @@ SIGNATURES = {
     "vc_update_window": (I, [I, I, I, I, PI64, PI64, PI64, PI64, PI64, I64, PI64]),
     "vc_topk_select": (I, [P, I, I, I, P, P]),
     "vc_key_scores": (I, [P, I, I, I, P, P, P]),
+    "vc_argmax_rows": (I, [P, I, I, P, P]),
     "vc_step": (I, [P, C.POINTER(StepItem), I, PI32, PF]),
     "vc_decode_step": (I, [P, PI, I, PI32]),
     "vc_draft_step": (I, [P, PI, I, PI32]),

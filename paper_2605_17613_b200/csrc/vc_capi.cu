@@ -248,10 +248,77 @@ int vc_request_history(vc_engine* e, int slot, int32_t* out, int cap, int* n) {
   });
 }
 
+namespace {
+void fill_meta(vc::Engine& en, int slot, vc_compressed_meta* out);
+}
+
 int vc_compress(vc_engine* e, int slot, vc_compressed_meta* out) {
   return guard([&] {
     vc::Engine& en = E(e);
     en.compress(slot);
+    fill_meta(en, slot, out);
+  });
+}
+
+// speckv::compress(spec, shape, ratio, seed) (compressor.hpp:70-71) on the
+// engine's compressed tier.  The engine's tier is fixed at creation (quant
+// bits or a drop tier sized for drop_ratio); the spec must fit it:
+//   quant-uniform  spec.bits == quant_bits (KIVI codes of every position);
+//   drop-uniform / drop-window  the reference's own drop indices
+//     (speckv::compress, compressor.cpp:152-177 -- bit-identical, seeded by
+//     `seed`), complemented to kept sets and gathered into the drop tier;
+//   drop-topk  keep llround(ratio*T) positions per (layer, head) by score.
+int vc_compress_spec(vc_engine* e, int slot, const vc_compressor_spec* cs, double ratio, uint64_t seed,
+                     vc_compressed_meta* out) {
+  return guard([&] {
+    vc::Engine& en = E(e);
+    if (!cs) throw vc::ContractViolation("compress: null spec");
+    const auto& cfg = en.config();
+    const auto& m = en.model();
+    if (cs->mode != 0) throw speckv::ConfigError("compress: online mode goes through vc_update_window");
+    if (cs->kind == 2) {  // quant-uniform
+      if (cs->bits < 1 || cs->bits > 16) throw speckv::ConfigError("compressor.bits out of [1,16]");
+      if (cfg.quant_bits == 0 || cs->bits != cfg.quant_bits)
+        throw vc::ContractViolation("compress: the engine's quantised tier has another bit width");
+      en.compress(slot);
+    } else if (cs->kind == 0 || cs->kind == 1 || cs->kind == 3) {
+      if (!en.drop_mode()) throw vc::ContractViolation("compress: token-dropping spec on an engine without a drop tier");
+      if (!(ratio > 0.0 && ratio < 1.0)) throw speckv::ConfigError("compress: ratio out of (0,1)");
+      const int T = en.seq(slot).committed;
+      if (cs->kind == 3) {
+        en.compress_as(slot, ratio, nullptr, 0);
+      } else {
+        speckv::CompressorSpec spec;
+        spec.kind = cs->kind == 0 ? speckv::CompressorKind::DropUniform : speckv::CompressorKind::DropWindow;
+        spec.ratio = ratio;
+        spec.window = cs->window > 0 ? cs->window : 8;
+        spec.sink_tokens = cs->sink_tokens;
+        speckv::KvShape shape{m.layers, m.n_kv, T, static_cast<speckv::Bytes>(m.d) * 2 * 2};
+        const speckv::CompressedKVMeta meta = speckv::compress(spec, shape, ratio, seed);
+        const int64_t k = meta.retained_tokens(shape, 0);
+        std::vector<int32_t> kept(static_cast<size_t>(m.layers) * m.n_kv * k);
+        std::vector<uint8_t> dropped(static_cast<size_t>(T));
+        for (int l = 0; l < m.layers; ++l)
+          for (int h = 0; h < m.n_kv; ++h) {
+            std::fill(dropped.begin(), dropped.end(), 0);
+            for (int64_t p : meta.dropped_indices[l][h]) dropped[static_cast<size_t>(p)] = 1;
+            int32_t* dst = kept.data() + (static_cast<size_t>(l) * m.n_kv + h) * k;
+            int64_t j = 0;
+            for (int t = 0; t < T; ++t)
+              if (!dropped[t]) dst[j++] = t;
+            if (j != k) throw vc::ContractViolation("compress: kept count differs from the shape law");
+          }
+        en.compress_as(slot, ratio, kept.data(), static_cast<int>(k));
+      }
+    } else {
+      throw speckv::ConfigError("compress: unknown compressor kind");
+    }
+    fill_meta(en, slot, out);
+  });
+}
+
+namespace {
+void fill_meta(vc::Engine& en, int slot, vc_compressed_meta* out) {
     const auto& m = en.model();
     const vc::SeqState& s = en.seq(slot);
     if (en.drop_mode()) {
@@ -283,8 +350,8 @@ int vc_compress(vc_engine* e, int slot, vc_compressed_meta* out) {
       out->tail_tokens = s.tail_committed;
       out->retained_tokens = s.committed;
     }
-  });
 }
+}  // namespace
 
 int vc_drop_kept(vc_engine* e, int layer, int head, int32_t* out, int cap, int* n) {
   return guard([&] {
@@ -411,6 +478,13 @@ int vc_key_scores(const uint16_t* keys, int rows, int T, int d, const float* w, 
   return guard([&] {
     vc::check_cuda(vc::key_scores(keys, rows, T, d, static_cast<size_t>(T) * d, w, scores,
                                   static_cast<cudaStream_t>(stream)), "key_scores");
+  });
+}
+
+int vc_argmax_rows(const float* logits, int rows, int n, int32_t* out, void* stream) {
+  return guard([&] {
+    if (rows < 1 || n < 1) throw speckv::ConfigError("argmax: empty logits");
+    vc::check_cuda(vc::argmax_rows(logits, rows, n, out, static_cast<cudaStream_t>(stream)), "argmax_rows");
   });
 }
 

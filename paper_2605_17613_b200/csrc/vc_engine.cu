@@ -271,6 +271,7 @@ void Engine::alloc_all() {
     max_chunks_x_ = (drop_.cap + VC_DENSE_CHUNK - 1) / VC_DENSE_CHUNK;
     score_buf_ = dmalloc<float>(static_cast<size_t>(L) * m.n_kv * cap);
     kept_buf_ = dmalloc<int32_t>(static_cast<size_t>(L) * m.n_kv * kmax);
+    kept_cap_ = kmax;
     score_w_ = dmalloc<float>(d);
     std::vector<float> ones(d, 1.0f);  // score = L1 norm of the (post-RoPE) key
     VC_CK(cudaMemcpy(score_w_, ones.data(), d * 4, cudaMemcpyHostToDevice));
@@ -550,7 +551,9 @@ void Engine::quantise_groups(int slot, int g0, int ng, const KvPool& src, int sr
   VC_CK(cudaStreamSynchronize(st_));
 }
 
-void Engine::compress(int slot) {
+void Engine::compress(int slot) { compress_as(slot, cfg_.drop_ratio, nullptr, 0); }
+
+void Engine::compress_as(int slot, double ratio, const int32_t* kept_host, int k_host) {
   if (cfg_.quant_bits == 0 && !drop_mode()) throw ContractViolation("compress: compressed tier disabled");
   SeqState& s = seqs_.at(slot);
   const auto& m = cfg_.model;
@@ -564,7 +567,7 @@ void Engine::compress(int slot) {
     src_slot = 0;
   }
   if (drop_mode()) {
-    compress_drop(slot, src, src_slot);
+    compress_drop(slot, src, src_slot, ratio, kept_host, k_host);
     return;
   }
   const int ng = std::min(s.committed / VC_QGROUP, quant_.cap / VC_QGROUP);
@@ -584,17 +587,26 @@ void Engine::compress(int slot) {
 // order into the drop tier.  Count rule and error of speckv::compress
 // (/root/reference/proj/src/compressor.cpp:152-158); equal count per head
 // within a layer (the shape law, :83-86) by construction.
-void Engine::compress_drop(int slot, const KvPool& src, int src_slot) {
+void Engine::compress_drop(int slot, const KvPool& src, int src_slot, double ratio, const int32_t* kept_host,
+                           int k_host) {
   SeqState& s = seqs_.at(slot);
   const auto& m = cfg_.model;
   const int n_slices = m.layers * m.n_kv;
   const int T = s.committed;
-  const long long k = std::llround(cfg_.drop_ratio * static_cast<double>(T));
+  const long long k = kept_host ? k_host : std::llround(ratio * static_cast<double>(T));
   if (k < 1) throw ContractViolation("compress: drop ratio retains < 1 token");
-  if (k + cfg_.max_x + 2 > drop_.cap) throw ContractViolation("compress: drop tier capacity exceeded");
-  const uint16_t* keys = src.k + static_cast<size_t>(src_slot) * n_slices * src.cap * m.d;
-  VC_LAUNCH(key_scores(keys, n_slices, T, m.d, static_cast<size_t>(src.cap) * m.d, score_w_, score_buf_, st_));
-  VC_LAUNCH(topk_select(score_buf_, n_slices, T, static_cast<int>(k), kept_buf_, st_));
+  if (k > kept_cap_ || k + cfg_.max_x + 2 > drop_.cap)
+    throw ContractViolation("compress: drop tier capacity exceeded (ratio above the engine's drop_ratio)");
+  if (kept_host) {
+    // the kept set is given (drop-uniform / drop-window: the reference's own
+    // drop indices, complemented on the host): [slice][k] ascending positions
+    VC_CK(cudaMemcpyAsync(kept_buf_, kept_host, static_cast<size_t>(n_slices) * k * sizeof(int32_t),
+                          cudaMemcpyHostToDevice, st_));
+  } else {
+    const uint16_t* keys = src.k + static_cast<size_t>(src_slot) * n_slices * src.cap * m.d;
+    VC_LAUNCH(key_scores(keys, n_slices, T, m.d, static_cast<size_t>(src.cap) * m.d, score_w_, score_buf_, st_));
+    VC_LAUNCH(topk_select(score_buf_, n_slices, T, static_cast<int>(k), kept_buf_, st_));
+  }
   VC_LAUNCH(gather_kept(src, src_slot, kept_buf_, static_cast<int>(k), drop_, slot, n_slices, m.d, st_));
   last_kept_k_ = static_cast<int>(k);
   s.drop_len = static_cast<int>(k);

@@ -113,6 +113,9 @@ class Engine {
 
   // Quantise the committed prefix into the compressed tier (offline compress).
   void compress(int slot);
+  // Same with an explicit retained ratio (drop tier, <= drop_ratio) or an
+  // explicit kept set kept_host [layers*n_kv][k_host] (ascending positions).
+  void compress_as(int slot, double ratio, const int32_t* kept_host, int k_host);
 
   // ---- steps ---------------------------------------------------------
   // Executes one forward over the items; writes argmax per input row into
@@ -196,7 +199,8 @@ class Engine {
   void enqueue_forward(int M, int n_draft, int n_dense1, int n_densev, int max_rows_v,
                        bool want_logits);
   void quantise_groups(int slot, int g0, int ng, const KvPool& src, int src_slot);
-  void compress_drop(int slot, const KvPool& src, int src_slot);
+  void compress_drop(int slot, const KvPool& src, int src_slot, double ratio, const int32_t* kept_host,
+                     int k_host);
 
   EngineConfig cfg_;
   int device_ = 0;
@@ -217,6 +221,7 @@ class Engine {
   float* score_w_ = nullptr;    // [d] per-channel score weights (ones)
   int32_t* kept_buf_ = nullptr; // [layers*n_kv][k] kept positions of the last compress
   int last_kept_k_ = 0;
+  int kept_cap_ = 0;            // kept positions per slice kept_buf_ holds
   uint16_t *host_k_ = nullptr, *host_v_ = nullptr;
   // prefix store (pinned): full K/V [slice][T][d], records [slice][ng][words], tails [slice][tc][d]
   uint16_t *pre_k_ = nullptr, *pre_v_ = nullptr, *pre_kt_ = nullptr, *pre_vt_ = nullptr;

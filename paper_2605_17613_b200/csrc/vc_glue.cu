@@ -101,6 +101,10 @@ __global__ void argmax_kernel(const float* logits, int N, int32_t* out) {
     int idx = si[0];
     for (int w = 1; w < static_cast<int>(blockDim.x >> 5); ++w)
       if (sv[w] > b || (sv[w] == b && si[w] < idx)) { b = sv[w]; idx = si[w]; }
+    // std::max_element semantics (specloop.cpp:260: `largest < *it` moves on):
+    // a NaN at index 0 is never replaced, later NaNs never win, and a row with
+    // nothing above -inf keeps index 0
+    if (idx == 0x7fffffff || isnan(row[0])) idx = 0;
     out[blockIdx.x] = idx;
   }
 }

@@ -216,6 +216,19 @@ class Engine:
         check(self.lib.vc_compress(self.h, slot, C.byref(m)))
         return {f: getattr(m, f) for f, _ in m._fields_}
 
+    COMPRESSOR_KINDS = {"drop-uniform": 0, "drop-window": 1, "quant-uniform": 2, "drop-topk": 3}
+
+    def compress_spec(self, slot, kind: str, ratio: float = 0.0, seed: int = 0, bits: int = 4,
+                      sink_tokens: int = 0, window: int = 8) -> dict:
+        """speckv::compress(spec, shape, ratio, seed) on this engine's GPU tier
+        (vc_compress_spec): drop-uniform / drop-window drop the reference's own
+        indices for `seed`; drop-topk keeps the top scores; quant-uniform needs
+        bits == the engine's quant_bits."""
+        cs = _lib.CompressorSpec(self.COMPRESSOR_KINDS[kind], 0, bits, window, sink_tokens)
+        m = _lib.CompressedMeta()
+        check(self.lib.vc_compress_spec(self.h, slot, C.byref(cs), float(ratio), seed, C.byref(m)))
+        return {f: getattr(m, f) for f, _ in m._fields_}
+
     def drop_kept(self, layer, head):
         """Kept positions (ascending) of one (layer, head) from the last drop-topk compress."""
         n = C.c_int()

@@ -44,7 +44,8 @@ def test_mode_exclusivity_and_ratio_are_config_errors():
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("Tn,k", [(3000, 1), (3000, 600), (3000, 3000), (4097, 819)])
+@pytest.mark.parametrize("Tn,k", [(3000, 1), (3000, 600), (3000, 3000), (4097, 819),
+                                  (32768, 6554), (131072, 26214)])  # configs[2]: 128K, c = 0.2
 def test_key_scores_and_topk_bit_exact(cuda, Tn, k):
     torch = cuda
     rng = np.random.default_rng(Tn + k)
@@ -52,6 +53,8 @@ def test_key_scores_and_topk_bit_exact(cuda, Tn, k):
     keys = T.f32_to_bf16(rng.standard_normal((rows, Tn, d)).astype(np.float32))
     keys[1, 100:400] = keys[1, 0]          # ties: equal scores, lower position wins
     keys[2, :] = keys[2, 7]                # a row of all-equal scores
+    if Tn > 10000:                         # long rows: ties straddling the k-th score
+        keys[0, Tn // 2: Tn // 2 + 5000] = keys[0, 3]
     w = rng.uniform(0.5, 1.5, d).astype(np.float32)
     lib = _lib.load()
     kd = torch.from_numpy(keys.view(np.int16)).cuda()

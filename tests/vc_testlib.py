@@ -237,11 +237,17 @@ def tiny_weights(shape, seed=7, std=0.02):
     qkv_n = (shape.n_q + 2 * shape.n_kv) * d
     off = [0]
 
+    o = oracle()
+    kf = np.float32(std / (65536.0 * np.sqrt(1.0 / 3.0)))
+
     def nrm(*dims):
+        # vco_fill_normal_bf16: the C twin of normal_bf16 (same values, fast
+        # enough for 8B-shape layers)
         n = int(np.prod(dims))
-        a = normal_bf16(seed, off[0], n, std).reshape(dims)
+        a = np.empty(n, np.uint16)
+        o.vco_fill_normal_bf16(seed, off[0], n, kf, ptr(a, C.c_uint16))
         off[0] += n
-        return a
+        return a.reshape(dims)
 
     ones = lambda n: np.full(n, 0x3F80, np.uint16)  # noqa: E731
     w = {"embed": nrm(V, H), "attn_norm": [], "wqkv": [], "wo": [], "mlp_norm": [], "wgate": [],
