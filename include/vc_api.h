@@ -276,6 +276,17 @@ typedef struct {
   int K;                    /* output tokens per request */
   int64_t warmup_iterations;  /* iterations before the timed window */
   int64_t timed_iterations;   /* length of the timed window; 0 = run to completion */
+  /* Per-request tier placement (the reference's B_c knob, intra_throughput /
+   * optimize_intra, analytics.cpp:45-82,130-150): tier 1 only.  The first
+   * n_resident requests keep their full KV resident in HBM for the whole run
+   * (each owns staging slot i: loaded once, never reloaded -- B_g = n_resident),
+   * the other n - n_resident are offloaded (B_c) and reloaded per verify
+   * through staging slots [n_resident, n_stage) under the swap scheduler.
+   * Every request drafts on its compressed KV.  Residents run x_resident-token
+   * rounds (0 = x), verify as soon as a round is drafted, staggered so about
+   * n_resident / (x_resident + 1) windows verify per iteration.              */
+  int n_resident;
+  int x_resident;
 } vc_sched_desc;
 
 typedef struct {
@@ -298,7 +309,61 @@ typedef struct {
   double timed_step_device_ms; /* sum over the window's steps of each step's own device time
                                   (event pair around its H2D, graph and D2H): the window's
                                   device time minus the host-planning gaps between steps */
+  int64_t resident_verifies;  /* verifies of resident requests (full KV in HBM) */
+  double resident_accept;     /* their accepted drafted tokens per verify */
+  int64_t timed_resident_tokens; /* tokens the residents emitted inside the timed window */
+  /* SimMetrics (sim.hpp:52-74) of the whole run on the loop's host clock:
+   * throughput = tokens / wall time, warm = first and last 10% of the run's
+   * time cut (sim.cpp:103-109), request latency percentiles (completion -
+   * start; rank ceil(q n), sim.cpp:92-99), interconnect busy = copy-engine time
+   * / wall time, peak HBM = weights + compressed tier + full-KV slots.     */
+  double throughput;
+  double warm_throughput;
+  double p50_latency_s;
+  double p99_latency_s;
+  double interconnect_busy;
+  int64_t peak_hbm_bytes;
 } vc_sched_stats;
+
+/* Reference metrics of a loop (SimMetrics, sim.hpp:52-74) on the engine:
+ * the clock is the sum of the steps' device times (CUDA events around each
+ * step), so time spent outside steps -- admission, host planning -- is not
+ * charged, exactly as the reference charges T_iter = bytes / BW per step. */
+typedef struct {
+  double throughput;        /* tokens / clock */
+  double warm_throughput;   /* first and last 10% of the clock cut (sim.cpp:103-109) */
+  double p50_latency_s;     /* completion - arrival on that clock (sim.cpp:92-99) */
+  double p99_latency_s;
+  int64_t tokens;
+  int64_t iterations;
+  int64_t completed;
+  int64_t unserved;         /* requests that can never fit (sim.cpp:438-440) */
+  double clock_s;           /* sum of step device times */
+  double wall_ms;           /* host wall time of the loop */
+  double mean_batch;        /* requests per decode step */
+  int max_batch;
+  int64_t peak_hbm_bytes;   /* weights + resident full KV at the peak */
+  double full_batch_throughput; /* tokens / clock over the steps that ran with every
+                                   slot occupied: the capacity-capped steady state */
+} vc_loop_metrics;
+
+/* One request of a synthetic workload: prefix length, first input token,
+ * prefix-KV seed (vc_request_add_synthetic), arrival time (ms on the loop clock). */
+typedef struct {
+  int n_ctx;
+  int32_t first_token;
+  uint64_t seed;
+  double arrival_ms;
+} vc_request_desc;
+
+/* The reference's full-KV baseline (baseline_full_kv, sim.cpp:418-494) on the
+ * real engine: requests are admitted FIFO while a full-KV slot is free (the
+ * engine's max_slots full-KV slots ARE its HBM capacity: weights + resident +
+ * KV <= gpu_mem, sim.cpp:455-461), each decodes K tokens, one per step, and
+ * leaves.  Admission (synthesising the prefix KV) is not on the clock.
+ * out [n][K].                                                               */
+int vc_run_decode_fifo(vc_engine* e, const vc_request_desc* reqs, int n, int K, int32_t* out,
+                       vc_loop_metrics* m);
 
 int vc_run_scheduled(vc_engine* e, const int* slots, int n, const vc_sched_desc* sd,
                      int32_t* out, vc_sched_stats* stats);

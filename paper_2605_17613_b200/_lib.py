@@ -71,7 +71,8 @@ class StepItem(C.Structure):
 class SchedDesc(C.Structure):
     _fields_ = [("x", C.c_int), ("window", C.c_int), ("iteration_time", C.c_double),
                 ("link_bandwidth", C.c_double), ("hbm_capacity", C.c_int64), ("K", C.c_int),
-                ("warmup_iterations", C.c_int64), ("timed_iterations", C.c_int64)]
+                ("warmup_iterations", C.c_int64), ("timed_iterations", C.c_int64),
+                ("n_resident", C.c_int), ("x_resident", C.c_int)]
 
 
 class SchedStats(C.Structure):
@@ -80,7 +81,24 @@ class SchedStats(C.Structure):
                 ("h2d_ms", C.c_double), ("verify_wait_ms", C.c_double), ("mean_accept", C.c_double),
                 ("timed_iterations", C.c_int64), ("timed_tokens", C.c_int64),
                 ("timed_wall_ms", C.c_double), ("timed_device_ms", C.c_double),
-                ("timed_rows", C.c_double), ("timed_step_device_ms", C.c_double)]
+                ("timed_rows", C.c_double), ("timed_step_device_ms", C.c_double),
+                ("resident_verifies", C.c_int64), ("resident_accept", C.c_double),
+                ("timed_resident_tokens", C.c_int64), ("throughput", C.c_double),
+                ("warm_throughput", C.c_double), ("p50_latency_s", C.c_double), ("p99_latency_s", C.c_double),
+                ("interconnect_busy", C.c_double), ("peak_hbm_bytes", C.c_int64)]
+
+
+class LoopMetrics(C.Structure):
+    """vc_loop_metrics (SimMetrics, sim.hpp:52-74)."""
+    _fields_ = [("throughput", C.c_double), ("warm_throughput", C.c_double), ("p50_latency_s", C.c_double),
+                ("p99_latency_s", C.c_double), ("tokens", C.c_int64), ("iterations", C.c_int64),
+                ("completed", C.c_int64), ("unserved", C.c_int64), ("clock_s", C.c_double),
+                ("wall_ms", C.c_double), ("mean_batch", C.c_double), ("max_batch", C.c_int),
+                ("peak_hbm_bytes", C.c_int64), ("full_batch_throughput", C.c_double)]
+
+
+class RequestDesc(C.Structure):
+    _fields_ = [("n_ctx", C.c_int), ("first_token", C.c_int32), ("seed", C.c_uint64), ("arrival_ms", C.c_double)]
 
 
 class RemoteDesc(C.Structure):
@@ -152,6 +170,7 @@ SIGNATURES = {
     "vc_prefix_store": (I, [P, I]),
     "vc_prefix_load": (I, [P, I, I, C.c_int32, PU64]),
     "vc_run_remote_prefix": (I, [P, PI, I, C.POINTER(RemoteDesc), PI32, C.POINTER(RemoteStats)]),
+    "vc_run_decode_fifo": (I, [P, C.POINTER(RequestDesc), I, I, PI32, C.POINTER(LoopMetrics)]),
     "vc_reload_span": (I, [I64, D, D, PD, PI]),
     "vc_quant_kivi_slice": (I, [P, P, I, I, I, P, P, P, P, P]),
     "vc_attention_probe": (I, [P, I, I, I, P, I, I, PU16]),

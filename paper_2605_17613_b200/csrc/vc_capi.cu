@@ -22,6 +22,8 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
                           int32_t* out, vc_sched_stats* stats);
 int vc_run_remote_prefix_impl(vc::Engine& en, const int* slots, int n, const vc_remote_desc& rd,
                               int32_t* out, vc_remote_stats* stats);
+int vc_run_decode_fifo_impl(vc::Engine& en, const vc_request_desc* reqs, int n, int K, int32_t* out,
+                            vc_loop_metrics* m);
 
 namespace {
 
@@ -761,6 +763,11 @@ int vc_run_scheduled(vc_engine* e, const int* slots, int n, const vc_sched_desc*
     if (!sd) throw vc::ContractViolation("vc_run_scheduled: null descriptor");
     vc_run_scheduled_impl(E(e), slots, n, *sd, out, stats);
   });
+}
+
+int vc_run_decode_fifo(vc_engine* e, const vc_request_desc* reqs, int n, int K, int32_t* out,
+                       vc_loop_metrics* m) {
+  return guard([&] { vc_run_decode_fifo_impl(E(e), reqs, n, K, out, m); });
 }
 
 int vc_reload_span(int64_t bytes, double bandwidth, double iteration_time, double* iterations,

@@ -55,6 +55,15 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
   const bool staged = cfgE.full_tier == 1;
   if (sd.x < 1 || sd.x > cfgE.max_x) throw speckv::ConfigError("scheduled: x out of [1, max_x]");
   if (cfgE.quant_bits == 0 && cfgE.drop_ratio <= 0.0) throw vc::ContractViolation("scheduled: needs a compressed tier");
+  // per-request tier placement: requests [0, n_res) resident (B_g), the rest offloaded (B_c)
+  const int n_res = sd.n_resident;
+  const int n_off = n - n_res;
+  const int x_res = sd.x_resident > 0 ? sd.x_resident : sd.x;
+  if (n_res < 0 || n_res > n) throw speckv::ConfigError("scheduled: n_resident out of [0, n]");
+  if (n_res > 0 && !staged) throw speckv::ConfigError("scheduled: n_resident needs the host tier (full_tier 1)");
+  if (x_res > cfgE.max_x) throw speckv::ConfigError("scheduled: x_resident out of [1, max_x]");
+  if (staged && n_res + (n_off > 0 ? 1 : 0) > cfgE.n_stage)
+    throw speckv::ConfigError("scheduled: n_resident + 1 rotating staging slot exceed n_stage");
   const size_t bpt = en.full_kv_bytes_per_token();
 
   // ---- measure T_iter if not given: one draft step over every request ----
@@ -82,30 +91,32 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
   cfg.hardware.local_gpus = 1;
   cfg.model.weights_bytes = static_cast<speckv::Bytes>(en.weight_bytes());
   cfg.model.kv_bytes_per_token = static_cast<speckv::Bytes>(bpt);
-  speckv::Bytes kv_max = 0, resident_total = 0;
+  speckv::Bytes kv_max = 0, resident_total = 0, compressed_all = 0;
   std::vector<double> ratio(n);
   for (int i = 0; i < n; ++i) {
     const auto& s = en.seq(slots[i]);
     const speckv::Bytes kv = static_cast<speckv::Bytes>(s.committed) * bpt;
     kv_max = std::max(kv_max, kv);
     ratio[i] = std::min(1.0, static_cast<double>(en.compressed_bytes(slots[i])) / static_cast<double>(kv));
-    resident_total += static_cast<speckv::Bytes>(std::ceil(ratio[i] * kv));
+    compressed_all += static_cast<speckv::Bytes>(en.compressed_bytes(slots[i]));
+    if (i >= n_res) resident_total += static_cast<speckv::Bytes>(std::ceil(ratio[i] * kv));
   }
   // HBM ring capacity: weights + resident compressed caches + one full KV per
-  // staging slot, so the ring never books more reloads than we can stage.
-  const int n_stage = staged ? cfgE.n_stage : std::max(1, cfgE.max_verify);
+  // rotating staging slot, so the ring never books more reloads than we can
+  // stage.  Resident requests' full KV is a fixed carve-out outside the ring.
+  const int n_stage = staged ? cfgE.n_stage - n_res : std::max(1, cfgE.max_verify);
   cfg.hardware.gpu_mem = sd.hbm_capacity > 0
                              ? sd.hbm_capacity
-                             : cfg.model.weights_bytes + resident_total + n_stage * (kv_max + kv_max / 64);
+                             : cfg.model.weights_bytes + resident_total + std::max(1, n_stage) * (kv_max + kv_max / 64);
   cfg.acceptance.kind = speckv::AcceptanceModel::Kind::PerTokenIid;
   for (double c : ratio) cfg.acceptance.per_token_prob[c] = 0.99;
   cfg.draft_length = sd.x;
   cfg.lookahead_window = sd.window;
   cfg.iteration_time_mode = speckv::IterationTimeMode::Fixed;
   cfg.iteration_time = t_iter;
-  cfg.batch_size = n;
+  cfg.batch_size = std::max(1, n_off);
   cfg.kv_full_bytes = kv_max;
-  cfg.compression_ratio = ratio[0];
+  cfg.compression_ratio = ratio[n_off > 0 ? n_res : 0];
   cfg.output_tokens = sd.K;
   cfg.validate();
 
@@ -122,7 +133,7 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
   }();
   sched.set_expedite(expedite && staged);
   speckv::StepEvents ev;
-  for (int i = 0; i < n; ++i) {
+  for (int i = n_res; i < n; ++i) {
     speckv::Request r;
     r.id = i;
     r.kv_full_bytes = static_cast<speckv::Bytes>(en.seq(slots[i]).committed) * bpt;
@@ -134,7 +145,33 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
   std::vector<int> produced(n, 0);
   std::vector<int> stage_of(n, -1);
   std::vector<int> free_stages;
-  for (int s = n_stage - 1; s >= 0; --s) free_stages.push_back(s);
+  for (int s = (staged ? cfgE.n_stage : n_stage) - 1; s >= n_res; --s) free_stages.push_back(s);
+  // residents: full KV loaded once into their own staging slot (placement,
+  // not part of the serving loop); first rounds of x_res - (i mod (x_res+1))
+  // drafts stagger their verifies over the x_res + 1 iterations of a round
+  std::vector<int> round_x(n, 0);
+  for (int i = 0; i < n_res; ++i) {
+    stage_of[i] = i;
+    en.swap_wait(en.swap_begin(slots[i], i));
+    round_x[i] = x_res - (i % (x_res + 1));
+  }
+  int64_t res_verifies = 0;
+  double res_accepted = 0;
+  int64_t res_tokens_at_window = 0;
+  auto res_tokens = [&] {
+    int64_t t = 0;
+    for (int i = 0; i < n_res; ++i) t += produced[i];
+    return t;
+  };
+  auto residents_active = [&] {
+    for (int i = 0; i < n_res; ++i)
+      if (produced[i] < sd.K) return true;
+    return false;
+  };
+  // reference metrics on the loop's host clock (sim.cpp:80-109)
+  std::vector<std::pair<double, double>> emission;  // (seconds, tokens)
+  std::vector<double> done_at(n, -1.0);
+  const double h2d_ms_start = en.h2d_ms();
   struct Xfer {
     uint64_t id;
     speckv::ReservationId res;
@@ -168,13 +205,14 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
   const bool adapt = sd.iteration_time <= 0;
   double stall_ms = 0.0, h2d_ms_at_window = 0.0, h2d_bytes_at_window = 0.0;
   auto t_prev = std::chrono::steady_clock::now();
-  for (std::int64_t it = 0; !sched.idle() || !ev.arrivals.empty(); ++it) {
+  for (std::int64_t it = 0; !sched.idle() || !ev.arrivals.empty() || residents_active(); ++it) {
     if (it > guard_iters) throw speckv::ConfigError("scheduled loop stalled");
     if (adapt) sched.set_planning_iteration_time(t_plan);
     if (it == sd.warmup_iterations) {  // open the timed window
       int64_t tk = 0;
       for (int i = 0; i < n; ++i) tk += produced[i];
       tokens_at_window = tk;
+      res_tokens_at_window = res_tokens();
       en.reset_timing();
       window_start = std::chrono::steady_clock::now();
       vc::check_cuda(cudaEventRecord(win0, en.stream()), "window event");
@@ -242,6 +280,21 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
       t.tokens = {s.drafted.empty() ? s.pending : s.drafted.back()};
       items.push_back(std::move(t));
     }
+    // resident requests: draft their round, then verify against their own
+    // HBM-resident full KV (no reload)
+    std::vector<int> res_drafting, res_verifying;
+    for (int i = 0; i < n_res; ++i) {
+      if (produced[i] >= sd.K) continue;
+      const auto& s = en.seq(slots[i]);
+      if (static_cast<int>(s.drafted.size()) < round_x[i]) {
+        vc::StepItem t;
+        t.slot = slots[i];
+        t.mode = vc::RowMode::Draft;
+        t.tokens = {s.drafted.empty() ? s.pending : s.drafted.back()};
+        items.push_back(std::move(t));
+        res_drafting.push_back(i);
+      }
+    }
     std::vector<int> verifying;
     for (const auto& v : pr.verifies) {
       const int req = static_cast<int>(v.request);
@@ -257,11 +310,28 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
       items.push_back(std::move(t));
       verifying.push_back(req);
     }
+    for (int i = 0; i < n_res; ++i) {
+      if (produced[i] >= sd.K) continue;
+      const auto& s = en.seq(slots[i]);
+      if (static_cast<int>(s.drafted.size()) == round_x[i]) {
+        vc::StepItem t;
+        t.slot = slots[i];
+        t.mode = vc::RowMode::Verify;
+        t.stage = i;
+        t.tokens.push_back(s.pending);
+        t.tokens.insert(t.tokens.end(), s.drafted.begin(), s.drafted.end());
+        items.push_back(std::move(t));
+        res_verifying.push_back(i);
+      }
+    }
     std::vector<int32_t> row;
     if (!items.empty()) en.run_step(items, row);
     if (it >= sd.warmup_iterations) rows_in_window += static_cast<double>(row.size());
+    const double t_emit = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    double emitted_now = 0;
     size_t off = 0;
     for (speckv::RequestId id : pr.drafted) en.push_draft(slots[id], row[off++]);
+    for (int i : res_drafting) en.push_draft(slots[i], row[off++]);
     meas.accepted.clear();
     for (int req : verifying) {
       const int x_r = static_cast<int>(en.seq(slots[req]).drafted.size());
@@ -271,12 +341,32 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
       meas.accepted.push_back(static_cast<int>(em.size()) - 1);
       accepted_sum += static_cast<double>(em.size()) - 1;
       for (int32_t t : em)
-        if (produced[req] < sd.K) out[static_cast<size_t>(req) * sd.K + produced[req]++] = t;
+        if (produced[req] < sd.K) {
+          out[static_cast<size_t>(req) * sd.K + produced[req]++] = t;
+          emitted_now += 1;
+        }
+      if (produced[req] >= sd.K && done_at[req] < 0) done_at[req] = t_emit;
       if (staged) {
         free_stages.push_back(stage_of[req]);
         stage_of[req] = -1;
       }
     }
+    for (int i : res_verifying) {
+      const int x_r = static_cast<int>(en.seq(slots[i]).drafted.size());
+      std::vector<int32_t> p(row.begin() + off, row.begin() + off + x_r + 1);
+      off += x_r + 1;
+      const auto em = en.accept_commit(slots[i], p, i);
+      res_verifies += 1;
+      res_accepted += static_cast<double>(em.size()) - 1;
+      for (int32_t t : em)
+        if (produced[i] < sd.K) {
+          out[static_cast<size_t>(i) * sd.K + produced[i]++] = t;
+          emitted_now += 1;
+        }
+      if (produced[i] >= sd.K && done_at[i] < 0) done_at[i] = t_emit;
+      round_x[i] = x_res;
+    }
+    if (emitted_now > 0) emission.emplace_back(t_emit, emitted_now);
     // 5. the real step with measured accept counts
     const speckv::StepResult rr = sched.execution_step(ev);
     if (rr.drafted != pr.drafted || rr.verify_count != pr.verify_count)
@@ -309,10 +399,41 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
   for (const Xfer& x : inflight) en.swap_wait(x.id);
   for (int i = 0; i < n; ++i) en.discard_drafts(slots[i]);
   st.wall_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+  {  // SimMetrics on the host clock (finalize_metrics, sim.cpp:98-109)
+    const double end = st.wall_ms / 1e3;
+    double total = 0, warm = 0;
+    for (const auto& [t, k] : emission) {
+      total += k;
+      if (t >= 0.1 * end && t <= 0.9 * end) warm += k;
+    }
+    st.throughput = end > 0 ? total / end : 0.0;
+    st.warm_throughput = end > 0 ? warm / (0.8 * end) : 0.0;
+    std::vector<double> lat;
+    for (double d : done_at)
+      if (d >= 0) lat.push_back(d);
+    auto pct = [&](double q) {
+      if (lat.empty()) return 0.0;
+      std::sort(lat.begin(), lat.end());
+      size_t r = static_cast<size_t>(std::ceil(q * static_cast<double>(lat.size())));
+      r = std::min(std::max<size_t>(r, 1), lat.size());
+      return lat[r - 1];
+    };
+    st.p50_latency_s = pct(0.5);
+    st.p99_latency_s = pct(0.99);
+    st.interconnect_busy = end > 0 ? (en.h2d_ms() - h2d_ms_start) / 1e3 / end : 0.0;
+    const int64_t slot_bytes = static_cast<int64_t>(en.full_pool().cap) * static_cast<int64_t>(bpt);
+    st.peak_hbm_bytes = static_cast<int64_t>(en.weight_bytes()) + compressed_all +
+                        (staged ? static_cast<int64_t>(cfgE.n_stage) : static_cast<int64_t>(n)) * slot_bytes;
+  }
+  st.verifies += res_verifies;  // mean_accept below covers both tiers
+  accepted_sum += res_accepted;
+  st.resident_verifies = res_verifies;
+  st.resident_accept = res_verifies ? res_accepted / static_cast<double>(res_verifies) : 0.0;
   for (int i = 0; i < n; ++i) st.tokens += produced[i];
   if (st.iterations > sd.warmup_iterations) {
     st.timed_iterations = st.iterations - sd.warmup_iterations;
     st.timed_tokens = st.tokens - tokens_at_window;
+    st.timed_resident_tokens = res_tokens() - res_tokens_at_window;
     st.timed_wall_ms = std::chrono::duration<double, std::milli>(t1 - window_start).count();
     vc::check_cuda(cudaEventRecord(win1, en.stream()), "window event");
     vc::check_cuda(cudaEventSynchronize(win1), "window event");
@@ -543,5 +664,124 @@ int vc_run_remote_prefix_impl(vc::Engine& en, const int* slots, int n, const vc_
   st.h2d_bytes = en.h2d_bytes() - h2d_b0;
   st.h2d_ms = en.h2d_ms() - h2d_ms0;
   if (stats) *stats = st;
+  return VC_OK;
+}
+
+// ---------------------------------------------------------------------------
+// vc_run_decode_fifo: the reference's full-KV baseline (baseline_full_kv,
+// /root/reference/proj/src/sim.cpp:418-494) on real kernels.  Requests are
+// admitted FIFO (arrival order) while a full-KV slot is free -- the engine's
+// max_slots HBM slots are its capacity (weights + resident + KV <= gpu_mem,
+// :455-461) -- decode one token per step (:475-486) and leave after K.  The
+// clock is the sum of the steps' device times, as the reference's clock is
+// the sum of T_iter = (weights + resident) / BW per step (:471); admission
+// (writing the request's prefix KV) is free in the reference and is not on
+// the clock here either.
+int vc_run_decode_fifo_impl(vc::Engine& en, const vc_request_desc* reqs, int n, int K, int32_t* out,
+                            vc_loop_metrics* m) {
+  const auto& cfgE = en.config();
+  if (cfgE.full_tier != 0) throw speckv::ConfigError("fifo decode: needs the HBM full tier");
+  if (n < 1 || K < 1) throw speckv::ConfigError("fifo decode: n and K must be >= 1");
+  if (!reqs || !out) throw vc::ContractViolation("fifo decode: null workload");
+  vc_loop_metrics st{};
+  std::vector<int> order(n);
+  for (int i = 0; i < n; ++i) order[i] = i;
+  std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return reqs[a].arrival_ms < reqs[b].arrival_ms; });
+  const int cap_tokens = en.full_pool().cap;
+  std::deque<int> waiting;
+  size_t next = 0;
+  std::vector<int> free_slots;
+  for (int s = cfgE.max_slots - 1; s >= 0; --s) free_slots.push_back(s);
+  struct Active {
+    int req, slot, produced;
+  };
+  std::vector<Active> active;
+  std::vector<std::pair<double, double>> emission;
+  std::vector<double> latency;
+  double clock = 0.0;  // seconds of step device time
+  const size_t slot_bytes = static_cast<size_t>(cap_tokens) * en.full_kv_bytes_per_token();
+  double batch_sum = 0, full_tokens = 0, full_clock = 0;
+  const auto w0 = std::chrono::steady_clock::now();
+  std::vector<int32_t> row;
+  while (next < order.size() || !waiting.empty() || !active.empty()) {
+    while (next < order.size() && reqs[order[next]].arrival_ms <= clock * 1e3 + 1e-9) {
+      const int r = order[next++];
+      if (reqs[r].n_ctx + K + cfgE.max_x + 2 > cap_tokens) {  // can never fit (sim.cpp:438-440)
+        st.unserved += 1;
+        continue;
+      }
+      waiting.push_back(r);
+    }
+    while (!waiting.empty() && !free_slots.empty()) {  // FIFO admission
+      const int r = waiting.front();
+      waiting.pop_front();
+      const int s = free_slots.back();
+      free_slots.pop_back();
+      en.add_request_synthetic(s, reqs[r].n_ctx, reqs[r].first_token, reqs[r].seed, 4, 10.f);
+      active.push_back({r, s, 0});
+    }
+    if (active.empty()) {
+      if (next < order.size()) {
+        clock = std::max(clock, reqs[order[next]].arrival_ms / 1e3);
+        continue;
+      }
+      break;
+    }
+    st.max_batch = std::max<int>(st.max_batch, static_cast<int>(active.size()));
+    st.peak_hbm_bytes = std::max<int64_t>(st.peak_hbm_bytes, static_cast<int64_t>(en.weight_bytes() +
+                                                                                  active.size() * slot_bytes));
+    std::vector<vc::StepItem> its(active.size());
+    for (size_t i = 0; i < active.size(); ++i) {
+      its[i].slot = active[i].slot;
+      its[i].mode = vc::RowMode::Decode;
+      its[i].tokens = {en.seq(active[i].slot).pending};
+    }
+    const double before = en.device_ms();
+    en.run_step(its, row);
+    const double dt = (en.device_ms() - before) / 1e3;
+    clock += dt;
+    if (static_cast<int>(active.size()) == cfgE.max_slots) {
+      full_tokens += static_cast<double>(active.size());
+      full_clock += dt;
+    }
+    st.iterations += 1;
+    batch_sum += static_cast<double>(active.size());
+    std::vector<Active> still;
+    for (size_t i = 0; i < active.size(); ++i) {
+      Active a = active[i];
+      en.commit_decode(a.slot, row[i]);
+      out[static_cast<size_t>(a.req) * K + a.produced++] = row[i];
+      if (a.produced == K) {
+        latency.push_back(clock - reqs[a.req].arrival_ms / 1e3);
+        st.completed += 1;
+        en.release(a.slot);
+        free_slots.push_back(a.slot);
+      } else {
+        still.push_back(a);
+      }
+    }
+    emission.emplace_back(clock, static_cast<double>(active.size()));
+    st.tokens += static_cast<int64_t>(active.size());
+    active.swap(still);
+  }
+  st.clock_s = clock;
+  st.wall_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - w0).count();
+  st.mean_batch = st.iterations ? batch_sum / static_cast<double>(st.iterations) : 0.0;
+  st.throughput = clock > 0 ? static_cast<double>(st.tokens) / clock : 0.0;
+  double warm = 0;
+  for (const auto& [t, k] : emission)
+    if (t >= 0.1 * clock && t <= 0.9 * clock) warm += k;
+  st.warm_throughput = clock > 0 ? warm / (0.8 * clock) : 0.0;
+  std::sort(latency.begin(), latency.end());
+  auto pct = [&](double q) {
+    if (latency.empty()) return 0.0;
+    size_t r = static_cast<size_t>(std::ceil(q * static_cast<double>(latency.size())));
+    r = std::min(std::max<size_t>(r, 1), latency.size());
+    return latency[r - 1];
+  };
+  st.p50_latency_s = pct(0.5);
+  st.p99_latency_s = pct(0.99);
+  st.full_batch_throughput = full_clock > 0 ? full_tokens / full_clock : 0.0;
+  if (m) *m = st;
   return VC_OK;
 }

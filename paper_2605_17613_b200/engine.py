@@ -362,15 +362,28 @@ class Engine:
         return ms.value, b.value
 
     def run_scheduled(self, slots, K, x, window, iteration_time=0.0, link_bandwidth=0.0,
-                      hbm_capacity=0, warmup_iterations=0, timed_iterations=0):
+                      hbm_capacity=0, warmup_iterations=0, timed_iterations=0, n_resident=0, x_resident=0):
+        """n_resident > 0 (host tier): the first n_resident slots keep their full
+        KV resident in HBM (the reference's B_g = B - B_c; analytics.cpp:45-82)."""
         s = np.ascontiguousarray(slots, np.int32)
         out = np.zeros((s.size, K), np.int32)
         sd = _lib.SchedDesc(x, window, iteration_time, link_bandwidth, hbm_capacity, K,
-                            warmup_iterations, timed_iterations)
+                            warmup_iterations, timed_iterations, n_resident, x_resident)
         st = _lib.SchedStats()
         check(self.lib.vc_run_scheduled(self.h, _ptr(s, C.c_int), s.size, C.byref(sd),
                                         _ptr(out, C.c_int32), C.byref(st)))
         return out, {f: getattr(st, f) for f, _ in st._fields_}
+
+    def run_decode_fifo(self, requests, K):
+        """baseline_full_kv (sim.cpp:418-494): requests = [(n_ctx, first_token,
+        seed, arrival_ms)], admitted FIFO while a full-KV slot is free ->
+        (tokens [n][K], SimMetrics dict)."""
+        n = len(requests)
+        arr = (_lib.RequestDesc * n)(*[_lib.RequestDesc(int(a), int(b), int(c), float(d)) for a, b, c, d in requests])
+        out = np.zeros((n, K), np.int32)
+        m = _lib.LoopMetrics()
+        check(self.lib.vc_run_decode_fifo(self.h, arr, n, K, _ptr(out, C.c_int32), C.byref(m)))
+        return out, {f: getattr(m, f) for f, _ in m._fields_}
 
     # ---- remote prefix (configs[3]) --------------------------------------------
     def prefix_store(self, slot):

@@ -21,9 +21,10 @@ SHAPES = {
 }
 
 
-def _tol_check(got, want, rel=2e-2, abs_=2e-3):
+def _tol_check(got, want, rel=2e-2, abs_=2e-3, name="attention"):
     err = np.abs(got - want).max()
     bound = rel * np.abs(want).max() + abs_
+    print(f"MEASURED {name}: max_abs {err:.3e} rel {err / np.abs(want).max():.3e} bound {bound:.3e}")
     assert err <= bound, f"max err {err:.3e} > bound {bound:.3e}"
 
 
@@ -66,7 +67,7 @@ def test_draft_attention(cuda, name, n_ctx, bits):
             vv[ng * G:] = T.bf16_to_f32(v[layer, h, ng * G:])
             qf = T.bf16_to_f32(q[0, h * rep:(h + 1) * rep])
             want = _oracle_attn(np.ascontiguousarray(qf), kk, vv)
-            _tol_check(got[h * rep:(h + 1) * rep], want)
+            _tol_check(got[h * rep:(h + 1) * rep], want, name=f"draft {name} T={n_ctx} int{bits}")
     e.close()
 
 
@@ -90,7 +91,7 @@ def test_dense_attention(cuda, name, n_ctx, n_rows):
             qf = T.bf16_to_f32(q[:, h * rep:(h + 1) * rep]).reshape(n_rows * rep, s.d_head)
             lim = np.repeat(np.arange(n_rows) + n_ctx - n_rows + 1, rep)
             want = _oracle_attn(np.ascontiguousarray(qf), kk, vv, lim).reshape(n_rows, rep, s.d_head)
-            _tol_check(got[:, h * rep:(h + 1) * rep], want)
+            _tol_check(got[:, h * rep:(h + 1) * rep], want, name=f"dense {name} T={n_ctx} rows={n_rows}")
     e.close()
 
 

@@ -25,6 +25,12 @@ def _bound(ref):
     return REL * np.abs(ref).max() + ABS
 
 
+def _report(name, got, want):
+    err = float(np.abs(got - want).max())
+    print(f"MEASURED {name}: max_abs {err:.3e} rel {err / float(np.abs(want).max()):.3e} bound {_bound(want):.3e}")
+    return err
+
+
 @pytest.fixture(scope="module")
 def setup(cuda):
     w = T.tiny_weights(TINY, seed=7, std=0.02)
@@ -46,7 +52,7 @@ def test_decode_logits(setup):
     st = _oracle_state(om, k, v)
     want = om.forward(st, [17])
     got_tok, got = e.step([(0, 0, [17], -1)], want_logits=True)
-    err = np.abs(got - want).max()
+    err = _report("tiny decode logits vs oracle", got, want)
     assert err <= _bound(want), (err, _bound(want))
     assert got_tok[0] == np.argmax(got[0])
 
@@ -59,7 +65,7 @@ def test_verify_window_logits(setup):
     toks = [17, 3, 99, 1024, 5, 6, 7, 8, 9]
     want = om.forward(st, toks)
     _, got = e.step([(1, 2, toks, -1)], want_logits=True)
-    assert np.abs(got - want).max() <= _bound(want)
+    assert _report("tiny verify logits vs oracle", got, want) <= _bound(want)
 
 
 def test_draft_logits(setup):
@@ -79,7 +85,7 @@ def test_draft_logits(setup):
     st = om.new_kv(kq, vq)
     want = om.forward(st, [17])
     _, got = e.step([(2, 1, [17], -1)], want_logits=True)
-    assert np.abs(got - want).max() <= _bound(want)
+    assert _report("tiny draft logits vs oracle", got, want) <= _bound(want)
 
 
 def test_greedy_tokens_vs_oracle(setup):

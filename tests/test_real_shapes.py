@@ -30,11 +30,14 @@ REP8 = ModelShape(vocab=256, hidden=512, layers=2, n_q=16, n_kv=2, d_head=128, f
 REP4 = ModelShape(vocab=256, hidden=512, layers=1, n_q=8, n_kv=2, d_head=128, ffn=512)
 L8B_2 = ModelShape(vocab=128256, hidden=4096, layers=2, n_q=32, n_kv=8, d_head=128, ffn=14336)
 
-# bounds (rel, abs); see the module docstring
-ATTN_DRAFT = (1e-2, 1e-3)
-ATTN_DENSE = (1e-2, 1e-3)
-LOGITS = (2e-2, 1e-3)
-LOGITS_HF = (2.5e-2, 1e-3)
+# bounds (rel, abs): max|got - want| <= rel * max|want| + abs, about 2x the
+# largest error measured on a B200 (round 2, gpurun_out -> DESIGN.md §4):
+#   draft int4 1.11e-2 (128K), draft int2 1.37e-2, dense 4.3e-3,
+#   8B-shape logits 8.1e-3 (draft row), tiny engine vs HF fp64 6.2e-3
+ATTN_DRAFT = {4: (2.2e-2, 0.0), 2: (2.8e-2, 0.0)}
+ATTN_DENSE = (9e-3, 0.0)
+LOGITS = (1.6e-2, 0.0)
+LOGITS_HF = (1.3e-2, 0.0)
 
 
 def _err(got, want, bound, name):
@@ -88,7 +91,7 @@ def test_draft_attention_long_and_rep8(cuda, shape, n_ctx, bits):
     for h in range(s.n_kv):
         kk, vv = _dequant(k[layer, h], v[layer, h], bits, s.d_head)
         want = _oracle_attn(np.ascontiguousarray(T.bf16_to_f32(q[0, h * rep:(h + 1) * rep])), kk, vv)
-        _err(got[h * rep:(h + 1) * rep], want, ATTN_DRAFT, f"draft n_rep={rep} T={n_ctx} int{bits} head {h}")
+        _err(got[h * rep:(h + 1) * rep], want, ATTN_DRAFT[bits], f"draft n_rep={rep} T={n_ctx} int{bits} head {h}")
     e.close()
 
 

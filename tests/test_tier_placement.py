@@ -1,0 +1,101 @@
+"""Per-request tier placement (the reference's B_c knob) and the capacity-
+capped full-KV baseline, on the GPU with the tiny model.
+
+  * intra_throughput (/root/reference/proj/src/analytics.cpp:45-82): B_c of
+    the B requests keep their full KV offloaded to the host tier, the other
+    B_g = B - B_c keep it resident in HBM; every request drafts on its
+    compressed KV.  vc_run_scheduled's n_resident = B_g.  Output must stay
+    identical to full-KV greedy decode for both kinds of request.
+  * baseline_full_kv (sim.cpp:418-494): FIFO admission while a full-KV slot
+    is free (vc_run_decode_fifo); every request's tokens equal its own
+    unbatched greedy decode, at most max_slots are resident at once, requests
+    that can never fit are counted as unserved (:438-440)."""
+import numpy as np
+import pytest
+
+import vc_testlib as T
+from paper_2605_17613_b200 import TINY, Engine, _lib
+
+N_CTX = 1800
+K = 36
+
+
+@pytest.fixture(scope="module")
+def weights():
+    return T.tiny_weights(TINY, seed=7, std=0.02)
+
+
+def _base(weights, n, K=K, ctx=N_CTX):
+    ref = Engine(TINY, max_slots=n, max_ctx=ctx + K + 64, max_x=1, quant_bits=0)
+    ref.load_weights(weights)
+    for s in range(n):
+        ref.add_synthetic(s, ctx, 17 + s, seed=1 + s)
+    base, _ = ref.autoregress(list(range(n)), K)
+    ref.close()
+    return base
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n,n_res,n_stage,x,x_res", [(6, 3, 4, 8, 3), (5, 5, 5, 6, 2), (4, 1, 3, 8, 0)])
+def test_mixed_tier_lossless(cuda, weights, n, n_res, n_stage, x, x_res):
+    base = _base(weights, n)
+    e = Engine(TINY, max_slots=n, max_ctx=N_CTX + 400, max_x=16, quant_bits=4, full_tier=1, n_stage=n_stage,
+               max_verify=n_stage + 2)
+    e.load_weights(weights)
+    for s in range(n):
+        e.add_synthetic(s, N_CTX, 17 + s, seed=1 + s)
+        e.compress(s)
+    out, st = e.run_scheduled(list(range(n)), K, x=x, window=32, n_resident=n_res, x_resident=x_res)
+    np.testing.assert_array_equal(out, base)
+    assert st["tokens"] == n * K
+    assert st["resident_verifies"] > 0
+    if n_res < n:
+        assert st["verifies"] > st["resident_verifies"] and st["h2d_bytes"] > 0
+    # residents' rounds are x_res (or x) long: accepted per verify <= that
+    assert st["resident_accept"] <= (x_res or x)
+    assert 0 < st["throughput"] and 0 < st["p50_latency_s"] <= st["p99_latency_s"]
+    assert st["peak_hbm_bytes"] > 0
+    e.close()
+
+
+@pytest.mark.gpu
+def test_mixed_tier_config_errors(cuda):
+    e = Engine(TINY, max_slots=4, max_ctx=600, max_x=8, quant_bits=4, full_tier=1, n_stage=3)
+    for s in range(4):
+        e.add_synthetic(s, 300, 17, seed=1)
+        e.compress(s)
+    with pytest.raises(_lib.ConfigError):  # 3 residents + 1 rotating slot > 3 stages
+        e.run_scheduled([0, 1, 2, 3], 8, x=4, window=16, n_resident=3)
+    with pytest.raises(_lib.ConfigError):
+        e.run_scheduled([0, 1, 2, 3], 8, x=4, window=16, n_resident=5)
+    e.close()
+
+
+@pytest.mark.gpu
+def test_fifo_baseline_capacity_capped(cuda, weights):
+    n, slots = 5, 2
+    base = _base(weights, n, K=12)
+    e = Engine(TINY, max_slots=slots, max_ctx=N_CTX + 64, max_x=1, quant_bits=0)
+    e.load_weights(weights)
+    reqs = [(N_CTX, 17 + i, 1 + i, 0.0) for i in range(n)]
+    reqs.append((N_CTX + 10_000, 5, 9, 0.0))  # never fits a slot
+    out, m = e.run_decode_fifo(reqs, 12)
+    np.testing.assert_array_equal(out[:n], base)
+    assert m["completed"] == n and m["unserved"] == 1
+    assert m["max_batch"] == slots and m["tokens"] == n * 12
+    assert m["iterations"] == 3 * 12  # 2 + 2 + 1 requests, 12 steps each
+    assert m["throughput"] > 0 and m["p50_latency_s"] <= m["p99_latency_s"]
+    assert m["full_batch_throughput"] > 0
+    e.close()
+
+
+@pytest.mark.gpu
+def test_fifo_baseline_arrivals(cuda, weights):
+    """A request arriving later than the clock waits (sim.cpp:447-452)."""
+    e = Engine(TINY, max_slots=2, max_ctx=N_CTX + 64, max_x=1, quant_bits=0)
+    e.load_weights(weights)
+    out, m = e.run_decode_fifo([(N_CTX, 17, 1, 0.0), (N_CTX, 18, 2, 1e6)], 4)
+    assert m["completed"] == 2 and m["max_batch"] == 1
+    base = _base(weights, 2, K=4)
+    np.testing.assert_array_equal(out, base)
+    e.close()
