@@ -67,7 +67,12 @@ def parse():
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-secondary", action="store_true", help="skip the other tier's line")
     p.add_argument("--stages", type=int, default=8, help="HBM staging slots of the host tier")
+    p.add_argument("--stages-rot", type=int, default=3,
+                   help="rotating staging slots of the offloaded requests when some are resident")
     p.add_argument("--small", action="store_true", help="tiny model smoke run")
+    p.add_argument("--capped", action="store_true",
+                   help="capacity-capped regime: --batch (default 48) requests at 32K, FIFO full-KV baseline vs "
+                        "per-request placement")
     p.add_argument("--config", type=int, default=2, choices=[2, 3, 4],
                    help="2: BASELINE.json configs[1] (headline); 3: configs[2] -- 128K ctx, drop-topk c=0.2; "
                         "4: configs[3] -- remote prefix caching, 64K shared prefix, int2 draft KV")
@@ -213,6 +218,72 @@ def hbm_peak(peaks):
             if pref in k.lower():
                 return v, f"MEASURED_PEAKS.json {k}"
     return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def weight_read_bytes(shape) -> int:
+    """Weight bytes one forward pass streams: every layer's projections + the LM
+    head (the embedding table is gathered, not streamed)."""
+    H, F, V, d = shape.hidden, shape.ffn, shape.vocab, shape.d_head
+    per_layer = ((shape.n_q + 2 * shape.n_kv) * d * H + H * shape.n_q * d + 2 * F * H + H * F) * 2
+    return shape.layers * per_layer + V * H * 2
+
+
+def step_roofline(r, shape, peak_gbs):
+    """Algorithmic HBM bytes per second of a tier's timed window over the peak:
+    per iteration the weights once, the compressed KV of every drafting row, the
+    full KV of every verify window."""
+    s = r["st"]
+    it = max(s["timed_iterations"], 1)
+    kv_full = float(r["meta"]["full_bytes"])
+    comp = float(r["meta"]["payload_bytes"] + r["meta"]["aux_bytes"])
+    verifies = s["timed_verifies"]
+    draft_rows = max(s["timed_rows"] - s["timed_verify_rows"], 0.0)
+    bytes_ = it * weight_read_bytes(shape) + draft_rows * comp + verifies * kv_full
+    dev_s = s["timed_device_ms"] / 1e3
+    gbs = bytes_ / max(dev_s, 1e-9) / 1e9
+    return {"achieved_gbs": round(gbs, 1), "frac": round(gbs / peak_gbs, 3),
+            "bytes_per_iteration": int(bytes_ / it), "ms_per_iteration": round(s["timed_device_ms"] / it, 3),
+            "verifies": int(verifies), "drafting_rows": int(draft_rows),
+            "basis": "weights per iteration + compressed KV per drafting row + full KV per verify window"}
+
+
+def gamma_table(bits):
+    """Measured gamma(x) of int{bits} KIVI on configs[1]'s workload
+    (profiles/r02_gamma.json, tools/gamma_sweep.py), else the round-1 points."""
+    f = os.path.join(ROOT, "profiles", "r02_gamma.json")
+    if os.path.exists(f):
+        t = json.load(open(f))["tables"].get(f"int{bits}")
+        if t:
+            return {int(x): v["gamma"] for x, v in t.items() if v["gamma"] > 0}, "profiles/r02_gamma.json"
+    return {6: 5.15 / 6, 30: 21.1 / 30, 47: 21.4 / 47}, "round-1 measured points (x = 6, 30, 47)"
+
+
+def choose_placement(runs, B, base_ms_per_step, bits, weights):
+    """optimize_intra (analytics.cpp:130-150, knobs.py) with this run's measured
+    constants: HBM = the full-KV decode step's effective bandwidth, interconnect
+    = the host tier's measured H2D rate, c = compressed / full bytes, gamma(x)
+    measured, gpu_mem = the device's HBM."""
+    import torch
+    from paper_2605_17613_b200 import knobs
+    host = runs[1]
+    meta = host["meta"]
+    kv = int(meta["full_bytes"])
+    c = (meta["payload_bytes"] + meta["aux_bytes"]) / kv
+    bw_hbm = (weights + B * kv) / (base_ms_per_step / 1e3)
+    s = host["st"]
+    bw_inter = s["h2d_bytes"] / max(s["h2d_ms"] / 1e3, 1e-9)
+    gpu_mem = int(torch.cuda.mem_get_info()[1])
+    gtab, gsrc = gamma_table(bits)
+    hw = knobs.Hardware(bw_hbm, bw_inter, gpu_mem)
+    best = knobs.optimize_intra(hw, weights, kv, B, gtab, c)
+    pred_host = knobs.intra_throughput(B, host["x"], c, 1, hw, weights, kv, B, gtab)
+    return {"model": "intra_throughput / optimize_intra (analytics.cpp:45-150) restated in "
+                     "paper_2605_17613_b200/knobs.py, equal to oracle/_ref (tests/test_knobs.py)",
+            "constants": {"hbm_gbs": round(bw_hbm / 1e9, 1), "h2d_gbs": round(bw_inter / 1e9, 2), "c": round(c, 4),
+                          "gpu_mem": gpu_mem, "weights_read": weights, "kv_full": kv, "gamma_source": gsrc},
+            "optimizer": {"B_c": best[1], "x": best[2], "l": best[3], "predicted_tok_s": round(best[0], 1)},
+            "predicted_host_tier_tok_s": round(pred_host, 1) if pred_host else None,
+            "predicted_full_kv_tok_s": round(knobs.intra_throughput(0, 1, c, 1, hw, weights, kv, B, gtab), 1)}
 
 
 def combine_lossless(identical: bool, compared: int, dist=None, device=None):
@@ -387,6 +458,154 @@ def main_remote(args, rank, world, local):
 
 
 
+def main_capped(args, rank, world, local):
+    """The capacity-capped regime (VERDICT r1 "B_c tier
+    placement"): B requests at 32K context where full-KV decode cannot hold
+    them all.  Full-KV arm = the reference's baseline_full_kv (sim.cpp:418-494)
+    on the engine: FIFO admission into the B_max full-KV slots that fit next
+    to the weights (vc_run_decode_fifo); its steady state is the throughput
+    while every slot is busy.  VeriCache arm = per-request placement: every
+    request holds its compressed KV in HBM, B_g requests keep their full KV
+    resident (the staging slots that fit in the rest of HBM, minus the
+    rotating ones), B_c = B - B_g have theirs in pinned host memory and are
+    reloaded per verify by the swap scheduler.  Same weights, requests and
+    first tokens; every emitted token is compared with the full-KV arm's."""
+    import numpy as np
+    import psutil
+    import torch
+    import paper_2605_17613_b200 as vc
+    from paper_2605_17613_b200 import knobs
+    from paper_2605_17613_b200.shard import reduce_window, weak_shard
+
+    n_dev = torch.cuda.device_count()
+    local = local % n_dev
+    torch.cuda.set_device(local)
+    dist, coll_dev = None, "cuda"
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    peaks = json.load(open(PEAKS)) if os.path.exists(PEAKS) else {}
+    peak, peak_src = hbm_peak(peaks)
+    shape = vc.LLAMA3_8B
+    ctx, bits = args.ctx, args.bits
+    B = 48 if args.batch == 16 else args.batch
+    K, W = args.steps, args.warmup
+    shard = weak_shard(B, world, rank)
+    rng = np.random.default_rng(2 + shard.requests[0])
+    first = [int(t) for t in rng.integers(0, shape.vocab, B)]
+    rs, qs = 0.0002, 0.002
+    slots = list(range(B))
+    bpt = shape.kv_bytes_per_token
+    weights = weight_read_bytes(shape) + shape.vocab * shape.hidden * 2  # + embedding table (resident)
+    reserve = 6e9  # activations, logits, split-K partials, CUDA context
+    Kb = 64
+
+    # ---------------- full-KV arm: FIFO admission under HBM capacity
+    free = torch.cuda.mem_get_info()[0]
+    slot_b = (ctx + Kb + 8 + 130) * bpt
+    b_max = int((free - weights - reserve) // slot_b)
+    eb = vc.Engine(shape, max_slots=b_max, max_ctx=ctx + Kb + 8, max_x=1, quant_bits=0, full_tier=0,
+                   max_verify=1, device=local)
+    eb.init_weights(seed=0, std=0.02, resid_std=rs, q_std=qs)
+    reqs = [(ctx, first[i], shard.seeds[i], 0.0) for i in range(B)]
+    eb.run_decode_fifo(reqs[:2], 4)  # warm-up (graph capture of the first batch sizes)
+    base_out, mb = eb.run_decode_fifo(reqs, Kb)
+    eb.close()
+    del eb
+    torch.cuda.empty_cache()
+
+    # ---------------- VeriCache arm: per-request placement
+    x, x_res = (args.x or 47), 6
+    it_w, it_k = (W + 2) * (x + 1), K * (x + 1)
+    free = torch.cuda.mem_get_info()[0]
+    max_ctx = ctx + it_w + it_k + 3 * (x + 1) + 8
+    slot_b = (max_ctx + x + 130) * bpt
+    comp_b = ctx * bpt * (bits / 16.0) * 1.07 + 2 * (128 + x + 2) * 2 * shape.d_head * shape.layers * shape.n_kv
+    n_stage = int((free - weights - reserve - B * comp_b) // slot_b)
+    resident = max(0, min(B - 1, n_stage - args.stages_rot))
+    n_stage = resident + args.stages_rot
+    host_need = (B - resident) * slot_b
+    host_avail = psutil.virtual_memory().available
+    if host_need > 0.8 * host_avail:
+        raise SystemExit(f"capped: pinned host pool {host_need / 1e9:.0f} GB exceeds 80% of available host "
+                         f"memory {host_avail / 1e9:.0f} GB; lower --batch")
+    ev = vc.Engine(shape, max_slots=B, max_ctx=max_ctx, max_x=x, quant_bits=bits, full_tier=1, n_stage=n_stage,
+                   resident_slots=resident, max_verify=args.stages_rot + (resident + x_res) // (x_res + 1) + 2,
+                   device=local)
+    ev.init_weights(seed=0, std=0.02, resid_std=rs, q_std=qs)
+    for i in range(B):
+        ev.add_synthetic(i, ctx, first[i], seed=shard.seeds[i])
+        meta = ev.compress(i)
+    l0 = ev.stats()["kernel_launches"]
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    with Clocks(local) as clk:
+        out, st = ev.run_scheduled(slots, K=(it_w + it_k) * (x + 1), x=x, window=256, warmup_iterations=it_w,
+                                   timed_iterations=it_k, x_resident=x_res)
+    torch.cuda.synchronize()
+    launches = ev.stats()["kernel_launches"] - l0
+    hist = [ev.history(i) for i in slots]
+    ev.close()
+    cmp = [min(len(h), Kb) for h in hist]
+    identical = all(hist[i][:cmp[i]] == base_out[i, :cmp[i]].tolist() for i in slots)
+    identical, compared = combine_lossless(identical, int(sum(cmp)), dist, coll_dev)
+    tok, (dev_s, wall_s) = reduce_window(float(st["timed_tokens"]), [st["timed_device_ms"] / 1e3,
+                                                                      st["timed_wall_ms"] / 1e3], dist, coll_dev)
+    base_tok, (base_clock,) = reduce_window(mb["full_batch_throughput"] * 1.0, [1.0], dist, coll_dev)
+    value = tok / dev_s
+    base_value = base_tok  # sum of per-rank steady states
+    # the reference model at the same point: baseline_full_kv and optimize_intra
+    kv = int(meta["full_bytes"])
+    c = (meta["payload_bytes"] + meta["aux_bytes"]) / kv
+    bw_hbm = (weight_read_bytes(shape) + b_max * kv) / (1.0 / (mb["full_batch_throughput"] / b_max))
+    bw_inter = st["h2d_bytes"] / max(st["h2d_ms"] / 1e3, 1e-9)
+    gtab, gsrc = gamma_table(bits)
+    hw = knobs.Hardware(bw_hbm, bw_inter, int(torch.cuda.mem_get_info()[1]))
+    best = knobs.optimize_intra(hw, weight_read_bytes(shape), kv, B, gtab, c)
+    r = {"x": x, "st": st, "meta": meta, "resident": resident, "x_res": x_res}
+    if rank == 0:
+        line = {
+            "metric": METRIC + " (capacity-capped regime: steady-state tokens/s)",
+            "value": round(value, 2), "unit": "tokens/s", "n_gpus": world, "steps": K, "warmup": W,
+            "ms_per_step": round(dev_s * 1e3 / K, 3), "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16",
+            "data": "synthetic (random-init weights, calibrated q/o/down init; synthetic 32K prefix KV)",
+            "config": {"workload": f"capacity-capped: Llama-3-8B shape, {ctx} ctx, {B} requests/GPU, int{bits} KIVI; "
+                                   f"full-KV decode holds only {b_max} (FIFO admission, sim.cpp:418-494)",
+                       "global_batch": B * world, "seq_len": ctx, "draft_x_offloaded": x, "draft_x_resident": x_res,
+                       "step": "one speculative round of the offloaded requests: x+1 scheduler iterations",
+                       "parallelism": f"request-sharded dp{world}", "l2": "inputs larger than L2"},
+            "full_kv_decode": {"value": round(base_value, 2), "unit": "tokens/s", "B_max_resident": b_max,
+                               "mean_batch": round(mb["mean_batch"], 2), "whole_workload_tok_s": round(mb["throughput"], 2),
+                               "warm_tok_s": round(mb["warm_throughput"], 2), "p50_latency_s": round(mb["p50_latency_s"], 3),
+                               "p99_latency_s": round(mb["p99_latency_s"], 3), "completed": mb["completed"],
+                               "definition": "tokens / step device time over the steps with every slot busy"},
+            "speedup_vs_full_kv": round(value / base_value, 3),
+            "e2e": {"value": round(tok / wall_s, 2), "unit": "tokens/s",
+                    "h2d_bytes_per_step": int((st["timed_rows"] * 20 + st["h2d_bytes"]) / K),
+                    "d2h_bytes_per_step": int(st["timed_rows"] / K * 4)},
+            "placement": {"B_g_resident": resident, "B_c_offloaded": B - resident, "n_stage": n_stage,
+                          "resident_tokens_in_window": st["timed_resident_tokens"],
+                          "resident_accepted_per_verify": round(st["resident_accept"], 3),
+                          "accepted_per_verify": round(st["mean_accept"], 3),
+                          "h2d_gbs": round(bw_inter / 1e9, 1),
+                          "link_busy_frac": round(st["h2d_ms"] / max(st["timed_wall_ms"], 1e-9), 3),
+                          "pinned_host_gb": round(host_need / 1e9, 1)},
+            "step_roofline": step_roofline(r, shape, peak),
+            "reference_model": {"baseline_full_kv_tok_s": round(b_max / ((weight_read_bytes(shape) + b_max * kv) / bw_hbm), 1),
+                                "optimize_intra": {"B_c": best[1], "x": best[2], "l": best[3],
+                                                   "predicted_tok_s": round(best[0], 1)},
+                                "constants": {"hbm_gbs": round(bw_hbm / 1e9, 1), "h2d_gbs": round(bw_inter / 1e9, 1),
+                                              "c": round(c, 4), "gamma_source": gsrc}},
+            "tokens_identical_to_full_kv": identical, "tokens_compared": compared,
+            "gpu_launches": int(launches), "clocks": clk.summary(), "cpu_baseline": None,
+        }
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
 def main():
     args = parse()
     rank = int(os.environ.get("RANK", "0"))
@@ -397,6 +616,9 @@ def main():
         return
     if args.config == 4:
         main_remote(args, rank, world, local)
+        return
+    if args.capped:
+        main_capped(args, rank, world, local)
         return
     import numpy as np
     import torch
@@ -462,9 +684,12 @@ def main():
     del eb
     torch.cuda.empty_cache()
 
-    def vericache(tier, x_force=None):
+    def vericache(tier, x_force=None, resident=0, x_res=0):
         """One VeriCache run: compressed drafting + full-KV verify (tier 0: full KV
-        in HBM; tier 1: full KV in pinned host memory, reloaded per verify)."""
+        in HBM; tier 1: full KV in pinned host memory, reloaded per verify; tier 1
+        with resident > 0: per-request placement -- `resident` requests keep their
+        full KV in HBM (B_g) and verify with x_res-token rounds, the others (B_c)
+        are reloaded per verify)."""
         # host tier x=47: the verify window plus 15 drafting rows stays within one
         # 64-row GEMM tile and the booked reloads saturate PCIe (link busy 0.99)
         # HBM tier x=6: the measured optimum of an x sweep {4,6,8,10,12,16,24}
@@ -480,10 +705,13 @@ def main():
         it_w, it_k = (W + 2) * (x + 1), K * (x + 1)
         ev, err = None, None
         try:
-            ev = vc.Engine(shape, max_slots=B, max_ctx=ctx + it_w + it_k + 3 * (x + 1) + 8, max_x=x,
+            n_stage = (resident + (args.stages_rot if resident < B else 0)) if resident else args.stages
+            max_verify = (n_stage - resident + (resident + x_res) // (x_res + 1) + 2 if resident else
+                          (args.stages if tier else max(2, B // (x + 1) + 2)))
+            ev = vc.Engine(shape, max_slots=B, max_ctx=ctx + it_w + it_k + 3 * (x + 1) + 8, max_x=max(x, x_res),
                            quant_bits=0 if drop else args.bits, drop_ratio=drop, full_tier=tier,
-                           n_stage=args.stages if tier else 1,
-                           max_verify=args.stages if tier else max(2, B // (x + 1) + 2), device=local)
+                           n_stage=n_stage if tier else 1, max_verify=max_verify, device=local,
+                           resident_slots=resident)
         except vc.VcError as ex:
             err = ex
         if dist:  # every rank falls back together (the pinned pool may fail on one rank only)
@@ -498,7 +726,8 @@ def main():
         for i in range(B):
             ev.add_synthetic(i, ctx, first[i], seed=shard.seeds[i])
             meta = ev.compress(i)
-        ka = ev.kernel_bench(3 if drop else 0, slots, reps=5) if tier == head_tier else (None, None)
+        ka = (ev.kernel_bench(3 if drop else 0, slots, reps=5) if tier == head_tier and not resident
+              else (None, None))
         launches0 = ev.stats()["kernel_launches"]
         if dist:
             dist.barrier()
@@ -510,7 +739,7 @@ def main():
             torch.cuda.cudart().cudaProfilerStart()
         with Clocks(local) as clk:
             out, st = ev.run_scheduled(slots, K=(it_w + it_k) * (x + 1), x=x, window=window,
-                                       warmup_iterations=it_w, timed_iterations=it_k)
+                                       warmup_iterations=it_w, timed_iterations=it_k, x_resident=x_res)
         torch.cuda.synchronize()
         if prof:
             torch.cuda.cudart().cudaProfilerStop()
@@ -530,6 +759,7 @@ def main():
                                                  [st["timed_device_ms"] / 1e3, st["timed_wall_ms"] / 1e3],
                                                  dist, device=coll_dev)
         r = {"x": x, "window": window, "ramp": ramp, "st": st, "meta": meta, "ka": ka, "launches": launches,
+             "resident": resident, "x_res": x_res,
              "clocks": clk.summary(), "identical": identical, "compared": n_cmp,
              "tok": tok_all, "dev_s": dev_s, "wall_s": wall_s}
         return r
@@ -551,6 +781,18 @@ def main():
     long_run = None
     if cfg3 and not args.small and not args.x:
         long_run = vericache(0, x_force=32)  # configs[2]'s "long draft horizon", same workload
+    # per-request tier placement chosen by the reference's optimiser fed this
+    # run's measured constants (knobs.py = analytics.cpp:45-150, pinned by
+    # tests/test_knobs.py): B_c requests offloaded to the host tier, B_g resident
+    placed, knob_report = None, None
+    if not cfg3 and not args.small and not args.no_secondary and 1 in runs and note is None:
+        knob_report = choose_placement(runs, B, base_dev / Kb, args.bits, weight_read_bytes(shape))
+        b_c = knob_report["optimizer"]["B_c"]
+        if 0 < b_c < B:
+            try:
+                placed = vericache(1, x_force=runs[1]["x"], resident=B - b_c, x_res=knob_report["optimizer"]["x"])
+            except vc.VcError as ex:
+                knob_report["skipped"] = str(ex)
     h = runs[head_tier]
     st, x = h["st"], h["x"]
     tok_all, dev_s, wall_s = h["tok"], h["dev_s"], h["wall_s"]
@@ -566,6 +808,9 @@ def main():
 
     def tier_summary(r, tier):
         s = r["st"]
+        # step_roofline: algorithmic HBM bytes per second of the timed window
+        # over the peak (weights + compressed KV of every drafting row + full
+        # KV of every verify window, per iteration)
         d = {"value": round(r["tok"] / r["dev_s"], 2), "e2e": round(r["tok"] / r["wall_s"], 2),
              "speedup_vs_full_kv": round((r["tok"] / r["dev_s"]) / base_value, 3),
              "ms_per_step": round(r["dev_s"] * 1e3 / K, 3), "draft_x": r["x"], "lookahead_window": r["window"],
@@ -575,7 +820,17 @@ def main():
              "full_kv_in": "pinned host memory" if tier else "HBM",
              # share of the device window the steps themselves occupy (the rest:
              # host planning between steps, which the next round can overlap)
-             "gpu_busy_frac": round(s["timed_step_device_ms"] / max(s["timed_device_ms"], 1e-9), 3)}
+             "gpu_busy_frac": round(s["timed_step_device_ms"] / max(s["timed_device_ms"], 1e-9), 3),
+             "sim_metrics": {k: (round(s[k], 4) if isinstance(s[k], float) else s[k]) for k in
+                             ("throughput", "warm_throughput", "p50_latency_s", "p99_latency_s",
+                              "interconnect_busy", "peak_hbm_bytes")},
+             "step_roofline": step_roofline(r, shape, peak)}
+        if r.get("resident"):
+            d["placement"] = {"B_g_resident": r["resident"], "B_c_offloaded": B - r["resident"],
+                              "x_resident": r["x_res"], "x_offloaded": r["x"],
+                              "resident_verifies": s["resident_verifies"],
+                              "resident_accepted_per_verify": round(s["resident_accept"], 3),
+                              "timed_resident_tokens": s["timed_resident_tokens"]}
         if tier == 1:
             win_s = s["timed_wall_ms"] / 1e3
             d["swap"] = {"h2d_gbs": round(s["h2d_bytes"] / max(s["h2d_ms"], 1e-9) / 1e6, 1),
@@ -617,7 +872,9 @@ def main():
             "tokens_identical_to_full_kv": bool(h["identical"]), "tokens_compared": h["compared"],
             "accepted_per_verify": round(st["mean_accept"], 3), "verifies": st["verifies"],
             "late_transfers": st["late_transfers"],
-            "tiers": {("host" if t else "hbm"): tier_summary(r, t) for t, r in runs.items()},
+            "tiers": {**{("host" if t else "hbm"): tier_summary(r, t) for t, r in runs.items()},
+                      **({"placed": tier_summary(placed, 1)} if placed else {})},
+            **({"knobs": knob_report} if knob_report else {}),
             **({"long_horizon": tier_summary(long_run, 0)} if long_run else {}),
             "roofline": {"kernel": ("dense_umma_kernel<128,4> drafting over the drop tier" if cfg3 else
                                     "draft_attn_quant_kernel<128,4,4>") + f" (one launch per layer, {B} requests)",

@@ -81,6 +81,11 @@ typedef struct {
   int drop_window;   /* drop-topk tier, online mode (speckv::update, compressor.cpp:
                         208-243): tokens accepted after compress are kept in a
                         sliding window of the latest drop_window..2*drop_window; 0 = keep all */
+  int resident_slots; /* tier 1 per-request placement (the reference's B_g = B - B_c,
+                         analytics.cpp:45-82): slots [0, resident_slots) keep their
+                         full KV resident in HBM (staging slot `slot`, no host copy,
+                         never reloaded); the pinned host pool holds the other
+                         (offloaded) slots only.  n_stage >= resident_slots + 1. */
 } vc_runtime_desc;
 
 /* Mirrors speckv::CompressedKVMeta (compressor.hpp:56-65).  Quant-uniform:
@@ -277,15 +282,14 @@ typedef struct {
   int64_t warmup_iterations;  /* iterations before the timed window */
   int64_t timed_iterations;   /* length of the timed window; 0 = run to completion */
   /* Per-request tier placement (the reference's B_c knob, intra_throughput /
-   * optimize_intra, analytics.cpp:45-82,130-150): tier 1 only.  The first
-   * n_resident requests keep their full KV resident in HBM for the whole run
-   * (each owns staging slot i: loaded once, never reloaded -- B_g = n_resident),
-   * the other n - n_resident are offloaded (B_c) and reloaded per verify
-   * through staging slots [n_resident, n_stage) under the swap scheduler.
-   * Every request drafts on its compressed KV.  Residents run x_resident-token
-   * rounds (0 = x), verify as soon as a round is drafted, staggered so about
-   * n_resident / (x_resident + 1) windows verify per iteration.              */
-  int n_resident;
+   * optimize_intra, analytics.cpp:45-82,130-150), tier 1: requests in the
+   * engine's resident slots (vc_runtime_desc.resident_slots, B_g) verify
+   * against their HBM-resident full KV and are never reloaded; the others
+   * (B_c) are reloaded per verify through the rotating staging slots under
+   * the swap scheduler.  Every request drafts on its compressed KV.  Residents
+   * run x_resident-token rounds (0 = x), verify as soon as a round is
+   * drafted, staggered so about B_g / (x_resident + 1) windows verify per
+   * iteration.                                                              */
   int x_resident;
 } vc_sched_desc;
 
@@ -312,6 +316,8 @@ typedef struct {
   int64_t resident_verifies;  /* verifies of resident requests (full KV in HBM) */
   double resident_accept;     /* their accepted drafted tokens per verify */
   int64_t timed_resident_tokens; /* tokens the residents emitted inside the timed window */
+  int64_t timed_verifies;     /* verify windows executed inside the timed window */
+  double timed_verify_rows;   /* their rows (x+1 each); timed_rows - this = drafting rows */
   /* SimMetrics (sim.hpp:52-74) of the whole run on the loop's host clock:
    * throughput = tokens / wall time, warm = first and last 10% of the run's
    * time cut (sim.cpp:103-109), request latency percentiles (completion -

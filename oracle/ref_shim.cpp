@@ -200,3 +200,64 @@ int ref_update_window(int layers, int heads, int window, int sinks, int layer, i
 }
 
 }  // extern "C"
+
+// intra_throughput / optimize_intra (analytics.cpp:45-82, :130-150) with a
+// tabulated acceptance model {c -> {x_i -> gamma_i}}: pins the measured-
+// constant knob selection (paper_2605_17613_b200/knobs.py).  Returns the
+// throughput, -1 when infeasible (std::nullopt), or < -1 on error.
+#include "speckv/analytics.hpp"
+namespace {
+speckv::AcceptanceModel tab_model(double c, int n_tab, const int* xs, const double* gs) {
+  speckv::AcceptanceModel m;
+  m.kind = speckv::AcceptanceModel::Kind::Tabulated;
+  for (int i = 0; i < n_tab; ++i) m.table[c][xs[i]] = gs[i];
+  return m;
+}
+speckv::HardwareProfile hw_of(double bw_hbm, double bw_inter, int64_t gpu_mem) {
+  speckv::HardwareProfile hw;
+  hw.hbm_bandwidth = bw_hbm;
+  hw.interconnect_bandwidth = bw_inter;
+  hw.gpu_mem = gpu_mem;
+  hw.local_gpus = 1;
+  return hw;
+}
+}  // namespace
+extern "C" {
+double ref_intra_throughput(int b_c, int x, double c, int l, double bw_hbm, double bw_inter, int64_t gpu_mem,
+                            int64_t weights, int64_t kv_full, int batch, int n_tab, const int* xs,
+                            const double* gs) {
+  double out = -1.0;
+  int rc = guarded([&] {
+    auto v = speckv::intra_throughput(speckv::IntraKnobs{b_c, x, c, l}, hw_of(bw_hbm, bw_inter, gpu_mem), weights,
+                                      kv_full, batch, tab_model(c, n_tab, xs, gs));
+    out = v ? *v : -1.0;
+    return 0;
+  });
+  return rc < 0 ? -2.0 + rc : out;
+}
+
+// Grid: B_c in 0..batch, x in 1..x_max, the single c, l in 1..l_max.
+double ref_optimize_intra(double c, int x_max, int l_max, double bw_hbm, double bw_inter, int64_t gpu_mem,
+                          int64_t weights, int64_t kv_full, int batch, int n_tab, const int* xs, const double* gs,
+                          int* b_c, int* x, int* l) {
+  double out = -1.0;
+  int rc = guarded([&] {
+    speckv::IntraGrids g;
+    for (int i = 1; i <= x_max; ++i) g.draft_length.push_back(i);
+    g.compression.push_back(c);
+    for (int i = 1; i <= l_max; ++i) g.cycles_per_load.push_back(i);
+    for (int i = 0; i <= batch; ++i) g.offloaded_count.push_back(i);
+    auto best = speckv::optimize_intra(hw_of(bw_hbm, bw_inter, gpu_mem), weights, kv_full, batch,
+                                       tab_model(c, n_tab, xs, gs), g);
+    if (best) {
+      *b_c = best->knobs.offloaded_count;
+      *x = best->knobs.draft_length;
+      *l = best->knobs.cycles_per_load;
+      out = best->throughput;
+    }
+    return 0;
+  });
+  return rc < 0 ? -2.0 + rc : out;
+}
+
+}  // extern "C"

@@ -42,7 +42,8 @@ class RuntimeDesc(C.Structure):
     _fields_ = [("max_slots", C.c_int), ("max_ctx", C.c_int), ("max_x", C.c_int),
                 ("quant_bits", C.c_int), ("full_tier", C.c_int), ("n_stage", C.c_int),
                 ("max_verify", C.c_int), ("use_graphs", C.c_int), ("drop_ratio", C.c_double),
-                ("tp_size", C.c_int), ("tp_rank", C.c_int), ("drop_window", C.c_int)]
+                ("tp_size", C.c_int), ("tp_rank", C.c_int), ("drop_window", C.c_int),
+                ("resident_slots", C.c_int)]
 
 
 class CompressedMeta(C.Structure):
@@ -72,7 +73,7 @@ class SchedDesc(C.Structure):
     _fields_ = [("x", C.c_int), ("window", C.c_int), ("iteration_time", C.c_double),
                 ("link_bandwidth", C.c_double), ("hbm_capacity", C.c_int64), ("K", C.c_int),
                 ("warmup_iterations", C.c_int64), ("timed_iterations", C.c_int64),
-                ("n_resident", C.c_int), ("x_resident", C.c_int)]
+                ("x_resident", C.c_int)]
 
 
 class SchedStats(C.Structure):
@@ -83,7 +84,8 @@ class SchedStats(C.Structure):
                 ("timed_wall_ms", C.c_double), ("timed_device_ms", C.c_double),
                 ("timed_rows", C.c_double), ("timed_step_device_ms", C.c_double),
                 ("resident_verifies", C.c_int64), ("resident_accept", C.c_double),
-                ("timed_resident_tokens", C.c_int64), ("throughput", C.c_double),
+                ("timed_resident_tokens", C.c_int64), ("timed_verifies", C.c_int64),
+                ("timed_verify_rows", C.c_double), ("throughput", C.c_double),
                 ("warm_throughput", C.c_double), ("p50_latency_s", C.c_double), ("p99_latency_s", C.c_double),
                 ("interconnect_busy", C.c_double), ("peak_hbm_bytes", C.c_int64)]
 

@@ -92,6 +92,7 @@ int vc_engine_create(const vc_model_desc* model, const vc_runtime_desc* rt, int 
     c.use_graphs = rt->use_graphs;
     c.drop_ratio = rt->drop_ratio;
     c.drop_window = rt->drop_window;
+    c.resident_slots = rt->resident_slots;
     if (c.drop_window < 0 || (c.drop_window > 0 && c.drop_ratio <= 0.0))
       throw speckv::ConfigError("compressor: drop_window needs the drop-topk compressor");
     c.tp_size = rt->tp_size > 1 ? rt->tp_size : 1;
@@ -823,9 +824,10 @@ int vc_kv_read(vc_engine* e, int pool, int slot, int layer, int head, int pos, i
     const size_t off = (slice * p.cap + pos) * m.d;
     const size_t bytes = static_cast<size_t>(n) * m.d * 2;
     if (pool == 2) {
-      if (!en.host_pool_k()) throw vc::ContractViolation("no host pool");
-      std::memcpy(k, en.host_pool_k() + off, bytes);
-      std::memcpy(v, en.host_pool_v() + off, bytes);
+      if (!en.host_pool_k(slot)) throw vc::ContractViolation("no host pool (or the slot is resident)");
+      const size_t hoff = ((static_cast<size_t>(layer) * m.n_kv + head) * p.cap + pos) * m.d;
+      std::memcpy(k, en.host_pool_k(slot) + hoff, bytes);
+      std::memcpy(v, en.host_pool_v(slot) + hoff, bytes);
       return;
     }
     if (!p.k) throw vc::ContractViolation("pool not allocated");

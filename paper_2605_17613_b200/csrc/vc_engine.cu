@@ -75,6 +75,17 @@ __global__ void synth_kv_kernel(uint16_t* kbase, uint16_t* vbase, int cap, int n
 
 }  // namespace
 
+uint16_t* Engine::host_pool_k(int slot) const {
+  if (!host_k_ || resident(slot)) return nullptr;
+  const auto& m = cfg_.model;
+  return host_k_ + static_cast<size_t>(slot - cfg_.resident_slots) * m.layers * m.n_kv * full_.cap * m.d;
+}
+uint16_t* Engine::host_pool_v(int slot) const {
+  if (!host_v_ || resident(slot)) return nullptr;
+  const auto& m = cfg_.model;
+  return host_v_ + static_cast<size_t>(slot - cfg_.resident_slots) * m.layers * m.n_kv * full_.cap * m.d;
+}
+
 size_t Engine::full_kv_bytes_per_token() const {
   const auto& m = cfg_.model;
   return static_cast<size_t>(m.layers) * m.n_kv * m.d * 2 * 2;
@@ -82,6 +93,13 @@ size_t Engine::full_kv_bytes_per_token() const {
 
 Engine::Engine(const EngineConfig& cfg, int device) : cfg_(cfg), device_(device) {
   const auto& m = cfg_.model;
+  if (cfg_.resident_slots < 0 || cfg_.resident_slots > cfg_.max_slots)
+    throw ContractViolation("resident_slots out of [0, max_slots]");
+  if (cfg_.resident_slots > 0 && cfg_.full_tier != 1)
+    throw ContractViolation("resident_slots is a placement of the host tier (full_tier 1)");
+  if (cfg_.full_tier == 1 &&
+      cfg_.resident_slots + (cfg_.resident_slots < cfg_.max_slots ? 1 : 0) > cfg_.n_stage)
+    throw ContractViolation("n_stage must hold every resident slot plus one rotating staging slot");
   if (m.n_q % m.n_kv != 0 || (m.d != 64 && m.d != 128)) throw ContractViolation("unsupported head geometry");
   if (cfg_.quant_bits != 0 && cfg_.quant_bits != 2 && cfg_.quant_bits != 4)
     throw ContractViolation("quant_bits must be 0, 2 or 4");
@@ -237,9 +255,13 @@ void Engine::alloc_all() {
     full_.v = dmalloc<uint16_t>(slices * slice_elems);
   } else {
     full_.cap = cap;  // geometry of the host pool
-    const size_t bytes = slices * slice_elems * 2;
-    VC_CK(cudaHostAlloc(reinterpret_cast<void**>(&host_k_), bytes, cudaHostAllocDefault));
-    VC_CK(cudaHostAlloc(reinterpret_cast<void**>(&host_v_), bytes, cudaHostAllocDefault));
+    // the host pool holds the offloaded slots only (resident slots live in HBM)
+    const size_t host_slices = static_cast<size_t>(cfg_.max_slots - cfg_.resident_slots) * L * m.n_kv;
+    const size_t bytes = host_slices * slice_elems * 2;
+    if (bytes > 0) {
+      VC_CK(cudaHostAlloc(reinterpret_cast<void**>(&host_k_), bytes, cudaHostAllocDefault));
+      VC_CK(cudaHostAlloc(reinterpret_cast<void**>(&host_v_), bytes, cudaHostAllocDefault));
+    }
     const size_t st_slices = static_cast<size_t>(cfg_.n_stage) * L * m.n_kv;
     stage_.cap = cap;
     stage_.k = dmalloc<uint16_t>(st_slices * slice_elems);
@@ -441,9 +463,10 @@ void Engine::add_request_synthetic(int slot, int n_ctx, int32_t pending, uint64_
   const float k_norm = static_cast<float>(1.0 / (65536.0 * std::sqrt(1.0 / 3.0)));
   const float k_out = static_cast<float>(outlier_scale / (65536.0 * std::sqrt(1.0 / 3.0)));
   const int period = outlier_channels > 0 ? m.d / outlier_channels : 0;
-  // tier 1 synthesises into staging slot 0, then D2H into the host pool
+  // tier 1 synthesises into the request's own staging slot (resident) or the
+  // scratch staging slot, then D2H into the host pool (offloaded)
   KvPool dst = cfg_.full_tier == 0 ? full_ : stage_;
-  const int dslot = cfg_.full_tier == 0 ? slot : 0;
+  const int dslot = cfg_.full_tier == 0 || resident(slot) ? slot : scratch_stage();
   const size_t slice_elems = static_cast<size_t>(full_.cap) * m.d;
   uint16_t* kb = dst.k + static_cast<size_t>(dslot) * n_slices * slice_elems;
   uint16_t* vb = dst.v + static_cast<size_t>(dslot) * n_slices * slice_elems;
@@ -460,11 +483,11 @@ void Engine::add_request_synthetic(int slot, int n_ctx, int32_t pending, uint64_
   s.live = true;
   s.committed = n_ctx;
   s.pending = pending;
-  if (cfg_.full_tier == 1 && n_ctx > 0) {
+  if (cfg_.full_tier == 1 && !resident(slot) && n_ctx > 0) {
     const size_t pitch = static_cast<size_t>(full_.cap) * m.d * 2;
     const size_t width = static_cast<size_t>(n_ctx) * m.d * 2;
-    uint16_t* hk = host_k_ + static_cast<size_t>(slot) * n_slices * slice_elems;
-    uint16_t* hv = host_v_ + static_cast<size_t>(slot) * n_slices * slice_elems;
+    uint16_t* hk = host_pool_k(slot);
+    uint16_t* hv = host_pool_v(slot);
     VC_CK(cudaMemcpy2DAsync(hk, pitch, kb, pitch, width, n_slices, cudaMemcpyDeviceToHost, st_));
     VC_CK(cudaMemcpy2DAsync(hv, pitch, vb, pitch, width, n_slices, cudaMemcpyDeviceToHost, st_));
   }
@@ -479,14 +502,15 @@ void Engine::add_request_kv(int slot, int n_ctx, int32_t pending, const uint16_t
   const size_t slice_elems = static_cast<size_t>(full_.cap) * m.d;
   const size_t pitch = slice_elems * 2, spitch = static_cast<size_t>(n_ctx) * m.d * 2;
   if (n_ctx > 0) {
-    if (cfg_.full_tier == 0) {
-      uint16_t* kb = full_.k + static_cast<size_t>(slot) * n_slices * slice_elems;
-      uint16_t* vb = full_.v + static_cast<size_t>(slot) * n_slices * slice_elems;
+    if (cfg_.full_tier == 0 || resident(slot)) {
+      const KvPool& dp = cfg_.full_tier == 0 ? full_ : stage_;
+      uint16_t* kb = dp.k + static_cast<size_t>(slot) * n_slices * slice_elems;
+      uint16_t* vb = dp.v + static_cast<size_t>(slot) * n_slices * slice_elems;
       VC_CK(cudaMemcpy2DAsync(kb, pitch, k, spitch, spitch, n_slices, cudaMemcpyHostToDevice, st_));
       VC_CK(cudaMemcpy2DAsync(vb, pitch, v, spitch, spitch, n_slices, cudaMemcpyHostToDevice, st_));
     } else {
-      uint16_t* hk = host_k_ + static_cast<size_t>(slot) * n_slices * slice_elems;
-      uint16_t* hv = host_v_ + static_cast<size_t>(slot) * n_slices * slice_elems;
+      uint16_t* hk = host_pool_k(slot);
+      uint16_t* hv = host_pool_v(slot);
       for (int i = 0; i < n_slices; ++i) {
         std::memcpy(hk + i * slice_elems, k + static_cast<size_t>(i) * n_ctx * m.d, spitch);
         std::memcpy(hv + i * slice_elems, v + static_cast<size_t>(i) * n_ctx * m.d, spitch);
@@ -559,12 +583,15 @@ void Engine::compress_as(int slot, double ratio, const int32_t* kept_host, int k
   const auto& m = cfg_.model;
   KvPool src = full_;
   int src_slot = slot;
-  if (cfg_.full_tier == 1) {
-    // stream the prefix through staging slot 0
-    uint64_t id = swap_begin(slot, 0);
+  if (resident(slot)) {  // the full KV is already in its own staging slot
+    src = stage_;
+    src_slot = slot;
+  } else if (cfg_.full_tier == 1) {
+    // stream the prefix through the scratch staging slot
+    uint64_t id = swap_begin(slot, scratch_stage());
     swap_wait(id);
     src = stage_;
-    src_slot = 0;
+    src_slot = scratch_stage();
   }
   if (drop_mode()) {
     compress_drop(slot, src, src_slot, ratio, kept_host, k_host);
@@ -1018,7 +1045,9 @@ std::vector<int32_t> Engine::accept_commit(int slot, const std::vector<int32_t>&
     if (now - ng_now * VC_QGROUP > tail_cap_ - cfg_.max_x - 1)
       throw ContractViolation("accept: request exceeds max_ctx (compressed tail overflow)");
   }
-  if (staged) {
+  if (staged && resident(slot) && stage != slot)
+    throw ContractViolation("accept: a resident slot verifies in its own staging slot");
+  if (staged && !resident(slot)) {
     if (stage < 0) throw ContractViolation("accept: staged verify needs its stage");
     // exact KV of the committed rows back to the host pool
     const int n_slices = m.layers * m.n_kv;
@@ -1026,8 +1055,9 @@ std::vector<int32_t> Engine::accept_commit(int slot, const std::vector<int32_t>&
     const size_t off = static_cast<size_t>(old) * m.d;
     const size_t width = static_cast<size_t>(now - old) * m.d * 2;
     const size_t slice_elems = static_cast<size_t>(full_.cap) * m.d;
-    uint16_t* hk = host_k_ + static_cast<size_t>(slot) * n_slices * slice_elems + off;
-    uint16_t* hv = host_v_ + static_cast<size_t>(slot) * n_slices * slice_elems + off;
+    (void)slice_elems;
+    uint16_t* hk = host_pool_k(slot) + off;
+    uint16_t* hv = host_pool_v(slot) + off;
     const uint16_t* sk = stage_.k + static_cast<size_t>(stage) * n_slices * slice_elems + off;
     const uint16_t* sv = stage_.v + static_cast<size_t>(stage) * n_slices * slice_elems + off;
     VC_CK(cudaMemcpy2DAsync(hk, pitch, sk, pitch, width, n_slices, cudaMemcpyDeviceToHost, st_));
@@ -1208,7 +1238,9 @@ uint64_t Engine::prefix_load(int slot, int what, int32_t pending) {
 // ------------------------------------------------------------- host tier
 uint64_t Engine::swap_begin(int slot, int stage) {
   if (cfg_.full_tier != 1) throw ContractViolation("swap: host tier disabled");
-  if (stage < 0 || stage >= cfg_.n_stage) throw ContractViolation("swap: bad staging slot");
+  if (resident(slot)) throw ContractViolation("swap: the slot's full KV is resident (no host copy)");
+  if (stage < cfg_.resident_slots || stage >= cfg_.n_stage)
+    throw ContractViolation("swap: bad staging slot (resident slots own theirs)");
   const SeqState& s = seqs_.at(slot);
   const auto& m = cfg_.model;
   const int n_slices = m.layers * m.n_kv;
@@ -1217,8 +1249,8 @@ uint64_t Engine::swap_begin(int slot, int stage) {
   const size_t width = static_cast<size_t>(s.committed) * m.d * 2;
   uint16_t* dk = stage_.k + static_cast<size_t>(stage) * n_slices * slice_elems;
   uint16_t* dv = stage_.v + static_cast<size_t>(stage) * n_slices * slice_elems;
-  const uint16_t* hk = host_k_ + static_cast<size_t>(slot) * n_slices * slice_elems;
-  const uint16_t* hv = host_v_ + static_cast<size_t>(slot) * n_slices * slice_elems;
+  const uint16_t* hk = host_pool_k(slot);
+  const uint16_t* hv = host_pool_v(slot);
   // the stage may still be read by an in-flight step on the compute stream
   cudaEvent_t ready;
   VC_CK(cudaEventCreateWithFlags(&ready, cudaEventDisableTiming));

@@ -42,6 +42,11 @@ struct EngineConfig {
   int drop_window = 0;   // > 0: online sliding window over the tokens accepted after compress
   int full_tier = 0;    // 0: full KV in HBM; 1: pinned host pool + staging
   int n_stage = 2;      // HBM staging slots (tier 1)
+  // tier 1, per-request placement (the reference's B_g = B - B_c,
+  // analytics.cpp:45-82): slots [0, resident_slots) keep their full KV
+  // resident in HBM staging slot `slot` and have no host copy; the host pool
+  // holds slots [resident_slots, max_slots) only
+  int resident_slots = 0;
   int max_verify = 2;   // verify requests per step
   int use_graphs = 1;
   // head-sharded tensor parallelism: `model` is this rank's shard (n_q, n_kv,
@@ -153,6 +158,11 @@ class Engine {
   double h2d_ms() const { return h2d_ms_; }
   double h2d_bytes() const { return h2d_bytes_; }  // bytes of the completed reloads
 
+  // tier 1 placement: is the slot's full KV resident in HBM (its own stage)?
+  bool resident(int slot) const { return cfg_.full_tier == 1 && slot < cfg_.resident_slots; }
+  // staging slot used as scratch for offloaded requests (compress, synthesis)
+  int scratch_stage() const { return cfg_.resident_slots; }
+
   // ---- raw access for tests ------------------------------------------
   KvPool full_pool() const { return full_; }
   KvPool stage_pool() const { return stage_; }
@@ -162,8 +172,9 @@ class Engine {
   // kept positions (ascending) of the last drop-mode compress, row = layer*n_kv+head
   int last_kept_k() const { return last_kept_k_; }
   const int32_t* last_kept_device() const { return kept_buf_; }
-  uint16_t* host_pool_k() const { return host_k_; }
-  uint16_t* host_pool_v() const { return host_v_; }
+  // host-pool rows of an offloaded slot (nullptr for a resident slot)
+  uint16_t* host_pool_k(int slot) const;
+  uint16_t* host_pool_v(int slot) const;
   cudaStream_t stream() const { return st_; }
   size_t weight_bytes() const { return weight_bytes_; }
   size_t full_kv_bytes_per_token() const;

@@ -55,15 +55,19 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
   const bool staged = cfgE.full_tier == 1;
   if (sd.x < 1 || sd.x > cfgE.max_x) throw speckv::ConfigError("scheduled: x out of [1, max_x]");
   if (cfgE.quant_bits == 0 && cfgE.drop_ratio <= 0.0) throw vc::ContractViolation("scheduled: needs a compressed tier");
-  // per-request tier placement: requests [0, n_res) resident (B_g), the rest offloaded (B_c)
-  const int n_res = sd.n_resident;
+  // per-request tier placement: requests in the engine's resident slots keep
+  // their full KV in HBM (B_g), the rest are offloaded (B_c)
+  std::vector<int> res_idx;
+  std::vector<char> is_res(n, 0);
+  for (int i = 0; i < n; ++i)
+    if (en.resident(slots[i])) {
+      is_res[i] = 1;
+      res_idx.push_back(i);
+    }
+  const int n_res = static_cast<int>(res_idx.size());
   const int n_off = n - n_res;
   const int x_res = sd.x_resident > 0 ? sd.x_resident : sd.x;
-  if (n_res < 0 || n_res > n) throw speckv::ConfigError("scheduled: n_resident out of [0, n]");
-  if (n_res > 0 && !staged) throw speckv::ConfigError("scheduled: n_resident needs the host tier (full_tier 1)");
   if (x_res > cfgE.max_x) throw speckv::ConfigError("scheduled: x_resident out of [1, max_x]");
-  if (staged && n_res + (n_off > 0 ? 1 : 0) > cfgE.n_stage)
-    throw speckv::ConfigError("scheduled: n_resident + 1 rotating staging slot exceed n_stage");
   const size_t bpt = en.full_kv_bytes_per_token();
 
   // ---- measure T_iter if not given: one draft step over every request ----
@@ -99,12 +103,12 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
     kv_max = std::max(kv_max, kv);
     ratio[i] = std::min(1.0, static_cast<double>(en.compressed_bytes(slots[i])) / static_cast<double>(kv));
     compressed_all += static_cast<speckv::Bytes>(en.compressed_bytes(slots[i]));
-    if (i >= n_res) resident_total += static_cast<speckv::Bytes>(std::ceil(ratio[i] * kv));
+    if (!is_res[i]) resident_total += static_cast<speckv::Bytes>(std::ceil(ratio[i] * kv));
   }
   // HBM ring capacity: weights + resident compressed caches + one full KV per
   // rotating staging slot, so the ring never books more reloads than we can
   // stage.  Resident requests' full KV is a fixed carve-out outside the ring.
-  const int n_stage = staged ? cfgE.n_stage - n_res : std::max(1, cfgE.max_verify);
+  const int n_stage = staged ? cfgE.n_stage - cfgE.resident_slots : std::max(1, cfgE.max_verify);
   cfg.hardware.gpu_mem = sd.hbm_capacity > 0
                              ? sd.hbm_capacity
                              : cfg.model.weights_bytes + resident_total + std::max(1, n_stage) * (kv_max + kv_max / 64);
@@ -116,7 +120,9 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
   cfg.iteration_time = t_iter;
   cfg.batch_size = std::max(1, n_off);
   cfg.kv_full_bytes = kv_max;
-  cfg.compression_ratio = ratio[n_off > 0 ? n_res : 0];
+  int first_off = 0;
+  while (first_off < n - 1 && is_res[first_off]) ++first_off;
+  cfg.compression_ratio = ratio[first_off];
   cfg.output_tokens = sd.K;
   cfg.validate();
 
@@ -133,7 +139,8 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
   }();
   sched.set_expedite(expedite && staged);
   speckv::StepEvents ev;
-  for (int i = n_res; i < n; ++i) {
+  for (int i = 0; i < n; ++i) {
+    if (is_res[i]) continue;
     speckv::Request r;
     r.id = i;
     r.kv_full_bytes = static_cast<speckv::Bytes>(en.seq(slots[i]).committed) * bpt;
@@ -145,26 +152,27 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
   std::vector<int> produced(n, 0);
   std::vector<int> stage_of(n, -1);
   std::vector<int> free_stages;
-  for (int s = (staged ? cfgE.n_stage : n_stage) - 1; s >= n_res; --s) free_stages.push_back(s);
-  // residents: full KV loaded once into their own staging slot (placement,
-  // not part of the serving loop); first rounds of x_res - (i mod (x_res+1))
-  // drafts stagger their verifies over the x_res + 1 iterations of a round
+  const int stage_lo = staged ? cfgE.resident_slots : 0;
+  for (int s = (staged ? cfgE.n_stage : n_stage) - 1; s >= stage_lo; --s) free_stages.push_back(s);
+  // residents verify in their own staging slot (= their slot); first rounds
+  // of x_res - (j mod (x_res+1)) drafts stagger their verifies over the
+  // x_res + 1 iterations of a round
   std::vector<int> round_x(n, 0);
-  for (int i = 0; i < n_res; ++i) {
-    stage_of[i] = i;
-    en.swap_wait(en.swap_begin(slots[i], i));
-    round_x[i] = x_res - (i % (x_res + 1));
+  for (int j = 0; j < n_res; ++j) {
+    const int i = res_idx[j];
+    stage_of[i] = slots[i];
+    round_x[i] = x_res - (j % (x_res + 1));
   }
   int64_t res_verifies = 0;
   double res_accepted = 0;
   int64_t res_tokens_at_window = 0;
   auto res_tokens = [&] {
     int64_t t = 0;
-    for (int i = 0; i < n_res; ++i) t += produced[i];
+    for (int i : res_idx) t += produced[i];
     return t;
   };
   auto residents_active = [&] {
-    for (int i = 0; i < n_res; ++i)
+    for (int i : res_idx)
       if (produced[i] < sd.K) return true;
     return false;
   };
@@ -283,7 +291,7 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
     // resident requests: draft their round, then verify against their own
     // HBM-resident full KV (no reload)
     std::vector<int> res_drafting, res_verifying;
-    for (int i = 0; i < n_res; ++i) {
+    for (int i : res_idx) {
       if (produced[i] >= sd.K) continue;
       const auto& s = en.seq(slots[i]);
       if (static_cast<int>(s.drafted.size()) < round_x[i]) {
@@ -310,14 +318,14 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
       items.push_back(std::move(t));
       verifying.push_back(req);
     }
-    for (int i = 0; i < n_res; ++i) {
+    for (int i : res_idx) {
       if (produced[i] >= sd.K) continue;
       const auto& s = en.seq(slots[i]);
       if (static_cast<int>(s.drafted.size()) == round_x[i]) {
         vc::StepItem t;
         t.slot = slots[i];
         t.mode = vc::RowMode::Verify;
-        t.stage = i;
+        t.stage = slots[i];
         t.tokens.push_back(s.pending);
         t.tokens.insert(t.tokens.end(), s.drafted.begin(), s.drafted.end());
         items.push_back(std::move(t));
@@ -326,7 +334,14 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
     }
     std::vector<int32_t> row;
     if (!items.empty()) en.run_step(items, row);
-    if (it >= sd.warmup_iterations) rows_in_window += static_cast<double>(row.size());
+    if (it >= sd.warmup_iterations) {
+      rows_in_window += static_cast<double>(row.size());
+      for (const auto& t : items)
+        if (t.mode == vc::RowMode::Verify) {
+          st.timed_verifies += 1;
+          st.timed_verify_rows += static_cast<double>(t.tokens.size());
+        }
+    }
     const double t_emit = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     double emitted_now = 0;
     size_t off = 0;
@@ -355,7 +370,7 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
       const int x_r = static_cast<int>(en.seq(slots[i]).drafted.size());
       std::vector<int32_t> p(row.begin() + off, row.begin() + off + x_r + 1);
       off += x_r + 1;
-      const auto em = en.accept_commit(slots[i], p, i);
+      const auto em = en.accept_commit(slots[i], p, slots[i]);
       res_verifies += 1;
       res_accepted += static_cast<double>(em.size()) - 1;
       for (int32_t t : em)

@@ -102,14 +102,17 @@ class Engine:
 
     def __init__(self, model: ModelShape, *, max_slots=1, max_ctx=4096, max_x=16, quant_bits=4,
                  full_tier=0, n_stage=2, max_verify=2, use_graphs=True, device=0, drop_ratio=0.0,
-                 tp_size=1, tp_rank=0, drop_window=0):
+                 tp_size=1, tp_rank=0, drop_window=0, resident_slots=0):
         """quant_bits > 0: quant-uniform compressor (KIVI int4/int2);
         drop_ratio in (0, 1): drop-topk compressor keeping llround(c*T) tokens per
         (layer, head) -- the two are exclusive (compressor.cpp:245-254).
         tp_size > 1: this engine is rank tp_rank of a head-sharded tensor-parallel
         group (`model` is the full model; attach_nccl / attach_loopback before stepping).
         drop_window > 0 (drop-topk only): online mode -- tokens accepted after
-        compress stay in a sliding window of the latest drop_window..2*drop_window."""
+        compress stay in a sliding window of the latest drop_window..2*drop_window.
+        resident_slots > 0 (full_tier 1): per-request placement -- slots
+        [0, resident_slots) keep their full KV resident in HBM (the reference's
+        B_g), the pinned host pool holds the other slots only (B_c)."""
         self.lib = _lib.load()
         self.model = model
         self.max_x = max_x
@@ -117,7 +120,7 @@ class Engine:
                             model.d_head, model.ffn, model.rope_theta, model.rms_eps)
         rt = _lib.RuntimeDesc(max_slots, max_ctx, max_x, quant_bits, full_tier, n_stage,
                               max_verify, int(use_graphs), float(drop_ratio), int(tp_size), int(tp_rank),
-                              int(drop_window))
+                              int(drop_window), int(resident_slots))
         self.tp_size, self.tp_rank = int(tp_size), int(tp_rank)
         h = C.c_void_p()
         check(self.lib.vc_engine_create(C.byref(md), C.byref(rt), device, C.byref(h)))
@@ -362,13 +365,14 @@ class Engine:
         return ms.value, b.value
 
     def run_scheduled(self, slots, K, x, window, iteration_time=0.0, link_bandwidth=0.0,
-                      hbm_capacity=0, warmup_iterations=0, timed_iterations=0, n_resident=0, x_resident=0):
-        """n_resident > 0 (host tier): the first n_resident slots keep their full
-        KV resident in HBM (the reference's B_g = B - B_c; analytics.cpp:45-82)."""
+                      hbm_capacity=0, warmup_iterations=0, timed_iterations=0, x_resident=0):
+        """Requests in the engine's resident slots (resident_slots, the
+        reference's B_g; analytics.cpp:45-82) verify against their HBM-resident
+        full KV with x_resident-token rounds; the others are reloaded per verify."""
         s = np.ascontiguousarray(slots, np.int32)
         out = np.zeros((s.size, K), np.int32)
         sd = _lib.SchedDesc(x, window, iteration_time, link_bandwidth, hbm_capacity, K,
-                            warmup_iterations, timed_iterations, n_resident, x_resident)
+                            warmup_iterations, timed_iterations, x_resident)
         st = _lib.SchedStats()
         check(self.lib.vc_run_scheduled(self.h, _ptr(s, C.c_int), s.size, C.byref(sd),
                                         _ptr(out, C.c_int32), C.byref(st)))

@@ -40,12 +40,12 @@ def _base(weights, n, K=K, ctx=N_CTX):
 def test_mixed_tier_lossless(cuda, weights, n, n_res, n_stage, x, x_res):
     base = _base(weights, n)
     e = Engine(TINY, max_slots=n, max_ctx=N_CTX + 400, max_x=16, quant_bits=4, full_tier=1, n_stage=n_stage,
-               max_verify=n_stage + 2)
+               max_verify=n_stage + 2, resident_slots=n_res)
     e.load_weights(weights)
     for s in range(n):
         e.add_synthetic(s, N_CTX, 17 + s, seed=1 + s)
         e.compress(s)
-    out, st = e.run_scheduled(list(range(n)), K, x=x, window=32, n_resident=n_res, x_resident=x_res)
+    out, st = e.run_scheduled(list(range(n)), K, x=x, window=32, x_resident=x_res)
     np.testing.assert_array_equal(out, base)
     assert st["tokens"] == n * K
     assert st["resident_verifies"] > 0
@@ -58,16 +58,37 @@ def test_mixed_tier_lossless(cuda, weights, n, n_res, n_stage, x, x_res):
     e.close()
 
 
+def test_mixed_tier_config_errors():
+    """Rejected at engine creation, before any device allocation."""
+    with pytest.raises(_lib.ContractError):  # 3 residents + 1 rotating slot > 3 stages
+        Engine(TINY, max_slots=4, max_ctx=600, max_x=8, quant_bits=4, full_tier=1, n_stage=3, resident_slots=3)
+    with pytest.raises(_lib.ContractError):
+        Engine(TINY, max_slots=4, max_ctx=600, max_x=8, quant_bits=4, full_tier=1, n_stage=6, resident_slots=5)
+    with pytest.raises(_lib.ContractError):  # placement is a host-tier notion
+        Engine(TINY, max_slots=4, max_ctx=600, max_x=8, quant_bits=4, full_tier=0, resident_slots=2)
+
+
 @pytest.mark.gpu
-def test_mixed_tier_config_errors(cuda):
-    e = Engine(TINY, max_slots=4, max_ctx=600, max_x=8, quant_bits=4, full_tier=1, n_stage=3)
-    for s in range(4):
-        e.add_synthetic(s, 300, 17, seed=1)
+def test_resident_slots_have_no_host_copy(cuda, weights):
+    e = Engine(TINY, max_slots=3, max_ctx=600, max_x=8, quant_bits=4, full_tier=1, n_stage=3, resident_slots=2)
+    e.load_weights(weights)
+    for s in range(3):
+        e.add_synthetic(s, 300, 17, seed=1 + s)
         e.compress(s)
-    with pytest.raises(_lib.ConfigError):  # 3 residents + 1 rotating slot > 3 stages
-        e.run_scheduled([0, 1, 2, 3], 8, x=4, window=16, n_resident=3)
-    with pytest.raises(_lib.ConfigError):
-        e.run_scheduled([0, 1, 2, 3], 8, x=4, window=16, n_resident=5)
+    with pytest.raises(_lib.ContractError):
+        e.swap_begin(0, 2)   # a resident slot is never reloaded
+    with pytest.raises(_lib.ContractError):
+        e.swap_begin(2, 0)   # staging slot 0 belongs to resident slot 0
+    x = e.swap_begin(2, 2)
+    while not e.swap_poll(x):
+        pass
+    # resident slot 1's full KV sits in staging slot 1, offloaded slot 2's in the host pool
+    k, _ = T.synthetic_kv(TINY.layers, TINY.n_kv, 300, TINY.d_head, seed=2)
+    sk, _ = e.kv_read(1, 1, 1, 1, 0, 300)
+    np.testing.assert_array_equal(sk, k[1, 1])
+    k3, _ = T.synthetic_kv(TINY.layers, TINY.n_kv, 300, TINY.d_head, seed=3)
+    hk, _ = e.kv_read(2, 2, 0, 1, 0, 300)
+    np.testing.assert_array_equal(hk, k3[0, 1])
     e.close()
 
 
