@@ -158,6 +158,10 @@ int vc_engine_attach_nccl(vc_engine* e, const uint8_t* unique_id128);
 int vc_tp_loopback_create(int size, vc_tp_group** out);
 int vc_tp_loopback_destroy(vc_tp_group* g);
 int vc_engine_attach_loopback(vc_engine* e, vc_tp_group* g);
+/* Device time (us, CUDA events on the engine stream) of one combine: the
+ * all-gather of rows x hidden fp32 partials + the rank-order residual sum,
+ * averaged over reps; every rank of the group must call it together.       */
+int vc_tp_collective_bench(vc_engine* e, int rows, int reps, double* us);
 
 /* ---- requests ----------------------------------------------------------- */
 int vc_request_add_synthetic(vc_engine* e, int slot, int n_ctx, int32_t first_token, uint64_t seed,

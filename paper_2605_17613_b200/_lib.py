@@ -152,6 +152,7 @@ SIGNATURES = {
     "vc_tp_loopback_create": (I, [I, C.POINTER(P)]),
     "vc_tp_loopback_destroy": (I, [P]),
     "vc_engine_attach_loopback": (I, [P, P]),
+    "vc_tp_collective_bench": (I, [P, I, I, PD]),
     "vc_drop_indices": (I64, [I, I, I, I64, D, U64, I, PI64]),
     "vc_update_window": (I, [I, I, I, I, PI64, PI64, PI64, PI64, PI64, I64, PI64]),
     "vc_topk_select": (I, [P, I, I, I, P, P]),

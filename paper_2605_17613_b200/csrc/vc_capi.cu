@@ -141,6 +141,13 @@ int vc_engine_attach_nccl(vc_engine* e, const uint8_t* id) {
   });
 }
 
+int vc_tp_collective_bench(vc_engine* e, int rows, int reps, double* us) {
+  return guard([&] {
+    const double v = E(e).collective_bench(rows, reps);
+    if (us) *us = v;
+  });
+}
+
 int vc_tp_loopback_create(int size, vc_tp_group** out) {
   return guard([&] {
     if (!out) throw vc::ContractViolation("loopback: null out");

@@ -371,6 +371,24 @@ void Engine::attach_collective(std::unique_ptr<Collective> c) {
   launches_per_graph_.clear();
 }
 
+double Engine::collective_bench(int rows, int reps) {
+  if (!coll_) throw ContractViolation("collective_bench: no collective attached");
+  if (rows < 1 || rows > Mmax_ || reps < 1) throw ContractViolation("collective_bench: bad rows/reps");
+  const int H = cfg_.model.hidden;
+  float total = 0.f;
+  for (int r = 0; r <= reps; ++r) {  // r = 0 is warm-up
+    VC_CK(cudaEventRecord(ev_a_, st_));
+    coll_->all_gather(tp_y_, tp_g_, static_cast<size_t>(rows) * H, st_);
+    VC_LAUNCH(tp_residual(x_, tp_g_, cfg_.tp_size, rows, H, ss_part_, st_));
+    VC_CK(cudaEventRecord(ev_b_, st_));
+    VC_CK(cudaEventSynchronize(ev_b_));
+    float ms = 0.f;
+    VC_CK(cudaEventElapsedTime(&ms, ev_a_, ev_b_));
+    if (r > 0) total += ms;
+  }
+  return 1e3 * total / reps;
+}
+
 // ---------------------------------------------------------------- weights
 void Engine::init_weights_random(uint64_t seed, float stddev, float resid_std, float q_std) {
   const auto& m = cfg_.model;

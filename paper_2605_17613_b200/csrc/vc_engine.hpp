@@ -94,6 +94,9 @@ class Engine {
 
   // ---- tensor parallelism ---------------------------------------------
   void attach_collective(std::unique_ptr<Collective> c);
+  // Device time of one o_proj/down_proj combine (all-gather of rows x hidden
+  // fp32 partials + the rank-order residual sum), averaged over reps (us).
+  double collective_bench(int rows, int reps);
 
   // ---- weights -------------------------------------------------------
   void init_weights_random(uint64_t seed, float stddev, float resid_std = 0.f, float q_std = 0.f);

@@ -177,6 +177,12 @@ class Engine:
     def attach_loopback(self, group: "TpLoopback"):
         check(self.lib.vc_engine_attach_loopback(self.h, group.h))
 
+    def collective_bench(self, rows, reps=20) -> float:
+        """us per o_proj/down_proj combine (all-gather + rank-order sum) of `rows` rows."""
+        us = C.c_double()
+        check(self.lib.vc_tp_collective_bench(self.h, rows, reps, C.byref(us)))
+        return us.value
+
     def stats(self):
         n, b = C.c_uint64(), C.c_uint64()
         check(self.lib.vc_engine_stats(self.h, C.byref(n), C.byref(b)))
