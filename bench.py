@@ -60,6 +60,7 @@ def parse():
     p.add_argument("--x", type=int, default=0, help="draft horizon (0: per-tier default)")
     p.add_argument("--tier", default="host", choices=["host", "hbm"])
     p.add_argument("--window", type=int, default=0)
+    p.add_argument("--x-res", type=int, default=0, help="draft horizon of HBM-resident requests (placed tiers)")
     p.add_argument("--resid-std", type=float, default=-1.0,
                    help="std of o_proj/down_proj init (-1: calibrated 2e-4; 0: 0.02)")
     p.add_argument("--q-std", type=float, default=-1.0,
@@ -531,7 +532,7 @@ def main_capped(args, rank, world, local):
     torch.cuda.empty_cache()
 
     # ---------------- VeriCache arm: per-request placement
-    x, x_res = (args.x or 47), 6
+    x, x_res = (args.x or 47), (args.x_res or 6)
     it_w, it_k = (W + 2) * (x + 1), K * (x + 1)
     free = torch.cuda.mem_get_info()[0]
     max_ctx = ctx + it_w + it_k + 3 * (x + 1) + 8
@@ -607,7 +608,8 @@ def main_capped(args, rank, world, local):
                           "accepted_per_verify": round(st["mean_accept"], 3),
                           "h2d_gbs": round(bw_inter / 1e9, 1),
                           "link_busy_frac": round(st["h2d_ms"] / max(st["timed_wall_ms"], 1e-9), 3),
-                          "pinned_host_gb": round(host_need / 1e9, 1)},
+                          "pinned_host_gb": round(host_need / 1e9, 1),
+                          "gpu_busy_frac": round(st["timed_step_device_ms"] / max(st["timed_device_ms"], 1e-9), 3)},
             "step_roofline": step_roofline(r, shape, peak),
             "reference_model": {"baseline_full_kv_tok_s": round(b_max / ((weight_read_bytes(shape) + b_max * kv) / bw_hbm), 1),
                                 "optimize_intra": {"B_c": best[1], "x": best[2], "l": best[3],

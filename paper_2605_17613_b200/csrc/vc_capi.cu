@@ -832,6 +832,7 @@ int vc_kv_read(vc_engine* e, int pool, int slot, int layer, int head, int pos, i
     const size_t bytes = static_cast<size_t>(n) * m.d * 2;
     if (pool == 2) {
       if (!en.host_pool_k(slot)) throw vc::ContractViolation("no host pool (or the slot is resident)");
+      en.sync_host_pool();
       const size_t hoff = ((static_cast<size_t>(layer) * m.n_kv + head) * p.cap + pos) * m.d;
       std::memcpy(k, en.host_pool_k(slot) + hoff, bytes);
       std::memcpy(v, en.host_pool_v(slot) + hoff, bytes);

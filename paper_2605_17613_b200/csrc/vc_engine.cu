@@ -73,7 +73,46 @@ __global__ void synth_kv_kernel(uint16_t* kbase, uint16_t* vbase, int cap, int n
   }
 }
 
+// Step descriptors and results cross PCIe through mapped pinned memory read /
+// written by the SMs, never through the copy engine: the copy engine serves
+// the KV reloads, and a descriptor copy queued behind a reload stalls the
+// whole step until the reload lands (91 ms steps, tools/ce_probe.py).
+struct MappedSeg {
+  const uint32_t* src;
+  uint32_t* dst;
+  int words;
+};
+struct MappedCopy {
+  MappedSeg seg[3];
+  int n;
+};
+
+__global__ void mapped_copy_kernel(MappedCopy c) {
+  for (int s = 0; s < c.n; ++s) {
+    const MappedSeg g = c.seg[s];
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < g.words; i += gridDim.x * blockDim.x) g.dst[i] = g.src[i];
+  }
+}
+
+// A pitched copy issued as several smaller copies of `rows_per_copy` rows.
+// The copy engine runs one copy call to completion before it serves another
+// stream's copy: a step's tiny input H2D queued behind a 4.29 GB reload
+// waited the whole 77 ms (tools/ce_probe.py); behind a one-layer chunk it
+// waits microseconds.
+cudaError_t copy2d_chunked(void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t height,
+                           cudaMemcpyKind kind, cudaStream_t st, size_t rows_per_copy) {
+  for (size_t r = 0; r < height; r += rows_per_copy) {
+    const size_t h = std::min(rows_per_copy, height - r);
+    const cudaError_t e = cudaMemcpy2DAsync(static_cast<uint8_t*>(dst) + r * dpitch, dpitch,
+                                            static_cast<const uint8_t*>(src) + r * spitch, spitch, width, h, kind, st);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
+}
+
 }  // namespace
+
+void Engine::check_d2h() const { check_cuda(cudaStreamSynchronize(d2h_st_), "host pool commit"); }
 
 uint16_t* Engine::host_pool_k(int slot) const {
   if (!host_k_ || resident(slot)) return nullptr;
@@ -109,6 +148,9 @@ Engine::Engine(const EngineConfig& cfg, int device) : cfg_(cfg), device_(device)
   VC_CK(cudaSetDevice(device_));
   VC_CK(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
   VC_CK(cudaStreamCreateWithFlags(&copy_st_, cudaStreamNonBlocking));
+  VC_CK(cudaStreamCreateWithFlags(&d2h_st_, cudaStreamNonBlocking));
+  VC_CK(cudaEventCreateWithFlags(&ev_commit_, cudaEventDisableTiming));
+  VC_CK(cudaEventCreateWithFlags(&ev_d2h_, cudaEventDisableTiming));
   VC_CK(cudaEventCreate(&ev_a_));
   VC_CK(cudaEventCreate(&ev_b_));
   alloc_all();
@@ -119,6 +161,7 @@ Engine::~Engine() {
   cudaSetDevice(device_);
   cudaStreamSynchronize(st_);
   cudaStreamSynchronize(copy_st_);
+  cudaStreamSynchronize(d2h_st_);
   for (auto& [k, g] : graphs_) cudaGraphExecDestroy(g);
   for (auto& [k, x] : xfers_) {
     cudaEventDestroy(x.start);
@@ -138,8 +181,11 @@ Engine::~Engine() {
   if (h_out_) cudaFreeHost(h_out_);
   cudaEventDestroy(ev_a_);
   cudaEventDestroy(ev_b_);
+  cudaEventDestroy(ev_commit_);
+  cudaEventDestroy(ev_d2h_);
   cudaStreamDestroy(st_);
   cudaStreamDestroy(copy_st_);
+  cudaStreamDestroy(d2h_st_);
 }
 
 void Engine::attention_probe(int slot, int layer, int mode, const uint16_t* q_dev, int n_rows,
@@ -353,8 +399,10 @@ void Engine::alloc_all() {
   jobs_dev_ = dmalloc<QuantJob>(static_cast<size_t>(L) * m.n_kv);
   desc_bytes_ = Mmax_ * sizeof(int32_t) + Mmax_ * sizeof(RowDest) + n_seq_max * sizeof(AttnSeq) +
                 static_cast<size_t>(L) * m.n_kv * sizeof(QuantJob);
-  VC_CK(cudaHostAlloc(&h_desc_, desc_bytes_, cudaHostAllocDefault));
-  VC_CK(cudaHostAlloc(reinterpret_cast<void**>(&h_out_), Mmax_ * sizeof(int32_t), cudaHostAllocDefault));
+  VC_CK(cudaHostAlloc(&h_desc_, desc_bytes_, cudaHostAllocMapped));
+  VC_CK(cudaHostAlloc(reinterpret_cast<void**>(&h_out_), Mmax_ * sizeof(int32_t), cudaHostAllocMapped));
+  VC_CK(cudaHostGetDevicePointer(&d_hdesc_, h_desc_, 0));
+  VC_CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d_hout_), h_out_, 0));
 }
 
 void Engine::attach_collective(std::unique_ptr<Collective> c) {
@@ -587,8 +635,10 @@ void Engine::quantise_groups(int slot, int g0, int ng, const KvPool& src, int sr
     j.ng = ng;
     jobs[i] = j;
   }
-  VC_CK(cudaMemcpyAsync(jobs_dev_, jobs, n_slices * sizeof(QuantJob), cudaMemcpyHostToDevice, st_));
-  VC_LAUNCH(quant_kivi(jobs_dev_, n_slices, ng, m.d, cfg_.quant_bits, st_));
+  // the kernel reads the job table straight from mapped pinned memory (no copy engine)
+  const QuantJob* jobs_mapped = reinterpret_cast<const QuantJob*>(
+      static_cast<const uint8_t*>(d_hdesc_) + (reinterpret_cast<uint8_t*>(jobs) - static_cast<uint8_t*>(h_desc_)));
+  VC_LAUNCH(quant_kivi(jobs_mapped, n_slices, ng, m.d, cfg_.quant_bits, st_));
   // the pinned job table is reused by the next call: wait for the copy
   VC_CK(cudaStreamSynchronize(st_));
 }
@@ -916,16 +966,34 @@ void Engine::run_step(const std::vector<StepItem>& items, std::vector<int32_t>& 
     exec = itg->second;
   }
   VC_CK(cudaEventRecord(ev_a_, st_));
-  VC_CK(cudaMemcpyAsync(tok_in_, h_tok, Mb * sizeof(int32_t), cudaMemcpyHostToDevice, st_));
-  VC_CK(cudaMemcpyAsync(rows_dev_, h_rows, Mb * sizeof(RowDest), cudaMemcpyHostToDevice, st_));
-  VC_CK(cudaMemcpyAsync(seqs_dev_, h_seqs, k * sizeof(AttnSeq), cudaMemcpyHostToDevice, st_));
+  {  // descriptors: mapped pinned -> device by the SMs (see mapped_copy_kernel)
+    auto dev_of = [&](const void* h) {
+      return reinterpret_cast<const uint32_t*>(static_cast<const uint8_t*>(d_hdesc_) +
+                                               (static_cast<const uint8_t*>(h) - static_cast<const uint8_t*>(h_desc_)));
+    };
+    MappedCopy mc{};
+    mc.seg[0] = {dev_of(h_tok), reinterpret_cast<uint32_t*>(tok_in_), Mb};
+    mc.seg[1] = {dev_of(h_rows), reinterpret_cast<uint32_t*>(rows_dev_), static_cast<int>(Mb * sizeof(RowDest) / 4)};
+    mc.seg[2] = {dev_of(h_seqs), reinterpret_cast<uint32_t*>(seqs_dev_), static_cast<int>(k * sizeof(AttnSeq) / 4)};
+    mc.n = 3;
+    mapped_copy_kernel<<<8, 256, 0, st_>>>(mc);
+    VC_CK(cudaGetLastError());
+    ++launches_;
+  }
   if (exec) {
     VC_CK(cudaGraphLaunch(exec, st_));
     launches_ += launches_per_graph_[key];
   } else {
     enqueue_forward(Mb, nd, n1, nv, mrv, logits_host != nullptr);
   }
-  VC_CK(cudaMemcpyAsync(h_out_, tok_out_, M * sizeof(int32_t), cudaMemcpyDeviceToHost, st_));
+  {  // greedy tokens: device -> mapped pinned by the SMs
+    MappedCopy mc{};
+    mc.seg[0] = {reinterpret_cast<const uint32_t*>(tok_out_), reinterpret_cast<uint32_t*>(d_hout_), M};
+    mc.n = 1;
+    mapped_copy_kernel<<<1, 256, 0, st_>>>(mc);
+    VC_CK(cudaGetLastError());
+    ++launches_;
+  }
   if (logits_host)
     VC_CK(cudaMemcpyAsync(logits_host, logits_, static_cast<size_t>(M) * m.vocab * 4,
                           cudaMemcpyDeviceToHost, st_));
@@ -1078,8 +1146,17 @@ std::vector<int32_t> Engine::accept_commit(int slot, const std::vector<int32_t>&
     uint16_t* hv = host_pool_v(slot) + off;
     const uint16_t* sk = stage_.k + static_cast<size_t>(stage) * n_slices * slice_elems + off;
     const uint16_t* sv = stage_.v + static_cast<size_t>(stage) * n_slices * slice_elems + off;
-    VC_CK(cudaMemcpy2DAsync(hk, pitch, sk, pitch, width, n_slices, cudaMemcpyDeviceToHost, st_));
-    VC_CK(cudaMemcpy2DAsync(hv, pitch, sv, pitch, width, n_slices, cudaMemcpyDeviceToHost, st_));
+    // on its own stream: a D2H on the compute stream would queue behind an
+    // in-flight 4.29 GB reload in the copy engine and stall the next step for
+    // the rest of that reload (measured: 91 ms steps after every offloaded
+    // verify).  Later reloads (of this slot, or into this staging slot) wait
+    // for it through copy_st_.
+    VC_CK(cudaEventRecord(ev_commit_, st_));
+    VC_CK(cudaStreamWaitEvent(d2h_st_, ev_commit_, 0));
+    VC_CK(cudaMemcpy2DAsync(hk, pitch, sk, pitch, width, n_slices, cudaMemcpyDeviceToHost, d2h_st_));
+    VC_CK(cudaMemcpy2DAsync(hv, pitch, sv, pitch, width, n_slices, cudaMemcpyDeviceToHost, d2h_st_));
+    VC_CK(cudaEventRecord(ev_d2h_, d2h_st_));
+    VC_CK(cudaStreamWaitEvent(copy_st_, ev_d2h_, 0));
   }
   if (drop_mode()) {
     // the accepted rows' exact K/V (full tier) are appended to the compacted
@@ -1214,17 +1291,17 @@ uint64_t Engine::prefix_load(int slot, int what, int32_t pending) {
   if (what == 1) {
     const size_t slice_elems = static_cast<size_t>(full_.cap) * m.d;
     const size_t w = static_cast<size_t>(pre_T_) * m.d * 2;
-    VC_CK(cudaMemcpy2DAsync(full_.k + base * slice_elems, slice_elems * 2, pre_k_, w, w, n_slices,
-                            cudaMemcpyHostToDevice, copy_st_));
-    VC_CK(cudaMemcpy2DAsync(full_.v + base * slice_elems, slice_elems * 2, pre_v_, w, w, n_slices,
-                            cudaMemcpyHostToDevice, copy_st_));
+    VC_CK(copy2d_chunked(full_.k + base * slice_elems, slice_elems * 2, pre_k_, w, w, n_slices,
+                         cudaMemcpyHostToDevice, copy_st_, m.n_kv));
+    VC_CK(copy2d_chunked(full_.v + base * slice_elems, slice_elems * 2, pre_v_, w, w, n_slices,
+                         cudaMemcpyHostToDevice, copy_st_, m.n_kv));
   } else {
     const size_t words = quant_record_words(m.d, cfg_.quant_bits);
     const size_t slice_words = static_cast<size_t>(quant_.cap / VC_QGROUP) * words;
     const size_t rec_w = static_cast<size_t>(pre_ng_) * words * 4;
     if (rec_w)
-      VC_CK(cudaMemcpy2DAsync(quant_.rec + base * slice_words, slice_words * 4, pre_rec_, rec_w, rec_w, n_slices,
-                              cudaMemcpyHostToDevice, copy_st_));
+      VC_CK(copy2d_chunked(quant_.rec + base * slice_words, slice_words * 4, pre_rec_, rec_w, rec_w, n_slices,
+                           cudaMemcpyHostToDevice, copy_st_, m.n_kv));
     const size_t tail_w = static_cast<size_t>(pre_tc_) * m.d * 2;
     const size_t tpitch = static_cast<size_t>(tail_cap_) * m.d * 2;
     if (tail_w) {
@@ -1280,9 +1357,12 @@ uint64_t Engine::swap_begin(int slot, int stage) {
   VC_CK(cudaEventCreate(&x.start));
   VC_CK(cudaEventCreate(&x.done));
   VC_CK(cudaEventRecord(x.start, copy_st_));
-  if (width > 0) {
-    VC_CK(cudaMemcpy2DAsync(dk, pitch, hk, pitch, width, n_slices, cudaMemcpyHostToDevice, copy_st_));
-    VC_CK(cudaMemcpy2DAsync(dv, pitch, hv, pitch, width, n_slices, cudaMemcpyHostToDevice, copy_st_));
+  if (width > 0) {  // one layer (n_kv slices) of K, then of V, per copy
+    for (int l = 0; l < m.layers; ++l) {
+      const size_t o = static_cast<size_t>(l) * m.n_kv * slice_elems;
+      VC_CK(cudaMemcpy2DAsync(dk + o, pitch, hk + o, pitch, width, m.n_kv, cudaMemcpyHostToDevice, copy_st_));
+      VC_CK(cudaMemcpy2DAsync(dv + o, pitch, hv + o, pitch, width, m.n_kv, cudaMemcpyHostToDevice, copy_st_));
+    }
   }
   VC_CK(cudaEventRecord(x.done, copy_st_));
   const uint64_t id = next_xfer_++;

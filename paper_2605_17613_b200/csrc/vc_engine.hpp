@@ -176,6 +176,8 @@ class Engine {
   int last_kept_k() const { return last_kept_k_; }
   const int32_t* last_kept_device() const { return kept_buf_; }
   // host-pool rows of an offloaded slot (nullptr for a resident slot)
+  // wait for the commits still copying exact rows into the host pool
+  void sync_host_pool() const { check_d2h(); }
   uint16_t* host_pool_k(int slot) const;
   uint16_t* host_pool_v(int slot) const;
   cudaStream_t stream() const { return st_; }
@@ -209,6 +211,7 @@ class Engine {
     uint16_t* lm_head = nullptr;
   };
   void alloc_all();
+  void check_d2h() const;
   void set_kv_rows(const std::vector<StepItem>& items, std::vector<RowDest>& rows) const;
   void enqueue_forward(int M, int n_draft, int n_dense1, int n_densev, int max_rows_v,
                        bool want_logits);
@@ -219,6 +222,8 @@ class Engine {
   EngineConfig cfg_;
   int device_ = 0;
   cudaStream_t st_ = nullptr, copy_st_ = nullptr;
+  cudaStream_t d2h_st_ = nullptr;  // commit of exact rows back to the host pool
+  cudaEvent_t ev_commit_ = nullptr, ev_d2h_ = nullptr;
   Weights w_;
   void* weight_blob_ = nullptr;
   size_t weight_bytes_ = 0;
@@ -256,6 +261,8 @@ class Engine {
   QuantJob* jobs_dev_ = nullptr;
   // pinned staging of per-step descriptors
   void* h_desc_ = nullptr;
+  void* d_hdesc_ = nullptr;     // device view of the mapped h_desc_
+  int32_t* d_hout_ = nullptr;   // device view of the mapped h_out_
   size_t desc_bytes_ = 0;
   int32_t* h_out_ = nullptr;
   std::vector<SeqState> seqs_;
