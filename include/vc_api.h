@@ -86,6 +86,9 @@ typedef struct {
                          full KV resident in HBM (staging slot `slot`, no host copy,
                          never reloaded); the pinned host pool holds the other
                          (offloaded) slots only.  n_stage >= resident_slots + 1. */
+  int draft_depth;    /* rows one drafting request may carry in a step: 1 + the
+                         auxiliary proposals of the two-level composition
+                         (vc_run_speculative_composed); 0 or 1 = plain drafting */
 } vc_runtime_desc;
 
 /* Mirrors speckv::CompressedKVMeta (compressor.hpp:56-65).  Quant-uniform:
@@ -273,6 +276,25 @@ int vc_run_speculative(vc_engine* e, const int* slots, int n, int K, int x, int3
  * one full-KV pass.  ngram_rounds [n] = rounds that used an n-gram draft.     */
 int vc_run_speculative_ngram(vc_engine* e, const int* slots, int n, int K, int x, int ngram, int32_t* out,
                              int32_t* rounds, int max_rounds, int* n_rounds, int* ngram_rounds, double* ms);
+
+/* Two-level composition (composed_accept_length,
+ * analytics.cpp:413-422): lock-step rounds of x OUTER draft passes over the
+ * compressed KV; at each outer position an auxiliary prompt-lookup drafter
+ * (`ngram`-token key over the request's own context) proposes up to depth-1
+ * more tokens that ride the same pass as extra rows (needs draft_depth >=
+ * depth); proposals the compressed model confirms join the draft window, then
+ * one full-KV verify checks it all.  out [n][K].                            */
+typedef struct {
+  int64_t rounds, verifies, tokens;
+  int64_t draft_steps;    /* compressed-model passes */
+  int64_t drafted;        /* draft tokens verified (all rounds) */
+  int64_t aux_proposed;   /* auxiliary tokens offered to the compressed model */
+  int64_t aux_accepted;   /* of those, confirmed by it (gamma_e = accepted / proposed) */
+  double mean_accept;     /* accepted drafted tokens per verify */
+  double ms;              /* device time of the loop */
+} vc_compose_stats;
+int vc_run_speculative_composed(vc_engine* e, const int* slots, int n, int K, int x, int ngram, int depth,
+                                int32_t* out, vc_compose_stats* stats);
 
 /* Swap-scheduled loop (tier 1): SpecScheduler semantics drive real draft
  * rows, verify rows and H2D reloads (Algorithm 1).     */

@@ -43,7 +43,7 @@ class RuntimeDesc(C.Structure):
                 ("quant_bits", C.c_int), ("full_tier", C.c_int), ("n_stage", C.c_int),
                 ("max_verify", C.c_int), ("use_graphs", C.c_int), ("drop_ratio", C.c_double),
                 ("tp_size", C.c_int), ("tp_rank", C.c_int), ("drop_window", C.c_int),
-                ("resident_slots", C.c_int)]
+                ("resident_slots", C.c_int), ("draft_depth", C.c_int)]
 
 
 class CompressedMeta(C.Structure):
@@ -97,6 +97,12 @@ class LoopMetrics(C.Structure):
                 ("completed", C.c_int64), ("unserved", C.c_int64), ("clock_s", C.c_double),
                 ("wall_ms", C.c_double), ("mean_batch", C.c_double), ("max_batch", C.c_int),
                 ("peak_hbm_bytes", C.c_int64), ("full_batch_throughput", C.c_double)]
+
+
+class ComposeStats(C.Structure):
+    _fields_ = [("rounds", C.c_int64), ("verifies", C.c_int64), ("tokens", C.c_int64), ("draft_steps", C.c_int64),
+                ("drafted", C.c_int64), ("aux_proposed", C.c_int64), ("aux_accepted", C.c_int64),
+                ("mean_accept", C.c_double), ("ms", C.c_double)]
 
 
 class RequestDesc(C.Structure):
@@ -169,6 +175,7 @@ SIGNATURES = {
     "vc_run_decode": (I, [P, PI, I, I, PI32, PD]),
     "vc_run_speculative": (I, [P, PI, I, I, I, PI32, PI32, I, PI, PD]),
     "vc_run_speculative_ngram": (I, [P, PI, I, I, I, I, PI32, PI32, I, PI, PI, PD]),
+    "vc_run_speculative_composed": (I, [P, PI, I, I, I, I, I, PI32, C.POINTER(ComposeStats)]),
     "vc_run_scheduled": (I, [P, PI, I, C.POINTER(SchedDesc), PI32, C.POINTER(SchedStats)]),
     "vc_prefix_store": (I, [P, I]),
     "vc_prefix_load": (I, [P, I, I, C.c_int32, PU64]),

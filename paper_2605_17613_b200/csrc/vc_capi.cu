@@ -93,6 +93,7 @@ int vc_engine_create(const vc_model_desc* model, const vc_runtime_desc* rt, int 
     c.drop_ratio = rt->drop_ratio;
     c.drop_window = rt->drop_window;
     c.resident_slots = rt->resident_slots;
+    c.draft_depth = rt->draft_depth > 1 ? rt->draft_depth : 1;
     if (c.drop_window < 0 || (c.drop_window > 0 && c.drop_ratio <= 0.0))
       throw speckv::ConfigError("compressor: drop_window needs the drop-topk compressor");
     c.tp_size = rt->tp_size > 1 ? rt->tp_size : 1;
@@ -750,7 +751,120 @@ void speculative_loop(vc::Engine& en, const int* slots, int n, int K, int x, int
   }
 }
 
+// Two-level composition (composed_accept_length,
+// /root/reference/proj/src/analytics.cpp:413-422): each round makes x OUTER
+// draft passes of the target model over the compressed KV; at every outer
+// position an auxiliary drafter (prompt lookup over the request's own
+// context, `ngram`-token key) proposes up to depth-1 further tokens, which
+// ride the same pass as extra rows (engine draft rows, causal in the tail).
+// The compressed model keeps its own prediction p0 and each proposal e_j that
+// its previous row confirmed (p_{j-1} == e_j), so an outer pass appends
+// 1 + (confirmed proposals) tokens.  The full-KV verify then checks the whole
+// window; losslessness still rests on the verifier alone.
+void composed_loop(vc::Engine& en, const int* slots, int n, int K, int x, int ngram, int depth, int32_t* out,
+                   vc_compose_stats* stats) {
+  const auto& cfg = en.config();
+  if (x < 1 || x > cfg.max_x) throw speckv::ConfigError("composed: x out of [1, max_x]");
+  if (ngram < 1 || depth < 1) throw speckv::ConfigError("composed: ngram and depth must be >= 1");
+  if (depth > std::max(1, cfg.draft_depth)) throw speckv::ConfigError("composed: depth exceeds the engine's draft_depth");
+  if (cfg.full_tier != 0) throw vc::ContractViolation("composed loop needs the HBM full tier");
+  vc_compose_stats st{};
+  std::vector<int> produced(n, 0);
+  std::vector<vc::StepItem> its;
+  std::vector<int32_t> row;
+  double accepted_sum = 0;
+  cudaEvent_t w0, w1;
+  vc::check_cuda(cudaEventCreate(&w0), "event");
+  vc::check_cuda(cudaEventCreate(&w1), "event");
+  vc::check_cuda(cudaEventRecord(w0, en.stream()), "event");
+  for (;;) {
+    std::vector<int> act;
+    for (int i = 0; i < n; ++i)
+      if (produced[i] < K) act.push_back(i);
+    if (act.empty()) break;
+    st.rounds += 1;
+    for (int pass = 0; pass < x; ++pass) {  // x outer positions
+      std::vector<int> who;
+      std::vector<std::vector<int32_t>> props;
+      its.clear();
+      for (int i : act) {
+        const vc::SeqState& s = en.seq(slots[i]);
+        const int room = cfg.max_x - static_cast<int>(s.drafted.size());
+        if (room < 1) continue;
+        std::vector<int32_t> ctx = s.history.empty() ? std::vector<int32_t>{s.pending} : s.history;
+        ctx.insert(ctx.end(), s.drafted.begin(), s.drafted.end());
+        auto prop = ngram_proposal(ctx, ngram, std::min(depth - 1, room - 1));
+        vc::StepItem t;
+        t.slot = slots[i];
+        t.mode = vc::RowMode::Draft;
+        t.tokens = {ctx.back()};
+        t.tokens.insert(t.tokens.end(), prop.begin(), prop.end());
+        its.push_back(std::move(t));
+        who.push_back(i);
+        props.push_back(std::move(prop));
+      }
+      if (its.empty()) break;
+      en.run_step(its, row);
+      st.draft_steps += 1;
+      size_t off = 0;
+      for (size_t a = 0; a < who.size(); ++a) {
+        const int sl = slots[who[a]];
+        const auto& pr = props[a];
+        en.push_draft(sl, row[off]);
+        int matched = 0;
+        for (size_t j = 0; j < pr.size(); ++j) {
+          if (row[off + j] != pr[j]) break;  // row j assumed e_{j+1}: valid only if p_j confirmed it
+          en.push_draft(sl, row[off + j + 1]);
+          ++matched;
+        }
+        st.aux_proposed += static_cast<int64_t>(pr.size());
+        st.aux_accepted += matched;
+        off += pr.size() + 1;
+      }
+    }
+    its.assign(act.size(), vc::StepItem{});  // one verify pass over the full KV
+    for (size_t a = 0; a < act.size(); ++a) {
+      const vc::SeqState& s = en.seq(slots[act[a]]);
+      its[a].slot = slots[act[a]];
+      its[a].mode = vc::RowMode::Verify;
+      its[a].tokens.push_back(s.pending);
+      its[a].tokens.insert(its[a].tokens.end(), s.drafted.begin(), s.drafted.end());
+    }
+    en.run_step(its, row);
+    size_t off = 0;
+    for (size_t a = 0; a < act.size(); ++a) {
+      const int i = act[a];
+      const size_t xi = en.seq(slots[i]).drafted.size();
+      std::vector<int32_t> p(row.begin() + off, row.begin() + off + xi + 1);
+      off += xi + 1;
+      st.drafted += static_cast<int64_t>(xi);
+      const auto em = en.accept_commit(slots[i], p);
+      st.verifies += 1;
+      accepted_sum += static_cast<double>(em.size()) - 1;
+      for (int32_t t : em)
+        if (produced[i] < K) {
+          out[static_cast<size_t>(i) * K + produced[i]++] = t;
+          st.tokens += 1;
+        }
+    }
+  }
+  vc::check_cuda(cudaEventRecord(w1, en.stream()), "event");
+  vc::check_cuda(cudaEventSynchronize(w1), "event");
+  float dms = 0.f;
+  vc::check_cuda(cudaEventElapsedTime(&dms, w0, w1), "event");
+  cudaEventDestroy(w0);
+  cudaEventDestroy(w1);
+  st.ms = dms;
+  st.mean_accept = st.verifies ? accepted_sum / static_cast<double>(st.verifies) : 0.0;
+  if (stats) *stats = st;
+}
+
 }  // namespace
+
+int vc_run_speculative_composed(vc_engine* e, const int* slots, int n, int K, int x, int ngram, int depth,
+                                int32_t* out, vc_compose_stats* stats) {
+  return guard([&] { composed_loop(E(e), slots, n, K, x, ngram, depth, out, stats); });
+}
 
 int vc_run_speculative(vc_engine* e, const int* slots, int n, int K, int x, int32_t* out,
                        int32_t* rounds, int max_rounds, int* n_rounds, double* ms) {

@@ -346,7 +346,7 @@ void Engine::alloc_all() {
   }
   max_chunks_d_ = (cap + VC_DENSE_CHUNK - 1) / VC_DENSE_CHUNK;
   // ---- activations ---------------------------------------------------------
-  Mmax_ = static_cast<int>(round_up(cfg_.max_slots + cfg_.max_verify * (cfg_.max_x + 1), 64));
+  Mmax_ = static_cast<int>(round_up(draft_rows_max() + cfg_.max_verify * (cfg_.max_x + 1), 64));
   x_ = dmalloc<float>(static_cast<size_t>(Mmax_) * H);
   // tiled GEMM inputs carry 128 rows of slack (the last NT block may overrun Mp)
   xn_ = dmalloc<uint16_t>(static_cast<size_t>(Mmax_ + 128) * (H > F ? H : F));
@@ -387,14 +387,14 @@ void Engine::alloc_all() {
   tok_in_ = dmalloc<int32_t>(Mmax_);
   tok_out_ = dmalloc<int32_t>(Mmax_);
   const size_t prow_draft =
-      static_cast<size_t>(cfg_.max_slots + 4) *
+      static_cast<size_t>(draft_rows_max() + 4) *
       (drop_mode() ? max_chunks_x_ : draft_parts_per_seq(max_chunks_q_, tail_cap_));
   const size_t prow_dense = static_cast<size_t>(Mmax_) * max_chunks_d_;
   const size_t prow = (prow_draft + prow_dense) * m.n_q;
   part_.o = dmalloc<float>(prow * d);
   part_.ml = dmalloc<float>(prow * 2);
   rows_dev_ = dmalloc<RowDest>(Mmax_);
-  const int n_seq_max = 2 * (cfg_.max_slots + 4) + cfg_.max_verify + 4;
+  const int n_seq_max = 2 * (draft_rows_max() + 4) + cfg_.max_verify + 4;
   seqs_dev_ = dmalloc<AttnSeq>(n_seq_max);
   jobs_dev_ = dmalloc<QuantJob>(static_cast<size_t>(L) * m.n_kv);
   desc_bytes_ = Mmax_ * sizeof(int32_t) + Mmax_ * sizeof(RowDest) + n_seq_max * sizeof(AttnSeq) +
@@ -863,7 +863,7 @@ int bucket_seqs(int n) { return n == 0 ? 0 : (n + 3) / 4 * 4; }
 void Engine::run_step(const std::vector<StepItem>& items, std::vector<int32_t>& out,
                       float* logits_host) {
   const auto& m = cfg_.model;
-  const int n_seq_max = 2 * (cfg_.max_slots + 4) + cfg_.max_verify + 4;
+  const int n_seq_max = 2 * (draft_rows_max() + 4) + cfg_.max_verify + 4;
   int32_t* h_tok = static_cast<int32_t*>(h_desc_);
   RowDest* h_rows = reinterpret_cast<RowDest*>(h_tok + Mmax_);
   AttnSeq* h_seqs = reinterpret_cast<AttnSeq*>(h_rows + Mmax_);
@@ -877,24 +877,32 @@ void Engine::run_step(const std::vector<StepItem>& items, std::vector<int32_t>& 
     AttnSeq a{};
     a.row0 = M;
     a.n_rows = n;
-    if (it.mode == RowMode::Draft && drop_mode()) {
-      // drop tier: dense attention over the compacted kept + appended tokens
-      if (n != 1) throw ContractViolation("draft rows take one token");
-      if (s.drop_len + s.draft_len + 1 > drop_.cap) throw ContractViolation("drop tier full");
-      h_tok[M] = it.tokens[0];
-      h_rows[M] = RowDest{3, it.slot, s.drop_len + s.draft_len, s.committed + s.draft_len};
-      a.slot = it.slot;
-      a.kv_len = s.drop_len + s.draft_len + 1;
-      drafts.push_back(a);
-    } else if (it.mode == RowMode::Draft) {
-      if (cfg_.quant_bits == 0 || n != 1) throw ContractViolation("draft rows need the compressed tier");
-      if (s.tail_committed + s.draft_len + 1 > tail_cap_) throw ContractViolation("draft window overflow");
-      h_tok[M] = it.tokens[0];
-      h_rows[M] = RowDest{1, it.slot, s.tail_committed + s.draft_len, s.committed + s.draft_len};
-      a.slot = it.slot;
-      a.n_groups = s.n_groups;
-      a.tail_len = s.tail_committed + s.draft_len + 1;
-      drafts.push_back(a);
+    if (it.mode == RowMode::Draft) {
+      // n >= 1 rows over the compressed tier: the next draft input and, for
+      // the two-level composition, an auxiliary drafter's proposals after it
+      // (row i sees the draft window plus rows 0..i -- the qkv epilogue writes
+      // every row's K/V into the tail before attention runs).  Each row is its
+      // own draft sequence; rows past the accepted ones are overwritten later.
+      if (s.draft_len + n > cfg_.max_x + 1) throw ContractViolation("draft window overflow (rows past max_x)");
+      for (int i = 0; i < n; ++i) {
+        AttnSeq r = a;
+        r.row0 = M + i;
+        r.n_rows = 1;
+        r.slot = it.slot;
+        h_tok[M + i] = it.tokens[i];
+        if (drop_mode()) {  // drop tier: dense attention over the compacted kept + appended tokens
+          if (s.drop_len + s.draft_len + i + 1 > drop_.cap) throw ContractViolation("drop tier full");
+          h_rows[M + i] = RowDest{3, it.slot, s.drop_len + s.draft_len + i, s.committed + s.draft_len + i};
+          r.kv_len = s.drop_len + s.draft_len + i + 1;
+        } else {
+          if (cfg_.quant_bits == 0) throw ContractViolation("draft rows need the compressed tier");
+          if (s.tail_committed + s.draft_len + i + 1 > tail_cap_) throw ContractViolation("draft window overflow");
+          h_rows[M + i] = RowDest{1, it.slot, s.tail_committed + s.draft_len + i, s.committed + s.draft_len + i};
+          r.n_groups = s.n_groups;
+          r.tail_len = s.tail_committed + s.draft_len + i + 1;
+        }
+        drafts.push_back(r);
+      }
     } else {
       const bool staged = cfg_.full_tier == 1;
       if (staged && it.mode == RowMode::Decode) throw ContractViolation("decode rows need the HBM full tier");

@@ -14,6 +14,7 @@
 #pragma once
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <map>
 #include <memory>
@@ -47,6 +48,9 @@ struct EngineConfig {
   // resident in HBM staging slot `slot` and have no host copy; the host pool
   // holds slots [resident_slots, max_slots) only
   int resident_slots = 0;
+  // rows a drafting request may carry per step (1 + auxiliary proposals of
+  // the two-level composition); sizes the activation and partial buffers
+  int draft_depth = 1;
   int max_verify = 2;   // verify requests per step
   int use_graphs = 1;
   // head-sharded tensor parallelism: `model` is this rank's shard (n_q, n_kv,
@@ -162,6 +166,7 @@ class Engine {
   double h2d_bytes() const { return h2d_bytes_; }  // bytes of the completed reloads
 
   // tier 1 placement: is the slot's full KV resident in HBM (its own stage)?
+  int draft_rows_max() const { return cfg_.max_slots * std::max(1, cfg_.draft_depth); }
   bool resident(int slot) const { return cfg_.full_tier == 1 && slot < cfg_.resident_slots; }
   // staging slot used as scratch for offloaded requests (compress, synthesis)
   int scratch_stage() const { return cfg_.resident_slots; }

@@ -102,7 +102,7 @@ class Engine:
 
     def __init__(self, model: ModelShape, *, max_slots=1, max_ctx=4096, max_x=16, quant_bits=4,
                  full_tier=0, n_stage=2, max_verify=2, use_graphs=True, device=0, drop_ratio=0.0,
-                 tp_size=1, tp_rank=0, drop_window=0, resident_slots=0):
+                 tp_size=1, tp_rank=0, drop_window=0, resident_slots=0, draft_depth=1):
         """quant_bits > 0: quant-uniform compressor (KIVI int4/int2);
         drop_ratio in (0, 1): drop-topk compressor keeping llround(c*T) tokens per
         (layer, head) -- the two are exclusive (compressor.cpp:245-254).
@@ -120,7 +120,7 @@ class Engine:
                             model.d_head, model.ffn, model.rope_theta, model.rms_eps)
         rt = _lib.RuntimeDesc(max_slots, max_ctx, max_x, quant_bits, full_tier, n_stage,
                               max_verify, int(use_graphs), float(drop_ratio), int(tp_size), int(tp_rank),
-                              int(drop_window), int(resident_slots))
+                              int(drop_window), int(resident_slots), int(draft_depth))
         self.tp_size, self.tp_rank = int(tp_size), int(tp_rank)
         h = C.c_void_p()
         check(self.lib.vc_engine_create(C.byref(md), C.byref(rt), device, C.byref(h)))
@@ -357,6 +357,17 @@ class Engine:
                                                 _ptr(out, C.c_int32), _ptr(rounds, C.c_int32), max_rounds,
                                                 _ptr(nr, C.c_int), _ptr(ng, C.c_int), C.byref(ms)))
         return out, [rounds[i, : nr[i]].tolist() for i in range(s.size)], ng.tolist(), ms.value
+
+    def run_speculative_composed(self, slots, K, x, ngram=2, depth=2):
+        """Two-level composition: x outer compressed-KV draft
+        passes per round, each carrying up to depth-1 prompt-lookup proposals the
+        compressed model may confirm -> (tokens [n][K], stats dict)."""
+        s = np.ascontiguousarray(slots, np.int32)
+        out = np.zeros((s.size, K), np.int32)
+        st = _lib.ComposeStats()
+        check(self.lib.vc_run_speculative_composed(self.h, _ptr(s, C.c_int), s.size, K, x, ngram, depth,
+                                                   _ptr(out, C.c_int32), C.byref(st)))
+        return out, {f: getattr(st, f) for f, _ in st._fields_}
 
     def timing(self, reset=False):
         ms, n = C.c_double(), C.c_int64()
