@@ -277,6 +277,15 @@ int vc_run_speculative(vc_engine* e, const int* slots, int n, int K, int x, int3
 int vc_run_speculative_ngram(vc_engine* e, const int* slots, int n, int K, int x, int ngram, int32_t* out,
                              int32_t* rounds, int max_rounds, int* n_rounds, int* ngram_rounds, double* ms);
 
+/* One request of a synthetic workload: prefix length, first input token,
+ * prefix-KV seed (vc_request_add_synthetic), arrival time (ms on the loop clock). */
+typedef struct {
+  int n_ctx;
+  int32_t first_token;
+  uint64_t seed;
+  double arrival_ms;
+} vc_request_desc;
+
 /* Two-level composition (composed_accept_length,
  * analytics.cpp:413-422): lock-step rounds of x OUTER draft passes over the
  * compressed KV; at each outer position an auxiliary prompt-lookup drafter
@@ -317,6 +326,13 @@ typedef struct {
    * drafted, staggered so about B_g / (x_resident + 1) windows verify per
    * iteration.                                                              */
   int x_resident;
+  /* Requests arriving during the run (simulate_staggered's arrivals,
+   * sim.cpp:227-302): arrival_ms on the loop's host clock; each is admitted
+   * FIFO into a slot a finished request freed (synthetic prefix KV written
+   * and compressed at admission; a resident slot's request is resident).
+   * out then holds n + n_arrivals rows; latencies are completion - arrival. */
+  const vc_request_desc* arrivals;
+  int n_arrivals;
 } vc_sched_desc;
 
 typedef struct {
@@ -379,14 +395,7 @@ typedef struct {
                                    slot occupied: the capacity-capped steady state */
 } vc_loop_metrics;
 
-/* One request of a synthetic workload: prefix length, first input token,
- * prefix-KV seed (vc_request_add_synthetic), arrival time (ms on the loop clock). */
-typedef struct {
-  int n_ctx;
-  int32_t first_token;
-  uint64_t seed;
-  double arrival_ms;
-} vc_request_desc;
+
 
 /* The reference's full-KV baseline (baseline_full_kv, sim.cpp:418-494) on the
  * real engine: requests are admitted FIFO while a full-KV slot is free (the

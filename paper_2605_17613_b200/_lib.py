@@ -69,11 +69,15 @@ class StepItem(C.Structure):
                 ("tokens", C.POINTER(C.c_int32))]
 
 
+class RequestDesc(C.Structure):
+    _fields_ = [("n_ctx", C.c_int), ("first_token", C.c_int32), ("seed", C.c_uint64), ("arrival_ms", C.c_double)]
+
+
 class SchedDesc(C.Structure):
     _fields_ = [("x", C.c_int), ("window", C.c_int), ("iteration_time", C.c_double),
                 ("link_bandwidth", C.c_double), ("hbm_capacity", C.c_int64), ("K", C.c_int),
                 ("warmup_iterations", C.c_int64), ("timed_iterations", C.c_int64),
-                ("x_resident", C.c_int)]
+                ("x_resident", C.c_int), ("arrivals", C.POINTER(RequestDesc)), ("n_arrivals", C.c_int)]
 
 
 class SchedStats(C.Structure):
@@ -104,9 +108,6 @@ class ComposeStats(C.Structure):
                 ("drafted", C.c_int64), ("aux_proposed", C.c_int64), ("aux_accepted", C.c_int64),
                 ("mean_accept", C.c_double), ("ms", C.c_double)]
 
-
-class RequestDesc(C.Structure):
-    _fields_ = [("n_ctx", C.c_int), ("first_token", C.c_int32), ("seed", C.c_uint64), ("arrival_ms", C.c_double)]
 
 
 class RemoteDesc(C.Structure):

@@ -540,6 +540,22 @@ __global__ void __launch_bounds__(kWarps * 32, NREP == 8 ? 3 : VC_DRAFT_MINB) dr
     if (++cpart == kUPG) {
       cpart = 0;
       next_task(cc);
+      // fold the column's correction into O once per group: the MMA carries
+      // 1024 * sum(P') (the int->fp16 bias) that corr cancels; left to grow
+      // over a long range (a warp takes T / warps groups -- 14 at 16 x 32K)
+      // the two fp32 sums cancel catastrophically (logits off by 20-40% at
+      // 24-48 x 32K; tests/test_real_shapes.py::test_draft_batched_equals_single)
+      float c0 = corr0, c1 = corr1;
+#pragma unroll
+      for (int o = 4; o < 32; o <<= 1) {
+        c0 += __shfl_xor_sync(0xffffffffu, c0, o);
+        c1 += __shfl_xor_sync(0xffffffffu, c1, o);
+      }
+#pragma unroll
+      for (int ct = 0; ct < KS; ++ct) {
+        oacc[ct][0] += c0; oacc[ct][1] += c1; oacc[ct][2] += c0; oacc[ct][3] += c1;
+      }
+      corr0 = corr1 = 0.f;
     }
   }
   emit();  // the last (sequence, head) of the range

@@ -549,13 +549,23 @@ void Engine::add_request_synthetic(int slot, int n_ctx, int32_t pending, uint64_
   s.live = true;
   s.committed = n_ctx;
   s.pending = pending;
+  scratch_slot_ = -1;
   if (cfg_.full_tier == 1 && !resident(slot) && n_ctx > 0) {
+    scratch_slot_ = slot;
+    scratch_stage_used_ = dslot;
+    check_d2h();  // earlier commits into this slot's host rows land first
     const size_t pitch = static_cast<size_t>(full_.cap) * m.d * 2;
     const size_t width = static_cast<size_t>(n_ctx) * m.d * 2;
     uint16_t* hk = host_pool_k(slot);
     uint16_t* hv = host_pool_v(slot);
-    VC_CK(cudaMemcpy2DAsync(hk, pitch, kb, pitch, width, n_slices, cudaMemcpyDeviceToHost, st_));
-    VC_CK(cudaMemcpy2DAsync(hv, pitch, vb, pitch, width, n_slices, cudaMemcpyDeviceToHost, st_));
+    // the host copy goes on the commit stream (never the compute stream:
+    // it would queue behind an in-flight reload); later reloads wait for it
+    VC_CK(cudaEventRecord(ev_commit_, st_));
+    VC_CK(cudaStreamWaitEvent(d2h_st_, ev_commit_, 0));
+    VC_CK(copy2d_chunked(hk, pitch, kb, pitch, width, n_slices, cudaMemcpyDeviceToHost, d2h_st_, m.n_kv));
+    VC_CK(copy2d_chunked(hv, pitch, vb, pitch, width, n_slices, cudaMemcpyDeviceToHost, d2h_st_, m.n_kv));
+    VC_CK(cudaEventRecord(ev_d2h_, d2h_st_));
+    VC_CK(cudaStreamWaitEvent(copy_st_, ev_d2h_, 0));
   }
   VC_CK(cudaStreamSynchronize(st_));
 }
@@ -654,6 +664,10 @@ void Engine::compress_as(int slot, double ratio, const int32_t* kept_host, int k
   if (resident(slot)) {  // the full KV is already in its own staging slot
     src = stage_;
     src_slot = slot;
+  } else if (cfg_.full_tier == 1 && scratch_slot_ == slot) {
+    // just synthesised: the full KV is still in the scratch staging slot
+    src = stage_;
+    src_slot = scratch_stage_used_;
   } else if (cfg_.full_tier == 1) {
     // stream the prefix through the scratch staging slot
     uint64_t id = swap_begin(slot, scratch_stage());
@@ -864,6 +878,7 @@ void Engine::run_step(const std::vector<StepItem>& items, std::vector<int32_t>& 
                       float* logits_host) {
   const auto& m = cfg_.model;
   const int n_seq_max = 2 * (draft_rows_max() + 4) + cfg_.max_verify + 4;
+  scratch_slot_ = -1;  // a step may write any staging slot
   int32_t* h_tok = static_cast<int32_t*>(h_desc_);
   RowDest* h_rows = reinterpret_cast<RowDest*>(h_tok + Mmax_);
   AttnSeq* h_seqs = reinterpret_cast<AttnSeq*>(h_rows + Mmax_);
@@ -1342,6 +1357,7 @@ uint64_t Engine::prefix_load(int slot, int what, int32_t pending) {
 uint64_t Engine::swap_begin(int slot, int stage) {
   if (cfg_.full_tier != 1) throw ContractViolation("swap: host tier disabled");
   if (resident(slot)) throw ContractViolation("swap: the slot's full KV is resident (no host copy)");
+  scratch_slot_ = -1;
   if (stage < cfg_.resident_slots || stage >= cfg_.n_stage)
     throw ContractViolation("swap: bad staging slot (resident slots own theirs)");
   const SeqState& s = seqs_.at(slot);

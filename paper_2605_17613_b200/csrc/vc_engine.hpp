@@ -169,7 +169,9 @@ class Engine {
   int draft_rows_max() const { return cfg_.max_slots * std::max(1, cfg_.draft_depth); }
   bool resident(int slot) const { return cfg_.full_tier == 1 && slot < cfg_.resident_slots; }
   // staging slot used as scratch for offloaded requests (compress, synthesis)
-  int scratch_stage() const { return cfg_.resident_slots; }
+  int scratch_stage() const { return scratch_override_ >= 0 ? scratch_override_ : cfg_.resident_slots; }
+  // the serving loop lends a free rotating staging slot for an admission
+  void set_scratch_stage(int stage) { scratch_override_ = stage; }
 
   // ---- raw access for tests ------------------------------------------
   KvPool full_pool() const { return full_; }
@@ -246,6 +248,10 @@ class Engine {
   int32_t* kept_buf_ = nullptr; // [layers*n_kv][k] kept positions of the last compress
   int last_kept_k_ = 0;
   int kept_cap_ = 0;            // kept positions per slice kept_buf_ holds
+  int scratch_override_ = -1;   // staging slot used as scratch (-1: the first rotating one)
+  // offloaded slot whose freshly synthesised full KV still sits in staging
+  // slot scratch_stage_used_ (compress() then skips the reload)
+  int scratch_slot_ = -1, scratch_stage_used_ = -1;
   uint16_t *host_k_ = nullptr, *host_v_ = nullptr;
   // prefix store (pinned): full K/V [slice][T][d], records [slice][ng][words], tails [slice][tc][d]
   uint16_t *pre_k_ = nullptr, *pre_v_ = nullptr, *pre_kt_ = nullptr, *pre_vt_ = nullptr;

@@ -57,8 +57,16 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
   if (cfgE.quant_bits == 0 && cfgE.drop_ratio <= 0.0) throw vc::ContractViolation("scheduled: needs a compressed tier");
   // per-request tier placement: requests in the engine's resident slots keep
   // their full KV in HBM (B_g), the rest are offloaded (B_c)
+  // requests: [0, n) present at the start in `slots`; [n, n + n_arrivals)
+  // arrive later (sd.arrivals, host clock) and are admitted FIFO into the
+  // slots finished requests free (simulate_staggered's arrivals, sim.cpp:227-302)
+  const int n_arr = sd.n_arrivals > 0 ? sd.n_arrivals : 0;
+  if (n_arr > 0 && !sd.arrivals) throw vc::ContractViolation("scheduled: null arrivals");
+  const int n_total = n + n_arr;
+  std::vector<int> slot_of(n_total, -1);
+  for (int i = 0; i < n; ++i) slot_of[i] = slots[i];
   std::vector<int> res_idx;
-  std::vector<char> is_res(n, 0);
+  std::vector<char> is_res(n_total, 0);
   for (int i = 0; i < n; ++i)
     if (en.resident(slots[i])) {
       is_res[i] = 1;
@@ -96,7 +104,7 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
   cfg.model.weights_bytes = static_cast<speckv::Bytes>(en.weight_bytes());
   cfg.model.kv_bytes_per_token = static_cast<speckv::Bytes>(bpt);
   speckv::Bytes kv_max = 0, resident_total = 0, compressed_all = 0;
-  std::vector<double> ratio(n);
+  std::vector<double> ratio(n_total, 0.0);
   for (int i = 0; i < n; ++i) {
     const auto& s = en.seq(slots[i]);
     const speckv::Bytes kv = static_cast<speckv::Bytes>(s.committed) * bpt;
@@ -113,7 +121,7 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
                              ? sd.hbm_capacity
                              : cfg.model.weights_bytes + resident_total + std::max(1, n_stage) * (kv_max + kv_max / 64);
   cfg.acceptance.kind = speckv::AcceptanceModel::Kind::PerTokenIid;
-  for (double c : ratio) cfg.acceptance.per_token_prob[c] = 0.99;
+  for (int i = 0; i < n; ++i) cfg.acceptance.per_token_prob[ratio[i]] = 0.99;
   cfg.draft_length = sd.x;
   cfg.lookahead_window = sd.window;
   cfg.iteration_time_mode = speckv::IterationTimeMode::Fixed;
@@ -149,15 +157,15 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
     ev.arrivals.push_back(r);
   }
 
-  std::vector<int> produced(n, 0);
-  std::vector<int> stage_of(n, -1);
+  std::vector<int> produced(n_total, 0);
+  std::vector<int> stage_of(n_total, -1);
   std::vector<int> free_stages;
   const int stage_lo = staged ? cfgE.resident_slots : 0;
   for (int s = (staged ? cfgE.n_stage : n_stage) - 1; s >= stage_lo; --s) free_stages.push_back(s);
   // residents verify in their own staging slot (= their slot); first rounds
   // of x_res - (j mod (x_res+1)) drafts stagger their verifies over the
   // x_res + 1 iterations of a round
-  std::vector<int> round_x(n, 0);
+  std::vector<int> round_x(n_total, 0);
   for (int j = 0; j < n_res; ++j) {
     const int i = res_idx[j];
     stage_of[i] = slots[i];
@@ -178,7 +186,11 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
   };
   // reference metrics on the loop's host clock (sim.cpp:80-109)
   std::vector<std::pair<double, double>> emission;  // (seconds, tokens)
-  std::vector<double> done_at(n, -1.0);
+  std::vector<double> done_at(n_total, -1.0), t_arr(n_total, 0.0);
+  std::deque<int> queue;      // arrived, waiting for a slot
+  std::vector<int> free_slots;
+  int next_arr = 0;
+  std::vector<char> freed(n_total, 0);  // request's slot returned to free_slots
   const double h2d_ms_start = en.h2d_ms();
   struct Xfer {
     uint64_t id;
@@ -195,7 +207,7 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
   vc_sched_stats st{};
   double accepted_sum = 0;
   const auto t0 = std::chrono::steady_clock::now();
-  const std::int64_t guard_iters = 10000 + 20LL * (sd.window + sd.x) + 64LL * sd.K * n;
+  const std::int64_t guard_iters = 10000 + 20LL * (sd.window + sd.x) + 64LL * sd.K * n_total;
 
   int64_t tokens_at_window = 0;
   double rows_in_window = 0;
@@ -213,12 +225,64 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
   const bool adapt = sd.iteration_time <= 0;
   double stall_ms = 0.0, h2d_ms_at_window = 0.0, h2d_bytes_at_window = 0.0;
   auto t_prev = std::chrono::steady_clock::now();
-  for (std::int64_t it = 0; !sched.idle() || !ev.arrivals.empty() || residents_active(); ++it) {
+  for (std::int64_t it = 0;
+       !sched.idle() || !ev.arrivals.empty() || residents_active() || next_arr < n_arr || !queue.empty(); ++it) {
     if (it > guard_iters) throw speckv::ConfigError("scheduled loop stalled");
+    if (n_arr > 0) {  // arrivals and admissions
+      const double now_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+      while (next_arr < n_arr && sd.arrivals[next_arr].arrival_ms <= now_ms) {
+        t_arr[n + next_arr] = sd.arrivals[next_arr].arrival_ms / 1e3;
+        queue.push_back(n + next_arr++);
+      }
+      for (int r = 0; r < n_total; ++r)  // finished requests give their slot back
+        if (slot_of[r] >= 0 && !freed[r] && produced[r] >= sd.K &&
+            (is_res[r] || !sched.sessions().count(static_cast<speckv::RequestId>(r)))) {
+          freed[r] = 1;
+          free_slots.push_back(slot_of[r]);
+        }
+      while (!queue.empty() && !free_slots.empty()) {
+        const int r = queue.front();
+        const int slot = free_slots.front();
+        const bool res = en.resident(slot);
+        int scratch = -1;
+        if (staged && !res) {  // an offloaded admission borrows a free rotating stage
+          if (free_stages.empty()) break;
+          scratch = free_stages.back();
+          free_stages.pop_back();
+          en.set_scratch_stage(scratch);
+        }
+        queue.pop_front();
+        free_slots.erase(free_slots.begin());
+        const vc_request_desc& q = sd.arrivals[r - n];
+        en.add_request_synthetic(slot, q.n_ctx, q.first_token, q.seed, 4, 10.f);
+        en.compress(slot);
+        if (scratch >= 0) {
+          en.set_scratch_stage(-1);
+          free_stages.push_back(scratch);
+        }
+        slot_of[r] = slot;
+        const speckv::Bytes kv = static_cast<speckv::Bytes>(q.n_ctx) * bpt;
+        ratio[r] = std::min(1.0, static_cast<double>(en.compressed_bytes(slot)) / static_cast<double>(kv));
+        if (res) {
+          is_res[r] = 1;
+          res_idx.push_back(r);
+          stage_of[r] = slot;
+          round_x[r] = x_res;
+        } else {
+          speckv::Request a;
+          a.id = r;
+          a.kv_full_bytes = kv;
+          a.compression_ratio = ratio[r];
+          a.output_tokens = sd.K;
+          ev.arrivals.push_back(a);
+          cfg.acceptance.per_token_prob[ratio[r]] = 0.99;
+        }
+      }
+    }
     if (adapt) sched.set_planning_iteration_time(t_plan);
     if (it == sd.warmup_iterations) {  // open the timed window
       int64_t tk = 0;
-      for (int i = 0; i < n; ++i) tk += produced[i];
+      for (int i = 0; i < n_total; ++i) tk += produced[i];
       tokens_at_window = tk;
       res_tokens_at_window = res_tokens();
       en.reset_timing();
@@ -260,7 +324,7 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
         const int s = free_stages.back();
         free_stages.pop_back();
         stage_of[req] = s;
-        inflight.push_back({en.swap_begin(slots[req], s), r.id, req});
+        inflight.push_back({en.swap_begin(slot_of[req], s), r.id, req});
         kicked.insert(r.id);
       }
     }
@@ -281,9 +345,9 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
     // 4. one forward pass: drafting rows + verify windows
     std::vector<vc::StepItem> items;
     for (speckv::RequestId id : pr.drafted) {
-      const auto& s = en.seq(slots[id]);
+      const auto& s = en.seq(slot_of[id]);
       vc::StepItem t;
-      t.slot = slots[id];
+      t.slot = slot_of[id];
       t.mode = vc::RowMode::Draft;
       t.tokens = {s.drafted.empty() ? s.pending : s.drafted.back()};
       items.push_back(std::move(t));
@@ -293,10 +357,10 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
     std::vector<int> res_drafting, res_verifying;
     for (int i : res_idx) {
       if (produced[i] >= sd.K) continue;
-      const auto& s = en.seq(slots[i]);
+      const auto& s = en.seq(slot_of[i]);
       if (static_cast<int>(s.drafted.size()) < round_x[i]) {
         vc::StepItem t;
-        t.slot = slots[i];
+        t.slot = slot_of[i];
         t.mode = vc::RowMode::Draft;
         t.tokens = {s.drafted.empty() ? s.pending : s.drafted.back()};
         items.push_back(std::move(t));
@@ -306,11 +370,11 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
     std::vector<int> verifying;
     for (const auto& v : pr.verifies) {
       const int req = static_cast<int>(v.request);
-      const auto& s = en.seq(slots[req]);
+      const auto& s = en.seq(slot_of[req]);
       if (static_cast<int>(s.drafted.size()) != v.drafted)
         throw vc::ContractViolation("scheduled loop: draft count diverged from the scheduler");
       vc::StepItem t;
-      t.slot = slots[req];
+      t.slot = slot_of[req];
       t.mode = vc::RowMode::Verify;
       t.stage = staged ? stage_of[req] : -1;
       t.tokens.push_back(s.pending);
@@ -320,12 +384,12 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
     }
     for (int i : res_idx) {
       if (produced[i] >= sd.K) continue;
-      const auto& s = en.seq(slots[i]);
+      const auto& s = en.seq(slot_of[i]);
       if (static_cast<int>(s.drafted.size()) == round_x[i]) {
         vc::StepItem t;
-        t.slot = slots[i];
+        t.slot = slot_of[i];
         t.mode = vc::RowMode::Verify;
-        t.stage = slots[i];
+        t.stage = slot_of[i];
         t.tokens.push_back(s.pending);
         t.tokens.insert(t.tokens.end(), s.drafted.begin(), s.drafted.end());
         items.push_back(std::move(t));
@@ -345,14 +409,14 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
     const double t_emit = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     double emitted_now = 0;
     size_t off = 0;
-    for (speckv::RequestId id : pr.drafted) en.push_draft(slots[id], row[off++]);
-    for (int i : res_drafting) en.push_draft(slots[i], row[off++]);
+    for (speckv::RequestId id : pr.drafted) en.push_draft(slot_of[id], row[off++]);
+    for (int i : res_drafting) en.push_draft(slot_of[i], row[off++]);
     meas.accepted.clear();
     for (int req : verifying) {
-      const int x_r = static_cast<int>(en.seq(slots[req]).drafted.size());
+      const int x_r = static_cast<int>(en.seq(slot_of[req]).drafted.size());
       std::vector<int32_t> p(row.begin() + off, row.begin() + off + x_r + 1);
       off += x_r + 1;
-      const auto em = en.accept_commit(slots[req], p, staged ? stage_of[req] : -1);
+      const auto em = en.accept_commit(slot_of[req], p, staged ? stage_of[req] : -1);
       meas.accepted.push_back(static_cast<int>(em.size()) - 1);
       accepted_sum += static_cast<double>(em.size()) - 1;
       for (int32_t t : em)
@@ -367,10 +431,10 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
       }
     }
     for (int i : res_verifying) {
-      const int x_r = static_cast<int>(en.seq(slots[i]).drafted.size());
+      const int x_r = static_cast<int>(en.seq(slot_of[i]).drafted.size());
       std::vector<int32_t> p(row.begin() + off, row.begin() + off + x_r + 1);
       off += x_r + 1;
-      const auto em = en.accept_commit(slots[i], p, slots[i]);
+      const auto em = en.accept_commit(slot_of[i], p, slot_of[i]);
       res_verifies += 1;
       res_accepted += static_cast<double>(em.size()) - 1;
       for (int32_t t : em)
@@ -412,7 +476,8 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
   // a bounded window may end mid-round: land the in-flight reloads and roll
   // the open draft rounds back, so the slots can be scheduled again
   for (const Xfer& x : inflight) en.swap_wait(x.id);
-  for (int i = 0; i < n; ++i) en.discard_drafts(slots[i]);
+  for (int i = 0; i < n_total; ++i)
+    if (slot_of[i] >= 0 && !freed[i]) en.discard_drafts(slot_of[i]);
   st.wall_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
   {  // SimMetrics on the host clock (finalize_metrics, sim.cpp:98-109)
     const double end = st.wall_ms / 1e3;
@@ -423,9 +488,9 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
     }
     st.throughput = end > 0 ? total / end : 0.0;
     st.warm_throughput = end > 0 ? warm / (0.8 * end) : 0.0;
-    std::vector<double> lat;
-    for (double d : done_at)
-      if (d >= 0) lat.push_back(d);
+    std::vector<double> lat;  // completion - arrival (host clock)
+    for (int r = 0; r < n_total; ++r)
+      if (done_at[r] >= 0) lat.push_back(done_at[r] - t_arr[r]);
     auto pct = [&](double q) {
       if (lat.empty()) return 0.0;
       std::sort(lat.begin(), lat.end());
@@ -444,7 +509,7 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
   accepted_sum += res_accepted;
   st.resident_verifies = res_verifies;
   st.resident_accept = res_verifies ? res_accepted / static_cast<double>(res_verifies) : 0.0;
-  for (int i = 0; i < n; ++i) st.tokens += produced[i];
+  for (int i = 0; i < n_total; ++i) st.tokens += produced[i];
   if (st.iterations > sd.warmup_iterations) {
     st.timed_iterations = st.iterations - sd.warmup_iterations;
     st.timed_tokens = st.tokens - tokens_at_window;

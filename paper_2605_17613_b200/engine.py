@@ -382,14 +382,21 @@ class Engine:
         return ms.value, b.value
 
     def run_scheduled(self, slots, K, x, window, iteration_time=0.0, link_bandwidth=0.0,
-                      hbm_capacity=0, warmup_iterations=0, timed_iterations=0, x_resident=0):
+                      hbm_capacity=0, warmup_iterations=0, timed_iterations=0, x_resident=0, arrivals=None):
         """Requests in the engine's resident slots (resident_slots, the
         reference's B_g; analytics.cpp:45-82) verify against their HBM-resident
-        full KV with x_resident-token rounds; the others are reloaded per verify."""
+        full KV with x_resident-token rounds; the others are reloaded per verify.
+        arrivals = [(n_ctx, first_token, seed, arrival_ms)]: requests that arrive
+        during the run and take the slots finished requests free (out gains a
+        row per arrival)."""
         s = np.ascontiguousarray(slots, np.int32)
-        out = np.zeros((s.size, K), np.int32)
+        arr = arrivals or []
+        out = np.zeros((s.size + len(arr), K), np.int32)
+        ad = (_lib.RequestDesc * max(len(arr), 1))(*[_lib.RequestDesc(int(a), int(b), int(c), float(d))
+                                                     for a, b, c, d in arr])
         sd = _lib.SchedDesc(x, window, iteration_time, link_bandwidth, hbm_capacity, K,
-                            warmup_iterations, timed_iterations, x_resident)
+                            warmup_iterations, timed_iterations, x_resident,
+                            ad if arr else None, len(arr))
         st = _lib.SchedStats()
         check(self.lib.vc_run_scheduled(self.h, _ptr(s, C.c_int), s.size, C.byref(sd),
                                         _ptr(out, C.c_int32), C.byref(st)))

@@ -120,3 +120,31 @@ def test_fifo_baseline_arrivals(cuda, weights):
     base = _base(weights, 2, K=4)
     np.testing.assert_array_equal(out, base)
     e.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("tier,resident", [(0, 0), (1, 1), (1, 0)])
+def test_scheduled_loop_with_arrivals(cuda, weights, tier, resident):
+    """Requests arriving during the run take the slots finished ones free
+    (simulate_staggered's arrivals, sim.cpp:227-302); every request, initial
+    or arrived, emits exactly its own full-KV greedy decode."""
+    n, n_arr, K = 3, 4, 24
+    reqs = [(N_CTX - 100 * i, 17 + i, 1 + i) for i in range(n + n_arr)]
+    ref = Engine(TINY, max_slots=n + n_arr, max_ctx=N_CTX + K + 64, max_x=1, quant_bits=0)
+    ref.load_weights(weights)
+    for i, (ctx, tok, seed) in enumerate(reqs):
+        ref.add_synthetic(i, ctx, tok, seed=seed)
+    base, _ = ref.autoregress(list(range(n + n_arr)), K)
+    ref.close()
+    kw = dict(full_tier=1, n_stage=resident + 2, resident_slots=resident) if tier else {}
+    e = Engine(TINY, max_slots=n, max_ctx=N_CTX + 400, max_x=16, quant_bits=4, max_verify=4, **kw)
+    e.load_weights(weights)
+    for i in range(n):
+        e.add_synthetic(i, reqs[i][0], reqs[i][1], seed=reqs[i][2])
+        e.compress(i)
+    arrivals = [(reqs[n + j][0], reqs[n + j][1], reqs[n + j][2], 5.0 * j) for j in range(n_arr)]
+    out, st = e.run_scheduled(list(range(n)), K, x=6, window=32, arrivals=arrivals)
+    np.testing.assert_array_equal(out, base)
+    assert st["tokens"] == (n + n_arr) * K
+    assert 0 < st["p50_latency_s"] <= st["p99_latency_s"]
+    e.close()
