@@ -783,7 +783,7 @@ def main():
     n_dev = torch.cuda.device_count()
     torch.cuda.set_device(local % n_dev)
     local = local % n_dev
-    numa = bind_numa_local(local) if world > 1 else []  # NUMA-local pinned pool per rank
+    numa = bind_numa_local(local)  # NUMA-local pinned pool (per rank under torchrun)
     dist = None
     coll_dev = "cuda"
     if world > 1:

@@ -33,6 +33,54 @@
 
 namespace speckv::gpu {
 
+// speckv::compress(spec, shape, ratio, seed) (compressor.hpp:70-71) with the
+// reference's own types, applied to a request of the GPU engine: the shape is
+// the request's committed prefix, the GPU tier receives the data (vc_compress_spec:
+// KIVI codes, or the kept rows of the drop tier), and the returned metadata
+// is the reference's -- for the dropping kinds the exact dropped_indices the
+// reference computes for `seed` (the complement of the tier's kept rows).
+// Works with the reference headers or include/speckv_b200.hpp.
+template <class Meta, class Spec>
+Meta compress(vc_engine* e, int slot, const Spec& spec, double ratio, std::uint64_t seed = 0) {
+  vc_compressor_spec cs{};
+  const int kind = static_cast<int>(spec.kind);  // DropUniform 0, DropWindow 1, QuantUniform 2
+  cs.kind = kind;
+  cs.mode = static_cast<int>(spec.mode);
+  cs.bits = spec.bits;
+  cs.window = spec.window;
+  cs.sink_tokens = spec.sink_tokens;
+  vc_compressed_meta out{};
+  if (vc_compress_spec(e, slot, &cs, ratio, seed, &out) != VC_OK)
+    throw std::runtime_error(std::string("vericache: ") + vc_last_error());
+  Meta meta;
+  meta.bit_scheme = out.bit_scheme;
+  meta.payload_bytes = out.payload_bytes;
+  vc_seq_state st{};
+  vc_request_state(e, slot, &st);
+  // one kept list per (layer, head) of the engine's geometry
+  std::vector<std::int32_t> kept;
+  const bool dropping = kind != 2;
+  int layers = 0, heads = 0;
+  vc_engine_geometry(e, &layers, &heads);
+  meta.dropped_indices.assign(layers, std::vector<std::vector<std::int64_t>>(heads));
+  if (dropping) {
+    for (int l = 0; l < layers; ++l)
+      for (int h = 0; h < heads; ++h) {
+        int n = 0;
+        vc_drop_kept(e, l, h, nullptr, 0, &n);
+        kept.assign(static_cast<size_t>(n), 0);
+        vc_drop_kept(e, l, h, kept.data(), n, &n);
+        auto& d = meta.dropped_indices[l][h];
+        size_t j = 0;
+        for (std::int64_t t = 0; t < st.committed; ++t) {
+          if (j < kept.size() && kept[j] == t) { ++j; continue; }
+          d.push_back(t);
+        }
+      }
+  }
+  return meta;
+}
+
 class SlotOracles {
  public:
   // stage >= 0: the engine keeps the full KV in the pinned host pool; each

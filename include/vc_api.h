@@ -138,6 +138,8 @@ int vc_engine_load_weights(vc_engine* e, const uint16_t* embed, const uint16_t* 
                            const uint16_t* const* wup, const uint16_t* const* wdown,
                            const uint16_t* final_norm, const uint16_t* lm_head);
 int vc_engine_stats(vc_engine* e, uint64_t* kernel_launches, uint64_t* weight_bytes);
+/* This engine's KV geometry: layers and KV heads (this rank's share under TP). */
+int vc_engine_geometry(vc_engine* e, int* layers, int* kv_heads);
 /* Device time (CUDA events, H2D of a step's inputs -> D2H of its tokens)
  * summed over steps since the last reset.                                  */
 int vc_engine_timing(vc_engine* e, double* device_ms, int64_t* steps, int reset);

@@ -141,6 +141,7 @@ SIGNATURES = {
     "vc_engine_init_weights_scaled": (I, [P, U64, F, F, F]),
     "vc_engine_load_weights": (I, [P, PU16, PPU16, PPU16, PPU16, PPU16, PPU16, PPU16, PPU16, PU16, PU16]),
     "vc_engine_stats": (I, [P, PU64, PU64]),
+    "vc_engine_geometry": (I, [P, PI, PI]),
     "vc_engine_timing": (I, [P, PD, PI64, I]),
     "vc_kernel_bench": (I, [P, I, PI, I, I, PD, PD]),
     "vc_request_add_synthetic": (I, [P, I, I, C.c_int32, U64, I, F]),

@@ -142,6 +142,14 @@ int vc_engine_attach_nccl(vc_engine* e, const uint8_t* id) {
   });
 }
 
+int vc_engine_geometry(vc_engine* e, int* layers, int* kv_heads) {
+  return guard([&] {
+    const auto& m = E(e).model();
+    if (layers) *layers = m.layers;
+    if (kv_heads) *kv_heads = m.n_kv;
+  });
+}
+
 int vc_tp_collective_bench(vc_engine* e, int rows, int reps, double* us) {
   return guard([&] {
     const double v = E(e).collective_bench(rows, reps);

@@ -36,8 +36,18 @@ int main(int argc, char** argv) {
     ck(vc_engine_init_weights(e, 7, 0.02f));
     ck(vc_request_add_synthetic(e, 0, n_ctx, 17, 1, 4, 10.f));
   }
-  vc_compressed_meta meta;
-  ck(vc_compress(es, 0, &meta));
+  // the reference signature reaches the GPU tier (speckv::gpu::compress ->
+  // vc_compress_spec): quant-uniform at the engine's width, size law checked
+  speckv::CompressorSpec cspec;
+  cspec.kind = speckv::CompressorKind::QuantUniform;
+  cspec.bits = bits;
+  const auto meta = speckv::gpu::compress<speckv::CompressedKVMeta>(es, 0, cspec, 0.0, 0);
+  const speckv::KvShape shape{2, 2, n_ctx, 2 * 2 * 64};
+  meta.check_invariants(shape);
+  if (meta.bit_scheme != bits || meta.payload_bytes != shape.full_bytes() * bits / 16) {
+    std::fprintf(stderr, "compress meta mismatch\n");
+    return 1;
+  }
 
   const std::vector<speckv::Token> prompt = {17};
   speckv::gpu::SlotOracles full(ef, 0);

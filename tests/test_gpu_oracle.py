@@ -38,10 +38,13 @@ def test_adapter_builds_and_links():
 @pytest.mark.skipif(not os.path.isdir(REF_INC), reason="reference headers not present")
 def test_adapter_compiles_against_reference_headers(tmp_path):
     tu = tmp_path / "tu.cpp"
-    tu.write_text('#include "speckv/specloop.hpp"\n#include "speckv_gpu_oracle.hpp"\n'
+    tu.write_text('#include "speckv/specloop.hpp"\n#include "speckv/compressor.hpp"\n'
+                  '#include "speckv_gpu_oracle.hpp"\n'
                   "speckv::TokenOracle f(vc_engine* e) {\n"
                   "  speckv::gpu::SlotOracles o(e, 0);\n"
-                  "  return o.drafter<speckv::TokenOracle>();\n}\n")
+                  "  return o.drafter<speckv::TokenOracle>();\n}\n"
+                  "speckv::CompressedKVMeta g(vc_engine* e, const speckv::CompressorSpec& s) {\n"
+                  "  return speckv::gpu::compress<speckv::CompressedKVMeta>(e, 0, s, 0.25, 7);\n}\n")
     subprocess.check_call(["g++", "-std=c++20", "-fsyntax-only", "-I", REF_INC, "-I",
                            os.path.join(T.ROOT, "include"), str(tu)])
 
