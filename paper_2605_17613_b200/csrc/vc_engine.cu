@@ -537,6 +537,9 @@ void Engine::add_request_synthetic(int slot, int n_ctx, int32_t pending, uint64_
   uint16_t* kb = dst.k + static_cast<size_t>(dslot) * n_slices * slice_elems;
   uint16_t* vb = dst.v + static_cast<size_t>(dslot) * n_slices * slice_elems;
   if (n_ctx > 0) {
+    // the staging slot may still be read by an earlier host-pool copy (a
+    // previous synthesis or commit on the D2H stream): write it after that
+    if (cfg_.full_tier == 1) VC_CK(cudaStreamWaitEvent(st_, ev_d2h_, 0));
     const size_t total = static_cast<size_t>(n_ctx) * m.d * n_slices;
     int grid = static_cast<int>(std::min<size_t>((total + 255) / 256, 148 * 32));
     synth_kv_kernel<<<grid, 256, 0, st_>>>(kb, vb, full_.cap, n_ctx, m.d, n_slices, seed, k_norm,
@@ -585,6 +588,7 @@ void Engine::add_request_kv(int slot, int n_ctx, int32_t pending, const uint16_t
       VC_CK(cudaMemcpy2DAsync(kb, pitch, k, spitch, spitch, n_slices, cudaMemcpyHostToDevice, st_));
       VC_CK(cudaMemcpy2DAsync(vb, pitch, v, spitch, spitch, n_slices, cudaMemcpyHostToDevice, st_));
     } else {
+      check_d2h();  // no commit still writing these host rows
       uint16_t* hk = host_pool_k(slot);
       uint16_t* hv = host_pool_v(slot);
       for (int i = 0; i < n_slices; ++i) {
@@ -1036,6 +1040,9 @@ void Engine::run_step(const std::vector<StepItem>& items, std::vector<int32_t>& 
 
 void Engine::kernel_bench(int kind, const std::vector<int>& slots, int reps, double* ms,
                           double* bytes) {
+  // time the kernel alone: no copy of the setup still in flight
+  VC_CK(cudaStreamSynchronize(copy_st_));
+  check_d2h();
   const auto& m = cfg_.model;
   const int n = static_cast<int>(slots.size());
   AttnShape as;

@@ -148,3 +148,29 @@ def test_scheduled_loop_with_arrivals(cuda, weights, tier, resident):
     assert st["tokens"] == (n + n_arr) * K
     assert 0 < st["p50_latency_s"] <= st["p99_latency_s"]
     e.close()
+
+
+@pytest.mark.gpu
+def test_host_pool_setup_is_race_free(cuda):
+    """Consecutive admissions of large requests into the host tier: each
+    request's synthesis reuses the scratch staging slot while the previous
+    request's host-pool copy (D2H stream) may still read it -- the host pool
+    must hold exactly each request's own KV (compared with the HBM tier's copy
+    of the same synthetic prefixes, rows at the end of the last slices)."""
+    from paper_2605_17613_b200 import ModelShape
+    s = ModelShape(vocab=512, hidden=512, layers=4, n_q=32, n_kv=8, d_head=128, ffn=512)
+    ctx, n = 32768, 3
+    h = Engine(s, max_slots=n, max_ctx=ctx + 64, max_x=8, quant_bits=4, full_tier=1, n_stage=2)
+    f = Engine(s, max_slots=n, max_ctx=ctx + 64, max_x=8, quant_bits=0)
+    for i in range(n):
+        h.add_synthetic(i, ctx, 17, seed=11 + i)
+        h.compress(i)
+        f.add_synthetic(i, ctx, 17, seed=11 + i)
+    for i in range(n):
+        for layer, head in [(0, 0), (s.layers - 1, s.n_kv - 1)]:
+            hk, hv = h.kv_read(2, i, layer, head, ctx - 64, 64)
+            fk, fv = f.kv_read(0, i, layer, head, ctx - 64, 64)
+            np.testing.assert_array_equal(hk, fk)
+            np.testing.assert_array_equal(hv, fv)
+    h.close()
+    f.close()
