@@ -67,7 +67,10 @@ def parse():
                    help="std of the Q projection init (-1: calibrated 2e-3; 0: 0.02)")
     p.add_argument("--no-cpu", action="store_true")
     p.add_argument("--no-secondary", action="store_true", help="skip the other tier's line")
-    p.add_argument("--stages", type=int, default=8, help="HBM staging slots of the host tier")
+    p.add_argument("--stages", type=int, default=8, help="HBM staging slots of the host tier (--ring 0)")
+    p.add_argument("--ring", type=int, default=8,
+                   help="host tier: one-layer chunks of the streaming ring (0: whole-request staging slots)")
+    p.add_argument("--streams", type=int, default=2, help="host tier, --ring > 0: streamed verifies in flight")
     p.add_argument("--stages-rot", type=int, default=3,
                    help="rotating staging slots of the offloaded requests when some are resident")
     p.add_argument("--small", action="store_true", help="tiny model smoke run")
@@ -860,13 +863,18 @@ def main():
         it_w, it_k = (W + 2) * (x + 1), K * (x + 1)
         ev, err = None, None
         try:
-            n_stage = (resident + (args.stages_rot if resident < B else 0)) if resident else args.stages
-            max_verify = (n_stage - resident + (resident + x_res) // (x_res + 1) + 2 if resident else
-                          (args.stages if tier else max(2, B // (x + 1) + 2)))
+            ring = args.ring if tier == 1 and not drop else 0
+            if ring:  # offloaded verifies stream through the chunk ring, outside the steps
+                n_stage = resident
+                max_verify = (resident + x_res) // (x_res + 1) + 2 if resident else 2
+            else:
+                n_stage = (resident + (args.stages_rot if resident < B else 0)) if resident else args.stages
+                max_verify = (n_stage - resident + (resident + x_res) // (x_res + 1) + 2 if resident else
+                              (args.stages if tier else max(2, B // (x + 1) + 2)))
             ev = vc.Engine(shape, max_slots=B, max_ctx=ctx + it_w + it_k + 3 * (x + 1) + 8, max_x=max(x, x_res),
                            quant_bits=0 if drop else args.bits, drop_ratio=drop, full_tier=tier,
                            n_stage=n_stage if tier else 1, max_verify=max_verify, device=local,
-                           resident_slots=resident)
+                           resident_slots=resident, ring_chunks=ring, max_streams=args.streams)
         except vc.VcError as ex:
             err = ex
         if dist:  # every rank falls back together (the pinned pool may fail on one rank only)
@@ -991,7 +999,11 @@ def main():
             d["swap"] = {"h2d_gbs": round(s["h2d_bytes"] / max(s["h2d_ms"], 1e-9) / 1e6, 1),
                          "link_busy_frac": round(s["h2d_ms"] / 1e3 / max(win_s, 1e-9), 3),
                          "hidden_frac": round(max(0.0, 1.0 - s["verify_wait_ms"] / max(s["h2d_ms"], 1e-9)), 3),
-                         "late_transfers": s["late_transfers"], "stages": args.stages,
+                         "late_transfers": s["late_transfers"],
+                         "staging": (f"chunk ring: {args.ring} one-layer chunks + 2 admission chunks, "
+                                     f"{args.streams} streamed verifies in flight" if args.ring and not drop
+                                     else f"{args.stages} whole-request staging slots"),
+                         "staging_hbm_bytes": int(s["staging_bytes"]),
                          "bytes_per_reload": int(r["meta"]["full_bytes"])}
         return d
 

@@ -89,6 +89,13 @@ typedef struct {
   int draft_depth;    /* rows one drafting request may carry in a step: 1 + the
                          auxiliary proposals of the two-level composition
                          (vc_run_speculative_composed); 0 or 1 = plain drafting */
+  int ring_chunks;    /* tier 1 staging: > 0 streams every offloaded reload layer by
+                         layer into a ring of ring_chunks one-layer chunks and runs
+                         the verify range by range as layers land (vc_stream_*);
+                         staging HBM = (ring_chunks + 2) layers instead of the
+                         rotating whole-request slots (n_stage then holds only the
+                         resident slots).  0 = whole-request staging slots.       */
+  int max_streams;    /* ring_chunks > 0: streamed verifies in flight (0 -> 2) */
 } vc_runtime_desc;
 
 /* Mirrors speckv::CompressedKVMeta (compressor.hpp:56-65).  Quant-uniform:
@@ -259,6 +266,23 @@ int vc_accept_commit(vc_engine* e, int slot, const int32_t* preds, int stage, in
 /* ---- host tier ------------------------------------------------------------ */
 int vc_swap_begin(vc_engine* e, int slot, int stage, uint64_t* transfer_id);
 int vc_swap_poll(vc_engine* e, uint64_t transfer_id, int* done);
+/* Layer-chunked host tier (ring_chunks > 0): the reload the reference books
+ * over S_r windows (scheduler.cpp:15-23, :96-163) streamed one layer per
+ * chunk, with the verify pipelined on the landed layers.
+ *   vc_stream_begin    start streaming slot's committed full KV; *id
+ *   vc_stream_advance  run the verify over the layers landed since the last
+ *                      call (the slot's open round must be complete: it is
+ *                      the window scored); *done = 1 once all layers ran and
+ *                      the x+1 predictions are in preds (capacity x+1)
+ *   vc_stream_accept   accept + commit from the streamed verify (the exact
+ *                      window rows it wrote), frees the stream
+ *   vc_stream_abort    drop an unfinished stream (waits for its copies)     */
+int vc_stream_begin(vc_engine* e, int slot, int* id);
+int vc_stream_advance(vc_engine* e, int id, int* done, int32_t* preds);
+int vc_stream_accept(vc_engine* e, int slot, int id, int32_t* emitted, int* n_emitted);
+int vc_stream_abort(vc_engine* e, int id);
+/* HBM bytes of the host tier's staging (rotating slots or the chunk ring). */
+int vc_engine_staging_bytes(vc_engine* e, int64_t* bytes);
 
 /* ---- decode loops ----------------------------------------------------------- */
 /* Full-KV greedy decode of K tokens for each slot (the baseline).
@@ -373,6 +397,7 @@ typedef struct {
   double p99_latency_s;
   double interconnect_busy;
   int64_t peak_hbm_bytes;
+  int64_t staging_bytes;    /* HBM of the host tier's staging (vc_engine_staging_bytes) */
 } vc_sched_stats;
 
 /* Reference metrics of a loop (SimMetrics, sim.hpp:52-74) on the engine:

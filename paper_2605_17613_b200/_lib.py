@@ -43,7 +43,8 @@ class RuntimeDesc(C.Structure):
                 ("quant_bits", C.c_int), ("full_tier", C.c_int), ("n_stage", C.c_int),
                 ("max_verify", C.c_int), ("use_graphs", C.c_int), ("drop_ratio", C.c_double),
                 ("tp_size", C.c_int), ("tp_rank", C.c_int), ("drop_window", C.c_int),
-                ("resident_slots", C.c_int), ("draft_depth", C.c_int)]
+                ("resident_slots", C.c_int), ("draft_depth", C.c_int),
+                ("ring_chunks", C.c_int), ("max_streams", C.c_int)]
 
 
 class CompressedMeta(C.Structure):
@@ -91,7 +92,8 @@ class SchedStats(C.Structure):
                 ("timed_resident_tokens", C.c_int64), ("timed_verifies", C.c_int64),
                 ("timed_verify_rows", C.c_double), ("throughput", C.c_double),
                 ("warm_throughput", C.c_double), ("p50_latency_s", C.c_double), ("p99_latency_s", C.c_double),
-                ("interconnect_busy", C.c_double), ("peak_hbm_bytes", C.c_int64)]
+                ("interconnect_busy", C.c_double), ("peak_hbm_bytes", C.c_int64),
+                ("staging_bytes", C.c_int64)]
 
 
 class LoopMetrics(C.Structure):
@@ -174,6 +176,11 @@ SIGNATURES = {
     "vc_accept_commit": (I, [P, I, PI32, I, PI32, PI]),
     "vc_swap_begin": (I, [P, I, I, PU64]),
     "vc_swap_poll": (I, [P, U64, PI]),
+    "vc_stream_begin": (I, [P, I, PI]),
+    "vc_stream_advance": (I, [P, I, PI, C.POINTER(C.c_int32)]),
+    "vc_stream_accept": (I, [P, I, I, C.POINTER(C.c_int32), PI]),
+    "vc_stream_abort": (I, [P, I]),
+    "vc_engine_staging_bytes": (I, [P, C.POINTER(C.c_int64)]),
     "vc_run_decode": (I, [P, PI, I, I, PI32, PD]),
     "vc_run_speculative": (I, [P, PI, I, I, I, PI32, PI32, I, PI, PD]),
     "vc_run_speculative_ngram": (I, [P, PI, I, I, I, I, PI32, PI32, I, PI, PI, PD]),

@@ -94,6 +94,8 @@ int vc_engine_create(const vc_model_desc* model, const vc_runtime_desc* rt, int 
     c.drop_window = rt->drop_window;
     c.resident_slots = rt->resident_slots;
     c.draft_depth = rt->draft_depth > 1 ? rt->draft_depth : 1;
+    c.ring_chunks = rt->ring_chunks;
+    c.max_streams = rt->max_streams > 0 ? rt->max_streams : 2;
     if (c.drop_window < 0 || (c.drop_window > 0 && c.drop_ratio <= 0.0))
       throw speckv::ConfigError("compressor: drop_window needs the drop-topk compressor");
     c.tp_size = rt->tp_size > 1 ? rt->tp_size : 1;
@@ -607,6 +609,39 @@ int vc_swap_begin(vc_engine* e, int slot, int stage, uint64_t* transfer_id) {
 
 int vc_swap_poll(vc_engine* e, uint64_t transfer_id, int* done) {
   return guard([&] { *done = E(e).swap_done(transfer_id) ? 1 : 0; });
+}
+
+int vc_stream_begin(vc_engine* e, int slot, int* id) {
+  return guard([&] { *id = E(e).stream_begin(slot); });
+}
+
+int vc_stream_advance(vc_engine* e, int id, int* done, int32_t* preds) {
+  return guard([&] {
+    vc::Engine& en = E(e);
+    en.stream_pump();
+    *done = en.stream_advance(id);
+    if (*done && preds) {
+      const auto p = en.stream_preds(id);
+      std::memcpy(preds, p.data(), p.size() * sizeof(int32_t));
+    }
+  });
+}
+
+int vc_stream_accept(vc_engine* e, int slot, int id, int32_t* emitted, int* n_emitted) {
+  return guard([&] {
+    vc::Engine& en = E(e);
+    auto em = en.accept_commit_stream(slot, en.stream_preds(id), id);
+    std::memcpy(emitted, em.data(), em.size() * sizeof(int32_t));
+    *n_emitted = static_cast<int>(em.size());
+  });
+}
+
+int vc_stream_abort(vc_engine* e, int id) {
+  return guard([&] { E(e).stream_end(id); });
+}
+
+int vc_engine_staging_bytes(vc_engine* e, int64_t* bytes) {
+  return guard([&] { *bytes = static_cast<int64_t>(E(e).staging_bytes()); });
 }
 
 // ---------------------------------------------------------- remote prefix

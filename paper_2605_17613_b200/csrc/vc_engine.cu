@@ -27,6 +27,11 @@ void check_cuda(cudaError_t e, const char* what) {
 namespace {
 
 size_t round_up(size_t x, size_t a) { return (x + a - 1) / a * a; }
+int bucket_rows(int M) {
+  if (M <= 64) return (M + 15) / 16 * 16;
+  if (M <= 128) return (M + 31) / 32 * 32;
+  return (M + 63) / 64 * 64;
+}
 
 template <class T>
 T* dmalloc(size_t n) {
@@ -43,9 +48,11 @@ T* dmalloc(size_t n) {
 }
 
 // Synthetic prefix KV, bit-identical with tests/oracle_data.py.
+// i0: element offset of slice 0 in the request's [slice][pos][c] order (a
+// one-layer chunk synthesises its slices with the values of the whole request).
 __global__ void synth_kv_kernel(uint16_t* kbase, uint16_t* vbase, int cap, int n_ctx, int d,
                                 int n_slices, uint64_t seed, float k_norm, float k_out,
-                                int outlier_period) {
+                                int outlier_period, size_t i0) {
   const size_t per = static_cast<size_t>(n_ctx) * d;
   const size_t total = per * n_slices;
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
@@ -53,7 +60,7 @@ __global__ void synth_kv_kernel(uint16_t* kbase, uint16_t* vbase, int cap, int n
     const size_t slice = i / per, rem = i % per;
     const int c = static_cast<int>(rem % d);
     auto val = [&](uint64_t s, float k) {
-      uint64_t x = i + 0x9e3779b97f4a7c15ull;
+      uint64_t x = (i + i0) + 0x9e3779b97f4a7c15ull;
       x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
       x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
       x = x ^ (x >> 31);
@@ -136,9 +143,16 @@ Engine::Engine(const EngineConfig& cfg, int device) : cfg_(cfg), device_(device)
     throw ContractViolation("resident_slots out of [0, max_slots]");
   if (cfg_.resident_slots > 0 && cfg_.full_tier != 1)
     throw ContractViolation("resident_slots is a placement of the host tier (full_tier 1)");
-  if (cfg_.full_tier == 1 &&
+  if (cfg_.ring_chunks < 0 || (cfg_.ring_chunks > 0 && cfg_.full_tier != 1))
+    throw ContractViolation("ring_chunks is a staging mode of the host tier (full_tier 1)");
+  if (cfg_.ring_chunks > 0 && (cfg_.ring_chunks < 2 || cfg_.max_streams < 1 || cfg_.quant_bits == 0 ||
+                               cfg_.tp_size > 1))
+    throw ContractViolation("ring_chunks: needs >= 2 chunks, max_streams >= 1, the quantised tier, no TP");
+  if (cfg_.full_tier == 1 && cfg_.ring_chunks == 0 &&
       cfg_.resident_slots + (cfg_.resident_slots < cfg_.max_slots ? 1 : 0) > cfg_.n_stage)
     throw ContractViolation("n_stage must hold every resident slot plus one rotating staging slot");
+  if (cfg_.ring_chunks > 0 && cfg_.n_stage < cfg_.resident_slots)
+    throw ContractViolation("n_stage must hold every resident slot");
   if (m.n_q % m.n_kv != 0 || (m.d != 64 && m.d != 128)) throw ContractViolation("unsupported head geometry");
   if (cfg_.quant_bits != 0 && cfg_.quant_bits != 2 && cfg_.quant_bits != 4)
     throw ContractViolation("quant_bits must be 0, 2 or 4");
@@ -167,6 +181,15 @@ Engine::~Engine() {
     cudaEventDestroy(x.start);
     cudaEventDestroy(x.done);
   }
+  for (auto& [k, v] : vstreams_)
+    if (v.ev_final) cudaEventDestroy(v.ev_final);
+  for (auto* evs : {&ring_start_, &ring_done_, &ring_free_, &ring_upload_})
+    for (cudaEvent_t e : *evs) cudaEventDestroy(e);
+  for (void* p : {static_cast<void*>(ring_.k), static_cast<void*>(ring_.v), static_cast<void*>(wbuf_.k),
+                  static_cast<void*>(wbuf_.v), static_cast<void*>(xsave_), static_cast<void*>(sssave_),
+                  static_cast<void*>(ring_seqs_dev_)})
+    if (p) cudaFree(p);
+  if (h_ring_) cudaFreeHost(h_ring_);
   void* ptrs[] = {weight_blob_, rope_cos_, rope_sin_, full_.k, full_.v, stage_.k, stage_.v,
                   quant_.rec, quant_.ktail, quant_.vtail, drop_.k, drop_.v, score_buf_, score_w_, kept_buf_,
                   tp_y_, tp_g_,
@@ -312,6 +335,23 @@ void Engine::alloc_all() {
     stage_.cap = cap;
     stage_.k = dmalloc<uint16_t>(st_slices * slice_elems);
     stage_.v = dmalloc<uint16_t>(st_slices * slice_elems);
+    if (ring_mode()) {
+      // ring_chunks one-layer chunks for streamed verifies + 2 admission chunks
+      const int nch = cfg_.ring_chunks + 2;
+      ring_.cap = cap;
+      ring_.k = dmalloc<uint16_t>(static_cast<size_t>(nch) * m.n_kv * slice_elems);
+      ring_.v = dmalloc<uint16_t>(static_cast<size_t>(nch) * m.n_kv * slice_elems);
+      ring_owner_.assign(nch, -1);
+      for (int i = 0; i < nch; ++i) {
+        cudaEvent_t a, b, c;
+        VC_CK(cudaEventCreate(&a));
+        VC_CK(cudaEventCreate(&b));
+        VC_CK(cudaEventCreateWithFlags(&c, cudaEventDisableTiming));
+        ring_start_.push_back(a);
+        ring_done_.push_back(b);
+        ring_free_.push_back(c);
+      }
+    }
   }
   tail_cap_ = static_cast<int>(round_up(VC_QGROUP + cfg_.max_x + 2, 8));
   if (cfg_.quant_bits > 0) {
@@ -356,9 +396,13 @@ void Engine::alloc_all() {
   {
     const KvPool& dp = cfg_.full_tier == 0 ? full_ : stage_;
     const size_t dslices = cfg_.full_tier == 0 ? slices : static_cast<size_t>(cfg_.n_stage) * L * m.n_kv;
-    if (!make_kv_maps(&dense_maps_, dp, dslices, d) ||
+    if ((dslices > 0 && !make_kv_maps(&dense_maps_, dp, dslices, d)) ||
         !make_q_map(&dense_maps_, qkv_, d, m.n_q + 2 * m.n_kv, Mmax_, qkv_n, m.n_q / m.n_kv))
       throw ContractViolation("dense attention: cannot encode TMA tensor maps for this shape");
+    if (ring_mode() &&
+        (!make_kv_maps(&ring_maps_, ring_, static_cast<size_t>(cfg_.ring_chunks + 2) * m.n_kv, d) ||
+         !make_q_map(&ring_maps_, qkv_, d, m.n_q + 2 * m.n_kv, Mmax_, qkv_n, m.n_q / m.n_kv)))
+      throw ContractViolation("chunk ring: cannot encode TMA tensor maps for this shape");
     if (drop_mode() && (!make_kv_maps(&drop_maps_, drop_, slices, d) ||
                         !make_q_map(&drop_maps_, qkv_, d, m.n_q + 2 * m.n_kv, Mmax_, qkv_n, m.n_q / m.n_kv)))
       throw ContractViolation("drop tier: cannot encode TMA tensor maps for this shape");
@@ -403,6 +447,24 @@ void Engine::alloc_all() {
   VC_CK(cudaHostAlloc(reinterpret_cast<void**>(&h_out_), Mmax_ * sizeof(int32_t), cudaHostAllocMapped));
   VC_CK(cudaHostGetDevicePointer(&d_hdesc_, h_desc_, 0));
   VC_CK(cudaHostGetDevicePointer(reinterpret_cast<void**>(&d_hout_), h_out_, 0));
+  if (ring_mode()) {  // streamed-verify state: exact window rows, carried hidden state, descriptors
+    const int nb = cfg_.max_streams;
+    wrows_ = bucket_rows(cfg_.max_x + 1);
+    wbuf_.cap = tail_cap_;
+    wbuf_.k = dmalloc<uint16_t>(static_cast<size_t>(nb) * L * m.n_kv * tail_cap_ * d);
+    wbuf_.v = dmalloc<uint16_t>(static_cast<size_t>(nb) * L * m.n_kv * tail_cap_ * d);
+    xsave_ = dmalloc<float>(static_cast<size_t>(nb) * wrows_ * H);
+    sssave_ = dmalloc<float>(static_cast<size_t>(nb) * wrows_ * (H / 128));
+    ring_seqs_dev_ = dmalloc<AttnSeq>(L);
+    VC_CK(cudaHostAlloc(&h_ring_, static_cast<size_t>(nb) * ring_desc_bytes(), cudaHostAllocMapped));
+    VC_CK(cudaHostGetDevicePointer(&d_hring_, h_ring_, 0));
+    vbuf_used_.assign(nb, 0);
+    for (int i = 0; i < nb; ++i) {
+      cudaEvent_t e;
+      VC_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      ring_upload_.push_back(e);
+    }
+  }
 }
 
 void Engine::attach_collective(std::unique_ptr<Collective> c) {
@@ -529,6 +591,43 @@ void Engine::add_request_synthetic(int slot, int n_ctx, int32_t pending, uint64_
   const float k_norm = static_cast<float>(1.0 / (65536.0 * std::sqrt(1.0 / 3.0)));
   const float k_out = static_cast<float>(outlier_scale / (65536.0 * std::sqrt(1.0 / 3.0)));
   const int period = outlier_channels > 0 ? m.d / outlier_channels : 0;
+  if (ring_mode() && !resident(slot)) {
+    // offloaded, chunk ring: synthesise one layer at a time into the two
+    // admission chunks and copy each into the host pool (no whole-request
+    // staging slot)
+    const size_t slice_elems = static_cast<size_t>(full_.cap) * m.d;
+    const size_t pitch = slice_elems * 2;
+    const size_t width = static_cast<size_t>(n_ctx) * m.d * 2;
+    check_d2h();  // earlier commits into this slot's host rows land first
+    for (int l = 0; l < m.layers && n_ctx > 0; ++l) {
+      const int c = cfg_.ring_chunks + (l & 1);
+      uint16_t* kb = ring_.k + static_cast<size_t>(c) * m.n_kv * slice_elems;
+      uint16_t* vb = ring_.v + static_cast<size_t>(c) * m.n_kv * slice_elems;
+      VC_CK(cudaStreamWaitEvent(st_, ring_free_[c], 0));  // the chunk's previous host copy is done
+      const size_t total = static_cast<size_t>(n_ctx) * m.d * m.n_kv;
+      const int grid = static_cast<int>(std::min<size_t>((total + 255) / 256, 148 * 32));
+      synth_kv_kernel<<<grid, 256, 0, st_>>>(kb, vb, full_.cap, n_ctx, m.d, m.n_kv, seed, k_norm, k_out, period,
+                                             static_cast<size_t>(l) * m.n_kv * n_ctx * m.d);
+      VC_CK(cudaGetLastError());
+      ++launches_;
+      VC_CK(cudaEventRecord(ev_commit_, st_));
+      VC_CK(cudaStreamWaitEvent(d2h_st_, ev_commit_, 0));
+      const size_t o = static_cast<size_t>(l) * m.n_kv * slice_elems;
+      VC_CK(cudaMemcpy2DAsync(host_pool_k(slot) + o, pitch, kb, pitch, width, m.n_kv, cudaMemcpyDeviceToHost, d2h_st_));
+      VC_CK(cudaMemcpy2DAsync(host_pool_v(slot) + o, pitch, vb, pitch, width, m.n_kv, cudaMemcpyDeviceToHost, d2h_st_));
+      VC_CK(cudaEventRecord(ring_free_[c], d2h_st_));
+    }
+    VC_CK(cudaEventRecord(ev_d2h_, d2h_st_));
+    VC_CK(cudaStreamWaitEvent(copy_st_, ev_d2h_, 0));  // later reloads of these rows wait for them
+    SeqState& s = seqs_[slot];
+    s = SeqState{};
+    s.live = true;
+    s.committed = n_ctx;
+    s.pending = pending;
+    scratch_slot_ = -1;
+    VC_CK(cudaStreamSynchronize(st_));
+    return;
+  }
   // tier 1 synthesises into the request's own staging slot (resident) or the
   // scratch staging slot, then D2H into the host pool (offloaded)
   KvPool dst = cfg_.full_tier == 0 ? full_ : stage_;
@@ -543,7 +642,7 @@ void Engine::add_request_synthetic(int slot, int n_ctx, int32_t pending, uint64_
     const size_t total = static_cast<size_t>(n_ctx) * m.d * n_slices;
     int grid = static_cast<int>(std::min<size_t>((total + 255) / 256, 148 * 32));
     synth_kv_kernel<<<grid, 256, 0, st_>>>(kb, vb, full_.cap, n_ctx, m.d, n_slices, seed, k_norm,
-                                           k_out, period);
+                                           k_out, period, 0);
     VC_CK(cudaGetLastError());
     ++launches_;
   }
@@ -631,19 +730,25 @@ void Engine::add_request_prefill(int slot, const int32_t* prompt, int n) {
 
 void Engine::release(int slot) { seqs_.at(slot) = SeqState{}; }
 
-void Engine::quantise_groups(int slot, int g0, int ng, const KvPool& src, int src_slot) {
+// Quantise groups [g0, g0+ng) of layers [layer0, layer0+layers) of `slot`
+// from src: src_slot's slices hold those layers' rows (layers * n_kv slices),
+// row r of a slice = absolute position r + origin.
+void Engine::quantise_groups(int slot, int g0, int ng, const KvPool& src, int src_slot, int origin,
+                             int layer0, int layers) {
   if (ng <= 0) return;
   const auto& m = cfg_.model;
-  const int n_slices = m.layers * m.n_kv;
+  if (layers < 0) layers = m.layers;
+  const int n_slices = layers * m.n_kv;
   QuantJob* jobs = reinterpret_cast<QuantJob*>(static_cast<uint8_t*>(h_desc_) + desc_bytes_ -
-                                               static_cast<size_t>(n_slices) * sizeof(QuantJob));
+                                               static_cast<size_t>(m.layers) * m.n_kv * sizeof(QuantJob));
   const size_t slice_words = static_cast<size_t>(quant_.cap / VC_QGROUP) * quant_record_words(m.d, cfg_.quant_bits);
   for (int i = 0; i < n_slices; ++i) {
     const size_t ss = static_cast<size_t>(src_slot) * n_slices + i;
-    const size_t ds = static_cast<size_t>(slot) * n_slices + i;
+    const size_t ds = (static_cast<size_t>(slot) * m.layers + layer0) * m.n_kv + i;
     QuantJob j;
-    j.k = src.k + ss * static_cast<size_t>(src.cap) * m.d;
-    j.v = src.v + ss * static_cast<size_t>(src.cap) * m.d;
+    // token 0 of group 0 (may lie before the source rows: only groups >= g0 are read)
+    j.k = src.k + ss * static_cast<size_t>(src.cap) * m.d - static_cast<ptrdiff_t>(origin) * m.d;
+    j.v = src.v + ss * static_cast<size_t>(src.cap) * m.d - static_cast<ptrdiff_t>(origin) * m.d;
     j.rec = quant_.rec + ds * slice_words;
     j.g0 = g0;
     j.ng = ng;
@@ -672,6 +777,36 @@ void Engine::compress_as(int slot, double ratio, const int32_t* kept_host, int k
     // just synthesised: the full KV is still in the scratch staging slot
     src = stage_;
     src_slot = scratch_stage_used_;
+  } else if (ring_mode()) {
+    // chunk ring: stream the prefix one layer at a time through the two
+    // admission chunks and quantise each layer as it lands
+    if (drop_mode()) throw ContractViolation("chunk ring: drop tier not supported");
+    const int ng = std::min(s.committed / VC_QGROUP, quant_.cap / VC_QGROUP);
+    const int tc = s.committed - ng * VC_QGROUP;
+    if (tc > tail_cap_ - cfg_.max_x - 1) throw ContractViolation("tail overflow");
+    const size_t slice_elems = static_cast<size_t>(full_.cap) * m.d;
+    const size_t pitch = slice_elems * 2;
+    const size_t width = static_cast<size_t>(s.committed) * m.d * 2;
+    check_d2h();  // commits still writing these host rows land first
+    for (int l = 0; l < m.layers; ++l) {
+      const int c = cfg_.ring_chunks + (l & 1);
+      uint16_t* kb = ring_.k + static_cast<size_t>(c) * m.n_kv * slice_elems;
+      uint16_t* vb = ring_.v + static_cast<size_t>(c) * m.n_kv * slice_elems;
+      VC_CK(cudaStreamWaitEvent(st_, ring_free_[c], 0));
+      const size_t o = static_cast<size_t>(l) * m.n_kv * slice_elems;
+      if (width > 0) {
+        VC_CK(cudaMemcpy2DAsync(kb, pitch, host_pool_k(slot) + o, pitch, width, m.n_kv, cudaMemcpyHostToDevice, st_));
+        VC_CK(cudaMemcpy2DAsync(vb, pitch, host_pool_v(slot) + o, pitch, width, m.n_kv, cudaMemcpyHostToDevice, st_));
+      }
+      quantise_groups(slot, 0, ng, ring_, c, 0, l, 1);
+      VC_LAUNCH(tail_refill(ring_, c, ng * VC_QGROUP, tc, quant_, slot * m.layers + l, 1, m.n_kv, m.d, st_));
+    }
+    s.n_groups = ng;
+    s.tail_committed = tc;
+    s.draft_len = 0;
+    s.drafted.clear();
+    VC_CK(cudaStreamSynchronize(st_));
+    return;
   } else if (cfg_.full_tier == 1) {
     // stream the prefix through the scratch staging slot
     uint64_t id = swap_begin(slot, scratch_stage());
@@ -870,11 +1005,6 @@ void Engine::enqueue_forward(int M, int n_draft, int n_dense1, int n_densev, int
 }
 
 namespace {
-int bucket_rows(int M) {
-  if (M <= 64) return (M + 15) / 16 * 16;
-  if (M <= 128) return (M + 31) / 32 * 32;
-  return (M + 63) / 64 * 64;
-}
 int bucket_seqs(int n) { return n == 0 ? 0 : (n + 3) / 4 * 4; }
 }  // namespace
 
@@ -1139,6 +1269,16 @@ void Engine::push_draft(int slot, int32_t tok) {
 }
 
 std::vector<int32_t> Engine::accept_commit(int slot, const std::vector<int32_t>& preds, int stage) {
+  const bool staged = cfg_.full_tier == 1;
+  if (staged && resident(slot) && stage != slot)
+    throw ContractViolation("accept: a resident slot verifies in its own staging slot");
+  if (staged && !resident(slot) && stage < 0) throw ContractViolation("accept: staged verify needs its stage");
+  const RowSrc src{staged ? stage_ : full_, staged ? stage : slot, 0};
+  return accept_commit_from(slot, preds, src, staged && !resident(slot));
+}
+
+std::vector<int32_t> Engine::accept_commit_from(int slot, const std::vector<int32_t>& preds, const RowSrc& src,
+                                                bool to_host) {
   SeqState& s = seqs_.at(slot);
   const int x = static_cast<int>(s.drafted.size());
   if (static_cast<int>(preds.size()) != x + 1) throw ContractViolation("accept: |preds| must be |drafted|+1");
@@ -1151,9 +1291,6 @@ std::vector<int32_t> Engine::accept_commit(int slot, const std::vector<int32_t>&
   const auto& m = cfg_.model;
   const int old = s.committed;
   const int now = old + 1 + mcount;
-  const bool staged = cfg_.full_tier == 1;
-  KvPool src = staged ? stage_ : full_;
-  const int src_slot = staged ? stage : slot;
   if (cfg_.quant_bits > 0 && !drop_mode()) {
     // the bf16 tail holds the residual group + the next draft window; past
     // max_ctx the quantised tier cannot take more groups (same bound as compress)
@@ -1161,21 +1298,16 @@ std::vector<int32_t> Engine::accept_commit(int slot, const std::vector<int32_t>&
     if (now - ng_now * VC_QGROUP > tail_cap_ - cfg_.max_x - 1)
       throw ContractViolation("accept: request exceeds max_ctx (compressed tail overflow)");
   }
-  if (staged && resident(slot) && stage != slot)
-    throw ContractViolation("accept: a resident slot verifies in its own staging slot");
-  if (staged && !resident(slot)) {
-    if (stage < 0) throw ContractViolation("accept: staged verify needs its stage");
+  if (src.origin > old) throw ContractViolation("accept: exact rows start after the committed prefix");
+  if (to_host) {
     // exact KV of the committed rows back to the host pool
     const int n_slices = m.layers * m.n_kv;
-    const size_t pitch = static_cast<size_t>(full_.cap) * m.d * 2;
-    const size_t off = static_cast<size_t>(old) * m.d;
+    const size_t dpitch = static_cast<size_t>(full_.cap) * m.d * 2;
+    const size_t spitch = static_cast<size_t>(src.pool.cap) * m.d * 2;
     const size_t width = static_cast<size_t>(now - old) * m.d * 2;
-    const size_t slice_elems = static_cast<size_t>(full_.cap) * m.d;
-    (void)slice_elems;
-    uint16_t* hk = host_pool_k(slot) + off;
-    uint16_t* hv = host_pool_v(slot) + off;
-    const uint16_t* sk = stage_.k + static_cast<size_t>(stage) * n_slices * slice_elems + off;
-    const uint16_t* sv = stage_.v + static_cast<size_t>(stage) * n_slices * slice_elems + off;
+    uint16_t* hk = host_pool_k(slot) + static_cast<size_t>(old) * m.d;
+    uint16_t* hv = host_pool_v(slot) + static_cast<size_t>(old) * m.d;
+    const size_t soff = (static_cast<size_t>(src.slot) * n_slices * src.pool.cap + (old - src.origin)) * m.d;
     // on its own stream: a D2H on the compute stream would queue behind an
     // in-flight 4.29 GB reload in the copy engine and stall the next step for
     // the rest of that reload (measured: 91 ms steps after every offloaded
@@ -1183,8 +1315,8 @@ std::vector<int32_t> Engine::accept_commit(int slot, const std::vector<int32_t>&
     // for it through copy_st_.
     VC_CK(cudaEventRecord(ev_commit_, st_));
     VC_CK(cudaStreamWaitEvent(d2h_st_, ev_commit_, 0));
-    VC_CK(cudaMemcpy2DAsync(hk, pitch, sk, pitch, width, n_slices, cudaMemcpyDeviceToHost, d2h_st_));
-    VC_CK(cudaMemcpy2DAsync(hv, pitch, sv, pitch, width, n_slices, cudaMemcpyDeviceToHost, d2h_st_));
+    VC_CK(cudaMemcpy2DAsync(hk, dpitch, src.pool.k + soff, spitch, width, n_slices, cudaMemcpyDeviceToHost, d2h_st_));
+    VC_CK(cudaMemcpy2DAsync(hv, dpitch, src.pool.v + soff, spitch, width, n_slices, cudaMemcpyDeviceToHost, d2h_st_));
     VC_CK(cudaEventRecord(ev_d2h_, d2h_st_));
     VC_CK(cudaStreamWaitEvent(copy_st_, ev_d2h_, 0));
   }
@@ -1192,7 +1324,8 @@ std::vector<int32_t> Engine::accept_commit(int slot, const std::vector<int32_t>&
     // the accepted rows' exact K/V (full tier) are appended to the compacted
     // tier; the draft window's entries beyond them are simply overwritten
     if (s.drop_len + (now - old) + cfg_.max_x + 2 > drop_.cap) throw ContractViolation("drop tier full");
-    VC_LAUNCH(copy_rows(src, src_slot, old, now - old, drop_, slot, s.drop_len, m.layers * m.n_kv, m.d, st_));
+    VC_LAUNCH(copy_rows(src.pool, src.slot, old - src.origin, now - old, drop_, slot, s.drop_len,
+                        m.layers * m.n_kv, m.d, st_));
     s.drop_len += now - old;
     // online mode (speckv::update semantics, compressor.cpp:208-243, with the
     // kept prefix as the sink): once 2W tokens have been appended, keep the
@@ -1204,10 +1337,12 @@ std::vector<int32_t> Engine::accept_commit(int slot, const std::vector<int32_t>&
     }
   } else if (cfg_.quant_bits > 0 && (s.n_groups > 0 || s.tail_committed > 0 || x > 0)) {
     const int ng_now = std::min(now / VC_QGROUP, quant_.cap / VC_QGROUP);
-    quantise_groups(slot, s.n_groups, ng_now - s.n_groups, src, src_slot);
+    if (ng_now > s.n_groups && s.n_groups * VC_QGROUP < src.origin)
+      throw ContractViolation("accept: exact rows do not cover the groups to quantise");
+    quantise_groups(slot, s.n_groups, ng_now - s.n_groups, src.pool, src.slot, src.origin);
     s.n_groups = ng_now;
     s.tail_committed = now - ng_now * VC_QGROUP;
-    VC_LAUNCH(tail_refill(src, src_slot, ng_now * VC_QGROUP, s.tail_committed, quant_, slot,
+    VC_LAUNCH(tail_refill(src.pool, src.slot, ng_now * VC_QGROUP - src.origin, s.tail_committed, quant_, slot,
                           m.layers, m.n_kv, m.d, st_));
   }
   s.committed = now;
@@ -1363,6 +1498,7 @@ uint64_t Engine::prefix_load(int slot, int what, int32_t pending) {
 // ------------------------------------------------------------- host tier
 uint64_t Engine::swap_begin(int slot, int stage) {
   if (cfg_.full_tier != 1) throw ContractViolation("swap: host tier disabled");
+  if (ring_mode()) throw ContractViolation("swap: the chunk-ring engine streams verifies (stream_begin)");
   if (resident(slot)) throw ContractViolation("swap: the slot's full KV is resident (no host copy)");
   scratch_slot_ = -1;
   if (stage < cfg_.resident_slots || stage >= cfg_.n_stage)
@@ -1424,6 +1560,321 @@ void Engine::swap_wait(uint64_t id) {
   if (it == xfers_.end()) return;
   VC_CK(cudaEventSynchronize(it->second.done));
   swap_done(id);
+}
+
+// --------------------------------------------- host tier, layer-chunked ring
+// The verify of an offloaded request reads its full KV one layer at a time,
+// so the reload is streamed in one-layer chunks (n_kv slices of K and of V,
+// 134 MB at 32K for Llama-3-8B) into a ring of ring_chunks chunks, and the
+// verify forward runs over each range of layers that has landed, its hidden
+// state carried in xsave_/sssave_ between ranges.  A chunk is released as
+// soon as the range that read it is enqueued (the next copy into it waits on
+// ring_free_ on the copy stream), so staging HBM is ring_chunks layers
+// instead of whole requests, the link streams back to back, and the verify
+// finishes one chunk after the last layer lands.  The reference books the
+// reload as bytes over S_r windows (scheduler.cpp:15-23, :96-163); here the
+// same booking drives chunk copies.  Batch invariance makes the range-by-range
+// forward bit-identical to a whole-window verify (same GEMM split per (N, K),
+// same 2048-key attention chunks, rows independent).
+size_t Engine::staging_bytes() const {
+  const auto& m = cfg_.model;
+  const size_t slab = static_cast<size_t>(m.n_kv) * full_.cap * m.d * 2 * 2;  // one layer, K and V
+  if (cfg_.full_tier != 1) return 0;
+  const size_t rot = ring_mode() ? 0 : static_cast<size_t>(cfg_.n_stage - cfg_.resident_slots) * m.layers * slab;
+  return rot + (ring_mode() ? static_cast<size_t>(cfg_.ring_chunks + 2) * slab : 0);
+}
+
+int Engine::stream_begin(int slot) {
+  if (!ring_mode()) throw ContractViolation("stream: the engine has no chunk ring (ring_chunks 0)");
+  if (resident(slot)) throw ContractViolation("stream: the slot's full KV is resident (no host copy)");
+  const SeqState& s = seqs_.at(slot);
+  if (!s.live) throw ContractViolation("stream: slot not live");
+  for (const auto& [id, v] : vstreams_)
+    if (v.slot == slot) throw ContractViolation("stream: the slot already has a streamed verify");
+  int buf = -1;
+  for (int i = 0; i < cfg_.max_streams; ++i)
+    if (!vbuf_used_[i]) { buf = i; break; }
+  if (buf < 0) throw ContractViolation("stream: max_streams streamed verifies already in flight");
+  vbuf_used_[buf] = 1;
+  VStream v;
+  v.slot = slot;
+  v.buf = buf;
+  v.base = ring_seq_;
+  ring_seq_ += cfg_.model.layers;
+  v.committed = s.committed;
+  v.origin = s.n_groups * VC_QGROUP;
+  VC_CK(cudaEventCreateWithFlags(&v.ev_final, cudaEventDisableTiming));
+  const int id = next_vstream_++;
+  vstreams_[id] = std::move(v);
+  vs_order_.push_back(id);
+  stream_pump();
+  return id;
+}
+
+void Engine::stream_issue_chunk(VStream& v) {
+  const auto& m = cfg_.model;
+  const int R = cfg_.ring_chunks;
+  const int l = v.issued;
+  const int c = static_cast<int>((v.base + l) % R);
+  ring_owner_[c] = v.base + l;
+  const size_t slice_elems = static_cast<size_t>(full_.cap) * m.d;
+  const size_t pitch = slice_elems * 2;
+  const size_t width = static_cast<size_t>(v.committed) * m.d * 2;
+  const size_t o = static_cast<size_t>(l) * m.n_kv * slice_elems;
+  uint16_t* dk = ring_.k + static_cast<size_t>(c) * m.n_kv * slice_elems;
+  uint16_t* dv = ring_.v + static_cast<size_t>(c) * m.n_kv * slice_elems;
+  // the chunk's previous layer has been read by its verify range
+  VC_CK(cudaStreamWaitEvent(copy_st_, ring_free_[c], 0));
+  VC_CK(cudaEventRecord(ring_start_[c], copy_st_));
+  if (width > 0) {
+    VC_CK(cudaMemcpy2DAsync(dk, pitch, host_pool_k(v.slot) + o, pitch, width, m.n_kv, cudaMemcpyHostToDevice, copy_st_));
+    VC_CK(cudaMemcpy2DAsync(dv, pitch, host_pool_v(v.slot) + o, pitch, width, m.n_kv, cudaMemcpyHostToDevice, copy_st_));
+  }
+  VC_CK(cudaEventRecord(ring_done_[c], copy_st_));
+  ++v.issued;
+}
+
+void Engine::stream_pump() {
+  // the link serves streams in begin order; a chunk is issued once the ring
+  // chunk it maps to has been released by the range that read its previous layer
+  const int R = cfg_.ring_chunks;
+  for (int id : vs_order_) {
+    VStream& v = vstreams_.at(id);
+    while (v.issued < cfg_.model.layers && ring_owner_[(v.base + v.issued) % R] < 0) stream_issue_chunk(v);
+    if (v.issued < cfg_.model.layers) break;
+  }
+}
+
+int Engine::stream_layers_done(int id) const { return vstreams_.at(id).done; }
+
+int Engine::stream_advance(int id) {
+  VStream& v = vstreams_.at(id);
+  const auto& m = cfg_.model;
+  const int R = cfg_.ring_chunks;
+  if (v.final_enqueued) {
+    const cudaError_t e = cudaEventQuery(v.ev_final);
+    if (e == cudaErrorNotReady) return 0;
+    check_cuda(e, "stream_advance");
+    if (v.preds.empty()) {
+      const int32_t* p = reinterpret_cast<const int32_t*>(static_cast<const uint8_t*>(h_ring_) +
+                                                          v.buf * ring_desc_bytes() + ring_desc_bytes() -
+                                                          static_cast<size_t>(wrows_) * 4);
+      v.preds.assign(p, p + v.x + 1);
+    }
+    return 1;
+  }
+  // chunks that have landed, in layer order
+  while (v.landed < v.issued) {
+    const int c = static_cast<int>((v.base + v.landed) % R);
+    const cudaError_t e = cudaEventQuery(ring_done_[c]);
+    if (e == cudaErrorNotReady) break;
+    check_cuda(e, "stream chunk");
+    float ms = 0.f;
+    VC_CK(cudaEventElapsedTime(&ms, ring_start_[c], ring_done_[c]));
+    h2d_ms_ += ms;
+    h2d_bytes_ += 2.0 * static_cast<double>(v.committed) * m.d * 2 * m.n_kv;
+    ++v.landed;
+  }
+  if (v.landed > v.done) {
+    if (v.x < 0) {  // the first range fixes the window the verify scores
+      const SeqState& s = seqs_.at(v.slot);
+      if (s.committed != v.committed) throw ContractViolation("stream: the request committed during its reload");
+      if (s.drafted.empty()) throw ContractViolation("stream: no drafted tokens to verify");
+      if (static_cast<int>(s.drafted.size()) + 1 > wrows_) throw ContractViolation("stream: window exceeds max_x");
+      v.x = static_cast<int>(s.drafted.size());
+      v.tokens.assign(1, s.pending);
+      v.tokens.insert(v.tokens.end(), s.drafted.begin(), s.drafted.end());
+    }
+    stream_range(v, v.done, v.landed);
+    v.done = v.landed;
+    stream_pump();
+  }
+  return 0;
+}
+
+std::vector<int32_t> Engine::stream_preds(int id) const {
+  const VStream& v = vstreams_.at(id);
+  if (v.preds.empty()) throw ContractViolation("stream: predictions not ready (stream_advance until 1)");
+  return v.preds;
+}
+
+std::vector<int32_t> Engine::accept_commit_stream(int slot, const std::vector<int32_t>& preds, int id) {
+  VStream& v = vstreams_.at(id);
+  if (v.slot != slot) throw ContractViolation("stream: slot mismatch");
+  if (v.preds.empty()) throw ContractViolation("stream: verify not finished");
+  const SeqState& s = seqs_.at(slot);
+  if (static_cast<int>(s.drafted.size()) != v.x || s.pending != v.tokens[0] ||
+      !std::equal(s.drafted.begin(), s.drafted.end(), v.tokens.begin() + 1))
+    throw ContractViolation("stream: the open round is not the window the verify scored");
+  const RowSrc src{wbuf_, v.buf, v.origin};
+  auto em = accept_commit_from(slot, preds, src, true);
+  stream_end(id);
+  return em;
+}
+
+void Engine::stream_end(int id) {
+  auto it = vstreams_.find(id);
+  if (it == vstreams_.end()) return;
+  VStream& v = it->second;
+  const int R = cfg_.ring_chunks;
+  const bool finished = v.final_enqueued && cudaEventQuery(v.ev_final) == cudaSuccess;
+  if (!finished) {
+    // abandoned mid-stream: its copies land and its ranges run first, then
+    // the chunks it still holds go back to the ring
+    VC_CK(cudaStreamSynchronize(copy_st_));
+    VC_CK(cudaStreamSynchronize(st_));
+    for (int l = v.done; l < v.issued; ++l) {
+      const int c = static_cast<int>((v.base + l) % R);
+      if (ring_owner_[c] == v.base + l) ring_owner_[c] = -1;
+    }
+  }
+  if (v.ev_final) cudaEventDestroy(v.ev_final);
+  vbuf_used_[v.buf] = 0;
+  vs_order_.erase(std::find(vs_order_.begin(), vs_order_.end(), id));
+  vstreams_.erase(it);
+  stream_pump();
+}
+
+// The verify forward of a streamed window over layers [a, b): the same
+// kernels as enqueue_forward's verify set, reading layer l's K/V from its ring
+// chunk (dense attention over the ring with one layer per chunk), with the
+// window's exact K/V rows [origin, committed + x + 1) of each layer copied to
+// the stream's window buffer for accept_commit_stream.
+void Engine::stream_range(VStream& v, int a, int b) {
+  const auto& m = cfg_.model;
+  const int L = m.layers, H = m.hidden, F = m.ffn, V = m.vocab, d = m.d;
+  const int qkv_n = (m.n_q + 2 * m.n_kv) * d;
+  const int R = cfg_.ring_chunks;
+  const int n = v.x + 1;
+  const int M = bucket_rows(n);
+  const int mrv = (n + 3) / 4 * 4;
+  const size_t slice_elems = static_cast<size_t>(full_.cap) * d;
+  // descriptors: this buf's mapped region (its previous upload has run)
+  VC_CK(cudaEventSynchronize(ring_upload_[v.buf]));
+  uint8_t* hb = static_cast<uint8_t*>(h_ring_) + v.buf * ring_desc_bytes();
+  const uint8_t* db = static_cast<const uint8_t*>(d_hring_) + v.buf * ring_desc_bytes();
+  int32_t* h_tok = reinterpret_cast<int32_t*>(hb);
+  RowDest* h_rows = reinterpret_cast<RowDest*>(hb + static_cast<size_t>(wrows_) * 4);
+  AttnSeq* h_seqs = reinterpret_cast<AttnSeq*>(hb + static_cast<size_t>(wrows_) * (4 + sizeof(RowDest)));
+  const int32_t* d_preds = reinterpret_cast<const int32_t*>(db + ring_desc_bytes() - static_cast<size_t>(wrows_) * 4);
+  const int c0 = static_cast<int>(v.base % R);
+  for (int i = 0; i < M; ++i) {
+    h_tok[i] = i < n ? v.tokens[i] : 0;
+    h_rows[i] = i < n ? RowDest{4, c0, v.committed + i, v.committed + i} : RowDest{-1, 0, 0, 0};
+  }
+  for (int l = a; l < b; ++l) {
+    AttnSeq q{};
+    q.slot = static_cast<int>((v.base + l) % R);
+    q.row0 = 0;
+    q.n_rows = n;
+    q.kv_len = v.committed + n;
+    q.part0 = 0;
+    h_seqs[l] = q;
+  }
+  {
+    auto dev = [&](const void* h) {
+      return reinterpret_cast<const uint32_t*>(db + (static_cast<const uint8_t*>(h) - hb));
+    };
+    MappedCopy mc{};
+    mc.seg[0] = {dev(h_tok), reinterpret_cast<uint32_t*>(tok_in_), M};
+    mc.seg[1] = {dev(h_rows), reinterpret_cast<uint32_t*>(rows_dev_), static_cast<int>(M * sizeof(RowDest) / 4)};
+    mc.seg[2] = {dev(h_seqs), reinterpret_cast<uint32_t*>(ring_seqs_dev_), static_cast<int>(L * sizeof(AttnSeq) / 4)};
+    mc.n = 3;
+    mapped_copy_kernel<<<8, 256, 0, st_>>>(mc);
+    VC_CK(cudaGetLastError());
+    ++launches_;
+    VC_CK(cudaEventRecord(ring_upload_[v.buf], st_));
+  }
+  AttnShape as;
+  as.layers = 1;  // one layer per ring chunk: slice = chunk * n_kv + head
+  as.n_kv = m.n_kv;
+  as.n_rep = m.n_q / m.n_kv;
+  as.d = d;
+  as.q_stride = qkv_n;
+  as.out_stride = m.n_q * d;
+  as.out_mp = M;
+  as.scale_log2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(d)));
+  as.draft_warps = draft_warps_;
+  as.draft_min_tasks = draft_min_tasks_;
+  float* xs = xsave_ + static_cast<size_t>(v.buf) * wrows_ * H;
+  float* sss = sssave_ + static_cast<size_t>(v.buf) * wrows_ * (H / 128);
+  if (a == 0) {
+    VC_LAUNCH(embed_norm(tok_in_, M, M, w_.embed, H, w_.attn_norm[0], m.eps, x_, xn_, st_));
+  } else {  // resume: the residual stream and its per-tile sums of squares after layer a-1
+    // (SM copies: a copy-engine D2D would queue behind the chunk reloads)
+    MappedCopy mc{};
+    mc.seg[0] = {reinterpret_cast<const uint32_t*>(xs), reinterpret_cast<uint32_t*>(x_), M * H};
+    mc.seg[1] = {reinterpret_cast<const uint32_t*>(sss), reinterpret_cast<uint32_t*>(ss_part_), M * (H / 128)};
+    mc.n = 2;
+    mapped_copy_kernel<<<64, 256, 0, st_>>>(mc);
+    VC_CK(cudaGetLastError());
+    ++launches_;
+    VC_LAUNCH(rms_apply(x_, ss_part_, M, M, H, w_.attn_norm[a], m.eps, xn_, st_));
+  }
+  GemmEpilogue eq;
+  eq.kind = Epi::Qkv;
+  eq.out_bf16 = qkv_;
+  eq.rows = rows_dev_;
+  eq.rope_cos = rope_cos_;
+  eq.rope_sin = rope_sin_;
+  eq.n_q = m.n_q;
+  eq.n_kv = m.n_kv;
+  eq.d = d;
+  eq.layers = L;
+  eq.ring = ring_;
+  eq.ring_n = R;
+  GemmEpilogue er;
+  er.kind = Epi::Residual;
+  er.x = x_;
+  er.ss_part = ss_part_;
+  GemmEpilogue es;
+  es.kind = Epi::Silu;
+  es.out_bf16 = act_;
+  for (int l = a; l < b; ++l) {
+    const int c = static_cast<int>((v.base + l) % R);
+    eq.layer = l;
+    VC_LAUNCH(gemm(xn_, M, M, H, w_.wqkv[l], qkv_n, eq, gws_, st_));
+    // the window's exact rows of this layer (written just now by the qkv
+    // epilogue) and the residual group before them -> the window buffer
+    VC_LAUNCH(copy_rows(ring_, c, v.origin, v.committed + n - v.origin, wbuf_, v.buf * L + l, 0, m.n_kv, d, st_));
+    VC_LAUNCH(dense_attention(as, ring_, ring_maps_, 0, ring_seqs_dev_ + l, 1, max_chunks_d_, mrv, part_, st_));
+    VC_LAUNCH(attention_combine(as, ring_seqs_dev_ + l, 1, max_chunks_d_, mrv, 1, part_, attn_, st_));
+    VC_LAUNCH(gemm(attn_, M, M, m.n_q * d, w_.wo[l], H, er, gws_, st_));
+    VC_LAUNCH(rms_apply(x_, ss_part_, M, M, H, w_.mlp_norm[l], m.eps, xn_, st_));
+    VC_LAUNCH(gemm(xn_, M, M, H, w_.wgu[l], 2 * F, es, gws_, st_));
+    VC_LAUNCH(gemm(act_, M, M, F, w_.wd[l], H, er, gws_, st_));
+    VC_LAUNCH(rms_apply(x_, ss_part_, M, M, H, l + 1 < L ? w_.attn_norm[l + 1] : w_.final_norm, m.eps, xn_, st_));
+  }
+  // the range has read its chunks: release them to the link
+  for (int l = a; l < b; ++l) {
+    const int c = static_cast<int>((v.base + l) % R);
+    VC_CK(cudaEventRecord(ring_free_[c], st_));
+    ring_owner_[c] = -1;
+  }
+  if (b < L) {
+    MappedCopy mc{};
+    mc.seg[0] = {reinterpret_cast<const uint32_t*>(x_), reinterpret_cast<uint32_t*>(xs), M * H};
+    mc.seg[1] = {reinterpret_cast<const uint32_t*>(ss_part_), reinterpret_cast<uint32_t*>(sss), M * (H / 128)};
+    mc.n = 2;
+    mapped_copy_kernel<<<64, 256, 0, st_>>>(mc);
+    VC_CK(cudaGetLastError());
+    ++launches_;
+  } else {
+    GemmEpilogue ef;
+    ef.kind = Epi::StoreF32;
+    ef.out_f32 = logits_;
+    VC_LAUNCH(gemm(xn_, M, M, H, w_.lm_head, V, ef, gws_, st_));
+    VC_LAUNCH(argmax_rows(logits_, M, V, tok_out_, st_));
+    MappedCopy mc{};
+    mc.seg[0] = {reinterpret_cast<const uint32_t*>(tok_out_), const_cast<uint32_t*>(reinterpret_cast<const uint32_t*>(d_preds)), n};
+    mc.n = 1;
+    mapped_copy_kernel<<<1, 256, 0, st_>>>(mc);
+    VC_CK(cudaGetLastError());
+    ++launches_;
+    VC_CK(cudaEventRecord(v.ev_final, st_));
+    v.final_enqueued = true;
+  }
+  (void)slice_elems;
 }
 
 }  // namespace vc

@@ -57,6 +57,13 @@ struct EngineConfig {
   // ffn already divided by tp_size); o_proj/down_proj partials are combined
   // through the attached Collective (vc_tp.h)
   int tp_size = 1, tp_rank = 0;
+  // tier 1, layer-chunked streaming: > 0 replaces the rotating whole-request
+  // staging slots by a ring of ring_chunks one-layer chunks ([kv-head][cap][d]
+  // K and V each); a verify runs layer range by layer range as its chunks
+  // land (Engine::stream_*), so staging HBM is ring_chunks layers, not
+  // n_stage whole requests.  n_stage then holds the resident slots only.
+  int ring_chunks = 0;
+  int max_streams = 2;  // streamed verifies in flight (saved hidden state + exact window rows each)
 };
 
 enum class RowMode : int { Decode = 0, Draft = 1, Verify = 2 };
@@ -149,6 +156,28 @@ class Engine {
   uint64_t swap_begin(int slot, int stage);
   bool swap_done(uint64_t id);
   void swap_wait(uint64_t id);
+  // ---- host tier, layer-chunked (ring_chunks > 0) ------------------------
+  // A streamed verify of an offloaded slot: its committed full KV streams
+  // layer by layer from the host pool into ring chunks on the copy stream
+  // (stream_pump issues a chunk as soon as its ring chunk is free); once the
+  // round's draft window is complete, stream_advance runs the verify forward
+  // over the layers that have landed (hidden state carried between ranges),
+  // releasing each chunk as soon as its layer ran.  When the last layer ran,
+  // the x+1 predictions are ready (stream_preds) and accept_commit_stream
+  // commits from the exact window rows the verify wrote (no staging slot).
+  int stream_begin(int slot);
+  void stream_pump();
+  // 0: in progress; 1: predictions ready.  Requires the slot's open round to
+  // be the window the verify scores (fixed by the first call that runs layers).
+  int stream_advance(int id);
+  std::vector<int32_t> stream_preds(int id) const;
+  std::vector<int32_t> accept_commit_stream(int slot, const std::vector<int32_t>& preds, int id);
+  void stream_end(int id);  // abandon / free (waits for its copies)
+  int streams_active() const { return static_cast<int>(vstreams_.size()); }
+  int stream_layers_done(int id) const;
+  bool ring_mode() const { return cfg_.full_tier == 1 && cfg_.ring_chunks > 0; }
+  // HBM bytes of the host tier's staging: rotating slots, or the chunk ring
+  size_t staging_bytes() const;
   // ---- remote prefix (configs[3]) -------------------------------------
   // The storage node's precomputed KV of one shared prefix: slot's committed
   // full KV and its compressed image (quant tier) snapshotted into pinned
@@ -222,7 +251,32 @@ class Engine {
   void set_kv_rows(const std::vector<StepItem>& items, std::vector<RowDest>& rows) const;
   void enqueue_forward(int M, int n_draft, int n_dense1, int n_densev, int max_rows_v,
                        bool want_logits);
-  void quantise_groups(int slot, int g0, int ng, const KvPool& src, int src_slot);
+  void quantise_groups(int slot, int g0, int ng, const KvPool& src, int src_slot, int origin = 0,
+                       int layer0 = 0, int layers = -1);
+  // where accept_commit reads the exact rows of the round: a pool slot whose
+  // rows are absolute positions minus `origin`
+  struct RowSrc {
+    KvPool pool;
+    int slot;
+    int origin;
+  };
+  std::vector<int32_t> accept_commit_from(int slot, const std::vector<int32_t>& preds, const RowSrc& src,
+                                          bool to_host);
+  struct VStream {
+    int slot = -1, buf = -1;
+    int64_t base = 0;          // chunk sequence number of layer 0 (ring chunk of layer l: (base + l) % R)
+    int issued = 0;            // layers whose chunk copies are enqueued
+    int landed = 0;            // layers whose chunk copies have completed (observed)
+    int done = 0;              // layers the verify forward has run
+    int committed = 0, origin = 0, x = -1;
+    std::vector<int32_t> tokens;  // verify inputs: pending + drafted (fixed at the first range)
+    bool final_enqueued = false;
+    cudaEvent_t ev_final = nullptr;
+    std::vector<int32_t> preds;
+  };
+  void stream_issue_chunk(VStream& v);
+  void stream_range(VStream& v, int a, int b);
+  void ring_fill_layer(int slot, int layer, int chunk, bool from_host);
   void compress_drop(int slot, const KvPool& src, int src_slot, double ratio, const int32_t* kept_host,
                      int k_host);
 
@@ -291,6 +345,27 @@ class Engine {
     double bytes;
   };
   std::map<uint64_t, Xfer> xfers_;
+  // layer-chunk ring (ring_mode)
+  KvPool ring_{};
+  DenseMaps ring_maps_{};
+  std::vector<int64_t> ring_owner_;           // chunk sequence number occupying each chunk (-1 free)
+  std::vector<cudaEvent_t> ring_start_, ring_done_, ring_free_;
+  std::vector<cudaEvent_t> ring_upload_;      // per buf: its last descriptor upload ran
+  // per buf mapped descriptor region: tokens[wrows] | rows[wrows] | seqs[layers] | preds[wrows]
+  size_t ring_desc_bytes() const {
+    return static_cast<size_t>(wrows_) * (4 + sizeof(RowDest) + 4) + cfg_.model.layers * sizeof(AttnSeq);
+  }
+  int64_t ring_seq_ = 0;                      // next chunk sequence number to hand out
+  std::map<int, VStream> vstreams_;
+  std::vector<int> vs_order_;                 // stream ids in begin order (the link serves them FIFO)
+  int next_vstream_ = 1;
+  std::vector<char> vbuf_used_;
+  KvPool wbuf_{};                             // [buf][layer][kv-head][tail_cap][d] exact window rows
+  float *xsave_ = nullptr, *sssave_ = nullptr;  // [buf][Wrows][H], [buf][Wrows][H/128]
+  int wrows_ = 0;
+  AttnSeq* ring_seqs_dev_ = nullptr;          // [layers] per-layer sequence of the range forward
+  void* h_ring_ = nullptr;                    // mapped pinned: tokens | rows | seqs | preds
+  void* d_hring_ = nullptr;
   double h2d_ms_ = 0.0, h2d_bytes_ = 0.0;
   uint64_t next_xfer_ = 1;
   cudaEvent_t ev_a_ = nullptr, ev_b_ = nullptr;

@@ -144,6 +144,9 @@ __device__ void epilogue_pass(const float* sT, int mbase, int M, int Mp, int n0,
         uint16_t* dst;
         if (rd.kind == 1) {
           dst = (is_v ? ep.draft.vtail : ep.draft.ktail) + (slice * ep.draft.tail_cap + rd.pos) * d;
+        } else if (rd.kind == 4) {
+          const size_t rs = static_cast<size_t>((rd.slot + ep.layer) % ep.ring_n) * ep.n_kv + kvh;
+          dst = (is_v ? ep.ring.v : ep.ring.k) + (rs * ep.ring.cap + rd.pos) * d;
         } else {
           const KvPool& p = rd.kind == 0 ? ep.full : (rd.kind == 2 ? ep.stage : ep.drop);
           dst = (is_v ? p.v : p.k) + (slice * p.cap + rd.pos) * d;

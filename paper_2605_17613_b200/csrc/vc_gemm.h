@@ -10,7 +10,8 @@ namespace vc {
 
 // Where a row's freshly computed K/V go (QKV epilogue).
 struct RowDest {
-  int kind;  // 0: full pool, 2: staging pool, 3: drop pool (slot, pos); 1: draft tail (pos = tail index); -1: none
+  int kind;  // 0: full pool, 2: staging pool, 3: drop pool (slot, pos); 1: draft tail (pos = tail index);
+             // 4: layer-chunk ring of a streamed verify (chunk of layer l = (slot + l) % ring_n); -1: none
   int slot;
   int pos;       // position inside the destination (absolute, or tail index for kind 1)
   int rope_pos;  // absolute position (RoPE)
@@ -36,6 +37,9 @@ struct GemmEpilogue {
   int n_q = 0, n_kv = 0, d = 0, layer = 0, layers = 0;
   KvPool full{}, stage{}, drop{};
   QuantPool draft{};
+  // kind 4 rows: ring of ring_n one-layer chunks, [chunk][kv-head][cap][d]
+  KvPool ring{};
+  int ring_n = 1;
 };
 
 struct GemmWorkspace {

@@ -116,7 +116,12 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
   // HBM ring capacity: weights + resident compressed caches + one full KV per
   // rotating staging slot, so the ring never books more reloads than we can
   // stage.  Resident requests' full KV is a fixed carve-out outside the ring.
-  const int n_stage = staged ? cfgE.n_stage - cfgE.resident_slots : std::max(1, cfgE.max_verify);
+  // chunk ring (ring_chunks > 0): reloads stream layer by layer and each
+  // verify runs range by range as its layers land; at most max_streams such
+  // verifies are in flight, so the scheduler books that many reloads
+  const bool ring = en.ring_mode();
+  const int n_stage = staged ? (ring ? cfgE.max_streams : cfgE.n_stage - cfgE.resident_slots)
+                             : std::max(1, cfgE.max_verify);
   cfg.hardware.gpu_mem = sd.hbm_capacity > 0
                              ? sd.hbm_capacity
                              : cfg.model.weights_bytes + resident_total + std::max(1, n_stage) * (kv_max + kv_max / 64);
@@ -145,7 +150,9 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
     const char* v = std::getenv("VC_EXPEDITE");
     return v && v[0] == '1';
   }();
-  sched.set_expedite(expedite && staged);
+  // the chunk ring always expedites: a finished streamed verify holds one of
+  // the max_streams stream slots, and the next reload cannot start behind it
+  sched.set_expedite((expedite || ring) && staged);
   speckv::StepEvents ev;
   for (int i = 0; i < n; ++i) {
     if (is_res[i]) continue;
@@ -198,6 +205,20 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
     int req;
   };
   std::vector<Xfer> inflight;
+  struct VStreamRef {
+    int id;
+    speckv::ReservationId res;
+    int req;
+    int64_t verify_iteration;  // the booked verify (the round may end short of x there)
+    bool ready;  // predictions in; the scheduler has been told the reload landed
+  };
+  std::vector<VStreamRef> vstreams;
+  // a streamed reload starts once its round has at most `lead` drafts to go
+  // (the verify can only run its first layers on a complete window)
+  static const int stream_lead = [] {
+    const char* v = std::getenv("VC_STREAM_LEAD");
+    return v ? std::atoi(v) : 2;
+  }();
   std::set<speckv::ReservationId> kicked;  // reloads already started
   constexpr int kLinkQueue = 2;            // copies kept queued on the link ahead of schedule
   static const bool early_kick = [] {
@@ -318,6 +339,16 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
         return a.verify_iteration != b.verify_iteration ? a.verify_iteration < b.verify_iteration : a.id < b.id;
       });
       for (const auto& r : want) {
+        if (ring) {
+          if (en.streams_active() >= cfgE.max_streams) break;
+          const int req = static_cast<int>(r.request_id);
+          if (static_cast<int>(en.seq(slot_of[req]).drafted.size()) + stream_lead < sd.x &&
+              sched.iteration() + stream_lead < r.verify_iteration)
+            continue;
+          vstreams.push_back({en.stream_begin(slot_of[req]), r.id, req, r.verify_iteration, false});
+          kicked.insert(r.id);
+          continue;
+        }
         if (free_stages.empty()) break;
         if (early_kick && r.span_begin > sched.iteration() && static_cast<int>(inflight.size()) >= kLinkQueue) break;
         const int req = static_cast<int>(r.request_id);
@@ -329,6 +360,21 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
       }
     }
     // 2. completions
+    if (ring) {
+      en.stream_pump();
+      for (auto& v : vstreams) {
+        if (v.ready) continue;
+        // the verify ranges run once the round's window is final: x drafts, or
+        // the booked verify iteration reached (Algorithm 1 stops drafting there)
+        if (static_cast<int>(en.seq(slot_of[v.req]).drafted.size()) < sd.x &&
+            sched.iteration() < v.verify_iteration)
+          continue;
+        if (en.stream_advance(v.id) == 1) {
+          v.ready = true;
+          ev.completed_transfers.push_back(v.res);
+        }
+      }
+    }
     for (size_t i = 0; i < inflight.size();) {
       if (en.swap_done(inflight[i].id)) {
         ev.completed_transfers.push_back(inflight[i].res);
@@ -367,12 +413,16 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
         res_drafting.push_back(i);
       }
     }
-    std::vector<int> verifying;
+    std::vector<int> verifying, ring_verifying;
     for (const auto& v : pr.verifies) {
       const int req = static_cast<int>(v.request);
       const auto& s = en.seq(slot_of[req]);
       if (static_cast<int>(s.drafted.size()) != v.drafted)
         throw vc::ContractViolation("scheduled loop: draft count diverged from the scheduler");
+      if (ring) {  // predictions came from the streamed verify's ranges
+        ring_verifying.push_back(req);
+        continue;
+      }
       vc::StepItem t;
       t.slot = slot_of[req];
       t.mode = vc::RowMode::Verify;
@@ -430,6 +480,24 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
         stage_of[req] = -1;
       }
     }
+    for (int req : ring_verifying) {
+      auto vit = std::find_if(vstreams.begin(), vstreams.end(), [&](const VStreamRef& v) { return v.req == req; });
+      if (vit == vstreams.end() || !vit->ready) throw vc::ContractViolation("scheduled loop: verify without a streamed result");
+      const auto em = en.accept_commit_stream(slot_of[req], en.stream_preds(vit->id), vit->id);
+      vstreams.erase(vit);
+      meas.accepted.push_back(static_cast<int>(em.size()) - 1);
+      accepted_sum += static_cast<double>(em.size()) - 1;
+      for (int32_t t : em)
+        if (produced[req] < sd.K) {
+          out[static_cast<size_t>(req) * sd.K + produced[req]++] = t;
+          emitted_now += 1;
+        }
+      if (produced[req] >= sd.K && done_at[req] < 0) done_at[req] = t_emit;
+      if (it >= sd.warmup_iterations) {
+        st.timed_verifies += 1;
+        st.timed_verify_rows += static_cast<double>(em.size());  // streamed: rows ran in earlier ranges
+      }
+    }
     for (int i : res_verifying) {
       const int x_r = static_cast<int>(en.seq(slot_of[i]).drafted.size());
       std::vector<int32_t> p(row.begin() + off, row.begin() + off + x_r + 1);
@@ -476,6 +544,7 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
   // a bounded window may end mid-round: land the in-flight reloads and roll
   // the open draft rounds back, so the slots can be scheduled again
   for (const Xfer& x : inflight) en.swap_wait(x.id);
+  for (const auto& v : vstreams) en.stream_end(v.id);
   for (int i = 0; i < n_total; ++i)
     if (slot_of[i] >= 0 && !freed[i]) en.discard_drafts(slot_of[i]);
   st.wall_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
@@ -503,7 +572,10 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
     st.interconnect_busy = end > 0 ? (en.h2d_ms() - h2d_ms_start) / 1e3 / end : 0.0;
     const int64_t slot_bytes = static_cast<int64_t>(en.full_pool().cap) * static_cast<int64_t>(bpt);
     st.peak_hbm_bytes = static_cast<int64_t>(en.weight_bytes()) + compressed_all +
-                        (staged ? static_cast<int64_t>(cfgE.n_stage) : static_cast<int64_t>(n)) * slot_bytes;
+                        (staged ? static_cast<int64_t>(cfgE.resident_slots) * slot_bytes +
+                                      static_cast<int64_t>(en.staging_bytes())
+                                : static_cast<int64_t>(n) * slot_bytes);
+    st.staging_bytes = static_cast<int64_t>(en.staging_bytes());
   }
   st.verifies += res_verifies;  // mean_accept below covers both tiers
   accepted_sum += res_accepted;

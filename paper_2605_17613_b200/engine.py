@@ -102,7 +102,8 @@ class Engine:
 
     def __init__(self, model: ModelShape, *, max_slots=1, max_ctx=4096, max_x=16, quant_bits=4,
                  full_tier=0, n_stage=2, max_verify=2, use_graphs=True, device=0, drop_ratio=0.0,
-                 tp_size=1, tp_rank=0, drop_window=0, resident_slots=0, draft_depth=1):
+                 tp_size=1, tp_rank=0, drop_window=0, resident_slots=0, draft_depth=1,
+                 ring_chunks=0, max_streams=2):
         """quant_bits > 0: quant-uniform compressor (KIVI int4/int2);
         drop_ratio in (0, 1): drop-topk compressor keeping llround(c*T) tokens per
         (layer, head) -- the two are exclusive (compressor.cpp:245-254).
@@ -112,7 +113,10 @@ class Engine:
         compress stay in a sliding window of the latest drop_window..2*drop_window.
         resident_slots > 0 (full_tier 1): per-request placement -- slots
         [0, resident_slots) keep their full KV resident in HBM (the reference's
-        B_g), the pinned host pool holds the other slots only (B_c)."""
+        B_g), the pinned host pool holds the other slots only (B_c).
+        ring_chunks > 0 (full_tier 1): reloads stream layer by layer into a ring
+        of one-layer chunks and each verify runs range by range as its layers
+        land (stream_*); n_stage then holds only the resident slots."""
         self.lib = _lib.load()
         self.model = model
         self.max_x = max_x
@@ -120,7 +124,8 @@ class Engine:
                             model.d_head, model.ffn, model.rope_theta, model.rms_eps)
         rt = _lib.RuntimeDesc(max_slots, max_ctx, max_x, quant_bits, full_tier, n_stage,
                               max_verify, int(use_graphs), float(drop_ratio), int(tp_size), int(tp_rank),
-                              int(drop_window), int(resident_slots), int(draft_depth))
+                              int(drop_window), int(resident_slots), int(draft_depth),
+                              int(ring_chunks), int(max_streams))
         self.tp_size, self.tp_rank = int(tp_size), int(tp_rank)
         h = C.c_void_p()
         check(self.lib.vc_engine_create(C.byref(md), C.byref(rt), device, C.byref(h)))
@@ -401,6 +406,36 @@ class Engine:
         check(self.lib.vc_run_scheduled(self.h, _ptr(s, C.c_int), s.size, C.byref(sd),
                                         _ptr(out, C.c_int32), C.byref(st)))
         return out, {f: getattr(st, f) for f, _ in st._fields_}
+
+    # ---- layer-chunked host tier (ring_chunks > 0) --------------------------------
+    def stream_begin(self, slot) -> int:
+        """Start streaming slot's committed full KV layer by layer (returns an id)."""
+        i = C.c_int()
+        check(self.lib.vc_stream_begin(self.h, slot, C.byref(i)))
+        return i.value
+
+    def stream_advance(self, sid, x):
+        """Run the verify over the layers landed so far (the open round must be
+        complete) -> the x+1 predictions once every layer ran, else None."""
+        done = C.c_int()
+        preds = np.zeros(x + 1, np.int32)
+        check(self.lib.vc_stream_advance(self.h, sid, C.byref(done), _ptr(preds, C.c_int32)))
+        return preds if done.value else None
+
+    def stream_accept(self, slot, sid):
+        """Accept + commit from the finished streamed verify -> emitted tokens."""
+        out = np.zeros(self.max_x + 2, np.int32)
+        n = C.c_int()
+        check(self.lib.vc_stream_accept(self.h, slot, sid, _ptr(out, C.c_int32), C.byref(n)))
+        return out[:n.value]
+
+    def stream_abort(self, sid):
+        check(self.lib.vc_stream_abort(self.h, sid))
+
+    def staging_bytes(self) -> int:
+        b = C.c_int64()
+        check(self.lib.vc_engine_staging_bytes(self.h, C.byref(b)))
+        return b.value
 
     def run_decode_fifo(self, requests, K):
         """baseline_full_kv (sim.cpp:418-494): requests = [(n_ctx, first_token,
