@@ -541,17 +541,21 @@ def main_capped(args, rank, world, local):
     max_ctx = ctx + it_w + it_k + 3 * (x + 1) + 8
     slot_b = (max_ctx + x + 130) * bpt
     comp_b = ctx * bpt * (bits / 16.0) * 1.07 + 2 * (128 + x + 2) * 2 * shape.d_head * shape.layers * shape.n_kv
-    n_stage = int((free - weights - reserve - B * comp_b) // slot_b)
-    resident = max(0, min(B - 1, n_stage - args.stages_rot))
-    n_stage = resident + args.stages_rot
+    # staging of the offloaded requests' reloads: the chunk ring (--ring > 0,
+    # ring + 2 one-layer chunks) or stages_rot whole-request slots
+    layer_b = slot_b / shape.layers
+    stage_b = (args.ring + 2) * layer_b if args.ring else args.stages_rot * slot_b
+    resident = max(0, min(B - 1, int((free - weights - reserve - B * comp_b - stage_b) // slot_b)))
+    n_stage = resident if args.ring else resident + args.stages_rot
     host_need = (B - resident) * slot_b
     host_avail = psutil.virtual_memory().available
     if host_need > 0.8 * host_avail:
         raise SystemExit(f"capped: pinned host pool {host_need / 1e9:.0f} GB exceeds 80% of available host "
                          f"memory {host_avail / 1e9:.0f} GB; lower --batch")
     ev = vc.Engine(shape, max_slots=B, max_ctx=max_ctx, max_x=x, quant_bits=bits, full_tier=1, n_stage=n_stage,
-                   resident_slots=resident, max_verify=args.stages_rot + (resident + x_res) // (x_res + 1) + 2,
-                   device=local)
+                   resident_slots=resident,
+                   max_verify=(0 if args.ring else args.stages_rot) + (resident + x_res) // (x_res + 1) + 2,
+                   device=local, ring_chunks=args.ring, max_streams=args.streams)
     ev.init_weights(seed=0, std=0.02, resid_std=rs, q_std=qs)
     for i in range(B):
         ev.add_synthetic(i, ctx, first[i], seed=shard.seeds[i])
@@ -606,6 +610,9 @@ def main_capped(args, rank, world, local):
                     "h2d_bytes_per_step": int((st["timed_rows"] * 20 + st["h2d_bytes"]) / K),
                     "d2h_bytes_per_step": int(st["timed_rows"] / K * 4)},
             "placement": {"B_g_resident": resident, "B_c_offloaded": B - resident, "n_stage": n_stage,
+                          "staging_hbm_bytes": int(st["staging_bytes"]),
+                          "staging": (f"chunk ring: {args.ring} one-layer chunks + 2, {args.streams} streams"
+                                      if args.ring else f"{args.stages_rot} rotating whole-request slots"),
                           "resident_tokens_in_window": st["timed_resident_tokens"],
                           "resident_accepted_per_verify": round(st["resident_accept"], 3),
                           "accepted_per_verify": round(st["mean_accept"], 3),

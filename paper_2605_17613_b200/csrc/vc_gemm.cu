@@ -29,6 +29,8 @@
 // fp32 accumulators in TMEM (double-buffered across a CTA's tiles), 8
 // epilogue warps read them with tcgen05.ld.  (r1: the mma.sync version this
 // replaces ran a 113-row verify step's projections 2.4x slower.)
+#include <cstdlib>
+
 #include "vc_common.cuh"
 #include "vc_gemm.h"
 #include "vc_tiled.cuh"
@@ -425,6 +427,158 @@ gemm_umma_kernel(const uint16_t* __restrict__ Xt, int Mp, int M, int K,
   if (warp == 1) tmem_dealloc(tbase, kAccCols);
 }
 
+// Cluster split-K for weights with few output tiles (qkv, o_proj, down_proj
+// at decode widths): tile t's K range is split over the S CTAs of one thread-
+// block cluster (rank r streams k-tiles [r*KT/S, (r+1)*KT/S)), each CTA parks
+// its fp32 accumulator in its own shared memory, and after one cluster barrier
+// rank r sums tokens [r*NT/S, (r+1)*NT/S) of all S partials over DSMEM in
+// rank order 0..S-1 and runs the fused epilogue on them.  Compared with the
+// stream-K fixup (partials through L2, a gpu-scope fence + atomic per tile,
+// then one finisher reading every partial) the reduction is spread over the
+// whole cluster and never leaves the GPC.  S depends only on (N, K): batch
+// invariance holds (a token's sum has the same operands in the same order at
+// every M).
+template <int NT, Epi E>
+__global__ void __launch_bounds__(kThreads, kCtasPerSm)
+gemm_cluster_kernel(const uint16_t* __restrict__ Xt, int Mp, int M, int K,
+                    const uint16_t* __restrict__ Wt, int N, int m0, GemmEpilogue ep, int S) {
+  constexpr int ST = Cfg<NT>::kStages;
+  constexpr int WB = Cfg<NT>::kW, XB = Cfg<NT>::kX;
+  constexpr uint32_t kAccCols = NT < 32 ? 32 : NT;
+  constexpr int kHalf = NT / 2;
+  static_assert(kBN * NT * 4 <= ST * (WB + XB), "the parked accumulator fits the pipeline stages");
+  extern __shared__ uint8_t gsm_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(gsm_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* sW = smem;
+  uint8_t* sX = smem + ST * WB;
+  float* sT = reinterpret_cast<float*>(smem + ST * (WB + XB));  // [16][kLD] epilogue staging
+  float* sAcc = reinterpret_cast<float*>(smem);                 // [NT][128] parked partial (reuses the stages)
+  __shared__ __align__(8) uint64_t full[ST], empty[ST], acc_full;
+  __shared__ uint32_t tmem_base_sh;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int KT = K / kBK;
+  const int rank = static_cast<int>(cluster_rank());
+  const int tile = blockIdx.x / S;
+  const int k_lo = rank * KT / S, k_hi = (rank + 1) * KT / S;
+  const int nk = k_hi - k_lo;
+  if (tid == 0) {
+    for (int s2 = 0; s2 < ST; ++s2) {
+      mbar_init(&full[s2], 1);
+      mbar_init(&empty[s2], 1);
+    }
+    mbar_init(&acc_full, 1);
+    fence_mbar_init();
+  }
+  if (warp == 1) tmem_alloc(&tmem_base_sh, kAccCols);
+  tmem_fence_before();
+  __syncthreads();
+  tmem_fence_after();
+  const uint32_t tbase = tmem_base_sh;
+  pdl_trigger();
+
+  if (warp == 0) {  // ---- TMA producer
+    if (lane == 0) {
+      const int pre = min(ST, nk);
+      for (int i = 0; i < pre; ++i) {  // weights do not depend on the previous kernel
+        mbar_expect_tx(&full[i], WB + XB);
+        tma_load_1d(sW + i * WB, Wt + (static_cast<size_t>(tile) * KT + k_lo + i) * 8192, WB, &full[i]);
+      }
+      pdl_wait();
+      for (int i = 0; i < pre; ++i)
+        tma_load_1d(sX + i * XB, Xt + (static_cast<size_t>(k_lo + i) * Mp + m0) * 64, XB, &full[i]);
+      for (int i = pre; i < nk; ++i) {
+        const int st = i % ST;
+        mbar_wait(&empty[st], ((i / ST) - 1) & 1);
+        mbar_expect_tx(&full[st], WB + XB);
+        tma_load_1d(sW + st * WB, Wt + (static_cast<size_t>(tile) * KT + k_lo + i) * 8192, WB, &full[st]);
+        tma_load_1d(sX + st * XB, Xt + (static_cast<size_t>(k_lo + i) * Mp + m0) * 64, XB, &full[st]);
+      }
+    }
+  } else if (warp == 1) {  // ---- MMA issuer
+    if (lane == 0) {
+      constexpr uint32_t idesc = umma_idesc_bf16(kBN, NT, false);
+      for (int i = 0; i < nk; ++i) {
+        const int st = i % ST;
+        mbar_wait(&full[st], (i / ST) & 1);
+        tmem_fence_after();
+        const uint32_t wa = smem_u32(sW + st * WB), xa = smem_u32(sX + st * XB);
+#pragma unroll
+        for (int kk = 0; kk < kBK / 16; ++kk)
+          umma_ss(tbase, umma_sdesc_sw128(wa + kk * 32, 16, 1024), umma_sdesc_sw128(xa + kk * 32, 16, 1024), idesc,
+                  i > 0 || kk > 0);
+        umma_commit(&empty[st]);
+      }
+      umma_commit(&acc_full);
+    }
+  } else {  // ---- park the partial: TMEM -> sAcc[token][feature]
+    pdl_wait();  // the epilogue writes buffers the previous kernel may read
+    const int et = tid - 64;
+    const int quarter = warp & 3;
+    const int feat = quarter * 32 + lane;
+    const int tok0 = et >= 128 ? kHalf : 0;
+    const uint32_t tacc = tbase + (static_cast<uint32_t>(quarter * 32) << 16) + tok0;
+    mbar_wait(&acc_full, 0);
+    tmem_fence_after();
+    for (int c = 0; c < kHalf; c += 8) {
+      uint32_t u[8];
+      asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];\n"
+                   : "=r"(u[0]), "=r"(u[1]), "=r"(u[2]), "=r"(u[3]), "=r"(u[4]), "=r"(u[5]), "=r"(u[6]), "=r"(u[7])
+                   : "r"(tacc + c));
+      tmem_wait_ld();
+#pragma unroll
+      for (int j = 0; j < 8; ++j) sAcc[(tok0 + c + j) * kBN + feat] = __uint_as_float(u[j]);
+    }
+    tmem_fence_before();
+  }
+  __syncwarp();
+  cluster_sync();  // every rank's partial is parked
+  if (warp >= 2) {
+    // ---- reduce my tokens over the cluster (rank order), then the epilogue
+    const int et = tid - 64;
+    const int t_lo = rank * NT / S, t_hi = (rank + 1) * NT / S;
+    const int n0 = tile * kBN;
+    for (int p0 = t_lo; p0 < t_hi && m0 + p0 < M; p0 += kEpiRows) {
+      const int rows = min(kEpiRows, t_hi - p0);
+      // rows x 32 float4 per pass; 256 threads
+      for (int e = et; e < rows * (kBN / 4); e += 256) {
+        const int t = e / (kBN / 4), f4 = e % (kBN / 4);
+        const float* src = sAcc + (p0 + t) * kBN + f4 * 4;
+        float4 acc = ld_dsmem_f4(dsmem_addr(src, 0));
+        for (int q = 1; q < S; ++q) {
+          const float4 v = ld_dsmem_f4(dsmem_addr(src, q));
+          acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
+        }
+        float* d = sT + t * kLD + f4 * 4;
+        d[0] = acc.x; d[1] = acc.y; d[2] = acc.z; d[3] = acc.w;
+      }
+      named_bar(1, 256);
+      epilogue_pass<E>(sT, m0 + p0, min(M, m0 + p0 + rows), Mp, n0, N, ep, et);
+      named_bar(1, 256);
+    }
+  }
+  __syncwarp();
+  cluster_sync();  // no rank leaves while another may still read its partial
+  if (warp == 1) tmem_dealloc(tbase, kAccCols);
+}
+
+// Cluster size for (N, K): S = min(5, stream-K contributors per tile, k-tiles);
+// below 3 the stream-K path (gate/up, LM head).  r2 sweep of a uniform S on
+// the mixed x=6 step (in-graph ms): stream-K 8.62, S=3 8.30, 4 8.13, 5 8.06,
+// 6 8.26, 8 8.49; S = round(148 / tiles) per shape (qkv 3, o/down 5) 8.11.
+// VC_GEMM_CLUSTER=n sets the cap (1 = stream-K everywhere).
+int cluster_splits(int N, int K) {
+  static const int cap = [] {
+    const char* v = std::getenv("VC_GEMM_CLUSTER");
+    return v && std::atoi(v) > 0 ? std::atoi(v) : 5;
+  }();
+  const int tiles = N / kBN, KT = K / kBK;
+  int S = kP / tiles;
+  if (S > cap) S = cap;
+  if (S > 8) S = 8;
+  if (S > KT) S = KT;
+  return S >= 3 ? S : 1;
+}
+
 int max_contributors(int N, int K) {
   const long KT = K / kBK, tiles = N / kBN, T = tiles * KT;
   int mx = 1;
@@ -438,6 +592,20 @@ int max_contributors(int N, int K) {
 template <int NT, Epi E>
 cudaError_t launch_nt(const uint16_t* Xt, int Mp, int M, int K, const uint16_t* Wt, int N,
                       const GemmEpilogue& ep, const GemmWorkspace& ws, cudaStream_t st) {
+  const int S = cluster_splits(N, K);
+  if (S > 1) {
+    auto kc = gemm_cluster_kernel<NT, E>;
+    const int smem = Cfg<NT>::kSmem;
+    cudaError_t e = cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    if (e != cudaSuccess) return e;
+    const unsigned grid = static_cast<unsigned>((N / kBN) * S);
+    for (int m0 = 0; m0 < M; m0 += NT) {
+      e = launch_pdl_cluster(kc, dim3(grid), dim3(kThreads), smem, st, static_cast<unsigned>(S), Xt, Mp, M, K, Wt,
+                             N, m0, ep, S);
+      if (e != cudaSuccess) return e;
+    }
+    return cudaSuccess;
+  }
   auto kern = gemm_umma_kernel<NT, E>;
   const int smem = Cfg<NT>::kSmem;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);

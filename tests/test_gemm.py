@@ -37,9 +37,11 @@ def test_gemm_matches_fp64(cuda, M, N, K):
     assert np.abs(y - ref).max() <= tol
 
 
-def test_gemm_batch_invariance(cuda):
+# (6144, 4096) qkv, (4096, 4096) o_proj and (4096, 14336) down_proj run the
+# cluster split-K path (S = 6, 8, 8); (28672, 4096) gate/up the stream-K path
+@pytest.mark.parametrize("N,K", [(6144, 4096), (4096, 4096), (4096, 14336), (28672, 4096)])
+def test_gemm_batch_invariance(cuda, N, K):
     rng = np.random.default_rng(0)
-    K, N = 4096, 6144
     X = T.f32_to_bf16(rng.standard_normal((200, K)).astype(np.float32))
     W = T.f32_to_bf16((rng.standard_normal((N, K)) * 0.02).astype(np.float32))
     full = _gemm(cuda, X, W)
