@@ -197,6 +197,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tmem_fence_after();
   const uint32_t tbase = tmem_base_sh;
   pdl_wait();  // q rows and the window's new K/V come from the qkv epilogue
+  if (s.trace && threadIdx.x == 0 && blockIdx.x < 4096) s.trace[blockIdx.x * 2] = vc_globaltimer();
 
   if (warp == 0) {
     // ===================== TMA producer =====================
@@ -503,6 +504,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   tmem_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc(tbase, 512);
+  if (s.trace && threadIdx.x == 0 && blockIdx.x < 4096) s.trace[blockIdx.x * 2 + 1] = vc_globaltimer();
 }
 
 template <int D, int NREP>

@@ -200,6 +200,14 @@ __global__ void __launch_bounds__(kWarps * 32, NREP == 8 ? 3 : VC_DRAFT_MINB) dr
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int TC = (pool.tail_cap + VC_TAIL_CHUNK - 1) / VC_TAIL_CHUNK;
   const int n_tail_ctas = n_seq * s.n_kv * TC;
+  // VC_ATTN_TRACE diagnostics: this CTA's start/end on the global timer
+  struct TraceEnd {
+    unsigned long long* tr;
+    __device__ ~TraceEnd() {
+      if (tr && threadIdx.x == 0 && blockIdx.x < 2048) tr[8192 + blockIdx.x * 2 + 1] = vc_globaltimer();
+    }
+  } trace_end{s.trace};
+  if (s.trace && threadIdx.x == 0 && blockIdx.x < 2048) s.trace[8192 + blockIdx.x * 2] = vc_globaltimer();
   pdl_trigger();
   if (static_cast<int>(blockIdx.x) < n_tail_ctas) {
     pdl_wait();  // the tail holds this step's new K/V (qkv epilogue)

@@ -169,6 +169,7 @@ Engine::Engine(const EngineConfig& cfg, int device) : cfg_(cfg), device_(device)
   VC_CK(cudaEventCreate(&ev_b_));
   alloc_all();
   seqs_.resize(cfg_.max_slots);
+  if (std::getenv("VC_ATTN_TRACE")) attn_trace_ = dmalloc<unsigned long long>(3 * 8192);
 }
 
 Engine::~Engine() {
@@ -934,6 +935,7 @@ void Engine::enqueue_forward(int M, int n_draft, int n_dense1, int n_densev, int
     const char* v = std::getenv("VC_SKIP");
     return v ? std::atoi(v) : 0;
   }();
+  unsigned long long* attn_trace = attn_trace_;
   VC_LAUNCH(embed_norm(tok_in_, M, M, w_.embed, H, w_.attn_norm[0], m.eps, x_, xn_, st_));
   trace("embed.x", x_, static_cast<size_t>(M) * H * 4);
   trace("w.gu0", w_.wgu[0], static_cast<size_t>(2) * F * H * 2);
@@ -952,12 +954,15 @@ void Engine::enqueue_forward(int M, int n_draft, int n_dense1, int n_densev, int
       c.mode = mode;
       c.rows = rows;
     };
+    if (attn_trace && l == 5) VC_CK(cudaMemsetAsync(attn_trace, 0, 3 * 8192 * 8, st_));
     if (skip & 1) {
     } else if (n_draft > 0 && drop_mode()) {
       VC_LAUNCH(dense_attention(as, drop_, drop_maps_, l, seqs_dev_, n_draft, max_chunks_x_, 1, part_, st_));
       add_set(seqs_dev_, n_draft, max_chunks_x_, 1, 1);
     } else if (n_draft > 0) {
-      VC_LAUNCH(draft_attention_quant(as, quant_, l, qkv_, seqs_dev_, n_draft, max_chunks_q_,
+      AttnShape tx = as;
+      if (l == 5) tx.trace = attn_trace;
+      VC_LAUNCH(draft_attention_quant(tx, quant_, l, qkv_, seqs_dev_, n_draft, max_chunks_q_,
                                       cfg_.quant_bits, part_, st_));
       add_set(seqs_dev_, n_draft, max_chunks_q_, 0, 1);
     }
@@ -967,7 +972,9 @@ void Engine::enqueue_forward(int M, int n_draft, int n_dense1, int n_densev, int
     }
     if (n_densev > 0 && !(skip & 1)) {
       const AttnSeq* sv = seqs_dev_ + n_draft + n_dense1;
-      VC_LAUNCH(dense_attention(as, dense_v_pool, dense_maps_, l, sv, n_densev, max_chunks_d_, max_rows_v, part_, st_));
+      AttnShape tv = as;
+      if (l == 5) tv.trace = attn_trace;
+      VC_LAUNCH(dense_attention(tv, dense_v_pool, dense_maps_, l, sv, n_densev, max_chunks_d_, max_rows_v, part_, st_));
       add_set(sv, n_densev, max_chunks_d_, 1, max_rows_v);
     }
     if (cs.n_sets > 0) VC_LAUNCH(attention_combine_sets(as, cs, part_, attn_, st_));
@@ -1166,6 +1173,28 @@ void Engine::run_step(const std::vector<StepItem>& items, std::vector<int32_t>& 
                  drafts.size(), dense1.size(), densev.size(), max_rows_v, ms);
   out.assign(h_out_, h_out_ + M);
   last_M_ = M;
+  if (attn_trace_) {  // diagnostics: layer 5's attention CTA timeline (ns from the first dense/draft start)
+    std::vector<unsigned long long> t(3 * 8192);
+    VC_CK(cudaMemcpy(t.data(), attn_trace_, t.size() * 8, cudaMemcpyDeviceToHost));
+    auto span = [&](size_t off, size_t n, unsigned long long& lo, unsigned long long& hi, int& cnt, double& avg) {
+      lo = ~0ull; hi = 0; cnt = 0; avg = 0;
+      for (size_t i = 0; i < n; ++i) {
+        const unsigned long long a = t[off + 2 * i], b = t[off + 2 * i + 1];
+        if (!a || !b) continue;
+        lo = std::min(lo, a); hi = std::max(hi, b); ++cnt; avg += static_cast<double>(b - a);
+      }
+      if (cnt) avg /= cnt;
+    };
+    unsigned long long dl, dh, ql, qh;
+    int dc, qc;
+    double da, qa;
+    span(0, 4096, dl, dh, dc, da);
+    span(8192, 2048, ql, qh, qc, qa);
+    const unsigned long long t0 = std::min(dc ? dl : ~0ull, qc ? ql : ~0ull);
+    std::fprintf(stderr, "ATTN dense ctas=%d [%.1f, %.1f] us avg %.1f | draft ctas=%d [%.1f, %.1f] us avg %.1f\n", dc,
+                 dc ? (dl - t0) / 1e3 : 0.0, dc ? (dh - t0) / 1e3 : 0.0, da / 1e3, qc, qc ? (ql - t0) / 1e3 : 0.0,
+                 qc ? (qh - t0) / 1e3 : 0.0, qa / 1e3);
+  }
 }
 
 void Engine::kernel_bench(int kind, const std::vector<int>& slots, int reps, double* ms,

@@ -371,6 +371,7 @@ class Engine {
   cudaEvent_t ev_a_ = nullptr, ev_b_ = nullptr;
   double device_ms_ = 0.0;
   int64_t steps_ = 0;
+  unsigned long long* attn_trace_ = nullptr;  // VC_ATTN_TRACE diagnostics buffer
 };
 
 // Thrown on CUDA failures; vc_api maps it to VC_ERR_CUDA.

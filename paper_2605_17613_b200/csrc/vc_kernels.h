@@ -86,7 +86,15 @@ struct AttnShape {
   float scale_log2;    // log2(e)/sqrt(d)
   int draft_warps;     // quantised-draft warps launched (persistent, draft_quant_warps)
   int draft_min_tasks; // fewest group tasks a draft warp takes (bounds partials per head)
+  // diagnostics (VC_ATTN_TRACE): per-CTA globaltimer at start/end, [2][4096] u64
+  // (dense CTAs at [0], draft CTAs at [4096]); nullptr = off
+  unsigned long long* trace = nullptr;
 };
+__device__ __forceinline__ unsigned long long vc_globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 
 // Draft-attention work split: the T = sum(n_groups * n_kv) group tasks of a
 // step, ordered (sequence, kv head, group), are cut into nw contiguous ranges
