@@ -71,6 +71,8 @@ def parse():
     p.add_argument("--ring", type=int, default=8,
                    help="host tier: one-layer chunks of the streaming ring (0: whole-request staging slots)")
     p.add_argument("--streams", type=int, default=2, help="host tier, --ring > 0: streamed verifies in flight")
+    p.add_argument("--drop-score", default="snapkv", choices=["snapkv", "norm"],
+                   help="--config 3 (drop-topk): SnapKV observation attention or the L1 key norm")
     p.add_argument("--stages-rot", type=int, default=3,
                    help="rotating staging slots of the offloaded requests when some are resident")
     p.add_argument("--small", action="store_true", help="tiny model smoke run")
@@ -134,16 +136,15 @@ class Clocks:
                 "reasons": sorted(reasons), "samples": len(load)}
 
 
-def cpu_port_sample(tokens: int = 3):
+def cpu_port_sample(tokens: int = 3, ctx: int = 32768):
     """The CPU oracle (vco_forward, fp64 accumulate, all host threads) on a
-    bounded sample of configs[1]: one Llama-3-8B-shape layer at 32K context
-    and the LM head, timed separately over `tokens` decode tokens, then
-    composed to a full token: t = 32 * t_layer + t_head."""
+    bounded sample of the workload: one Llama-3-8B-shape layer at `ctx`
+    context and the LM head, timed separately over `tokens` decode tokens,
+    then composed to a full token: t = 32 * t_layer + t_head."""
     import numpy as np
     import vc_testlib as T
     from paper_2605_17613_b200 import LLAMA3_8B, ModelShape
     s = LLAMA3_8B
-    ctx = 32768
     o = T.oracle()
     rng_off = [0]
 
@@ -181,7 +182,7 @@ def cpu_port_sample(tokens: int = 3):
     t_token = s.layers * t_layer + t_head
     return {"value": 1.0 / t_token, "unit": "tokens/s", "cores": int(o.vco_threads()), "kind": "port",
             "sample": f"oracle/vc_oracle.c vco_forward (fp64 accumulate, {int(o.vco_threads())} threads): one "
-                      f"Llama-3-8B-shape layer at 32K context and the LM head timed over {tokens} decode tokens "
+                      f"Llama-3-8B-shape layer at {ctx // 1024}K context and the LM head timed over {tokens} decode tokens "
                       f"each; token time = 32 x layer + head",
             "sample_seconds": round(tokens * (t_one + t_head), 2),
             "layer_s": round(t_layer, 4), "head_s": round(t_head, 4)}
@@ -470,7 +471,8 @@ def main_remote(args, rank, world, local):
                          "ms_per_launch": round(ka_ms / shape.layers, 4), "peak_source": peak_src},
             "compressed": {"bit_scheme": meta["bit_scheme"], "payload_bytes": meta["payload_bytes"],
                            "full_bytes": meta["full_bytes"]},
-            "gpu_launches": int(launches), "clocks": clk_summary, "cpu_baseline": None,
+            "gpu_launches": int(launches), "clocks": clk_summary,
+            "cpu_baseline": None if args.no_cpu or args.small else cpu_port_sample(ctx=ctx),
         }
         print(json.dumps(line), flush=True)
     if dist:
@@ -881,7 +883,8 @@ def main():
             ev = vc.Engine(shape, max_slots=B, max_ctx=ctx + it_w + it_k + 3 * (x + 1) + 8, max_x=max(x, x_res),
                            quant_bits=0 if drop else args.bits, drop_ratio=drop, full_tier=tier,
                            n_stage=n_stage if tier else 1, max_verify=max_verify, device=local,
-                           resident_slots=resident, ring_chunks=ring, max_streams=args.streams)
+                           resident_slots=resident, ring_chunks=ring, max_streams=args.streams,
+                           drop_score=args.drop_score if drop else "norm")
         except vc.VcError as ex:
             err = ex
         if dist:  # every rank falls back together (the pinned pool may fail on one rank only)
@@ -1032,7 +1035,7 @@ def main():
         return {"header": CSV_HEADER, "rows": rows}
 
     if rank == 0:
-        cpu = None if args.no_cpu or args.small else cpu_port_sample()
+        cpu = None if args.no_cpu or args.small else cpu_port_sample(ctx=ctx)
         meta = h["meta"]
         line = {
             "metric": METRIC,
@@ -1041,8 +1044,10 @@ def main():
             "vs_baseline": None, "dtype": "bf16",
             "data": f"synthetic (random-init weights N(0,0.02); q_proj N(0,{qs:.4g}), o/down_proj N(0,{rs:.4g}) "
                     f"calibrated to the paper's acceptance, 21.1 of x=30; synthetic 32K prefix KV)",
-            "config": {"workload": (f"configs[2]: Llama-3.1-8B shape, {ctx} ctx, drop-topk c={drop} (L1 key-norm "
-                                    f"scores, top-k per layer/head), batch {B}/GPU, full KV in HBM") if cfg3 else
+            "config": {"workload": (f"configs[2]: Llama-3.1-8B shape, {ctx} ctx, drop-topk c={drop} ("
+                                    + ("SnapKV observation-attention scores, pool 7, last 32 kept"
+                                       if args.drop_score == "snapkv" else "L1 key-norm scores")
+                                    + f", top-k per layer/head), batch {B}/GPU, full KV in HBM") if cfg3 else
                                    (f"configs[1]: {'tiny' if args.small else 'Llama-3-8B shape'}, {ctx} ctx, "
                                     f"int{args.bits} KIVI, batch {B}/GPU, full KV in "
                                     f"{'pinned host memory' if head_tier else 'HBM'}"),

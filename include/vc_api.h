@@ -96,6 +96,11 @@ typedef struct {
                          rotating whole-request slots (n_stage then holds only the
                          resident slots).  0 = whole-request staging slots.       */
   int max_streams;    /* ring_chunks > 0: streamed verifies in flight (0 -> 2) */
+  int drop_score;     /* drop-topk token scores: 0 = L1 norm of the post-RoPE key;
+                         1 = SnapKV (observation-window attention of the pending
+                         token, summed over the GQA group, max-pooled; HBM full tier) */
+  int snap_pool;      /* SnapKV max-pool width (0 -> 7) */
+  int snap_recent;    /* SnapKV: last positions always kept (< 0 -> 32) */
 } vc_runtime_desc;
 
 /* Mirrors speckv::CompressedKVMeta (compressor.hpp:56-65).  Quant-uniform:
@@ -283,6 +288,11 @@ int vc_stream_accept(vc_engine* e, int slot, int id, int32_t* emitted, int* n_em
 int vc_stream_abort(vc_engine* e, int id);
 /* HBM bytes of the host tier's staging (rotating slots or the chunk ring). */
 int vc_engine_staging_bytes(vc_engine* e, int64_t* bytes);
+/* Drop-topk introspection (tests): the scores of the last compress for one
+ * (layer, kv head) row (n <= T floats), and the SnapKV observation query of a
+ * layer ([n_q][d_head] bf16, post-RoPE).                                    */
+int vc_drop_scores(vc_engine* e, int layer, int head, float* out, int n);
+int vc_obs_query(vc_engine* e, int layer, uint16_t* out);
 
 /* ---- decode loops ----------------------------------------------------------- */
 /* Full-KV greedy decode of K tokens for each slot (the baseline).

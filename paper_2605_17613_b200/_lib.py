@@ -44,7 +44,8 @@ class RuntimeDesc(C.Structure):
                 ("max_verify", C.c_int), ("use_graphs", C.c_int), ("drop_ratio", C.c_double),
                 ("tp_size", C.c_int), ("tp_rank", C.c_int), ("drop_window", C.c_int),
                 ("resident_slots", C.c_int), ("draft_depth", C.c_int),
-                ("ring_chunks", C.c_int), ("max_streams", C.c_int)]
+                ("ring_chunks", C.c_int), ("max_streams", C.c_int),
+                ("drop_score", C.c_int), ("snap_pool", C.c_int), ("snap_recent", C.c_int)]
 
 
 class CompressedMeta(C.Structure):
@@ -181,6 +182,8 @@ SIGNATURES = {
     "vc_stream_accept": (I, [P, I, I, C.POINTER(C.c_int32), PI]),
     "vc_stream_abort": (I, [P, I]),
     "vc_engine_staging_bytes": (I, [P, C.POINTER(C.c_int64)]),
+    "vc_drop_scores": (I, [P, I, I, PF, I]),
+    "vc_obs_query": (I, [P, I, PU16]),
     "vc_run_decode": (I, [P, PI, I, I, PI32, PD]),
     "vc_run_speculative": (I, [P, PI, I, I, I, PI32, PI32, I, PI, PD]),
     "vc_run_speculative_ngram": (I, [P, PI, I, I, I, I, PI32, PI32, I, PI, PI, PD]),

@@ -96,6 +96,9 @@ int vc_engine_create(const vc_model_desc* model, const vc_runtime_desc* rt, int 
     c.draft_depth = rt->draft_depth > 1 ? rt->draft_depth : 1;
     c.ring_chunks = rt->ring_chunks;
     c.max_streams = rt->max_streams > 0 ? rt->max_streams : 2;
+    c.drop_score = rt->drop_score;
+    c.snap_pool = rt->snap_pool > 0 ? rt->snap_pool : 7;
+    c.snap_recent = rt->snap_recent >= 0 ? rt->snap_recent : 32;
     if (c.drop_window < 0 || (c.drop_window > 0 && c.drop_ratio <= 0.0))
       throw speckv::ConfigError("compressor: drop_window needs the drop-topk compressor");
     c.tp_size = rt->tp_size > 1 ? rt->tp_size : 1;
@@ -638,6 +641,14 @@ int vc_stream_accept(vc_engine* e, int slot, int id, int32_t* emitted, int* n_em
 
 int vc_stream_abort(vc_engine* e, int id) {
   return guard([&] { E(e).stream_end(id); });
+}
+
+int vc_drop_scores(vc_engine* e, int layer, int head, float* out, int n) {
+  return guard([&] { E(e).drop_scores(layer, head, out, n); });
+}
+
+int vc_obs_query(vc_engine* e, int layer, uint16_t* out) {
+  return guard([&] { E(e).obs_query(layer, out); });
 }
 
 int vc_engine_staging_bytes(vc_engine* e, int64_t* bytes) {

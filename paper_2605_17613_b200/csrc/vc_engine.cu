@@ -159,6 +159,10 @@ Engine::Engine(const EngineConfig& cfg, int device) : cfg_(cfg), device_(device)
   if (cfg_.drop_ratio < 0.0 || cfg_.drop_ratio >= 1.0) throw ContractViolation("drop_ratio must be in [0, 1)");
   if (cfg_.drop_ratio > 0.0 && cfg_.quant_bits != 0)
     throw ContractViolation("token-dropping and quantising compressors are exclusive");  // compressor.cpp:245-254
+  if (cfg_.drop_score != 0 && cfg_.drop_score != 1) throw ContractViolation("drop_score must be 0 (key norm) or 1 (SnapKV)");
+  if (cfg_.drop_score == 1 && (cfg_.full_tier != 0 || cfg_.snap_pool < 1 || cfg_.snap_recent < 0 ||
+                               m.n_q / m.n_kv > 8))
+    throw ContractViolation("SnapKV scores need the HBM full tier, snap_pool >= 1, snap_recent >= 0, n_rep <= 8");
   VC_CK(cudaSetDevice(device_));
   VC_CK(cudaStreamCreateWithFlags(&st_, cudaStreamNonBlocking));
   VC_CK(cudaStreamCreateWithFlags(&copy_st_, cudaStreamNonBlocking));
@@ -193,6 +197,7 @@ Engine::~Engine() {
   if (h_ring_) cudaFreeHost(h_ring_);
   void* ptrs[] = {weight_blob_, rope_cos_, rope_sin_, full_.k, full_.v, stage_.k, stage_.v,
                   quant_.rec, quant_.ktail, quant_.vtail, drop_.k, drop_.v, score_buf_, score_w_, kept_buf_,
+                  snap_logits_, snap_ms_, obs_q_, attn_trace_,
                   tp_y_, tp_g_,
                   x_, xn_, qkv_, attn_, act_, gws_.partial, gws_.counters, ss_part_, logits_,
                   tok_in_, tok_out_, part_.o, part_.ml, rows_dev_, seqs_dev_, jobs_dev_};
@@ -384,6 +389,11 @@ void Engine::alloc_all() {
     score_w_ = dmalloc<float>(d);
     std::vector<float> ones(d, 1.0f);  // score = L1 norm of the (post-RoPE) key
     VC_CK(cudaMemcpy(score_w_, ones.data(), d * 4, cudaMemcpyHostToDevice));
+    if (cfg_.drop_score == 1) {
+      snap_logits_ = dmalloc<float>(static_cast<size_t>(m.n_q) * cap);
+      snap_ms_ = dmalloc<float>(static_cast<size_t>(m.n_q) * 2);
+      obs_q_ = dmalloc<uint16_t>(static_cast<size_t>(L) * m.n_q * d);
+    }
   }
   max_chunks_d_ = (cap + VC_DENSE_CHUNK - 1) / VC_DENSE_CHUNK;
   // ---- activations ---------------------------------------------------------
@@ -853,7 +863,35 @@ void Engine::compress_drop(int slot, const KvPool& src, int src_slot, double rat
                           cudaMemcpyHostToDevice, st_));
   } else {
     const uint16_t* keys = src.k + static_cast<size_t>(src_slot) * n_slices * src.cap * m.d;
-    VC_LAUNCH(key_scores(keys, n_slices, T, m.d, static_cast<size_t>(src.cap) * m.d, score_w_, score_buf_, st_));
+    const size_t pitch = static_cast<size_t>(src.cap) * m.d;
+    if (cfg_.drop_score == 1) {
+      // SnapKV: the observation query is the pending token's (the prompt's
+      // last token) -- one decode-shaped forward over the full KV, its q heads
+      // captured per layer; nothing is committed (its K/V row at position T is
+      // rewritten with the same values by the request's first real step)
+      if (T + 1 > full_.cap) throw ContractViolation("compress: no room for the observation row");
+      std::vector<int32_t> out;
+      StepItem it;
+      it.slot = slot;
+      it.mode = RowMode::Decode;
+      it.tokens = {s.pending};
+      capture_q_ = true;
+      try {
+        run_step({it}, out);
+      } catch (...) {
+        capture_q_ = false;
+        throw;
+      }
+      capture_q_ = false;
+      const float sl2 = static_cast<float>(1.4426950408889634 / std::sqrt(static_cast<double>(m.d)));
+      for (int l = 0; l < m.layers; ++l)
+        VC_LAUNCH(snap_scores(keys + static_cast<size_t>(l) * m.n_kv * pitch, pitch, m.n_kv, T, m.d, m.n_q / m.n_kv,
+                              obs_q_ + static_cast<size_t>(l) * m.n_q * m.d, sl2, cfg_.snap_pool, cfg_.snap_recent,
+                              snap_logits_, snap_ms_, score_buf_ + static_cast<size_t>(l) * m.n_kv * T, st_));
+    } else {
+      VC_LAUNCH(key_scores(keys, n_slices, T, m.d, pitch, score_w_, score_buf_, st_));
+    }
+    score_T_ = T;
     VC_LAUNCH(topk_select(score_buf_, n_slices, T, static_cast<int>(k), kept_buf_, st_));
   }
   VC_LAUNCH(gather_kept(src, src_slot, kept_buf_, static_cast<int>(k), drop_, slot, n_slices, m.d, st_));
@@ -865,6 +903,21 @@ void Engine::compress_drop(int slot, const KvPool& src, int src_slot, double rat
   s.draft_len = 0;
   s.drafted.clear();
   VC_CK(cudaStreamSynchronize(st_));
+}
+
+void Engine::drop_scores(int layer, int head, float* out, int n) const {
+  const auto& m = cfg_.model;
+  if (!score_buf_ || layer < 0 || layer >= m.layers || head < 0 || head >= m.n_kv || n > score_T_)
+    throw ContractViolation("drop_scores: no drop-topk compress or row out of range");
+  check_cuda(cudaMemcpy(out, score_buf_ + (static_cast<size_t>(layer) * m.n_kv + head) * score_T_,
+                        static_cast<size_t>(n) * 4, cudaMemcpyDeviceToHost), "drop_scores");
+}
+
+void Engine::obs_query(int layer, uint16_t* out) const {
+  const auto& m = cfg_.model;
+  if (!obs_q_ || layer < 0 || layer >= m.layers) throw ContractViolation("obs_query: no SnapKV engine");
+  check_cuda(cudaMemcpy(out, obs_q_ + static_cast<size_t>(layer) * m.n_q * m.d, static_cast<size_t>(m.n_q) * m.d * 2,
+                        cudaMemcpyDeviceToHost), "obs_query");
 }
 
 size_t Engine::compressed_bytes(int slot) const {
@@ -944,6 +997,15 @@ void Engine::enqueue_forward(int M, int n_draft, int n_dense1, int n_densev, int
     eq.layer = l;
     VC_LAUNCH(gemm(xn_, M, M, H, w_.wqkv[l], qkv_n, eq, gws_, st_));
     trace("qkv", qkv_, static_cast<size_t>(M) * qkv_n * 2);
+    if (capture_q_) {  // SnapKV observation query: row 0's q heads of this layer
+      MappedCopy mc{};
+      mc.seg[0] = {reinterpret_cast<const uint32_t*>(qkv_),
+                   reinterpret_cast<uint32_t*>(obs_q_ + static_cast<size_t>(l) * m.n_q * d), m.n_q * d / 2};
+      mc.n = 1;
+      mapped_copy_kernel<<<4, 256, 0, st_>>>(mc);
+      VC_CK(cudaGetLastError());
+      ++launches_;
+    }
     // the step's attention kernels, then ONE combine over all their partials
     CombineSets cs;
     auto add_set = [&](const AttnSeq* sq, int n, int max_chunks, int mode, int rows) {
@@ -1109,7 +1171,7 @@ void Engine::run_step(const std::vector<StepItem>& items, std::vector<int32_t>& 
   if (cfg_.tp_size > 1 && !coll_) throw ContractViolation("tensor-parallel engine: attach a collective first");
   cudaGraphExec_t exec = nullptr;
   std::string key;
-  if (cfg_.use_graphs && (!coll_ || coll_->graph_capturable())) {  // capture before the timed window opens
+  if (cfg_.use_graphs && !capture_q_ && (!coll_ || coll_->graph_capturable())) {  // capture before the timed window opens
     std::ostringstream ks;
     ks << Mb << ':' << nd << ':' << n1 << ':' << nv << ':' << mrv;
     key = ks.str();

@@ -64,6 +64,14 @@ struct EngineConfig {
   // n_stage whole requests.  n_stage then holds the resident slots only.
   int ring_chunks = 0;
   int max_streams = 2;  // streamed verifies in flight (saved hidden state + exact window rows each)
+  // drop-topk token scores: 0 = L1 norm of the post-RoPE key; 1 = SnapKV
+  // (Li et al., 2024): attention of the observation query (the request's
+  // pending token, one decode-shaped forward over the full KV) summed over the
+  // GQA group, max-pooled over snap_pool positions, the last snap_recent
+  // positions always kept
+  int drop_score = 0;
+  int snap_pool = 7;
+  int snap_recent = 32;
 };
 
 enum class RowMode : int { Decode = 0, Draft = 1, Verify = 2 };
@@ -210,6 +218,10 @@ class Engine {
   bool drop_mode() const { return cfg_.drop_ratio > 0.0; }
   // kept positions (ascending) of the last drop-mode compress, row = layer*n_kv+head
   int last_kept_k() const { return last_kept_k_; }
+  // the drop-topk scores of the last compress (row = layer*n_kv+head, T floats)
+  // and the SnapKV observation query per layer ([n_q][d] bf16, post-RoPE)
+  void drop_scores(int layer, int head, float* out, int n) const;
+  void obs_query(int layer, uint16_t* out) const;
   const int32_t* last_kept_device() const { return kept_buf_; }
   // host-pool rows of an offloaded slot (nullptr for a resident slot)
   // wait for the commits still copying exact rows into the host pool
@@ -297,7 +309,11 @@ class Engine {
   KvPool drop_{};
   DenseMaps drop_maps_{};
   int max_chunks_x_ = 0;
-  float* score_buf_ = nullptr;  // [layers*n_kv][max_ctx] key scores of one compress
+  float* score_buf_ = nullptr;  // [layers*n_kv][T] key scores of the last compress
+  int score_T_ = 0;
+  float *snap_logits_ = nullptr, *snap_ms_ = nullptr;  // SnapKV scratch (one layer)
+  uint16_t* obs_q_ = nullptr;   // [layers][n_q*d] observation query of the last SnapKV compress
+  bool capture_q_ = false;      // enqueue_forward copies row 0's q heads into obs_q_ per layer
   float* score_w_ = nullptr;    // [d] per-channel score weights (ones)
   int32_t* kept_buf_ = nullptr; // [layers*n_kv][k] kept positions of the last compress
   int last_kept_k_ = 0;

@@ -120,6 +120,87 @@ __global__ void __launch_bounds__(kThreads) topk_kernel(const float* scores, int
   }
 }
 
+
+// ---- SnapKV observation-window scores (Li et al., 2024) --------------------
+// logits[h][r][t] = (q_{h*R+r} . k_{h,t}) * scale_log2 over the layer's
+// slices; one thread per key position, the group's queries in shared memory.
+__global__ void snap_logits_kernel(const uint16_t* keys, size_t pitch, int T, int d, int n_rep,
+                                   const uint16_t* q, float scale_log2, float* logits) {
+  extern __shared__ float sq[];  // [n_rep][d]
+  const int h = blockIdx.y;
+  for (int i = threadIdx.x; i < n_rep * d; i += blockDim.x) sq[i] = bf2f(q[static_cast<size_t>(h) * n_rep * d + i]);
+  __syncthreads();
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  const uint4* k = reinterpret_cast<const uint4*>(keys + h * pitch + static_cast<size_t>(t) * d);
+  float acc[8];
+#pragma unroll
+  for (int r = 0; r < 8; ++r) acc[r] = 0.f;
+  for (int c8 = 0; c8 < d / 8; ++c8) {
+    const uint4 w = k[c8];
+    const uint32_t u[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float lo = __uint_as_float(u[j] << 16), hi = __uint_as_float(u[j] & 0xffff0000u);
+      const int c = c8 * 8 + 2 * j;
+#pragma unroll
+      for (int r = 0; r < 8; ++r)
+        if (r < n_rep) acc[r] = __fmaf_rn(hi, sq[r * d + c + 1], __fmaf_rn(lo, sq[r * d + c], acc[r]));
+    }
+  }
+  for (int r = 0; r < n_rep; ++r) logits[(static_cast<size_t>(h) * n_rep + r) * T + t] = acc[r] * scale_log2;
+}
+
+// per (head, rep) row: m = max_t logit, s = sum_t 2^(logit - m)  (fixed block order)
+__global__ void __launch_bounds__(1024) snap_norm_kernel(const float* logits, int T, float* ms) {
+  __shared__ float red[32];
+  const float* row = logits + static_cast<size_t>(blockIdx.x) * T;
+  float m = -INFINITY;
+  for (int t = threadIdx.x; t < T; t += blockDim.x) m = fmaxf(m, row[t]);
+  m = warp_max(m);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = m;
+  __syncthreads();
+  if (threadIdx.x < 32) {
+    float v = threadIdx.x < blockDim.x / 32 ? red[threadIdx.x] : -INFINITY;
+    v = warp_max(v);
+    if (threadIdx.x == 0) red[0] = v;
+  }
+  __syncthreads();
+  m = red[0];
+  __syncthreads();
+  float sum = 0.f;
+  for (int t = threadIdx.x; t < T; t += blockDim.x) sum += exp2f(row[t] - m);
+  sum = warp_sum(sum);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sum;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float v = 0.f;
+    for (int w = 0; w < static_cast<int>(blockDim.x / 32); ++w) v += red[w];
+    ms[blockIdx.x * 2] = m;
+    ms[blockIdx.x * 2 + 1] = v;
+  }
+}
+
+// attention mass of key t summed over the group's queries, max-pooled over
+// [t - pool/2, t + pool/2] (SnapKV's clustering), the last `recent` positions
+// forced in (score +inf)
+__global__ void snap_scores_kernel(const float* logits, const float* ms, int T, int n_rep, int pool, int recent,
+                                   float* scores) {
+  const int h = blockIdx.y;
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= T) return;
+  float best = 0.f;
+  const int lo = max(0, t - pool / 2), hi = min(T - 1, t + pool / 2);
+  for (int j = lo; j <= hi; ++j) {
+    float a = 0.f;
+    for (int r = 0; r < n_rep; ++r) {
+      const int row = h * n_rep + r;
+      a += exp2f(logits[static_cast<size_t>(row) * T + j] - ms[row * 2]) / ms[row * 2 + 1];
+    }
+    best = fmaxf(best, a);
+  }
+  scores[static_cast<size_t>(h) * T + t] = t >= T - recent ? INFINITY : best;
+}
 }  // namespace
 
 cudaError_t key_scores(const uint16_t* keys, int rows, int T, int d, size_t row_pitch, const float* w,
@@ -136,6 +217,17 @@ cudaError_t topk_select(const float* scores, int rows, int T, int k, int32_t* ke
   if (rows <= 0) return cudaSuccess;
   if (k < 1 || k > T) return cudaErrorInvalidValue;
   topk_kernel<<<rows, kThreads, 0, st>>>(scores, T, k, kept);
+  return cudaGetLastError();
+}
+
+cudaError_t snap_scores(const uint16_t* keys, size_t pitch, int n_kv, int T, int d, int n_rep, const uint16_t* q,
+                        float scale_log2, int pool, int recent, float* logits, float* ms, float* scores,
+                        cudaStream_t st) {
+  if (T <= 0 || n_rep > 8) return cudaErrorInvalidValue;
+  snap_logits_kernel<<<dim3((T + 127) / 128, n_kv), 128, static_cast<size_t>(n_rep) * d * 4, st>>>(
+      keys, pitch, T, d, n_rep, q, scale_log2, logits);
+  snap_norm_kernel<<<n_kv * n_rep, 1024, 0, st>>>(logits, T, ms);
+  snap_scores_kernel<<<dim3((T + 255) / 256, n_kv), 256, 0, st>>>(logits, ms, T, n_rep, pool, recent, scores);
   return cudaGetLastError();
 }
 

@@ -103,7 +103,7 @@ class Engine:
     def __init__(self, model: ModelShape, *, max_slots=1, max_ctx=4096, max_x=16, quant_bits=4,
                  full_tier=0, n_stage=2, max_verify=2, use_graphs=True, device=0, drop_ratio=0.0,
                  tp_size=1, tp_rank=0, drop_window=0, resident_slots=0, draft_depth=1,
-                 ring_chunks=0, max_streams=2):
+                 ring_chunks=0, max_streams=2, drop_score="norm", snap_pool=7, snap_recent=32):
         """quant_bits > 0: quant-uniform compressor (KIVI int4/int2);
         drop_ratio in (0, 1): drop-topk compressor keeping llround(c*T) tokens per
         (layer, head) -- the two are exclusive (compressor.cpp:245-254).
@@ -116,7 +116,13 @@ class Engine:
         B_g), the pinned host pool holds the other slots only (B_c).
         ring_chunks > 0 (full_tier 1): reloads stream layer by layer into a ring
         of one-layer chunks and each verify runs range by range as its layers
-        land (stream_*); n_stage then holds only the resident slots."""
+        land (stream_*); n_stage then holds only the resident slots.
+        drop_score (drop-topk): "norm" = L1 norm of the post-RoPE key; "snapkv" =
+        SnapKV observation-window attention (the pending token's query over the
+        full KV, summed over the GQA group, max-pooled over snap_pool positions,
+        the last snap_recent positions always kept)."""
+        if drop_score not in ("norm", "snapkv"):
+            raise ValueError("drop_score is 'norm' or 'snapkv'")
         self.lib = _lib.load()
         self.model = model
         self.max_x = max_x
@@ -125,7 +131,8 @@ class Engine:
         rt = _lib.RuntimeDesc(max_slots, max_ctx, max_x, quant_bits, full_tier, n_stage,
                               max_verify, int(use_graphs), float(drop_ratio), int(tp_size), int(tp_rank),
                               int(drop_window), int(resident_slots), int(draft_depth),
-                              int(ring_chunks), int(max_streams))
+                              int(ring_chunks), int(max_streams), 1 if drop_score == "snapkv" else 0,
+                              int(snap_pool), int(snap_recent))
         self.tp_size, self.tp_rank = int(tp_size), int(tp_rank)
         h = C.c_void_p()
         check(self.lib.vc_engine_create(C.byref(md), C.byref(rt), device, C.byref(h)))
@@ -242,6 +249,18 @@ class Engine:
         m = _lib.CompressedMeta()
         check(self.lib.vc_compress_spec(self.h, slot, C.byref(cs), float(ratio), seed, C.byref(m)))
         return {f: getattr(m, f) for f, _ in m._fields_}
+
+    def drop_scores(self, layer, head, n):
+        """Scores of the last drop-topk compress for one (layer, kv head): n floats."""
+        out = np.zeros(n, np.float32)
+        check(self.lib.vc_drop_scores(self.h, layer, head, _ptr(out, C.c_float), n))
+        return out
+
+    def obs_query(self, layer):
+        """SnapKV observation query of a layer: [n_q][d_head] bf16 bits (post-RoPE)."""
+        out = np.zeros((self.model.n_q, self.model.d_head), np.uint16)
+        check(self.lib.vc_obs_query(self.h, layer, _ptr(out, C.c_uint16)))
+        return out
 
     def drop_kept(self, layer, head):
         """Kept positions (ascending) of one (layer, head) from the last drop-topk compress."""
