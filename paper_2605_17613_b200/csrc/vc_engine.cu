@@ -993,9 +993,31 @@ void Engine::enqueue_forward(int M, int n_draft, int n_dense1, int n_densev, int
   trace("embed.x", x_, static_cast<size_t>(M) * H * 4);
   trace("w.gu0", w_.wgu[0], static_cast<size_t>(2) * F * H * 2);
   trace("w.qkv0", w_.wqkv[0], static_cast<size_t>(qkv_n) * H * 2);
+  // RMSNorm fused into the projection that consumes it (GemmNormIn): the qkv
+  // GEMM of layers >= 1 and every gate/up GEMM build their bf16 activation
+  // tiles from the residual stream and its per-tile sums of squares (bit-
+  // identical to rms_apply; 2 fewer launches per layer).  VC_FUSE_NORM=0
+  // restores the separate rms_apply launches.
+  static const bool fuse_norm = [] {
+    const char* v = std::getenv("VC_FUSE_NORM");
+    return !(v && v[0] == '0');
+  }();
+  auto norm_in = [&](const uint16_t* w) {
+    GemmNormIn n;
+    n.x = x_;
+    n.ss = ss_part_;
+    n.w = w;
+    n.eps = m.eps;
+    return n;
+  };
   for (int l = 0; l < L; ++l) {
     eq.layer = l;
-    VC_LAUNCH(gemm(xn_, M, M, H, w_.wqkv[l], qkv_n, eq, gws_, st_));
+    if (fuse_norm && l > 0) {
+      const GemmNormIn nq = norm_in(w_.attn_norm[l]);
+      VC_LAUNCH(gemm(nullptr, M, M, H, w_.wqkv[l], qkv_n, eq, gws_, st_, &nq));
+    } else {
+      VC_LAUNCH(gemm(xn_, M, M, H, w_.wqkv[l], qkv_n, eq, gws_, st_));
+    }
     trace("qkv", qkv_, static_cast<size_t>(M) * qkv_n * 2);
     if (capture_q_) {  // SnapKV observation query: row 0's q heads of this layer
       MappedCopy mc{};
@@ -1045,7 +1067,7 @@ void Engine::enqueue_forward(int M, int n_draft, int n_dense1, int n_densev, int
     // then the next RMSNorm.  (r1: fusing the RMSNorm into the residual
     // epilogue -- tile finishers spin until every tile's ss_part is in -- was
     // bit-identical but 3% slower per step than this launch.)
-    auto residual_gemm = [&](const uint16_t* Xt, int Kd, const uint16_t* Wt, const uint16_t* norm_w) {
+    auto residual_gemm = [&](const uint16_t* Xt, int Kd, const uint16_t* Wt, const uint16_t* norm_w, bool norm_next) {
       if (!coll_) {
         VC_LAUNCH(gemm(Xt, M, M, Kd, Wt, H, er, gws_, st_));
       } else {
@@ -1056,16 +1078,21 @@ void Engine::enqueue_forward(int M, int n_draft, int n_dense1, int n_densev, int
         coll_->all_gather(tp_y_, tp_g_, static_cast<size_t>(M) * H, st_);
         VC_LAUNCH(tp_residual(x_, tp_g_, cfg_.tp_size, M, H, ss_part_, st_));
       }
-      if (!(skip & 2)) VC_LAUNCH(rms_apply(x_, ss_part_, M, M, H, norm_w, m.eps, xn_, st_));
+      if (!(skip & 2) && norm_next) VC_LAUNCH(rms_apply(x_, ss_part_, M, M, H, norm_w, m.eps, xn_, st_));
     };
-    residual_gemm(attn_, m.n_q * d, w_.wo[l], w_.mlp_norm[l]);
+    residual_gemm(attn_, m.n_q * d, w_.wo[l], w_.mlp_norm[l], !fuse_norm);
     trace("attn", attn_, static_cast<size_t>(M) * m.n_q * d * 2);
     trace("x.o", x_, static_cast<size_t>(M) * H * 4);
     trace("ss.o", ss_part_, static_cast<size_t>(M) * (H / 128) * 4);
     trace("xn.o", xn_, static_cast<size_t>(M) * H * 2);
-    VC_LAUNCH(gemm(xn_, M, M, H, w_.wgu[l], 2 * F, es, gws_, st_));
+    if (fuse_norm) {
+      const GemmNormIn ng = norm_in(w_.mlp_norm[l]);
+      VC_LAUNCH(gemm(nullptr, M, M, H, w_.wgu[l], 2 * F, es, gws_, st_, &ng));
+    } else {
+      VC_LAUNCH(gemm(xn_, M, M, H, w_.wgu[l], 2 * F, es, gws_, st_));
+    }
     trace("act", act_, static_cast<size_t>(M) * F * 2);
-    residual_gemm(act_, F, w_.wd[l], l + 1 < L ? w_.attn_norm[l + 1] : w_.final_norm);
+    residual_gemm(act_, F, w_.wd[l], l + 1 < L ? w_.attn_norm[l + 1] : w_.final_norm, !fuse_norm || l + 1 == L);
     trace("x.d", x_, static_cast<size_t>(M) * H * 4);
   }
   VC_LAUNCH(gemm(xn_, M, M, H, w_.lm_head, V, ef, gws_, st_));

@@ -441,7 +441,7 @@ gemm_umma_kernel(const uint16_t* __restrict__ Xt, int Mp, int M, int K,
 template <int NT, Epi E>
 __global__ void __launch_bounds__(kThreads, kCtasPerSm)
 gemm_cluster_kernel(const uint16_t* __restrict__ Xt, int Mp, int M, int K,
-                    const uint16_t* __restrict__ Wt, int N, int m0, GemmEpilogue ep, int S) {
+                    const uint16_t* __restrict__ Wt, int N, int m0, GemmEpilogue ep, int S, GemmNormIn nin) {
   constexpr int ST = Cfg<NT>::kStages;
   constexpr int WB = Cfg<NT>::kW, XB = Cfg<NT>::kX;
   constexpr uint32_t kAccCols = NT < 32 ? 32 : NT;
@@ -455,15 +455,17 @@ gemm_cluster_kernel(const uint16_t* __restrict__ Xt, int Mp, int M, int K,
   float* sAcc = reinterpret_cast<float*>(smem);                 // [NT][128] parked partial (reuses the stages)
   __shared__ __align__(8) uint64_t full[ST], empty[ST], acc_full;
   __shared__ uint32_t tmem_base_sh;
+  __shared__ float sR[NT];  // fused RMSNorm: per-row scale
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int KT = K / kBK;
   const int rank = static_cast<int>(cluster_rank());
   const int tile = blockIdx.x / S;
   const int k_lo = rank * KT / S, k_hi = (rank + 1) * KT / S;
   const int nk = k_hi - k_lo;
+  const bool fused = nin.x != nullptr;  // the 8 epilogue warps write the X half of every stage
   if (tid == 0) {
     for (int s2 = 0; s2 < ST; ++s2) {
-      mbar_init(&full[s2], 1);
+      mbar_init(&full[s2], fused ? 9 : 1);
       mbar_init(&empty[s2], 1);
     }
     mbar_init(&acc_full, 1);
@@ -479,19 +481,21 @@ gemm_cluster_kernel(const uint16_t* __restrict__ Xt, int Mp, int M, int K,
   if (warp == 0) {  // ---- TMA producer
     if (lane == 0) {
       const int pre = min(ST, nk);
+      const uint32_t tx = fused ? WB : WB + XB;
       for (int i = 0; i < pre; ++i) {  // weights do not depend on the previous kernel
-        mbar_expect_tx(&full[i], WB + XB);
+        mbar_expect_tx(&full[i], tx);
         tma_load_1d(sW + i * WB, Wt + (static_cast<size_t>(tile) * KT + k_lo + i) * 8192, WB, &full[i]);
       }
       pdl_wait();
-      for (int i = 0; i < pre; ++i)
-        tma_load_1d(sX + i * XB, Xt + (static_cast<size_t>(k_lo + i) * Mp + m0) * 64, XB, &full[i]);
+      if (!fused)
+        for (int i = 0; i < pre; ++i)
+          tma_load_1d(sX + i * XB, Xt + (static_cast<size_t>(k_lo + i) * Mp + m0) * 64, XB, &full[i]);
       for (int i = pre; i < nk; ++i) {
         const int st = i % ST;
         mbar_wait(&empty[st], ((i / ST) - 1) & 1);
-        mbar_expect_tx(&full[st], WB + XB);
+        mbar_expect_tx(&full[st], tx);
         tma_load_1d(sW + st * WB, Wt + (static_cast<size_t>(tile) * KT + k_lo + i) * 8192, WB, &full[st]);
-        tma_load_1d(sX + st * XB, Xt + (static_cast<size_t>(k_lo + i) * Mp + m0) * 64, XB, &full[st]);
+        if (!fused) tma_load_1d(sX + st * XB, Xt + (static_cast<size_t>(k_lo + i) * Mp + m0) * 64, XB, &full[st]);
       }
     }
   } else if (warp == 1) {  // ---- MMA issuer
@@ -513,6 +517,89 @@ gemm_cluster_kernel(const uint16_t* __restrict__ Xt, int Mp, int M, int K,
   } else {  // ---- park the partial: TMEM -> sAcc[token][feature]
     pdl_wait();  // the epilogue writes buffers the previous kernel may read
     const int et = tid - 64;
+    if (fused) {
+      // ---- fused RMSNorm: the activation half of every stage, in the
+      // swizzled layout a bulk copy of rms_apply's tiled output would land
+      const int H = K;
+      const int tiles = H / kBN;
+      if (et < NT) {
+        const int m = m0 + et;
+        float r = 0.f;
+        if (m < M) {
+          const float* sp = nin.ss + static_cast<size_t>(m) * tiles;
+          float sum = 0.f;
+          for (int t = 0; t < tiles; ++t) sum += sp[t];
+          r = rsqrtf(sum / H + nin.eps);
+        }
+        sR[et] = r;
+      }
+      named_bar(1, 256);
+      // register pipeline: the x / w loads of stage i + kPF are in flight
+      // while stage i is converted and stored (a stage's loads alone are an
+      // L2 round trip, which would otherwise pace every stage)
+      constexpr int kCPT = NT * 8 / 256 > 0 ? NT * 8 / 256 : 1;  // 16-B chunks per thread per stage
+      constexpr int kPF = kCPT >= 4 ? 1 : (kCPT == 2 ? 2 : 4);   // stages in flight
+      struct Chunk {
+        float4 a, b;
+        uint4 w;
+      };
+      Chunk buf[kPF][kCPT];
+      auto load = [&](int i, Chunk* c) {
+        const int k0 = (k_lo + i) * kBK;
+#pragma unroll
+        for (int j = 0; j < kCPT; ++j) {
+          const int e = et + j * 256;
+          const int r = e >> 3, cc = e & 7;
+          const int m = m0 + r;
+          if (e < NT * 8 && m < M) {
+            const float4* xp = reinterpret_cast<const float4*>(nin.x + static_cast<size_t>(m) * H + k0 + cc * 8);
+            c[j].a = xp[0];
+            c[j].b = xp[1];
+            c[j].w = *reinterpret_cast<const uint4*>(nin.w + k0 + cc * 8);
+          }
+        }
+      };
+#pragma unroll
+      for (int p = 0; p < kPF; ++p)
+        if (p < nk) load(p, buf[p]);
+      for (int i0 = 0; i0 < nk; i0 += kPF) {
+#pragma unroll
+      for (int p = 0; p < kPF; ++p) {
+        const int i = i0 + p;
+        if (i >= nk) break;
+        const int st = i % ST;
+        if (i >= ST) mbar_wait(&empty[st], ((i / ST) - 1) & 1);
+        uint8_t* dst = sX + st * XB;
+        Chunk* c = buf[p];
+#pragma unroll
+        for (int j = 0; j < kCPT; ++j) {
+          const int e = et + j * 256;
+          if (e >= NT * 8) continue;
+          const int r = e >> 3, cc = e & 7;
+          uint4 o = make_uint4(0u, 0u, 0u, 0u);
+          if (m0 + r < M) {
+            const float rs = sR[r];
+            const float xv[8] = {c[j].a.x, c[j].a.y, c[j].a.z, c[j].a.w, c[j].b.x, c[j].b.y, c[j].b.z, c[j].b.w};
+            const uint32_t ww[4] = {c[j].w.x, c[j].w.y, c[j].w.z, c[j].w.w};
+            uint32_t pk[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const float w0 = __uint_as_float(ww[q] << 16), w1 = __uint_as_float(ww[q] & 0xffff0000u);
+              const uint32_t lo = f2bf(__fmul_rn(__fmul_rn(xv[2 * q], rs), w0));
+              const uint32_t hi = f2bf(__fmul_rn(__fmul_rn(xv[2 * q + 1], rs), w1));
+              pk[q] = lo | (hi << 16);
+            }
+            o = make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          }
+          *reinterpret_cast<uint4*>(dst + r * 128 + ((cc ^ (r & 7)) << 4)) = o;
+        }
+        if (i + kPF < nk) load(i + kPF, c);
+        fence_proxy_async();  // generic-proxy stores -> the tensor core's async-proxy reads
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&full[st]);
+      }
+      }
+    }
     const int quarter = warp & 3;
     const int feat = quarter * 32 + lane;
     const int tok0 = et >= 128 ? kHalf : 0;
@@ -561,8 +648,10 @@ gemm_cluster_kernel(const uint16_t* __restrict__ Xt, int Mp, int M, int K,
   if (warp == 1) tmem_dealloc(tbase, kAccCols);
 }
 
-// Cluster size for (N, K): S = min(5, stream-K contributors per tile, k-tiles);
-// below 3 the stream-K path (gate/up, LM head).  r2 sweep of a uniform S on
+// Cluster size for (N, K): S = min(5, stream-K contributors per tile, k-tiles),
+// S = 1 for wide weights (gate/up, LM head: one CTA per 128-feature tile, no
+// split; r2: mixed step 8.18 -> 8.01 ms vs their stream-K).  Below
+// VC_GEMM_CLUSTER_MIN (default 1) the stream-K kernel runs instead.  r2 sweep of a uniform S on
 // the mixed x=6 step (in-graph ms): stream-K 8.62, S=3 8.30, 4 8.13, 5 8.06,
 // 6 8.26, 8 8.49; S = round(148 / tiles) per shape (qkv 3, o/down 5) 8.11.
 // VC_GEMM_CLUSTER=n sets the cap (1 = stream-K everywhere).
@@ -571,12 +660,17 @@ int cluster_splits(int N, int K) {
     const char* v = std::getenv("VC_GEMM_CLUSTER");
     return v && std::atoi(v) > 0 ? std::atoi(v) : 5;
   }();
+  static const int min_s = [] {
+    const char* v = std::getenv("VC_GEMM_CLUSTER_MIN");
+    return v && std::atoi(v) > 0 ? std::atoi(v) : 1;
+  }();
   const int tiles = N / kBN, KT = K / kBK;
   int S = kP / tiles;
   if (S > cap) S = cap;
   if (S > 8) S = 8;
   if (S > KT) S = KT;
-  return S >= 3 ? S : 1;
+  if (S < 1) S = 1;
+  return S >= min_s ? S : 0;
 }
 
 int max_contributors(int N, int K) {
@@ -591,9 +685,11 @@ int max_contributors(int N, int K) {
 
 template <int NT, Epi E>
 cudaError_t launch_nt(const uint16_t* Xt, int Mp, int M, int K, const uint16_t* Wt, int N,
-                      const GemmEpilogue& ep, const GemmWorkspace& ws, cudaStream_t st) {
-  const int S = cluster_splits(N, K);
-  if (S > 1) {
+                      const GemmEpilogue& ep, const GemmWorkspace& ws, cudaStream_t st, const GemmNormIn* norm) {
+  int S = cluster_splits(N, K);
+  if (norm && S < 1) S = std::max(1, std::min(kP / (N / kBN), 8));  // the fused input needs the cluster kernel
+  const GemmNormIn nin = norm ? *norm : GemmNormIn{};
+  if (S >= 1) {
     auto kc = gemm_cluster_kernel<NT, E>;
     const int smem = Cfg<NT>::kSmem;
     cudaError_t e = cudaFuncSetAttribute(kc, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
@@ -601,7 +697,7 @@ cudaError_t launch_nt(const uint16_t* Xt, int Mp, int M, int K, const uint16_t* 
     const unsigned grid = static_cast<unsigned>((N / kBN) * S);
     for (int m0 = 0; m0 < M; m0 += NT) {
       e = launch_pdl_cluster(kc, dim3(grid), dim3(kThreads), smem, st, static_cast<unsigned>(S), Xt, Mp, M, K, Wt,
-                             N, m0, ep, S);
+                             N, m0, ep, S, nin);
       if (e != cudaSuccess) return e;
     }
     return cudaSuccess;
@@ -623,11 +719,11 @@ cudaError_t launch_nt(const uint16_t* Xt, int Mp, int M, int K, const uint16_t* 
 
 template <Epi E>
 cudaError_t launch_e(const uint16_t* Xt, int Mp, int M, int K, const uint16_t* Wt, int N,
-                     const GemmEpilogue& ep, const GemmWorkspace& ws, cudaStream_t st) {
-  if (M <= 16) return launch_nt<16, E>(Xt, Mp, M, K, Wt, N, ep, ws, st);
-  if (M <= 32) return launch_nt<32, E>(Xt, Mp, M, K, Wt, N, ep, ws, st);
-  if (M <= 64) return launch_nt<64, E>(Xt, Mp, M, K, Wt, N, ep, ws, st);
-  return launch_nt<128, E>(Xt, Mp, M, K, Wt, N, ep, ws, st);
+                     const GemmEpilogue& ep, const GemmWorkspace& ws, cudaStream_t st, const GemmNormIn* norm) {
+  if (M <= 16) return launch_nt<16, E>(Xt, Mp, M, K, Wt, N, ep, ws, st, norm);
+  if (M <= 32) return launch_nt<32, E>(Xt, Mp, M, K, Wt, N, ep, ws, st, norm);
+  if (M <= 64) return launch_nt<64, E>(Xt, Mp, M, K, Wt, N, ep, ws, st, norm);
+  return launch_nt<128, E>(Xt, Mp, M, K, Wt, N, ep, ws, st, norm);
 }
 
 __global__ void retile_weight_kernel(const uint16_t* src, int N, int K, uint16_t* dst) {
@@ -660,14 +756,15 @@ size_t gemm_partial_floats(int M, int N, int K) {
 int gemm_tiles(int, int N) { return N / kBN; }
 
 cudaError_t gemm(const uint16_t* Xt, int Mp, int M, int K, const uint16_t* Wt, int N,
-                 const GemmEpilogue& ep, const GemmWorkspace& ws, cudaStream_t st) {
+                 const GemmEpilogue& ep, const GemmWorkspace& ws, cudaStream_t st, const GemmNormIn* norm) {
   if (M <= 0) return cudaSuccess;
   if (N % kBN != 0 || K % kBK != 0 || Mp < M) return cudaErrorInvalidValue;
+  if (norm && (!norm->x || !norm->ss || !norm->w)) return cudaErrorInvalidValue;
   switch (ep.kind) {
-    case Epi::StoreF32: return launch_e<Epi::StoreF32>(Xt, Mp, M, K, Wt, N, ep, ws, st);
-    case Epi::Residual: return launch_e<Epi::Residual>(Xt, Mp, M, K, Wt, N, ep, ws, st);
-    case Epi::Qkv: return launch_e<Epi::Qkv>(Xt, Mp, M, K, Wt, N, ep, ws, st);
-    case Epi::Silu: return launch_e<Epi::Silu>(Xt, Mp, M, K, Wt, N, ep, ws, st);
+    case Epi::StoreF32: return launch_e<Epi::StoreF32>(Xt, Mp, M, K, Wt, N, ep, ws, st, norm);
+    case Epi::Residual: return launch_e<Epi::Residual>(Xt, Mp, M, K, Wt, N, ep, ws, st, norm);
+    case Epi::Qkv: return launch_e<Epi::Qkv>(Xt, Mp, M, K, Wt, N, ep, ws, st, norm);
+    case Epi::Silu: return launch_e<Epi::Silu>(Xt, Mp, M, K, Wt, N, ep, ws, st, norm);
   }
   return cudaErrorInvalidValue;
 }

@@ -42,6 +42,17 @@ struct GemmEpilogue {
   int ring_n = 1;
 };
 
+// Fused RMSNorm input (x != nullptr): the GEMM's activation tiles are
+// produced in shared memory as bf16(x[m][k] * r_m * w[k]) with
+// r_m = rsqrt(sum_t ss[m][t] / H + eps) -- exactly rms_apply's arithmetic, so
+// the result is bit-identical to rms_apply followed by the plain GEMM.
+struct GemmNormIn {
+  const float* x = nullptr;     // [Mp][H] fp32 residual stream
+  const float* ss = nullptr;    // [Mp][H/128] per-tile sums of squares
+  const uint16_t* w = nullptr;  // [H] bf16 norm weight
+  float eps = 0.f;
+};
+
 struct GemmWorkspace {
   float* partial = nullptr;   // split partials, fragment order
   int* counters = nullptr;    // one per output tile, self-resetting
@@ -57,7 +68,8 @@ int gemm_tiles(int M, int N);
 // layout with Mp padded rows; Wt: weights in the tiled layout (vc_tiled.cuh).
 // N must be a multiple of 128, K of 64.
 cudaError_t gemm(const uint16_t* Xt, int Mp, int M, int K, const uint16_t* Wt, int N,
-                 const GemmEpilogue& epi, const GemmWorkspace& ws, cudaStream_t st);
+                 const GemmEpilogue& epi, const GemmWorkspace& ws, cudaStream_t st,
+                 const GemmNormIn* norm = nullptr);
 // Logical row-major -> tiled layouts (weights at load time, probes).
 cudaError_t retile_weight(const uint16_t* src, int N, int K, uint16_t* dst, cudaStream_t st);
 cudaError_t retile_act(const uint16_t* src, int M, int K, int Mp, uint16_t* dst, cudaStream_t st);

@@ -2,6 +2,8 @@
 batch-invariant -- a row's result is bit-identical for any number of rows
 in the batch (the property the losslessness invariant rests on).
 Tolerance: bf16 inputs, fp32 accumulate: |y - y64| <= 1e-3 * sqrt(K) * rms(y64) + 1e-5."""
+import os
+
 import numpy as np
 import pytest
 
@@ -50,3 +52,41 @@ def test_gemm_batch_invariance(cuda, N, K):
         np.testing.assert_array_equal(sub, full[:m])
     # a row in the middle of a batch == the same row alone
     np.testing.assert_array_equal(_gemm(cuda, X[150:151].copy(), W)[0], full[150])
+
+
+_FUSE_SCRIPT = r"""
+import hashlib, sys
+sys.path.insert(0, %r); sys.path.insert(0, %r)
+import os
+
+import numpy as np
+import vc_testlib as T
+from paper_2605_17613_b200 import TINY, Engine
+w = T.tiny_weights(TINY, seed=7, std=0.02)
+e = Engine(TINY, max_slots=4, max_ctx=1200, max_x=16, quant_bits=4)
+e.load_weights(w)
+h = hashlib.sha256()
+for s in range(4):
+    e.add_synthetic(s, 700 + 50 * s, 17 + s, seed=1 + s)
+for rows in (1, 9):  # one decode row per request (M=4) and verify windows (M=40)
+    items = [(s, 2 if rows > 1 else 0, [17 + s + i for i in range(rows)], -1) for s in range(4)]
+    out, logits = e.step(items, want_logits=True)
+    h.update(logits.tobytes()); h.update(out.tobytes())
+print(h.hexdigest())
+"""
+
+
+@pytest.mark.gpu
+def test_fused_rmsnorm_gemm_is_bit_identical(cuda):
+    """GemmNormIn (RMSNorm fused into the qkv and gate/up GEMMs) gives the
+    same logits, bit for bit, as the separate rms_apply launches."""
+    import subprocess
+    import sys
+    code = _FUSE_SCRIPT % (T.ROOT, os.path.join(T.ROOT, "tests"))
+    digests = []
+    for fuse in ("0", "1"):
+        env = dict(os.environ, VC_FUSE_NORM=fuse)
+        r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300)
+        assert r.returncode == 0, r.stderr[-2000:]
+        digests.append(r.stdout.strip().splitlines()[-1])
+    assert digests[0] == digests[1]
