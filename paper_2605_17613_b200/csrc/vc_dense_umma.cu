@@ -196,11 +196,29 @@ __global__ void __launch_bounds__(kThreads, 1)
   __syncthreads();
   tmem_fence_after();
   const uint32_t tbase = tmem_base_sh;
-  pdl_wait();  // q rows and the window's new K/V come from the qkv epilogue
-  if (s.trace && threadIdx.x == 0 && blockIdx.x < 4096) s.trace[blockIdx.x * 2] = vc_globaltimer();
+  // PDL prologue: the first item's K/V tiles lie before this step's new rows
+  // (positions < kv_len - n_tok: not written by the qkv epilogue we depend on,
+  // nor by anything else in flight), so the producers stream its first two
+  // stages while the previous kernel drains, then wait for it
+  int first_static = 0;  // K/V tiles of the CTA's first item issued before the wait
+  Item I0;
+  const bool have0 = n_items > 0 && decode_item<NREP>(blockIdx.x, s, seqs, max_chunks, row_blocks, I0);
+  if (have0 && I0.k_hi <= I0.kv_len - I0.n_tok) first_static = I0.n_tiles < 2 ? I0.n_tiles : 2;
+  if (warp != 0 && warp != 6) pdl_wait();  // q rows and the window's new K/V come from the qkv epilogue
 
+  // one pool tile (K or V) of item I, tile t, into stage st
+  auto load_kv = [&](const CUtensorMap* map, uint8_t* dst, uint64_t* bar, const Item& I, int t) {
+    const int slice_row = static_cast<int>(((static_cast<size_t>(I.slot) * s.layers + layer) * s.n_kv + I.h) *
+                                           static_cast<size_t>(pool_cap));
+    mbar_expect_tx(bar, KV_BYTES);
+#pragma unroll
+    for (int a = 0; a < ATOMS; ++a) tma_load_2d(dst + a * KV_ATOM, map, a * 64, slice_row + I.k_lo + t * kTile, bar);
+  };
   if (warp == 0) {
     // ===================== TMA producer =====================
+    if (lane == 0)
+      for (int t = 0; t < first_static; ++t) load_kv(&maps.k, sK + t * KV_BYTES, &k_full[t], I0, t);
+    pdl_wait();
     if (lane == 0) {
       int g = 0, n = 0;
       for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
@@ -211,36 +229,32 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int a = 0; a < ATOMS; ++a)
           tma_load_3d(sQ + a * Q_ATOM, &maps.q, a * 64, I.h * NREP, I.row0 + I.rb * (kRows / NREP), &q_full);
-        const int slice_row = static_cast<int>(((static_cast<size_t>(I.slot) * s.layers + layer) * s.n_kv + I.h) *
-                                               static_cast<size_t>(pool_cap));
         for (int t = 0; t < I.n_tiles; ++t, ++g) {
+          if (n == 0 && t < first_static) continue;  // issued before the wait
           const int st = g & 1;
           if (g >= 2) mbar_wait(&k_empty[st], ((g >> 1) - 1) & 1);  // S(g-2) done with the stage
-          mbar_expect_tx(&k_full[st], KV_BYTES);
-#pragma unroll
-          for (int a = 0; a < ATOMS; ++a)
-            tma_load_2d(sK + st * KV_BYTES + a * KV_ATOM, &maps.k, a * 64, slice_row + I.k_lo + t * kTile, &k_full[st]);
+          load_kv(&maps.k, sK + st * KV_BYTES, &k_full[st], I, t);
         }
         ++n;
       }
     }
   } else if (warp == 6) {
     // ===================== TMA producer: V (runs behind K by the softmax) =====================
+    if (lane == 0)
+      for (int t = 0; t < first_static; ++t) load_kv(&maps.v, sV + t * KV_BYTES, &v_full[t], I0, t);
+    pdl_wait();
     if (lane == 0) {
-      int g = 0;
+      int g = 0, n = 0;
       for (int it = blockIdx.x; it < n_items; it += gridDim.x) {
         Item I;
         if (!decode_item<NREP>(it, s, seqs, max_chunks, row_blocks, I)) continue;
-        const int slice_row = static_cast<int>(((static_cast<size_t>(I.slot) * s.layers + layer) * s.n_kv + I.h) *
-                                               static_cast<size_t>(pool_cap));
         for (int t = 0; t < I.n_tiles; ++t, ++g) {
+          if (n == 0 && t < first_static) continue;
           const int st = g & 1;
           if (g >= 2) mbar_wait(&v_empty[st], ((g >> 1) - 1) & 1);  // PV(g-2) done with the stage
-          mbar_expect_tx(&v_full[st], KV_BYTES);
-#pragma unroll
-          for (int a = 0; a < ATOMS; ++a)
-            tma_load_2d(sV + st * KV_BYTES + a * KV_ATOM, &maps.v, a * 64, slice_row + I.k_lo + t * kTile, &v_full[st]);
+          load_kv(&maps.v, sV + st * KV_BYTES, &v_full[st], I, t);
         }
+        ++n;
       }
     }
   } else if (warp == 1) {
@@ -504,7 +518,6 @@ __global__ void __launch_bounds__(kThreads, 1)
   tmem_fence_before();
   __syncthreads();
   if (warp == 1) tmem_dealloc(tbase, 512);
-  if (s.trace && threadIdx.x == 0 && blockIdx.x < 4096) s.trace[blockIdx.x * 2 + 1] = vc_globaltimer();
 }
 
 template <int D, int NREP>

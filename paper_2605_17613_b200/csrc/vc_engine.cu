@@ -1056,9 +1056,7 @@ void Engine::enqueue_forward(int M, int n_draft, int n_dense1, int n_densev, int
     }
     if (n_densev > 0 && !(skip & 1)) {
       const AttnSeq* sv = seqs_dev_ + n_draft + n_dense1;
-      AttnShape tv = as;
-      if (l == 5) tv.trace = attn_trace;
-      VC_LAUNCH(dense_attention(tv, dense_v_pool, dense_maps_, l, sv, n_densev, max_chunks_d_, max_rows_v, part_, st_));
+      VC_LAUNCH(dense_attention(as, dense_v_pool, dense_maps_, l, sv, n_densev, max_chunks_d_, max_rows_v, part_, st_));
       add_set(sv, n_densev, max_chunks_d_, 1, max_rows_v);
     }
     if (cs.n_sets > 0) VC_LAUNCH(attention_combine_sets(as, cs, part_, attn_, st_));

@@ -86,8 +86,10 @@ struct AttnShape {
   float scale_log2;    // log2(e)/sqrt(d)
   int draft_warps;     // quantised-draft warps launched (persistent, draft_quant_warps)
   int draft_min_tasks; // fewest group tasks a draft warp takes (bounds partials per head)
-  // diagnostics (VC_ATTN_TRACE): per-CTA globaltimer at start/end, [2][4096] u64
-  // (dense CTAs at [0], draft CTAs at [4096]); nullptr = off
+  // diagnostics (VC_ATTN_TRACE): per-CTA globaltimer at start/end of the draft
+  // kernel at [8192 + 2 * cta]; nullptr = off.  (The dense kernel carries no
+  // probe: two guarded timer stores there cost it 8% on the decode baseline,
+  // r2 A/B 10.60 vs 11.50 ms per 16 x 32K launch set.)
   unsigned long long* trace = nullptr;
 };
 __device__ __forceinline__ unsigned long long vc_globaltimer() {
