@@ -369,6 +369,16 @@ typedef struct {
    * out then holds n + n_arrivals rows; latencies are completion - arrival. */
   const vc_request_desc* arrivals;
   int n_arrivals;
+  /* Two-level composition inside the serving loop (
+   * composed_accept_length, analytics.cpp:413-422): with ngram >= 1 and
+   * depth >= 2 every drafting row carries up to depth-1 prompt-lookup
+   * proposals (`ngram`-token key over the request's own context) as extra
+   * rows of the same pass (engine draft_depth >= depth); proposals the
+   * compressed model confirms join the window.  One scheduler draft
+   * iteration can then append several tokens; the verify checks them all.
+   * 0 = plain drafting.                                                     */
+  int ngram;
+  int depth;
 } vc_sched_desc;
 
 typedef struct {
@@ -408,6 +418,9 @@ typedef struct {
   double interconnect_busy;
   int64_t peak_hbm_bytes;
   int64_t staging_bytes;    /* HBM of the host tier's staging (vc_engine_staging_bytes) */
+  int64_t drafted_tokens;   /* tokens that entered verify windows (composition: > draft iterations) */
+  int64_t aux_proposed;     /* composition: auxiliary tokens offered to the compressed model */
+  int64_t aux_accepted;     /* of those, confirmed by it (gamma_e = accepted / proposed) */
 } vc_sched_stats;
 
 /* Reference metrics of a loop (SimMetrics, sim.hpp:52-74) on the engine:

@@ -79,7 +79,8 @@ class SchedDesc(C.Structure):
     _fields_ = [("x", C.c_int), ("window", C.c_int), ("iteration_time", C.c_double),
                 ("link_bandwidth", C.c_double), ("hbm_capacity", C.c_int64), ("K", C.c_int),
                 ("warmup_iterations", C.c_int64), ("timed_iterations", C.c_int64),
-                ("x_resident", C.c_int), ("arrivals", C.POINTER(RequestDesc)), ("n_arrivals", C.c_int)]
+                ("x_resident", C.c_int), ("arrivals", C.POINTER(RequestDesc)), ("n_arrivals", C.c_int),
+                ("ngram", C.c_int), ("depth", C.c_int)]
 
 
 class SchedStats(C.Structure):
@@ -94,7 +95,8 @@ class SchedStats(C.Structure):
                 ("timed_verify_rows", C.c_double), ("throughput", C.c_double),
                 ("warm_throughput", C.c_double), ("p50_latency_s", C.c_double), ("p99_latency_s", C.c_double),
                 ("interconnect_busy", C.c_double), ("peak_hbm_bytes", C.c_int64),
-                ("staging_bytes", C.c_int64)]
+                ("staging_bytes", C.c_int64), ("drafted_tokens", C.c_int64),
+                ("aux_proposed", C.c_int64), ("aux_accepted", C.c_int64)]
 
 
 class LoopMetrics(C.Structure):

@@ -712,22 +712,6 @@ int vc_run_decode(vc_engine* e, const int* slots, int n, int K, int32_t* out, do
 
 namespace {
 
-// Prompt-lookup n-gram proposal: the continuation (<= x tokens) that followed
-// the most recent earlier occurrence of the last `ng` emitted tokens.
-std::vector<int32_t> ngram_proposal(const std::vector<int32_t>& h, int ng, int x) {
-  std::vector<int32_t> out;
-  const int n = static_cast<int>(h.size());
-  if (ng < 1 || n <= ng) return out;
-  for (int j = n - ng - 1; j >= 0; --j) {
-    bool hit = true;
-    for (int k = 0; k < ng && hit; ++k) hit = h[j + k] == h[n - ng + k];
-    if (!hit) continue;
-    for (int k = j + ng; k < n && static_cast<int>(out.size()) < x; ++k) out.push_back(h[k]);
-    break;
-  }
-  return out;
-}
-
 // Lock-step rounds (speckv::run_speculative, specloop.cpp:58-79).  With
 // ngram > 0 the round's drafter is composed: a request whose emitted history
 // repeats its last `ngram` tokens takes the n-gram continuation as its draft
@@ -751,7 +735,7 @@ void speculative_loop(vc::Engine& en, const int* slots, int n, int K, int x, int
       if (produced[i] < K) act.push_back(i);
     if (act.empty()) break;
     for (int i : act) {
-      const auto prop = ngram_proposal(en.seq(slots[i]).history, ngram, x);
+      const auto prop = vc::ngram_proposal(en.seq(slots[i]).history, ngram, x);
       if (prop.empty()) {
         model.push_back(i);
         continue;
@@ -847,7 +831,7 @@ void composed_loop(vc::Engine& en, const int* slots, int n, int K, int x, int ng
         if (room < 1) continue;
         std::vector<int32_t> ctx = s.history.empty() ? std::vector<int32_t>{s.pending} : s.history;
         ctx.insert(ctx.end(), s.drafted.begin(), s.drafted.end());
-        auto prop = ngram_proposal(ctx, ngram, std::min(depth - 1, room - 1));
+        auto prop = vc::ngram_proposal(ctx, ngram, std::min(depth - 1, room - 1));
         vc::StepItem t;
         t.slot = slots[i];
         t.mode = vc::RowMode::Draft;

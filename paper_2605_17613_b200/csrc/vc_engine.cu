@@ -17,6 +17,20 @@ void check_cuda(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw CudaError(std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+std::vector<int32_t> ngram_proposal(const std::vector<int32_t>& h, int ng, int x) {
+  std::vector<int32_t> out;
+  const int n = static_cast<int>(h.size());
+  if (ng < 1 || n <= ng) return out;
+  for (int j = n - ng - 1; j >= 0; --j) {
+    bool hit = true;
+    for (int k = 0; k < ng && hit; ++k) hit = h[j + k] == h[n - ng + k];
+    if (!hit) continue;
+    for (int k = j + ng; k < n && static_cast<int>(out.size()) < x; ++k) out.push_back(h[k]);
+    break;
+  }
+  return out;
+}
+
 #define VC_CK(expr) check_cuda((expr), #expr)
 #define VC_LAUNCH(expr)           \
   do {                            \

@@ -400,4 +400,8 @@ struct ContractViolation : std::logic_error {
 
 void check_cuda(cudaError_t e, const char* what);
 
+// Prompt-lookup n-gram proposal: the continuation (<= x tokens) that followed
+// the most recent earlier occurrence of the last `ng` tokens of h.
+std::vector<int32_t> ngram_proposal(const std::vector<int32_t>& h, int ng, int x);
+
 }  // namespace vc

@@ -75,6 +75,10 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
   const int n_res = static_cast<int>(res_idx.size());
   const int n_off = n - n_res;
   const int x_res = sd.x_resident > 0 ? sd.x_resident : sd.x;
+  // two-level composition: prompt-lookup proposals ride each drafting row
+  const bool composed = sd.ngram >= 1 && sd.depth >= 2;
+  if (composed && sd.depth > std::max(1, cfgE.draft_depth))
+    throw speckv::ConfigError("scheduled: depth exceeds the engine's draft_depth");
   if (x_res > cfgE.max_x) throw speckv::ConfigError("scheduled: x_resident out of [1, max_x]");
   const size_t bpt = en.full_kv_bytes_per_token();
 
@@ -390,14 +394,36 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
     const speckv::StepResult pr = plan.execution_step(ev);
     // 4. one forward pass: drafting rows + verify windows
     std::vector<vc::StepItem> items;
-    for (speckv::RequestId id : pr.drafted) {
-      const auto& s = en.seq(slot_of[id]);
+    std::vector<std::vector<int32_t>> props;  // per drafting item: auxiliary proposals (composition)
+    // a drafting row: the window's last token, plus (composition) the
+    // prompt-lookup continuation of the request's context, bounded by `cap`
+    // tokens of window
+    // returns false (no row) once a composed window already holds `cap`
+    // tokens: the scheduler may still count draft iterations for it
+    std::vector<char> drew;  // per scheduler drafting session: a row was added
+    auto draft_item = [&](int slot, int cap) {
+      const auto& s = en.seq(slot);
+      if (composed && static_cast<int>(s.drafted.size()) >= std::min(cap, cfgE.max_x)) {
+        drew.push_back(0);
+        return;
+      }
+      drew.push_back(1);
       vc::StepItem t;
-      t.slot = slot_of[id];
+      t.slot = slot;
       t.mode = vc::RowMode::Draft;
       t.tokens = {s.drafted.empty() ? s.pending : s.drafted.back()};
+      std::vector<int32_t> prop;
+      const int room = std::min(cap, cfgE.max_x) - static_cast<int>(s.drafted.size()) - 1;
+      if (composed && room > 0) {
+        std::vector<int32_t> ctx = s.history.empty() ? std::vector<int32_t>{s.pending} : s.history;
+        ctx.insert(ctx.end(), s.drafted.begin(), s.drafted.end());
+        prop = vc::ngram_proposal(ctx, sd.ngram, std::min(sd.depth - 1, room));
+        t.tokens.insert(t.tokens.end(), prop.begin(), prop.end());
+      }
       items.push_back(std::move(t));
-    }
+      props.push_back(std::move(prop));
+    };
+    for (speckv::RequestId id : pr.drafted) draft_item(slot_of[id], composed ? sd.x : cfgE.max_x);
     // resident requests: draft their round, then verify against their own
     // HBM-resident full KV (no reload)
     std::vector<int> res_drafting, res_verifying;
@@ -405,11 +431,7 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
       if (produced[i] >= sd.K) continue;
       const auto& s = en.seq(slot_of[i]);
       if (static_cast<int>(s.drafted.size()) < round_x[i]) {
-        vc::StepItem t;
-        t.slot = slot_of[i];
-        t.mode = vc::RowMode::Draft;
-        t.tokens = {s.drafted.empty() ? s.pending : s.drafted.back()};
-        items.push_back(std::move(t));
+        draft_item(slot_of[i], round_x[i]);
         res_drafting.push_back(i);
       }
     }
@@ -417,7 +439,9 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
     for (const auto& v : pr.verifies) {
       const int req = static_cast<int>(v.request);
       const auto& s = en.seq(slot_of[req]);
-      if (static_cast<int>(s.drafted.size()) != v.drafted)
+      // (composition: confirmed proposals make the window longer than the
+      // scheduler's draft iterations)
+      if (composed ? static_cast<int>(s.drafted.size()) < v.drafted : static_cast<int>(s.drafted.size()) != v.drafted)
         throw vc::ContractViolation("scheduled loop: draft count diverged from the scheduler");
       if (ring) {  // predictions came from the streamed verify's ranges
         ring_verifying.push_back(req);
@@ -435,7 +459,7 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
     for (int i : res_idx) {
       if (produced[i] >= sd.K) continue;
       const auto& s = en.seq(slot_of[i]);
-      if (static_cast<int>(s.drafted.size()) == round_x[i]) {
+      if (static_cast<int>(s.drafted.size()) >= round_x[i]) {
         vc::StepItem t;
         t.slot = slot_of[i];
         t.mode = vc::RowMode::Verify;
@@ -459,13 +483,31 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
     const double t_emit = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     double emitted_now = 0;
     size_t off = 0;
-    for (speckv::RequestId id : pr.drafted) en.push_draft(slot_of[id], row[off++]);
-    for (int i : res_drafting) en.push_draft(slot_of[i], row[off++]);
+    // the pass's own prediction, then (composition) each proposal its previous
+    // row confirmed: row j assumed proposal j, valid only if p_j matched it
+    size_t di = 0, dn = 0;
+    auto take_draft = [&](int slot) {
+      if (!drew[dn++]) return;
+      const auto& pr_ = props[di++];
+      en.push_draft(slot, row[off]);
+      int matched = 0;
+      for (size_t j = 0; j < pr_.size(); ++j) {
+        if (row[off + j] != pr_[j]) break;
+        en.push_draft(slot, row[off + j + 1]);
+        ++matched;
+      }
+      st.aux_proposed += static_cast<int64_t>(pr_.size());
+      st.aux_accepted += matched;
+      off += pr_.size() + 1;
+    };
+    for (speckv::RequestId id : pr.drafted) take_draft(slot_of[id]);
+    for (int i : res_drafting) take_draft(slot_of[i]);
     meas.accepted.clear();
     for (int req : verifying) {
       const int x_r = static_cast<int>(en.seq(slot_of[req]).drafted.size());
       std::vector<int32_t> p(row.begin() + off, row.begin() + off + x_r + 1);
       off += x_r + 1;
+      st.drafted_tokens += x_r;
       const auto em = en.accept_commit(slot_of[req], p, staged ? stage_of[req] : -1);
       meas.accepted.push_back(static_cast<int>(em.size()) - 1);
       accepted_sum += static_cast<double>(em.size()) - 1;
@@ -483,6 +525,7 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
     for (int req : ring_verifying) {
       auto vit = std::find_if(vstreams.begin(), vstreams.end(), [&](const VStreamRef& v) { return v.req == req; });
       if (vit == vstreams.end() || !vit->ready) throw vc::ContractViolation("scheduled loop: verify without a streamed result");
+      st.drafted_tokens += static_cast<int64_t>(en.seq(slot_of[req]).drafted.size());
       const auto em = en.accept_commit_stream(slot_of[req], en.stream_preds(vit->id), vit->id);
       vstreams.erase(vit);
       meas.accepted.push_back(static_cast<int>(em.size()) - 1);
@@ -502,6 +545,7 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
       const int x_r = static_cast<int>(en.seq(slot_of[i]).drafted.size());
       std::vector<int32_t> p(row.begin() + off, row.begin() + off + x_r + 1);
       off += x_r + 1;
+      st.drafted_tokens += x_r;
       const auto em = en.accept_commit(slot_of[i], p, slot_of[i]);
       res_verifies += 1;
       res_accepted += static_cast<double>(em.size()) - 1;

@@ -406,13 +406,16 @@ class Engine:
         return ms.value, b.value
 
     def run_scheduled(self, slots, K, x, window, iteration_time=0.0, link_bandwidth=0.0,
-                      hbm_capacity=0, warmup_iterations=0, timed_iterations=0, x_resident=0, arrivals=None):
+                      hbm_capacity=0, warmup_iterations=0, timed_iterations=0, x_resident=0, arrivals=None,
+                      ngram=0, depth=0):
         """Requests in the engine's resident slots (resident_slots, the
         reference's B_g; analytics.cpp:45-82) verify against their HBM-resident
         full KV with x_resident-token rounds; the others are reloaded per verify.
         arrivals = [(n_ctx, first_token, seed, arrival_ms)]: requests that arrive
         during the run and take the slots finished requests free (out gains a
-        row per arrival)."""
+        row per arrival).  ngram >= 1, depth >= 2: two-level composition -- every
+        drafting row carries up to depth-1 prompt-lookup proposals (engine
+        draft_depth >= depth)."""
         s = np.ascontiguousarray(slots, np.int32)
         arr = arrivals or []
         out = np.zeros((s.size + len(arr), K), np.int32)
@@ -420,7 +423,7 @@ class Engine:
                                                      for a, b, c, d in arr])
         sd = _lib.SchedDesc(x, window, iteration_time, link_bandwidth, hbm_capacity, K,
                             warmup_iterations, timed_iterations, x_resident,
-                            ad if arr else None, len(arr))
+                            ad if arr else None, len(arr), int(ngram), int(depth))
         st = _lib.SchedStats()
         check(self.lib.vc_run_scheduled(self.h, _ptr(s, C.c_int), s.size, C.byref(sd),
                                         _ptr(out, C.c_int32), C.byref(st)))

@@ -76,3 +76,33 @@ def test_composed_depth1_equals_plain(cuda, weights):
     b, rounds, _ = e.run_speculative([1], 32, 5)
     np.testing.assert_array_equal(a, b)
     e.close()
+
+
+@pytest.mark.parametrize("tier,ring,depth", [(0, 0, 3), (1, 0, 3), (1, 3, 4)])
+def test_composed_scheduled_lossless(cuda, weights, tier, ring, depth):
+    """Composition inside the swap-scheduled loop (vc_run_scheduled with
+    ngram/depth): proposals ride the drafting rows of the staggered loop, for
+    the HBM tier, the staged host tier and the chunk-ring host tier."""
+    n, K = 3, 40
+    ref = Engine(TINY, max_slots=n, max_ctx=N_CTX + 200, max_x=1, quant_bits=0)
+    ref.load_weights(weights)
+    for s in range(n):
+        ref.add_synthetic(s, N_CTX, 17 + s, seed=1 + s)
+    base, _ = ref.autoregress(list(range(n)), K)
+    ref.close()
+    if tier == 1:
+        e = Engine(TINY, max_slots=n, max_ctx=N_CTX + 400, max_x=24, quant_bits=4, full_tier=1,
+                   n_stage=0 if ring else 3, ring_chunks=ring, max_verify=4, draft_depth=depth)
+    else:
+        e = Engine(TINY, max_slots=n, max_ctx=N_CTX + 400, max_x=24, quant_bits=4, max_verify=4, draft_depth=depth)
+    e.load_weights(weights)
+    for s in range(n):
+        e.add_synthetic(s, N_CTX, 17 + s, seed=1 + s)
+        e.compress(s)
+    out, st = e.run_scheduled(list(range(n)), K, x=8, window=32, ngram=1, depth=depth)
+    np.testing.assert_array_equal(out, base)
+    assert st["aux_accepted"] <= st["aux_proposed"]
+    assert st["drafted_tokens"] >= st["verifies"]
+    print(f"MEASURED scheduled composition tier={tier} ring={ring}: accepted/verify {st['mean_accept']:.2f}, "
+          f"aux {st['aux_accepted']}/{st['aux_proposed']}")
+    e.close()
