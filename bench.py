@@ -975,7 +975,8 @@ def main():
     base_value = B * world * Kb / bdev_s
     ka_bytes = h["ka"][1]
     achieved = ka_bytes / (ka_ms / 1e3) / 1e9
-    traffic, traffic_src = draft_traffic() if not cfg3 else (None, None)
+    # the committed ncu capture is of the int4 kernel at this workload
+    traffic, traffic_src = draft_traffic() if not cfg3 and args.bits == 4 and B == 16 else (None, None)
     rows = st["timed_rows"]
     h2d = (rows * (4 + 16) + st["h2d_bytes"]) / K  # per round: step inputs (token + row descriptor) + KV reloads
 
@@ -1074,7 +1075,7 @@ def main():
             "reference_csv": reference_csv(),
             **({"long_horizon": tier_summary(long_run, 0)} if long_run else {}),
             "roofline": {"kernel": ("dense_umma_kernel<128,4> drafting over the drop tier" if cfg3 else
-                                    "draft_attn_quant_kernel<128,4,4>") + f" (one launch per layer, {B} requests)",
+                                    f"draft_attn_quant_kernel<128,{args.bits},4>") + f" (one launch per layer, {B} requests)",
                          "bound": "hbm", "achieved": round(achieved, 1), "peak": round(peak, 1), "unit": "GB/s",
                          "frac": round(achieved / peak, 3),
                          "traffic": traffic, "traffic_source": traffic_src,
