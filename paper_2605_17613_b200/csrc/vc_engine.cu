@@ -159,9 +159,12 @@ Engine::Engine(const EngineConfig& cfg, int device) : cfg_(cfg), device_(device)
     throw ContractViolation("resident_slots is a placement of the host tier (full_tier 1)");
   if (cfg_.ring_chunks < 0 || (cfg_.ring_chunks > 0 && cfg_.full_tier != 1))
     throw ContractViolation("ring_chunks is a staging mode of the host tier (full_tier 1)");
-  if (cfg_.ring_chunks > 0 && (cfg_.ring_chunks < 2 || cfg_.max_streams < 1 || cfg_.quant_bits == 0 ||
-                               cfg_.tp_size > 1))
-    throw ContractViolation("ring_chunks: needs >= 2 chunks, max_streams >= 1, the quantised tier, no TP");
+  if (cfg_.ring_chunks > 0 &&
+      (cfg_.ring_chunks < 2 || cfg_.max_streams < 1 || cfg_.tp_size > 1 ||
+       (cfg_.quant_bits == 0 && !(cfg_.drop_ratio > 0.0 && cfg_.drop_window == 0 && cfg_.drop_score == 0))))
+    throw ContractViolation(
+        "ring_chunks: needs >= 2 chunks, max_streams >= 1, no TP, and the quantised tier or the drop-topk tier "
+        "(offline, key-norm scores)");
   if (cfg_.full_tier == 1 && cfg_.ring_chunks == 0 &&
       cfg_.resident_slots + (cfg_.resident_slots < cfg_.max_slots ? 1 : 0) > cfg_.n_stage)
     throw ContractViolation("n_stage must hold every resident slot plus one rotating staging slot");
@@ -202,8 +205,11 @@ Engine::~Engine() {
   }
   for (auto& [k, v] : vstreams_)
     if (v.ev_final) cudaEventDestroy(v.ev_final);
-  for (auto* evs : {&ring_start_, &ring_done_, &ring_free_, &ring_upload_})
+  for (auto* evs : {&ring_start_, &ring_done_, &ring_free_, &ring_upload_, &ring_landed_})
     for (cudaEvent_t e : *evs) cudaEventDestroy(e);
+  if (exp_st_) cudaStreamDestroy(exp_st_);
+  for (void* p : {static_cast<void*>(land_.k), static_cast<void*>(land_.v), static_cast<void*>(kept_all_)})
+    if (p) cudaFree(p);
   for (void* p : {static_cast<void*>(ring_.k), static_cast<void*>(ring_.v), static_cast<void*>(wbuf_.k),
                   static_cast<void*>(wbuf_.v), static_cast<void*>(xsave_), static_cast<void*>(sssave_),
                   static_cast<void*>(ring_seqs_dev_)})
@@ -488,6 +494,19 @@ void Engine::alloc_all() {
       cudaEvent_t e;
       VC_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
       ring_upload_.push_back(e);
+    }
+    if (drop_mode()) {
+      const size_t chunk = static_cast<size_t>(m.n_kv) * ring_.cap * d;
+      land_.cap = ring_.cap;
+      land_.k = dmalloc<uint16_t>(static_cast<size_t>(cfg_.ring_chunks) * chunk);
+      land_.v = dmalloc<uint16_t>(static_cast<size_t>(cfg_.ring_chunks) * chunk);
+      kept_all_ = dmalloc<int32_t>(static_cast<size_t>(cfg_.max_slots) * L * m.n_kv * kept_cap_);
+      for (int i = 0; i < cfg_.ring_chunks; ++i) {
+        cudaEvent_t e;
+        VC_CK(cudaEventCreate(&e));
+        ring_landed_.push_back(e);
+      }
+      VC_CK(cudaStreamCreateWithFlags(&exp_st_, cudaStreamNonBlocking));
     }
   }
 }
@@ -802,10 +821,68 @@ void Engine::compress_as(int slot, double ratio, const int32_t* kept_host, int k
     // just synthesised: the full KV is still in the scratch staging slot
     src = stage_;
     src_slot = scratch_stage_used_;
+  } else if (ring_mode() && drop_mode()) {
+    // chunk ring over the drop tier: one layer at a time through the two
+    // admission chunks -- score + top-k (or the given kept set), kept rows
+    // into the drop tier, and the DROPPED rows compacted back into the host
+    // pool: a verify then reloads only (1 - c) of the full KV
+    // (analytics.cpp:77-78 charges exactly that) and rebuilds the rest from
+    // the drop tier (expand_dropped)
+    if (s.drop_T > 0) throw ContractViolation("compress: the host pool already holds only the dropped rows");
+    const int T = s.committed;
+    const long long k = kept_host ? k_host : std::llround(ratio * static_cast<double>(T));
+    if (k < 1) throw ContractViolation("compress: drop ratio retains < 1 token");
+    if (k > kept_cap_ || k + cfg_.max_x + 2 > drop_.cap)
+      throw ContractViolation("compress: drop tier capacity exceeded (ratio above the engine's drop_ratio)");
+    const size_t slice_elems = static_cast<size_t>(full_.cap) * m.d;
+    const size_t pitch = slice_elems * 2;
+    const int ca = cfg_.ring_chunks, cb = cfg_.ring_chunks + 1;  // full rows / compacted dropped rows
+    uint16_t* kb = ring_.k + static_cast<size_t>(cb) * m.n_kv * slice_elems;
+    uint16_t* vb = ring_.v + static_cast<size_t>(cb) * m.n_kv * slice_elems;
+    check_d2h();
+    VC_CK(cudaStreamSynchronize(st_));
+    int32_t* kept = kept_of(slot);
+    for (int l = 0; l < m.layers; ++l) {
+      const size_t o = static_cast<size_t>(l) * m.n_kv * slice_elems;
+      int32_t* kl = kept + static_cast<size_t>(l) * m.n_kv * k;
+      VC_CK(cudaMemcpy2DAsync(ring_.k + static_cast<size_t>(ca) * m.n_kv * slice_elems, pitch, host_pool_k(slot) + o,
+                              pitch, static_cast<size_t>(T) * m.d * 2, m.n_kv, cudaMemcpyHostToDevice, st_));
+      VC_CK(cudaMemcpy2DAsync(ring_.v + static_cast<size_t>(ca) * m.n_kv * slice_elems, pitch, host_pool_v(slot) + o,
+                              pitch, static_cast<size_t>(T) * m.d * 2, m.n_kv, cudaMemcpyHostToDevice, st_));
+      if (kept_host) {
+        VC_CK(cudaMemcpyAsync(kl, kept_host + static_cast<size_t>(l) * m.n_kv * k,
+                              static_cast<size_t>(m.n_kv) * k * sizeof(int32_t), cudaMemcpyHostToDevice, st_));
+      } else {
+        float* sc = score_buf_ + static_cast<size_t>(l) * m.n_kv * T;
+        VC_LAUNCH(key_scores(ring_.k + static_cast<size_t>(ca) * m.n_kv * slice_elems, m.n_kv, T, m.d, slice_elems,
+                             score_w_, sc, st_));
+        VC_LAUNCH(topk_select(sc, m.n_kv, T, static_cast<int>(k), kl, st_));
+      }
+      VC_LAUNCH(gather_kept(ring_, ca, kl, static_cast<int>(k), drop_, slot * m.layers + l, m.n_kv, m.d, st_));
+      VC_LAUNCH(compact_dropped(ring_, ca, kl, static_cast<int>(k), T, ring_, cb, m.n_kv, m.d, st_));
+      const size_t w = static_cast<size_t>(T - k) * m.d * 2;
+      if (w > 0) {
+        VC_CK(cudaMemcpy2DAsync(host_pool_k(slot) + o, pitch, kb, pitch, w, m.n_kv, cudaMemcpyDeviceToHost, st_));
+        VC_CK(cudaMemcpy2DAsync(host_pool_v(slot) + o, pitch, vb, pitch, w, m.n_kv, cudaMemcpyDeviceToHost, st_));
+      }
+      VC_CK(cudaStreamSynchronize(st_));  // the admission chunks are reused by the next layer
+    }
+    VC_CK(cudaMemcpyAsync(kept_buf_, kept, static_cast<size_t>(m.layers) * m.n_kv * k * sizeof(int32_t),
+                          cudaMemcpyDeviceToDevice, st_));
+    score_T_ = T;
+    last_kept_k_ = static_cast<int>(k);
+    s.drop_len = static_cast<int>(k);
+    s.drop_base = static_cast<int>(k);
+    s.drop_T = T;
+    s.n_groups = 0;
+    s.tail_committed = 0;
+    s.draft_len = 0;
+    s.drafted.clear();
+    VC_CK(cudaStreamSynchronize(st_));
+    return;
   } else if (ring_mode()) {
     // chunk ring: stream the prefix one layer at a time through the two
     // admission chunks and quantise each layer as it lands
-    if (drop_mode()) throw ContractViolation("chunk ring: drop tier not supported");
     const int ng = std::min(s.committed / VC_QGROUP, quant_.cap / VC_QGROUP);
     const int tc = s.committed - ng * VC_QGROUP;
     if (tc > tail_cap_ - cfg_.max_x - 1) throw ContractViolation("tail overflow");
@@ -912,6 +989,7 @@ void Engine::compress_drop(int slot, const KvPool& src, int src_slot, double rat
   last_kept_k_ = static_cast<int>(k);
   s.drop_len = static_cast<int>(k);
   s.drop_base = static_cast<int>(k);
+  s.drop_T = T;
   s.n_groups = 0;
   s.tail_committed = 0;
   s.draft_len = 0;
@@ -1711,7 +1789,7 @@ size_t Engine::staging_bytes() const {
   const size_t slab = static_cast<size_t>(m.n_kv) * full_.cap * m.d * 2 * 2;  // one layer, K and V
   if (cfg_.full_tier != 1) return 0;
   const size_t rot = ring_mode() ? 0 : static_cast<size_t>(cfg_.n_stage - cfg_.resident_slots) * m.layers * slab;
-  return rot + (ring_mode() ? static_cast<size_t>(cfg_.ring_chunks + 2) * slab : 0);
+  return rot + (ring_mode() ? static_cast<size_t>(cfg_.ring_chunks + 2 + (land_.k ? cfg_.ring_chunks : 0)) * slab : 0);
 }
 
 int Engine::stream_begin(int slot) {
@@ -1732,8 +1810,15 @@ int Engine::stream_begin(int slot) {
   v.base = ring_seq_;
   ring_seq_ += cfg_.model.layers;
   v.committed = s.committed;
-  v.origin = s.n_groups * VC_QGROUP;
+  // the exact rows accept needs: the residual group + window (quantised
+  // tier), or only the window (drop tier: accepted rows are appended there)
+  v.origin = drop_mode() ? s.committed : s.n_groups * VC_QGROUP;
+  if (drop_mode() && s.drop_T == 0) throw ContractViolation("stream: compress the request first");
   VC_CK(cudaEventCreateWithFlags(&v.ev_final, cudaEventDisableTiming));
+  if (drop_mode()) {  // the rebuild reads drop-tier rows the compute stream appended
+    VC_CK(cudaEventRecord(ev_commit_, st_));
+    VC_CK(cudaStreamWaitEvent(exp_st_, ev_commit_, 0));
+  }
   const int id = next_vstream_++;
   vstreams_[id] = std::move(v);
   vs_order_.push_back(id);
@@ -1756,11 +1841,32 @@ void Engine::stream_issue_chunk(VStream& v) {
   // the chunk's previous layer has been read by its verify range
   VC_CK(cudaStreamWaitEvent(copy_st_, ring_free_[c], 0));
   VC_CK(cudaEventRecord(ring_start_[c], copy_st_));
-  if (width > 0) {
-    VC_CK(cudaMemcpy2DAsync(dk, pitch, host_pool_k(v.slot) + o, pitch, width, m.n_kv, cudaMemcpyHostToDevice, copy_st_));
-    VC_CK(cudaMemcpy2DAsync(dv, pitch, host_pool_v(v.slot) + o, pitch, width, m.n_kv, cudaMemcpyHostToDevice, copy_st_));
+  if (drop_mode()) {
+    // only the dropped rows cross the link; the rebuild (position order,
+    // kept rows and rows accepted since compress from the drop tier) runs on
+    // its own stream as soon as they land
+    const SeqState& s = seqs_.at(v.slot);
+    const int T = s.drop_T, k = s.drop_base;
+    const size_t w = static_cast<size_t>(T - k) * m.d * 2;
+    uint16_t* lk = land_.k + static_cast<size_t>(c) * m.n_kv * slice_elems;
+    uint16_t* lv = land_.v + static_cast<size_t>(c) * m.n_kv * slice_elems;
+    if (w > 0) {
+      VC_CK(cudaMemcpy2DAsync(lk, pitch, host_pool_k(v.slot) + o, pitch, w, m.n_kv, cudaMemcpyHostToDevice, copy_st_));
+      VC_CK(cudaMemcpy2DAsync(lv, pitch, host_pool_v(v.slot) + o, pitch, w, m.n_kv, cudaMemcpyHostToDevice, copy_st_));
+    }
+    VC_CK(cudaEventRecord(ring_landed_[c], copy_st_));
+    VC_CK(cudaStreamWaitEvent(exp_st_, ring_landed_[c], 0));
+    VC_CK(expand_dropped(land_, c, drop_, v.slot * m.layers + l, kept_of(v.slot) + static_cast<size_t>(l) * m.n_kv * k,
+                         k, T, v.committed, ring_, c, m.n_kv, m.d, exp_st_));
+    ++launches_;
+    VC_CK(cudaEventRecord(ring_done_[c], exp_st_));
+  } else {
+    if (width > 0) {
+      VC_CK(cudaMemcpy2DAsync(dk, pitch, host_pool_k(v.slot) + o, pitch, width, m.n_kv, cudaMemcpyHostToDevice, copy_st_));
+      VC_CK(cudaMemcpy2DAsync(dv, pitch, host_pool_v(v.slot) + o, pitch, width, m.n_kv, cudaMemcpyHostToDevice, copy_st_));
+    }
+    VC_CK(cudaEventRecord(ring_done_[c], copy_st_));
   }
-  VC_CK(cudaEventRecord(ring_done_[c], copy_st_));
   ++v.issued;
 }
 
@@ -1800,9 +1906,11 @@ int Engine::stream_advance(int id) {
     if (e == cudaErrorNotReady) break;
     check_cuda(e, "stream chunk");
     float ms = 0.f;
-    VC_CK(cudaEventElapsedTime(&ms, ring_start_[c], ring_done_[c]));
+    VC_CK(cudaEventElapsedTime(&ms, ring_start_[c], drop_mode() ? ring_landed_[c] : ring_done_[c]));
     h2d_ms_ += ms;
-    h2d_bytes_ += 2.0 * static_cast<double>(v.committed) * m.d * 2 * m.n_kv;
+    const SeqState& s = seqs_.at(v.slot);
+    const int rows = drop_mode() ? s.drop_T - s.drop_base : v.committed;
+    h2d_bytes_ += 2.0 * static_cast<double>(rows) * m.d * 2 * m.n_kv;
     ++v.landed;
   }
   if (v.landed > v.done) {
@@ -1837,7 +1945,7 @@ std::vector<int32_t> Engine::accept_commit_stream(int slot, const std::vector<in
       !std::equal(s.drafted.begin(), s.drafted.end(), v.tokens.begin() + 1))
     throw ContractViolation("stream: the open round is not the window the verify scored");
   const RowSrc src{wbuf_, v.buf, v.origin};
-  auto em = accept_commit_from(slot, preds, src, true);
+  auto em = accept_commit_from(slot, preds, src, !drop_mode());
   stream_end(id);
   return em;
 }
@@ -1852,6 +1960,7 @@ void Engine::stream_end(int id) {
     // abandoned mid-stream: its copies land and its ranges run first, then
     // the chunks it still holds go back to the ring
     VC_CK(cudaStreamSynchronize(copy_st_));
+    if (exp_st_) VC_CK(cudaStreamSynchronize(exp_st_));
     VC_CK(cudaStreamSynchronize(st_));
     for (int l = v.done; l < v.issued; ++l) {
       const int c = static_cast<int>((v.base + l) % R);

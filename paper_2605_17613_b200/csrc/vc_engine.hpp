@@ -93,6 +93,7 @@ struct SeqState {
   int draft_len = 0;      // drafted tokens of the open round (their KV in the tail)
   int drop_len = 0;       // drop tier: kept prefix tokens + exact tokens appended since
   int drop_base = 0;      // drop tier: rows of the compress-time kept prefix
+  int drop_T = 0;         // drop tier: positions the compress covered (kept + dropped)
   std::vector<int32_t> drafted;
   std::vector<int32_t> history;  // every emitted token
 };
@@ -377,6 +378,16 @@ class Engine {
   int next_vstream_ = 1;
   std::vector<char> vbuf_used_;
   KvPool wbuf_{};                             // [buf][layer][kv-head][tail_cap][d] exact window rows
+  // drop tier over the chunk ring: the host pool holds only each slice's
+  // dropped rows (compacted); a layer lands in land_[c] and is rebuilt into
+  // ring_[c] from the landed rows + the drop tier (expand_dropped on exp_st_)
+  KvPool land_{};
+  int32_t* kept_all_ = nullptr;               // [slot][layer*n_kv][k] kept positions per request
+  std::vector<cudaEvent_t> ring_landed_;
+  cudaStream_t exp_st_ = nullptr;
+  int32_t* kept_of(int slot) const {
+    return kept_all_ + static_cast<size_t>(slot) * cfg_.model.layers * cfg_.model.n_kv * kept_cap_;
+  }
   float *xsave_ = nullptr, *sssave_ = nullptr;  // [buf][Wrows][H], [buf][Wrows][H/128]
   int wrows_ = 0;
   AttnSeq* ring_seqs_dev_ = nullptr;          // [layers] per-layer sequence of the range forward

@@ -94,6 +94,15 @@ cudaError_t tail_refill(KvPool src, int src_slot, int src_pos, int n, QuantPool 
 // -> positions 0..k of dst_slot (compacted, position order).
 cudaError_t gather_kept(KvPool src, int src_slot, const int32_t* kept, int k, KvPool dst, int dst_slot,
                         int n_slices, int d, cudaStream_t st);
+// Drop tier over the host tier: the rows of [0, T) NOT in the kept set
+// (kept [slice][k] ascending), compacted in position order into dst rows
+// [0, T - k); and the inverse -- a chunk rebuilt in position order for
+// [0, n) from the landed compact rows, the drop tier's kept rows and the
+// drop tier's exact rows appended since compress (rows k + p - T).
+cudaError_t compact_dropped(KvPool src, int src_slot, const int32_t* kept, int k, int T, KvPool dst, int dst_slot,
+                            int n_slices, int d, cudaStream_t st);
+cudaError_t expand_dropped(KvPool land, int land_slot, KvPool drop, int drop_slot, const int32_t* kept, int k, int T,
+                           int n, KvPool dst, int dst_slot, int n_slices, int d, cudaStream_t st);
 // Copy token rows [src_pos, src_pos+n) of every slice to [dst_pos, dst_pos+n).
 cudaError_t copy_rows(KvPool src, int src_slot, int src_pos, int n, KvPool dst, int dst_slot, int dst_pos,
                       int n_slices, int d, cudaStream_t st);

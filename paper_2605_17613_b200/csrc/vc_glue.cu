@@ -1,3 +1,4 @@
+#include <algorithm>
 // vc_glue.cu -- model glue outside the GEMM epilogues: embedding + RMSNorm,
 // the RMSNorm apply that follows a residual epilogue, greedy argmax, the
 // synthetic initialiser and the draft-tail refill.  All reductions run in a
@@ -166,6 +167,72 @@ __global__ void gather_kept_kernel(KvPool src, int src_slot, const int32_t* kept
   }
 }
 
+// rank of position p among the slice's kept positions (sorted ascending):
+// the number of kept positions < p
+VC_DEV int kept_rank(const int32_t* kp, int k, int p) {
+  int lo = 0, hi = k;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (kp[mid] < p) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// dropped rows of [0, T) (the complement of the kept set) compacted in
+// position order: dropped position p -> row p - rank(p)
+__global__ void compact_dropped_kernel(KvPool src, int src_slot, const int32_t* kept, int k, int T, KvPool dst,
+                                       int dst_slot, int n_slices, int d) {
+  const int sl = blockIdx.y;
+  const size_t s_slice = static_cast<size_t>(src_slot) * n_slices + sl;
+  const size_t d_slice = static_cast<size_t>(dst_slot) * n_slices + sl;
+  const int32_t* kp = kept + static_cast<size_t>(sl) * k;
+  const int vec = d / 8;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < T * vec; i += gridDim.x * blockDim.x) {
+    const int p = i / vec, c = i % vec;
+    const int r = kept_rank(kp, k, p);
+    if (r < k && kp[r] == p) continue;  // kept: lives in the drop tier
+    const size_t so = (s_slice * src.cap + p) * d, dof = (d_slice * dst.cap + (p - r)) * d;
+    reinterpret_cast<uint4*>(dst.k + dof)[c] = reinterpret_cast<const uint4*>(src.k + so)[c];
+    reinterpret_cast<uint4*>(dst.v + dof)[c] = reinterpret_cast<const uint4*>(src.v + so)[c];
+  }
+}
+
+// a full-KV chunk rebuilt in position order for p in [0, n): p < T dropped ->
+// landed row p - rank(p); p < T kept -> drop-tier row rank(p); p >= T (exact
+// rows accepted since compress) -> drop-tier row k + p - T
+__global__ void expand_dropped_kernel(KvPool land, int land_slot, KvPool drop, int drop_slot, const int32_t* kept,
+                                      int k, int T, int n, KvPool dst, int dst_slot, int n_slices, int d) {
+  const int sl = blockIdx.y;
+  const size_t l_slice = static_cast<size_t>(land_slot) * n_slices + sl;
+  const size_t r_slice = static_cast<size_t>(drop_slot) * n_slices + sl;
+  const size_t d_slice = static_cast<size_t>(dst_slot) * n_slices + sl;
+  const int32_t* kp = kept + static_cast<size_t>(sl) * k;
+  const int vec = d / 8;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n * vec; i += gridDim.x * blockDim.x) {
+    const int p = i / vec, c = i % vec;
+    const uint16_t *sk, *sv;
+    if (p >= T) {
+      const size_t so = (r_slice * drop.cap + k + (p - T)) * d;
+      sk = drop.k + so;
+      sv = drop.v + so;
+    } else {
+      const int r = kept_rank(kp, k, p);
+      if (r < k && kp[r] == p) {
+        const size_t so = (r_slice * drop.cap + r) * d;
+        sk = drop.k + so;
+        sv = drop.v + so;
+      } else {
+        const size_t so = (l_slice * land.cap + (p - r)) * d;
+        sk = land.k + so;
+        sv = land.v + so;
+      }
+    }
+    const size_t dof = (d_slice * dst.cap + p) * d;
+    reinterpret_cast<uint4*>(dst.k + dof)[c] = reinterpret_cast<const uint4*>(sk)[c];
+    reinterpret_cast<uint4*>(dst.v + dof)[c] = reinterpret_cast<const uint4*>(sv)[c];
+  }
+}
+
 __global__ void copy_rows_kernel(KvPool src, int src_slot, int src_pos, int n, KvPool dst, int dst_slot,
                                  int dst_pos, int n_slices, int d) {
   const int sl = blockIdx.x;
@@ -232,6 +299,24 @@ cudaError_t gather_kept(KvPool src, int src_slot, const int32_t* kept, int k, Kv
                         int n_slices, int d, cudaStream_t st) {
   if (k <= 0 || n_slices <= 0) return cudaSuccess;
   gather_kept_kernel<<<dim3((k + 63) / 64, n_slices), 256, 0, st>>>(src, src_slot, kept, k, dst, dst_slot, n_slices, d);
+  return cudaGetLastError();
+}
+
+cudaError_t compact_dropped(KvPool src, int src_slot, const int32_t* kept, int k, int T, KvPool dst, int dst_slot,
+                            int n_slices, int d, cudaStream_t st) {
+  if (T <= 0 || n_slices <= 0) return cudaSuccess;
+  const size_t work = static_cast<size_t>(T) * (d / 8);
+  compact_dropped_kernel<<<dim3(static_cast<unsigned>(std::min<size_t>((work + 255) / 256, 1024)), n_slices), 256, 0,
+                           st>>>(src, src_slot, kept, k, T, dst, dst_slot, n_slices, d);
+  return cudaGetLastError();
+}
+
+cudaError_t expand_dropped(KvPool land, int land_slot, KvPool drop, int drop_slot, const int32_t* kept, int k, int T,
+                           int n, KvPool dst, int dst_slot, int n_slices, int d, cudaStream_t st) {
+  if (n <= 0 || n_slices <= 0) return cudaSuccess;
+  const size_t work = static_cast<size_t>(n) * (d / 8);
+  expand_dropped_kernel<<<dim3(static_cast<unsigned>(std::min<size_t>((work + 255) / 256, 1024)), n_slices), 256, 0,
+                          st>>>(land, land_slot, drop, drop_slot, kept, k, T, n, dst, dst_slot, n_slices, d);
   return cudaGetLastError();
 }
 

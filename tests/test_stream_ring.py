@@ -11,7 +11,10 @@ range-by-range verify bit-identical to the whole-window verify:
     round after round, with the ring smaller than the model's layer count
     (chunks recycled inside one verify) and two streams in flight;
   * the swap-scheduled loop over the ring emits exactly full-KV greedy decode;
-  * an aborted stream gives its chunks back."""
+  * an aborted stream gives its chunks back;
+  * over the drop-topk tier the host pool keeps only the dropped rows and a
+    reload moves (1 - c) of the prefix (analytics.cpp:77-78), the rest
+    rebuilt from the drop tier."""
 import dataclasses
 import time
 
@@ -143,9 +146,80 @@ def test_stream_ring_config_errors():
         Engine(TINY6, max_slots=2, max_ctx=600, max_x=8, quant_bits=4, full_tier=0, ring_chunks=4)
     with pytest.raises(_lib.ContractError):  # at least two chunks
         Engine(TINY6, max_slots=2, max_ctx=600, max_x=8, quant_bits=4, full_tier=1, n_stage=0, ring_chunks=1)
-    with pytest.raises(_lib.ContractError):  # the quantised compressed tier
-        Engine(TINY6, max_slots=2, max_ctx=600, max_x=8, quant_bits=0, drop_ratio=0.2, full_tier=1, n_stage=0,
-               ring_chunks=4)
+    with pytest.raises(_lib.ContractError):  # the drop tier only offline (no sliding window over appended rows)
+        Engine(TINY6, max_slots=2, max_ctx=600, max_x=8, quant_bits=0, drop_ratio=0.2, drop_window=64, full_tier=1,
+               n_stage=0, ring_chunks=4)
     with pytest.raises(_lib.ContractError):  # resident slots still need their stages
         Engine(TINY6, max_slots=3, max_ctx=600, max_x=8, quant_bits=4, full_tier=1, n_stage=1, resident_slots=2,
                ring_chunks=4)
+
+
+def _drop_engine(w, ring, slots=2):
+    if ring:
+        e = Engine(TINY6, max_slots=slots, max_ctx=2000, max_x=8, quant_bits=0, drop_ratio=0.25, full_tier=1,
+                   n_stage=0, ring_chunks=ring, max_streams=2, max_verify=4)
+    else:
+        e = Engine(TINY6, max_slots=slots, max_ctx=2000, max_x=8, quant_bits=0, drop_ratio=0.25, max_verify=4)
+    e.load_weights(w)
+    return e
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("ring", [2, 4])
+def test_drop_tier_stream_reloads_only_dropped_rows(cuda, w6, ring):
+    """Drop tier over the chunk ring: the host pool keeps only the dropped
+    rows, a streamed verify reloads (1 - c) of the full KV and rebuilds the
+    kept rows (and the rows accepted since compress) from the drop tier --
+    predictions and tokens equal the HBM-resident drop tier's, round by round."""
+    a, b = _drop_engine(w6, 0), _drop_engine(w6, ring)
+    for e in (a, b):
+        for s, n in enumerate(CTX):
+            e.add_synthetic(s, n, 17 + s, seed=1 + s)
+            e.compress(s)
+    for layer in (0, 5):  # the same kept sets
+        np.testing.assert_array_equal(a.drop_kept(layer, 1), b.drop_kept(layer, 1))
+    x = 5
+    for rnd in range(5):
+        for _ in range(x):
+            np.testing.assert_array_equal(a.draft([0, 1]), b.draft([0, 1]))
+        pa = a.verify([0, 1])
+        sids = [b.stream_begin(s) for s in (0, 1)]
+        got = [None, None]
+
+        def step():
+            for i, sid in enumerate(sids):
+                if got[i] is None:
+                    got[i] = b.stream_advance(sid, x)
+            return got if all(g is not None for g in got) else None
+        _until(step)
+        np.testing.assert_array_equal(np.concatenate(got), pa, err_msg=f"round {rnd}: predictions differ")
+        for s in (0, 1):
+            assert a.accept_commit(s, pa[s * (x + 1):(s + 1) * (x + 1)]) == b.stream_accept(s, sids[s]).tolist()
+    for s in (0, 1):
+        assert a.history(s) == b.history(s)
+        assert a.state(s)["drop_len"] == b.state(s)["drop_len"]
+    a.close()
+    b.close()
+
+
+@pytest.mark.gpu
+def test_drop_tier_ring_scheduled_lossless(cuda, w6):
+    n, K = 4, 40
+    ctx = [900 + 150 * s for s in range(n)]
+    ref = Engine(TINY6, max_slots=n, max_ctx=2000, max_x=1, quant_bits=0)
+    ref.load_weights(w6)
+    for s in range(n):
+        ref.add_synthetic(s, ctx[s], 17 + s, seed=1 + s)
+    base, _ = ref.autoregress(list(range(n)), K)
+    ref.close()
+    e = _drop_engine(w6, 3, slots=n)
+    for s in range(n):
+        e.add_synthetic(s, ctx[s], 17 + s, seed=1 + s)
+        e.compress(s)
+    out, st = e.run_scheduled(list(range(n)), K, x=6, window=32)
+    np.testing.assert_array_equal(out, base)
+    # every reload moved (1 - c) of the prefix: the dropped rows only
+    per_token = 2 * TINY6.layers * TINY6.n_kv * TINY6.d_head * 2
+    full = sum(ctx) / n * per_token
+    assert 0 < st["h2d_bytes"] <= 0.76 * full * st["verifies"]
+    e.close()
