@@ -91,3 +91,17 @@ def optimize_intra(hw: Hardware, weights: int, kv_full: int, batch: int, gamma_t
                 if best is None or v > best[0]:
                     best = (v, b_c, x, l)
     return best
+
+
+def composed_accept_length(x: int, gamma_x: float, d_e: int, gamma_e: float) -> float:
+    """Accepted tokens per verify of the two-level composition
+    (composed_accept_length, /root/reference/proj/src/analytics.cpp:413-422):
+    gamma * x * (1 + gamma_e * (d_e - 1)), gamma = the compressed model's
+    acceptance at x (expected_gamma), gamma_e = the auxiliary drafter's."""
+    if d_e < 1:
+        raise ValueError("composed_accept_length: d_e must be >= 1")
+    ge = 0.0 if d_e == 1 else gamma_e
+    if d_e > 1 and not 0.0 <= ge <= 1.0:
+        raise ValueError("composed_accept_length: gamma_e out of [0,1]")
+    return gamma_x * x * (1.0 + ge * (d_e - 1.0))
+

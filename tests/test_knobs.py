@@ -84,3 +84,13 @@ def test_optimize_intra_equals_reference(batch, kv, c):
     got = K.optimize_intra(B200, W8B, kv, batch, table, c)
     assert want > 0 and got is not None
     assert got == (want, bc.value, x.value, l.value)
+
+
+def test_composed_accept_length_matches_reference_formula():
+    """analytics.cpp:413-422: gamma * x * (1 + gamma_e * (d_e - 1)); d_e = 1 ignores gamma_e."""
+    from paper_2605_17613_b200 import knobs
+    assert knobs.composed_accept_length(8, 0.5, 1, 0.9) == 4.0
+    assert abs(knobs.composed_accept_length(6, 0.8, 3, 0.25) - 0.8 * 6 * 1.5) < 1e-12
+    import pytest
+    with pytest.raises(ValueError):
+        knobs.composed_accept_length(6, 0.8, 3, 1.5)
