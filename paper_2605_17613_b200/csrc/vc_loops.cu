@@ -233,6 +233,7 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
   double accepted_sum = 0;
   const auto t0 = std::chrono::steady_clock::now();
   const std::int64_t guard_iters = 10000 + 20LL * (sd.window + sd.x) + 64LL * sd.K * n_total;
+  std::int64_t idle_iters = 0;
 
   int64_t tokens_at_window = 0;
   double rows_in_window = 0;
@@ -252,7 +253,10 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
   auto t_prev = std::chrono::steady_clock::now();
   for (std::int64_t it = 0;
        !sched.idle() || !ev.arrivals.empty() || residents_active() || next_arr < n_arr || !queue.empty(); ++it) {
-    if (it > guard_iters) throw speckv::ConfigError("scheduled loop stalled");
+    // iterations that ran no step (every session waiting on the link) do not
+    // count toward the stall guard: a slow device (e.g. under a sanitizer)
+    // legitimately spins through many of them
+    if (it - idle_iters > guard_iters) throw speckv::ConfigError("scheduled loop stalled");
     if (n_arr > 0) {  // arrivals and admissions
       const double now_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
       while (next_arr < n_arr && sd.arrivals[next_arr].arrival_ms <= now_ms) {
@@ -471,7 +475,12 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
       }
     }
     std::vector<int32_t> row;
-    if (!items.empty()) en.run_step(items, row);
+    if (!items.empty()) {
+      en.run_step(items, row);
+    } else if (pr.verifies.empty()) {
+      ++idle_iters;
+      std::this_thread::sleep_for(std::chrono::microseconds(20));  // nothing to run: let the link progress
+    }
     if (it >= sd.warmup_iterations) {
       rows_in_window += static_cast<double>(row.size());
       for (const auto& t : items)
