@@ -859,12 +859,13 @@ def main():
         are reloaded per verify)."""
         # host tier x=47: the verify window plus 15 drafting rows stays within one
         # 64-row GEMM tile and the booked reloads saturate PCIe (link busy 0.99)
-        # HBM tier x=6: the measured optimum of an x sweep {4,6,8,10,12,16,24}
-        # (1398 / 1360 / 1343 / 1235 / 1045 tok/s at x = 6 / 8 / 12 / 16 / 24)
+        # HBM tier x=7: the measured optimum of an x sweep {5,6,7,8,10} on the
+        # round-2 kernels (1.362 / 1.393 / 1.409 / 1.326 / 1.284x), and the
+        # reference optimiser's choice (knobs.optimize_intra: x = 7)
         # configs[2] x=3: the measured optimum of {3,4,6,8,10,16,32,64} (397 / 389 /
         # 361 / 354 / 329 / 267 / 173 / 94 tok/s; the drop tier's acceptance on
         # synthetic KV falls fast with x); the long horizon x=32 is reported beside it
-        x = x_force or args.x or (47 if tier == 1 else (3 if cfg3 else 6))
+        x = x_force or args.x or (47 if tier == 1 else (3 if cfg3 else 7))
         window = args.window or max(2 * x + 8, 48 if tier == 0 else 256)
         ramp = 2 * (x + 1)  # warm-up includes two ramp rounds: every request has drafted and verified
         # a step = one speculative round: x+1 scheduler iterations (every request
