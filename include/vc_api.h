@@ -101,6 +101,11 @@ typedef struct {
                          token, summed over the GQA group, max-pooled; HBM full tier) */
   int snap_pool;      /* SnapKV max-pool width (0 -> 7) */
   int snap_recent;    /* SnapKV: last positions always kept (< 0 -> 32) */
+  int host_pack;      /* ring_chunks > 0, quantised tier: the host pool stores its
+                         128-token blocks losslessly packed (per-channel exponent
+                         base + 4-bit offsets + sign|mantissa bytes, escapes for
+                         outliers; ~0.76 of the bytes on the link).  0 = default (on),
+                         1 = on, -1 = off (raw bf16 rows) */
 } vc_runtime_desc;
 
 /* Mirrors speckv::CompressedKVMeta (compressor.hpp:56-65).  Quant-uniform:
@@ -243,6 +248,12 @@ int vc_update_window(int heads, int window, int sink_tokens, int n_req, const in
  * scores device [rows][T] fp32, kept device [rows][k] int32 ascending.    */
 int vc_topk_select(const float* scores, int rows, int T, int k, int32_t* kept, void* stream);
 /* Key-norm scores s_t = sum_c |k_tc| w_c for device bf16 keys [rows][T][d]. */
+/* Host-pool packing round trip (device pointers, tests): src bf16 [slices][n_rows][d]
+ * is packed per 128-token block (vc_pack.cu) and unpacked into out (same
+ * layout, rows padded to whole blocks); *overflow = 1 + the first block with
+ * more escapes than the format holds (0 = every block packed).             */
+int vc_pack_roundtrip(const uint16_t* src, int n_rows, int n_slices, int d, uint16_t* out, int* overflow,
+                      void* stream);
 int vc_key_scores(const uint16_t* keys, int rows, int T, int d, const float* w, float* scores,
                   void* stream);
 

@@ -45,7 +45,8 @@ class RuntimeDesc(C.Structure):
                 ("tp_size", C.c_int), ("tp_rank", C.c_int), ("drop_window", C.c_int),
                 ("resident_slots", C.c_int), ("draft_depth", C.c_int),
                 ("ring_chunks", C.c_int), ("max_streams", C.c_int),
-                ("drop_score", C.c_int), ("snap_pool", C.c_int), ("snap_recent", C.c_int)]
+                ("drop_score", C.c_int), ("snap_pool", C.c_int), ("snap_recent", C.c_int),
+                ("host_pack", C.c_int)]
 
 
 class CompressedMeta(C.Structure):
@@ -170,6 +171,7 @@ SIGNATURES = {
     "vc_update_window": (I, [I, I, I, I, PI64, PI64, PI64, PI64, PI64, I64, PI64]),
     "vc_topk_select": (I, [P, I, I, I, P, P]),
     "vc_key_scores": (I, [P, I, I, I, P, P, P]),
+    "vc_pack_roundtrip": (I, [P, I, I, I, P, PI, P]),
     "vc_argmax_rows": (I, [P, I, I, P, P]),
     "vc_step": (I, [P, C.POINTER(StepItem), I, PI32, PF]),
     "vc_decode_step": (I, [P, PI, I, PI32]),

@@ -99,6 +99,7 @@ int vc_engine_create(const vc_model_desc* model, const vc_runtime_desc* rt, int 
     c.drop_score = rt->drop_score;
     c.snap_pool = rt->snap_pool > 0 ? rt->snap_pool : 7;
     c.snap_recent = rt->snap_recent >= 0 ? rt->snap_recent : 32;
+    c.host_pack = rt->host_pack < 0 ? 0 : 1;
     if (c.drop_window < 0 || (c.drop_window > 0 && c.drop_ratio <= 0.0))
       throw speckv::ConfigError("compressor: drop_window needs the drop-topk compressor");
     c.tp_size = rt->tp_size > 1 ? rt->tp_size : 1;
@@ -494,6 +495,28 @@ int vc_topk_select(const float* scores, int rows, int T, int k, int32_t* kept, v
   return guard([&] {
     if (k < 1 || k > T) throw speckv::ConfigError("topk: k out of [1, T]");
     vc::check_cuda(vc::topk_select(scores, rows, T, k, kept, static_cast<cudaStream_t>(stream)), "topk_select");
+  });
+}
+
+int vc_pack_roundtrip(const uint16_t* src, int n_rows, int n_slices, int d, uint16_t* out, int* overflow,
+                      void* stream) {
+  return guard([&] {
+    auto st = static_cast<cudaStream_t>(stream);
+    const int nb = (n_rows + 127) / 128;
+    const size_t PB = vc::packed_block_bytes(d);
+    uint8_t* buf = nullptr;
+    int* ovf = nullptr;
+    vc::check_cuda(cudaMalloc(&buf, static_cast<size_t>(n_slices) * nb * PB), "cudaMalloc");
+    vc::check_cuda(cudaMalloc(&ovf, sizeof(int)), "cudaMalloc");
+    vc::check_cuda(cudaMemsetAsync(ovf, 0, sizeof(int), st), "memset");
+    vc::check_cuda(vc::pack_blocks(src, static_cast<size_t>(n_rows) * d, 0, n_rows, nb, n_slices, d, buf, nb * PB, ovf,
+                                   st), "pack_blocks");
+    vc::check_cuda(vc::unpack_blocks(buf, nb * PB, nb, n_slices, d, out, static_cast<size_t>(nb) * 128 * d, st),
+                   "unpack_blocks");
+    vc::check_cuda(cudaMemcpyAsync(overflow, ovf, sizeof(int), cudaMemcpyDeviceToHost, st), "copy");
+    vc::check_cuda(cudaStreamSynchronize(st), "sync");
+    cudaFree(buf);
+    cudaFree(ovf);
   });
 }
 

@@ -208,7 +208,8 @@ Engine::~Engine() {
   for (auto* evs : {&ring_start_, &ring_done_, &ring_free_, &ring_upload_, &ring_landed_})
     for (cudaEvent_t e : *evs) cudaEventDestroy(e);
   if (exp_st_) cudaStreamDestroy(exp_st_);
-  for (void* p : {static_cast<void*>(land_.k), static_cast<void*>(land_.v), static_cast<void*>(kept_all_)})
+  for (void* p : {static_cast<void*>(land_.k), static_cast<void*>(land_.v), static_cast<void*>(kept_all_),
+                  static_cast<void*>(pack_overflow_), static_cast<void*>(pack_stage_)})
     if (p) cudaFree(p);
   for (void* p : {static_cast<void*>(ring_.k), static_cast<void*>(ring_.v), static_cast<void*>(wbuf_.k),
                   static_cast<void*>(wbuf_.v), static_cast<void*>(xsave_), static_cast<void*>(sssave_),
@@ -495,12 +496,20 @@ void Engine::alloc_all() {
       VC_CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
       ring_upload_.push_back(e);
     }
-    if (drop_mode()) {
+    if (host_pack_on()) {
+      pack_overflow_ = dmalloc<int>(1);
+      pack_stage_ = dmalloc<uint8_t>(4 * static_cast<size_t>(L) * m.n_kv * packed_block_bytes(d));
+    }
+    if (drop_mode() || host_pack_on()) {
       const size_t chunk = static_cast<size_t>(m.n_kv) * ring_.cap * d;
       land_.cap = ring_.cap;
       land_.k = dmalloc<uint16_t>(static_cast<size_t>(cfg_.ring_chunks) * chunk);
       land_.v = dmalloc<uint16_t>(static_cast<size_t>(cfg_.ring_chunks) * chunk);
+    }
+    if (drop_mode()) {
       kept_all_ = dmalloc<int32_t>(static_cast<size_t>(cfg_.max_slots) * L * m.n_kv * kept_cap_);
+    }
+    if (drop_mode() || host_pack_on()) {
       for (int i = 0; i < cfg_.ring_chunks; ++i) {
         cudaEvent_t e;
         VC_CK(cudaEventCreate(&e));
@@ -643,6 +652,50 @@ void Engine::add_request_synthetic(int slot, int n_ctx, int32_t pending, uint64_
     const size_t pitch = slice_elems * 2;
     const size_t width = static_cast<size_t>(n_ctx) * m.d * 2;
     check_d2h();  // earlier commits into this slot's host rows land first
+    auto synth_layer = [&](int l, int c) {
+      const size_t total = static_cast<size_t>(n_ctx) * m.d * m.n_kv;
+      const int grid = static_cast<int>(std::min<size_t>((total + 255) / 256, 148 * 32));
+      synth_kv_kernel<<<grid, 256, 0, st_>>>(ring_.k + static_cast<size_t>(c) * m.n_kv * slice_elems,
+                                             ring_.v + static_cast<size_t>(c) * m.n_kv * slice_elems, full_.cap, n_ctx,
+                                             m.d, m.n_kv, seed, k_norm, k_out, period,
+                                             static_cast<size_t>(l) * m.n_kv * n_ctx * m.d);
+      VC_CK(cudaGetLastError());
+      ++launches_;
+    };
+    if (host_pack_on() && n_ctx > 0) {
+      // lossless packing: pass 1 finds the blocks every layer packs (a block
+      // with too many escapes is stored raw, and so is everything after it),
+      // pass 2 stores packed blocks + raw rows
+      const int nb = (n_ctx + VC_QGROUP - 1) / VC_QGROUP;
+      int P = nb;
+      const int ca = cfg_.ring_chunks, cb = cfg_.ring_chunks + 1;
+      for (int l = 0; l < m.layers; ++l) {
+        synth_layer(l, ca);
+        VC_CK(cudaMemsetAsync(pack_overflow_, 0, sizeof(int), st_));
+        for (int kv = 0; kv < 2; ++kv)
+          VC_CK(pack_blocks((kv ? ring_.v : ring_.k) + static_cast<size_t>(ca) * m.n_kv * slice_elems, slice_elems, 0,
+                            n_ctx, nb, m.n_kv, m.d,
+                            reinterpret_cast<uint8_t*>((kv ? ring_.v : ring_.k) + static_cast<size_t>(cb) * m.n_kv * slice_elems),
+                            pitch, pack_overflow_, st_));
+        int f = 0;
+        VC_CK(cudaMemcpyAsync(&f, pack_overflow_, sizeof(int), cudaMemcpyDeviceToHost, st_));
+        VC_CK(cudaStreamSynchronize(st_));
+        if (f > 0) P = std::min(P, f - 1);
+      }
+      for (int l = 0; l < m.layers; ++l) {
+        synth_layer(l, ca);
+        host_store_layer(slot, l, ca, cb, n_ctx, P);
+      }
+      SeqState& s = seqs_[slot];
+      s = SeqState{};
+      s.live = true;
+      s.committed = n_ctx;
+      s.pending = pending;
+      s.packed_blocks = P;
+      scratch_slot_ = -1;
+      VC_CK(cudaStreamSynchronize(st_));
+      return;
+    }
     for (int l = 0; l < m.layers && n_ctx > 0; ++l) {
       const int c = cfg_.ring_chunks + (l & 1);
       uint16_t* kb = ring_.k + static_cast<size_t>(c) * m.n_kv * slice_elems;
@@ -896,7 +949,10 @@ void Engine::compress_as(int slot, double ratio, const int32_t* kept_host, int k
       uint16_t* vb = ring_.v + static_cast<size_t>(c) * m.n_kv * slice_elems;
       VC_CK(cudaStreamWaitEvent(st_, ring_free_[c], 0));
       const size_t o = static_cast<size_t>(l) * m.n_kv * slice_elems;
-      if (width > 0) {
+      if (s.packed_blocks > 0) {
+        VC_CK(cudaStreamSynchronize(st_));  // the other admission chunk is the unpack scratch
+        host_load_layer(slot, l, c, cfg_.ring_chunks + ((l + 1) & 1), s.committed, s.packed_blocks);
+      } else if (width > 0) {
         VC_CK(cudaMemcpy2DAsync(kb, pitch, host_pool_k(slot) + o, pitch, width, m.n_kv, cudaMemcpyHostToDevice, st_));
         VC_CK(cudaMemcpy2DAsync(vb, pitch, host_pool_v(slot) + o, pitch, width, m.n_kv, cudaMemcpyHostToDevice, st_));
       }
@@ -1512,10 +1568,41 @@ std::vector<int32_t> Engine::accept_commit_from(int slot, const std::vector<int3
     const int n_slices = m.layers * m.n_kv;
     const size_t dpitch = static_cast<size_t>(full_.cap) * m.d * 2;
     const size_t spitch = static_cast<size_t>(src.pool.cap) * m.d * 2;
-    const size_t width = static_cast<size_t>(now - old) * m.d * 2;
-    uint16_t* hk = host_pool_k(slot) + static_cast<size_t>(old) * m.d;
-    uint16_t* hv = host_pool_v(slot) + static_cast<size_t>(old) * m.d;
-    const size_t soff = (static_cast<size_t>(src.slot) * n_slices * src.pool.cap + (old - src.origin)) * m.d;
+    int raw_from = old;  // rows [raw_from, now) go to the host raw
+    if (s.packed_blocks > 0 && old < s.packed_blocks * VC_QGROUP) {
+      // the window ends inside the packed prefix: re-pack its blocks from the
+      // exact rows (the block's earlier rows are in src too: origin is the
+      // residual group's start); a block that no longer packs ends the prefix
+      const int P = s.packed_blocks;
+      const int b0 = old / VC_QGROUP, b1 = std::min(P, (now + VC_QGROUP - 1) / VC_QGROUP);
+      if (src.origin > b0 * VC_QGROUP) throw ContractViolation("accept: exact rows do not cover the packed block");
+      const int nblk = b1 - b0;
+      const size_t PB = packed_block_bytes(m.d);
+      VC_CK(cudaStreamWaitEvent(st_, ev_d2h_, 0));  // the staging of the previous commit has left
+      VC_CK(cudaMemsetAsync(pack_overflow_, 0, sizeof(int), st_));
+      for (int kv = 0; kv < 2; ++kv)
+        VC_CK(pack_blocks((kv ? src.pool.v : src.pool.k) + static_cast<size_t>(src.slot) * n_slices * src.pool.cap * m.d,
+                          static_cast<size_t>(src.pool.cap) * m.d, b0 * VC_QGROUP - src.origin, now - b0 * VC_QGROUP,
+                          nblk, n_slices, m.d, pack_stage_ + kv * static_cast<size_t>(n_slices) * 2 * PB, nblk * PB,
+                          pack_overflow_, st_));
+      int f = 0;
+      VC_CK(cudaMemcpyAsync(&f, pack_overflow_, sizeof(int), cudaMemcpyDeviceToHost, st_));
+      VC_CK(cudaStreamSynchronize(st_));
+      const int newP = f > 0 ? b0 + f - 1 : P;
+      VC_CK(cudaEventRecord(ev_commit_, st_));
+      VC_CK(cudaStreamWaitEvent(d2h_st_, ev_commit_, 0));
+      if (newP > b0)
+        for (int kv = 0; kv < 2; ++kv)
+          VC_CK(cudaMemcpy2DAsync(reinterpret_cast<uint8_t*>(kv ? host_pool_v(slot) : host_pool_k(slot)) + b0 * PB,
+                                  dpitch, pack_stage_ + kv * static_cast<size_t>(n_slices) * 2 * PB, nblk * PB,
+                                  (newP - b0) * PB, n_slices, cudaMemcpyDeviceToHost, d2h_st_));
+      s.packed_blocks = newP;
+      raw_from = newP * VC_QGROUP;
+    }
+    const size_t width = static_cast<size_t>(std::max(0, now - raw_from)) * m.d * 2;
+    uint16_t* hk = host_pool_k(slot) + static_cast<size_t>(raw_from) * m.d;
+    uint16_t* hv = host_pool_v(slot) + static_cast<size_t>(raw_from) * m.d;
+    const size_t soff = (static_cast<size_t>(src.slot) * n_slices * src.pool.cap + (raw_from - src.origin)) * m.d;
     // on its own stream: a D2H on the compute stream would queue behind an
     // in-flight 4.29 GB reload in the copy engine and stall the next step for
     // the rest of that reload (measured: 91 ms steps after every offloaded
@@ -1523,8 +1610,11 @@ std::vector<int32_t> Engine::accept_commit_from(int slot, const std::vector<int3
     // for it through copy_st_.
     VC_CK(cudaEventRecord(ev_commit_, st_));
     VC_CK(cudaStreamWaitEvent(d2h_st_, ev_commit_, 0));
-    VC_CK(cudaMemcpy2DAsync(hk, dpitch, src.pool.k + soff, spitch, width, n_slices, cudaMemcpyDeviceToHost, d2h_st_));
-    VC_CK(cudaMemcpy2DAsync(hv, dpitch, src.pool.v + soff, spitch, width, n_slices, cudaMemcpyDeviceToHost, d2h_st_));
+    if (width > 0) {
+      if (raw_from < src.origin) throw ContractViolation("accept: exact rows start after the raw host rows");
+      VC_CK(cudaMemcpy2DAsync(hk, dpitch, src.pool.k + soff, spitch, width, n_slices, cudaMemcpyDeviceToHost, d2h_st_));
+      VC_CK(cudaMemcpy2DAsync(hv, dpitch, src.pool.v + soff, spitch, width, n_slices, cudaMemcpyDeviceToHost, d2h_st_));
+    }
     VC_CK(cudaEventRecord(ev_d2h_, d2h_st_));
     VC_CK(cudaStreamWaitEvent(copy_st_, ev_d2h_, 0));
   }
@@ -1784,6 +1874,67 @@ void Engine::swap_wait(uint64_t id) {
 // same booking drives chunk copies.  Batch invariance makes the range-by-range
 // forward bit-identical to a whole-window verify (same GEMM split per (N, K),
 // same 2048-key attention chunks, rows independent).
+// Host pool layout of a packed slot (per slice region of cap*d*2 bytes):
+// blocks [0, P) packed back to back at b * PB bytes, rows [128 P, ...) raw at
+// their natural row offset (128 P rows * d * 2 bytes >= P * PB: no overlap).
+void Engine::host_store_layer(int slot, int l, int craw, int cpk, int n, int P) {
+  const auto& m = cfg_.model;
+  const size_t slice_elems = static_cast<size_t>(full_.cap) * m.d;
+  const size_t pitch = slice_elems * 2;
+  const size_t o = static_cast<size_t>(l) * m.n_kv * slice_elems;
+  const size_t PB = packed_block_bytes(m.d);
+  const int r0 = std::min(n, P * VC_QGROUP);
+  for (int kv = 0; kv < 2; ++kv) {
+    uint16_t* raw = (kv ? ring_.v : ring_.k) + static_cast<size_t>(craw) * m.n_kv * slice_elems;
+    uint8_t* pk = reinterpret_cast<uint8_t*>((kv ? ring_.v : ring_.k) + static_cast<size_t>(cpk) * m.n_kv * slice_elems);
+    if (P > 0) VC_CK(pack_blocks(raw, slice_elems, 0, n, P, m.n_kv, m.d, pk, pitch, pack_overflow_, st_));
+  }
+  VC_CK(cudaEventRecord(ev_commit_, st_));
+  VC_CK(cudaStreamWaitEvent(d2h_st_, ev_commit_, 0));
+  for (int kv = 0; kv < 2; ++kv) {
+    uint16_t* host = (kv ? host_pool_v(slot) : host_pool_k(slot)) + o;
+    uint16_t* raw = (kv ? ring_.v : ring_.k) + static_cast<size_t>(craw) * m.n_kv * slice_elems;
+    uint8_t* pk = reinterpret_cast<uint8_t*>((kv ? ring_.v : ring_.k) + static_cast<size_t>(cpk) * m.n_kv * slice_elems);
+    if (P > 0)
+      VC_CK(cudaMemcpy2DAsync(host, pitch, pk, pitch, P * PB, m.n_kv, cudaMemcpyDeviceToHost, d2h_st_));
+    if (n > r0)
+      VC_CK(cudaMemcpy2DAsync(host + static_cast<size_t>(r0) * m.d, pitch, raw + static_cast<size_t>(r0) * m.d, pitch,
+                              static_cast<size_t>(n - r0) * m.d * 2, m.n_kv, cudaMemcpyDeviceToHost, d2h_st_));
+  }
+  VC_CK(cudaStreamSynchronize(d2h_st_));  // both chunks are reused by the next layer
+}
+
+void Engine::host_load_layer(int slot, int l, int craw, int cpk, int n, int P) {
+  const auto& m = cfg_.model;
+  const size_t slice_elems = static_cast<size_t>(full_.cap) * m.d;
+  const size_t pitch = slice_elems * 2;
+  const size_t o = static_cast<size_t>(l) * m.n_kv * slice_elems;
+  const size_t PB = packed_block_bytes(m.d);
+  const int r0 = std::min(n, P * VC_QGROUP);
+  for (int kv = 0; kv < 2; ++kv) {
+    const uint16_t* host = (kv ? host_pool_v(slot) : host_pool_k(slot)) + o;
+    uint16_t* raw = (kv ? ring_.v : ring_.k) + static_cast<size_t>(craw) * m.n_kv * slice_elems;
+    uint8_t* pk = reinterpret_cast<uint8_t*>((kv ? ring_.v : ring_.k) + static_cast<size_t>(cpk) * m.n_kv * slice_elems);
+    if (P > 0) {
+      VC_CK(cudaMemcpy2DAsync(pk, pitch, host, pitch, P * PB, m.n_kv, cudaMemcpyHostToDevice, st_));
+      VC_CK(unpack_blocks(pk, pitch, P, m.n_kv, m.d, raw, slice_elems, st_));
+    }
+    if (n > r0)
+      VC_CK(cudaMemcpy2DAsync(raw + static_cast<size_t>(r0) * m.d, pitch, host + static_cast<size_t>(r0) * m.d, pitch,
+                              static_cast<size_t>(n - r0) * m.d * 2, m.n_kv, cudaMemcpyHostToDevice, st_));
+  }
+}
+
+double Engine::reload_bytes(int slot) const {
+  const auto& m = cfg_.model;
+  const SeqState& s = seqs_.at(slot);
+  const double slices = 2.0 * m.layers * m.n_kv;  // K and V
+  if (ring_mode() && drop_mode()) return slices * (s.drop_T - s.drop_base) * m.d * 2.0;
+  const int r0 = std::min(s.committed, s.packed_blocks * VC_QGROUP);
+  return slices * (static_cast<double>(s.packed_blocks) * packed_block_bytes(m.d) +
+                   static_cast<double>(s.committed - r0) * m.d * 2.0);
+}
+
 size_t Engine::staging_bytes() const {
   const auto& m = cfg_.model;
   const size_t slab = static_cast<size_t>(m.n_kv) * full_.cap * m.d * 2 * 2;  // one layer, K and V
@@ -1860,6 +2011,30 @@ void Engine::stream_issue_chunk(VStream& v) {
                          k, T, v.committed, ring_, c, m.n_kv, m.d, exp_st_));
     ++launches_;
     VC_CK(cudaEventRecord(ring_done_[c], exp_st_));
+  } else if (seqs_.at(v.slot).packed_blocks > 0) {
+    // packed blocks land in land_[c] and are unpacked into the chunk on the
+    // rebuild stream; the raw tail rows go straight into the chunk
+    const int P = seqs_.at(v.slot).packed_blocks;
+    const int r0 = std::min(v.committed, P * VC_QGROUP);
+    const size_t PB = packed_block_bytes(m.d);
+    for (int kv = 0; kv < 2; ++kv) {
+      const uint16_t* host = (kv ? host_pool_v(v.slot) : host_pool_k(v.slot)) + o;
+      uint8_t* lp = reinterpret_cast<uint8_t*>((kv ? land_.v : land_.k) + static_cast<size_t>(c) * m.n_kv * slice_elems);
+      uint16_t* dst = kv ? dv : dk;
+      VC_CK(cudaMemcpy2DAsync(lp, pitch, host, pitch, P * PB, m.n_kv, cudaMemcpyHostToDevice, copy_st_));
+      if (v.committed > r0)
+        VC_CK(cudaMemcpy2DAsync(dst + static_cast<size_t>(r0) * m.d, pitch, host + static_cast<size_t>(r0) * m.d, pitch,
+                                static_cast<size_t>(v.committed - r0) * m.d * 2, m.n_kv, cudaMemcpyHostToDevice,
+                                copy_st_));
+    }
+    VC_CK(cudaEventRecord(ring_landed_[c], copy_st_));
+    VC_CK(cudaStreamWaitEvent(exp_st_, ring_landed_[c], 0));
+    for (int kv = 0; kv < 2; ++kv)
+      VC_CK(unpack_blocks(reinterpret_cast<const uint8_t*>((kv ? land_.v : land_.k) +
+                                                          static_cast<size_t>(c) * m.n_kv * slice_elems),
+                          pitch, P, m.n_kv, m.d, kv ? dv : dk, slice_elems, exp_st_));
+    launches_ += 2;
+    VC_CK(cudaEventRecord(ring_done_[c], exp_st_));
   } else {
     if (width > 0) {
       VC_CK(cudaMemcpy2DAsync(dk, pitch, host_pool_k(v.slot) + o, pitch, width, m.n_kv, cudaMemcpyHostToDevice, copy_st_));
@@ -1906,11 +2081,18 @@ int Engine::stream_advance(int id) {
     if (e == cudaErrorNotReady) break;
     check_cuda(e, "stream chunk");
     float ms = 0.f;
-    VC_CK(cudaEventElapsedTime(&ms, ring_start_[c], drop_mode() ? ring_landed_[c] : ring_done_[c]));
-    h2d_ms_ += ms;
     const SeqState& s = seqs_.at(v.slot);
-    const int rows = drop_mode() ? s.drop_T - s.drop_base : v.committed;
-    h2d_bytes_ += 2.0 * static_cast<double>(rows) * m.d * 2 * m.n_kv;
+    const bool rebuilt = drop_mode() || s.packed_blocks > 0;  // the link time ends when the rows landed
+    VC_CK(cudaEventElapsedTime(&ms, ring_start_[c], rebuilt ? ring_landed_[c] : ring_done_[c]));
+    h2d_ms_ += ms;
+    if (drop_mode()) {
+      h2d_bytes_ += 2.0 * static_cast<double>(s.drop_T - s.drop_base) * m.d * 2 * m.n_kv;
+    } else {
+      const int r0 = std::min(v.committed, s.packed_blocks * VC_QGROUP);
+      h2d_bytes_ += 2.0 * m.n_kv *
+                    (static_cast<double>(s.packed_blocks) * packed_block_bytes(m.d) +
+                     static_cast<double>(v.committed - r0) * m.d * 2);
+    }
     ++v.landed;
   }
   if (v.landed > v.done) {

@@ -64,6 +64,9 @@ struct EngineConfig {
   // n_stage whole requests.  n_stage then holds the resident slots only.
   int ring_chunks = 0;
   int max_streams = 2;  // streamed verifies in flight (saved hidden state + exact window rows each)
+  // chunk ring over the quantised tier: store the host pool's 128-token
+  // blocks losslessly packed (vc_pack.cu, ~0.76 of the bytes on the link)
+  int host_pack = 1;
   // drop-topk token scores: 0 = L1 norm of the post-RoPE key; 1 = SnapKV
   // (Li et al., 2024): attention of the observation query (the request's
   // pending token, one decode-shaped forward over the full KV) summed over the
@@ -94,6 +97,7 @@ struct SeqState {
   int drop_len = 0;       // drop tier: kept prefix tokens + exact tokens appended since
   int drop_base = 0;      // drop tier: rows of the compress-time kept prefix
   int drop_T = 0;         // drop tier: positions the compress covered (kept + dropped)
+  int packed_blocks = 0;  // host tier (chunk ring): leading 128-token blocks stored packed, the rest raw
   std::vector<int32_t> drafted;
   std::vector<int32_t> history;  // every emitted token
 };
@@ -187,6 +191,9 @@ class Engine {
   bool ring_mode() const { return cfg_.full_tier == 1 && cfg_.ring_chunks > 0; }
   // HBM bytes of the host tier's staging: rotating slots, or the chunk ring
   size_t staging_bytes() const;
+  // bytes a reload of the slot's committed full KV moves over the link
+  // (packed blocks + raw rows, or the drop tier's dropped rows, or raw)
+  double reload_bytes(int slot) const;
   // ---- remote prefix (configs[3]) -------------------------------------
   // The storage node's precomputed KV of one shared prefix: slot's committed
   // full KV and its compressed image (quant tier) snapshotted into pinned
@@ -288,6 +295,13 @@ class Engine {
     std::vector<int32_t> preds;
   };
   void stream_issue_chunk(VStream& v);
+  bool host_pack_on() const { return ring_mode() && !drop_mode() && cfg_.host_pack > 0; }
+  // the slot's host rows of layer l (n_kv slices, rows [0, n)): raw chunk
+  // `craw` -> host pool, blocks [0, P) packed through chunk `cpk`; and back
+  void host_store_layer(int slot, int l, int craw, int cpk, int n, int P);
+  void host_load_layer(int slot, int l, int craw, int cpk, int n, int P);
+  int* pack_overflow_ = nullptr;              // device: 1 + first block that did not pack (0 = all packed)
+  uint8_t* pack_stage_ = nullptr;             // accept-time packing of the window's block: [2][layers*n_kv][PB]
   void stream_range(VStream& v, int a, int b);
   void ring_fill_layer(int slot, int layer, int chunk, bool from_host);
   void compress_drop(int slot, const KvPool& src, int src_slot, double ratio, const int32_t* kept_host,

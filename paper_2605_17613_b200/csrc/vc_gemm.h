@@ -103,6 +103,21 @@ cudaError_t compact_dropped(KvPool src, int src_slot, const int32_t* kept, int k
                             int n_slices, int d, cudaStream_t st);
 cudaError_t expand_dropped(KvPool land, int land_slot, KvPool drop, int drop_slot, const int32_t* kept, int k, int T,
                            int n, KvPool dst, int dst_slot, int n_slices, int d, cudaStream_t st);
+// Lossless packing of 128-token bf16 blocks (vc_pack.cu): per channel an
+// exponent base, per value a 4-bit exponent offset + sign|mantissa byte,
+// escapes for values more than 14 binades below their channel's maximum.
+constexpr int kPackEscCap = 60;
+__host__ __device__ constexpr size_t packed_block_bytes(int d) {
+  return (static_cast<size_t>(d) + 128u * d / 2 + 128u * d + 4 + 4u * kPackEscCap + 15) / 16 * 16;
+}
+// src rows [src_row0 + 128 b, ...) of each slice (slice pitch in elements),
+// n_valid rows from src_row0 (the last block may be partial); dst packed
+// block b of slice s at dst + s * dst_slice_pitch + b * packed_block_bytes(d)
+// (bytes).  *overflow = max(1 + block) over blocks with > kPackEscCap escapes.
+cudaError_t pack_blocks(const uint16_t* src, size_t src_slice_pitch, int src_row0, int n_valid, int n_blocks,
+                        int n_slices, int d, uint8_t* dst, size_t dst_slice_pitch, int* overflow, cudaStream_t st);
+cudaError_t unpack_blocks(const uint8_t* src, size_t src_slice_pitch, int n_blocks, int n_slices, int d, uint16_t* dst,
+                          size_t dst_slice_pitch, cudaStream_t st);
 // Copy token rows [src_pos, src_pos+n) of every slice to [dst_pos, dst_pos+n).
 cudaError_t copy_rows(KvPool src, int src_slot, int src_pos, int n, KvPool dst, int dst_slot, int dst_pos,
                       int n_slices, int d, cudaStream_t st);

@@ -97,7 +97,18 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
     for (int r = 0; r < 3; ++r) en.run_step(probe, o);
     t_iter = std::chrono::duration<double>(std::chrono::steady_clock::now() - a).count() / 3;
   }
-  const double bw = sd.link_bandwidth > 0 ? sd.link_bandwidth : (staged ? 55e9 : 1e15);
+  double bw = sd.link_bandwidth > 0 ? sd.link_bandwidth : (staged ? 55e9 : 1e15);
+  if (staged && en.ring_mode()) {
+    // the scheduler books reloads in full-KV bytes (scheduler.cpp:96-163);
+    // a packed or drop-tier reload moves fewer: plan with the effective rate
+    double raw = 0.0, moved = 0.0;
+    for (int i = 0; i < n; ++i)
+      if (!en.resident(slots[i])) {
+        raw += static_cast<double>(en.seq(slots[i]).committed) * bpt;
+        moved += en.reload_bytes(slots[i]);
+      }
+    if (moved > 0.0 && raw > moved) bw *= raw / moved;
+  }
 
   // ---- SystemConfig of this serving instance ------------------------------
   speckv::SystemConfig cfg;

@@ -103,7 +103,7 @@ class Engine:
     def __init__(self, model: ModelShape, *, max_slots=1, max_ctx=4096, max_x=16, quant_bits=4,
                  full_tier=0, n_stage=2, max_verify=2, use_graphs=True, device=0, drop_ratio=0.0,
                  tp_size=1, tp_rank=0, drop_window=0, resident_slots=0, draft_depth=1,
-                 ring_chunks=0, max_streams=2, drop_score="norm", snap_pool=7, snap_recent=32):
+                 ring_chunks=0, max_streams=2, drop_score="norm", snap_pool=7, snap_recent=32, host_pack=True):
         """quant_bits > 0: quant-uniform compressor (KIVI int4/int2);
         drop_ratio in (0, 1): drop-topk compressor keeping llround(c*T) tokens per
         (layer, head) -- the two are exclusive (compressor.cpp:245-254).
@@ -120,7 +120,9 @@ class Engine:
         drop_score (drop-topk): "norm" = L1 norm of the post-RoPE key; "snapkv" =
         SnapKV observation-window attention (the pending token's query over the
         full KV, summed over the GQA group, max-pooled over snap_pool positions,
-        the last snap_recent positions always kept)."""
+        the last snap_recent positions always kept).
+        host_pack (ring_chunks > 0, quantised tier): the host pool's 128-token
+        blocks are stored losslessly packed (~0.76 of the link bytes per reload)."""
         if drop_score not in ("norm", "snapkv"):
             raise ValueError("drop_score is 'norm' or 'snapkv'")
         self.lib = _lib.load()
@@ -132,7 +134,7 @@ class Engine:
                               max_verify, int(use_graphs), float(drop_ratio), int(tp_size), int(tp_rank),
                               int(drop_window), int(resident_slots), int(draft_depth),
                               int(ring_chunks), int(max_streams), 1 if drop_score == "snapkv" else 0,
-                              int(snap_pool), int(snap_recent))
+                              int(snap_pool), int(snap_recent), 1 if host_pack else -1)
         self.tp_size, self.tp_rank = int(tp_size), int(tp_rank)
         h = C.c_void_p()
         check(self.lib.vc_engine_create(C.byref(md), C.byref(rt), device, C.byref(h)))

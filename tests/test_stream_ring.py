@@ -15,6 +15,7 @@ range-by-range verify bit-identical to the whole-window verify:
   * over the drop-topk tier the host pool keeps only the dropped rows and a
     reload moves (1 - c) of the prefix (analytics.cpp:77-78), the rest
     rebuilt from the drop tier."""
+import ctypes as C
 import dataclasses
 import time
 
@@ -36,7 +37,7 @@ def w6():
 def _engine(w, ring, **kw):
     if ring:
         e = Engine(TINY6, max_slots=kw.get("slots", 2), max_ctx=2000, max_x=8, quant_bits=4, full_tier=1,
-                   n_stage=0, ring_chunks=ring, max_streams=2, max_verify=4)
+                   n_stage=0, ring_chunks=ring, max_streams=2, max_verify=4, host_pack=kw.get("pack", True))
     else:
         e = Engine(TINY6, max_slots=kw.get("slots", 2), max_ctx=2000, max_x=8, quant_bits=4, full_tier=1,
                    n_stage=3, max_verify=4)
@@ -54,9 +55,9 @@ def _until(fn, timeout=30.0):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("ring", [2, 3, 8])
-def test_streamed_verify_equals_staged_verify(cuda, w6, ring):
-    a, b = _engine(w6, 0), _engine(w6, ring)
+@pytest.mark.parametrize("ring,pack", [(2, True), (3, False), (8, True)])
+def test_streamed_verify_equals_staged_verify(cuda, w6, ring, pack):
+    a, b = _engine(w6, 0), _engine(w6, ring, pack=pack)
     for e in (a, b):
         for s, n in enumerate(CTX):
             e.add_synthetic(s, n, 17 + s, seed=1 + s)
@@ -117,8 +118,59 @@ def test_stream_ring_scheduled_lossless(cuda, w6):
     np.testing.assert_array_equal(out, base)
     assert st["verifies"] > 0 and st["h2d_bytes"] > 0
     layer_bytes = 2 * TINY6.n_kv * 2048 * TINY6.d_head * 2  # K and V of one layer at cap 2048
-    assert st["staging_bytes"] == e.staging_bytes() == (3 + 2) * layer_bytes
+    # the ring + 2 admission chunks, and the landing chunks the packed blocks arrive in
+    assert st["staging_bytes"] == e.staging_bytes() == (3 + 2 + 3) * layer_bytes
+    # packed host pool: a reload moves ~0.76 of the raw bytes
+    per_token = 2 * TINY6.layers * TINY6.n_kv * TINY6.d_head * 2
+    raw = (900 + 150 * 1.5) * per_token  # mean prefix
+    assert st["h2d_bytes"] <= 0.80 * raw * st["verifies"] * 1.1
     e.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("d", [64, 128])
+@pytest.mark.parametrize("n_rows", [1, 100, 128, 300])
+def test_pack_roundtrip_bit_exact(cuda, d, n_rows):
+    """The host pool's lossless packing (vc_pack.cu) restores every bf16 bit:
+    normal values, outlier channels (x1000), a few zeros / subnormals / tiny
+    values (escapes), partial last blocks.  (A channel holding inf or NaN
+    escapes every other value of the block: overflow, stored raw.)"""
+    torch = cuda
+    rng = np.random.default_rng(n_rows + d)
+    slices = 3
+    x = rng.standard_normal((slices, n_rows, d)).astype(np.float32)
+    x[:, :, 5] *= 1000.0  # an outlier channel
+    x[0, : min(3, n_rows), 7] = 0.0
+    x[1, 0, 9] = 1e-39  # subnormal
+    x[1, 0, 10] = 1e-30  # far below the channel's maximum
+    bits = T.f32_to_bf16(x)
+    src = torch.from_numpy(bits.view(np.int16).copy()).cuda()
+    nb = (n_rows + 127) // 128
+    out = torch.zeros((slices, nb * 128, d), dtype=torch.int16, device="cuda")
+    ovf = C.c_int(-1)
+    lib = _lib.load()
+    assert lib.vc_pack_roundtrip(src.data_ptr(), n_rows, slices, d, out.data_ptr(), C.byref(ovf),
+                                 torch.cuda.current_stream().cuda_stream) == 0
+    assert ovf.value == 0
+    got = out.cpu().numpy().view(np.uint16)[:, :n_rows]
+    np.testing.assert_array_equal(got, bits)
+
+
+@pytest.mark.gpu
+def test_pack_overflow_is_reported(cuda):
+    """A block with more escapes than the format holds (here: one channel
+    whose values are all zero but one) reports overflow: the engine stores it
+    raw.  (An all-zero channel packs: its exponent base is 0.)"""
+    torch = cuda
+    x = np.random.default_rng(0).standard_normal((1, 128, 128)).astype(np.float32)
+    x[0, 1:, 3] = 0.0
+    src = torch.from_numpy(T.f32_to_bf16(x).view(np.int16).copy()).cuda()
+    out = torch.zeros_like(src)
+    ovf = C.c_int(0)
+    lib = _lib.load()
+    assert lib.vc_pack_roundtrip(src.data_ptr(), 128, 1, 128, out.data_ptr(), C.byref(ovf),
+                                 torch.cuda.current_stream().cuda_stream) == 0
+    assert ovf.value == 1  # 1 + block 0
 
 
 @pytest.mark.gpu
