@@ -278,6 +278,11 @@ def choose_placement(runs, B, base_ms_per_step, bits, weights):
     bw_hbm = (weights + B * kv) / (base_ms_per_step / 1e3)
     s = host["st"]
     bw_inter = s["h2d_bytes"] / max(s["h2d_ms"] / 1e3, 1e-9)
+    # a packed host pool moves fewer bytes than the full KV the model charges:
+    # the model's link rate is the full-KV bytes per second the link delivers
+    moved_over_raw = s["h2d_bytes"] / max(s["verifies"] * kv, 1.0)
+    if 0.5 < moved_over_raw < 1.0:
+        bw_inter /= moved_over_raw
     gpu_mem = int(torch.cuda.mem_get_info()[1])
     gtab, gsrc = gamma_table(bits)
     hw = knobs.Hardware(bw_hbm, bw_inter, gpu_mem)
@@ -285,7 +290,8 @@ def choose_placement(runs, B, base_ms_per_step, bits, weights):
     pred_host = knobs.intra_throughput(B, host["x"], c, 1, hw, weights, kv, B, gtab)
     return {"model": "intra_throughput / optimize_intra (analytics.cpp:45-150) restated in "
                      "paper_2605_17613_b200/knobs.py, equal to oracle/_ref (tests/test_knobs.py)",
-            "constants": {"hbm_gbs": round(bw_hbm / 1e9, 1), "h2d_gbs": round(bw_inter / 1e9, 2), "c": round(c, 4),
+            "constants": {"hbm_gbs": round(bw_hbm / 1e9, 1), "h2d_full_kv_gbs": round(bw_inter / 1e9, 2),
+                          "reload_bytes_over_full_kv": round(moved_over_raw, 4), "c": round(c, 4),
                           "gpu_mem": gpu_mem, "weights_read": weights, "kv_full": kv, "gamma_source": gsrc},
             "optimizer": {"B_c": best[1], "x": best[2], "l": best[3], "predicted_tok_s": round(best[0], 1)},
             "predicted_host_tier_tok_s": round(pred_host, 1) if pred_host else None,
