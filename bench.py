@@ -280,8 +280,8 @@ def choose_placement(runs, B, base_ms_per_step, bits, weights):
     bw_inter = s["h2d_bytes"] / max(s["h2d_ms"] / 1e3, 1e-9)
     # a packed host pool moves fewer bytes than the full KV the model charges:
     # the model's link rate is the full-KV bytes per second the link delivers
-    moved_over_raw = s["h2d_bytes"] / max(s["verifies"] * kv, 1.0)
-    if 0.5 < moved_over_raw < 1.0:
+    moved_over_raw = s["reload_over_full"]
+    if 0.0 < moved_over_raw < 1.0:
         bw_inter /= moved_over_raw
     gpu_mem = int(torch.cuda.mem_get_info()[1])
     gtab, gsrc = gamma_table(bits)
@@ -1022,7 +1022,8 @@ def main():
                                      f"{args.streams} streamed verifies in flight" if args.ring and not drop
                                      else f"{args.stages} whole-request staging slots"),
                          "staging_hbm_bytes": int(s["staging_bytes"]),
-                         "bytes_per_reload": int(r["meta"]["full_bytes"])}
+                         "bytes_per_reload": int(r["meta"]["full_bytes"]),
+                         "reload_bytes_over_full_kv": round(s["reload_over_full"], 4)}
         return d
 
     def reference_csv():

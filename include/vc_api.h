@@ -432,6 +432,8 @@ typedef struct {
   int64_t drafted_tokens;   /* tokens that entered verify windows (composition: > draft iterations) */
   int64_t aux_proposed;     /* composition: auxiliary tokens offered to the compressed model */
   int64_t aux_accepted;     /* of those, confirmed by it (gamma_e = accepted / proposed) */
+  double reload_over_full;  /* bytes a reload moves / the full KV it restores (packed host
+                               pool ~0.76, drop tier 1-c, raw 1), over the offloaded requests */
 } vc_sched_stats;
 
 /* Reference metrics of a loop (SimMetrics, sim.hpp:52-74) on the engine:

@@ -97,7 +97,7 @@ class SchedStats(C.Structure):
                 ("warm_throughput", C.c_double), ("p50_latency_s", C.c_double), ("p99_latency_s", C.c_double),
                 ("interconnect_busy", C.c_double), ("peak_hbm_bytes", C.c_int64),
                 ("staging_bytes", C.c_int64), ("drafted_tokens", C.c_int64),
-                ("aux_proposed", C.c_int64), ("aux_accepted", C.c_int64)]
+                ("aux_proposed", C.c_int64), ("aux_accepted", C.c_int64), ("reload_over_full", C.c_double)]
 
 
 class LoopMetrics(C.Structure):

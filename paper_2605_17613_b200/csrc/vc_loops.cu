@@ -98,6 +98,7 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
     t_iter = std::chrono::duration<double>(std::chrono::steady_clock::now() - a).count() / 3;
   }
   double bw = sd.link_bandwidth > 0 ? sd.link_bandwidth : (staged ? 55e9 : 1e15);
+  double reload_over_full = 1.0;
   if (staged && en.ring_mode()) {
     // the scheduler books reloads in full-KV bytes (scheduler.cpp:96-163);
     // a packed or drop-tier reload moves fewer: plan with the effective rate
@@ -108,6 +109,7 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
         moved += en.reload_bytes(slots[i]);
       }
     if (moved > 0.0 && raw > moved) bw *= raw / moved;
+    if (raw > 0.0) reload_over_full = moved / raw;
   }
 
   // ---- SystemConfig of this serving instance ------------------------------
@@ -241,6 +243,7 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
     return !(v && v[0] == '0');
   }();
   vc_sched_stats st{};
+  st.reload_over_full = reload_over_full;
   double accepted_sum = 0;
   const auto t0 = std::chrono::steady_clock::now();
   const std::int64_t guard_iters = 10000 + 20LL * (sd.window + sd.x) + 64LL * sd.K * n_total;
