@@ -248,6 +248,7 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
   const auto t0 = std::chrono::steady_clock::now();
   const std::int64_t guard_iters = 10000 + 20LL * (sd.window + sd.x) + 64LL * sd.K * n_total;
   std::int64_t idle_iters = 0;
+  auto last_progress = std::chrono::steady_clock::now();
 
   int64_t tokens_at_window = 0;
   double rows_in_window = 0;
@@ -271,6 +272,8 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
     // count toward the stall guard: a slow device (e.g. under a sanitizer)
     // legitimately spins through many of them
     if (it - idle_iters > guard_iters) throw speckv::ConfigError("scheduled loop stalled");
+    if (std::chrono::duration<double>(std::chrono::steady_clock::now() - last_progress).count() > 120.0)
+      throw speckv::ConfigError("scheduled loop stalled (no step, verify or transfer for 120 s)");
     if (n_arr > 0) {  // arrivals and admissions
       const double now_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
       while (next_arr < n_arr && sd.arrivals[next_arr].arrival_ms <= now_ms) {
@@ -288,7 +291,8 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
         const int slot = free_slots.front();
         const bool res = en.resident(slot);
         int scratch = -1;
-        if (staged && !res) {  // an offloaded admission borrows a free rotating stage
+        if (staged && !res && !ring) {  // an offloaded admission borrows a free rotating stage
+          // (the chunk ring admits through its own two admission chunks)
           if (free_stages.empty()) break;
           scratch = free_stages.back();
           free_stages.pop_back();
@@ -489,6 +493,8 @@ int vc_run_scheduled_impl(vc::Engine& en, const int* slots, int n, const vc_sche
       }
     }
     std::vector<int32_t> row;
+    if (!items.empty() || !pr.verifies.empty() || !ev.completed_transfers.empty())
+      last_progress = std::chrono::steady_clock::now();
     if (!items.empty()) {
       en.run_step(items, row);
     } else if (pr.verifies.empty()) {

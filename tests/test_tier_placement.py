@@ -123,8 +123,8 @@ def test_fifo_baseline_arrivals(cuda, weights):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("tier,resident", [(0, 0), (1, 1), (1, 0)])
-def test_scheduled_loop_with_arrivals(cuda, weights, tier, resident):
+@pytest.mark.parametrize("tier,resident,ring", [(0, 0, 0), (1, 1, 0), (1, 0, 0), (1, 0, 2), (1, 1, 3)])
+def test_scheduled_loop_with_arrivals(cuda, weights, tier, resident, ring):
     """Requests arriving during the run take the slots finished ones free
     (simulate_staggered's arrivals, sim.cpp:227-302); every request, initial
     or arrived, emits exactly its own full-KV greedy decode."""
@@ -136,7 +136,10 @@ def test_scheduled_loop_with_arrivals(cuda, weights, tier, resident):
         ref.add_synthetic(i, ctx, tok, seed=seed)
     base, _ = ref.autoregress(list(range(n + n_arr)), K)
     ref.close()
-    kw = dict(full_tier=1, n_stage=resident + 2, resident_slots=resident) if tier else {}
+    # ring > 0: the chunk ring (packed host pool); admissions of arrivals
+    # pack and store through the admission chunks while streams are in flight
+    kw = (dict(full_tier=1, n_stage=resident + (0 if ring else 2), resident_slots=resident, ring_chunks=ring)
+          if tier else {})
     e = Engine(TINY, max_slots=n, max_ctx=N_CTX + 400, max_x=16, quant_bits=4, max_verify=4, **kw)
     e.load_weights(weights)
     for i in range(n):
