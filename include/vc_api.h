@@ -105,7 +105,8 @@ typedef struct {
                          128-token blocks losslessly packed (per-channel exponent
                          base + 4-bit offsets + sign|mantissa bytes, escapes for
                          outliers; ~0.76 of the bytes on the link).  0 = default (on),
-                         1 = on, -1 = off (raw bf16 rows) */
+                         1 = on, -1 = off (raw bf16 rows); k >= 2 = on with at most
+                         k-1 packed blocks per request (tests the raw-tail path) */
 } vc_runtime_desc;
 
 /* Mirrors speckv::CompressedKVMeta (compressor.hpp:56-65).  Quant-uniform:

@@ -99,7 +99,7 @@ int vc_engine_create(const vc_model_desc* model, const vc_runtime_desc* rt, int 
     c.drop_score = rt->drop_score;
     c.snap_pool = rt->snap_pool > 0 ? rt->snap_pool : 7;
     c.snap_recent = rt->snap_recent >= 0 ? rt->snap_recent : 32;
-    c.host_pack = rt->host_pack < 0 ? 0 : 1;
+    c.host_pack = rt->host_pack < 0 ? 0 : (rt->host_pack >= 2 ? rt->host_pack : 1);
     if (c.drop_window < 0 || (c.drop_window > 0 && c.drop_ratio <= 0.0))
       throw speckv::ConfigError("compressor: drop_window needs the drop-topk compressor");
     c.tp_size = rt->tp_size > 1 ? rt->tp_size : 1;

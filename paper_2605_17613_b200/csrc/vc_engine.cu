@@ -682,6 +682,7 @@ void Engine::add_request_synthetic(int slot, int n_ctx, int32_t pending, uint64_
         VC_CK(cudaStreamSynchronize(st_));
         if (f > 0) P = std::min(P, f - 1);
       }
+      if (cfg_.host_pack >= 2) P = std::min(P, cfg_.host_pack - 1);
       for (int l = 0; l < m.layers; ++l) {
         synth_layer(l, ca);
         host_store_layer(slot, l, ca, cb, n_ctx, P);

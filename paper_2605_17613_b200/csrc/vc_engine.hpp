@@ -65,7 +65,9 @@ struct EngineConfig {
   int ring_chunks = 0;
   int max_streams = 2;  // streamed verifies in flight (saved hidden state + exact window rows each)
   // chunk ring over the quantised tier: store the host pool's 128-token
-  // blocks losslessly packed (vc_pack.cu, ~0.76 of the bytes on the link)
+  // blocks losslessly packed (vc_pack.cu, ~0.76 of the bytes on the link).
+  // 0 off, 1 on; k >= 2: on with at most k - 1 packed blocks per request (a
+  // test knob for the raw-tail path that only incompressible data reaches)
   int host_pack = 1;
   // drop-topk token scores: 0 = L1 norm of the post-RoPE key; 1 = SnapKV
   // (Li et al., 2024): attention of the observation query (the request's

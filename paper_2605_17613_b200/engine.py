@@ -134,7 +134,8 @@ class Engine:
                               max_verify, int(use_graphs), float(drop_ratio), int(tp_size), int(tp_rank),
                               int(drop_window), int(resident_slots), int(draft_depth),
                               int(ring_chunks), int(max_streams), 1 if drop_score == "snapkv" else 0,
-                              int(snap_pool), int(snap_recent), 1 if host_pack else -1)
+                              int(snap_pool), int(snap_recent),
+                              (int(host_pack) if not isinstance(host_pack, bool) else (1 if host_pack else -1)))
         self.tp_size, self.tp_rank = int(tp_size), int(tp_rank)
         h = C.c_void_p()
         check(self.lib.vc_engine_create(C.byref(md), C.byref(rt), device, C.byref(h)))

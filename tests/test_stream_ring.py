@@ -55,7 +55,9 @@ def _until(fn, timeout=30.0):
 
 
 @pytest.mark.gpu
-@pytest.mark.parametrize("ring,pack", [(2, True), (3, False), (8, True)])
+# pack: True (every block packed), False (raw pool), 6 (at most 5 packed
+# blocks: the rest of each request, and every row accepted later, raw)
+@pytest.mark.parametrize("ring,pack", [(2, True), (3, False), (8, True), (3, 6)])
 def test_streamed_verify_equals_staged_verify(cuda, w6, ring, pack):
     a, b = _engine(w6, 0), _engine(w6, ring, pack=pack)
     for e in (a, b):
