@@ -46,7 +46,10 @@ constexpr int kChunk = VC_DENSE_CHUNK;
 #define VC_DENSE_TAU 12.0f  // r1: 12 vs 8 = -1.2% per mixed step, 4 = +6%; bf16 P and fp32 sums keep 2^12 exact in range
 #endif
 constexpr float kTau = VC_DENSE_TAU;  // lazy rescale threshold (log2 units)
-constexpr int kThreads = 224;     // producer(Q,K) | MMA | 4 softmax | producer(V)
+// producer(Q,K) | MMA | 2 x 4 softmax warps (two column groups) | producer(V)
+constexpr int kSoftGroups = 2;
+constexpr int kThreads = 32 * (3 + 4 * kSoftGroups);
+constexpr int kWarpV = 2 + 4 * kSoftGroups;
 static_assert(kChunk % kTile == 0, "chunks are whole tiles");
 
 struct Item {
@@ -177,12 +180,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       mbar_init(&v_empty[i], 1);
       mbar_init(&s_full[i], 1);
       mbar_init(&s_empty[i], 1);
-      mbar_init(&p_full[i], 4);
+      mbar_init(&p_full[i], 4 * kSoftGroups);
     }
     mbar_init(&o_full[0], 1);
     mbar_init(&o_full[1], 1);
-    mbar_init(&o_empty[0], 4);
-    mbar_init(&o_empty[1], 4);
+    mbar_init(&o_empty[0], 4 * kSoftGroups);
+    mbar_init(&o_empty[1], 4 * kSoftGroups);
     fence_mbar_init();
     tma_prefetch_desc(&maps.q);
     tma_prefetch_desc(&maps.k);
@@ -238,7 +241,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         ++n;
       }
     }
-  } else if (warp == 6) {
+  } else if (warp == kWarpV) {
     // ===================== TMA producer: V (runs behind K by the softmax) =====================
     if (lane == 0)
       for (int t = 0; t < first_static; ++t) load_kv(&maps.v, sV + t * KV_BYTES, &v_full[t], I0, t);
@@ -330,13 +333,24 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
   } else {
     // ===================== softmax (thread = key) + epilogue (thread = channel) =====================
+    // two groups of 4 warps: group g owns the query columns [c_lo, c_hi) of
+    // every item (16-column granules, group 0 takes the odd one), so a wide
+    // verify window's softmax runs on twice the threads; rows are independent,
+    // so each group keeps its own barrier and its own lazy-rescale vote
     const int quarter = warp & 3;
+    const int grp = (warp - 2) / 4;
+    const int gbar = 1 + grp;                             // the group's named barrier
     const int tid = quarter * 32 + lane;                 // key within the tile / channel / row index
     const uint32_t tlane = tbase + (static_cast<uint32_t>(quarter * 32) << 16);
     const int Hq = s.n_kv * NREP;
-    // columns [0, npad) of a per-item TMEM buffer scaled by alpha_sh (16-column steps, never past npad)
-    auto rescale = [&](uint32_t col0, int npad) {
-      for (int c = 0; c < npad; c += 16) {
+    auto col_range = [&](int npad, int& lo, int& hi) {
+      const int half = ((npad >> 4) + 1) >> 1;
+      lo = grp == 0 ? 0 : half * 16;
+      hi = grp == 0 ? half * 16 : npad;
+    };
+    // columns [c_lo, c_hi) of a per-item TMEM buffer scaled by alpha_sh (16-column steps)
+    auto rescale = [&](uint32_t col0, int c_lo, int c_hi) {
+      for (int c = c_lo; c < c_hi; c += 16) {
         uint32_t v[16];
         tmem_ld16(tlane + col0 + c, v);
         tmem_wait_ld();
@@ -351,10 +365,12 @@ __global__ void __launch_bounds__(kThreads, 1)
       const float* m_run = m_run2[ob];
       const int rows = min(kRows, I.n_tok * NREP - I.rb * kRows);
       const int npad = (rows + 15) & ~15;
+      int c_lo, c_hi;
+      col_range(npad, c_lo, c_hi);
       mbar_wait(&o_full[ob], (ni >> 1) & 1);
       tmem_fence_after();
       if (quarter == 0) {  // L: every lane holds the same row sums; lane 0's are used
-        for (int c = 0; c < npad; c += 16) {
+        for (int c = c_lo; c < c_hi; c += 16) {
           uint32_t v[16];
           tmem_ld16(tlane + kColL + ob * kRows + c, v);
           tmem_wait_ld();
@@ -363,8 +379,8 @@ __global__ void __launch_bounds__(kThreads, 1)
             for (int j = 0; j < 16; ++j) l_sh[c + j] = __uint_as_float(v[j]);
         }
       }
-      named_bar(1, 128);
-      for (int c = 0; c < npad; c += 16) {
+      named_bar(gbar, 128);
+      for (int c = c_lo; c < c_hi; c += 16) {
         uint32_t v[16];
         tmem_ld16(tlane + kColO + ob * kRows + c, v);
         tmem_wait_ld();
@@ -381,7 +397,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           }
         }
       }
-      if (tid < rows) {
+      if (tid >= c_lo && tid < c_hi && tid < rows) {
         const int r = I.rb * kRows + tid;
         const int tok = r / NREP, rep = r % NREP;
         if (I.k_lo < I.kv_len - I.n_tok + tok + 1) {
@@ -391,7 +407,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       tmem_fence_before();
-      named_bar(1, 128);  // l_sh reads done before the next epilogue refills it
+      named_bar(gbar, 128);  // l_sh reads done before the next epilogue refills it
       if (lane == 0) mbar_arrive(&o_empty[ob]);
     };
     int g = 0, n = 0;
@@ -403,8 +419,10 @@ __global__ void __launch_bounds__(kThreads, 1)
       float* m_run = m_run2[ob];
       const int rows = min(kRows, I.n_tok * NREP - I.rb * kRows);
       const int npad = (rows + 15) & ~15;
+      int c_lo, c_hi;
+      col_range(npad, c_lo, c_hi);
       // per-row visibility limit (absolute key) inside this chunk; padding rows see nothing
-      if (tid < kRows) {
+      if (tid >= c_lo && tid < c_hi) {
         const int tok = (I.rb * kRows + tid) / NREP;
         lim_col[tid] = tid < rows ? min(I.k_hi, I.kv_len - I.n_tok + tok + 1) : I.k_lo;
         // padding columns: m = +inf makes every P 0 and keeps them out of the max
@@ -412,7 +430,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       const int tok_first = (I.rb * kRows) / NREP;
       const int lim_min = min(I.k_hi, I.kv_len - I.n_tok + tok_first + 1);   // earliest row's limit
-      named_bar(1, 128);
+      named_bar(gbar, 128);
       for (int t = 0; t < I.n_tiles; ++t, ++g) {
         const int sb = g & 1;
         const int key0 = I.k_lo + t * kTile;
@@ -446,15 +464,15 @@ __global__ void __launch_bounds__(kThreads, 1)
         };
         // 32 columns per TMEM load + wait where they fit (fewer serialised waits)
         auto write_p = [&](bool track, float& over) {
-          int c = 0;
-          for (; c + 32 <= npad; c += 32) {
+          int c = c_lo;
+          for (; c + 32 <= c_hi; c += 32) {
             uint32_t v[32];
             tmem_ld32(tS + c, v);
             tmem_wait_ld();
             p16(v, c, track, over);
             p16(v + 16, c + 16, track, over);
           }
-          if (c < npad) {
+          if (c < c_hi) {
             uint32_t v[16];
             tmem_ld16(tS + c, v);
             tmem_wait_ld();
@@ -464,10 +482,10 @@ __global__ void __launch_bounds__(kThreads, 1)
         // optimistic pass: P with the running max; note how far any score overshoots it
         float over = -INFINITY;
         if (t > 0) write_p(true, over);
-        const bool refresh = bar_or(1, 128, t == 0 || over > kTau);
+        const bool refresh = c_hi > c_lo && bar_or(gbar, 128, t == 0 || over > kTau);
         if (refresh) {
           // exact per-row tile max (warp transpose-reduce, then across the 4 warps)
-          for (int c = 0; c < npad; c += 32) {
+          for (int c = c_lo; c < c_hi; c += 32) {
             uint32_t v[32];
             tmem_ld32(tS + c, v);   // may read past npad: those columns are discarded
             tmem_wait_ld();
@@ -478,27 +496,27 @@ __global__ void __launch_bounds__(kThreads, 1)
               x[j] = (c + j < rows && key < lim_col[col]) ? __uint_as_float(v[j]) * s.scale_log2 : -INFINITY;
             }
             const float cm = warp_colmax(x, lane);
-            if (c + lane < kRows) wmax[quarter][c + lane] = cm;
+            if (c + lane < c_hi) wmax[quarter][c + lane] = cm;
           }
-          named_bar(1, 128);
+          named_bar(gbar, 128);
           bool grew = false;
-          if (tid < rows) {
+          if (tid >= c_lo && tid < c_hi && tid < rows) {
             const float mt = fmaxf(fmaxf(wmax[0][tid], wmax[1][tid]), fmaxf(wmax[2][tid], wmax[3][tid]));
             const float mo = m_run[tid];
             const float mn = fmaxf(mo, mt);
             grew = mn > mo + kTau || (mo == -INFINITY && mn != -INFINITY);
             alpha_sh[tid] = grew ? ex2(mo - mn) : 1.f;
             if (grew) m_run[tid] = mn;
-          } else if (tid < kRows) {
+          } else if (tid >= c_lo && tid < c_hi) {
             alpha_sh[tid] = 1.f;
           }
-          const bool any_grew = bar_or(1, 128, grew && t > 0);
+          const bool any_grew = bar_or(gbar, 128, grew && t > 0);
           if (any_grew) {
             // O^T / L hold tiles < t: wait for PV(t-1), scale the columns of the rows that moved
             mbar_wait(&s_empty[(g - 1) & 1], ((g - 1) >> 1) & 1);
             tmem_fence_after();
-            rescale(kColO + ob * kRows, npad);
-            rescale(kColL + ob * kRows, npad);
+            rescale(kColO + ob * kRows, c_lo, c_hi);
+            rescale(kColL + ob * kRows, c_lo, c_hi);
             tmem_wait_st();
           }
           write_p(false, over);  // P again with the refreshed maxima
