@@ -260,4 +260,17 @@ double ref_optimize_intra(double c, int x_max, int l_max, double bw_hbm, double 
   return rc < 0 ? -2.0 + rc : out;
 }
 
+// composed_accept_length (analytics.cpp:413-422) with gamma(x) tabulated at
+// one point and a constant gamma_e: pins knobs.composed_accept_length.
+double ref_composed_accept_length(int x, double c, int d_e, double gamma_x, double gamma_e) {
+  double out = -1.0;
+  int rc = guarded([&] {
+    const int xs[1] = {x};
+    const double gs[1] = {gamma_x};
+    out = speckv::composed_accept_length(x, c, d_e, tab_model(c, 1, xs, gs), [&](int) { return gamma_e; });
+    return 0;
+  });
+  return rc < 0 ? -2.0 + rc : out;
+}
+
 }  // extern "C"

@@ -86,11 +86,16 @@ def test_optimize_intra_equals_reference(batch, kv, c):
     assert got == (want, bc.value, x.value, l.value)
 
 
-def test_composed_accept_length_matches_reference_formula():
-    """analytics.cpp:413-422: gamma * x * (1 + gamma_e * (d_e - 1)); d_e = 1 ignores gamma_e."""
-    from paper_2605_17613_b200 import knobs
-    assert knobs.composed_accept_length(8, 0.5, 1, 0.9) == 4.0
-    assert abs(knobs.composed_accept_length(6, 0.8, 3, 0.25) - 0.8 * 6 * 1.5) < 1e-12
-    import pytest
+def test_composed_accept_length_matches_reference():
+    """knobs.composed_accept_length == the compiled reference's
+    composed_accept_length (analytics.cpp:413-422) with gamma(x) tabulated at x."""
+    r = _ref()
+    r.ref_composed_accept_length.restype = C.c_double
+    r.ref_composed_accept_length.argtypes = [C.c_int, C.c_double, C.c_int, C.c_double, C.c_double]
+    for x, c, d_e, g, ge in [(8, 0.27, 1, 0.5, 0.9), (6, 0.27, 3, 0.872, 0.25), (47, 0.14, 4, 0.42, 0.0),
+                             (16, 0.2, 2, 0.7, 1.0)]:
+        want = r.ref_composed_accept_length(x, c, d_e, g, ge)
+        assert want >= 0
+        assert abs(K.composed_accept_length(x, g, d_e, ge) - want) <= 1e-12 * max(1.0, want)
     with pytest.raises(ValueError):
-        knobs.composed_accept_length(6, 0.8, 3, 1.5)
+        K.composed_accept_length(6, 0.8, 3, 1.5)
