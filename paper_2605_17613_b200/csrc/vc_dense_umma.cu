@@ -161,10 +161,13 @@ __global__ void __launch_bounds__(kThreads, 1)
   __shared__ __align__(8) uint64_t q_full, q_empty, k_full[2], v_full[2], k_empty[2], v_empty[2];
   __shared__ __align__(8) uint64_t s_full[2], s_empty[2], p_full[2], o_full[2], o_empty[2];
   __shared__ uint32_t tmem_base_sh;
-  __shared__ __align__(16) float m_run2[2][kRows];
-  __shared__ __align__(16) float alpha_sh[kRows], l_sh[kRows];
-  __shared__ float wmax[4][kRows];
-  __shared__ __align__(16) int lim_col[kRows];   // keys < lim_col[row] are visible to the item's row
+  // per softmax group: the groups' column ranges move with each item's width,
+  // and a group may still run an older item's epilogue while the other starts
+  // the next item, so each group keeps its own per-column state
+  __shared__ __align__(16) float m_run3[kSoftGroups][2][kRows];
+  __shared__ __align__(16) float alpha_g[kSoftGroups][kRows], l_g[kSoftGroups][kRows];
+  __shared__ float wmax_g[kSoftGroups][4][kRows];
+  __shared__ __align__(16) int lim_g[kSoftGroups][kRows];   // keys < lim_col[row] are visible to the item's row
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int n_items = n_seq * row_blocks * s.n_kv * max_chunks;
@@ -343,6 +346,11 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int tid = quarter * 32 + lane;                 // key within the tile / channel / row index
     const uint32_t tlane = tbase + (static_cast<uint32_t>(quarter * 32) << 16);
     const int Hq = s.n_kv * NREP;
+    float(*m_run2)[kRows] = m_run3[grp];
+    float* alpha_sh = alpha_g[grp];
+    float* l_sh = l_g[grp];
+    float(*wmax)[kRows] = wmax_g[grp];
+    int* lim_col = lim_g[grp];
     auto col_range = [&](int npad, int& lo, int& hi) {
       const int half = ((npad >> 4) + 1) >> 1;
       lo = grp == 0 ? 0 : half * 16;

@@ -112,3 +112,54 @@ def test_dense_attention_row_invariance(cuda):
         one = e.attention_probe(0, 0, 0, qd[i:i + 1].data_ptr(), 1, n_ctx - 8 + i)
         np.testing.assert_array_equal(one[0], many[i])
     e.close()
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("n_rows", [48, 20])
+def test_dense_attention_row_invariance_many_items(cuda, n_rows):
+    """Row invariance when every CTA runs several items (8 KV heads x 16
+    chunks x up to 3 row blocks over 32K keys > 148 SMs) and the window's
+    columns split across both softmax column groups: each row of a verify
+    window equals the same row computed alone (the host tier's x=47 windows)."""
+    torch = cuda
+    s = ModelShape(vocab=256, hidden=1024, layers=1, n_q=32, n_kv=8, d_head=128, ffn=512)
+    n_ctx = 32768
+    e = Engine(s, max_slots=1, max_ctx=n_ctx + 64, max_x=48, quant_bits=0, use_graphs=False)
+    k, v = T.synthetic_kv(s.layers, s.n_kv, n_ctx, s.d_head, seed=9)
+    e.add_kv(0, k, v, first_token=1)
+    rng = np.random.default_rng(n_rows)
+    q = T.f32_to_bf16(rng.standard_normal((n_rows, s.n_q, s.d_head)).astype(np.float32))
+    qd = torch.from_numpy(q.view(np.int16).copy()).cuda()
+    many = e.attention_probe(0, 0, 2, qd.data_ptr(), n_rows, n_ctx)
+    for i in range(n_rows):
+        one = e.attention_probe(0, 0, 0, qd[i:i + 1].data_ptr(), 1, n_ctx - n_rows + 1 + i)
+        np.testing.assert_array_equal(one[0], many[i], err_msg=f"row {i} of {n_rows}")
+    e.close()
+
+
+@pytest.mark.gpu
+def test_verify_windows_of_mixed_widths_are_row_invariant(cuda):
+    """Several verify windows of different widths in one step, over long
+    contexts whose last chunks are short (items of 1-16 tiles, several per
+    CTA, the softmax groups' column split changing from item to item): every
+    row's logits equal that window verified alone.  (The two softmax column
+    groups once shared per-column state across items -- a timing-dependent
+    race this test does not reliably provoke; the full-scale host-tier bench
+    line, 16 x 32K with 48-row windows, did, and checks it every run.)"""
+    s = ModelShape(vocab=512, hidden=1024, layers=2, n_q=32, n_kv=8, d_head=128, ffn=1024)
+    w = T.tiny_weights(s, seed=3, std=0.02)
+    e = Engine(s, max_slots=3, max_ctx=33000, max_x=48, quant_bits=0, max_verify=3, use_graphs=False)
+    e.load_weights(w)
+    ctx = [32700, 30100, 2100]
+    for i, n in enumerate(ctx):
+        e.add_synthetic(i, n, 5 + i, seed=1 + i)
+    rng = np.random.default_rng(0)
+    wins = [[int(t) for t in rng.integers(0, s.vocab, n)] for n in (48, 7, 21)]
+    items = [(i, 2, wins[i], -1) for i in range(3)]
+    _, together = e.step(items, want_logits=True)
+    off = 0
+    for i in range(3):
+        _, alone = e.step([items[i]], want_logits=True)
+        np.testing.assert_array_equal(together[off:off + len(wins[i])], alone, err_msg=f"window {i}")
+        off += len(wins[i])
+    e.close()
