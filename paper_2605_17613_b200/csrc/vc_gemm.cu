@@ -599,6 +599,12 @@ gemm_cluster_kernel(const uint16_t* __restrict__ Xt, int Mp, int M, int K,
         if (lane == 0) mbar_arrive(&full[st]);
       }
       }
+      // The park below overwrites the stages.  It is already ordered after
+      // these stores (store -> full arrive -> MMA -> commit -> acc_full), but
+      // racecheck does not follow tcgen05.commit arrivals; a named barrier
+      // states the same order in a form it tracks (it costs nothing: every
+      // epilogue warp waits on acc_full next anyway).
+      named_bar(1, 256);
     }
     const int quarter = warp & 3;
     const int feat = quarter * 32 + lane;

@@ -277,3 +277,31 @@ def test_drop_tier_ring_scheduled_lossless(cuda, w6):
     full = sum(ctx) / n * per_token
     assert 0 < st["h2d_bytes"] <= 0.76 * full * st["verifies"]
     e.close()
+
+
+@pytest.mark.gpu
+def test_host_tier_wide_windows_lossless(cuda):
+    """The host tier at its operating point, scaled down in depth only: 8
+    KV heads of 128 channels over 32K keys, 48-row verify windows streamed
+    through the ring (3 row blocks x 8 heads x 16 chunks, several items per
+    CTA with the softmax groups' column split changing from item to item),
+    the packed host pool -- the emitted tokens equal full-KV greedy decode."""
+    s = dataclasses.replace(TINY, vocab=512, hidden=1024, layers=2, n_q=32, n_kv=8, d_head=128, ffn=1024)
+    w = T.tiny_weights(s, seed=5, std=0.02)
+    n, K, ctx = 6, 96, [32000 - 700 * i for i in range(6)]
+    ref = Engine(s, max_slots=n, max_ctx=32800, max_x=1, quant_bits=0)
+    ref.load_weights(w)
+    for i in range(n):
+        ref.add_synthetic(i, ctx[i], 5 + i, seed=1 + i)
+    base, _ = ref.autoregress(list(range(n)), K)
+    ref.close()
+    e = Engine(s, max_slots=n, max_ctx=32800, max_x=47, quant_bits=4, full_tier=1, n_stage=0, ring_chunks=4,
+               max_verify=4)
+    e.load_weights(w)
+    for i in range(n):
+        e.add_synthetic(i, ctx[i], 5 + i, seed=1 + i)
+        e.compress(i)
+    out, st = e.run_scheduled(list(range(n)), K, x=47, window=256)
+    np.testing.assert_array_equal(out, base)
+    assert st["verifies"] > 0
+    e.close()
