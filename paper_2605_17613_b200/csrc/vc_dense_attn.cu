@@ -15,7 +15,9 @@ constexpr int kMaxParts = 512;  // chunks per sequence the combine can merge (25
 template <int D>
 __global__ void combine_kernel(AttnShape s, CombineSets cs, Partials part, uint16_t* out) {
   pdl_trigger();
-  pdl_wait();
+  // Everything up to the partial-row indices depends only on the step's
+  // sequence table (host-written before the step, never by a kernel), so it
+  // runs before the PDL wait, overlapping the attention kernel's tail.
   // this block's (set, sequence, query row): set k covers n * rows blocks
   int k = 0, b = blockIdx.x;
   while (k + 1 < cs.n_sets && b >= cs.set[k].n * cs.set[k].rows) {
@@ -60,33 +62,46 @@ __global__ void combine_kernel(AttnShape s, CombineSets cs, Partials part, uint1
   const int n_all = n_parts + n_tail;
   __shared__ float s_m[kMaxParts], s_f[kMaxParts], s_lp[kMaxParts];
   __shared__ size_t s_row[kMaxParts];
-  __shared__ float s_M, s_l;
+  __shared__ float s_l;
+  for (int c = threadIdx.x; c < n_all; c += blockDim.x)
+    s_row[c] = prow_of(c < n_parts ? c : max_chunks + (c - n_parts));
+  __syncthreads();
+  pdl_wait();
   for (int c = threadIdx.x; c < n_all; c += blockDim.x) {  // every (m, l) load in parallel
-    const size_t pr = prow_of(c < n_parts ? c : max_chunks + (c - n_parts));
-    s_row[c] = pr;
-    const float2 ml = *reinterpret_cast<const float2*>(part.ml + pr * 2);
+    const float2 ml = *reinterpret_cast<const float2*>(part.ml + s_row[c] * 2);
     s_m[c] = ml.x;
     s_lp[c] = ml.y;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {  // shared memory only: no global-latency chain
+  if (threadIdx.x < 32) {  // warp 0: M (exact, order-free), weights, l by a fixed lane-strided + xor tree
+    const int ln = threadIdx.x;
     float M = -INFINITY;
-    for (int c = 0; c < n_all; ++c) M = fmaxf(M, s_m[c]);
+    for (int c = ln; c < n_all; c += 32) M = fmaxf(M, s_m[c]);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
     float l = 0.f;
-    for (int c = 0; c < n_all; ++c) {  // fixed order
+    for (int c = ln; c < n_all; c += 32) {
       const float f = (s_m[c] == -INFINITY) ? 0.f : exp2f(s_m[c] - M);
       s_f[c] = f;
-      l += f * s_lp[c];
+      l = fmaf(f, s_lp[c], l);
     }
-    s_M = M;
-    s_l = l;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
+    if (ln == 0) s_l = l;
   }
   __syncthreads();
   const float l = s_l;
+  constexpr int kBatch = 16;  // partial rows in flight per thread
   for (int c0 = threadIdx.x; c0 < D; c0 += blockDim.x) {
     float o = 0.f;
-#pragma unroll 4
-    for (int c = 0; c < n_all; ++c) o += s_f[c] * part.o[s_row[c] * D + c0];
+    for (int c = 0; c < n_all; c += kBatch) {
+      float v[kBatch];
+#pragma unroll
+      for (int j = 0; j < kBatch; ++j) v[j] = c + j < n_all ? part.o[s_row[c + j] * D + c0] : 0.f;
+#pragma unroll
+      for (int j = 0; j < kBatch; ++j)
+        if (c + j < n_all) o = fmaf(s_f[c + j], v[j], o);  // fixed (chunk) order
+    }
     const uint16_t v = f2bf(l > 0.f ? o / l : 0.f);
     if (s.out_mp > 0)
       out[atile_idx(sq.row0 + tok, hq * D + c0, s.out_mp)] = v;

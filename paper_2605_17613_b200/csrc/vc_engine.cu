@@ -1132,7 +1132,8 @@ void Engine::enqueue_forward(int M, int n_draft, int n_dense1, int n_densev, int
   ef.kind = Epi::StoreF32;
   ef.out_f32 = logits_;
   // VC_SKIP (diagnostics only, wrong results): bit 0 skips attention + combine,
-  // bit 1 skips rms_apply -- to time the rest of a step in its CUDA graph
+  // bit 1 skips rms_apply, bit 2 the combine, bits 3-6 the qkv / o / gate-up /
+  // down GEMMs -- to attribute a step's in-graph time
   static const int skip = [] {
     const char* v = std::getenv("VC_SKIP");
     return v ? std::atoi(v) : 0;
@@ -1161,7 +1162,8 @@ void Engine::enqueue_forward(int M, int n_draft, int n_dense1, int n_densev, int
   };
   for (int l = 0; l < L; ++l) {
     eq.layer = l;
-    if (fuse_norm && l > 0) {
+    if (skip & 8) {
+    } else if (fuse_norm && l > 0) {
       const GemmNormIn nq = norm_in(w_.attn_norm[l]);
       VC_LAUNCH(gemm(nullptr, M, M, H, w_.wqkv[l], qkv_n, eq, gws_, st_, &nq));
     } else {
@@ -1208,7 +1210,7 @@ void Engine::enqueue_forward(int M, int n_draft, int n_dense1, int n_densev, int
       VC_LAUNCH(dense_attention(as, dense_v_pool, dense_maps_, l, sv, n_densev, max_chunks_d_, max_rows_v, part_, st_));
       add_set(sv, n_densev, max_chunks_d_, 1, max_rows_v);
     }
-    if (cs.n_sets > 0) VC_LAUNCH(attention_combine_sets(as, cs, part_, attn_, st_));
+    if (cs.n_sets > 0 && !(skip & 4)) VC_LAUNCH(attention_combine_sets(as, cs, part_, attn_, st_));
     // residual projection: fused residual epilogue, or (tensor parallel) the
     // rank's partial -> all-gather -> fixed rank-order sum + residual (vc_tp.h);
     // then the next RMSNorm.  (r1: fusing the RMSNorm into the residual
@@ -1216,7 +1218,7 @@ void Engine::enqueue_forward(int M, int n_draft, int n_dense1, int n_densev, int
     // bit-identical but 3% slower per step than this launch.)
     auto residual_gemm = [&](const uint16_t* Xt, int Kd, const uint16_t* Wt, const uint16_t* norm_w, bool norm_next) {
       if (!coll_) {
-        VC_LAUNCH(gemm(Xt, M, M, Kd, Wt, H, er, gws_, st_));
+        if (!(skip & (Kd == H ? 16 : 64))) VC_LAUNCH(gemm(Xt, M, M, Kd, Wt, H, er, gws_, st_));
       } else {
         GemmEpilogue ey;
         ey.kind = Epi::StoreF32;
@@ -1232,7 +1234,8 @@ void Engine::enqueue_forward(int M, int n_draft, int n_dense1, int n_densev, int
     trace("x.o", x_, static_cast<size_t>(M) * H * 4);
     trace("ss.o", ss_part_, static_cast<size_t>(M) * (H / 128) * 4);
     trace("xn.o", xn_, static_cast<size_t>(M) * H * 2);
-    if (fuse_norm) {
+    if (skip & 32) {
+    } else if (fuse_norm) {
       const GemmNormIn ng = norm_in(w_.mlp_norm[l]);
       VC_LAUNCH(gemm(nullptr, M, M, H, w_.wgu[l], 2 * F, es, gws_, st_, &ng));
     } else {

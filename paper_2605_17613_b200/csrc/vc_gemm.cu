@@ -29,7 +29,9 @@
 // fp32 accumulators in TMEM (double-buffered across a CTA's tiles), 8
 // epilogue warps read them with tcgen05.ld.  (r1: the mma.sync version this
 // replaces ran a 113-row verify step's projections 2.4x slower.)
+#include <cstdio>
 #include <cstdlib>
+#include <vector>
 
 #include "vc_common.cuh"
 #include "vc_gemm.h"
@@ -49,6 +51,7 @@ constexpr int kSms = 148;
 #endif
 constexpr int kP = VC_GEMM_GRID_PER_SM * kSms;  // stream-K grid upper bound (a function of nothing but the GPU)
 constexpr int kEpiRows = 16;           // epilogue staging pass (tokens)
+constexpr int kMaxS = 8;               // cluster split-K ranks (portable cluster size)
 constexpr int kLD = kBN + 4;
 #ifndef VC_FIXUP_UNROLL
 #define VC_FIXUP_UNROLL 4       // contributors in flight per loop trip, NT = 16
@@ -57,6 +60,24 @@ constexpr int kLD = kBN + 4;
 #define VC_FIXUP_UNROLL_WIDE 2  // contributors in flight per loop trip, NT >= 32 (4 float4 each)
 #endif
 constexpr int kFixUnroll = VC_FIXUP_UNROLL, kFixUnrollWide = VC_FIXUP_UNROLL_WIDE;
+
+#ifdef VC_GEMM_TRACE
+// Diagnostics build (-DVC_GEMM_TRACE): per cluster-kernel launch and CTA, the
+// global timer at start, after the producer's PDL wait, when the accumulator
+// is complete, after the partial exchange and at exit; dumped by
+// vc_gemm_trace_dump() (tools/gemm_trace.py).  Production builds compile none of it.
+constexpr int kTrLaunches = 512, kTrCtas = 256, kTrPts = 7;
+__device__ unsigned long long g_gemm_trace[kTrLaunches * kTrCtas * kTrPts];
+int g_gemm_trace_nk[kTrLaunches * 3];  // host: (N, K, S) per launch slot
+int g_gemm_trace_next = 0;  // host: next launch slot (one counter for every instantiation)
+VC_DEV void gtrace(int id, int pt) {
+  if (id >= 0 && id < kTrLaunches && blockIdx.x < kTrCtas)
+    g_gemm_trace[(static_cast<size_t>(id) * kTrCtas + blockIdx.x) * kTrPts + pt] = vc_globaltimer();
+}
+#define VC_GTRACE(pt) gtrace(nin.trace, pt)
+#else
+#define VC_GTRACE(pt)
+#endif
 
 template <int NT>
 struct Cfg {
@@ -73,15 +94,62 @@ __host__ __device__ inline long grid_of(long T) { return T < kP ? T : kP; }
 // CTA index owning global k-tile g under the split [q*T/P, (q+1)*T/P).
 __host__ __device__ inline long owner(long g, long T) { return ((g + 1) * grid_of(T) - 1) / T; }
 
-// Epilogue over one staged pass of 16 tokens x 128 features (sT).
+// Epilogue operands that do not depend on the accumulator: the residual
+// stream slice a Residual thread adds to, and a Qkv thread's row destination
+// and RoPE factors.  The cluster kernel's epilogue warps load them while the
+// tiles stream (tools/gemm_trace.py, r2: o/down exchange -> exit 2.05 -> 1.5 us;
+// the qkv epilogue stays ~2 us, its cost is not these loads).
+template <Epi E>
+struct EpiPre {
+  bool ok = false;
+};
+template <>
+struct EpiPre<Epi::Residual> {
+  bool ok = false;
+  float4 a, b;
+};
+template <>
+struct EpiPre<Epi::Qkv> {
+  bool ok = false;
+  RowDest rd;
+  float c[4], s[4];
+};
+
+template <Epi E>
+__device__ void epilogue_load(EpiPre<E>& pre, int m, int M, int n0, int N, const GemmEpilogue& ep, int sub) {
+  pre.ok = true;
+  if (m >= M) return;
+  if constexpr (E == Epi::Residual) {
+    const float4* xp = reinterpret_cast<const float4*>(ep.x + static_cast<size_t>(m) * N + n0 + sub * 8);
+    pre.a = xp[0];
+    pre.b = xp[1];
+  } else if constexpr (E == Epi::Qkv) {
+    pre.rd = ep.rows[m];
+    const int half = ep.d / 2;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const int pr = sub * 4 + i, jj = pr % half;
+      const int head = (n0 + (pr / half) * ep.d + jj) / ep.d;
+      pre.c[i] = pre.s[i] = 0.f;
+      if (head < ep.n_q + ep.n_kv) {
+        pre.c[i] = ep.rope_cos[static_cast<size_t>(pre.rd.rope_pos) * half + jj];
+        pre.s[i] = ep.rope_sin[static_cast<size_t>(pre.rd.rope_pos) * half + jj];
+      }
+    }
+  }
+}
+
+// Epilogue over one staged pass of 16 tokens x 128 features (sT); `pre`
+// holds the pass's operands if they were loaded early.
 template <Epi E>
 __device__ void epilogue_pass(const float* sT, int mbase, int M, int Mp, int n0, int N,
-                              const GemmEpilogue& ep, int tid) {
+                              const GemmEpilogue& ep, int tid, EpiPre<E> pre = EpiPre<E>{}) {
   const int t = tid >> 4;          // row of the pass
   const int sub = tid & 15;        // 16 threads per row
   const int m = mbase + t;
   const bool live = m < M;
   const float* row = sT + t * kLD;
+  if (!pre.ok) epilogue_load<E>(pre, m, M, n0, N, ep, sub);
   if constexpr (E == Epi::StoreF32) {
     if (live) {
       float4* dst = reinterpret_cast<float4*>(ep.out_f32 + static_cast<size_t>(m) * N + n0 + sub * 8);
@@ -92,7 +160,7 @@ __device__ void epilogue_pass(const float* sT, int mbase, int M, int Mp, int n0,
     float sq = 0.f;
     if (live) {
       float4* xp = reinterpret_cast<float4*>(ep.x + static_cast<size_t>(m) * N + n0 + sub * 8);
-      float4 a = xp[0], b = xp[1];
+      float4 a = pre.a, b = pre.b;
       a.x += row[sub * 8 + 0]; a.y += row[sub * 8 + 1]; a.z += row[sub * 8 + 2]; a.w += row[sub * 8 + 3];
       b.x += row[sub * 8 + 4]; b.y += row[sub * 8 + 5]; b.z += row[sub * 8 + 6]; b.w += row[sub * 8 + 7];
       xp[0] = a;
@@ -119,7 +187,7 @@ __device__ void epilogue_pass(const float* sT, int mbase, int M, int Mp, int n0,
   } else {  // Qkv: bf16 round, RoPE on q/k heads, scatter k/v to the pools
     if (!live) return;
     const int d = ep.d, half = d / 2;
-    const RowDest rd = ep.rows[m];
+    const RowDest rd = pre.rd;
 #pragma unroll
     for (int i = 0; i < 4; ++i) {
       const int pr = sub * 4 + i;                 // rotation pair within the tile
@@ -128,8 +196,8 @@ __device__ void epilogue_pass(const float* sT, int mbase, int M, int Mp, int n0,
       const int head = (n0 + fa) / d;
       float a = bf2f(f2bf(row[fa])), b = bf2f(f2bf(row[fb]));
       if (head < ep.n_q + ep.n_kv) {
-        const float c = ep.rope_cos[static_cast<size_t>(rd.rope_pos) * half + jj];
-        const float s = ep.rope_sin[static_cast<size_t>(rd.rope_pos) * half + jj];
+        const float c = pre.c[i];
+        const float s = pre.s[i];
         const float ra = __fsub_rn(__fmul_rn(a, c), __fmul_rn(b, s));
         const float rb = __fadd_rn(__fmul_rn(b, c), __fmul_rn(a, s));
         a = ra;
@@ -463,6 +531,8 @@ gemm_cluster_kernel(const uint16_t* __restrict__ Xt, int Mp, int M, int K,
   const int k_lo = rank * KT / S, k_hi = (rank + 1) * KT / S;
   const int nk = k_hi - k_lo;
   const bool fused = nin.x != nullptr;  // the 8 epilogue warps write the X half of every stage
+  if (tid == 0) VC_GTRACE(0);
+  EpiPre<E> pre0;  // epilogue warps: operands of their first pass, loaded early
   if (tid == 0) {
     for (int s2 = 0; s2 < ST; ++s2) {
       mbar_init(&full[s2], fused ? 9 : 1);
@@ -487,6 +557,7 @@ gemm_cluster_kernel(const uint16_t* __restrict__ Xt, int Mp, int M, int K,
         tma_load_1d(sW + i * WB, Wt + (static_cast<size_t>(tile) * KT + k_lo + i) * 8192, WB, &full[i]);
       }
       pdl_wait();
+      VC_GTRACE(1);
       if (!fused)
         for (int i = 0; i < pre; ++i)
           tma_load_1d(sX + i * XB, Xt + (static_cast<size_t>(k_lo + i) * Mp + m0) * 64, XB, &full[i]);
@@ -517,26 +588,18 @@ gemm_cluster_kernel(const uint16_t* __restrict__ Xt, int Mp, int M, int K,
   } else {  // ---- park the partial: TMEM -> sAcc[token][feature]
     pdl_wait();  // the epilogue writes buffers the previous kernel may read
     const int et = tid - 64;
+    // the first epilogue pass's accumulator-independent operands: in flight
+    // while the tiles stream
+    epilogue_load<E>(pre0, m0 + rank * NT / S + (et >> 4), M, tile * kBN, N, ep, et & 15);
     if (fused) {
       // ---- fused RMSNorm: the activation half of every stage, in the
       // swizzled layout a bulk copy of rms_apply's tiled output would land
       const int H = K;
       const int tiles = H / kBN;
-      if (et < NT) {
-        const int m = m0 + et;
-        float r = 0.f;
-        if (m < M) {
-          const float* sp = nin.ss + static_cast<size_t>(m) * tiles;
-          float sum = 0.f;
-          for (int t = 0; t < tiles; ++t) sum += sp[t];
-          r = rsqrtf(sum / H + nin.eps);
-        }
-        sR[et] = r;
-      }
-      named_bar(1, 256);
       // register pipeline: the x / w loads of stage i + kPF are in flight
       // while stage i is converted and stored (a stage's loads alone are an
-      // L2 round trip, which would otherwise pace every stage)
+      // L2 round trip, which would otherwise pace every stage); the first
+      // stages' loads go out before the row scales are summed
       constexpr int kCPT = NT * 8 / 256 > 0 ? NT * 8 / 256 : 1;  // 16-B chunks per thread per stage
       constexpr int kPF = kCPT >= 4 ? 1 : (kCPT == 2 ? 2 : 4);   // stages in flight
       struct Chunk {
@@ -562,6 +625,19 @@ gemm_cluster_kernel(const uint16_t* __restrict__ Xt, int Mp, int M, int K,
 #pragma unroll
       for (int p = 0; p < kPF; ++p)
         if (p < nk) load(p, buf[p]);
+      if (et < NT) {
+        const int m = m0 + et;
+        float r = 0.f;
+        if (m < M) {
+          const float* sp = nin.ss + static_cast<size_t>(m) * tiles;
+          float sum = 0.f;
+#pragma unroll 8
+          for (int t = 0; t < tiles; ++t) sum += sp[t];
+          r = rsqrtf(sum / H + nin.eps);
+        }
+        sR[et] = r;
+      }
+      named_bar(1, 256);
       for (int i0 = 0; i0 < nk; i0 += kPF) {
 #pragma unroll
       for (int p = 0; p < kPF; ++p) {
@@ -611,6 +687,7 @@ gemm_cluster_kernel(const uint16_t* __restrict__ Xt, int Mp, int M, int K,
     const int tok0 = et >= 128 ? kHalf : 0;
     const uint32_t tacc = tbase + (static_cast<uint32_t>(quarter * 32) << 16) + tok0;
     mbar_wait(&acc_full, 0);
+    if (et == 0) VC_GTRACE(2);
     tmem_fence_after();
     for (int c = 0; c < kHalf; c += 8) {
       uint32_t u[8];
@@ -625,6 +702,7 @@ gemm_cluster_kernel(const uint16_t* __restrict__ Xt, int Mp, int M, int K,
   }
   __syncwarp();
   cluster_sync();  // every rank's partial is parked
+  if (tid == 64) VC_GTRACE(3);
   if (warp >= 2) {
     // ---- reduce my tokens over the cluster (rank order), then the epilogue
     const int et = tid - 64;
@@ -636,21 +714,31 @@ gemm_cluster_kernel(const uint16_t* __restrict__ Xt, int Mp, int M, int K,
       for (int e = et; e < rows * (kBN / 4); e += 256) {
         const int t = e / (kBN / 4), f4 = e % (kBN / 4);
         const float* src = sAcc + (p0 + t) * kBN + f4 * 4;
-        float4 acc = ld_dsmem_f4(dsmem_addr(src, 0));
-        for (int q = 1; q < S; ++q) {
-          const float4 v = ld_dsmem_f4(dsmem_addr(src, q));
-          acc.x += v.x; acc.y += v.y; acc.z += v.z; acc.w += v.w;
-        }
+        // every rank's partial in flight at once, summed in rank order
+        float4 v[kMaxS];
+#pragma unroll
+        for (int q = 0; q < kMaxS; ++q)
+          if (q < S) v[q] = ld_dsmem_f4(dsmem_addr(src, q));
+        float4 acc = v[0];
+#pragma unroll
+        for (int q = 1; q < kMaxS; ++q)
+          if (q < S) {
+            acc.x += v[q].x; acc.y += v[q].y; acc.z += v[q].z; acc.w += v[q].w;
+          }
         float* d = sT + t * kLD + f4 * 4;
         d[0] = acc.x; d[1] = acc.y; d[2] = acc.z; d[3] = acc.w;
       }
       named_bar(1, 256);
-      epilogue_pass<E>(sT, m0 + p0, min(M, m0 + p0 + rows), Mp, n0, N, ep, et);
+      if (et == 0 && p0 == t_lo) VC_GTRACE(5);
+      epilogue_pass<E>(sT, m0 + p0, min(M, m0 + p0 + rows), Mp, n0, N, ep, et,
+                       p0 == t_lo ? pre0 : EpiPre<E>{});
+      if (et == 0 && p0 == t_lo) VC_GTRACE(6);
       named_bar(1, 256);
     }
   }
   __syncwarp();
   cluster_sync();  // no rank leaves while another may still read its partial
+  if (tid == 64) VC_GTRACE(4);
   if (warp == 1) tmem_dealloc(tbase, kAccCols);
 }
 
@@ -673,7 +761,7 @@ int cluster_splits(int N, int K) {
   const int tiles = N / kBN, KT = K / kBK;
   int S = kP / tiles;
   if (S > cap) S = cap;
-  if (S > 8) S = 8;
+  if (S > kMaxS) S = kMaxS;
   if (S > KT) S = KT;
   if (S < 1) S = 1;
   return S >= min_s ? S : 0;
@@ -694,7 +782,15 @@ cudaError_t launch_nt(const uint16_t* Xt, int Mp, int M, int K, const uint16_t* 
                       const GemmEpilogue& ep, const GemmWorkspace& ws, cudaStream_t st, const GemmNormIn* norm) {
   int S = cluster_splits(N, K);
   if (norm && S < 1) S = std::max(1, std::min(kP / (N / kBN), 8));  // the fused input needs the cluster kernel
-  const GemmNormIn nin = norm ? *norm : GemmNormIn{};
+  GemmNormIn nin = norm ? *norm : GemmNormIn{};
+#ifdef VC_GEMM_TRACE
+  nin.trace = g_gemm_trace_next < kTrLaunches ? g_gemm_trace_next++ : -1;
+  if (nin.trace >= 0) {  // host-side: a symbol copy is not allowed inside a stream capture
+    g_gemm_trace_nk[3 * nin.trace] = N;
+    g_gemm_trace_nk[3 * nin.trace + 1] = K;
+    g_gemm_trace_nk[3 * nin.trace + 2] = S;
+  }
+#endif
   if (S >= 1) {
     auto kc = gemm_cluster_kernel<NT, E>;
     const int smem = Cfg<NT>::kSmem;
@@ -774,6 +870,20 @@ cudaError_t gemm(const uint16_t* Xt, int Mp, int M, int K, const uint16_t* Wt, i
   }
   return cudaErrorInvalidValue;
 }
+
+#ifdef VC_GEMM_TRACE
+extern "C" int vc_gemm_trace_dump(const char* path) {
+  std::vector<unsigned long long> t(static_cast<size_t>(kTrLaunches) * kTrCtas * kTrPts);
+  std::vector<int> nk(g_gemm_trace_nk, g_gemm_trace_nk + kTrLaunches * 3);
+  if (cudaMemcpyFromSymbol(t.data(), g_gemm_trace, t.size() * 8) != cudaSuccess) return 1;
+  FILE* f = std::fopen(path, "wb");
+  if (!f) return 2;
+  std::fwrite(nk.data(), 4, nk.size(), f);
+  std::fwrite(t.data(), 8, t.size(), f);
+  std::fclose(f);
+  return 0;
+}
+#endif
 
 cudaError_t retile_weight(const uint16_t* src, int N, int K, uint16_t* dst, cudaStream_t st) {
   retile_weight_kernel<<<148 * 8, 256, 0, st>>>(src, N, K, dst);

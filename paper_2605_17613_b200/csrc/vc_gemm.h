@@ -51,6 +51,7 @@ struct GemmNormIn {
   const float* ss = nullptr;    // [Mp][H/128] per-tile sums of squares
   const uint16_t* w = nullptr;  // [H] bf16 norm weight
   float eps = 0.f;
+  int trace = -1;  // VC_GEMM_TRACE builds only: this launch's slot in the phase trace
 };
 
 struct GemmWorkspace {
