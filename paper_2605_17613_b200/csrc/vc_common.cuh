@@ -220,6 +220,30 @@ VC_DEV void tma_load_1d(void* dst, const void* src, uint32_t bytes, uint64_t* ba
       "l"(src), "r"(bytes), "r"(smem_u32(bar))
       : "memory");
 }
+// Streamed-once operands (weights, compressed KV records) are read with an
+// L2 evict-first policy so the 15 GB of weights and the compressed cache a step
+// streams do not push out what is re-read soon: activations, partials, the
+// next kernel's code.  VC_L2_HINT=0 builds the plain copy (A/B).
+#ifndef VC_L2_HINT
+#define VC_L2_HINT 1
+#endif
+VC_DEV uint64_t l2_policy_evict_first() {
+  uint64_t p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+VC_DEV void tma_load_1d_stream(void* dst, const void* src, uint32_t bytes, uint64_t* bar, uint64_t policy) {
+#if VC_L2_HINT
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint [%0], [%1], %2, [%3], %4;" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar)), "l"(policy)
+      : "memory");
+#else
+  (void)policy;
+  tma_load_1d(dst, src, bytes, bar);
+#endif
+}
 // Bulk prefetch of global memory into L2 (no shared-memory destination).
 VC_DEV void prefetch_l2_bulk(const void* src, uint32_t bytes) {
   asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes) : "memory");

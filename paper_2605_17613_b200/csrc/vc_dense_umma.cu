@@ -212,13 +212,22 @@ __global__ void __launch_bounds__(kThreads, 1)
   if (have0 && I0.k_hi <= I0.kv_len - I0.n_tok) first_static = I0.n_tiles < 2 ? I0.n_tiles : 2;
   if (warp != 0 && warp != 6) pdl_wait();  // q rows and the window's new K/V come from the qkv epilogue
 
-  // one pool tile (K or V) of item I, tile t, into stage st
+  // one pool tile (K or V) of item I, tile t, into stage st.  With one row
+  // block per window nothing re-reads a tile, so it streams through L2
+  // evict-first; wider windows' row blocks re-read it from L2 (normal policy)
+  const uint64_t kv_pol = l2_policy_evict_first();
   auto load_kv = [&](const CUtensorMap* map, uint8_t* dst, uint64_t* bar, const Item& I, int t) {
     const int slice_row = static_cast<int>(((static_cast<size_t>(I.slot) * s.layers + layer) * s.n_kv + I.h) *
                                            static_cast<size_t>(pool_cap));
     mbar_expect_tx(bar, KV_BYTES);
+    if (row_blocks == 1) {
 #pragma unroll
-    for (int a = 0; a < ATOMS; ++a) tma_load_2d(dst + a * KV_ATOM, map, a * 64, slice_row + I.k_lo + t * kTile, bar);
+      for (int a = 0; a < ATOMS; ++a)
+        tma_load_2d_hint(dst + a * KV_ATOM, map, a * 64, slice_row + I.k_lo + t * kTile, bar, kv_pol);
+    } else {
+#pragma unroll
+      for (int a = 0; a < ATOMS; ++a) tma_load_2d(dst + a * KV_ATOM, map, a * 64, slice_row + I.k_lo + t * kTile, bar);
+    }
   };
   if (warp == 0) {
     // ===================== TMA producer =====================

@@ -293,12 +293,13 @@ __global__ void __launch_bounds__(kWarps * 32, NREP == 8 ? 3 : VC_DRAFT_MINB) dr
     const uint32_t* src = pc.slice + static_cast<size_t>(pc.g) * GEO::GREC;
     uint32_t* dst = stage0 + st * GEO::STAGE;
     if (lane == 0) {
+      const uint64_t pol = l2_policy_evict_first();  // each record is read once per step
       if (ppart == 0) {
         mbar_expect_tx(bar + st, GEO::STAGE * 4);
-        tma_load_1d(dst, src, GEO::STAGE * 4, bar + st);
+        tma_load_1d_stream(dst, src, GEO::STAGE * 4, bar + st, pol);
       } else {
         mbar_expect_tx(bar + st, GEO::UREC * 4);
-        tma_load_1d(dst + GEO::OFF_K, src + D + ppart * GEO::UREC, GEO::UREC * 4, bar + st);
+        tma_load_1d_stream(dst + GEO::OFF_K, src + D + ppart * GEO::UREC, GEO::UREC * 4, bar + st, pol);
       }
     }
     if (++ppart == kUPG) {

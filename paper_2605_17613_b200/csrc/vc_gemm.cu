@@ -552,9 +552,10 @@ gemm_cluster_kernel(const uint16_t* __restrict__ Xt, int Mp, int M, int K,
     if (lane == 0) {
       const int pre = min(ST, nk);
       const uint32_t tx = fused ? WB : WB + XB;
+      const uint64_t pol = l2_policy_evict_first();  // weights are read once per step
       for (int i = 0; i < pre; ++i) {  // weights do not depend on the previous kernel
         mbar_expect_tx(&full[i], tx);
-        tma_load_1d(sW + i * WB, Wt + (static_cast<size_t>(tile) * KT + k_lo + i) * 8192, WB, &full[i]);
+        tma_load_1d_stream(sW + i * WB, Wt + (static_cast<size_t>(tile) * KT + k_lo + i) * 8192, WB, &full[i], pol);
       }
       pdl_wait();
       VC_GTRACE(1);
@@ -565,7 +566,7 @@ gemm_cluster_kernel(const uint16_t* __restrict__ Xt, int Mp, int M, int K,
         const int st = i % ST;
         mbar_wait(&empty[st], ((i / ST) - 1) & 1);
         mbar_expect_tx(&full[st], tx);
-        tma_load_1d(sW + st * WB, Wt + (static_cast<size_t>(tile) * KT + k_lo + i) * 8192, WB, &full[st]);
+        tma_load_1d_stream(sW + st * WB, Wt + (static_cast<size_t>(tile) * KT + k_lo + i) * 8192, WB, &full[st], pol);
         if (!fused) tma_load_1d(sX + st * XB, Xt + (static_cast<size_t>(k_lo + i) * Mp + m0) * 64, XB, &full[st]);
       }
     }
