@@ -1,4 +1,4 @@
-# host-tier draft horizon sweep (ring streaming makes the verify window independent of the drafting step's tile)
+# Host-tier draft-horizon sweep (bench.py --tier host --x N)
 for x in 63 95 47; do
 timeout 1200 python bench.py --tier host --x $x --no-cpu --no-secondary > gpurun_out/hx_$x.json 2> gpurun_out/hx_$x.err; echo "x=$x rc=$?"
 python - <<PY
