@@ -3,6 +3,8 @@
 // chunks) and of the dense kernel (vc_dense_umma.cu: VC_DENSE_CHUNK-key
 // absolute chunks) in a fixed order, and writes bf16 attention rows (row-major
 // or in the o_proj GEMM's tiled layout).
+#include <cstdio>
+
 #include "vc_common.cuh"
 #include "vc_kernels.h"
 #include "vc_tiled.cuh"
@@ -12,8 +14,29 @@ namespace {
 
 constexpr int kMaxParts = 512;  // chunks per sequence the combine can merge (256K ctx)
 
+#ifdef VC_COMBINE_TRACE
+// Diagnostics build: per CTA (blockIdx.x + gridDim.x * blockIdx.z < 4096) of
+// every launch, globaltimer at start / after the index math / after the PDL
+// wait / after the (m, l) loads / after M, l / at exit.  Read back with
+// vc_combine_trace_dump (tools/_trace).
+__device__ unsigned long long g_comb_trace[64][4096][6];
+__device__ int g_comb_launch;
+#define VC_CTRACE(pt)                                                                   \
+  do {                                                                                  \
+    const int cid = blockIdx.x + gridDim.x * blockIdx.z;                                \
+    if (threadIdx.x == 0 && cid < 4096) g_comb_trace[ctr_l & 63][cid][pt] = vc_globaltimer(); \
+  } while (0)
+#else
+#define VC_CTRACE(pt)
+#endif
+
 template <int D>
 __global__ void combine_kernel(AttnShape s, CombineSets cs, Partials part, uint16_t* out) {
+#ifdef VC_COMBINE_TRACE
+  const int ctr_l = cs.n_sets >> 8;
+  cs.n_sets &= 255;
+#endif
+  VC_CTRACE(0);
   pdl_trigger();
   // Everything up to the partial-row indices depends only on the step's
   // sequence table (host-written before the step, never by a kernel), so it
@@ -60,54 +83,54 @@ __global__ void combine_kernel(AttnShape s, CombineSets cs, Partials part, uint1
   // draft mode: the tail-chunk partials are merged after the quantised chunks, in order
   const int n_tail = mode == 0 ? (sq.tail_len + VC_TAIL_CHUNK - 1) / VC_TAIL_CHUNK : 0;
   const int n_all = n_parts + n_tail;
-  __shared__ float s_m[kMaxParts], s_f[kMaxParts], s_lp[kMaxParts];
+  __shared__ float s_m[kMaxParts], s_lp[kMaxParts];
   __shared__ size_t s_row[kMaxParts];
-  __shared__ float s_l;
   for (int c = threadIdx.x; c < n_all; c += blockDim.x)
     s_row[c] = prow_of(c < n_parts ? c : max_chunks + (c - n_parts));
   __syncthreads();
+  VC_CTRACE(1);
   pdl_wait();
+  VC_CTRACE(2);
+#ifdef VC_COMBINE_NOOP
+  return;  // diagnostics build: the launch and its PDL boundary without the merge
+#endif
   for (int c = threadIdx.x; c < n_all; c += blockDim.x) {  // every (m, l) load in parallel
     const float2 ml = *reinterpret_cast<const float2*>(part.ml + s_row[c] * 2);
     s_m[c] = ml.x;
     s_lp[c] = ml.y;
   }
   __syncthreads();
-  if (threadIdx.x < 32) {  // warp 0: M (exact, order-free), weights, l by a fixed lane-strided + xor tree
-    const int ln = threadIdx.x;
-    float M = -INFINITY;
-    for (int c = ln; c < n_all; c += 32) M = fmaxf(M, s_m[c]);
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) M = fmaxf(M, __shfl_xor_sync(0xffffffffu, M, o));
-    float l = 0.f;
-    for (int c = ln; c < n_all; c += 32) {
-      const float f = (s_m[c] == -INFINITY) ? 0.f : exp2f(s_m[c] - M);
-      s_f[c] = f;
-      l = fmaf(f, s_lp[c], l);
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) l += __shfl_xor_sync(0xffffffffu, l, o);
-    if (ln == 0) s_l = l;
-  }
-  __syncthreads();
-  const float l = s_l;
+  VC_CTRACE(3);
+  // Every thread (= one channel) merges on its own: M, then the weights, l
+  // and O in chunk order.  Short loops instead of a warp-0 reduction and a
+  // second barrier: this kernel runs once per layer with cold instruction
+  // caches, so its cost is mostly its code footprint (r2 phase trace: the
+  // shuffle-tree version spent 2.2 us per CTA computing M and l).
+  float M = -INFINITY;
+  for (int c = 0; c < n_all; ++c) M = fmaxf(M, s_m[c]);
+  VC_CTRACE(4);
+  const int c0 = threadIdx.x;  // blockDim.x == D
+  float l = 0.f, o = 0.f;
   constexpr int kBatch = 16;  // partial rows in flight per thread
-  for (int c0 = threadIdx.x; c0 < D; c0 += blockDim.x) {
-    float o = 0.f;
-    for (int c = 0; c < n_all; c += kBatch) {
-      float v[kBatch];
+  for (int c = 0; c < n_all; c += kBatch) {
+    float v[kBatch];
 #pragma unroll
-      for (int j = 0; j < kBatch; ++j) v[j] = c + j < n_all ? part.o[s_row[c + j] * D + c0] : 0.f;
+    for (int j = 0; j < kBatch; ++j) v[j] = c + j < n_all ? part.o[s_row[c + j] * D + c0] : 0.f;
 #pragma unroll
-      for (int j = 0; j < kBatch; ++j)
-        if (c + j < n_all) o = fmaf(s_f[c + j], v[j], o);  // fixed (chunk) order
-    }
-    const uint16_t v = f2bf(l > 0.f ? o / l : 0.f);
-    if (s.out_mp > 0)
-      out[atile_idx(sq.row0 + tok, hq * D + c0, s.out_mp)] = v;
-    else
-      out[static_cast<size_t>(sq.row0 + tok) * s.out_stride + static_cast<size_t>(hq) * D + c0] = v;
+    for (int j = 0; j < kBatch; ++j)
+      if (c + j < n_all) {
+        const float mc = s_m[c + j];
+        const float f = mc == -INFINITY ? 0.f : exp2f(mc - M);
+        l = fmaf(f, s_lp[c + j], l);
+        o = fmaf(f, v[j], o);
+      }
   }
+  const uint16_t v = f2bf(l > 0.f ? o / l : 0.f);
+  if (s.out_mp > 0)
+    out[atile_idx(sq.row0 + tok, hq * D + c0, s.out_mp)] = v;
+  else
+    out[static_cast<size_t>(sq.row0 + tok) * s.out_stride + static_cast<size_t>(hq) * D + c0] = v;
+  VC_CTRACE(5);
 }
 
 }  // namespace
@@ -122,6 +145,12 @@ cudaError_t attention_combine_sets(const AttnShape& s, const CombineSets& cs, Pa
   }
   if (n <= 0) return cudaSuccess;
   dim3 grid(n, 1, s.n_kv * s.n_rep);
+#ifdef VC_COMBINE_TRACE
+  static int launch_no = 0;
+  CombineSets ct = cs;
+  ct.n_sets |= (launch_no++ & 63) << 8;
+  if (s.d == 128) return launch_pdl(combine_kernel<128>, grid, dim3(128), 0, st, s, ct, part, out);
+#endif
   if (s.d == 128) return launch_pdl(combine_kernel<128>, grid, dim3(128), 0, st, s, cs, part, out);
   if (s.d == 64) return launch_pdl(combine_kernel<64>, grid, dim3(64), 0, st, s, cs, part, out);
   return cudaErrorInvalidValue;
@@ -140,5 +169,17 @@ cudaError_t attention_combine(const AttnShape& s, const AttnSeq* seqs, int n_seq
   cs.n_sets = 1;
   return attention_combine_sets(s, cs, part, out, st);
 }
+
+#ifdef VC_COMBINE_TRACE
+extern "C" int vc_combine_trace_dump(const char* path) {
+  static unsigned long long h[64][4096][6];
+  if (cudaMemcpyFromSymbol(h, g_comb_trace, sizeof(h)) != cudaSuccess) return 1;
+  FILE* f = std::fopen(path, "wb");
+  if (!f) return 2;
+  std::fwrite(h, 1, sizeof(h), f);
+  std::fclose(f);
+  return 0;
+}
+#endif
 
 }  // namespace vc
