@@ -190,11 +190,12 @@ __global__ void __launch_bounds__(kWarps * 32, NREP == 8 ? 3 : VC_DRAFT_MINB) dr
   constexpr int kUPG = kG / kUnit;
 
   extern __shared__ __align__(128) uint32_t dsm[];   // [kWarps][2][STAGE]
-  // per-warp q, fp32 pre-scaled by scale_log2, laid out [channel pair][8 head
-  // columns] (padding heads zero) so the group setup reads one conflict-free
-  // float2 per lane; the tail CTAs reuse it for NREP*D fp32 q values
-  __shared__ __align__(16) float2 sq_q[kWarps][D / 2 * 8];
-  static_assert(kWarps * (D / 2) * 8 * 2 >= NREP * D, "tail q fits");
+  // per-warp q, fp32 pre-scaled by scale_log2, laid out [channel pair][NREP
+  // heads] so the group setup reads one float2 per lane (lanes feeding a
+  // padding head column, hn >= NREP, use zeros); the tail CTAs reuse it for
+  // NREP*D fp32 q values
+  __shared__ __align__(16) float2 sq_q[kWarps][D / 2 * NREP];
+  static_assert(kWarps * (D / 2) * NREP * 2 >= NREP * D, "tail q fits");
   __shared__ __align__(8) uint64_t bars[kWarps][kStages];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -391,15 +392,11 @@ __global__ void __launch_bounds__(kWarps * 32, NREP == 8 ? 3 : VC_DRAFT_MINB) dr
     const uint16_t* qrow = qkv + static_cast<size_t>(seqs[cur.seq].row0) * s.q_stride +
                            static_cast<size_t>(cur.head) * NREP * D;
     __syncwarp();
-    for (int i = lane; i < D / 2 * 8; i += 32) {
-      const int cp = i >> 3, h = i & 7;
-      float2 v = make_float2(0.f, 0.f);
-      if (h < NREP) {
-        const uint32_t qq = *reinterpret_cast<const uint32_t*>(qrow + h * D + 2 * cp);
-        v = make_float2(bf2f(static_cast<uint16_t>(qq & 0xffffu)) * s.scale_log2,
-                        bf2f(static_cast<uint16_t>(qq >> 16)) * s.scale_log2);
-      }
-      sq_q[warp][i] = v;
+    for (int i = lane; i < D / 2 * NREP; i += 32) {
+      const int cp = i / NREP, h = i % NREP;
+      const uint32_t qq = *reinterpret_cast<const uint32_t*>(qrow + h * D + 2 * cp);
+      sq_q[warp][i] = make_float2(bf2f(static_cast<uint16_t>(qq & 0xffffu)) * s.scale_log2,
+                                  bf2f(static_cast<uint16_t>(qq >> 16)) * s.scale_log2);
     }
     __syncwarp();
   };
@@ -426,7 +423,8 @@ __global__ void __launch_bounds__(kWarps * 32, NREP == 8 ? 3 : VC_DRAFT_MINB) dr
       // part in fp32 FFMAs, the -1024 part (over the fp16 q' the MMA sees) by
       // one extra MMA per k-step against a constant-1024 A tile
       float bias_part = 0.f;
-      const float2* qf = sq_q[warp] + hn;
+      const float2* qf = sq_q[warp] + (hn < NREP ? hn : 0);
+      const bool live_col = hn < NREP;
 #pragma unroll
       for (int k = 0; k < KS; ++k) {
         const int c0 = k * 16 + 2 * (lane & 3);
@@ -434,7 +432,7 @@ __global__ void __launch_bounds__(kWarps * 32, NREP == 8 ? 3 : VC_DRAFT_MINB) dr
         for (int hi = 0; hi < 2; ++hi) {  // channels c0,c0+1 then c0+8,c0+9
           const int c = c0 + 8 * hi;
           const uint2 sz = *reinterpret_cast<const uint2*>(sb + GEO::OFF_KSZ + c);  // (s_c|z_c), (s_c1|z_c1)
-          const float2 q = qf[(c >> 1) * 8];
+          const float2 q = live_col ? qf[(c >> 1) * NREP] : make_float2(0.f, 0.f);
           const uint32_t q16 = hi ? pack_h2(q.x * kHiScale, q.y * kHiScale) : pack_h2(q.x, q.y);
           const uint32_t bq = hmul2_u32(q16, __byte_perm(sz.x, sz.y, 0x5410));
           const float2 z = h2_to_f2(__byte_perm(sz.x, sz.y, 0x7632));
