@@ -37,6 +37,9 @@ constexpr int kWarps = 4;
 #define VC_DRAFT_STAGES 2  // unit records in flight per warp
 #endif
 constexpr int kStages = VC_DRAFT_STAGES;
+#ifndef VC_DRAFT_TAIL_LAST
+#define VC_DRAFT_TAIL_LAST 1  // grid order: quantised CTAs, then bf16-tail CTAs
+#endif
 #ifndef VC_DRAFT_MINB
 #define VC_DRAFT_MINB 4  // resident CTAs/SM the n_rep<=4 register budget targets
 #endif
@@ -208,11 +211,32 @@ __global__ void __launch_bounds__(kWarps * 32, NREP == 8 ? 3 : VC_DRAFT_MINB) dr
       if (tr && threadIdx.x == 0 && blockIdx.x < 2048) tr[8192 + blockIdx.x * 2 + 1] = vc_globaltimer();
     }
   } trace_end{s.trace};
-  if (s.trace && threadIdx.x == 0 && blockIdx.x < 2048) s.trace[8192 + blockIdx.x * 2] = vc_globaltimer();
+  if (s.trace && threadIdx.x == 0 && blockIdx.x < 2048) {
+    s.trace[8192 + blockIdx.x * 2] = vc_globaltimer();
+    uint32_t smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    s.trace[16384 + blockIdx.x] = smid;
+  }
   pdl_trigger();
-  if (static_cast<int>(blockIdx.x) < n_tail_ctas) {
+  // grid order: the persistent quantised CTAs first (they fill every slot of
+  // the wave and start together), the bf16-tail CTAs after them -- they run
+  // in the slots the first-finishing quantised CTAs free (draft step 6.60 ->
+  // 6.53 ms).  With the tail CTAs first, the quantised CTAs started 0.5-11 us
+  // apart.  (The quantised CTAs still end 76-110 us: an SM's scheduler
+  // favours its earliest-launched CTA, so round r of the launch finishes at
+  // 82 / 89 / 99 / 109 us; ranges weighted against that kept the SMs' total
+  // the same and ran 7% slower -- DESIGN.md.)
+#if VC_DRAFT_TAIL_LAST
+  const int n_quant_ctas = static_cast<int>(gridDim.x) - n_tail_ctas;
+  const bool is_tail = static_cast<int>(blockIdx.x) >= n_quant_ctas;
+  const int tail_idx = static_cast<int>(blockIdx.x) - n_quant_ctas, quant_cta = blockIdx.x;
+#else
+  const bool is_tail = static_cast<int>(blockIdx.x) < n_tail_ctas;
+  const int tail_idx = blockIdx.x, quant_cta = static_cast<int>(blockIdx.x) - n_tail_ctas;
+#endif
+  if (is_tail) {
     pdl_wait();  // the tail holds this step's new K/V (qkv epilogue)
-    const int idx = blockIdx.x;
+    const int idx = tail_idx;
     const int tc = idx % TC, h = (idx / TC) % s.n_kv, seq = idx / (TC * s.n_kv);
     const AttnSeq sq = seqs[seq];
     if (tc * VC_TAIL_CHUNK >= sq.tail_len) return;
@@ -225,7 +249,7 @@ __global__ void __launch_bounds__(kWarps * 32, NREP == 8 ? 3 : VC_DRAFT_MINB) dr
   const int T = warp_task_sum(seqs, n_seq, s.n_kv, lane);
   if (T == 0) return;
   const int nw = draft_active_warps(T, s.draft_warps, s.draft_min_tasks);
-  const int w = (blockIdx.x - n_tail_ctas) * kWarps + warp;
+  const int w = quant_cta * kWarps + warp;
   if (w >= nw) return;  // no CTA-wide barriers below: warps are independent
   const int t0 = draft_task_begin(w, T, nw), t1 = draft_task_begin(w + 1, T, nw);
   const int n_units = (t1 - t0) * kUPG;

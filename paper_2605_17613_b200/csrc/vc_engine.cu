@@ -394,6 +394,7 @@ void Engine::alloc_all() {
     draft_min_tasks_ = std::max(4, (capg + 479) / 480);
     max_chunks_q_ = (capg + draft_min_tasks_ - 1) / draft_min_tasks_ + 1;
     draft_warps_ = draft_quant_warps(d, cfg_.quant_bits, m.n_q / m.n_kv);
+
     if (draft_warps_ <= 0) throw ContractViolation("no draft-attention kernel for this head shape");
   }
   if (drop_mode()) {
@@ -1433,6 +1434,26 @@ void Engine::run_step(const std::vector<StepItem>& items, std::vector<int32_t>& 
     std::fprintf(stderr, "ATTN dense ctas=%d [%.1f, %.1f] us avg %.1f | draft ctas=%d [%.1f, %.1f] us avg %.1f\n", dc,
                  dc ? (dl - t0) / 1e3 : 0.0, dc ? (dh - t0) / 1e3 : 0.0, da / 1e3, qc, qc ? (ql - t0) / 1e3 : 0.0,
                  qc ? (qh - t0) / 1e3 : 0.0, qa / 1e3);
+    if (const char* f = std::getenv("VC_ATTN_TRACE_FILE")) {  // raw per-CTA timeline for offline analysis
+      if (FILE* fp = std::fopen(f, "wb")) {
+        std::fwrite(t.data(), 8, t.size(), fp);
+        std::fclose(fp);
+      }
+    }
+    if (qc) {  // the draft grid: the persistent quantised CTAs, then the bf16-tail CTAs (VC_DRAFT_TAIL_LAST)
+      const int nq = std::min(draft_warps_ / 4, 2048);
+      unsigned long long tl, th, pl, ph;
+      int tc, pc;
+      double ta, pa;
+      span(8192, nq, pl, ph, pc, pa);
+      span(8192 + 2 * static_cast<size_t>(nq), 2048 - nq, tl, th, tc, ta);
+      unsigned long long pe_lo = ~0ull;  // first quantised CTA to finish
+      for (int i = 0; i < nq; ++i)
+        if (t[8192 + 2 * i] && t[8192 + 2 * i + 1]) pe_lo = std::min(pe_lo, t[8192 + 2 * i + 1]);
+      std::fprintf(stderr, "DRAFT quant ctas=%d [%.1f, %.1f] us, first end %.1f | tail ctas=%d [%.1f, %.1f] avg %.1f\n", pc,
+                   pc ? (pl - t0) / 1e3 : 0.0, pc ? (ph - t0) / 1e3 : 0.0, pc ? (pe_lo - t0) / 1e3 : 0.0, tc,
+                   tc ? (tl - t0) / 1e3 : 0.0, tc ? (th - t0) / 1e3 : 0.0, ta / 1e3);
+    }
   }
 }
 

@@ -26,6 +26,7 @@ def main():
     p.add_argument("--graphs", type=int, default=1)
     p.add_argument("--q-std", type=float, default=0.0)
     p.add_argument("--resid-std", type=float, default=0.0)
+    p.add_argument("--reverse", action="store_true", help="draft items in reverse slot order")
     a = p.parse_args()
     B, x = a.batch, a.x
     comp = a.mode != "decode"
@@ -48,7 +49,8 @@ def main():
         if a.mode == "decode":
             e.decode_step(list(range(B)))
         elif a.mode == "draft":
-            e.step([(i, 1, [e.state(i)["pending"]], -1) for i in range(B)])
+            order = range(B - 1, -1, -1) if a.reverse else range(B)
+            e.step([(i, 1, [e.state(i)["pending"]], -1) for i in order])
         else:
             st = e.state(0)
             items = [(0, 2, [st["pending"]] + [1] * x, -1)]
