@@ -43,7 +43,35 @@ constexpr int kStages = VC_DRAFT_STAGES;
 #ifndef VC_DRAFT_MINB
 #define VC_DRAFT_MINB 4  // resident CTAs/SM the n_rep<=4 register budget targets
 #endif
+#ifndef VC_DRAFT_BIAS_MMA
+// the 1024 * sum(P') correction by one MMA per tile instead of per-lane
+// f16->f32 sums: int2 needs it (its rows +8 carry a x4, below); for int4 it
+// measured neutral (16 x 32K set 3.674 vs 3.670 ms) and stays off
+#define VC_DRAFT_BIAS_MMA 0
+#endif
+#ifndef VC_INT2_NOSHIFT
+#define VC_INT2_NOSHIFT 1  // int2: four masks per byte, rows +8 carry a x4 the epilogues undo
+#endif
+#ifndef VC_SHIFT_IMAD
+// the unpack's byte shift as IMAD.HI (FMA pipe) instead of SHF (ALU pipe,
+// with the lop3s): measured slower (16 x 32K int4 set 3.67 -> 4.14 ms, int2
+// 3.47 -> 3.64: the IMAD's latency lands on every A fragment), so off
+#define VC_SHIFT_IMAD 0
+#endif
 constexpr int kUnit = VC_QUNIT;  // tokens per pipeline unit = one unit record
+
+// x >> 8.  The unpack is ALU-pipe heavy (lop3 + the shift: 55% of the ALU
+// pipe, whose throttle is a top stall); mul.hi by 2^24 would run on the FMA
+// pipe (ptxas keeps it an IMAD.HI.U32) -- slower, see VC_SHIFT_IMAD.
+VC_DEV uint32_t shr8(uint32_t x) {
+#if VC_SHIFT_IMAD
+  uint32_t r;
+  asm("mul.hi.u32 %0, %1, %2;" : "=r"(r) : "r"(x), "r"(0x01000000u));
+  return r;
+#else
+  return x >> 8;
+#endif
+}
 constexpr float kTau = 8.0f;      // lazy rescale: running max may lag the true max by 2^8
 
 template <int D, int BITS>
@@ -337,23 +365,37 @@ __global__ void __launch_bounds__(kWarps * 32, NREP == 8 ? 3 : VC_DRAFT_MINB) dr
   // the matching 1/16.  int2: word holds two k-steps, sub selects one.
   auto unpack = [&](uint32_t wd, int sub, uint32_t* a) {
     if constexpr (BITS == 4) {
-      const uint32_t w8 = wd >> 8;
+      const uint32_t w8 = shr8(wd);
       a[0] = nib_to_h2(wd, 0x000f000fu);
       a[1] = nib_to_h2(w8, 0x000f000fu);
       a[2] = nib_to_h2(wd, 0x00f000f0u);
       a[3] = nib_to_h2(w8, 0x00f000f0u);
     } else {
-      // int2: code j of a byte sits at bits 2j; pairs 0/1 read bits 0-1 of the
-      // byte and of the byte >> 2, pairs 2/3 bits 4-5 of the same two words
-      // (1024 + 16c, scaled back by the B operand like int4): 3 shifts + 8
-      // lop3 per word of 16 codes instead of a shift per pair
+      // int2: code j of a byte sits at bits 2j.  Pairs 2/3 (k or token +8)
+      // read bits 4-7 (1024 + 16c, scaled back by the B operand like int4).
+#if VC_INT2_NOSHIFT
+      // Rows +8 (a[1], a[3]) read bits 2-3 / 6-7 of the same byte in place:
+      // 1024 + 4c / 1024 + 64c, so their code part carries a x4 that the
+      // score epilogue (K) and the O fold / emit (V) divide out: 1 shift + 8
+      // lop3 per word of 16 codes
+      const uint32_t lo = sub ? shr8(wd) : wd;
+      a[0] = nib_to_h2(lo, 0x00030003u);
+      a[1] = nib_to_h2(lo, 0x000c000cu);
+      a[2] = nib_to_h2(lo, 0x00300030u);
+      a[3] = nib_to_h2(lo, 0x00c000c0u);
+#else
       const uint32_t lo = sub ? wd >> 8 : wd, lo2 = lo >> 2;
       a[0] = nib_to_h2(lo, 0x00030003u);
       a[1] = nib_to_h2(lo2, 0x00030003u);
       a[2] = nib_to_h2(lo, 0x00300030u);
       a[3] = nib_to_h2(lo2, 0x00300030u);
+#endif
     }
   };
+  // x4 on the code part of rows +8 (int2, VC_INT2_NOSHIFT); 1 otherwise.
+  // 16 x 32K int2 set: 3.674 ms (3 shifts per word) -> 3.473 ms
+  constexpr float kRow8 = (BITS == 2 && VC_INT2_NOSHIFT) ? 4.f : 1.f;
+  constexpr bool kBiasMma = VC_DRAFT_BIAS_MMA || kRow8 != 1.f;
   constexpr float kHiScale = 0.0625f;  // B-operand scale of pairs 2/3 (their A holds 1024 + 16c)
   if (lane == 0) {
     for (int i = 0; i < kStages; ++i) mbar_init(bar + i, 1);
@@ -368,22 +410,44 @@ __global__ void __launch_bounds__(kWarps * 32, NREP == 8 ? 3 : VC_DRAFT_MINB) dr
   const int Hq = s.n_kv * NREP;
   float mrun0, mrun1, lsum0, lsum1, corr0, corr1;
   float oacc[KS][4];
+  // kBiasMma: corr holds the zero-point part sum(p * vzero) per lane,
+  // bacc (an MMA accumulator, A = 1024) the int->fp16 bias 1024 * sum(P') of
+  // columns hc0 / hc0+1 over the whole warp (C-fragment [0] / [1]); else corr
+  // holds both parts per lane
+  float bacc[4];
   auto reset = [&]() {
     mrun0 = mrun1 = -INFINITY;
     lsum0 = lsum1 = corr0 = corr1 = 0.f;
+    bacc[0] = bacc[1] = bacc[2] = bacc[3] = 0.f;
 #pragma unroll
     for (int ct = 0; ct < KS; ++ct) oacc[ct][0] = oacc[ct][1] = oacc[ct][2] = oacc[ct][3] = 0.f;
   };
+  // the O corrections of rows g (A) and g+8 (B, whose code part carries kRow8)
+  // from the warp-reduced zero-point sums z and the bias sums
+  auto corrections = [&](float z0, float z1, float& a0, float& a1, float& b0, float& b1) {
+    if constexpr (kBiasMma) {
+      a0 = z0 - bacc[0];
+      a1 = z1 - bacc[1];
+      b0 = kRow8 * z0 - bacc[0];
+      b1 = kRow8 * z1 - bacc[1];
+    } else {
+      a0 = b0 = z0;
+      a1 = b1 = z1;
+    }
+  };
   // the partial of the consumer's current (sequence, head)
   auto emit = [&]() {
-    float l0 = lsum0, l1 = lsum1, c0 = corr0, c1 = corr1;
+    float l0 = lsum0, l1 = lsum1, z0 = corr0, z1 = corr1;
 #pragma unroll
     for (int o = 4; o < 32; o <<= 1) {  // over the 8 lanes sharing a head column
       l0 += __shfl_xor_sync(0xffffffffu, l0, o);
       l1 += __shfl_xor_sync(0xffffffffu, l1, o);
-      c0 += __shfl_xor_sync(0xffffffffu, c0, o);
-      c1 += __shfl_xor_sync(0xffffffffu, c1, o);
+      z0 += __shfl_xor_sync(0xffffffffu, z0, o);
+      z1 += __shfl_xor_sync(0xffffffffu, z1, o);
     }
+    float c0, c1, c08, c18;
+    corrections(z0, z1, c0, c1, c08, c18);
+    constexpr float kInv8 = 1.f / kRow8;
     const int p0 = cur.base + cur.head * cur.ng;  // first task of the (sequence, head)
     const int slot = w - draft_task_warp(p0, T, nw);
     const size_t prow = static_cast<size_t>(seqs[cur.seq].part0 + slot) * Hq + cur.head * NREP + hc0;
@@ -392,7 +456,7 @@ __global__ void __launch_bounds__(kWarps * 32, NREP == 8 ? 3 : VC_DRAFT_MINB) dr
       for (int ct = 0; ct < KS; ++ct) {
         const int c = ct * 16 + (lane >> 2);
         part.o[prow * D + c] = oacc[ct][0] + c0;
-        part.o[prow * D + c + 8] = oacc[ct][2] + c0;
+        part.o[prow * D + c + 8] = (oacc[ct][2] + c08) * kInv8;
       }
       if (lane < 4) {
         part.ml[prow * 2] = mrun0;
@@ -404,7 +468,7 @@ __global__ void __launch_bounds__(kWarps * 32, NREP == 8 ? 3 : VC_DRAFT_MINB) dr
       for (int ct = 0; ct < KS; ++ct) {
         const int c = ct * 16 + (lane >> 2);
         part.o[(prow + 1) * D + c] = oacc[ct][1] + c1;
-        part.o[(prow + 1) * D + c + 8] = oacc[ct][3] + c1;
+        part.o[(prow + 1) * D + c + 8] = (oacc[ct][3] + c18) * kInv8;
       }
       if (lane < 4) {
         part.ml[(prow + 1) * 2] = mrun1;
@@ -427,7 +491,7 @@ __global__ void __launch_bounds__(kWarps * 32, NREP == 8 ? 3 : VC_DRAFT_MINB) dr
   reset();
   load_q();
   uint32_t b0[KS], b1[KS];
-  float bias0 = 0.f, bias1 = 0.f;
+  float bias0 = 0.f, bias1 = 0.f, bias08 = 0.f, bias18 = 0.f;
   int cpart = 0;
 
   for (int u = 0; u < n_units; ++u) {
@@ -470,8 +534,12 @@ __global__ void __launch_bounds__(kWarps * 32, NREP == 8 ? 3 : VC_DRAFT_MINB) dr
       for (int k = 0; k < KS; ++k) mma_f16(c1024, kA1024, kA1024, kA1024, kA1024, b0[k], b1[k]);
       bias_part += __shfl_xor_sync(0xffffffffu, bias_part, 1);
       bias_part += __shfl_xor_sync(0xffffffffu, bias_part, 2);
-      bias0 = __shfl_sync(0xffffffffu, bias_part, hc0 * 4) - c1024[0];
-      bias1 = __shfl_sync(0xffffffffu, bias_part, (hc0 + 1) * 4) - c1024[1];
+      const float zq0 = __shfl_sync(0xffffffffu, bias_part, hc0 * 4);
+      const float zq1 = __shfl_sync(0xffffffffu, bias_part, (hc0 + 1) * 4);
+      bias0 = zq0 - c1024[0];
+      bias1 = zq1 - c1024[1];
+      bias08 = zq0 - c1024[0] * (1.f / kRow8);  // rows +8: raw / kRow8 + bias08
+      bias18 = zq1 - c1024[1] * (1.f / kRow8);
     }
 
     // S^T tiles of the unit's kUnit tokens
@@ -497,7 +565,13 @@ __global__ void __launch_bounds__(kWarps * 32, NREP == 8 ? 3 : VC_DRAFT_MINB) dr
         unpack((BITS == 4) ? kw[k] : kw[k >> 1], k & 1, a);
         mma_f16(sacc[m], a[0], a[1], a[2], a[3], b0[k], b1[k]);
       }
-      sacc[m][0] += bias0; sacc[m][1] += bias1; sacc[m][2] += bias0; sacc[m][3] += bias1;
+      sacc[m][0] += bias0; sacc[m][1] += bias1;
+      if constexpr (kRow8 == 1.f) {
+        sacc[m][2] += bias0; sacc[m][3] += bias1;
+      } else {
+        sacc[m][2] = fmaf(sacc[m][2], 1.f / kRow8, bias08);
+        sacc[m][3] = fmaf(sacc[m][3], 1.f / kRow8, bias18);
+      }
     }
 
     // online softmax (columns hc0, hc0+1; rows spread over lane>>2 and +8)
@@ -520,6 +594,9 @@ __global__ void __launch_bounds__(kWarps * 32, NREP == 8 ? 3 : VC_DRAFT_MINB) dr
       mrun0 = mn0;
       mrun1 = mn1;
       lsum0 *= al0; lsum1 *= al1; corr0 *= al0; corr1 *= al1;
+      if constexpr (kBiasMma) {
+        bacc[0] *= al0; bacc[1] *= al1;
+      }
 #pragma unroll
       for (int ct = 0; ct < KS; ++ct) {
         oacc[ct][0] *= al0; oacc[ct][1] *= al1; oacc[ct][2] *= al0; oacc[ct][3] *= al1;
@@ -536,11 +613,21 @@ __global__ void __launch_bounds__(kWarps * 32, NREP == 8 ? 3 : VC_DRAFT_MINB) dr
       lsum1 += p1 + p3;
       const uint32_t pk01 = pack_h2(p0 * sza.x, p1 * sza.x);
       const uint32_t pk23 = pack_h2(p2 * szb.x * kHiScale, p3 * szb.x * kHiScale);  // tokens +8
-      const float2 h01 = h2_to_f2(pk01), h23 = h2_to_f2(pk23);
-      corr0 += p0 * sza.y + p2 * szb.y - 1024.f * (h01.x + h23.x);
-      corr1 += p1 * sza.y + p3 * szb.y - 1024.f * (h01.y + h23.y);
-      bp0[m] = movmatrix_trans(pk01);
-      bp1[m] = movmatrix_trans(pk23);
+      if constexpr (kBiasMma) {
+        corr0 += p0 * sza.y + p2 * szb.y;
+        corr1 += p1 * sza.y + p3 * szb.y;
+        bp0[m] = movmatrix_trans(pk01);
+        bp1[m] = movmatrix_trans(pk23);
+        // 1024 * sum over the tile's tokens of P' (exactly the B operand the
+        // PV MMA sees), per head column, accumulated across tiles
+        mma_f16(bacc, 0x64006400u, 0x64006400u, 0x64006400u, 0x64006400u, bp0[m], bp1[m]);
+      } else {
+        const float2 h01 = h2_to_f2(pk01), h23 = h2_to_f2(pk23);
+        corr0 += p0 * sza.y + p2 * szb.y - 1024.f * (h01.x + h23.x);
+        corr1 += p1 * sza.y + p3 * szb.y - 1024.f * (h01.y + h23.y);
+        bp0[m] = movmatrix_trans(pk01);
+        bp1[m] = movmatrix_trans(pk23);
+      }
     }
 
     // O^T += Vcodes^T . P'^T
@@ -576,17 +663,20 @@ __global__ void __launch_bounds__(kWarps * 32, NREP == 8 ? 3 : VC_DRAFT_MINB) dr
       // over a long range (a warp takes T / warps groups -- 14 at 16 x 32K)
       // the two fp32 sums cancel catastrophically (logits off by 20-40% at
       // 24-48 x 32K; tests/test_real_shapes.py::test_draft_batched_equals_single)
-      float c0 = corr0, c1 = corr1;
+      float z0 = corr0, z1 = corr1;
 #pragma unroll
       for (int o = 4; o < 32; o <<= 1) {
-        c0 += __shfl_xor_sync(0xffffffffu, c0, o);
-        c1 += __shfl_xor_sync(0xffffffffu, c1, o);
+        z0 += __shfl_xor_sync(0xffffffffu, z0, o);
+        z1 += __shfl_xor_sync(0xffffffffu, z1, o);
       }
+      float c0, c1, c08, c18;
+      corrections(z0, z1, c0, c1, c08, c18);
 #pragma unroll
       for (int ct = 0; ct < KS; ++ct) {
-        oacc[ct][0] += c0; oacc[ct][1] += c1; oacc[ct][2] += c0; oacc[ct][3] += c1;
+        oacc[ct][0] += c0; oacc[ct][1] += c1; oacc[ct][2] += c08; oacc[ct][3] += c18;
       }
       corr0 = corr1 = 0.f;
+      bacc[0] = bacc[1] = bacc[2] = bacc[3] = 0.f;
     }
   }
   emit();  // the last (sequence, head) of the range
