@@ -40,3 +40,11 @@ def test_step_roofline_bytes_model():
     want = 10 * w + 140 * (1_073_741_824 + 67_108_864) + 20 * 4_294_967_296
     assert out["bytes_per_iteration"] == int(want / 10)
     assert abs(out["achieved_gbs"] - want / 0.09 / 1e9) < 0.1
+
+
+def test_sim_metrics_null_latency_without_completions():
+    base = {"throughput": 10.0, "warm_throughput": 11.0, "interconnect_busy": 0.5, "peak_hbm_bytes": 7}
+    m = bench.sim_metrics(dict(base, p50_latency_s=0.0, p99_latency_s=0.0))
+    assert m["p50_latency_s"] is None and m["p99_latency_s"] is None and "latency_note" in m
+    m = bench.sim_metrics(dict(base, p50_latency_s=1.5, p99_latency_s=2.25))
+    assert m["p50_latency_s"] == 1.5 and m["p99_latency_s"] == 2.25 and "latency_note" not in m
