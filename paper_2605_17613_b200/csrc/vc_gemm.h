@@ -105,16 +105,23 @@ cudaError_t compact_dropped(KvPool src, int src_slot, const int32_t* kept, int k
 cudaError_t expand_dropped(KvPool land, int land_slot, KvPool drop, int drop_slot, const int32_t* kept, int k, int T,
                            int n, KvPool dst, int dst_slot, int n_slices, int d, cudaStream_t st);
 // Lossless packing of 128-token bf16 blocks (vc_pack.cu): per channel an
-// exponent base, per value a 4-bit exponent offset + sign|mantissa byte,
+// exponent base; per value a 2-bit exponent code (offsets 1-3 below the
+// base, or 0 = "see the secondary stream") and the sign|mantissa byte; a
+// secondary stream of 4-bit offsets (0..14, 15 = escape) for the values
+// coded 0, in value order, up to kPackSecNum / kPackSecDen of a block;
 // escapes for values more than 14 binades below their channel's maximum.
 constexpr int kPackEscCap = 60;
+constexpr int kPackSecNum = 7, kPackSecDen = 25;  // secondary capacity: 0.28 of the values
+__host__ __device__ constexpr int packed_sec_cap(int d) { return 128 * d * kPackSecNum / kPackSecDen / 8 * 8; }
 __host__ __device__ constexpr size_t packed_block_bytes(int d) {
-  return (static_cast<size_t>(d) + 128u * d / 2 + 128u * d + 4 + 4u * kPackEscCap + 15) / 16 * 16;
+  return (static_cast<size_t>(d) + 128u * d / 4 + 128u * d + 4 + packed_sec_cap(d) / 2 + 4 + 4u * kPackEscCap + 15) /
+         16 * 16;
 }
 // src rows [src_row0 + 128 b, ...) of each slice (slice pitch in elements),
 // n_valid rows from src_row0 (the last block may be partial); dst packed
 // block b of slice s at dst + s * dst_slice_pitch + b * packed_block_bytes(d)
-// (bytes).  *overflow = max(1 + block) over blocks with > kPackEscCap escapes.
+// (bytes).  *overflow = max(1 + block) over blocks with > kPackEscCap escapes
+// or more secondary offsets than packed_sec_cap(d).
 cudaError_t pack_blocks(const uint16_t* src, size_t src_slice_pitch, int src_row0, int n_valid, int n_blocks,
                         int n_slices, int d, uint8_t* dst, size_t dst_slice_pitch, int* overflow, cudaStream_t st);
 cudaError_t unpack_blocks(const uint8_t* src, size_t src_slice_pitch, int n_blocks, int n_slices, int d, uint16_t* dst,
