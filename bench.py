@@ -877,7 +877,9 @@ def main():
         full KV in HBM (B_g) and verify with x_res-token rounds, the others (B_c)
         are reloaded per verify)."""
         # host tier x=47: the verify window plus 15 drafting rows stays within one
-        # 64-row GEMM tile and the booked reloads saturate PCIe (link busy 0.99)
+        # 64-row GEMM tile and the booked reloads saturate PCIe (link busy 0.99);
+        # sweep on the final code (profiles/r02_host_x_sweep.txt): x=31 / 47 / 63 / 95
+        # -> 331 / 421 / 426 / 394 tok/s (accepted 17.0 / 21.8 / 22.0 / 23.3)
         # HBM tier x=7: the measured optimum of an x sweep {5,6,7,8,10} on the
         # round-2 kernels (1.362 / 1.393 / 1.409 / 1.326 / 1.284x), and the
         # reference optimiser's choice (knobs.optimize_intra: x = 7)

@@ -1,5 +1,5 @@
 # Host-tier draft-horizon sweep (bench.py --tier host --x N)
-for x in 63 95 47; do
+for x in ${XS:-31 47 63 95}; do
 timeout 1200 python bench.py --tier host --x $x --no-cpu --no-secondary > gpurun_out/hx_$x.json 2> gpurun_out/hx_$x.err; echo "x=$x rc=$?"
 python - <<PY
 import json
