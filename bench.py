@@ -347,6 +347,26 @@ def sim_metrics(s):
     return m
 
 
+def pinned_h2d_peak(torch, nbytes=1 << 30, reps=3):
+    """GB/s of a plain pinned-host -> device copy (the link's measured peak)."""
+    try:
+        h = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+        g = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+        best = 0.0
+        for _ in range(reps):
+            a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record()
+            g.copy_(h, non_blocking=True)
+            b.record()
+            b.synchronize()
+            best = max(best, nbytes / (a.elapsed_time(b) / 1e3) / 1e9)
+        del h, g
+        torch.cuda.empty_cache()
+        return round(best, 1)
+    except RuntimeError:
+        return None
+
+
 def main_remote(args, rank, world, local):
     """configs[3]: remote prefix caching.  A 64K prefix is precomputed at the
     storage node (pinned host memory) in both forms: its full KV and its int2
@@ -826,6 +846,7 @@ def main():
             dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     peaks = json.load(open(PEAKS)) if os.path.exists(PEAKS) else {}
     peak, peak_src = hbm_peak(peaks)
+    link_peak = pinned_h2d_peak(torch)  # before the pool pins ~50 GB: the link alone
     shape = vc.TINY if args.small else vc.LLAMA3_8B
     B, ctx, K, W = args.batch, args.ctx, args.steps, args.warmup
     if args.small:
@@ -1037,6 +1058,14 @@ def main():
                          "staging_hbm_bytes": int(s["staging_bytes"]),
                          "bytes_per_reload": int(r["meta"]["full_bytes"]),
                          "reload_bytes_over_full_kv": round(s["reload_over_full"], 4)}
+            # the link roofline (north_star: H2D GB/s against the PCIe link): the
+            # packed bytes' rate over a plain pinned H2D copy measured in this
+            # process, and the full-KV rate the packing makes of it
+            h2d = d["swap"]["h2d_gbs"]
+            d["swap"]["link_roofline"] = {
+                "achieved_gbs": h2d, "peak_gbs": link_peak, "frac": round(h2d / link_peak, 3) if link_peak else None,
+                "peak_source": "best of 3 pinned 1 GiB cudaMemcpyAsync H2D in this process",
+                "full_kv_gbs_effective": round(h2d / max(s["reload_over_full"], 1e-9), 1)}
         return d
 
     def reference_csv():
