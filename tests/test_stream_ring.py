@@ -176,6 +176,28 @@ def test_pack_overflow_is_reported(cuda):
 
 
 @pytest.mark.gpu
+def test_pack_secondary_overflow_is_reported(cuda):
+    """A block whose exponents spread evenly over 13 binades below each
+    channel's maximum puts most values outside the 2-bit codes (offsets 1-3):
+    the secondary stream (0.28 of the values) overflows with no escape at all,
+    and the block is reported (stored raw).  Its neighbour block packs."""
+    torch = cuda
+    rng = np.random.default_rng(1)
+    x = rng.standard_normal((1, 256, 128)).astype(np.float32)
+    expo = (np.arange(128)[:, None] + np.arange(128)[None, :]) % 13  # offsets 0..12 in every channel
+    x[0, :128] = np.sign(x[0, :128]) * (1.0 + rng.random((128, 128))) * 2.0 ** (-expo)
+    bits = T.f32_to_bf16(x)
+    src = torch.from_numpy(bits.view(np.int16).copy()).cuda()
+    out = torch.zeros_like(src)
+    ovf = C.c_int(0)
+    lib = _lib.load()
+    assert lib.vc_pack_roundtrip(src.data_ptr(), 256, 1, 128, out.data_ptr(), C.byref(ovf),
+                                 torch.cuda.current_stream().cuda_stream) == 0
+    assert ovf.value == 1  # 1 + block 0; block 1 (Gaussian) packs
+    np.testing.assert_array_equal(out.cpu().numpy().view(np.uint16)[:, 128:], bits[:, 128:])
+
+
+@pytest.mark.gpu
 def test_stream_abort_releases_the_ring(cuda, w6):
     b = _engine(w6, 2)
     for s, n in enumerate(CTX):
