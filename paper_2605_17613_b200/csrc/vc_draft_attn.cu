@@ -45,8 +45,9 @@ constexpr int kStages = VC_DRAFT_STAGES;
 #endif
 #ifndef VC_DRAFT_BIAS_MMA
 // the 1024 * sum(P') correction by one MMA per tile instead of per-lane
-// f16->f32 sums: int2 needs it (its rows +8 carry a x4, below); for int4 it
-// measured neutral (16 x 32K set 3.674 vs 3.670 ms) and stays off
+// f16->f32 sums (int2's rows +8 need that sum apart from the zero-point sum:
+// the MMA, or VC_INT2_SPLIT's per-lane sums, which measured faster); for int4
+// it measured neutral (16 x 32K set 3.674 vs 3.670 ms) and stays off
 #define VC_DRAFT_BIAS_MMA 0
 #endif
 #ifndef VC_INT2_NOSHIFT
@@ -393,9 +394,17 @@ __global__ void __launch_bounds__(kWarps * 32, NREP == 8 ? 3 : VC_DRAFT_MINB) dr
     }
   };
   // x4 on the code part of rows +8 (int2, VC_INT2_NOSHIFT); 1 otherwise.
-  // 16 x 32K int2 set: 3.674 ms (3 shifts per word) -> 3.473 ms
+  // 16 x 32K int2 set: 3.674 ms (3 shifts per word) -> 3.473 ms (bias MMA)
+  // -> 3.411 ms (per-lane split sums, VC_INT2_SPLIT)
   constexpr float kRow8 = (BITS == 2 && VC_INT2_NOSHIFT) ? 4.f : 1.f;
-  constexpr bool kBiasMma = VC_DRAFT_BIAS_MMA || kRow8 != 1.f;
+#ifndef VC_INT2_SPLIT
+// int2: the zero-point and 1024-bias sums kept apart per lane (f16->f32 +
+// FADD, reduced at the fold) instead of the bias MMA: 16 x 32K int2 set
+// 3.475 -> 3.411 ms, and no register spill
+#define VC_INT2_SPLIT 1
+#endif
+  constexpr bool kSplit = VC_INT2_SPLIT && kRow8 != 1.f;
+  constexpr bool kBiasMma = (VC_DRAFT_BIAS_MMA || kRow8 != 1.f) && !kSplit;
   constexpr float kHiScale = 0.0625f;  // B-operand scale of pairs 2/3 (their A holds 1024 + 16c)
   if (lane == 0) {
     for (int i = 0; i < kStages; ++i) mbar_init(bar + i, 1);
@@ -424,8 +433,20 @@ __global__ void __launch_bounds__(kWarps * 32, NREP == 8 ? 3 : VC_DRAFT_MINB) dr
   };
   // the O corrections of rows g (A) and g+8 (B, whose code part carries kRow8)
   // from the warp-reduced zero-point sums z and the bias sums
+  // (kSplit: bacc[0] / [1] hold per-lane sums of P', reduced here)
   auto corrections = [&](float z0, float z1, float& a0, float& a1, float& b0, float& b1) {
-    if constexpr (kBiasMma) {
+    if constexpr (kSplit) {
+      float s0 = bacc[0], s1 = bacc[1];
+#pragma unroll
+      for (int o = 4; o < 32; o <<= 1) {
+        s0 += __shfl_xor_sync(0xffffffffu, s0, o);
+        s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+      }
+      a0 = z0 - 1024.f * s0;
+      a1 = z1 - 1024.f * s1;
+      b0 = kRow8 * z0 - 1024.f * s0;
+      b1 = kRow8 * z1 - 1024.f * s1;
+    } else if constexpr (kBiasMma) {
       a0 = z0 - bacc[0];
       a1 = z1 - bacc[1];
       b0 = kRow8 * z0 - bacc[0];
@@ -594,7 +615,7 @@ __global__ void __launch_bounds__(kWarps * 32, NREP == 8 ? 3 : VC_DRAFT_MINB) dr
       mrun0 = mn0;
       mrun1 = mn1;
       lsum0 *= al0; lsum1 *= al1; corr0 *= al0; corr1 *= al1;
-      if constexpr (kBiasMma) {
+      if constexpr (kBiasMma || kSplit) {
         bacc[0] *= al0; bacc[1] *= al1;
       }
 #pragma unroll
@@ -621,6 +642,14 @@ __global__ void __launch_bounds__(kWarps * 32, NREP == 8 ? 3 : VC_DRAFT_MINB) dr
         // 1024 * sum over the tile's tokens of P' (exactly the B operand the
         // PV MMA sees), per head column, accumulated across tiles
         mma_f16(bacc, 0x64006400u, 0x64006400u, 0x64006400u, 0x64006400u, bp0[m], bp1[m]);
+      } else if constexpr (kSplit) {
+        const float2 h01 = h2_to_f2(pk01), h23 = h2_to_f2(pk23);
+        corr0 += p0 * sza.y + p2 * szb.y;
+        corr1 += p1 * sza.y + p3 * szb.y;
+        bacc[0] += h01.x + h23.x;
+        bacc[1] += h01.y + h23.y;
+        bp0[m] = movmatrix_trans(pk01);
+        bp1[m] = movmatrix_trans(pk23);
       } else {
         const float2 h01 = h2_to_f2(pk01), h23 = h2_to_f2(pk23);
         corr0 += p0 * sza.y + p2 * szb.y - 1024.f * (h01.x + h23.x);
