@@ -53,6 +53,9 @@ constexpr int kStages = VC_DRAFT_STAGES;
 #ifndef VC_INT2_NOSHIFT
 #define VC_INT2_NOSHIFT 1  // int2: four masks per byte, rows +8 carry a x4 the epilogues undo
 #endif
+#ifndef VC_QK_CHAINS
+#define VC_QK_CHAINS 1  // dependent MMA chains per score tile (2: even / odd k-steps)
+#endif
 #ifndef VC_SHIFT_IMAD
 // the unpack's byte shift as IMAD.HI (FMA pipe) instead of SHF (ALU pipe,
 // with the lop3s): measured slower (16 x 32K int4 set 3.67 -> 4.14 ms, int2
@@ -580,12 +583,25 @@ __global__ void __launch_bounds__(kWarps * 32, NREP == 8 ? 3 : VC_DRAFT_MINB) dr
         }
       }
       sacc[m][0] = sacc[m][1] = sacc[m][2] = sacc[m][3] = 0.f;
+#if VC_QK_CHAINS == 2
+      // two accumulator chains over the k-steps (even / odd), summed after:
+      // halves the dependent MMA chain of a tile (diagnostics A/B)
+      float s2[4] = {0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int k = 0; k < KS; ++k) {
+        uint32_t a[4];
+        unpack((BITS == 4) ? kw[k] : kw[k >> 1], k & 1, a);
+        mma_f16((k & 1) ? s2 : sacc[m], a[0], a[1], a[2], a[3], b0[k], b1[k]);
+      }
+      sacc[m][0] += s2[0]; sacc[m][1] += s2[1]; sacc[m][2] += s2[2]; sacc[m][3] += s2[3];
+#else
 #pragma unroll
       for (int k = 0; k < KS; ++k) {
         uint32_t a[4];
         unpack((BITS == 4) ? kw[k] : kw[k >> 1], k & 1, a);
         mma_f16(sacc[m], a[0], a[1], a[2], a[3], b0[k], b1[k]);
       }
+#endif
       sacc[m][0] += bias0; sacc[m][1] += bias1;
       if constexpr (kRow8 == 1.f) {
         sacc[m][2] += bias0; sacc[m][3] += bias1;
